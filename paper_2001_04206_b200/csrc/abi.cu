@@ -1,0 +1,963 @@
+// abi.cu -- implementation of include/lane_b200.h (the C ABI).
+//
+// One translation unit: the kernels are header-only (.cuh) and instantiated
+// here.  Every entry point is wrapped by guard(): C++ exceptions never cross
+// the ABI; they become status codes + lane_b200_last_error().
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cmath>
+#include <cstdint>
+#include <cstdlib>
+#include <cstring>
+#include <string>
+#include <vector>
+
+#include "common.cuh"
+#include "layer_kernels.cuh"
+#include "minibatch.cuh"
+#include "sgd_persistent.cuh"
+
+using namespace lane_b200;
+
+namespace {
+
+thread_local std::string g_last_error;
+
+template <class F>
+int guard(F&& f) {
+    try {
+        f();
+        return LANE_OK;
+    } catch (const Error& e) {
+        g_last_error = e.what();
+        return e.code;
+    } catch (const std::bad_alloc&) {
+        g_last_error = "host allocation failed";
+        return LANE_ERR_INTERNAL;
+    } catch (const std::exception& e) {
+        g_last_error = e.what();
+        return LANE_ERR_INTERNAL;
+    }
+}
+
+// ---- host SplitMix64, bit-identical to lane::SeededRng (tensor.hpp:13-44) ----
+struct SplitMix64 {
+    uint64_t state;
+    explicit SplitMix64(uint64_t s) : state(s) {}
+    uint64_t next_u64() {
+        state += 0x9E3779B97F4A7C15ULL;
+        uint64_t z = state;
+        z = (z ^ (z >> 30)) * 0xBF58476D1CE4E5B9ULL;
+        z = (z ^ (z >> 27)) * 0x94D049BB133111EBULL;
+        return z ^ (z >> 31);
+    }
+    float next_float() { return static_cast<float>(next_u64() >> 40) * 0x1p-24f; }
+    // tensor.cpp:7-15 (host float arithmetic; this TU's host code is compiled
+    // for baseline x86-64 with -ffp-contract=off: no FMA, like the reference)
+    float uniform(float lo, float hi) {
+        const float scale = hi - lo;
+        const float prod = next_float() * scale;
+        const float v = lo + prod;
+        return v < hi ? v : std::nextafter(hi, lo);
+    }
+    size_t below(size_t n) {
+        return static_cast<size_t>((static_cast<unsigned __int128>(next_u64()) * n) >> 64);
+    }
+};
+
+uint64_t fnv1a64(const void* data, size_t len, uint64_t h) {
+    const unsigned char* b = static_cast<const unsigned char*>(data);
+    for (size_t i = 0; i < len; ++i) {
+        h ^= b[i];
+        h *= 0x100000001b3ULL;
+    }
+    return h;
+}
+
+int blocks_for(size_t n, int threads, int cap) {
+    return static_cast<int>(std::max<size_t>(1, std::min<size_t>(cap, (n + threads - 1) / threads)));
+}
+
+}  // namespace
+
+// ============================================================== objects ===
+
+struct lane_b200_ctx {
+    int device = 0;
+    cudaStream_t stream = nullptr;
+    int numerics = LANE_NUMERICS_FAST;
+    uint64_t launches = 0;
+    int sm_count = 148;
+    size_t max_smem_optin = 0;
+    int* error_flag = nullptr;  // device: set by kernels that bail out
+    std::vector<void*> scratch;
+    MinibatchComm comm;  // NCCL communicator (mini-batch DP), see minibatch.cuh
+
+    void count(int n = 1) { launches += static_cast<uint64_t>(n); }
+    void check_launch() {
+        cudaError_t e = cudaGetLastError();
+        if (e != cudaSuccess)
+            throw Error(LANE_ERR_CUDA, std::string("kernel launch: ") + cudaGetErrorString(e));
+    }
+    void check_device_error() {
+        int flag = 0;
+        LANE_CUDA(cudaMemcpyAsync(&flag, error_flag, sizeof(int), cudaMemcpyDeviceToHost, stream));
+        LANE_CUDA(cudaStreamSynchronize(stream));
+        if (flag) {
+            LANE_CUDA(cudaMemsetAsync(error_flag, 0, sizeof(int), stream));
+            throw Error(LANE_ERR_CUDA, "device exchange timed out (persistent kernel aborted)");
+        }
+    }
+};
+
+struct LayerBufs {
+    size_t I = 0, O = 0;
+    float* buf[LANE_BUF_COUNT] = {};
+    size_t cnt[LANE_BUF_COUNT] = {};
+};
+
+struct lane_b200_net {
+    lane_b200_ctx* ctx = nullptr;
+    size_t input_width = 0, n_hidden = 0, classes = 0, max_batch = 1;
+    std::vector<LayerBufs> layers;
+    char* arena = nullptr;
+    size_t arena_bytes = 0;
+    float* params = nullptr;  // [W_0 | b_0 | W_1 | b_1 | ...]
+    size_t params_count = 0;
+    float* grads = nullptr;  // [G_0 | gb_0 | G_1 | gb_1 | ...] (allreduce target)
+    size_t grads_count = 0;
+    float* target_stage = nullptr;  // classes * max_batch
+    float* scratch = nullptr;       // split-K partials / uploaded next-layer tensors
+    size_t scratch_count = 0;
+    long long* step = nullptr;
+    double* loss_dev = nullptr;
+    unsigned long long* correct_dev = nullptr;
+    unsigned long long* slots = nullptr;
+    size_t slots_count = 0;
+    // dataset staging for train()/evaluate() (uploaded once per call)
+    float* data = nullptr;
+    size_t data_count = 0;
+    uint32_t* order = nullptr;
+    size_t order_count = 0;
+    MinibatchState mb;  // activations + workspaces of the mini-batch path
+
+    LayerBufs& L(size_t l) { return layers.at(l); }
+    size_t out_layer() const { return n_hidden; }
+};
+
+namespace {
+
+void* dev_alloc(size_t bytes) {
+    void* p = nullptr;
+    LANE_CUDA(cudaMalloc(&p, std::max<size_t>(bytes, 256)));
+    return p;
+}
+
+void ensure(float*& p, size_t& have, size_t need) {
+    if (have >= need) return;
+    if (p) LANE_CUDA(cudaFree(p));
+    p = static_cast<float*>(dev_alloc(need * sizeof(float)));
+    have = need;
+}
+
+void check_eta(float eta) {
+    // LearningRate (layers.hpp:11-19)
+    if (!(eta > 0.0f)) throw Error(LANE_ERR_CONFIG, "LearningRate: eta must be positive");
+}
+
+void check_layer(lane_b200_net* net, size_t layer) {
+    if (!net) throw Error(LANE_ERR_CONFIG, "null network");
+    if (layer >= net->layers.size()) throw Error(LANE_ERR_CONFIG, "layer index out of range");
+}
+
+// ---------------------------------------------------------------- layers ---
+
+void run_layer_forward(lane_b200_net* net, size_t l, const float* src) {
+    lane_b200_ctx* c = net->ctx;
+    LayerBufs& Ly = net->L(l);
+    const int I = static_cast<int>(Ly.I), O = static_cast<int>(Ly.O);
+    const bool softmax = l == net->out_layer();
+    const int act = softmax ? ACT_NONE : ACT_TANH;
+    const bool strict = c->numerics == LANE_NUMERICS_STRICT;
+    float* z = Ly.buf[LANE_BUF_NETIN];
+    float* a = Ly.buf[LANE_BUF_OUTPUTS];
+    if (strict || I < 512) {
+        // thread per output, sequential i: exact reference order (and the
+        // fastest choice when I is small)
+        k_netin_strict<<<blocks_for(O, 128, 1 << 20), 128, 0, c->stream>>>(
+            src, Ly.buf[LANE_BUF_INPUTS], Ly.buf[LANE_BUF_W], Ly.buf[LANE_BUF_B], z, a, I, O, act);
+        c->count();
+    } else {
+        const int colblocks = (O + 31) / 32;
+        int S = std::max(1, std::min((2 * c->sm_count + colblocks - 1) / colblocks, I / 64));
+        const int chunk = (I + S - 1) / S;
+        S = (I + chunk - 1) / chunk;
+        ensure(net->scratch, net->scratch_count, static_cast<size_t>(S) * O);
+        k_netin_fast_part<<<dim3(colblocks, S), dim3(32, 8), 0, c->stream>>>(src, Ly.buf[LANE_BUF_W],
+                                                                            net->scratch, I, O, chunk);
+        k_netin_fast_finish<<<blocks_for(O, 128, 1 << 20), 128, 0, c->stream>>>(
+            net->scratch, S, src, Ly.buf[LANE_BUF_INPUTS], I, Ly.buf[LANE_BUF_B], z, a, O, act);
+        c->count(2);
+    }
+    if (softmax) {
+        const int th = std::min(1024, ((O + 31) / 32) * 32);
+        k_softmax<<<1, th, 0, c->stream>>>(z, a, O, strict ? 1 : 0);
+        c->count();
+    }
+    c->check_launch();
+}
+
+void run_fc_backward(lane_b200_net* net, size_t l, const float* nW, const float* nd, int N,
+                     float eta) {
+    lane_b200_ctx* c = net->ctx;
+    LayerBufs& Ly = net->L(l);
+    const int I = static_cast<int>(Ly.I), O = static_cast<int>(Ly.O);
+    const float neg_eta = -eta;
+    if (c->numerics == LANE_NUMERICS_STRICT || N < 64) {
+        k_delta_fc_strict<<<blocks_for(O, 128, 1 << 20), 128, 0, c->stream>>>(
+            Ly.buf[LANE_BUF_OUTPUTS], nW, nd, Ly.buf[LANE_BUF_DELTAS], Ly.buf[LANE_BUF_DELTA_BIASES],
+            neg_eta, O, N);
+    } else {
+        k_delta_fc_fast<<<blocks_for(static_cast<size_t>(O) * 32, 256, 1 << 20), 256, 0, c->stream>>>(
+            Ly.buf[LANE_BUF_OUTPUTS], nW, nd, Ly.buf[LANE_BUF_DELTAS], Ly.buf[LANE_BUF_DELTA_BIASES],
+            neg_eta, O, N);
+    }
+    k_outer<<<blocks_for(static_cast<size_t>(I) * O, 256, 8 * c->sm_count), 256, 0, c->stream>>>(
+        Ly.buf[LANE_BUF_DELTAS], Ly.buf[LANE_BUF_INPUTS], Ly.buf[LANE_BUF_G], Ly.buf[LANE_BUF_DW],
+        neg_eta, I, O);
+    c->count(2);
+    c->check_launch();
+}
+
+void run_softmax_backward(lane_b200_net* net, const float* t_dev, float eta) {
+    lane_b200_ctx* c = net->ctx;
+    LayerBufs& Ly = net->L(net->out_layer());
+    const int I = static_cast<int>(Ly.I), O = static_cast<int>(Ly.O);
+    k_delta_softmax<<<blocks_for(O, 128, 1 << 20), 128, 0, c->stream>>>(
+        Ly.buf[LANE_BUF_OUTPUTS], t_dev, Ly.buf[LANE_BUF_DELTAS], Ly.buf[LANE_BUF_DELTA_BIASES], -eta, O);
+    k_outer<<<blocks_for(static_cast<size_t>(I) * O, 256, 8 * c->sm_count), 256, 0, c->stream>>>(
+        Ly.buf[LANE_BUF_DELTAS], Ly.buf[LANE_BUF_INPUTS], Ly.buf[LANE_BUF_G], Ly.buf[LANE_BUF_DW], -eta,
+        I, O);
+    c->count(2);
+    c->check_launch();
+}
+
+void run_apply_updates(lane_b200_net* net, size_t l) {
+    lane_b200_ctx* c = net->ctx;
+    LayerBufs& Ly = net->L(l);
+    const size_t n = Ly.I * Ly.O;
+    k_apply_updates<<<blocks_for(n / 4 + Ly.O, 256, 8 * c->sm_count), 256, 0, c->stream>>>(
+        Ly.buf[LANE_BUF_W], Ly.buf[LANE_BUF_DW], n, Ly.buf[LANE_BUF_B], Ly.buf[LANE_BUF_DELTA_BIASES],
+        static_cast<int>(Ly.O));
+    c->count();
+    c->check_launch();
+}
+
+void run_backward_plan(lane_b200_net* net, const float* t_dev, float eta) {
+    // BackwardPlan::run (network.cpp:122-138)
+    run_softmax_backward(net, t_dev, eta);
+    for (size_t l = net->n_hidden; l-- > 0;) {
+        LayerBufs& nx = net->L(l + 1);
+        run_fc_backward(net, l, nx.buf[LANE_BUF_W], nx.buf[LANE_BUF_DELTAS], static_cast<int>(nx.O), eta);
+    }
+    for (size_t l = 0; l < net->layers.size(); ++l) run_apply_updates(net, l);
+}
+
+void run_forward_chain(lane_b200_net* net) {
+    for (size_t l = 0; l < net->layers.size(); ++l) {
+        const float* src = l == 0 ? net->L(0).buf[LANE_BUF_INPUTS] : net->L(l - 1).buf[LANE_BUF_OUTPUTS];
+        run_layer_forward(net, l, src);
+    }
+}
+
+// ------------------------------------------------ fused persistent path ---
+
+struct SgdPlan {
+    bool ok = false;
+    int G = 0, npc = 0, wpn = 1;
+    size_t smem = 0;
+};
+
+int next_pow2(int v) {
+    int p = 1;
+    while (p < v) p <<= 1;
+    return p;
+}
+
+SgdPlan plan_persistent(lane_b200_net* net) {
+    SgdPlan p;
+    lane_b200_ctx* c = net->ctx;
+    if (net->n_hidden != 1 || c->numerics != LANE_NUMERICS_FAST) return p;
+    const int I = static_cast<int>(net->input_width), H = static_cast<int>(net->L(0).O),
+              C = static_cast<int>(net->classes);
+    if (C > kSgdMaxC) return p;
+    int G = std::min(c->sm_count, H);
+    if (const char* e = std::getenv("LANE_B200_SGD_CTAS")) G = std::max(1, std::min(std::atoi(e), std::min(c->sm_count, H)));
+    const int npc = (H + G - 1) / G;
+    G = (H + npc - 1) / npc;
+    const int wpn = npc >= kSgdWarps ? 1 : kSgdWarps / next_pow2(npc);
+    const SgdSmem L(I, C, npc, wpn, G);
+    if (L.total > c->max_smem_optin) return p;
+    p.ok = true;
+    p.G = G;
+    p.npc = npc;
+    p.wpn = wpn;
+    p.smem = L.total;
+    return p;
+}
+
+void launch_persistent(lane_b200_net* net, const SgdPlan& P, const float* X, const float* T, size_t n,
+                       const uint32_t* order, size_t n_steps, float eta, double* loss_sum,
+                       unsigned long long* correct) {
+    lane_b200_ctx* c = net->ctx;
+    LayerBufs& L0 = net->L(0);
+    LayerBufs& L1 = net->L(1);
+    const size_t need = 2ull * P.G * net->classes;
+    if (net->slots_count < need) {
+        if (net->slots) LANE_CUDA(cudaFree(net->slots));
+        net->slots = static_cast<unsigned long long*>(dev_alloc(need * 8));
+        net->slots_count = need;
+    }
+    LANE_CUDA(cudaMemsetAsync(net->slots, 0, need * 8, c->stream));
+    SgdArgs A{};
+    A.I = static_cast<int>(net->input_width);
+    A.H = static_cast<int>(L0.O);
+    A.C = static_cast<int>(net->classes);
+    A.G = P.G;
+    A.npc = P.npc;
+    A.wpn = P.wpn;
+    A.X = X;
+    A.T = T;
+    A.order = order;
+    A.n = static_cast<long long>(n);
+    A.n_steps = static_cast<long long>(n_steps);
+    A.neg_eta = -eta;
+    A.W0 = L0.buf[LANE_BUF_W];
+    A.b0 = L0.buf[LANE_BUF_B];
+    A.W1 = L1.buf[LANE_BUF_W];
+    A.b1 = L1.buf[LANE_BUF_B];
+    A.slots = net->slots;
+    A.x0 = L0.buf[LANE_BUF_INPUTS];
+    A.z0 = L0.buf[LANE_BUF_NETIN];
+    A.a0 = L0.buf[LANE_BUF_OUTPUTS];
+    A.d0 = L0.buf[LANE_BUF_DELTAS];
+    A.db0 = L0.buf[LANE_BUF_DELTA_BIASES];
+    A.x1 = L1.buf[LANE_BUF_INPUTS];
+    A.z1 = L1.buf[LANE_BUF_NETIN];
+    A.a1 = L1.buf[LANE_BUF_OUTPUTS];
+    A.d1 = L1.buf[LANE_BUF_DELTAS];
+    A.db1 = L1.buf[LANE_BUF_DELTA_BIASES];
+    A.loss_sum = loss_sum;
+    A.correct = correct;
+    A.error = c->error_flag;
+    static size_t configured = 0;
+    if (P.smem > configured) {
+        LANE_CUDA(cudaFuncSetAttribute(k_sgd_persistent, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                       static_cast<int>(P.smem)));
+        configured = P.smem;
+    }
+    void* args[] = {&A};
+    LANE_CUDA(cudaLaunchCooperativeKernel(reinterpret_cast<void*>(k_sgd_persistent), dim3(P.G),
+                                          dim3(kSgdThreads), args, P.smem, c->stream));
+    c->count();
+    // G and DW of the last sample, as the reference's stream_out leaves them
+    for (size_t l = 0; l < 2; ++l) {
+        LayerBufs& Ly = net->L(l);
+        k_outer<<<blocks_for(Ly.I * Ly.O, 256, 8 * c->sm_count), 256, 0, c->stream>>>(
+            Ly.buf[LANE_BUF_DELTAS], Ly.buf[LANE_BUF_INPUTS], Ly.buf[LANE_BUF_G], Ly.buf[LANE_BUF_DW],
+            -eta, static_cast<int>(Ly.I), static_cast<int>(Ly.O));
+        c->count();
+    }
+    c->check_launch();
+}
+
+// Per-sample layer-kernel stream (STRICT numerics, deep nets, C > 128 or
+// slices that do not fit on chip): one captured CUDA graph per step.
+void stream_layer_path(lane_b200_net* net, const float* X, const float* T, size_t n,
+                       const uint32_t* order, size_t n_steps, float eta, double* loss_sum,
+                       unsigned long long* correct, bool train) {
+    lane_b200_ctx* c = net->ctx;
+    LANE_CUDA(cudaMemsetAsync(net->step, 0, sizeof(long long), c->stream));
+    const int I = static_cast<int>(net->input_width), C = static_cast<int>(net->classes);
+    cudaGraph_t graph = nullptr;
+    cudaGraphExec_t exec = nullptr;
+    const uint64_t before = c->launches;
+    LANE_CUDA(cudaStreamBeginCapture(c->stream, cudaStreamCaptureModeThreadLocal));
+    try {
+        k_stage_sample<<<1, 256, 0, c->stream>>>(X, T, order, static_cast<long long>(n), net->step,
+                                                 net->L(0).buf[LANE_BUF_INPUTS], I, net->target_stage, C);
+        c->count();
+        run_forward_chain(net);
+        LayerBufs& out = net->L(net->out_layer());
+        if (loss_sum || correct) {
+            k_loss_accumulate<<<1, 32, 0, c->stream>>>(out.buf[LANE_BUF_OUTPUTS], net->target_stage, C,
+                                                       loss_sum, correct);
+            c->count();
+        }
+        if (train) run_backward_plan(net, net->target_stage, eta);
+        k_step_advance<<<1, 32, 0, c->stream>>>(net->step);
+        c->count();
+    } catch (...) {
+        cudaStreamEndCapture(c->stream, &graph);
+        if (graph) cudaGraphDestroy(graph);
+        throw;
+    }
+    LANE_CUDA(cudaStreamEndCapture(c->stream, &graph));
+    const uint64_t per_step = c->launches - before;
+    c->launches = before;
+    LANE_CUDA(cudaGraphInstantiate(&exec, graph, 0));
+    for (size_t s = 0; s < n_steps; ++s) LANE_CUDA(cudaGraphLaunch(exec, c->stream));
+    c->count(static_cast<int>(per_step * n_steps));
+    LANE_CUDA(cudaGraphExecDestroy(exec));
+    LANE_CUDA(cudaGraphDestroy(graph));
+}
+
+void sgd_stream_impl(lane_b200_net* net, const float* X, const float* T, size_t n, const uint32_t* order,
+                     size_t n_steps, float eta, double* loss_sum, unsigned long long* correct) {
+    check_eta(eta);
+    if (n == 0) throw Error(LANE_ERR_TRAINING, "sgd_stream: empty sample set");
+    if (!X || !T) throw Error(LANE_ERR_CONFIG, "sgd_stream: null data");
+    if (n_steps == 0) return;
+    const SgdPlan P = plan_persistent(net);
+    if (P.ok)
+        launch_persistent(net, P, X, T, n, order, n_steps, eta, loss_sum, correct);
+    else
+        stream_layer_path(net, X, T, n, order, n_steps, eta, loss_sum, correct, true);
+}
+
+}  // namespace
+
+// ============================================================ the ABI ===
+
+extern "C" {
+
+int lane_b200_abi_version(void) { return LANE_B200_ABI_VERSION; }
+
+const char* lane_b200_last_error(void) { return g_last_error.c_str(); }
+
+int lane_b200_ctx_create(int device, lane_b200_ctx** out) {
+    return guard([&] {
+        if (!out) throw Error(LANE_ERR_CONFIG, "null out");
+        int ndev = 0;
+        LANE_CUDA(cudaGetDeviceCount(&ndev));
+        if (device < 0 || device >= ndev) throw Error(LANE_ERR_CONFIG, "no such CUDA device");
+        LANE_CUDA(cudaSetDevice(device));
+        cudaDeviceProp prop{};
+        LANE_CUDA(cudaGetDeviceProperties(&prop, device));
+        if (prop.major != 10) throw Error(LANE_ERR_CONFIG, "lane_b200 is built for sm_100a (B200) only");
+        auto* c = new lane_b200_ctx();
+        c->device = device;
+        c->sm_count = prop.multiProcessorCount;
+        c->max_smem_optin = prop.sharedMemPerBlockOptin;
+        LANE_CUDA(cudaStreamCreateWithFlags(&c->stream, cudaStreamNonBlocking));
+        c->error_flag = static_cast<int*>(dev_alloc(sizeof(int)));
+        LANE_CUDA(cudaMemsetAsync(c->error_flag, 0, sizeof(int), c->stream));
+        if (const char* e = std::getenv("LANE_B200_NUMERICS"))
+            c->numerics = std::strcmp(e, "strict") == 0 ? LANE_NUMERICS_STRICT : LANE_NUMERICS_FAST;
+        *out = c;
+    });
+}
+
+int lane_b200_ctx_destroy(lane_b200_ctx* c) {
+    return guard([&] {
+        if (!c) return;
+        cudaSetDevice(c->device);
+        cudaStreamSynchronize(c->stream);
+        comm_destroy(c->comm);
+        for (void* p : c->scratch) cudaFree(p);
+        cudaFree(c->error_flag);
+        cudaStreamDestroy(c->stream);
+        delete c;
+    });
+}
+
+int lane_b200_ctx_set_numerics(lane_b200_ctx* c, int mode) {
+    return guard([&] {
+        if (!c || (mode != LANE_NUMERICS_STRICT && mode != LANE_NUMERICS_FAST))
+            throw Error(LANE_ERR_CONFIG, "bad numerics mode");
+        c->numerics = mode;
+    });
+}
+
+int lane_b200_ctx_get_numerics(lane_b200_ctx* c, int* mode) {
+    return guard([&] {
+        if (!c || !mode) throw Error(LANE_ERR_CONFIG, "null argument");
+        *mode = c->numerics;
+    });
+}
+
+int lane_b200_sync(lane_b200_ctx* c) {
+    return guard([&] {
+        if (!c) throw Error(LANE_ERR_CONFIG, "null context");
+        LANE_CUDA(cudaStreamSynchronize(c->stream));
+        c->check_device_error();
+    });
+}
+
+int lane_b200_ctx_stream(lane_b200_ctx* c, void** stream) {
+    return guard([&] {
+        if (!c || !stream) throw Error(LANE_ERR_CONFIG, "null argument");
+        *stream = c->stream;
+    });
+}
+
+int lane_b200_kernel_launches(lane_b200_ctx* c, uint64_t* count) {
+    return guard([&] {
+        if (!c || !count) throw Error(LANE_ERR_CONFIG, "null argument");
+        *count = c->launches;
+    });
+}
+
+int lane_b200_dev_alloc(lane_b200_ctx* c, size_t bytes, void** dev) {
+    return guard([&] {
+        if (!c || !dev) throw Error(LANE_ERR_CONFIG, "null argument");
+        LANE_CUDA(cudaSetDevice(c->device));
+        *dev = dev_alloc(bytes);
+        c->scratch.push_back(*dev);
+    });
+}
+
+int lane_b200_dev_free(lane_b200_ctx* c, void* dev) {
+    return guard([&] {
+        if (!c) throw Error(LANE_ERR_CONFIG, "null context");
+        auto it = std::find(c->scratch.begin(), c->scratch.end(), dev);
+        if (it == c->scratch.end()) throw Error(LANE_ERR_CONFIG, "pointer not owned by context");
+        LANE_CUDA(cudaStreamSynchronize(c->stream));
+        LANE_CUDA(cudaFree(dev));
+        c->scratch.erase(it);
+    });
+}
+
+int lane_b200_memcpy_h2d(lane_b200_ctx* c, void* dev, const void* host, size_t bytes) {
+    return guard([&] {
+        if (!c) throw Error(LANE_ERR_CONFIG, "null context");
+        LANE_CUDA(cudaMemcpyAsync(dev, host, bytes, cudaMemcpyHostToDevice, c->stream));
+    });
+}
+
+int lane_b200_memcpy_d2h(lane_b200_ctx* c, void* host, const void* dev, size_t bytes) {
+    return guard([&] {
+        if (!c) throw Error(LANE_ERR_CONFIG, "null context");
+        LANE_CUDA(cudaMemcpyAsync(host, dev, bytes, cudaMemcpyDeviceToHost, c->stream));
+        LANE_CUDA(cudaStreamSynchronize(c->stream));
+    });
+}
+
+// ---------------------------------------------------------------- net ---
+
+int lane_b200_net_create(lane_b200_ctx* c, size_t input_width, const size_t* hidden, size_t n_hidden,
+                         size_t classes, size_t max_batch, lane_b200_net** out) {
+    return guard([&] {
+        if (!c || !out) throw Error(LANE_ERR_CONFIG, "null argument");
+        // FeedForwardNetwork ctor validation (network.cpp:28-42)
+        if (input_width == 0) throw Error(LANE_ERR_CONFIG, "network: input_width must be >= 1");
+        if (classes < 2) throw Error(LANE_ERR_CONFIG, "network: need at least 2 classes");
+        for (size_t l = 0; l < n_hidden; ++l)
+            if (hidden[l] == 0) throw Error(LANE_ERR_CONFIG, "network: hidden layer size must be >= 1");
+        if (max_batch == 0) throw Error(LANE_ERR_CONFIG, "network: max_batch must be >= 1");
+        LANE_CUDA(cudaSetDevice(c->device));
+        auto* net = new lane_b200_net();
+        net->ctx = c;
+        net->input_width = input_width;
+        net->n_hidden = n_hidden;
+        net->classes = classes;
+        net->max_batch = max_batch;
+        size_t w = input_width;
+        for (size_t l = 0; l <= n_hidden; ++l) {
+            LayerBufs Ly;
+            Ly.I = w;
+            Ly.O = l < n_hidden ? hidden[l] : classes;
+            w = Ly.O;
+            net->layers.push_back(Ly);
+        }
+        // arena: params | grads | DW,db | per-sample vectors (x B rows)
+        auto pad = [](size_t n) { return (n + 63) & ~size_t(63); };  // 256-byte pieces
+        size_t off = 0;
+        std::vector<size_t> offs;
+        for (auto& Ly : net->layers) {
+            Ly.cnt[LANE_BUF_W] = Ly.cnt[LANE_BUF_G] = Ly.cnt[LANE_BUF_DW] = Ly.I * Ly.O;
+            Ly.cnt[LANE_BUF_B] = Ly.cnt[LANE_BUF_NETIN] = Ly.cnt[LANE_BUF_OUTPUTS] = Ly.cnt[LANE_BUF_DELTAS] =
+                Ly.cnt[LANE_BUF_DELTA_BIASES] = Ly.cnt[LANE_BUF_BIAS_GRAD] = Ly.O;
+            Ly.cnt[LANE_BUF_INPUTS] = Ly.I;
+        }
+        size_t params_begin = off;
+        for (auto& Ly : net->layers) {
+            offs.push_back(off); off += pad(Ly.I * Ly.O);  // W
+            offs.push_back(off); off += pad(Ly.O);         // b
+        }
+        net->params_count = off - params_begin;
+        size_t grads_begin = off;
+        for (auto& Ly : net->layers) {
+            offs.push_back(off); off += pad(Ly.I * Ly.O);  // G
+            offs.push_back(off); off += pad(Ly.O);         // bias grad
+        }
+        net->grads_count = off - grads_begin;
+        for (auto& Ly : net->layers) {
+            offs.push_back(off); off += pad(Ly.I * Ly.O);  // DW
+            offs.push_back(off); off += pad(Ly.O);         // db
+        }
+        for (auto& Ly : net->layers) {
+            offs.push_back(off); off += pad(Ly.I * max_batch);  // inputs
+            offs.push_back(off); off += pad(Ly.O * max_batch);  // netin
+            offs.push_back(off); off += pad(Ly.O * max_batch);  // outputs
+            offs.push_back(off); off += pad(Ly.O * max_batch);  // deltas
+        }
+        size_t stage_off = off;
+        off += pad(classes * max_batch);
+        net->arena_bytes = off * sizeof(float);
+        net->arena = static_cast<char*>(dev_alloc(net->arena_bytes));
+        LANE_CUDA(cudaMemsetAsync(net->arena, 0, net->arena_bytes, c->stream));
+        float* base = reinterpret_cast<float*>(net->arena);
+        size_t k = 0;
+        for (auto& Ly : net->layers) { Ly.buf[LANE_BUF_W] = base + offs[k++]; Ly.buf[LANE_BUF_B] = base + offs[k++]; }
+        for (auto& Ly : net->layers) { Ly.buf[LANE_BUF_G] = base + offs[k++]; Ly.buf[LANE_BUF_BIAS_GRAD] = base + offs[k++]; }
+        for (auto& Ly : net->layers) { Ly.buf[LANE_BUF_DW] = base + offs[k++]; Ly.buf[LANE_BUF_DELTA_BIASES] = base + offs[k++]; }
+        for (auto& Ly : net->layers) {
+            Ly.buf[LANE_BUF_INPUTS] = base + offs[k++];
+            Ly.buf[LANE_BUF_NETIN] = base + offs[k++];
+            Ly.buf[LANE_BUF_OUTPUTS] = base + offs[k++];
+            Ly.buf[LANE_BUF_DELTAS] = base + offs[k++];
+        }
+        net->params = base + params_begin;
+        net->grads = base + grads_begin;
+        net->target_stage = base + stage_off;
+        net->step = static_cast<long long*>(dev_alloc(sizeof(long long)));
+        net->loss_dev = static_cast<double*>(dev_alloc(sizeof(double)));
+        net->correct_dev = static_cast<unsigned long long*>(dev_alloc(sizeof(unsigned long long)));
+        // split-K partials of the FAST forward (sized up front: the forward is
+        // also captured into CUDA graphs, where allocation is not allowed)
+        size_t part = 0;
+        for (auto& Ly : net->layers) part = std::max(part, (2 * (size_t)c->sm_count + (Ly.O + 31) / 32) * 32);
+        ensure(net->scratch, net->scratch_count, part);
+        *out = net;
+    });
+}
+
+int lane_b200_net_init_seeded(lane_b200_net* net, uint64_t seed) {
+    return guard([&] {
+        if (!net) throw Error(LANE_ERR_CONFIG, "null network");
+        // build_network (network.cpp:55-66): hidden layers in order, then output
+        SplitMix64 rng(seed);
+        std::vector<float> host;
+        for (auto& Ly : net->layers) {
+            host.resize(Ly.I * Ly.O);
+            const float bound = 1.0f / std::sqrt(static_cast<float>(Ly.I));
+            for (float& v : host) v = rng.uniform(-bound, bound);
+            LANE_CUDA(cudaMemcpyAsync(Ly.buf[LANE_BUF_W], host.data(), host.size() * sizeof(float),
+                                      cudaMemcpyHostToDevice, net->ctx->stream));
+            LANE_CUDA(cudaMemsetAsync(Ly.buf[LANE_BUF_B], 0, Ly.O * sizeof(float), net->ctx->stream));
+            LANE_CUDA(cudaStreamSynchronize(net->ctx->stream));
+        }
+    });
+}
+
+int lane_b200_net_destroy(lane_b200_net* net) {
+    return guard([&] {
+        if (!net) return;
+        cudaSetDevice(net->ctx->device);
+        cudaStreamSynchronize(net->ctx->stream);
+        minibatch_free(net->mb);
+        cudaFree(net->arena);
+        cudaFree(net->scratch);
+        cudaFree(net->step);
+        cudaFree(net->loss_dev);
+        cudaFree(net->correct_dev);
+        cudaFree(net->slots);
+        cudaFree(net->data);
+        cudaFree(net->order);
+        delete net;
+    });
+}
+
+int lane_b200_net_shape(lane_b200_net* net, size_t layer, size_t* ci, size_t* co) {
+    return guard([&] {
+        check_layer(net, layer);
+        if (ci) *ci = net->L(layer).I;
+        if (co) *co = net->L(layer).O;
+    });
+}
+
+int lane_b200_net_n_layers(lane_b200_net* net, size_t* n) {
+    return guard([&] {
+        if (!net || !n) throw Error(LANE_ERR_CONFIG, "null argument");
+        *n = net->layers.size();
+    });
+}
+
+int lane_b200_buf_read(lane_b200_net* net, size_t layer, int buf, float* host, size_t count) {
+    return guard([&] {
+        check_layer(net, layer);
+        if (buf < 0 || buf >= LANE_BUF_COUNT) throw Error(LANE_ERR_CONFIG, "bad buffer id");
+        LayerBufs& Ly = net->L(layer);
+        if (count != Ly.cnt[buf]) throw Error(LANE_ERR_SHAPE, "buf_read: count mismatch");
+        LANE_CUDA(cudaMemcpyAsync(host, Ly.buf[buf], count * sizeof(float), cudaMemcpyDeviceToHost,
+                                  net->ctx->stream));
+        LANE_CUDA(cudaStreamSynchronize(net->ctx->stream));
+        net->ctx->check_device_error();
+    });
+}
+
+int lane_b200_buf_write(lane_b200_net* net, size_t layer, int buf, const float* host, size_t count) {
+    return guard([&] {
+        check_layer(net, layer);
+        if (buf < 0 || buf >= LANE_BUF_COUNT) throw Error(LANE_ERR_CONFIG, "bad buffer id");
+        LayerBufs& Ly = net->L(layer);
+        if (count != Ly.cnt[buf]) throw Error(LANE_ERR_SHAPE, "buf_write: count mismatch");
+        LANE_CUDA(cudaMemcpyAsync(Ly.buf[buf], host, count * sizeof(float), cudaMemcpyHostToDevice,
+                                  net->ctx->stream));
+        LANE_CUDA(cudaStreamSynchronize(net->ctx->stream));
+    });
+}
+
+int lane_b200_buf_device_ptr(lane_b200_net* net, size_t layer, int buf, float** dev, size_t* count) {
+    return guard([&] {
+        check_layer(net, layer);
+        if (buf < 0 || buf >= LANE_BUF_COUNT) throw Error(LANE_ERR_CONFIG, "bad buffer id");
+        if (dev) *dev = net->L(layer).buf[buf];
+        if (count) *count = net->L(layer).cnt[buf];
+    });
+}
+
+int lane_b200_net_hash(lane_b200_net* net, uint64_t* hash) {
+    return guard([&] {
+        if (!net || !hash) throw Error(LANE_ERR_CONFIG, "null argument");
+        uint64_t h = 0xcbf29ce484222325ULL;
+        std::vector<float> host;
+        for (auto& Ly : net->layers) {
+            for (int b : {LANE_BUF_W, LANE_BUF_B}) {
+                host.resize(Ly.cnt[b]);
+                LANE_CUDA(cudaMemcpyAsync(host.data(), Ly.buf[b], host.size() * sizeof(float),
+                                          cudaMemcpyDeviceToHost, net->ctx->stream));
+                LANE_CUDA(cudaStreamSynchronize(net->ctx->stream));
+                h = fnv1a64(host.data(), host.size() * sizeof(float), h);
+            }
+        }
+        net->ctx->check_device_error();
+        *hash = h;
+    });
+}
+
+// ---------------------------------------------------------- layer API ---
+
+int lane_b200_layer_forward(lane_b200_net* net, size_t layer, const float* x_host, size_t len) {
+    return guard([&] {
+        check_layer(net, layer);
+        LayerBufs& Ly = net->L(layer);
+        const float* src;
+        if (x_host) {
+            // compute_netin (layers.cpp:28-31)
+            if (len != Ly.I)
+                throw Error(LANE_ERR_SHAPE, "forward: input length " + std::to_string(len) +
+                                                " != cols_input " + std::to_string(Ly.I));
+            LANE_CUDA(cudaMemcpyAsync(Ly.buf[LANE_BUF_INPUTS], x_host, len * sizeof(float),
+                                      cudaMemcpyHostToDevice, net->ctx->stream));
+            src = Ly.buf[LANE_BUF_INPUTS];
+        } else {
+            if (layer == 0) throw Error(LANE_ERR_CONFIG, "forward: layer 0 needs an input vector");
+            src = net->L(layer - 1).buf[LANE_BUF_OUTPUTS];
+        }
+        run_layer_forward(net, layer, src);
+    });
+}
+
+int lane_b200_fc_backward(lane_b200_net* net, size_t layer, const float* nW_host, size_t rows,
+                          size_t cols, const float* nd_host, size_t nd_len, float eta) {
+    return guard([&] {
+        check_layer(net, layer);
+        check_eta(eta);
+        if (layer >= net->n_hidden) throw Error(LANE_ERR_CONFIG, "fc_backward: not a hidden layer");
+        LayerBufs& Ly = net->L(layer);
+        const float* nW;
+        const float* nd;
+        size_t N;
+        if (nW_host) {
+            // FullyConnectedLayer::backward shape checks (layers.cpp:53-58)
+            if (rows != Ly.O) throw Error(LANE_ERR_SHAPE, "fc backward: next_weights.rows != cols_out");
+            if (nd_len != cols) throw Error(LANE_ERR_SHAPE, "fc backward: next_deltas length != next_weights.cols");
+            ensure(net->scratch, net->scratch_count, rows * cols + cols);
+            LANE_CUDA(cudaMemcpyAsync(net->scratch, nW_host, rows * cols * sizeof(float),
+                                      cudaMemcpyHostToDevice, net->ctx->stream));
+            LANE_CUDA(cudaMemcpyAsync(net->scratch + rows * cols, nd_host, cols * sizeof(float),
+                                      cudaMemcpyHostToDevice, net->ctx->stream));
+            nW = net->scratch;
+            nd = net->scratch + rows * cols;
+            N = cols;
+        } else {
+            LayerBufs& nx = net->L(layer + 1);
+            nW = nx.buf[LANE_BUF_W];
+            nd = nx.buf[LANE_BUF_DELTAS];
+            N = nx.O;
+        }
+        run_fc_backward(net, layer, nW, nd, static_cast<int>(N), eta);
+        if (nW_host) LANE_CUDA(cudaStreamSynchronize(net->ctx->stream));  // scratch reuse
+    });
+}
+
+int lane_b200_softmax_backward(lane_b200_net* net, const float* t_host, size_t len, float eta) {
+    return guard([&] {
+        if (!net) throw Error(LANE_ERR_CONFIG, "null network");
+        check_eta(eta);
+        // SoftmaxOutputLayer::backward (layers.cpp:90-92)
+        if (len != net->classes) throw Error(LANE_ERR_SHAPE, "softmax backward: target length != cols_out");
+        LANE_CUDA(cudaMemcpyAsync(net->target_stage, t_host, len * sizeof(float), cudaMemcpyHostToDevice,
+                                  net->ctx->stream));
+        run_softmax_backward(net, net->target_stage, eta);
+    });
+}
+
+int lane_b200_apply_updates(lane_b200_net* net, size_t layer) {
+    return guard([&] {
+        check_layer(net, layer);
+        run_apply_updates(net, layer);
+    });
+}
+
+// -------------------------------------------------------- network API ---
+
+int lane_b200_forward(lane_b200_net* net, const float* x_host, float* probs_host) {
+    return guard([&] {
+        if (!net || !x_host) throw Error(LANE_ERR_CONFIG, "null argument");
+        LANE_CUDA(cudaMemcpyAsync(net->L(0).buf[LANE_BUF_INPUTS], x_host, net->input_width * sizeof(float),
+                                  cudaMemcpyHostToDevice, net->ctx->stream));
+        run_forward_chain(net);
+        if (probs_host) {
+            LANE_CUDA(cudaMemcpyAsync(probs_host, net->L(net->out_layer()).buf[LANE_BUF_OUTPUTS],
+                                      net->classes * sizeof(float), cudaMemcpyDeviceToHost, net->ctx->stream));
+            LANE_CUDA(cudaStreamSynchronize(net->ctx->stream));
+        }
+    });
+}
+
+int lane_b200_backward_plan_run(lane_b200_net* net, const float* t_host, float eta) {
+    return guard([&] {
+        if (!net || !t_host) throw Error(LANE_ERR_CONFIG, "null argument");
+        check_eta(eta);
+        LANE_CUDA(cudaMemcpyAsync(net->target_stage, t_host, net->classes * sizeof(float),
+                                  cudaMemcpyHostToDevice, net->ctx->stream));
+        run_backward_plan(net, net->target_stage, eta);
+    });
+}
+
+int lane_b200_sgd_stream(lane_b200_net* net, const float* X, const float* T, size_t n, const uint32_t* order,
+                         size_t n_steps, float eta, double* loss_sum, uint64_t* correct) {
+    return guard([&] {
+        if (!net) throw Error(LANE_ERR_CONFIG, "null network");
+        sgd_stream_impl(net, X, T, n, order, n_steps, eta, loss_sum,
+                        reinterpret_cast<unsigned long long*>(correct));
+    });
+}
+
+int lane_b200_train(lane_b200_net* net, const float* X_host, const float* T_host, size_t n, float eta,
+                    float max_error, size_t max_epochs, uint64_t seed, float* mean_loss_out,
+                    float* accuracy_out, size_t* epochs_run) {
+    return guard([&] {
+        if (!net) throw Error(LANE_ERR_CONFIG, "null network");
+        check_eta(eta);
+        // train (network.cpp:142-150)
+        if (n == 0) throw Error(LANE_ERR_TRAINING, "train: empty training set");
+        lane_b200_ctx* c = net->ctx;
+        const size_t I = net->input_width, C = net->classes;
+        ensure(net->data, net->data_count, n * (I + C));
+        if (net->order_count < n) {
+            if (net->order) LANE_CUDA(cudaFree(net->order));
+            net->order = static_cast<uint32_t*>(dev_alloc(n * sizeof(uint32_t)));
+            net->order_count = n;
+        }
+        float* Xd = net->data;
+        float* Td = net->data + n * I;
+        LANE_CUDA(cudaMemcpyAsync(Xd, X_host, n * I * sizeof(float), cudaMemcpyHostToDevice, c->stream));
+        LANE_CUDA(cudaMemcpyAsync(Td, T_host, n * C * sizeof(float), cudaMemcpyHostToDevice, c->stream));
+        SplitMix64 shuffle(seed);  // one generator for the whole run (network.cpp:153)
+        std::vector<uint32_t> order(n);
+        for (size_t k = 0; k < n; ++k) order[k] = static_cast<uint32_t>(k);
+        size_t ran = 0;
+        for (size_t epoch = 1; epoch <= max_epochs; ++epoch) {
+            for (size_t i = n; i > 1; --i) std::swap(order[i - 1], order[shuffle.below(i)]);
+            LANE_CUDA(cudaMemcpyAsync(net->order, order.data(), n * sizeof(uint32_t), cudaMemcpyHostToDevice,
+                                      c->stream));
+            LANE_CUDA(cudaMemsetAsync(net->loss_dev, 0, sizeof(double), c->stream));
+            LANE_CUDA(cudaMemsetAsync(net->correct_dev, 0, sizeof(unsigned long long), c->stream));
+            sgd_stream_impl(net, Xd, Td, n, net->order, n, eta, net->loss_dev, net->correct_dev);
+            double loss_sum = 0;
+            unsigned long long correct = 0;
+            LANE_CUDA(cudaMemcpyAsync(&loss_sum, net->loss_dev, sizeof(double), cudaMemcpyDeviceToHost, c->stream));
+            LANE_CUDA(cudaMemcpyAsync(&correct, net->correct_dev, sizeof(correct), cudaMemcpyDeviceToHost, c->stream));
+            LANE_CUDA(cudaStreamSynchronize(c->stream));
+            c->check_device_error();
+            const float mean_loss = static_cast<float>(loss_sum / static_cast<double>(n));
+            const float acc = static_cast<float>(correct) / static_cast<float>(n);
+            if (mean_loss_out) mean_loss_out[ran] = mean_loss;
+            if (accuracy_out) accuracy_out[ran] = acc;
+            ++ran;
+            if (mean_loss <= max_error) break;
+        }
+        if (epochs_run) *epochs_run = ran;
+    });
+}
+
+int lane_b200_evaluate(lane_b200_net* net, const float* X_host, const float* T_host, size_t n, float* mean_loss,
+                       float* accuracy) {
+    return guard([&] {
+        if (!net) throw Error(LANE_ERR_CONFIG, "null network");
+        // evaluate (network.cpp:186-191)
+        if (n == 0) throw Error(LANE_ERR_TRAINING, "evaluate: empty test set");
+        lane_b200_ctx* c = net->ctx;
+        const size_t I = net->input_width, C = net->classes;
+        ensure(net->data, net->data_count, n * (I + C));
+        float* Xd = net->data;
+        float* Td = net->data + n * I;
+        LANE_CUDA(cudaMemcpyAsync(Xd, X_host, n * I * sizeof(float), cudaMemcpyHostToDevice, c->stream));
+        LANE_CUDA(cudaMemcpyAsync(Td, T_host, n * C * sizeof(float), cudaMemcpyHostToDevice, c->stream));
+        LANE_CUDA(cudaMemsetAsync(net->loss_dev, 0, sizeof(double), c->stream));
+        LANE_CUDA(cudaMemsetAsync(net->correct_dev, 0, sizeof(unsigned long long), c->stream));
+        stream_layer_path(net, Xd, Td, n, nullptr, n, 1.0f, net->loss_dev, net->correct_dev, false);
+        double loss_sum = 0;
+        unsigned long long correct = 0;
+        LANE_CUDA(cudaMemcpyAsync(&loss_sum, net->loss_dev, sizeof(double), cudaMemcpyDeviceToHost, c->stream));
+        LANE_CUDA(cudaMemcpyAsync(&correct, net->correct_dev, sizeof(correct), cudaMemcpyDeviceToHost, c->stream));
+        LANE_CUDA(cudaStreamSynchronize(c->stream));
+        if (mean_loss) *mean_loss = static_cast<float>(loss_sum / static_cast<double>(n));
+        if (accuracy) *accuracy = static_cast<float>(correct) / static_cast<float>(n);
+    });
+}
+
+// ------------------------------------------------- mini-batch + comms ---
+
+int lane_b200_minibatch_step(lane_b200_net* net, const float* X, const float* T, size_t B, float eta, float mu,
+                             double* loss_sum) {
+    return guard([&] {
+        if (!net) throw Error(LANE_ERR_CONFIG, "null network");
+        check_eta(eta);
+        if (B == 0 || B > net->max_batch) throw Error(LANE_ERR_SHAPE, "minibatch: B must be in [1, max_batch]");
+        minibatch_step(*net->ctx, *net, X, T, B, eta, mu, loss_sum);
+    });
+}
+
+int lane_b200_nccl_unique_id(void* id_out, size_t id_bytes) {
+    return guard([&] { nccl_unique_id(id_out, id_bytes); });
+}
+
+int lane_b200_comm_init(lane_b200_ctx* c, int rank, int world, const void* id, size_t id_bytes) {
+    return guard([&] {
+        if (!c) throw Error(LANE_ERR_CONFIG, "null context");
+        LANE_CUDA(cudaSetDevice(c->device));
+        comm_init(c->comm, rank, world, id, id_bytes);
+    });
+}
+
+int lane_b200_comm_destroy(lane_b200_ctx* c) {
+    return guard([&] {
+        if (!c) throw Error(LANE_ERR_CONFIG, "null context");
+        comm_destroy(c->comm);
+    });
+}
+
+int lane_b200_allreduce_grads(lane_b200_net* net) {
+    return guard([&] {
+        if (!net) throw Error(LANE_ERR_CONFIG, "null network");
+        allreduce_grads(net->ctx->comm, net->grads, net->grads_count, net->ctx->stream);
+    });
+}
+
+}  // extern "C"

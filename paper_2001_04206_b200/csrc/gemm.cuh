@@ -1,0 +1,180 @@
+// gemm.cuh -- fp32 GEMMs of the mini-batch path with fused epilogues.
+//
+// Three operand layouts cover the whole step (row-major everywhere):
+//   NN  C[M,N] = A[M,K]   B[K,N]      forward   Z = X W
+//   NT  C[M,N] = A[M,K]   B[N,K]^T    dgrad     S = D' W'^T  (W' is O x O')
+//   TN  C[M,N] = A[K,M]^T B[K,N]      wgrad     G = X^T D
+// Epilogues: STORE, BIAS (+b[n]), BIAS_TANH (z and tanh(z)), TANH_GRAD
+// ((1 - a^2) * acc with a = aux[m,n]).
+//
+// This file holds the SIMT (CUDA-core FFMA) kernel: exact fp32 products with
+// fp32 accumulation, 128x128x8 tiles, 8x8 outputs per thread, double-buffered
+// shared memory.  gemm() dispatches large GEMMs to the tcgen05 3xTF32 kernel
+// (gemm_tc.cuh) when it is enabled and the shape qualifies.
+#pragma once
+
+#include "common.cuh"
+
+namespace lane_b200 {
+
+enum class GemmOp { NN, NT, TN };
+enum class Epi { STORE, BIAS, BIAS_TANH, TANH_GRAD };
+
+struct GemmCtx {
+    cudaStream_t stream;
+    int sm_count;
+    float** ws;
+    size_t* ws_count;
+    uint64_t* launches;
+};
+
+inline void ensure_ws(GemmCtx& g, size_t count) {
+    if (*g.ws_count >= count) return;
+    if (*g.ws) LANE_CUDA(cudaFree(*g.ws));
+    LANE_CUDA(cudaMalloc(reinterpret_cast<void**>(g.ws), count * sizeof(float)));
+    *g.ws_count = count;
+}
+
+template <Epi E>
+__device__ __forceinline__ void epilogue_store(int m, int n, int N, float acc, float* C, float* C2,
+                                               const float* bias, const float* aux) {
+    const size_t idx = (size_t)m * N + n;
+    if constexpr (E == Epi::STORE) {
+        C[idx] = acc;
+    } else if constexpr (E == Epi::BIAS) {
+        C[idx] = sadd(acc, bias[n]);
+    } else if constexpr (E == Epi::BIAS_TANH) {
+        const float z = sadd(acc, bias[n]);
+        C[idx] = z;
+        C2[idx] = lane_libm::tanhf(z);
+    } else {
+        C[idx] = tanh_grad(aux[idx], acc);
+    }
+}
+
+constexpr int kBM = 128, kBN = 128, kBK = 8;
+
+template <GemmOp OP, Epi E>
+__global__ void __launch_bounds__(256) k_gemm_simt(int M, int N, int K, const float* __restrict__ A,
+                                                   int lda, const float* __restrict__ B, int ldb,
+                                                   float* __restrict__ C, float* __restrict__ C2,
+                                                   const float* __restrict__ bias,
+                                                   const float* __restrict__ aux) {
+    __shared__ __align__(16) float As[2][kBK][kBM];
+    __shared__ __align__(16) float Bs[2][kBK][kBN];
+    const int tid = threadIdx.x;
+    const int m0 = blockIdx.y * kBM, n0 = blockIdx.x * kBN;
+    const int tx = tid % 16, ty = tid / 16;
+
+    float a_reg[4], b_reg[4];
+    auto load_tiles = [&](int k0) {
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+            if constexpr (OP == GemmOp::TN) {
+                // A[k*lda + m]: k = tid/32, m = (tid%32)*4 + u
+                const int k = k0 + tid / 32, m = m0 + (tid % 32) * 4 + u;
+                a_reg[u] = (k < K && m < M) ? A[(size_t)k * lda + m] : 0.0f;
+            } else {
+                // A[m*lda + k]: m = tid/2, k = (tid%2)*4 + u
+                const int m = m0 + tid / 2, k = k0 + (tid % 2) * 4 + u;
+                a_reg[u] = (k < K && m < M) ? A[(size_t)m * lda + k] : 0.0f;
+            }
+            if constexpr (OP == GemmOp::NT) {
+                // B[n*ldb + k]: n = tid/2, k = (tid%2)*4 + u
+                const int n = n0 + tid / 2, k = k0 + (tid % 2) * 4 + u;
+                b_reg[u] = (k < K && n < N) ? B[(size_t)n * ldb + k] : 0.0f;
+            } else {
+                // B[k*ldb + n]: k = tid/32, n = (tid%32)*4 + u
+                const int k = k0 + tid / 32, n = n0 + (tid % 32) * 4 + u;
+                b_reg[u] = (k < K && n < N) ? B[(size_t)k * ldb + n] : 0.0f;
+            }
+        }
+    };
+    auto store_tiles = [&](int buf) {
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+            if constexpr (OP == GemmOp::TN) As[buf][tid / 32][(tid % 32) * 4 + u] = a_reg[u];
+            else As[buf][(tid % 2) * 4 + u][tid / 2] = a_reg[u];
+            if constexpr (OP == GemmOp::NT) Bs[buf][(tid % 2) * 4 + u][tid / 2] = b_reg[u];
+            else Bs[buf][tid / 32][(tid % 32) * 4 + u] = b_reg[u];
+        }
+    };
+
+    float acc[8][8];
+#pragma unroll
+    for (int i = 0; i < 8; ++i)
+#pragma unroll
+        for (int j = 0; j < 8; ++j) acc[i][j] = 0.0f;
+
+    load_tiles(0);
+    store_tiles(0);
+    __syncthreads();
+    int buf = 0;
+    for (int k0 = 0; k0 < K; k0 += kBK) {
+        const bool more = k0 + kBK < K;
+        if (more) load_tiles(k0 + kBK);
+#pragma unroll
+        for (int kk = 0; kk < kBK; ++kk) {
+            const float4 a0 = *reinterpret_cast<const float4*>(&As[buf][kk][ty * 4]);
+            const float4 a1 = *reinterpret_cast<const float4*>(&As[buf][kk][64 + ty * 4]);
+            const float4 b0 = *reinterpret_cast<const float4*>(&Bs[buf][kk][tx * 4]);
+            const float4 b1 = *reinterpret_cast<const float4*>(&Bs[buf][kk][64 + tx * 4]);
+            const float av[8] = {a0.x, a0.y, a0.z, a0.w, a1.x, a1.y, a1.z, a1.w};
+            const float bv[8] = {b0.x, b0.y, b0.z, b0.w, b1.x, b1.y, b1.z, b1.w};
+#pragma unroll
+            for (int i = 0; i < 8; ++i)
+#pragma unroll
+                for (int j = 0; j < 8; ++j) acc[i][j] = fmaf(av[i], bv[j], acc[i][j]);
+        }
+        if (more) {
+            store_tiles(buf ^ 1);
+            __syncthreads();
+            buf ^= 1;
+        }
+    }
+#pragma unroll
+    for (int i = 0; i < 8; ++i) {
+        const int m = m0 + (i < 4 ? ty * 4 + i : 64 + ty * 4 + (i - 4));
+        if (m >= M) continue;
+#pragma unroll
+        for (int j = 0; j < 8; ++j) {
+            const int n = n0 + (j < 4 ? tx * 4 + j : 64 + tx * 4 + (j - 4));
+            if (n < N) epilogue_store<E>(m, n, N, acc[i][j], C, C2, bias, aux);
+        }
+    }
+}
+
+template <GemmOp OP>
+void gemm_simt_dispatch(GemmCtx& g, int M, int N, int K, const float* A, int lda, const float* B, int ldb,
+                        Epi e, float* C, float* C2, const float* bias, const float* aux) {
+    const dim3 grid((N + kBN - 1) / kBN, (M + kBM - 1) / kBM);
+    switch (e) {
+        case Epi::STORE:
+            k_gemm_simt<OP, Epi::STORE><<<grid, 256, 0, g.stream>>>(M, N, K, A, lda, B, ldb, C, C2, bias, aux);
+            break;
+        case Epi::BIAS:
+            k_gemm_simt<OP, Epi::BIAS><<<grid, 256, 0, g.stream>>>(M, N, K, A, lda, B, ldb, C, C2, bias, aux);
+            break;
+        case Epi::BIAS_TANH:
+            k_gemm_simt<OP, Epi::BIAS_TANH><<<grid, 256, 0, g.stream>>>(M, N, K, A, lda, B, ldb, C, C2, bias,
+                                                                         aux);
+            break;
+        case Epi::TANH_GRAD:
+            k_gemm_simt<OP, Epi::TANH_GRAD><<<grid, 256, 0, g.stream>>>(M, N, K, A, lda, B, ldb, C, C2, bias,
+                                                                         aux);
+            break;
+    }
+    *g.launches += 1;
+}
+
+inline void gemm(GemmCtx& g, GemmOp op, int M, int N, int K, const float* A, int lda, const float* B, int ldb,
+                 Epi e, float* C, float* C2, const float* bias, const float* aux) {
+    if (M <= 0 || N <= 0) return;
+    switch (op) {
+        case GemmOp::NN: gemm_simt_dispatch<GemmOp::NN>(g, M, N, K, A, lda, B, ldb, e, C, C2, bias, aux); break;
+        case GemmOp::NT: gemm_simt_dispatch<GemmOp::NT>(g, M, N, K, A, lda, B, ldb, e, C, C2, bias, aux); break;
+        case GemmOp::TN: gemm_simt_dispatch<GemmOp::TN>(g, M, N, K, A, lda, B, ldb, e, C, C2, bias, aux); break;
+    }
+}
+
+}  // namespace lane_b200

@@ -1,0 +1,222 @@
+// minibatch.cuh -- the mini-batch / momentum / data-parallel extension
+// (SURVEY.md 8a row a15, 8e).  Not in the reference; defined so
+// that B=1, mu=0 reduces to BackwardPlan::run (oracle/lane_oracle.c
+// lo_minibatch_step):
+//     G  = (1/B_global) * sum_b delta_b (x) x_b
+//     DW = mu*DW + (-eta)*G   (DW = (-eta)*G when mu == 0)
+//     W += DW ;  biases likewise.
+// Per layer the step is three GEMMs -- forward Z = X W (+b, tanh), dgrad
+// S = D' W'^T (x tanh'), wgrad G = X^T D -- plus a row softmax and the update.
+// Data parallel: each rank runs its local batch, the flat gradient-sum buffer
+// (G and bias sums of every layer, contiguous) is summed with ONE NCCL fp32
+// allreduce, then every rank applies the identical update.
+#pragma once
+
+#include <nccl.h>
+
+#include <cstring>
+
+#include "common.cuh"
+#include "gemm.cuh"
+
+namespace lane_b200 {
+
+#define LANE_NCCL(call)                                                                   \
+    do {                                                                                  \
+        ncclResult_t r_ = (call);                                                         \
+        if (r_ != ncclSuccess)                                                            \
+            throw ::lane_b200::Error(LANE_ERR_NCCL, std::string(#call) + ": " +           \
+                                                        ncclGetErrorString(r_));          \
+    } while (0)
+
+struct MinibatchComm {
+    ncclComm_t comm = nullptr;
+    int rank = 0, world = 1;
+};
+
+struct MinibatchState {
+    float* ws = nullptr;  // GEMM workspace (split-K partials / 3xTF32 splits)
+    size_t ws_count = 0;
+};
+
+inline void minibatch_free(MinibatchState& s) {
+    if (s.ws) cudaFree(s.ws);
+    s.ws = nullptr;
+    s.ws_count = 0;
+}
+
+inline void nccl_unique_id(void* out, size_t bytes) {
+    if (!out || bytes < sizeof(ncclUniqueId)) throw Error(LANE_ERR_CONFIG, "unique id buffer too small");
+    ncclUniqueId id;
+    LANE_NCCL(ncclGetUniqueId(&id));
+    std::memcpy(out, &id, sizeof(id));
+}
+
+inline void comm_init(MinibatchComm& c, int rank, int world, const void* id, size_t bytes) {
+    if (world < 1 || rank < 0 || rank >= world) throw Error(LANE_ERR_CONFIG, "bad rank/world");
+    if (!id || bytes < sizeof(ncclUniqueId)) throw Error(LANE_ERR_CONFIG, "bad unique id");
+    if (c.comm) {
+        ncclCommDestroy(c.comm);
+        c.comm = nullptr;
+    }
+    ncclUniqueId uid;
+    std::memcpy(&uid, id, sizeof(uid));
+    LANE_NCCL(ncclCommInitRank(&c.comm, world, uid, rank));
+    c.rank = rank;
+    c.world = world;
+}
+
+inline void comm_destroy(MinibatchComm& c) {
+    if (c.comm) ncclCommDestroy(c.comm);
+    c.comm = nullptr;
+    c.rank = 0;
+    c.world = 1;
+}
+
+inline void allreduce_grads(MinibatchComm& c, float* grads, size_t count, cudaStream_t stream) {
+    if (!c.comm || c.world == 1) return;
+    LANE_NCCL(ncclAllReduce(grads, grads, count, ncclFloat32, ncclSum, c.comm, stream));
+}
+
+// ------------------------------------------------------------- kernels ---
+
+// Row softmax + output deltas + cross entropy for a batch (one warp per row,
+// C <= 128): P = softmax(Z + b) (Z already has the bias), D = P - T,
+// loss_sum += sum_rows CE (double, row order via a serial final pass).
+__global__ void k_softmax_rows(const float* __restrict__ Z, float* __restrict__ P,
+                               const float* __restrict__ T, float* __restrict__ D,
+                               float* __restrict__ row_loss, int B, int C) {
+    const int warp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5, lane = threadIdx.x & 31;
+    if (warp >= B) return;
+    const float* z = Z + (size_t)warp * C;
+    const float* t = T + (size_t)warp * C;
+    float e[4];
+    float m = -INFINITY;
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+        const int k = lane + 32 * q;
+        if (k < C) m = fmaxf(m, z[k]);
+    }
+    m = warp_max(m);
+    float s = 0.0f;
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+        const int k = lane + 32 * q;
+        e[q] = k < C ? lane_libm::expf(ssub(z[k], m)) : 0.0f;
+        s += e[q];
+    }
+    s = warp_sum(s);
+    float loss = 0.0f;
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+        const int k = lane + 32 * q;
+        if (k < C) {
+            const float p = __fdiv_rn(e[q], s);
+            P[(size_t)warp * C + k] = p;
+            D[(size_t)warp * C + k] = ssub(p, t[k]);
+            if (t[k] != 0.0f) loss = smul(t[k], lane_libm::logf(p < 1e-12f ? 1e-12f : p));
+        }
+    }
+    loss = warp_sum(loss);
+    if (lane == 0 && row_loss) row_loss[warp] = -loss;
+}
+
+__global__ void k_loss_rows(const float* __restrict__ row_loss, int B, double* loss_sum) {
+    if (threadIdx.x != 0 || blockIdx.x != 0 || !loss_sum) return;
+    double s = *loss_sum;
+    for (int b = 0; b < B; ++b) s += (double)row_loss[b];
+    *loss_sum = s;
+}
+
+// Column sums of D (B x O): gb[o] = sum_b D[b][o]  (bias-gradient sums).
+__global__ void k_colsum(const float* __restrict__ D, float* __restrict__ gb, int B, int O) {
+    const int o = blockIdx.x * blockDim.x + threadIdx.x;
+    if (o >= O) return;
+    float s = 0.0f;
+    for (int b = 0; b < B; ++b) s += D[(size_t)b * O + o];
+    gb[o] = s;
+}
+
+// Momentum SGD on a flat range: g = gsum * invB; DW = mu*DW + (-eta)*g;
+// W += DW.  Writes the mean gradient back to gsum (LANE_BUF_G semantics).
+__global__ void k_momentum_update(float* __restrict__ W, float* __restrict__ DW,
+                                  float* __restrict__ gsum, size_t n, float invB, float neg_eta,
+                                  float mu) {
+    for (size_t e = (size_t)blockIdx.x * blockDim.x + threadIdx.x; e < n;
+         e += (size_t)gridDim.x * blockDim.x) {
+        const float g = smul(gsum[e], invB);
+        gsum[e] = g;
+        const float step = smul(neg_eta, g);
+        const float dw = mu == 0.0f ? step : sadd(smul(mu, DW[e]), step);
+        DW[e] = dw;
+        W[e] = sadd(W[e], dw);
+    }
+}
+
+// --------------------------------------------------------------- driver ---
+
+template <class Ctx, class Net>
+void minibatch_step(Ctx& c, Net& net, const float* X, const float* T, size_t Bsz, float eta,
+                    float mu, double* loss_sum) {
+    const int B = static_cast<int>(Bsz);
+    const int nl = static_cast<int>(net.layers.size());
+    const int C = static_cast<int>(net.classes);
+    if (C > 128) throw Error(LANE_ERR_CONFIG, "minibatch: classes must be <= 128");
+    cudaStream_t st = c.stream;
+    GemmCtx g{c.stream, c.sm_count, &net.mb.ws, &net.mb.ws_count, &c.launches};
+    // cache the batch as the first layer's inputs (LayerState::inputs)
+    LANE_CUDA(cudaMemcpyAsync(net.L(0).buf[LANE_BUF_INPUTS], X, Bsz * net.input_width * sizeof(float),
+                              cudaMemcpyDeviceToDevice, st));
+    // forward
+    for (int l = 0; l < nl; ++l) {
+        auto& Ly = net.L(l);
+        // layer l > 0 reads the previous layer's outputs in place (no copy)
+        const float* in = l == 0 ? net.L(0).buf[LANE_BUF_INPUTS] : net.L(l - 1).buf[LANE_BUF_OUTPUTS];
+        const bool last = l == nl - 1;
+        gemm(g, GemmOp::NN, B, (int)Ly.O, (int)Ly.I, in, (int)Ly.I, Ly.buf[LANE_BUF_W], (int)Ly.O,
+             last ? Epi::BIAS : Epi::BIAS_TANH, Ly.buf[LANE_BUF_NETIN], Ly.buf[LANE_BUF_OUTPUTS],
+             Ly.buf[LANE_BUF_B], nullptr);
+    }
+    auto& out = net.L(nl - 1);
+    LANE_CUDA(cudaMemcpyAsync(net.target_stage, T, Bsz * C * sizeof(float), cudaMemcpyDeviceToDevice, st));
+    ensure_ws(g, (size_t)B);  // per-row losses live in the GEMM workspace between GEMMs
+    k_softmax_rows<<<(B * 32 + 255) / 256, 256, 0, st>>>(out.buf[LANE_BUF_NETIN], out.buf[LANE_BUF_OUTPUTS],
+                                                          net.target_stage, out.buf[LANE_BUF_DELTAS],
+                                                          net.mb.ws, B, C);
+    k_loss_rows<<<1, 32, 0, st>>>(net.mb.ws, B, loss_sum);
+    c.launches += 2;
+    // dgrad (pre-update weights): D_l = (D_{l+1} W_{l+1}^T) * (1 - A_l^2)
+    for (int l = nl - 2; l >= 0; --l) {
+        auto& Ly = net.L(l);
+        auto& nx = net.L(l + 1);
+        gemm(g, GemmOp::NT, B, (int)Ly.O, (int)nx.O, nx.buf[LANE_BUF_DELTAS], (int)nx.O, nx.buf[LANE_BUF_W],
+             (int)nx.O, Epi::TANH_GRAD, Ly.buf[LANE_BUF_DELTAS], nullptr, nullptr, Ly.buf[LANE_BUF_OUTPUTS]);
+    }
+    // wgrad sums: G_l = X_l^T D_l ; gb_l = colsum(D_l)
+    for (int l = 0; l < nl; ++l) {
+        auto& Ly = net.L(l);
+        const float* in = l == 0 ? net.L(0).buf[LANE_BUF_INPUTS] : net.L(l - 1).buf[LANE_BUF_OUTPUTS];
+        gemm(g, GemmOp::TN, (int)Ly.I, (int)Ly.O, B, in, (int)Ly.I,
+             Ly.buf[LANE_BUF_DELTAS], (int)Ly.O, Epi::STORE, Ly.buf[LANE_BUF_G], nullptr, nullptr, nullptr);
+        k_colsum<<<((int)Ly.O + 127) / 128, 128, 0, st>>>(Ly.buf[LANE_BUF_DELTAS], Ly.buf[LANE_BUF_BIAS_GRAD],
+                                                          B, (int)Ly.O);
+        c.launches += 1;
+    }
+    // data parallel: one allreduce of the flat gradient-sum buffer
+    allreduce_grads(c.comm, net.grads, net.grads_count, st);
+    const float invB = 1.0f / static_cast<float>(Bsz * static_cast<size_t>(c.comm.world));
+    for (int l = 0; l < nl; ++l) {
+        auto& Ly = net.L(l);
+        const size_t n = Ly.I * Ly.O;
+        k_momentum_update<<<std::min<size_t>(8 * c.sm_count, (n + 255) / 256), 256, 0, st>>>(
+            Ly.buf[LANE_BUF_W], Ly.buf[LANE_BUF_DW], Ly.buf[LANE_BUF_G], n, invB, -eta, mu);
+        k_momentum_update<<<((int)Ly.O + 255) / 256, 256, 0, st>>>(Ly.buf[LANE_BUF_B],
+                                                                   Ly.buf[LANE_BUF_DELTA_BIASES],
+                                                                   Ly.buf[LANE_BUF_BIAS_GRAD], Ly.O, invB,
+                                                                   -eta, mu);
+        c.launches += 2;
+    }
+    c.check_launch();
+}
+
+}  // namespace lane_b200

@@ -1,0 +1,403 @@
+// sgd_persistent.cuh -- fused online-SGD for the reference's one-hidden-layer
+// topology (tanh FC -> softmax/CE), batch 1, as ONE persistent kernel.
+//
+// Reference per sample (network.cpp:164-170 -> :122-138, layers.hpp:28-61,
+// layers.cpp:18-49, :71-87):
+//   forward:  z0 = x W0 + b0, a = tanh(z0);  z1 = a W1 + b1, p = softmax(z1)
+//   backward: d1 = p - t;  d0 = (1 - a^2) * (W1 d1)   (pre-update W1)
+//   update:   W1 += -eta (a (x) d1); b1 += -eta d1; W0 += -eta (x (x) d0); b0 += -eta d0
+//
+// B200 design:
+//  * The hidden neurons are partitioned across G co-resident CTAs (cooperative
+//    launch).  CTA c owns columns [h0, h1) of W0 and the matching rows of W1;
+//    both slices live in SHARED MEMORY for the whole sample stream (weights
+//    never touch HBM between samples; up to ~29 MB across 148 SMs).
+//  * Everything except the 10-wide logit reduction is CTA-local.  Each sample
+//    needs exactly one cross-CTA exchange: every CTA publishes its C partial
+//    logits as 64-bit {value, sample-tag} words (single-copy atomic, so the
+//    tag doubles as the arrival flag -- no separate barrier), then every CTA
+//    gathers all G*C words from L2 and reduces them in a fixed order, so all
+//    CTAs hold bit-identical logits / probabilities / output deltas.
+//  * The update of sample s is applied lazily while sample s+1 streams the
+//    same smem weights through its forward dot products (one read-modify-write
+//    pass over each weight per sample, the algorithmic minimum).  The update
+//    arithmetic is the reference's exactly: w + (-eta * (delta * x)), three
+//    separately rounded operations.
+//  * The next sample's x/t rows are prefetched with cp.async into a triple
+//    buffer (x(s-1) for the lazy update, x(s) for the forward, x(s+1) landing).
+//  * tanh/exp/log are the bit-exact glibc restatements (lane_libm.cuh).  The
+//    dot products are FMA trees (FAST numerics); STRICT numerics use the
+//    layer-kernel path instead.
+#pragma once
+
+#include "common.cuh"
+
+namespace lane_b200 {
+
+constexpr int kSgdThreads = 256;
+constexpr int kSgdWarps = kSgdThreads / 32;
+constexpr int kSgdMaxC = 128;  // logits per lane: kSgdMaxC / 32
+
+struct SgdArgs {
+    int I, H, C;
+    int G;    // co-resident CTAs
+    int npc;  // hidden neurons per CTA (max)
+    int wpn;  // warps cooperating on one neuron's forward dot product
+    const float* X;
+    const float* T;
+    const uint32_t* order;
+    long long n, n_steps;
+    float neg_eta;
+    float *W0, *b0, *W1, *b1;
+    unsigned long long* slots;  // [2][G][C] {value bits | tag << 32}
+    // reference LayerState buffers after the last sample
+    float *x0, *z0, *a0, *d0, *db0;  // hidden layer
+    float *x1, *z1, *a1, *d1, *db1;  // output layer
+    double* loss_sum;
+    unsigned long long* correct;
+    int* error;  // set to 1 when an exchange times out (bug guard, never hangs)
+};
+
+struct SgdSmem {
+    int I, C, Ip, Cp, npc, wpn, G;
+    size_t w0s, w1s, xb, tb, b0s, z0s, a0s, ap, dp, b1s, zl, pl, dl, gat, red, red1, total;
+    __host__ __device__ SgdSmem(int I_, int C_, int npc_, int wpn_, int G_)
+        : I(I_), C(C_), npc(npc_), wpn(wpn_), G(G_) {
+        Ip = (I + 3) & ~3;
+        Cp = (C + 3) & ~3;
+        size_t o = 0;
+        auto take = [&](size_t n) {
+            size_t at = o;
+            o += (n + 3) & ~size_t(3);  // 16-byte aligned pieces
+            return at;
+        };
+        w0s = take((size_t)npc * I);
+        w1s = take((size_t)npc * C);
+        xb = take(3 * (size_t)Ip);
+        tb = take(3 * (size_t)Cp);
+        b0s = take(npc);
+        z0s = take(npc);
+        a0s = take(npc);
+        ap = take(npc);
+        dp = take(npc);
+        b1s = take(Cp);
+        zl = take(Cp);
+        pl = take(Cp);
+        dl = take(Cp);
+        gat = take((size_t)G * C);
+        red = take((size_t)npc * 8);
+        red1 = take((size_t)kSgdWarps * Cp);
+        total = o * sizeof(float);
+    }
+};
+
+__device__ __forceinline__ uint32_t smem_u32(const void* p) {
+    return static_cast<uint32_t>(__cvta_generic_to_shared(p));
+}
+__device__ __forceinline__ void cp_async4(void* s, const void* g) {
+    asm volatile("cp.async.ca.shared.global [%0], [%1], 4;\n" ::"r"(smem_u32(s)), "l"(g));
+}
+__device__ __forceinline__ void cp_async16(void* s, const void* g) {
+    asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(smem_u32(s)), "l"(g));
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;\n"); }
+template <int N>
+__device__ __forceinline__ void cp_async_wait() {
+    asm volatile("cp.async.wait_group %0;\n" ::"n"(N));
+}
+__device__ __forceinline__ unsigned long long ld_relaxed_u64(const unsigned long long* p) {
+    unsigned long long v;
+    asm volatile("ld.relaxed.gpu.global.u64 %0, [%1];\n" : "=l"(v) : "l"(p));
+    return v;
+}
+__device__ __forceinline__ void st_relaxed_u64(unsigned long long* p, unsigned long long v) {
+    asm volatile("st.relaxed.gpu.global.u64 [%0], %1;\n" ::"l"(p), "l"(v));
+}
+__device__ __forceinline__ unsigned long long globaltimer_ns() {
+    unsigned long long t;
+    asm volatile("mov.u64 %0, %%globaltimer;\n" : "=l"(t));
+    return t;
+}
+
+// Issue the cp.async copies of sample row k into the smem slot.
+__device__ __forceinline__ void prefetch_sample(const SgdArgs& A, long long s, float* xdst,
+                                                float* tdst) {
+    const long long k = A.order ? (long long)A.order[s] : s % A.n;
+    const float* xs = A.X + k * A.I;
+    const float* ts = A.T + k * A.C;
+    const bool vec = ((A.I & 3) == 0) && ((reinterpret_cast<uintptr_t>(xs) & 15) == 0);
+    if (vec) {
+        for (int q = threadIdx.x; q < (A.I >> 2); q += kSgdThreads) cp_async16(xdst + 4 * q, xs + 4 * q);
+    } else {
+        for (int i = threadIdx.x; i < A.I; i += kSgdThreads) cp_async4(xdst + i, xs + i);
+    }
+    for (int c = threadIdx.x; c < A.C; c += kSgdThreads) cp_async4(tdst + c, ts + c);
+}
+
+__global__ void __launch_bounds__(kSgdThreads, 1) k_sgd_persistent(SgdArgs A) {
+    extern __shared__ __align__(16) float sm[];
+    const SgdSmem L(A.I, A.C, A.npc, A.wpn, A.G);
+    float* w0s = sm + L.w0s;
+    float* w1s = sm + L.w1s;
+    float* b0s = sm + L.b0s;
+    float* z0s = sm + L.z0s;
+    float* a0s = sm + L.a0s;
+    float* ap = sm + L.ap;
+    float* dp = sm + L.dp;
+    float* b1s = sm + L.b1s;
+    float* zl = sm + L.zl;
+    float* pl = sm + L.pl;
+    float* dl = sm + L.dl;
+    float* gat = sm + L.gat;
+    float* red = sm + L.red;
+    float* red1 = sm + L.red1;
+    __shared__ int s_abort;
+
+    const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+    const int I = A.I, H = A.H, C = A.C, G = A.G, cta = blockIdx.x;
+    const int h0 = min(H, cta * A.npc), h1 = min(H, h0 + A.npc), nloc = h1 - h0;
+    const float neg_eta = A.neg_eta;
+    const int wpn = A.wpn, nper = kSgdWarps / wpn;
+
+    // ---- stage this CTA's weight slices into shared memory (once) ----
+    for (int e = tid; e < nloc * I; e += kSgdThreads) {
+        const int j = e / I, i = e - j * I;
+        w0s[e] = A.W0[(size_t)i * H + h0 + j];
+    }
+    for (int e = tid; e < nloc * C; e += kSgdThreads) w1s[e] = A.W1[(size_t)h0 * C + e];
+    for (int j = tid; j < nloc; j += kSgdThreads) b0s[j] = A.b0[h0 + j];
+    for (int k = tid; k < C; k += kSgdThreads) b1s[k] = A.b1[k];
+    if (tid == 0) s_abort = 0;
+    double loss_acc = 0.0;
+    unsigned long long correct_acc = 0;
+    if (cta == 0 && tid == 0 && A.loss_sum) loss_acc = *A.loss_sum;
+
+    if (A.n_steps > 0) prefetch_sample(A, 0, sm + L.xb, sm + L.tb);
+    cp_async_commit();
+    __syncthreads();
+
+    long long s = 0;
+    for (; s < A.n_steps; ++s) {
+        const int cur = (int)(s % 3), prv = (int)((s + 2) % 3), nxt = (int)((s + 1) % 3);
+        const float* xc = sm + L.xb + (size_t)cur * L.Ip;
+        const float* xp = sm + L.xb + (size_t)prv * L.Ip;
+        const float* tc = sm + L.tb + (size_t)cur * L.Cp;
+        const bool lazy = s > 0;
+        if (s + 1 < A.n_steps)
+            prefetch_sample(A, s + 1, sm + L.xb + (size_t)nxt * L.Ip, sm + L.tb + (size_t)nxt * L.Cp);
+        cp_async_commit();
+        cp_async_wait<1>();
+        __syncthreads();
+
+        // ---- hidden forward with the lazy W0 update of sample s-1 ----
+        for (int r = 0; r * nper < nloc; ++r) {
+            const int jl = r * nper + warp / wpn, part = warp % wpn;
+            if (jl < nloc) {
+                const int i0 = (int)((long long)part * I / wpn), i1 = (int)((long long)(part + 1) * I / wpn);
+                float* wrow = w0s + (size_t)jl * I;
+                float acc = 0.0f;
+                if (lazy) {
+                    const float dj = dp[jl];
+                    for (int i = i0 + lane; i < i1; i += 32) {
+                        const float w = sgd_apply(wrow[i], neg_eta, dj, xp[i]);
+                        wrow[i] = w;
+                        acc = fmaf(xc[i], w, acc);
+                    }
+                } else {
+                    for (int i = i0 + lane; i < i1; i += 32) acc = fmaf(xc[i], wrow[i], acc);
+                }
+                acc = warp_sum(acc);
+                if (lane == 0) red[jl * wpn + part] = acc;
+            }
+        }
+        __syncthreads();
+        for (int j = tid; j < nloc; j += kSgdThreads) {
+            if (lazy) b0s[j] = sadd(b0s[j], smul(neg_eta, dp[j]));
+            float z = red[j * wpn];
+            for (int p = 1; p < wpn; ++p) z += red[j * wpn + p];
+            z = sadd(z, b0s[j]);
+            z0s[j] = z;
+            a0s[j] = lane_libm::tanhf(z);
+        }
+        __syncthreads();
+
+        // ---- partial logits with the lazy W1 update of sample s-1 ----
+        {
+            float acc[kSgdMaxC / 32];
+#pragma unroll
+            for (int m = 0; m < kSgdMaxC / 32; ++m) acc[m] = 0.0f;
+            for (int j = warp; j < nloc; j += kSgdWarps) {
+                const float aj = a0s[j], apj = ap[j];
+                float* wrow = w1s + (size_t)j * C;
+#pragma unroll
+                for (int m = 0; m < kSgdMaxC / 32; ++m) {
+                    const int k = lane + 32 * m;
+                    if (k < C) {
+                        float w = wrow[k];
+                        if (lazy) {
+                            w = sgd_apply(w, neg_eta, dl[k], apj);
+                            wrow[k] = w;
+                        }
+                        acc[m] = fmaf(aj, w, acc[m]);
+                    }
+                }
+            }
+#pragma unroll
+            for (int m = 0; m < kSgdMaxC / 32; ++m) {
+                const int k = lane + 32 * m;
+                if (k < C) red1[warp * L.Cp + k] = acc[m];
+            }
+        }
+        __syncthreads();
+        const uint32_t tag = (uint32_t)(s + 1);
+        unsigned long long* slot = A.slots + (size_t)(s & 1) * G * C;
+        for (int k = tid; k < C; k += kSgdThreads) {
+            float P = red1[k];
+            for (int w = 1; w < kSgdWarps; ++w) P += red1[w * L.Cp + k];
+            st_relaxed_u64(slot + (size_t)cta * C + k,
+                           ((unsigned long long)tag << 32) | __float_as_uint(P));
+            if (lazy) b1s[k] = sadd(b1s[k], smul(neg_eta, dl[k]));
+        }
+
+        // ---- exchange: gather every CTA's partial logits (tag == arrival) ----
+        // Up to 8 independent L2 loads in flight per thread; re-poll only the
+        // words whose tag has not arrived yet.
+        {
+            const unsigned long long t0 = globaltimer_ns();
+            const int GC = G * C;
+            for (int base = tid; base < GC; base += kSgdThreads * 8) {
+                unsigned long long v[8];
+#pragma unroll
+                for (int u = 0; u < 8; ++u) {
+                    const int e = base + u * kSgdThreads;
+                    v[u] = e < GC ? ld_relaxed_u64(slot + e) : ((unsigned long long)tag << 32);
+                }
+#pragma unroll
+                for (int u = 0; u < 8; ++u) {
+                    const int e = base + u * kSgdThreads;
+                    if (e < GC) {
+                        while ((uint32_t)(v[u] >> 32) != tag) {
+                            if (globaltimer_ns() - t0 > 5000000000ull) {  // 5 s: a bug, not a wait
+                                s_abort = 1;
+                                break;
+                            }
+                            v[u] = ld_relaxed_u64(slot + e);
+                        }
+                        gat[e] = __uint_as_float((uint32_t)v[u]);
+                    }
+                }
+            }
+        }
+        __syncthreads();
+        if (s_abort) break;
+        for (int k = warp; k < C; k += kSgdWarps) {
+            float v = 0.0f;
+            for (int c = lane; c < G; c += 32) v += gat[c * C + k];
+            v = warp_sum(v);
+            if (lane == 0) zl[k] = sadd(v, b1s[k]);
+        }
+        __syncthreads();
+
+        // ---- softmax, output deltas, loss (warp 0; identical in every CTA) ----
+        if (warp == 0) {
+            float e[kSgdMaxC / 32];
+            float m = -INFINITY;
+#pragma unroll
+            for (int q = 0; q < kSgdMaxC / 32; ++q) {
+                const int k = lane + 32 * q;
+                if (k < C) m = fmaxf(m, zl[k]);
+            }
+            m = warp_max(m);
+            float sum = 0.0f;
+#pragma unroll
+            for (int q = 0; q < kSgdMaxC / 32; ++q) {
+                const int k = lane + 32 * q;
+                e[q] = k < C ? lane_libm::expf(ssub(zl[k], m)) : 0.0f;
+                sum += e[q];
+            }
+            sum = warp_sum(sum);
+#pragma unroll
+            for (int q = 0; q < kSgdMaxC / 32; ++q) {
+                const int k = lane + 32 * q;
+                if (k < C) {
+                    const float p = __fdiv_rn(e[q], sum);
+                    pl[k] = p;
+                    dl[k] = ssub(p, tc[k]);
+                }
+            }
+            __syncwarp();
+            if (cta == 0 && lane == 0) {
+                float loss = 0.0f;
+                int bp = 0, bt = 0;
+                for (int o = 0; o < C; ++o) {
+                    if (tc[o] != 0.0f) {
+                        const float q = pl[o] < 1e-12f ? 1e-12f : pl[o];
+                        loss = ssub(loss, smul(tc[o], lane_libm::logf(q)));
+                    }
+                    if (pl[o] > pl[bp]) bp = o;
+                    if (tc[o] > tc[bt]) bt = o;
+                }
+                loss_acc = __dadd_rn(loss_acc, (double)loss);
+                correct_acc += bp == bt;
+            }
+        }
+        __syncthreads();
+
+        // ---- hidden deltas with pre-update W1 (already holds W1(s)) ----
+        for (int j = tid; j < nloc; j += kSgdThreads) {
+            const float* wrow = w1s + (size_t)j * C;
+            // sequential k, separately rounded: exactly fc_backward_tuple's sum
+            float acc = 0.0f;
+            for (int k = 0; k < C; ++k) acc = sadd(acc, smul(dl[k], wrow[k]));
+            dp[j] = tanh_grad(a0s[j], acc);
+            ap[j] = a0s[j];
+        }
+        __syncthreads();
+    }
+
+    if (s_abort) {
+        if (tid == 0) atomicExch(A.error, 1);
+        return;
+    }
+    cp_async_wait<0>();
+
+    // ---- apply the last pending update and write everything back ----
+    if (A.n_steps > 0) {
+        const int last = (int)((A.n_steps - 1) % 3);
+        const float* xl = sm + L.xb + (size_t)last * L.Ip;
+        for (int e = tid; e < nloc * I; e += kSgdThreads) {
+            const int j = e / I, i = e - j * I;
+            A.W0[(size_t)i * H + h0 + j] = sgd_apply(w0s[e], neg_eta, dp[j], xl[i]);
+        }
+        for (int e = tid; e < nloc * C; e += kSgdThreads) {
+            const int j = e / C, k = e - j * C;
+            A.W1[(size_t)h0 * C + e] = sgd_apply(w1s[e], neg_eta, dl[k], ap[j]);
+        }
+        for (int j = tid; j < nloc; j += kSgdThreads) {
+            const float db = smul(neg_eta, dp[j]);
+            A.b0[h0 + j] = sadd(b0s[j], db);
+            A.z0[h0 + j] = z0s[j];
+            A.a0[h0 + j] = ap[j];
+            A.d0[h0 + j] = dp[j];
+            A.db0[h0 + j] = db;
+            A.x1[h0 + j] = ap[j];
+        }
+        if (cta == 0) {
+            for (int i = tid; i < I; i += kSgdThreads) A.x0[i] = xl[i];
+            for (int k = tid; k < C; k += kSgdThreads) {
+                const float db = smul(neg_eta, dl[k]);
+                A.b1[k] = sadd(b1s[k], db);
+                A.z1[k] = zl[k];
+                A.a1[k] = pl[k];
+                A.d1[k] = dl[k];
+                A.db1[k] = db;
+            }
+            if (tid == 0) {
+                if (A.loss_sum) *A.loss_sum = loss_acc;
+                if (A.correct) *A.correct += correct_acc;
+            }
+        }
+    }
+}
+
+}  // namespace lane_b200

@@ -1,0 +1,437 @@
+"""GPU parity: the CUDA path (through the C ABI) against the CPU oracle.
+
+The oracle (oracle/lane_oracle.c) is pinned bit-for-bit to the reference by
+tests/test_oracle.py; the golden fixture tests/golden/golden.npz comes from
+the reference itself.
+
+Tolerances:
+  STRICT numerics: bit-identical -- every buffer, every step, every epoch
+    statistic (the device uses the reference's evaluation order, separately
+    rounded mul/add, and bit-exact restatements of glibc tanhf/expf/logf).
+  FAST numerics: per step, every reduced quantity within
+    |gpu - cpu| <= 1e-5 * sum_k |a_k * b_k| (condition-aware), checked here in
+    its normwise form max|gpu - cpu| <= 1e-5 * max|cpu| per buffer;
+    over an epoch, mean loss within 1e-4 relative and identical accuracy
+    counts up to argmax ties.
+"""
+import ctypes as C
+import os
+
+import numpy as np
+import pytest
+
+from oracle import pyoracle as po
+
+pytestmark = pytest.mark.gpu
+
+GOLD = np.load(os.path.join(os.path.dirname(__file__), "golden", "golden.npz"))
+IRIS = os.path.join(os.path.dirname(__file__), "golden", "iris_normalized.txt")
+BUFS = ("weights", "gradients", "delta_weights", "biases", "inputs", "netin", "outputs",
+        "deltas", "delta_biases")
+
+
+@pytest.fixture(scope="module")
+def lane():
+    from paper_2001_04206_b200 import lane as L
+    return L
+
+
+@pytest.fixture(scope="module")
+def dev(lane):
+    d = lane.Device(0)
+    yield d
+    d.close()
+
+
+@pytest.fixture
+def strict(dev, lane):
+    old = dev.numerics
+    dev.numerics = lane.NUMERICS_STRICT
+    yield dev
+    dev.numerics = old
+
+
+@pytest.fixture
+def fast(dev, lane):
+    old = dev.numerics
+    dev.numerics = lane.NUMERICS_FAST
+    yield dev
+    dev.numerics = old
+
+
+def bits(a):
+    return np.ascontiguousarray(a, np.float32).view(np.uint32)
+
+
+def assert_bitwise(a, b, what=""):
+    a, b = np.asarray(a, np.float32).reshape(-1), np.asarray(b, np.float32).reshape(-1)
+    bad = np.nonzero(bits(a) != bits(b))[0]
+    assert bad.size == 0, f"{what}: {bad.size} of {a.size} differ, first {bad[:5]} " \
+                          f"gpu {a[bad[:5]]} cpu {b[bad[:5]]}"
+
+
+def assert_close(gpu, cpu, rtol=1e-5, what=""):
+    gpu, cpu = np.asarray(gpu, np.float64).reshape(-1), np.asarray(cpu, np.float64).reshape(-1)
+    scale = max(np.max(np.abs(cpu)), 1e-30)
+    err = np.max(np.abs(gpu - cpu)) if cpu.size else 0.0
+    assert err <= rtol * scale, f"{what}: normwise err {err / scale:.3e} > {rtol:g}"
+
+
+def layer_arrays(layer):
+    return {b: getattr(layer, b) for b in BUFS}
+
+
+def oracle_arrays(orc, l):
+    return {b: orc.get(l, i) for i, b in enumerate(BUFS)}
+
+
+# ------------------------------------------------------------ init ----------
+
+@pytest.mark.parametrize("F,H,C", [(4, [8], 3), (784, [128], 10), (16, [12, 9], 5), (3, [], 2)])
+def test_build_network_bitwise(lane, dev, F, H, C):
+    net = lane.build_network(F, H, C, seed=42, device=dev)
+    orc = po.OracleNet(F, H, C, seed=42)
+    for l, layer in enumerate(net.layers):
+        assert_bitwise(layer.weights, orc.get(l, po.W), f"W{l}")
+        assert not np.any(layer.biases)
+    assert net.hash() == orc.hash()
+
+
+def test_device_tanhf_bitwise_vs_glibc(lane, strict):
+    # Layer with I=1, W[0][j] = z_j, x = 1: netin_j = (0 + 1*z_j) + 0 = z_j, a = tanhf(z_j)
+    rs = np.random.default_rng(3)
+    z = np.concatenate([rs.standard_normal(40000) * 4, rs.uniform(-30, 30, 20000),
+                        rs.standard_normal(4000) * 1e-3,
+                        np.float32([0.0, 1.0, -1.0, 22.0, 9.01, 0.5493, -0.3466])]).astype(np.float32)
+    net = lane.FeedForwardNetwork(1, [z.size], 2, device=strict)
+    net.hidden[0].weights = z.reshape(1, -1)
+    a = net.hidden[0].forward(np.ones(1, np.float32))
+    libm = C.CDLL("libm.so.6")
+    libm.tanhf.restype, libm.tanhf.argtypes = C.c_float, [C.c_float]
+    want = np.array([libm.tanhf(float(v)) for v in z], np.float32)
+    assert_bitwise(net.hidden[0].netin, z, "netin")
+    assert_bitwise(a, want, "tanhf")
+
+
+# ------------------------------------------------------- layer KATs ---------
+
+def test_softmax_backward_hand_kat(lane, dev):
+    # proj/tests/test_layers.cpp:125-142 (layer 1 -> 2 as the output of a 1-[1]-2 net)
+    net = lane.FeedForwardNetwork(3, [1], 2, device=dev)
+    out = net.output
+    out.outputs = [0.7, 0.3]
+    out.inputs = [2.0]
+    out.backward([1.0, 0.0], lane.LearningRate(0.1))
+    np.testing.assert_allclose(out.deltas, [-0.3, 0.3], rtol=1e-6)
+    np.testing.assert_allclose(out.gradients[0], [-0.6, 0.6], rtol=1e-6)
+    np.testing.assert_allclose(out.delta_weights[0], [0.06, -0.06], rtol=1e-6)
+    np.testing.assert_allclose(out.delta_biases, [0.03, -0.03], rtol=1e-6)
+    with pytest.raises(lane.ShapeError):
+        out.backward([1.0], lane.LearningRate(0.1))
+
+
+def test_fc_backward_hand_kat_and_shape_errors(lane, dev):
+    # proj/tests/test_layers.cpp:209-222
+    net = lane.FeedForwardNetwork(1, [1], 2, device=dev)
+    h = net.hidden[0]
+    h.outputs = [0.5]
+    h.inputs = [1.0]
+    h.backward(np.array([[3.0]]), [0.2], lane.LearningRate(0.1))
+    np.testing.assert_allclose(h.deltas, [0.45], rtol=1e-6)
+    with pytest.raises(lane.ShapeError):
+        h.backward(np.zeros((2, 1)), [0.2], lane.LearningRate(0.1))
+    with pytest.raises(lane.ShapeError):
+        h.backward(np.zeros((1, 1)), [0.2, 0.3], lane.LearningRate(0.1))
+
+
+def test_zero_signal_cases(lane, dev):
+    # proj/tests/test_layers.cpp:144-161, :224-238
+    net = lane.FeedForwardNetwork(2, [3], 3, device=dev)
+    net.output.outputs = [0, 1, 0]
+    net.output.inputs = [0.4, -0.2, 0.1]
+    net.output.backward([0, 1, 0], 0.5)
+    for b in ("deltas", "gradients", "delta_weights", "delta_biases"):
+        assert not np.any(getattr(net.output, b))
+    net.hidden[0].forward([0.5, -0.5])
+    net.hidden[0].backward(np.ones((3, 2)), [0.0, 0.0], 0.1)
+    assert not np.any(net.hidden[0].deltas) and not np.any(net.hidden[0].gradients)
+
+
+def test_apply_updates_kat(lane, dev):
+    # proj/tests/test_layers.cpp:240-258
+    net = lane.FeedForwardNetwork(1, [1], 2, device=dev)
+    h = net.hidden[0]
+    h.weights = [[1.0]]
+    h.delta_weights = [[-0.06]]
+    h.delta_biases = [0.5]
+    h.apply_updates()
+    assert h.weights[0, 0] == np.float32(0.94) and h.biases[0] == np.float32(0.5)
+    h.apply_updates()
+    np.testing.assert_allclose(h.weights[0, 0], 0.88, rtol=1e-6)
+
+
+def test_learning_rate_must_be_positive(lane, dev):
+    with pytest.raises(lane.ConfigError):
+        lane.LearningRate(0.0)
+    net = lane.FeedForwardNetwork(2, [2], 2, device=dev)
+    with pytest.raises(lane.ConfigError):
+        net.output.backward([1, 0], -0.1)
+    with pytest.raises(lane.ConfigError):
+        lane.FeedForwardNetwork(2, [0], 2, device=dev)
+    with pytest.raises(lane.ConfigError):
+        lane.FeedForwardNetwork(2, [3], 1, device=dev)
+
+
+# --------------------------------------- layer backward / forward vs golden -
+
+@pytest.mark.parametrize("mode", ["strict", "fast"])
+def test_layer_backward_matches_reference_golden(lane, dev, mode):
+    dev.numerics = lane.NUMERICS_STRICT if mode == "strict" else lane.NUMERICS_FAST
+    try:
+        for c in range(24):
+            I, O = GOLD[f"smb{c}_shape"]
+            v = GOLD[f"smb{c}_in"]
+            net = lane.FeedForwardNetwork(3, [I], O, device=dev)
+            net.output.outputs = v[:O]
+            net.output.inputs = v[O:O + I]
+            net.output.backward(v[O + I:], 0.05)
+            for k in ("deltas", "gradients", "delta_weights", "delta_biases"):
+                assert_bitwise(getattr(net.output, k), GOLD[f"smb{c}_{k}"], f"smb{c} {k}")
+        for c in range(24):
+            I, O, N = GOLD[f"fcb{c}_shape"]
+            v = GOLD[f"fcb{c}_in"]
+            net = lane.FeedForwardNetwork(I, [O], 2, device=dev)
+            h = net.hidden[0]
+            h.outputs = v[:O]
+            h.inputs = v[O:O + I]
+            h.backward(v[O + I:O + I + O * N].reshape(O, N), v[O + I + O * N:], 0.05)
+            for k in ("deltas", "gradients", "delta_weights", "delta_biases"):
+                assert_bitwise(getattr(h, k), GOLD[f"fcb{c}_{k}"], f"fcb{c} {k}")
+    finally:
+        dev.numerics = lane.NUMERICS_FAST
+
+
+def test_layer_forward_matches_reference_golden_strict(lane, strict):
+    for c in range(16):
+        W, b, x = GOLD[f"fwd{c}_W"], GOLD[f"fwd{c}_b"], GOLD[f"fwd{c}_x"]
+        I, O = W.shape
+        if c % 2:  # softmax layer = output of a (I)-[]-(O) net
+            net = lane.FeedForwardNetwork(I, [], O, device=strict)
+            layer = net.output
+        else:
+            net = lane.FeedForwardNetwork(I, [O], 2, device=strict)
+            layer = net.hidden[0]
+        layer.weights = W
+        layer.biases = b
+        layer.forward(x)
+        assert_bitwise(layer.netin, GOLD[f"fwd{c}_z"], f"fwd{c} z")
+        assert_bitwise(layer.outputs, GOLD[f"fwd{c}_a"], f"fwd{c} a")
+
+
+@pytest.mark.parametrize("I,O", [(340, 4096), (4096, 10), (784, 128), (1024, 257)])
+def test_layer_forward_fast_within_tolerance(lane, fast, I, O):
+    rs = np.random.default_rng(I + O)
+    W = (rs.uniform(-1, 1, (I, O)) / np.sqrt(I)).astype(np.float32)
+    b = rs.uniform(-0.1, 0.1, O).astype(np.float32)
+    x = rs.uniform(0, 1, I).astype(np.float32)
+    net = lane.FeedForwardNetwork(I, [O], 2, device=fast)
+    net.hidden[0].weights = W
+    net.hidden[0].biases = b
+    net.hidden[0].forward(x)
+    z_ref, a_ref = po.oracle_layer_forward("fc", W, b, x)
+    cond = np.abs(x)[:, None].T @ np.abs(W)  # sum_i |x_i W_ij|
+    err = np.abs(net.hidden[0].netin.astype(np.float64) - z_ref)
+    assert np.all(err <= 1e-5 * cond.reshape(-1) + 1e-30)
+    assert_close(net.hidden[0].outputs, a_ref, 1e-5, "a")
+
+
+# ---------------------------------------------------- network steps ---------
+
+@pytest.mark.parametrize("name,F,H,C,eta,steps", [
+    ("c1", 4, [8], 3, 0.01, 4), ("c2", 784, [128], 10, 0.01, 3),
+    ("c4", 340, [256], 10, 1e-4, 2), ("deep", 16, [12, 9], 5, 0.05, 4)])
+def test_backward_plan_steps_bitwise_vs_reference_golden(lane, strict, name, F, H, C, eta, steps):
+    X, T = po.synthetic_dataset(F, C, 8, 9)
+    net = lane.build_network(F, H, C, seed=42, device=strict)
+    plan = lane.BackwardPlan(net, lane.LearningRate(eta))
+    assert net.hash() == int(GOLD[f"{name}_hash0"][0])
+    for s in range(steps):
+        assert_bitwise(net.forward(X[s]), GOLD[f"{name}_probs"][s], f"probs step {s}")
+        plan.run(T[s])
+        assert net.hash() == int(GOLD[f"{name}_hashes"][s]), f"weights hash step {s}"
+        d = np.concatenate([layer.deltas for layer in net.layers])
+        assert_bitwise(d, GOLD[f"{name}_deltas"][s], f"deltas step {s}")
+
+
+def test_backward_plan_all_buffers_bitwise_vs_oracle(lane, strict):
+    X, T = po.synthetic_dataset(50, 7, 4, 1)
+    net = lane.build_network(50, [33, 17], 7, seed=5, device=strict)
+    orc = po.OracleNet(50, [33, 17], 7, seed=5)
+    for s in range(4):
+        net.forward(X[s])
+        orc.forward(X[s])
+        lane.BackwardPlan(net, 0.02).run(T[s])
+        orc.backward_plan_run(T[s], 0.02)
+        for l, layer in enumerate(net.layers):
+            got, want = layer_arrays(layer), oracle_arrays(orc, l)
+            for b in BUFS:
+                assert_bitwise(got[b], want[b], f"step {s} layer {l} {b}")
+
+
+# ------------------------------------------ fused persistent online SGD -----
+
+def upload(dev, a, dtype=np.float32):
+    a = np.ascontiguousarray(a, dtype)
+    p = dev.alloc(a.nbytes)
+    dev.h2d(p, a)
+    return p
+
+
+@pytest.mark.parametrize("F,H,C,n,steps,eta,ctas", [
+    (784, [128], 10, 64, 200, 0.01, None),   # C2 shape
+    (340, [1024], 10, 32, 40, 1e-4, None),   # C4 shape
+    (4, [8], 3, 12, 60, 0.1, None),          # C1 shape
+    (13, [37], 41, 9, 30, 0.05, 5),          # ragged: I%4 != 0, C > 32, H % G != 0
+    (6, [3], 2, 5, 17, 0.2, None),           # H < 8 warps, C == 2
+    (784, [128], 10, 64, 1, 0.01, 16),       # a single step
+])
+def test_sgd_stream_fast_vs_oracle(lane, fast, monkeypatch, F, H, C, n, steps, eta, ctas):
+    if ctas:
+        monkeypatch.setenv("LANE_B200_SGD_CTAS", str(ctas))
+    X, T = po.synthetic_dataset(F, C, n, 9)
+    order = np.random.default_rng(1).integers(0, n, steps).astype(np.uint32)
+    net = lane.build_network(F, H, C, seed=42, device=fast)
+    orc = po.OracleNet(F, H, C, seed=42)
+    want_loss = orc.sgd_run(X, T, steps, eta, order=order)
+    Xd, Td, Od = upload(fast, X), upload(fast, T), upload(fast, order, np.uint32)
+    Ld = upload(fast, np.zeros(1, np.float64), np.float64)
+    before = fast.kernel_launches
+    net.sgd_stream(Xd, Td, n, steps, eta, order_dev=Od, loss_dev=Ld)
+    fast.sync()
+    assert fast.kernel_launches - before <= 3  # one persistent kernel (+ G/DW materialisation)
+    loss = np.zeros(1, np.float64)
+    fast.d2h(loss, Ld)
+    assert abs(loss[0] - want_loss) <= 1e-4 * abs(want_loss)
+    for l, layer in enumerate(net.layers):
+        got, want = layer_arrays(layer), oracle_arrays(orc, l)
+        for b in BUFS:
+            rtol = 1e-5 if steps == 1 else 2e-4
+            assert_close(got[b], want[b], rtol, f"layer {l} {b}")
+    for p in (Xd, Td, Od, Ld):
+        fast.free(p)
+
+
+# ----------------------------------------------------- train / evaluate -----
+
+def iris():
+    X, T = po.load_dataset(IRIS, 4, 3)
+    return po.split(X, T, 0.9, 42)
+
+
+def test_train_strict_iris_one_epoch_bitwise_vs_reference_golden(lane, strict):
+    Xtr, Ttr, _, _ = iris()
+    net = lane.build_network(4, [8], 3, seed=42, device=strict)
+    st = lane.train(net, lane.DataSet(Xtr, Ttr),
+                    lane.TrainerConfig(lane.LearningRate(0.1), 0.0, 1, 42))
+    assert_bitwise([st[0].mean_loss, st[0].accuracy], GOLD["iris1_stats"], "epoch stats")
+    assert net.hash() == int(GOLD["iris1_hash"][0])
+
+
+def test_train_strict_xor_77_epochs(lane, strict):
+    # proj/tests/test_training.cpp:204-221 regression oracle, bit-for-bit
+    Xx = np.float32([[0, 0], [0, 1], [1, 0], [1, 1]])
+    Tx = np.float32([[1, 0], [0, 1], [0, 1], [1, 0]])
+    net = lane.build_network(2, [4], 2, seed=111, device=strict)
+    st = lane.train(net, lane.DataSet(Xx, Tx), lane.TrainerConfig(lane.LearningRate(0.5), 0.05, 5000, 111))
+    assert len(st) == 77
+    assert_bitwise([s.mean_loss for s in st], GOLD["xor_curve"], "loss curve")
+    assert lane.evaluate(net, lane.DataSet(Xx, Tx)).accuracy == 1.0
+
+
+@pytest.mark.parametrize("mode", ["strict", "fast"])
+def test_train_iris_acceptance_c5(lane, dev, mode):
+    # proj/tests/acceptance.cpp:443-469: 135/15 split, hidden [8], acc >= 0.9
+    dev.numerics = lane.NUMERICS_STRICT if mode == "strict" else lane.NUMERICS_FAST
+    try:
+        Xtr, Ttr, Xte, Tte = iris()
+        net = lane.build_network(4, [8], 3, seed=42, device=dev)
+        st = lane.train(net, lane.DataSet(Xtr, Ttr),
+                        lane.TrainerConfig(lane.LearningRate(0.1), 0.05, 2000, 42))
+        res = lane.evaluate(net, lane.DataSet(Xte, Tte))
+        assert res.accuracy >= 0.9
+        curve = np.array([s.mean_loss for s in st], np.float32)
+        if mode == "strict":
+            assert len(st) == int(GOLD["irisC5_epochs"][0])
+            assert_bitwise(curve, GOLD["irisC5_curve"], "loss curve")
+        else:
+            ref = GOLD["irisC5_curve"]
+            k = min(len(curve), len(ref))
+            np.testing.assert_allclose(curve[:k], ref[:k], rtol=1e-4)
+            assert abs(len(st) - len(ref)) <= 1
+    finally:
+        dev.numerics = lane.NUMERICS_FAST
+
+
+def test_train_fast_c2_epoch_loss_curve(lane, fast):
+    X, T = po.synthetic_dataset(784, 10, 2000, 9)
+    net = lane.build_network(784, [128], 10, seed=42, device=fast)
+    orc = po.OracleNet(784, [128], 10, seed=42)
+    st = lane.train(net, lane.DataSet(X, T), lane.TrainerConfig(lane.LearningRate(0.01), 0.0, 2, 42))
+    ref = orc.train(X, T, 0.01, max_epochs=2, seed=42)
+    for g, r in zip(st, ref):
+        assert abs(g.mean_loss - r[1]) <= 1e-4 * abs(r[1])
+        assert abs(g.accuracy - r[2]) <= 2.0 / len(X)
+    assert_close(net.hidden[0].weights, orc.get(0, po.W), 1e-4, "W0")
+
+
+def test_train_rejects_empty_or_mismatched(lane, dev):
+    net = lane.build_network(2, [4], 2, seed=3, device=dev)
+    with pytest.raises(lane.TrainingError):
+        lane.train(net, lane.DataSet(np.zeros((0, 2), np.float32), np.zeros((0, 2), np.float32)),
+                   lane.TrainerConfig())
+    with pytest.raises(lane.ShapeError):
+        lane.train(net, lane.DataSet(np.zeros((4, 3), np.float32), np.eye(2, dtype=np.float32)[[0, 1, 0, 1]]),
+                   lane.TrainerConfig())
+
+
+def test_evaluate_ties_to_lowest_class(lane, dev):
+    # proj/tests/test_training.cpp:282-300
+    net = lane.FeedForwardNetwork(2, [], 3, device=dev)
+    d = lane.DataSet(np.full((3, 2), 0.5, np.float32), np.eye(3, dtype=np.float32))
+    np.testing.assert_allclose(lane.evaluate(net, d).accuracy, 1.0 / 3.0, rtol=1e-6)
+
+
+# ---------------------------------------------------- mini-batch ext -------
+
+def test_minibatch_b1_mu0_reduces_to_backward_plan(lane, fast):
+    X, T = po.synthetic_dataset(24, 5, 3, 2)
+    net = lane.build_network(24, [16, 12], 5, seed=9, device=fast, max_batch=4)
+    orc = po.OracleNet(24, [16, 12], 5, seed=9)
+    Xd, Td = upload(fast, X), upload(fast, T)
+    for s in range(3):
+        net.minibatch_step(Xd + s * 24 * 4, Td + s * 5 * 4, 1, 0.05, 0.0)
+        orc.forward(X[s])
+        orc.backward_plan_run(T[s], 0.05)
+    for l, layer in enumerate(net.layers):
+        assert_close(layer.weights, orc.get(l, po.W), 1e-5, f"W{l}")
+        assert_close(layer.biases, orc.get(l, po.B), 1e-5, f"b{l}")
+    fast.free(Xd)
+    fast.free(Td)
+
+
+@pytest.mark.parametrize("F,H,C,B,mu", [(64, [96, 80], 10, 32, 0.9), (130, [200], 7, 17, 0.0),
+                                        (1024, [512, 512], 10, 64, 0.9)])
+def test_minibatch_momentum_vs_oracle(lane, fast, F, H, C, B, mu):
+    X, T = po.synthetic_dataset(F, C, 3 * B, 4)
+    net = lane.build_network(F, H, C, seed=1, device=fast, max_batch=B)
+    orc = po.OracleNet(F, H, C, seed=1)
+    Xd, Td = upload(fast, X), upload(fast, T)
+    for s in range(3):
+        net.minibatch_step(Xd + s * B * F * 4, Td + s * B * C * 4, B, 0.05, mu)
+        orc.minibatch_step(X[s * B:(s + 1) * B], T[s * B:(s + 1) * B], 0.05, mu)
+    for l, layer in enumerate(net.layers):
+        assert_close(layer.gradients, orc.get(l, po.G), 1e-4, f"G{l}")
+        assert_close(layer.delta_weights, orc.get(l, po.DW), 1e-4, f"DW{l}")
+        assert_close(layer.weights, orc.get(l, po.W), 1e-5, f"W{l}")
+    fast.free(Xd)
+    fast.free(Td)
