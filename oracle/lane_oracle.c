@@ -306,7 +306,7 @@ double lo_sgd_run(lo_net* net, const float* X, const float* T, size_t n, const u
     const size_t I = net->input_width, C = net->layers[net->n_hidden].out;
     double loss = 0.0;
     for (size_t s = 0; s < n_steps; ++s) {
-        const size_t k = order ? order[s % n] : s % n;
+        const size_t k = order ? order[s] : s % n;
         const float* p = lo_net_forward(net, X + k * I);
         loss += (double)lo_cross_entropy(p, T + k * C, C);
         lo_backward_plan_run(net, T + k * C, eta);

@@ -116,9 +116,10 @@ size_t lo_train(lo_net* net, const float* X, const float* T, size_t n, float eta
 /* evaluate, network.cpp:184-204 */
 lo_epoch_stats lo_evaluate(lo_net* net, const float* X, const float* T, size_t n);
 
-/* Per-sample SGD over a fixed sample order (the bench / measure loop,
- * bench.cpp:62-70 with order[k] = k mod n): forward + BackwardPlan::run for
- * n_steps samples.  Returns the summed cross entropy (double). */
+/* Per-sample SGD over a sample stream (the bench measure() loop,
+ * bench.cpp:62-70): sample s uses row order[s] (order has n_steps entries) or
+ * s mod n when order is NULL; forward + BackwardPlan::run per sample.  Returns
+ * the summed cross entropy (double). */
 double lo_sgd_run(lo_net* net, const float* X, const float* T, size_t n, const uint32_t* order,
                   size_t n_steps, float eta);
 

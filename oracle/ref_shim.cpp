@@ -250,8 +250,8 @@ float lr_cross_entropy(const float* p, const float* t, std::size_t n) {
 }
 
 // The reference measure() loop (bench.cpp:55-73): per iteration one sample,
-// net.forward + plan.run on one device.  Sample k = order[it % n] (order may be
-// null => it % n).  Returns the wall seconds of the timed iterations; the
+// net.forward + plan.run on one device.  Sample k = order[it] (order holds
+// warmup + timed entries; null => it % n).  Returns the wall seconds of the timed iterations; the
 // per-phase means (copy_in, kernel, copy_out summed over layers, forward) are
 // written to phase_ms[4] when non-null.
 double lr_sgd_bench(void* netp, const float* X, const float* T, std::size_t n,
@@ -274,7 +274,7 @@ double lr_sgd_bench(void* netp, const float* X, const float* T, std::size_t n,
         clk::time_point t0;
         for (std::size_t it = 0; it < warmup + timed; ++it) {
             if (it == warmup) t0 = clk::now();
-            const std::size_t k = order ? order[it % n] : it % n;
+            const std::size_t k = order ? order[it] : it % n;
             auto f0 = clk::now();
             net.forward(xs[k]);
             auto f1 = clk::now();

@@ -93,6 +93,10 @@ struct lane_b200_ctx {
     int* error_flag = nullptr;  // device: set by kernels that bail out
     std::vector<void*> scratch;
     MinibatchComm comm;  // NCCL communicator (mini-batch DP), see minibatch.cuh
+    // Networks keep their context alive: ctx_destroy with live networks only
+    // marks the context; the last net_destroy releases it (no dangling ctx).
+    int live_nets = 0;
+    bool destroy_requested = false;
 
     void count(int n = 1) { launches += static_cast<uint64_t>(n); }
     void check_launch() {
@@ -275,6 +279,7 @@ void run_forward_chain(lane_b200_net* net) {
 
 struct SgdPlan {
     bool ok = false;
+    bool cluster = false;  // single thread-block cluster, DSMEM exchange
     int G = 0, npc = 0, wpn = 1;
     size_t smem = 0;
 };
@@ -285,6 +290,34 @@ int next_pow2(int v) {
     return p;
 }
 
+bool cluster_fits(int CS, size_t smem) {
+    static int cached_cs = 0;
+    static size_t cached_smem = 0;
+    static bool cached_ok = false;
+    if (CS == cached_cs && smem == cached_smem) return cached_ok;
+    LANE_CUDA(cudaFuncSetAttribute(k_sgd_cluster, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
+    LANE_CUDA(cudaFuncSetAttribute(k_sgd_cluster, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                   static_cast<int>(smem)));
+    cudaLaunchConfig_t cfg{};
+    cfg.gridDim = dim3(CS);
+    cfg.blockDim = dim3(kClThreads);
+    cfg.dynamicSmemBytes = smem;
+    cudaLaunchAttribute at[1];
+    at[0].id = cudaLaunchAttributeClusterDimension;
+    at[0].val.clusterDim.x = CS;
+    at[0].val.clusterDim.y = 1;
+    at[0].val.clusterDim.z = 1;
+    cfg.attrs = at;
+    cfg.numAttrs = 1;
+    int n = 0;
+    const cudaError_t e = cudaOccupancyMaxActiveClusters(&n, k_sgd_cluster, &cfg);
+    cudaGetLastError();
+    cached_cs = CS;
+    cached_smem = smem;
+    cached_ok = e == cudaSuccess && n >= 1;
+    return cached_ok;
+}
+
 SgdPlan plan_persistent(lane_b200_net* net) {
     SgdPlan p;
     lane_b200_ctx* c = net->ctx;
@@ -292,6 +325,25 @@ SgdPlan plan_persistent(lane_b200_net* net) {
     const int I = static_cast<int>(net->input_width), H = static_cast<int>(net->L(0).O),
               C = static_cast<int>(net->classes);
     if (C > kSgdMaxC) return p;
+    const char* mode = std::getenv("LANE_B200_SGD_MODE");
+    if (!mode || std::strcmp(mode, "grid") != 0) {
+        // single-cluster plan: the whole hidden layer on <= 16 SMs
+        int CS = std::min(16, H);
+        if (const char* e = std::getenv("LANE_B200_SGD_CLUSTER")) CS = std::max(1, std::min(std::atoi(e), std::min(16, H)));
+        const int npc = (H + CS - 1) / CS;
+        CS = (H + npc - 1) / npc;
+        const int wpn = npc >= kClWarps ? 1 : kClWarps / next_pow2(npc);
+        const ClSmem L(I, C, npc, wpn, CS);
+        if (L.total <= c->max_smem_optin && cluster_fits(CS, L.total)) {
+            p.ok = p.cluster = true;
+            p.G = CS;
+            p.npc = npc;
+            p.wpn = wpn;
+            p.smem = L.total;
+            return p;
+        }
+        if (mode && std::strcmp(mode, "cluster") == 0) return p;
+    }
     int G = std::min(c->sm_count, H);
     if (const char* e = std::getenv("LANE_B200_SGD_CTAS")) G = std::max(1, std::min(std::atoi(e), std::min(c->sm_count, H)));
     const int npc = (H + G - 1) / G;
@@ -351,15 +403,32 @@ void launch_persistent(lane_b200_net* net, const SgdPlan& P, const float* X, con
     A.loss_sum = loss_sum;
     A.correct = correct;
     A.error = c->error_flag;
-    static size_t configured = 0;
-    if (P.smem > configured) {
-        LANE_CUDA(cudaFuncSetAttribute(k_sgd_persistent, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                       static_cast<int>(P.smem)));
-        configured = P.smem;
+    if (P.cluster) {
+        cluster_fits(P.G, P.smem);  // sets the function attributes
+        cudaLaunchConfig_t cfg{};
+        cfg.gridDim = dim3(P.G);
+        cfg.blockDim = dim3(kClThreads);
+        cfg.dynamicSmemBytes = P.smem;
+        cfg.stream = c->stream;
+        cudaLaunchAttribute at[1];
+        at[0].id = cudaLaunchAttributeClusterDimension;
+        at[0].val.clusterDim.x = P.G;
+        at[0].val.clusterDim.y = 1;
+        at[0].val.clusterDim.z = 1;
+        cfg.attrs = at;
+        cfg.numAttrs = 1;
+        LANE_CUDA(cudaLaunchKernelEx(&cfg, k_sgd_cluster, A));
+    } else {
+        static size_t configured = 0;
+        if (P.smem > configured) {
+            LANE_CUDA(cudaFuncSetAttribute(k_sgd_persistent, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                           static_cast<int>(P.smem)));
+            configured = P.smem;
+        }
+        void* args[] = {&A};
+        LANE_CUDA(cudaLaunchCooperativeKernel(reinterpret_cast<void*>(k_sgd_persistent), dim3(P.G),
+                                              dim3(kSgdThreads), args, P.smem, c->stream));
     }
-    void* args[] = {&A};
-    LANE_CUDA(cudaLaunchCooperativeKernel(reinterpret_cast<void*>(k_sgd_persistent), dim3(P.G),
-                                          dim3(kSgdThreads), args, P.smem, c->stream));
     c->count();
     // G and DW of the last sample, as the reference's stream_out leaves them
     for (size_t l = 0; l < 2; ++l) {
@@ -459,16 +528,24 @@ int lane_b200_ctx_create(int device, lane_b200_ctx** out) {
     });
 }
 
+static void release_ctx(lane_b200_ctx* c) {
+    cudaSetDevice(c->device);
+    cudaStreamSynchronize(c->stream);
+    comm_destroy(c->comm);
+    for (void* p : c->scratch) cudaFree(p);
+    cudaFree(c->error_flag);
+    cudaStreamDestroy(c->stream);
+    delete c;
+}
+
 int lane_b200_ctx_destroy(lane_b200_ctx* c) {
     return guard([&] {
         if (!c) return;
-        cudaSetDevice(c->device);
-        cudaStreamSynchronize(c->stream);
-        comm_destroy(c->comm);
-        for (void* p : c->scratch) cudaFree(p);
-        cudaFree(c->error_flag);
-        cudaStreamDestroy(c->stream);
-        delete c;
+        if (c->live_nets > 0) {
+            c->destroy_requested = true;  // released by the last net_destroy
+            return;
+        }
+        release_ctx(c);
     });
 }
 
@@ -557,6 +634,7 @@ int lane_b200_net_create(lane_b200_ctx* c, size_t input_width, const size_t* hid
             if (hidden[l] == 0) throw Error(LANE_ERR_CONFIG, "network: hidden layer size must be >= 1");
         if (max_batch == 0) throw Error(LANE_ERR_CONFIG, "network: max_batch must be >= 1");
         LANE_CUDA(cudaSetDevice(c->device));
+        if (c->destroy_requested) throw Error(LANE_ERR_CONFIG, "context is being destroyed");
         auto* net = new lane_b200_net();
         net->ctx = c;
         net->input_width = input_width;
@@ -630,6 +708,7 @@ int lane_b200_net_create(lane_b200_ctx* c, size_t input_width, const size_t* hid
         size_t part = 0;
         for (auto& Ly : net->layers) part = std::max(part, (2 * (size_t)c->sm_count + (Ly.O + 31) / 32) * 32);
         ensure(net->scratch, net->scratch_count, part);
+        c->live_nets++;
         *out = net;
     });
 }
@@ -666,7 +745,9 @@ int lane_b200_net_destroy(lane_b200_net* net) {
         cudaFree(net->slots);
         cudaFree(net->data);
         cudaFree(net->order);
+        lane_b200_ctx* c = net->ctx;
         delete net;
+        if (--c->live_nets == 0 && c->destroy_requested) release_ctx(c);
     });
 }
 

@@ -400,4 +400,313 @@ __global__ void __launch_bounds__(kSgdThreads, 1) k_sgd_persistent(SgdArgs A) {
     }
 }
 
+
+// ===========================================================================
+// Cluster variant: the whole hidden layer lives in ONE thread-block cluster
+// (<= 16 CTAs on one GPC), and the per-sample exchange of partial logits goes
+// through distributed shared memory instead of L2: every CTA pushes its C
+// partials into every peer's smem slot with st.shared::cluster, then a single
+// hardware cluster barrier (arrive.release / wait.acquire) publishes them.
+// Latency per exchange ~ one cluster barrier, no polling, no L2 traffic.
+// Used when the slices fit on CS <= 16 SMs (e.g. 784-128-10: 8 neurons/CTA).
+// ===========================================================================
+
+constexpr int kClThreads = 512;
+constexpr int kClWarps = kClThreads / 32;
+
+struct ClSmem {
+    int I, C, Ip, Cp, npc, wpn, CS;
+    size_t w0s, w1s, xb, tb, b0s, z0s, a0s, ap, dp, b1s, zl, pl, dl, gat, red, red1, total;
+    __host__ __device__ ClSmem(int I_, int C_, int npc_, int wpn_, int CS_)
+        : I(I_), C(C_), npc(npc_), wpn(wpn_), CS(CS_) {
+        Ip = (I + 3) & ~3;
+        Cp = (C + 3) & ~3;
+        size_t o = 0;
+        auto take = [&](size_t n) {
+            size_t at = o;
+            o += (n + 3) & ~size_t(3);
+            return at;
+        };
+        w0s = take((size_t)npc * I);
+        w1s = take((size_t)npc * C);
+        xb = take(3 * (size_t)Ip);
+        tb = take(3 * (size_t)Cp);
+        b0s = take(npc);
+        z0s = take(npc);
+        a0s = take(npc);
+        ap = take(npc);
+        dp = take(npc);
+        b1s = take(Cp);
+        zl = take(Cp);
+        pl = take(Cp);
+        dl = take(Cp);
+        gat = take(2 * (size_t)CS * Cp);  // [parity][rank][k]
+        red = take((size_t)npc * kClWarps);
+        red1 = take((size_t)kClWarps * Cp);
+        total = o * sizeof(float);
+    }
+};
+
+__device__ __forceinline__ uint32_t cluster_ctarank() {
+    uint32_t r;
+    asm volatile("mov.u32 %0, %%cluster_ctarank;\n" : "=r"(r));
+    return r;
+}
+__device__ __forceinline__ uint32_t mapa_shared(uint32_t addr, uint32_t rank) {
+    uint32_t r;
+    asm volatile("mapa.shared::cluster.u32 %0, %1, %2;\n" : "=r"(r) : "r"(addr), "r"(rank));
+    return r;
+}
+__device__ __forceinline__ void st_cluster_f32(uint32_t addr, float v) {
+    asm volatile("st.shared::cluster.f32 [%0], %1;\n" ::"r"(addr), "f"(v) : "memory");
+}
+__device__ __forceinline__ void cluster_sync_all() {
+    asm volatile("barrier.cluster.arrive.release.aligned;\n"
+                 "barrier.cluster.wait.acquire.aligned;\n" ::: "memory");
+}
+
+// Issue the cp.async copies of sample s into an smem slot (block-strided).
+__device__ __forceinline__ void prefetch_sample_bs(const SgdArgs& A, long long s, float* xdst,
+                                                   float* tdst, int nthreads) {
+    const long long k = A.order ? (long long)A.order[s] : s % A.n;
+    const float* xs = A.X + k * A.I;
+    const float* ts = A.T + k * A.C;
+    const bool vec = ((A.I & 3) == 0) && ((reinterpret_cast<uintptr_t>(xs) & 15) == 0);
+    if (vec) {
+        for (int q = threadIdx.x; q < (A.I >> 2); q += nthreads) cp_async16(xdst + 4 * q, xs + 4 * q);
+    } else {
+        for (int i = threadIdx.x; i < A.I; i += nthreads) cp_async4(xdst + i, xs + i);
+    }
+    for (int c = threadIdx.x; c < A.C; c += nthreads) cp_async4(tdst + c, ts + c);
+}
+
+__global__ void __launch_bounds__(kClThreads, 1) k_sgd_cluster(SgdArgs A) {
+    extern __shared__ __align__(16) float sm[];
+    const ClSmem L(A.I, A.C, A.npc, A.wpn, A.G);
+    float* w0s = sm + L.w0s;
+    float* w1s = sm + L.w1s;
+    float* b0s = sm + L.b0s;
+    float* z0s = sm + L.z0s;
+    float* a0s = sm + L.a0s;
+    float* ap = sm + L.ap;
+    float* dp = sm + L.dp;
+    float* b1s = sm + L.b1s;
+    float* zl = sm + L.zl;
+    float* pl = sm + L.pl;
+    float* dl = sm + L.dl;
+    float* gat = sm + L.gat;
+    float* red = sm + L.red;
+    float* red1 = sm + L.red1;
+
+    const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+    const int I = A.I, H = A.H, C = A.C, CS = A.G;
+    const int rank = (int)cluster_ctarank();
+    const int h0 = min(H, rank * A.npc), h1 = min(H, h0 + A.npc), nloc = h1 - h0;
+    const float neg_eta = A.neg_eta;
+    const int wpn = A.wpn, nper = kClWarps / wpn;
+
+    for (int e = tid; e < nloc * I; e += kClThreads) {
+        const int j = e / I, i = e - j * I;
+        w0s[e] = A.W0[(size_t)i * H + h0 + j];
+    }
+    for (int e = tid; e < nloc * C; e += kClThreads) w1s[e] = A.W1[(size_t)h0 * C + e];
+    for (int j = tid; j < nloc; j += kClThreads) b0s[j] = A.b0[h0 + j];
+    for (int k = tid; k < C; k += kClThreads) b1s[k] = A.b1[k];
+    double loss_acc = 0.0;
+    unsigned long long correct_acc = 0;
+    if (rank == 0 && tid == 0 && A.loss_sum) loss_acc = *A.loss_sum;
+    // peer addresses of my row in everyone's gather buffer
+    const uint32_t gat_base = smem_u32(gat);
+
+    if (A.n_steps > 0) prefetch_sample_bs(A, 0, sm + L.xb, sm + L.tb, kClThreads);
+    cp_async_commit();
+    cluster_sync_all();  // all CTAs resident and initialised before any remote store
+
+    long long s = 0;
+    for (; s < A.n_steps; ++s) {
+        const int cur = (int)(s % 3), prv = (int)((s + 2) % 3), nxt = (int)((s + 1) % 3);
+        const float* xc = sm + L.xb + (size_t)cur * L.Ip;
+        const float* xp = sm + L.xb + (size_t)prv * L.Ip;
+        const float* tc = sm + L.tb + (size_t)cur * L.Cp;
+        const bool lazy = s > 0;
+        if (s + 1 < A.n_steps)
+            prefetch_sample_bs(A, s + 1, sm + L.xb + (size_t)nxt * L.Ip, sm + L.tb + (size_t)nxt * L.Cp,
+                               kClThreads);
+        cp_async_commit();
+        cp_async_wait<1>();
+        __syncthreads();
+
+        // hidden forward + lazy W0 update (all warps)
+        for (int r = 0; r * nper < nloc; ++r) {
+            const int jl = r * nper + warp / wpn, part = warp % wpn;
+            if (jl < nloc) {
+                const int i0 = (int)((long long)part * I / wpn), i1 = (int)((long long)(part + 1) * I / wpn);
+                float* wrow = w0s + (size_t)jl * I;
+                float acc = 0.0f;
+                if (lazy) {
+                    const float dj = dp[jl];
+                    for (int i = i0 + lane; i < i1; i += 32) {
+                        const float w = sgd_apply(wrow[i], neg_eta, dj, xp[i]);
+                        wrow[i] = w;
+                        acc = fmaf(xc[i], w, acc);
+                    }
+                } else {
+                    for (int i = i0 + lane; i < i1; i += 32) acc = fmaf(xc[i], wrow[i], acc);
+                }
+                acc = warp_sum(acc);
+                if (lane == 0) red[jl * wpn + part] = acc;
+            }
+        }
+        __syncthreads();
+        for (int j = tid; j < nloc; j += kClThreads) {
+            if (lazy) b0s[j] = sadd(b0s[j], smul(neg_eta, dp[j]));
+            float z = red[j * wpn];
+            for (int p = 1; p < wpn; ++p) z += red[j * wpn + p];
+            z = sadd(z, b0s[j]);
+            z0s[j] = z;
+            a0s[j] = lane_libm::tanhf(z);
+        }
+        __syncthreads();
+        // partial logits + lazy W1 update (warps over j, lanes over k)
+        {
+            float acc[kSgdMaxC / 32];
+#pragma unroll
+            for (int m = 0; m < kSgdMaxC / 32; ++m) acc[m] = 0.0f;
+            for (int j = warp; j < nloc; j += kClWarps) {
+                const float aj = a0s[j], apj = ap[j];
+                float* wrow = w1s + (size_t)j * C;
+#pragma unroll
+                for (int m = 0; m < kSgdMaxC / 32; ++m) {
+                    const int k = lane + 32 * m;
+                    if (k < C) {
+                        float w = wrow[k];
+                        if (lazy) {
+                            w = sgd_apply(w, neg_eta, dl[k], apj);
+                            wrow[k] = w;
+                        }
+                        acc[m] = fmaf(aj, w, acc[m]);
+                    }
+                }
+            }
+#pragma unroll
+            for (int m = 0; m < kSgdMaxC / 32; ++m) {
+                const int k = lane + 32 * m;
+                if (k < C) red1[warp * L.Cp + k] = acc[m];
+            }
+        }
+        __syncthreads();
+        const int par = (int)(s & 1);
+        // push my partials into every peer's gather row [par][rank][k]
+        for (int e = tid; e < C * CS; e += kClThreads) {
+            const int k = e % C, peer = e / C;
+            float P = red1[k];
+            for (int w = 1; w < kClWarps; ++w) P += red1[w * L.Cp + k];
+            const uint32_t off = (uint32_t)(((size_t)(par * CS + rank) * L.Cp + k) * sizeof(float));
+            st_cluster_f32(mapa_shared(gat_base + off, (uint32_t)peer), P);
+        }
+        if (lazy)
+            for (int k = tid; k < C; k += kClThreads) b1s[k] = sadd(b1s[k], smul(neg_eta, dl[k]));
+        cluster_sync_all();
+
+        // warp 0: logits, softmax, output deltas, loss; then hidden deltas
+        if (warp == 0) {
+            float e[kSgdMaxC / 32];
+            float m = -INFINITY;
+#pragma unroll
+            for (int q = 0; q < kSgdMaxC / 32; ++q) {
+                const int k = lane + 32 * q;
+                e[q] = 0.0f;
+                if (k < C) {
+                    float v = 0.0f;
+                    for (int c = 0; c < CS; ++c) v += gat[(size_t)(par * CS + c) * L.Cp + k];
+                    v = sadd(v, b1s[k]);
+                    zl[k] = v;
+                    e[q] = v;
+                    m = fmaxf(m, v);
+                }
+            }
+            m = warp_max(m);
+            float sum = 0.0f;
+#pragma unroll
+            for (int q = 0; q < kSgdMaxC / 32; ++q) {
+                const int k = lane + 32 * q;
+                e[q] = k < C ? lane_libm::expf(ssub(e[q], m)) : 0.0f;
+                sum += e[q];
+            }
+            sum = warp_sum(sum);
+#pragma unroll
+            for (int q = 0; q < kSgdMaxC / 32; ++q) {
+                const int k = lane + 32 * q;
+                if (k < C) {
+                    const float p = __fdiv_rn(e[q], sum);
+                    pl[k] = p;
+                    dl[k] = ssub(p, tc[k]);
+                }
+            }
+            __syncwarp();
+            for (int j = lane; j < nloc; j += 32) {
+                const float* wrow = w1s + (size_t)j * C;
+                float acc = 0.0f;
+                for (int k = 0; k < C; ++k) acc = sadd(acc, smul(dl[k], wrow[k]));
+                dp[j] = tanh_grad(a0s[j], acc);
+                ap[j] = a0s[j];
+            }
+        }
+        if (rank == 0 && warp == 0 && lane == 0) {
+            float loss = 0.0f;
+            int bp = 0, bt = 0;
+            for (int o = 0; o < C; ++o) {
+                if (tc[o] != 0.0f) {
+                    const float q = pl[o] < 1e-12f ? 1e-12f : pl[o];
+                    loss = ssub(loss, smul(tc[o], lane_libm::logf(q)));
+                }
+                if (pl[o] > pl[bp]) bp = o;
+                if (tc[o] > tc[bt]) bt = o;
+            }
+            loss_acc = __dadd_rn(loss_acc, (double)loss);
+            correct_acc += bp == bt;
+        }
+    }
+    cp_async_wait<0>();
+    __syncthreads();
+
+    if (A.n_steps > 0) {
+        const int last = (int)((A.n_steps - 1) % 3);
+        const float* xl = sm + L.xb + (size_t)last * L.Ip;
+        for (int e = tid; e < nloc * I; e += kClThreads) {
+            const int j = e / I, i = e - j * I;
+            A.W0[(size_t)i * H + h0 + j] = sgd_apply(w0s[e], neg_eta, dp[j], xl[i]);
+        }
+        for (int e = tid; e < nloc * C; e += kClThreads) {
+            const int j = e / C, k = e - j * C;
+            A.W1[(size_t)h0 * C + e] = sgd_apply(w1s[e], neg_eta, dl[k], ap[j]);
+        }
+        for (int j = tid; j < nloc; j += kClThreads) {
+            const float db = smul(neg_eta, dp[j]);
+            A.b0[h0 + j] = sadd(b0s[j], db);
+            A.z0[h0 + j] = z0s[j];
+            A.a0[h0 + j] = ap[j];
+            A.d0[h0 + j] = dp[j];
+            A.db0[h0 + j] = db;
+            A.x1[h0 + j] = ap[j];
+        }
+        if (rank == 0) {
+            for (int i = tid; i < I; i += kClThreads) A.x0[i] = xl[i];
+            for (int k = tid; k < C; k += kClThreads) {
+                const float db = smul(neg_eta, dl[k]);
+                A.b1[k] = sadd(b1s[k], db);
+                A.z1[k] = zl[k];
+                A.a1[k] = pl[k];
+                A.d1[k] = dl[k];
+                A.db1[k] = db;
+            }
+            if (tid == 0) {
+                if (A.loss_sum) *A.loss_sum = loss_acc;
+                if (A.correct) *A.correct += correct_acc;
+            }
+        }
+    }
+    cluster_sync_all();  // no CTA exits while a peer may still store into it
+}
+
 }  // namespace lane_b200

@@ -295,9 +295,13 @@ def upload(dev, a, dtype=np.float32):
     (6, [3], 2, 5, 17, 0.2, None),           # H < 8 warps, C == 2
     (784, [128], 10, 64, 1, 0.01, 16),       # a single step
 ])
-def test_sgd_stream_fast_vs_oracle(lane, fast, monkeypatch, F, H, C, n, steps, eta, ctas):
+@pytest.mark.parametrize("mode", ["cluster", "grid"])
+def test_sgd_stream_fast_vs_oracle(lane, fast, monkeypatch, mode, F, H, C, n, steps, eta, ctas):
+    # cluster: one thread-block cluster, DSMEM exchange; grid: all SMs, L2 exchange
+    monkeypatch.setenv("LANE_B200_SGD_MODE", mode)
     if ctas:
-        monkeypatch.setenv("LANE_B200_SGD_CTAS", str(ctas))
+        monkeypatch.setenv("LANE_B200_SGD_CTAS" if mode == "grid" else "LANE_B200_SGD_CLUSTER",
+                           str(min(ctas, 16)))
     X, T = po.synthetic_dataset(F, C, n, 9)
     order = np.random.default_rng(1).integers(0, n, steps).astype(np.uint32)
     net = lane.build_network(F, H, C, seed=42, device=fast)
