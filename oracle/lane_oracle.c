@@ -319,12 +319,21 @@ double lo_sgd_run(lo_net* net, const float* X, const float* T, size_t n, const u
 double lo_minibatch_step(lo_net* net, const float* X, const float* T, size_t B, float eta,
                          float mu) {
     const size_t nh = net->n_hidden, I = net->input_width, C = net->layers[nh].out;
-    /* accumulators: gradient sums per layer, bias sums per layer */
+    /* accumulators: gradient sums per layer, bias sums per layer; the
+     * velocities (DW, db) are saved first because the per-sample reference
+     * backward overwrites delta_weights/delta_biases (layers.hpp:35, :39). */
     float** gsum = calloc(nh + 1, sizeof(float*));
     float** bsum = calloc(nh + 1, sizeof(float*));
+    float** vW = calloc(nh + 1, sizeof(float*));
+    float** vb = calloc(nh + 1, sizeof(float*));
     for (size_t l = 0; l <= nh; ++l) {
-        gsum[l] = calloc(net->layers[l].in * net->layers[l].out, sizeof(float));
-        bsum[l] = calloc(net->layers[l].out, sizeof(float));
+        const size_t m = net->layers[l].in * net->layers[l].out, o = net->layers[l].out;
+        gsum[l] = calloc(m, sizeof(float));
+        bsum[l] = calloc(o, sizeof(float));
+        vW[l] = malloc(m * sizeof(float));
+        vb[l] = malloc(o * sizeof(float));
+        memcpy(vW[l], net->layers[l].DW, m * sizeof(float));
+        memcpy(vb[l], net->layers[l].db, o * sizeof(float));
     }
     double loss = 0.0;
     for (size_t s = 0; s < B; ++s) {
@@ -346,19 +355,23 @@ double lo_minibatch_step(lo_net* net, const float* X, const float* T, size_t B, 
         for (size_t k = 0; k < n; ++k) {
             const float g = gsum[l][k] * invB;
             L->G[k] = g;
-            L->DW[k] = mu == 0.0f ? -eta * g : mu * L->DW[k] + -eta * g;
+            L->DW[k] = mu == 0.0f ? -eta * g : mu * vW[l][k] + -eta * g;
             L->W[k] += L->DW[k];
         }
         for (size_t o = 0; o < L->out; ++o) {
             const float g = bsum[l][o] * invB;
-            L->db[o] = mu == 0.0f ? -eta * g : mu * L->db[o] + -eta * g;
+            L->db[o] = mu == 0.0f ? -eta * g : mu * vb[l][o] + -eta * g;
             L->b[o] += L->db[o];
         }
         free(gsum[l]);
         free(bsum[l]);
+        free(vW[l]);
+        free(vb[l]);
     }
     free(gsum);
     free(bsum);
+    free(vW);
+    free(vb);
     return loss;
 }
 

@@ -9,6 +9,7 @@
 #include <cmath>
 #include <cstdint>
 #include <cstdlib>
+#include <cstdio>
 #include <cstring>
 #include <string>
 #include <vector>
@@ -403,6 +404,14 @@ void launch_persistent(lane_b200_net* net, const SgdPlan& P, const float* X, con
     A.loss_sum = loss_sum;
     A.correct = correct;
     A.error = c->error_flag;
+    const char* trace_path = std::getenv("LANE_B200_SGD_TRACE");
+    unsigned long long* trace = nullptr;
+    const size_t trace_n = static_cast<size_t>(kTraceSamples) * kTracePhases;
+    if (trace_path) {
+        trace = static_cast<unsigned long long*>(dev_alloc(trace_n * 8));
+        LANE_CUDA(cudaMemsetAsync(trace, 0, trace_n * 8, c->stream));
+    }
+    A.trace = trace;
     if (P.cluster) {
         cluster_fits(P.G, P.smem);  // sets the function attributes
         cudaLaunchConfig_t cfg{};
@@ -430,6 +439,20 @@ void launch_persistent(lane_b200_net* net, const SgdPlan& P, const float* X, con
                                               dim3(kSgdThreads), args, P.smem, c->stream));
     }
     c->count();
+    if (trace) {  // debug: per-phase cycle stamps of CTA 0
+        std::vector<unsigned long long> h(trace_n);
+        LANE_CUDA(cudaMemcpyAsync(h.data(), trace, trace_n * 8, cudaMemcpyDeviceToHost, c->stream));
+        LANE_CUDA(cudaStreamSynchronize(c->stream));
+        LANE_CUDA(cudaFree(trace));
+        if (FILE* f = std::fopen(trace_path, "a")) {
+            std::fprintf(f, "# plan cluster=%d G=%d npc=%d wpn=%d\n", P.cluster ? 1 : 0, P.G, P.npc, P.wpn);
+            for (int s = 0; s < kTraceSamples; ++s) {
+                for (int ph = 0; ph < kTracePhases; ++ph) std::fprintf(f, "%llu ", h[s * kTracePhases + ph]);
+                std::fprintf(f, "\n");
+            }
+            std::fclose(f);
+        }
+    }
     // G and DW of the last sample, as the reference's stream_out leaves them
     for (size_t l = 0; l < 2; ++l) {
         LayerBufs& Ly = net->L(l);

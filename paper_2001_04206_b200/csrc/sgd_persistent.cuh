@@ -56,7 +56,15 @@ struct SgdArgs {
     double* loss_sum;
     unsigned long long* correct;
     int* error;  // set to 1 when an exchange times out (bug guard, never hangs)
+    unsigned long long* trace;  // debug: per-phase clock64 of CTA 0 for the first kTraceSamples
 };
+
+constexpr int kTraceSamples = 64, kTracePhases = 8;
+#define SGD_TRACE(ph)                                                                     \
+    do {                                                                                  \
+        if (A.trace && tid == 0 && rank == 0 && s < kTraceSamples)                        \
+            A.trace[s * kTracePhases + (ph)] = clock64();                                 \
+    } while (0)
 
 struct SgdSmem {
     int I, C, Ip, Cp, npc, wpn, G;
@@ -529,12 +537,14 @@ __global__ void __launch_bounds__(kClThreads, 1) k_sgd_cluster(SgdArgs A) {
         const float* xp = sm + L.xb + (size_t)prv * L.Ip;
         const float* tc = sm + L.tb + (size_t)cur * L.Cp;
         const bool lazy = s > 0;
+        SGD_TRACE(0);
         if (s + 1 < A.n_steps)
             prefetch_sample_bs(A, s + 1, sm + L.xb + (size_t)nxt * L.Ip, sm + L.tb + (size_t)nxt * L.Cp,
                                kClThreads);
         cp_async_commit();
         cp_async_wait<1>();
         __syncthreads();
+        SGD_TRACE(1);
 
         // hidden forward + lazy W0 update (all warps)
         for (int r = 0; r * nper < nloc; ++r) {
@@ -558,6 +568,7 @@ __global__ void __launch_bounds__(kClThreads, 1) k_sgd_cluster(SgdArgs A) {
             }
         }
         __syncthreads();
+        SGD_TRACE(2);
         for (int j = tid; j < nloc; j += kClThreads) {
             if (lazy) b0s[j] = sadd(b0s[j], smul(neg_eta, dp[j]));
             float z = red[j * wpn];
@@ -567,6 +578,7 @@ __global__ void __launch_bounds__(kClThreads, 1) k_sgd_cluster(SgdArgs A) {
             a0s[j] = lane_libm::tanhf(z);
         }
         __syncthreads();
+        SGD_TRACE(3);
         // partial logits + lazy W1 update (warps over j, lanes over k)
         {
             float acc[kSgdMaxC / 32];
@@ -595,6 +607,7 @@ __global__ void __launch_bounds__(kClThreads, 1) k_sgd_cluster(SgdArgs A) {
             }
         }
         __syncthreads();
+        SGD_TRACE(4);
         const int par = (int)(s & 1);
         // push my partials into every peer's gather row [par][rank][k]
         for (int e = tid; e < C * CS; e += kClThreads) {
@@ -606,7 +619,9 @@ __global__ void __launch_bounds__(kClThreads, 1) k_sgd_cluster(SgdArgs A) {
         }
         if (lazy)
             for (int k = tid; k < C; k += kClThreads) b1s[k] = sadd(b1s[k], smul(neg_eta, dl[k]));
+        SGD_TRACE(5);
         cluster_sync_all();
+        SGD_TRACE(6);
 
         // warp 0: logits, softmax, output deltas, loss; then hidden deltas
         if (warp == 0) {
@@ -666,6 +681,7 @@ __global__ void __launch_bounds__(kClThreads, 1) k_sgd_cluster(SgdArgs A) {
             loss_acc = __dadd_rn(loss_acc, (double)loss);
             correct_acc += bp == bt;
         }
+        SGD_TRACE(7);
     }
     cp_async_wait<0>();
     __syncthreads();
