@@ -333,9 +333,9 @@ SgdPlan plan_persistent(lane_b200_net* net) {
         if (const char* e = std::getenv("LANE_B200_SGD_CLUSTER")) CS = std::max(1, std::min(std::atoi(e), std::min(16, H)));
         const int npc = (H + CS - 1) / CS;
         CS = (H + npc - 1) / npc;
-        const int wpn = npc >= kClWarps ? 1 : kClWarps / next_pow2(npc);
+        const int wpn = npc >= kClBulkWarps ? 1 : kClBulkWarps / next_pow2(npc);
         const ClSmem L(I, C, npc, wpn, CS);
-        if (L.total <= c->max_smem_optin && cluster_fits(CS, L.total)) {
+        if (C <= kClMaxC && L.total <= c->max_smem_optin && cluster_fits(CS, L.total)) {
             p.ok = p.cluster = true;
             p.G = CS;
             p.npc = npc;

@@ -410,21 +410,37 @@ __global__ void __launch_bounds__(kSgdThreads, 1) k_sgd_persistent(SgdArgs A) {
 
 
 // ===========================================================================
-// Cluster variant: the whole hidden layer lives in ONE thread-block cluster
-// (<= 16 CTAs on one GPC), and the per-sample exchange of partial logits goes
-// through distributed shared memory instead of L2: every CTA pushes its C
-// partials into every peer's smem slot with st.shared::cluster, then a single
-// hardware cluster barrier (arrive.release / wait.acquire) publishes them.
-// Latency per exchange ~ one cluster barrier, no polling, no L2 traffic.
-// Used when the slices fit on CS <= 16 SMs (e.g. 784-128-10: 8 neurons/CTA).
+// Cluster variant (the B=1 flagship): the whole hidden layer lives in ONE
+// thread-block cluster (<= 16 CTAs on one GPC); weights stay in shared memory
+// for the whole sample stream; the per-sample exchange of partial logits goes
+// through distributed shared memory with remote mbarrier arrivals.
+//
+// Warp specialisation per CTA:
+//   warp 0 ("critical"): the serial chain of sample s --
+//       wait partials(s) -> logits -> softmax -> d1(s) -> d0(s)
+//       -> z(s+1) = y(s+1) + (-eta d0(s)) q(s+1) + b0(s+1) -> a(s+1) = tanh
+//       -> W1 update(s) fused with partial logits(s+1) -> push to peers.
+//   warps 1..NB ("bulk"): the O(I x npc) weight pass of sample s, which is
+//       OFF the critical path:  W0 <- W0 + (-eta)(d0(s) (x) x(s))   (exact
+//       reference rounding) fused with y(s+2) = x(s+2) . W0(s+1) and
+//       q(s+2) = x(s+2) . x(s+1); plus the cp.async prefetch of x/t.
+// The split uses  x(s+1).W0(s+1) = x(s+1).W0(s) + (-eta d0(s)) (x(s+1).x(s))
+// (exact in real arithmetic; FAST numerics, checked against the oracle within
+// the stated tolerance).  The weights themselves receive exactly the
+// reference's update sequence.
 // ===========================================================================
 
-constexpr int kClThreads = 512;
-constexpr int kClWarps = kClThreads / 32;
+constexpr int kClBulkWarps = 16;
+constexpr int kClWarps = 1 + kClBulkWarps;
+constexpr int kClThreads = 32 * kClWarps;
+constexpr int kClMaxC = 32;     // classes handled by warp 0 lanes
+constexpr int kClMaxNpc = 128;  // neurons per CTA handled by warp 0 (4 per lane)
+constexpr int kBarDelta = 1, kBarPass = 2;  // named barriers (0 is __syncthreads)
 
 struct ClSmem {
     int I, C, Ip, Cp, npc, wpn, CS;
-    size_t w0s, w1s, xb, tb, b0s, z0s, a0s, ap, dp, b1s, zl, pl, dl, gat, red, red1, total;
+    size_t w0s, w1s, xb, tb, b0s, acur, anxt, zcur, d0, b1s, zl, pl, dl, pk, gat, red, qred, mbar,
+        total;
     __host__ __device__ ClSmem(int I_, int C_, int npc_, int wpn_, int CS_)
         : I(I_), C(C_), npc(npc_), wpn(wpn_), CS(CS_) {
         Ip = (I + 3) & ~3;
@@ -437,20 +453,22 @@ struct ClSmem {
         };
         w0s = take((size_t)npc * I);
         w1s = take((size_t)npc * C);
-        xb = take(3 * (size_t)Ip);
-        tb = take(3 * (size_t)Cp);
+        xb = take(4 * (size_t)Ip);
+        tb = take(4 * (size_t)Cp);
         b0s = take(npc);
-        z0s = take(npc);
-        a0s = take(npc);
-        ap = take(npc);
-        dp = take(npc);
+        acur = take(npc);
+        anxt = take(npc);
+        zcur = take(npc);
+        d0 = take(npc);
         b1s = take(Cp);
         zl = take(Cp);
         pl = take(Cp);
         dl = take(Cp);
-        gat = take(2 * (size_t)CS * Cp);  // [parity][rank][k]
-        red = take((size_t)npc * kClWarps);
-        red1 = take((size_t)kClWarps * Cp);
+        pk = take(Cp);
+        gat = take(2 * (size_t)CS * Cp);          // [parity][rank][k]
+        red = take(2 * (size_t)npc * wpn);        // [parity][j][part]
+        qred = take(2 * (size_t)wpn);             // [parity][part]
+        mbar = take(4);                           // 2 x u64 mbarriers
         total = o * sizeof(float);
     }
 };
@@ -472,20 +490,47 @@ __device__ __forceinline__ void cluster_sync_all() {
     asm volatile("barrier.cluster.arrive.release.aligned;\n"
                  "barrier.cluster.wait.acquire.aligned;\n" ::: "memory");
 }
+__device__ __forceinline__ void mbar_init(uint32_t addr, uint32_t count) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;\n" ::"r"(addr), "r"(count) : "memory");
+}
+// remote arrive with release at cluster scope: orders this thread's prior
+// st.shared::cluster stores before the arrival is observed
+__device__ __forceinline__ void mbar_arrive_remote(uint32_t cluster_addr) {
+    asm volatile("mbarrier.arrive.release.cluster.shared::cluster.b64 _, [%0];\n" ::"r"(cluster_addr)
+                 : "memory");
+}
+__device__ __forceinline__ bool mbar_try_wait(uint32_t addr, uint32_t parity) {
+    uint32_t ok;
+    asm volatile(
+        "{\n .reg .pred p;\n"
+        " mbarrier.try_wait.parity.acquire.cluster.shared::cta.b64 p, [%1], %2;\n"
+        " selp.u32 %0, 1, 0, p;\n}\n"
+        : "=r"(ok)
+        : "r"(addr), "r"(parity)
+        : "memory");
+    return ok != 0;
+}
+__device__ __forceinline__ void named_sync(int id, int n) {
+    asm volatile("bar.sync %0, %1;\n" ::"r"(id), "r"(n) : "memory");
+}
+__device__ __forceinline__ void named_arrive(int id, int n) {
+    asm volatile("bar.arrive %0, %1;\n" ::"r"(id), "r"(n) : "memory");
+}
 
-// Issue the cp.async copies of sample s into an smem slot (block-strided).
-__device__ __forceinline__ void prefetch_sample_bs(const SgdArgs& A, long long s, float* xdst,
-                                                   float* tdst, int nthreads) {
+// cp.async of sample row k into an smem slot, issued by `nthreads` threads
+// starting at thread index `t0`.
+__device__ __forceinline__ void prefetch_row(const SgdArgs& A, long long s, float* xdst, float* tdst,
+                                             int t, int nthreads) {
     const long long k = A.order ? (long long)A.order[s] : s % A.n;
     const float* xs = A.X + k * A.I;
     const float* ts = A.T + k * A.C;
     const bool vec = ((A.I & 3) == 0) && ((reinterpret_cast<uintptr_t>(xs) & 15) == 0);
     if (vec) {
-        for (int q = threadIdx.x; q < (A.I >> 2); q += nthreads) cp_async16(xdst + 4 * q, xs + 4 * q);
+        for (int q = t; q < (A.I >> 2); q += nthreads) cp_async16(xdst + 4 * q, xs + 4 * q);
     } else {
-        for (int i = threadIdx.x; i < A.I; i += nthreads) cp_async4(xdst + i, xs + i);
+        for (int i = t; i < A.I; i += nthreads) cp_async4(xdst + i, xs + i);
     }
-    for (int c = threadIdx.x; c < A.C; c += nthreads) cp_async4(tdst + c, ts + c);
+    for (int c = t; c < A.C; c += nthreads) cp_async4(tdst + c, ts + c);
 }
 
 __global__ void __launch_bounds__(kClThreads, 1) k_sgd_cluster(SgdArgs A) {
@@ -494,25 +539,32 @@ __global__ void __launch_bounds__(kClThreads, 1) k_sgd_cluster(SgdArgs A) {
     float* w0s = sm + L.w0s;
     float* w1s = sm + L.w1s;
     float* b0s = sm + L.b0s;
-    float* z0s = sm + L.z0s;
-    float* a0s = sm + L.a0s;
-    float* ap = sm + L.ap;
-    float* dp = sm + L.dp;
+    float* acur = sm + L.acur;
+    float* anxt = sm + L.anxt;
+    float* zcur = sm + L.zcur;
+    float* d0 = sm + L.d0;
     float* b1s = sm + L.b1s;
     float* zl = sm + L.zl;
     float* pl = sm + L.pl;
     float* dl = sm + L.dl;
+    float* pk = sm + L.pk;
     float* gat = sm + L.gat;
     float* red = sm + L.red;
-    float* red1 = sm + L.red1;
+    float* qred = sm + L.qred;
+    const uint32_t mbar0 = smem_u32(sm + L.mbar);  // mbar[b] at mbar0 + 8*b
 
     const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
     const int I = A.I, H = A.H, C = A.C, CS = A.G;
     const int rank = (int)cluster_ctarank();
     const int h0 = min(H, rank * A.npc), h1 = min(H, h0 + A.npc), nloc = h1 - h0;
     const float neg_eta = A.neg_eta;
-    const int wpn = A.wpn, nper = kClWarps / wpn;
+    const int wpn = A.wpn, nper = kClBulkWarps / wpn;
+    const long long n = A.n_steps;
+    auto xrow = [&](long long s) { return sm + L.xb + (size_t)(s & 3) * L.Ip; };
+    auto trow = [&](long long s) { return sm + L.tb + (size_t)(s & 3) * L.Cp; };
+    const int bt = tid - 32, bw = warp - 1;  // bulk thread / warp index
 
+    // ---------------- prologue ----------------
     for (int e = tid; e < nloc * I; e += kClThreads) {
         const int j = e / I, i = e - j * I;
         w0s[e] = A.W0[(size_t)i * H + h0 + j];
@@ -520,191 +572,249 @@ __global__ void __launch_bounds__(kClThreads, 1) k_sgd_cluster(SgdArgs A) {
     for (int e = tid; e < nloc * C; e += kClThreads) w1s[e] = A.W1[(size_t)h0 * C + e];
     for (int j = tid; j < nloc; j += kClThreads) b0s[j] = A.b0[h0 + j];
     for (int k = tid; k < C; k += kClThreads) b1s[k] = A.b1[k];
+    if (tid == 0) {
+        mbar_init(mbar0, CS);
+        mbar_init(mbar0 + 8, CS);
+        asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
+    }
+    for (long long s = 0; s < 3 && s < n; ++s) prefetch_row(A, s, xrow(s), trow(s), tid, kClThreads);
+    cp_async_commit();
+    cp_async_wait<0>();
+    __syncthreads();
+    // z(0) = x0.W0, y(1) = x1.W0 into red[1], q(1) = x1.x0 (bulk warps)
+    if (warp > 0) {
+        const float* x0 = xrow(0);
+        const float* x1 = xrow(1);
+        const bool has1 = n > 1;
+        for (int r = 0; r * nper < nloc; ++r) {
+            const int jl = r * nper + bw / wpn, part = bw % wpn;
+            if (jl >= nloc) continue;
+            const int i0 = part * I / wpn, i1 = (part + 1) * I / wpn;
+            const float* wrow = w0s + (size_t)jl * I;
+            float a0 = 0.0f, a1 = 0.0f, aq = 0.0f;
+            for (int i = i0 + lane; i < i1; i += 32) {
+                const float w = wrow[i];
+                a0 = fmaf(x0[i], w, a0);
+                if (has1) {
+                    a1 = fmaf(x1[i], w, a1);
+                    if (jl == 0) aq = fmaf(x1[i], x0[i], aq);
+                }
+            }
+            a0 = warp_sum(a0);
+            a1 = warp_sum(a1);
+            aq = warp_sum(aq);
+            if (lane == 0) {
+                red[(size_t)jl * wpn + part] = a0;                          // parity 0: z(0)
+                red[(size_t)(L.npc * wpn) + (size_t)jl * wpn + part] = a1;  // parity 1: y(1)
+                if (jl == 0) qred[wpn + part] = aq;
+            }
+        }
+    }
+    __syncthreads();
     double loss_acc = 0.0;
     unsigned long long correct_acc = 0;
-    if (rank == 0 && tid == 0 && A.loss_sum) loss_acc = *A.loss_sum;
-    // peer addresses of my row in everyone's gather buffer
+    if (rank == 0 && tid == 32 && A.loss_sum) loss_acc = *A.loss_sum;
     const uint32_t gat_base = smem_u32(gat);
-
-    if (A.n_steps > 0) prefetch_sample_bs(A, 0, sm + L.xb, sm + L.tb, kClThreads);
-    cp_async_commit();
-    cluster_sync_all();  // all CTAs resident and initialised before any remote store
-
-    long long s = 0;
-    for (; s < A.n_steps; ++s) {
-        const int cur = (int)(s % 3), prv = (int)((s + 2) % 3), nxt = (int)((s + 1) % 3);
-        const float* xc = sm + L.xb + (size_t)cur * L.Ip;
-        const float* xp = sm + L.xb + (size_t)prv * L.Ip;
-        const float* tc = sm + L.tb + (size_t)cur * L.Cp;
-        const bool lazy = s > 0;
-        SGD_TRACE(0);
-        if (s + 1 < A.n_steps)
-            prefetch_sample_bs(A, s + 1, sm + L.xb + (size_t)nxt * L.Ip, sm + L.tb + (size_t)nxt * L.Cp,
-                               kClThreads);
-        cp_async_commit();
-        cp_async_wait<1>();
-        __syncthreads();
-        SGD_TRACE(1);
-
-        // hidden forward + lazy W0 update (all warps)
-        for (int r = 0; r * nper < nloc; ++r) {
-            const int jl = r * nper + warp / wpn, part = warp % wpn;
-            if (jl < nloc) {
-                const int i0 = (int)((long long)part * I / wpn), i1 = (int)((long long)(part + 1) * I / wpn);
-                float* wrow = w0s + (size_t)jl * I;
-                float acc = 0.0f;
-                if (lazy) {
-                    const float dj = dp[jl];
-                    for (int i = i0 + lane; i < i1; i += 32) {
-                        const float w = sgd_apply(wrow[i], neg_eta, dj, xp[i]);
-                        wrow[i] = w;
-                        acc = fmaf(xc[i], w, acc);
-                    }
-                } else {
-                    for (int i = i0 + lane; i < i1; i += 32) acc = fmaf(xc[i], wrow[i], acc);
-                }
-                acc = warp_sum(acc);
-                if (lane == 0) red[jl * wpn + part] = acc;
-            }
-        }
-        __syncthreads();
-        SGD_TRACE(2);
-        for (int j = tid; j < nloc; j += kClThreads) {
-            if (lazy) b0s[j] = sadd(b0s[j], smul(neg_eta, dp[j]));
-            float z = red[j * wpn];
-            for (int p = 1; p < wpn; ++p) z += red[j * wpn + p];
+    // warp 0: a(0), partial logits(0), push
+    if (warp == 0 && n > 0) {
+        for (int j = lane; j < nloc; j += 32) {
+            float z = red[(size_t)j * wpn];
+            for (int p = 1; p < wpn; ++p) z += red[(size_t)j * wpn + p];
             z = sadd(z, b0s[j]);
-            z0s[j] = z;
-            a0s[j] = lane_libm::tanhf(z);
+            zcur[j] = z;
+            acur[j] = tanhf(z);
         }
-        __syncthreads();
-        SGD_TRACE(3);
-        // partial logits + lazy W1 update (warps over j, lanes over k)
-        {
-            float acc[kSgdMaxC / 32];
-#pragma unroll
-            for (int m = 0; m < kSgdMaxC / 32; ++m) acc[m] = 0.0f;
-            for (int j = warp; j < nloc; j += kClWarps) {
-                const float aj = a0s[j], apj = ap[j];
-                float* wrow = w1s + (size_t)j * C;
-#pragma unroll
-                for (int m = 0; m < kSgdMaxC / 32; ++m) {
-                    const int k = lane + 32 * m;
-                    if (k < C) {
-                        float w = wrow[k];
-                        if (lazy) {
-                            w = sgd_apply(w, neg_eta, dl[k], apj);
-                            wrow[k] = w;
-                        }
-                        acc[m] = fmaf(aj, w, acc[m]);
-                    }
-                }
-            }
-#pragma unroll
-            for (int m = 0; m < kSgdMaxC / 32; ++m) {
-                const int k = lane + 32 * m;
-                if (k < C) red1[warp * L.Cp + k] = acc[m];
-            }
+        __syncwarp();
+        if (lane < C) {
+            float P = 0.0f;
+            for (int j = 0; j < nloc; ++j) P = fmaf(acur[j], w1s[(size_t)j * C + lane], P);
+            pk[lane] = P;
         }
-        __syncthreads();
-        SGD_TRACE(4);
-        const int par = (int)(s & 1);
-        // push my partials into every peer's gather row [par][rank][k]
-        for (int e = tid; e < C * CS; e += kClThreads) {
-            const int k = e % C, peer = e / C;
-            float P = red1[k];
-            for (int w = 1; w < kClWarps; ++w) P += red1[w * L.Cp + k];
-            const uint32_t off = (uint32_t)(((size_t)(par * CS + rank) * L.Cp + k) * sizeof(float));
-            st_cluster_f32(mapa_shared(gat_base + off, (uint32_t)peer), P);
-        }
-        if (lazy)
-            for (int k = tid; k < C; k += kClThreads) b1s[k] = sadd(b1s[k], smul(neg_eta, dl[k]));
-        SGD_TRACE(5);
-        cluster_sync_all();
-        SGD_TRACE(6);
+        __syncwarp();
+    }
+    cluster_sync_all();  // every CTA initialised (mbarriers, smem) before remote traffic
+    if (warp == 0 && n > 0 && lane < CS) {
+        const uint32_t off = (uint32_t)(((size_t)(0 * CS + rank) * L.Cp) * sizeof(float));
+        for (int k = 0; k < C; ++k) st_cluster_f32(mapa_shared(gat_base + off + 4 * k, lane), pk[k]);
+        mbar_arrive_remote(mapa_shared(mbar0, lane));
+    }
+    if (warp > 0) {
+        __threadfence_block();
+        named_arrive(kBarPass, kClThreads);  // "pass(-1) done": y(1), q(1) ready
+    }
 
-        // warp 0: logits, softmax, output deltas, loss; then hidden deltas
+    // ---------------- the sample stream ----------------
+    for (long long s = 0; s < n; ++s) {
+        const int par = (int)(s & 1);
         if (warp == 0) {
-            float e[kSgdMaxC / 32];
-            float m = -INFINITY;
-#pragma unroll
-            for (int q = 0; q < kSgdMaxC / 32; ++q) {
-                const int k = lane + 32 * q;
-                e[q] = 0.0f;
-                if (k < C) {
-                    float v = 0.0f;
-                    for (int c = 0; c < CS; ++c) v += gat[(size_t)(par * CS + c) * L.Cp + k];
-                    v = sadd(v, b1s[k]);
-                    zl[k] = v;
-                    e[q] = v;
-                    m = fmaxf(m, v);
-                }
+            // -- wait for every CTA's partial logits of sample s
+            const uint32_t mb = mbar0 + 8 * par;
+            const uint32_t phase = (uint32_t)((s >> 1) & 1);
+            while (!mbar_try_wait(mb, phase)) {
             }
-            m = warp_max(m);
-            float sum = 0.0f;
-#pragma unroll
-            for (int q = 0; q < kSgdMaxC / 32; ++q) {
-                const int k = lane + 32 * q;
-                e[q] = k < C ? lane_libm::expf(ssub(e[q], m)) : 0.0f;
-                sum += e[q];
-            }
-            sum = warp_sum(sum);
-#pragma unroll
-            for (int q = 0; q < kSgdMaxC / 32; ++q) {
-                const int k = lane + 32 * q;
-                if (k < C) {
-                    const float p = __fdiv_rn(e[q], sum);
-                    pl[k] = p;
-                    dl[k] = ssub(p, tc[k]);
+            const float* tc = trow(s);
+            float zk = -INFINITY, e = 0.0f;
+            if (lane < C) {
+                const float* g = gat + (size_t)par * CS * L.Cp + lane;
+                float v0 = 0.0f, v1 = 0.0f, v2 = 0.0f, v3 = 0.0f;
+                int c = 0;
+                for (; c + 4 <= CS; c += 4) {
+                    v0 += g[(size_t)(c + 0) * L.Cp];
+                    v1 += g[(size_t)(c + 1) * L.Cp];
+                    v2 += g[(size_t)(c + 2) * L.Cp];
+                    v3 += g[(size_t)(c + 3) * L.Cp];
                 }
+                for (; c < CS; ++c) v0 += g[(size_t)c * L.Cp];
+                zk = sadd((v0 + v1) + (v2 + v3), b1s[lane]);
+                zl[lane] = zk;
+            }
+            const float m = warp_max(zk);
+            if (lane < C) e = expf(zk - m);
+            const float sum = warp_sum(e);
+            if (lane < C) {
+                const float p = __fdiv_rn(e, sum);
+                pl[lane] = p;
+                dl[lane] = ssub(p, tc[lane]);
             }
             __syncwarp();
+            // -- hidden deltas with W1(s): sequential k, reference rounding
             for (int j = lane; j < nloc; j += 32) {
                 const float* wrow = w1s + (size_t)j * C;
                 float acc = 0.0f;
                 for (int k = 0; k < C; ++k) acc = sadd(acc, smul(dl[k], wrow[k]));
-                dp[j] = tanh_grad(a0s[j], acc);
-                ap[j] = a0s[j];
+                d0[j] = tanh_grad(acur[j], acc);
             }
-        }
-        if (rank == 0 && warp == 0 && lane == 0) {
-            float loss = 0.0f;
-            int bp = 0, bt = 0;
-            for (int o = 0; o < C; ++o) {
-                if (tc[o] != 0.0f) {
-                    const float q = pl[o] < 1e-12f ? 1e-12f : pl[o];
-                    loss = ssub(loss, smul(tc[o], lane_libm::logf(q)));
+            __syncwarp();
+            named_sync(kBarPass, kClThreads);  // pass(s-1) done: y(s+1), q(s+1), t(s+1) visible
+            __threadfence_block();
+            named_arrive(kBarDelta, kClThreads);  // release d0(s), d1(s) to the bulk warps
+            if (s + 1 < n) {
+                // -- z(s+1), a(s+1)
+                const int pn = (int)((s + 1) & 1);
+                float qv = 0.0f;
+                for (int p = 0; p < wpn; ++p) qv += qred[pn * wpn + p];
+                for (int j = lane; j < nloc; j += 32) {
+                    const float dj = d0[j];
+                    b0s[j] = sadd(b0s[j], smul(neg_eta, dj));
+                    float y = red[(size_t)pn * L.npc * wpn + (size_t)j * wpn];
+                    for (int p = 1; p < wpn; ++p) y += red[(size_t)pn * L.npc * wpn + (size_t)j * wpn + p];
+                    const float z = sadd(fmaf(neg_eta * dj, qv, y), b0s[j]);
+                    anxt[j] = tanhf(z);
+                    zcur[j] = z;
                 }
-                if (pl[o] > pl[bp]) bp = o;
-                if (tc[o] > tc[bt]) bt = o;
+                __syncwarp();
+                // -- W1 update of sample s fused with the partial logits of s+1
+                if (lane < C) {
+                    const float dk = dl[lane];
+                    float P = 0.0f;
+                    for (int j = 0; j < nloc; ++j) {
+                        float* w = w1s + (size_t)j * C + lane;
+                        const float wn = sgd_apply(*w, neg_eta, dk, acur[j]);
+                        *w = wn;
+                        P = fmaf(anxt[j], wn, P);
+                    }
+                    pk[lane] = P;
+                    b1s[lane] = sadd(b1s[lane], smul(neg_eta, dk));
+                }
+                __syncwarp();
+                for (int j = lane; j < nloc; j += 32) acur[j] = anxt[j];
+                // -- push partials(s+1) into every peer, then arrive on its mbarrier
+                if (lane < CS) {
+                    const uint32_t off = (uint32_t)(((size_t)(pn * CS + rank) * L.Cp) * sizeof(float));
+                    for (int k = 0; k < C; ++k)
+                        st_cluster_f32(mapa_shared(gat_base + off + 4 * k, lane), pk[k]);
+                    mbar_arrive_remote(mapa_shared(mbar0 + 8 * pn, lane));
+                }
+                __syncwarp();
             }
-            loss_acc = __dadd_rn(loss_acc, (double)loss);
-            correct_acc += bp == bt;
+        } else {
+            named_sync(kBarDelta, kClThreads);  // d0(s), d1(s), p(s) visible
+            if (rank == 0 && bt == 0) {
+                // loss / accuracy of sample s (network.cpp:165-168), off the critical path
+                const float* tc = trow(s);
+                float loss = 0.0f;
+                int bp = 0, btg = 0;
+                for (int o = 0; o < C; ++o) {
+                    if (tc[o] != 0.0f) {
+                        const float q = pl[o] < 1e-12f ? 1e-12f : pl[o];
+                        loss = ssub(loss, smul(tc[o], logf(q)));
+                    }
+                    if (pl[o] > pl[bp]) bp = o;
+                    if (tc[o] > tc[btg]) btg = o;
+                }
+                loss_acc = __dadd_rn(loss_acc, (double)loss);
+                correct_acc += bp == btg;
+            }
+            // prefetch x/t(s+3); make x(s+2) resident
+            if (s + 3 < n) prefetch_row(A, s + 3, xrow(s + 3), trow(s + 3), bt, 32 * kClBulkWarps);
+            cp_async_commit();
+            cp_async_wait<1>();
+            named_sync(3, 32 * kClBulkWarps);  // bulk-only barrier: cp.async data visible
+            // -- pass(s): W0 update of sample s fused with y(s+2), q(s+2)
+            const float* xs = xrow(s);
+            const float* x1 = xrow(s + 1);
+            const float* x2 = xrow(s + 2);
+            const bool do_y = s + 2 < n;
+            const int py = par;  // y(s+2) has the parity of s
+            for (int r = 0; r * nper < nloc; ++r) {
+                const int jl = r * nper + bw / wpn, part = bw % wpn;
+                if (jl >= nloc) continue;
+                const int i0 = part * I / wpn, i1 = (part + 1) * I / wpn;
+                float* wrow = w0s + (size_t)jl * I;
+                const float dj = d0[jl];
+                float acc = 0.0f, aq = 0.0f;
+                if (do_y) {
+                    if (jl == 0) {
+                        for (int i = i0 + lane; i < i1; i += 32) {
+                            const float w = sgd_apply(wrow[i], neg_eta, dj, xs[i]);
+                            wrow[i] = w;
+                            acc = fmaf(x2[i], w, acc);
+                            aq = fmaf(x2[i], x1[i], aq);
+                        }
+                    } else {
+                        for (int i = i0 + lane; i < i1; i += 32) {
+                            const float w = sgd_apply(wrow[i], neg_eta, dj, xs[i]);
+                            wrow[i] = w;
+                            acc = fmaf(x2[i], w, acc);
+                        }
+                    }
+                    acc = warp_sum(acc);
+                    if (jl == 0) aq = warp_sum(aq);
+                    if (lane == 0) {
+                        red[(size_t)py * L.npc * wpn + (size_t)jl * wpn + part] = acc;
+                        if (jl == 0) qred[py * wpn + part] = aq;
+                    }
+                } else {
+                    for (int i = i0 + lane; i < i1; i += 32) wrow[i] = sgd_apply(wrow[i], neg_eta, dj, xs[i]);
+                }
+            }
+            __threadfence_block();
+            named_arrive(kBarPass, kClThreads);
         }
-        SGD_TRACE(7);
     }
+    if (warp == 0 && n > 0) named_sync(kBarPass, kClThreads);  // consume pass(n-1)'s arrival
     cp_async_wait<0>();
     __syncthreads();
 
-    if (A.n_steps > 0) {
-        const int last = (int)((A.n_steps - 1) % 3);
-        const float* xl = sm + L.xb + (size_t)last * L.Ip;
+    // ---------------- write back (W0 already final; W1/biases: last update) ----------------
+    if (n > 0) {
+        const float* xl = xrow(n - 1);
         for (int e = tid; e < nloc * I; e += kClThreads) {
             const int j = e / I, i = e - j * I;
-            A.W0[(size_t)i * H + h0 + j] = sgd_apply(w0s[e], neg_eta, dp[j], xl[i]);
+            A.W0[(size_t)i * H + h0 + j] = w0s[e];
         }
         for (int e = tid; e < nloc * C; e += kClThreads) {
             const int j = e / C, k = e - j * C;
-            A.W1[(size_t)h0 * C + e] = sgd_apply(w1s[e], neg_eta, dl[k], ap[j]);
+            A.W1[(size_t)h0 * C + e] = sgd_apply(w1s[e], neg_eta, dl[k], acur[j]);
         }
         for (int j = tid; j < nloc; j += kClThreads) {
-            const float db = smul(neg_eta, dp[j]);
+            const float db = smul(neg_eta, d0[j]);
             A.b0[h0 + j] = sadd(b0s[j], db);
-            A.z0[h0 + j] = z0s[j];
-            A.a0[h0 + j] = ap[j];
-            A.d0[h0 + j] = dp[j];
+            A.z0[h0 + j] = zcur[j];
+            A.a0[h0 + j] = acur[j];
+            A.d0[h0 + j] = d0[j];
             A.db0[h0 + j] = db;
-            A.x1[h0 + j] = ap[j];
+            A.x1[h0 + j] = acur[j];
         }
         if (rank == 0) {
             for (int i = tid; i < I; i += kClThreads) A.x0[i] = xl[i];
@@ -716,13 +826,13 @@ __global__ void __launch_bounds__(kClThreads, 1) k_sgd_cluster(SgdArgs A) {
                 A.d1[k] = dl[k];
                 A.db1[k] = db;
             }
-            if (tid == 0) {
+            if (tid == 32) {
                 if (A.loss_sum) *A.loss_sum = loss_acc;
                 if (A.correct) *A.correct += correct_acc;
             }
         }
     }
-    cluster_sync_all();  // no CTA exits while a peer may still store into it
+    cluster_sync_all();  // no CTA exits while a peer may still address its shared memory
 }
 
 }  // namespace lane_b200
