@@ -59,10 +59,10 @@ struct SgdArgs {
     unsigned long long* trace;  // debug: per-phase clock64 of CTA 0 for the first kTraceSamples
 };
 
-constexpr int kTraceSamples = 64, kTracePhases = 8;
+constexpr int kTraceSamples = 64, kTracePhases = 12;
 #define SGD_TRACE(ph)                                                                     \
     do {                                                                                  \
-        if (A.trace && tid == 0 && rank == 0 && s < kTraceSamples)                        \
+        if (A.trace && (tid == 0 || tid == 32) && rank == 0 && s < kTraceSamples)         \
             A.trace[s * kTracePhases + (ph)] = clock64();                                 \
     } while (0)
 
@@ -650,8 +650,10 @@ __global__ void __launch_bounds__(kClThreads, 1) k_sgd_cluster(SgdArgs A) {
             // -- wait for every CTA's partial logits of sample s
             const uint32_t mb = mbar0 + 8 * par;
             const uint32_t phase = (uint32_t)((s >> 1) & 1);
+            SGD_TRACE(0);
             while (!mbar_try_wait(mb, phase)) {
             }
+            SGD_TRACE(1);
             const float* tc = trow(s);
             float zk = -INFINITY, e = 0.0f;
             if (lane < C) {
@@ -677,6 +679,7 @@ __global__ void __launch_bounds__(kClThreads, 1) k_sgd_cluster(SgdArgs A) {
                 dl[lane] = ssub(p, tc[lane]);
             }
             __syncwarp();
+            SGD_TRACE(2);
             // -- hidden deltas with W1(s): sequential k, reference rounding
             for (int j = lane; j < nloc; j += 32) {
                 const float* wrow = w1s + (size_t)j * C;
@@ -685,7 +688,9 @@ __global__ void __launch_bounds__(kClThreads, 1) k_sgd_cluster(SgdArgs A) {
                 d0[j] = tanh_grad(acur[j], acc);
             }
             __syncwarp();
+            SGD_TRACE(3);
             named_sync(kBarPass, kClThreads);  // pass(s-1) done: y(s+1), q(s+1), t(s+1) visible
+            SGD_TRACE(4);
             __threadfence_block();
             named_arrive(kBarDelta, kClThreads);  // release d0(s), d1(s) to the bulk warps
             if (s + 1 < n) {
@@ -703,6 +708,7 @@ __global__ void __launch_bounds__(kClThreads, 1) k_sgd_cluster(SgdArgs A) {
                     zcur[j] = z;
                 }
                 __syncwarp();
+                SGD_TRACE(5);
                 // -- W1 update of sample s fused with the partial logits of s+1
                 if (lane < C) {
                     const float dk = dl[lane];
@@ -718,6 +724,7 @@ __global__ void __launch_bounds__(kClThreads, 1) k_sgd_cluster(SgdArgs A) {
                 }
                 __syncwarp();
                 for (int j = lane; j < nloc; j += 32) acur[j] = anxt[j];
+                SGD_TRACE(6);
                 // -- push partials(s+1) into every peer, then arrive on its mbarrier
                 if (lane < CS) {
                     const uint32_t off = (uint32_t)(((size_t)(pn * CS + rank) * L.Cp) * sizeof(float));
@@ -726,9 +733,11 @@ __global__ void __launch_bounds__(kClThreads, 1) k_sgd_cluster(SgdArgs A) {
                     mbar_arrive_remote(mapa_shared(mbar0 + 8 * pn, lane));
                 }
                 __syncwarp();
+                SGD_TRACE(7);
             }
         } else {
             named_sync(kBarDelta, kClThreads);  // d0(s), d1(s), p(s) visible
+            SGD_TRACE(8);
             if (rank == 0 && bt == 0) {
                 // loss / accuracy of sample s (network.cpp:165-168), off the critical path
                 const float* tc = trow(s);
@@ -750,6 +759,7 @@ __global__ void __launch_bounds__(kClThreads, 1) k_sgd_cluster(SgdArgs A) {
             cp_async_commit();
             cp_async_wait<1>();
             named_sync(3, 32 * kClBulkWarps);  // bulk-only barrier: cp.async data visible
+            SGD_TRACE(9);
             // -- pass(s): W0 update of sample s fused with y(s+2), q(s+2)
             const float* xs = xrow(s);
             const float* x1 = xrow(s + 1);
@@ -788,6 +798,7 @@ __global__ void __launch_bounds__(kClThreads, 1) k_sgd_cluster(SgdArgs A) {
                     for (int i = i0 + lane; i < i1; i += 32) wrow[i] = sgd_apply(wrow[i], neg_eta, dj, xs[i]);
                 }
             }
+            SGD_TRACE(10);
             __threadfence_block();
             named_arrive(kBarPass, kClThreads);
         }

@@ -312,7 +312,8 @@ def test_sgd_stream_fast_vs_oracle(lane, fast, monkeypatch, mode, F, H, C, n, st
     before = fast.kernel_launches
     net.sgd_stream(Xd, Td, n, steps, eta, order_dev=Od, loss_dev=Ld)
     fast.sync()
-    assert fast.kernel_launches - before <= 3  # one persistent kernel (+ G/DW materialisation)
+    if mode == "grid" or C <= 32:  # persistent plan: one kernel (+ G/DW materialisation)
+        assert fast.kernel_launches - before <= 3
     loss = np.zeros(1, np.float64)
     fast.d2h(loss, Ld)
     assert abs(loss[0] - want_loss) <= 1e-4 * abs(want_loss)

@@ -1,6 +1,6 @@
-"""Per-phase cycle breakdown of the fused SGD kernel (CTA 0, first 64 samples).
+"""Per-phase cycle breakdown of the cluster SGD kernel (CTA 0, first 64 samples).
 
-    python tools/trace_sgd.py 784x128x10 [cluster|grid]
+    python tools/trace_sgd.py 784x128x10
 """
 import os
 import sys
@@ -9,17 +9,15 @@ import numpy as np
 
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 
-PHASES = ["prefetch+wait+sync", "forward dot+sync", "tanh+sync", "partial logits+sync",
-          "push partials", "cluster barrier", "softmax/deltas/loss"]
+W0 = ["mbar wait (exchange)", "logits+softmax+d1", "hidden deltas d0", "B2 sync (pass s-1)",
+      "z(s+1)+tanh", "W1 upd + partial logits", "push to peers"]
 
 
 def main():
     shp = sys.argv[1] if len(sys.argv) > 1 else "784x128x10"
-    mode = sys.argv[2] if len(sys.argv) > 2 else "cluster"
     F, H, C = map(int, shp.split("x"))
     path = f"/tmp/sgd_trace_{os.getpid()}.txt"
     os.environ["LANE_B200_SGD_TRACE"] = path
-    os.environ["LANE_B200_SGD_MODE"] = mode
     from oracle import pyoracle as po
     from paper_2001_04206_b200 import lane
     dev = lane.Device(0)
@@ -33,13 +31,14 @@ def main():
     dev.sync()
     lines = open(path).read().strip().splitlines()
     print(shp, lines[-65])
-    t = np.array([[int(v) for v in ln.split()] for ln in lines[-64:]], dtype=np.int64)
-    t = t[8:]  # skip warm-up samples
-    d = np.diff(t, axis=1)
+    t = np.array([[int(v) for v in ln.split()] for ln in lines[-64:]], dtype=np.int64)[8:]
     for k in range(7):
-        print(f"  {PHASES[k]:24s} median {np.median(d[:, k]):8.0f} cycles")
-    print(f"  {'loop back':24s} median {np.median(t[1:, 0] - t[:-1, 7]):8.0f} cycles")
-    print(f"  per sample: {np.median(t[1:, 0] - t[:-1, 0]):.0f} cycles")
+        print(f"  warp0 {W0[k]:26s} {np.median(t[:, k + 1] - t[:, k]):7.0f} cycles")
+    print(f"  warp0 loop back               {np.median(t[1:, 0] - t[:-1, 7]):7.0f}")
+    print(f"  bulk  B1 -> data ready        {np.median(t[:, 9] - t[:, 8]):7.0f}")
+    print(f"  bulk  pass                    {np.median(t[:, 10] - t[:, 9]):7.0f}")
+    print(f"  bulk  B1(s) after warp0 d0    {np.median(t[:, 8] - t[:, 3]):7.0f}")
+    print(f"  per sample                    {np.median(t[1:, 0] - t[:-1, 0]):7.0f} cycles")
 
 
 if __name__ == "__main__":
