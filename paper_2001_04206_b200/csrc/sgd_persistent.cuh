@@ -62,7 +62,8 @@ struct SgdArgs {
 constexpr int kTraceSamples = 64, kTracePhases = 12;
 #define SGD_TRACE(ph)                                                                     \
     do {                                                                                  \
-        if (A.trace && (tid == 0 || tid == 32) && rank == 0 && s < kTraceSamples)         \
+        if (A.trace && (tid == 0 || tid == 32 * (kClWarps - 1)) && rank == 0 &&          \
+            s < kTraceSamples)                                                            \
             A.trace[s * kTracePhases + (ph)] = clock64();                                 \
     } while (0)
 
@@ -562,7 +563,11 @@ __global__ void __launch_bounds__(kClThreads, 1) k_sgd_cluster(SgdArgs A) {
     const long long n = A.n_steps;
     auto xrow = [&](long long s) { return sm + L.xb + (size_t)(s & 3) * L.Ip; };
     auto trow = [&](long long s) { return sm + L.tb + (size_t)(s & 3) * L.Cp; };
-    const int bt = tid - 32, bw = warp - 1;  // bulk thread / warp index
+    // The critical warp is the LAST warp: the SM's warp arbiter favours the
+    // highest warp id, so the serial chain wins issue slots over the bulk pass.
+    const bool critical = warp == kClWarps - 1;
+    const int bw = warp;  // bulk warp index (warps 0..kClBulkWarps-1)
+    const int bt = tid;   // bulk thread index
 
     // ---------------- prologue ----------------
     for (int e = tid; e < nloc * I; e += kClThreads) {
@@ -581,8 +586,8 @@ __global__ void __launch_bounds__(kClThreads, 1) k_sgd_cluster(SgdArgs A) {
     cp_async_commit();
     cp_async_wait<0>();
     __syncthreads();
-    // z(0) = x0.W0, y(1) = x1.W0 into red[1], q(1) = x1.x0 (bulk warps)
-    if (warp > 0) {
+    // z(0) = x0.W0 -> red[0], y(1) = x1.W0 -> red[1], q(1) = x1.x0 (bulk warps)
+    if (!critical) {
         const float* x0 = xrow(0);
         const float* x1 = xrow(1);
         const bool has1 = n > 1;
@@ -604,8 +609,8 @@ __global__ void __launch_bounds__(kClThreads, 1) k_sgd_cluster(SgdArgs A) {
             a1 = warp_sum(a1);
             aq = warp_sum(aq);
             if (lane == 0) {
-                red[(size_t)jl * wpn + part] = a0;                          // parity 0: z(0)
-                red[(size_t)(L.npc * wpn) + (size_t)jl * wpn + part] = a1;  // parity 1: y(1)
+                red[(size_t)jl * wpn + part] = a0;
+                red[(size_t)(L.npc * wpn) + (size_t)jl * wpn + part] = a1;
                 if (jl == 0) qred[wpn + part] = aq;
             }
         }
@@ -613,10 +618,10 @@ __global__ void __launch_bounds__(kClThreads, 1) k_sgd_cluster(SgdArgs A) {
     __syncthreads();
     double loss_acc = 0.0;
     unsigned long long correct_acc = 0;
-    if (rank == 0 && tid == 32 && A.loss_sum) loss_acc = *A.loss_sum;
+    const bool stats = critical && rank == 0 && lane == 0;
+    if (stats && A.loss_sum) loss_acc = *A.loss_sum;
     const uint32_t gat_base = smem_u32(gat);
-    // warp 0: a(0), partial logits(0), push
-    if (warp == 0 && n > 0) {
+    if (critical && n > 0) {
         for (int j = lane; j < nloc; j += 32) {
             float z = red[(size_t)j * wpn];
             for (int p = 1; p < wpn; ++p) z += red[(size_t)j * wpn + p];
@@ -633,20 +638,22 @@ __global__ void __launch_bounds__(kClThreads, 1) k_sgd_cluster(SgdArgs A) {
         __syncwarp();
     }
     cluster_sync_all();  // every CTA initialised (mbarriers, smem) before remote traffic
-    if (warp == 0 && n > 0 && lane < CS) {
-        const uint32_t off = (uint32_t)(((size_t)(0 * CS + rank) * L.Cp) * sizeof(float));
+    if (critical && n > 0 && lane < CS) {
+        const uint32_t off = (uint32_t)(((size_t)rank * L.Cp) * sizeof(float));
         for (int k = 0; k < C; ++k) st_cluster_f32(mapa_shared(gat_base + off + 4 * k, lane), pk[k]);
         mbar_arrive_remote(mapa_shared(mbar0, lane));
     }
-    if (warp > 0) {
+    if (!critical) {
         __threadfence_block();
         named_arrive(kBarPass, kClThreads);  // "pass(-1) done": y(1), q(1) ready
     }
+    // bulk: sample index of the next prefetch, tracked without 64-bit division
+    long long kpre = A.n > 0 ? 3 % A.n : 0;
 
     // ---------------- the sample stream ----------------
     for (long long s = 0; s < n; ++s) {
         const int par = (int)(s & 1);
-        if (warp == 0) {
+        if (critical) {
             // -- wait for every CTA's partial logits of sample s
             const uint32_t mb = mbar0 + 8 * par;
             const uint32_t phase = (uint32_t)((s >> 1) & 1);
@@ -655,7 +662,7 @@ __global__ void __launch_bounds__(kClThreads, 1) k_sgd_cluster(SgdArgs A) {
             }
             SGD_TRACE(1);
             const float* tc = trow(s);
-            float zk = -INFINITY, e = 0.0f;
+            float zk = -INFINITY, e = 0.0f, dk = 0.0f;
             if (lane < C) {
                 const float* g = gat + (size_t)par * CS * L.Cp + lane;
                 float v0 = 0.0f, v1 = 0.0f, v2 = 0.0f, v3 = 0.0f;
@@ -668,31 +675,33 @@ __global__ void __launch_bounds__(kClThreads, 1) k_sgd_cluster(SgdArgs A) {
                 }
                 for (; c < CS; ++c) v0 += g[(size_t)c * L.Cp];
                 zk = sadd((v0 + v1) + (v2 + v3), b1s[lane]);
-                zl[lane] = zk;
             }
             const float m = warp_max(zk);
             if (lane < C) e = expf(zk - m);
             const float sum = warp_sum(e);
             if (lane < C) {
                 const float p = __fdiv_rn(e, sum);
+                dk = ssub(p, tc[lane]);
+                zl[lane] = zk;
                 pl[lane] = p;
-                dl[lane] = ssub(p, tc[lane]);
+                dl[lane] = dk;
             }
-            __syncwarp();
             SGD_TRACE(2);
-            // -- hidden deltas with W1(s): sequential k, reference rounding
-            for (int j = lane; j < nloc; j += 32) {
-                const float* wrow = w1s + (size_t)j * C;
+            // -- hidden deltas with W1(s): d1 broadcast by shuffles, sequential
+            //    k in reference rounding
+            for (int j0 = 0; j0 < nloc; j0 += 32) {
+                const int j = j0 + lane;
+                const float* wrow = w1s + (size_t)min(j, nloc - 1) * C;
                 float acc = 0.0f;
-                for (int k = 0; k < C; ++k) acc = sadd(acc, smul(dl[k], wrow[k]));
-                d0[j] = tanh_grad(acur[j], acc);
+                for (int k = 0; k < C; ++k) acc = sadd(acc, smul(__shfl_sync(0xffffffffu, dk, k), wrow[k]));
+                if (j < nloc) d0[j] = tanh_grad(acur[j], acc);
             }
             __syncwarp();
             SGD_TRACE(3);
             named_sync(kBarPass, kClThreads);  // pass(s-1) done: y(s+1), q(s+1), t(s+1) visible
             SGD_TRACE(4);
             __threadfence_block();
-            named_arrive(kBarDelta, kClThreads);  // release d0(s), d1(s) to the bulk warps
+            named_arrive(kBarDelta, kClThreads);  // release d0(s) to the bulk warps
             if (s + 1 < n) {
                 // -- z(s+1), a(s+1)
                 const int pn = (int)((s + 1) & 1);
@@ -700,10 +709,12 @@ __global__ void __launch_bounds__(kClThreads, 1) k_sgd_cluster(SgdArgs A) {
                 for (int p = 0; p < wpn; ++p) qv += qred[pn * wpn + p];
                 for (int j = lane; j < nloc; j += 32) {
                     const float dj = d0[j];
-                    b0s[j] = sadd(b0s[j], smul(neg_eta, dj));
-                    float y = red[(size_t)pn * L.npc * wpn + (size_t)j * wpn];
-                    for (int p = 1; p < wpn; ++p) y += red[(size_t)pn * L.npc * wpn + (size_t)j * wpn + p];
-                    const float z = sadd(fmaf(neg_eta * dj, qv, y), b0s[j]);
+                    const float b = sadd(b0s[j], smul(neg_eta, dj));
+                    b0s[j] = b;
+                    const float* ry = red + (size_t)pn * L.npc * wpn + (size_t)j * wpn;
+                    float y = ry[0];
+                    for (int p = 1; p < wpn; ++p) y += ry[p];
+                    const float z = sadd(fmaf(neg_eta * dj, qv, y), b);
                     anxt[j] = tanhf(z);
                     zcur[j] = z;
                 }
@@ -711,15 +722,25 @@ __global__ void __launch_bounds__(kClThreads, 1) k_sgd_cluster(SgdArgs A) {
                 SGD_TRACE(5);
                 // -- W1 update of sample s fused with the partial logits of s+1
                 if (lane < C) {
-                    const float dk = dl[lane];
-                    float P = 0.0f;
-                    for (int j = 0; j < nloc; ++j) {
-                        float* w = w1s + (size_t)j * C + lane;
-                        const float wn = sgd_apply(*w, neg_eta, dk, acur[j]);
-                        *w = wn;
-                        P = fmaf(anxt[j], wn, P);
+                    float P0 = 0.0f, P1 = 0.0f;
+                    int j = 0;
+                    for (; j + 2 <= nloc; j += 2) {
+                        float* w0p = w1s + (size_t)j * C + lane;
+                        float* w1p = w0p + C;
+                        const float wa = sgd_apply(*w0p, neg_eta, dk, acur[j]);
+                        const float wb = sgd_apply(*w1p, neg_eta, dk, acur[j + 1]);
+                        *w0p = wa;
+                        *w1p = wb;
+                        P0 = fmaf(anxt[j], wa, P0);
+                        P1 = fmaf(anxt[j + 1], wb, P1);
                     }
-                    pk[lane] = P;
+                    if (j < nloc) {
+                        float* w0p = w1s + (size_t)j * C + lane;
+                        const float wa = sgd_apply(*w0p, neg_eta, dk, acur[j]);
+                        *w0p = wa;
+                        P0 = fmaf(anxt[j], wa, P0);
+                    }
+                    pk[lane] = P0 + P1;
                     b1s[lane] = sadd(b1s[lane], smul(neg_eta, dk));
                 }
                 __syncwarp();
@@ -728,19 +749,16 @@ __global__ void __launch_bounds__(kClThreads, 1) k_sgd_cluster(SgdArgs A) {
                 // -- push partials(s+1) into every peer, then arrive on its mbarrier
                 if (lane < CS) {
                     const uint32_t off = (uint32_t)(((size_t)(pn * CS + rank) * L.Cp) * sizeof(float));
-                    for (int k = 0; k < C; ++k)
-                        st_cluster_f32(mapa_shared(gat_base + off + 4 * k, lane), pk[k]);
+                    const uint32_t dst = mapa_shared(gat_base + off, lane);
+                    for (int k = 0; k < C; ++k) st_cluster_f32(dst + 4 * k, pk[k]);
                     mbar_arrive_remote(mapa_shared(mbar0 + 8 * pn, lane));
                 }
                 __syncwarp();
                 SGD_TRACE(7);
             }
-        } else {
-            named_sync(kBarDelta, kClThreads);  // d0(s), d1(s), p(s) visible
-            SGD_TRACE(8);
-            if (rank == 0 && bt == 0) {
-                // loss / accuracy of sample s (network.cpp:165-168), off the critical path
-                const float* tc = trow(s);
+            if (stats) {
+                // loss / accuracy of sample s (network.cpp:165-168) while the
+                // exchange of s+1 is in flight
                 float loss = 0.0f;
                 int bp = 0, btg = 0;
                 for (int o = 0; o < C; ++o) {
@@ -754,8 +772,25 @@ __global__ void __launch_bounds__(kClThreads, 1) k_sgd_cluster(SgdArgs A) {
                 loss_acc = __dadd_rn(loss_acc, (double)loss);
                 correct_acc += bp == btg;
             }
+            __syncwarp();
+        } else {
+            named_sync(kBarDelta, kClThreads);  // d0(s) visible
+            SGD_TRACE(8);
             // prefetch x/t(s+3); make x(s+2) resident
-            if (s + 3 < n) prefetch_row(A, s + 3, xrow(s + 3), trow(s + 3), bt, 32 * kClBulkWarps);
+            if (s + 3 < n) {
+                const long long kk = A.order ? (long long)A.order[s + 3] : kpre;
+                const float* xs = A.X + kk * A.I;
+                const float* ts = A.T + kk * A.C;
+                float* xd = xrow(s + 3);
+                float* td = trow(s + 3);
+                if (((A.I & 3) == 0) && ((reinterpret_cast<uintptr_t>(xs) & 15) == 0)) {
+                    for (int q = bt; q < (I >> 2); q += 32 * kClBulkWarps) cp_async16(xd + 4 * q, xs + 4 * q);
+                } else {
+                    for (int i = bt; i < I; i += 32 * kClBulkWarps) cp_async4(xd + i, xs + i);
+                }
+                for (int c = bt; c < C; c += 32 * kClBulkWarps) cp_async4(td + c, ts + c);
+                if (++kpre == A.n) kpre = 0;
+            }
             cp_async_commit();
             cp_async_wait<1>();
             named_sync(3, 32 * kClBulkWarps);  // bulk-only barrier: cp.async data visible
@@ -772,30 +807,36 @@ __global__ void __launch_bounds__(kClThreads, 1) k_sgd_cluster(SgdArgs A) {
                 const int i0 = part * I / wpn, i1 = (part + 1) * I / wpn;
                 float* wrow = w0s + (size_t)jl * I;
                 const float dj = d0[jl];
-                float acc = 0.0f, aq = 0.0f;
+                float acc0 = 0.0f, acc1 = 0.0f, aq0 = 0.0f, aq1 = 0.0f;
+                int i = i0 + lane;
                 if (do_y) {
-                    if (jl == 0) {
-                        for (int i = i0 + lane; i < i1; i += 32) {
-                            const float w = sgd_apply(wrow[i], neg_eta, dj, xs[i]);
-                            wrow[i] = w;
-                            acc = fmaf(x2[i], w, acc);
-                            aq = fmaf(x2[i], x1[i], aq);
-                        }
-                    } else {
-                        for (int i = i0 + lane; i < i1; i += 32) {
-                            const float w = sgd_apply(wrow[i], neg_eta, dj, xs[i]);
-                            wrow[i] = w;
-                            acc = fmaf(x2[i], w, acc);
+                    const bool qrow = jl == 0;
+                    for (; i + 32 < i1; i += 64) {
+                        const float wa = sgd_apply(wrow[i], neg_eta, dj, xs[i]);
+                        const float wb = sgd_apply(wrow[i + 32], neg_eta, dj, xs[i + 32]);
+                        wrow[i] = wa;
+                        wrow[i + 32] = wb;
+                        acc0 = fmaf(x2[i], wa, acc0);
+                        acc1 = fmaf(x2[i + 32], wb, acc1);
+                        if (qrow) {
+                            aq0 = fmaf(x2[i], x1[i], aq0);
+                            aq1 = fmaf(x2[i + 32], x1[i + 32], aq1);
                         }
                     }
-                    acc = warp_sum(acc);
-                    if (jl == 0) aq = warp_sum(aq);
+                    if (i < i1) {
+                        const float wa = sgd_apply(wrow[i], neg_eta, dj, xs[i]);
+                        wrow[i] = wa;
+                        acc0 = fmaf(x2[i], wa, acc0);
+                        if (qrow) aq0 = fmaf(x2[i], x1[i], aq0);
+                    }
+                    const float acc = warp_sum(acc0 + acc1);
+                    const float aq = qrow ? warp_sum(aq0 + aq1) : 0.0f;
                     if (lane == 0) {
                         red[(size_t)py * L.npc * wpn + (size_t)jl * wpn + part] = acc;
-                        if (jl == 0) qred[py * wpn + part] = aq;
+                        if (qrow) qred[py * wpn + part] = aq;
                     }
                 } else {
-                    for (int i = i0 + lane; i < i1; i += 32) wrow[i] = sgd_apply(wrow[i], neg_eta, dj, xs[i]);
+                    for (; i < i1; i += 32) wrow[i] = sgd_apply(wrow[i], neg_eta, dj, xs[i]);
                 }
             }
             SGD_TRACE(10);
@@ -803,7 +844,7 @@ __global__ void __launch_bounds__(kClThreads, 1) k_sgd_cluster(SgdArgs A) {
             named_arrive(kBarPass, kClThreads);
         }
     }
-    if (warp == 0 && n > 0) named_sync(kBarPass, kClThreads);  // consume pass(n-1)'s arrival
+    if (critical && n > 0) named_sync(kBarPass, kClThreads);  // consume pass(n-1)'s arrival
     cp_async_wait<0>();
     __syncthreads();
 
@@ -837,10 +878,10 @@ __global__ void __launch_bounds__(kClThreads, 1) k_sgd_cluster(SgdArgs A) {
                 A.d1[k] = dl[k];
                 A.db1[k] = db;
             }
-            if (tid == 32) {
-                if (A.loss_sum) *A.loss_sum = loss_acc;
-                if (A.correct) *A.correct += correct_acc;
-            }
+        }
+        if (stats) {
+            if (A.loss_sum) *A.loss_sum = loss_acc;
+            if (A.correct) *A.correct += correct_acc;
         }
     }
     cluster_sync_all();  // no CTA exits while a peer may still address its shared memory
