@@ -500,6 +500,21 @@ __device__ __forceinline__ void mbar_arrive_remote(uint32_t cluster_addr) {
     asm volatile("mbarrier.arrive.release.cluster.shared::cluster.b64 _, [%0];\n" ::"r"(cluster_addr)
                  : "memory");
 }
+// local arrive that also raises the expected transaction bytes of the phase
+__device__ __forceinline__ void mbar_arrive_expect_tx(uint32_t addr, uint32_t bytes) {
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;\n" ::"r"(addr), "r"(bytes)
+                 : "memory");
+}
+// asynchronous remote store that completes `16 bytes` of the remote mbarrier's
+// transaction count on arrival: no fence, no separate arrive
+__device__ __forceinline__ void st_async_v4(uint32_t remote_addr, float a, float b, float c, float d,
+                                            uint32_t remote_mbar) {
+    asm volatile(
+        "st.async.shared::cluster.mbarrier::complete_tx::bytes.v4.f32 [%0], {%1, %2, %3, %4}, [%5];\n" ::"r"(
+            remote_addr),
+        "f"(a), "f"(b), "f"(c), "f"(d), "r"(remote_mbar)
+        : "memory");
+}
 __device__ __forceinline__ bool mbar_try_wait(uint32_t addr, uint32_t parity) {
     uint32_t ok;
     asm volatile(
@@ -577,10 +592,16 @@ __global__ void __launch_bounds__(kClThreads, 1) k_sgd_cluster(SgdArgs A) {
     for (int e = tid; e < nloc * C; e += kClThreads) w1s[e] = A.W1[(size_t)h0 * C + e];
     for (int j = tid; j < nloc; j += kClThreads) b0s[j] = A.b0[h0 + j];
     for (int k = tid; k < C; k += kClThreads) b1s[k] = A.b1[k];
+    // Exchange protocol: each sample's partial logits arrive as st.async
+    // transactions (CS peers x Cp floats) completing the receiver's mbarrier
+    // (arrival count 1 = the local expect_tx arm).
+    const uint32_t xbytes = (uint32_t)(CS * L.Cp * sizeof(float));
     if (tid == 0) {
-        mbar_init(mbar0, CS);
-        mbar_init(mbar0 + 8, CS);
+        mbar_init(mbar0, 1);
+        mbar_init(mbar0 + 8, 1);
         asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
+        if (n > 0) mbar_arrive_expect_tx(mbar0, xbytes);
+        if (n > 1) mbar_arrive_expect_tx(mbar0 + 8, xbytes);
     }
     for (long long s = 0; s < 3 && s < n; ++s) prefetch_row(A, s, xrow(s), trow(s), tid, kClThreads);
     cp_async_commit();
@@ -630,18 +651,19 @@ __global__ void __launch_bounds__(kClThreads, 1) k_sgd_cluster(SgdArgs A) {
             acur[j] = tanhf(z);
         }
         __syncwarp();
-        if (lane < C) {
+        if (lane < L.Cp) {
             float P = 0.0f;
-            for (int j = 0; j < nloc; ++j) P = fmaf(acur[j], w1s[(size_t)j * C + lane], P);
+            if (lane < C)
+                for (int j = 0; j < nloc; ++j) P = fmaf(acur[j], w1s[(size_t)j * C + lane], P);
             pk[lane] = P;
         }
         __syncwarp();
     }
     cluster_sync_all();  // every CTA initialised (mbarriers, smem) before remote traffic
     if (critical && n > 0 && lane < CS) {
-        const uint32_t off = (uint32_t)(((size_t)rank * L.Cp) * sizeof(float));
-        for (int k = 0; k < C; ++k) st_cluster_f32(mapa_shared(gat_base + off + 4 * k, lane), pk[k]);
-        mbar_arrive_remote(mapa_shared(mbar0, lane));
+        const uint32_t dst = mapa_shared(gat_base + (uint32_t)(rank * L.Cp * sizeof(float)), lane);
+        const uint32_t rb = mapa_shared(mbar0, lane);
+        for (int q = 0; q < L.Cp; q += 4) st_async_v4(dst + 4 * q, pk[q], pk[q + 1], pk[q + 2], pk[q + 3], rb);
     }
     if (!critical) {
         __threadfence_block();
@@ -660,6 +682,9 @@ __global__ void __launch_bounds__(kClThreads, 1) k_sgd_cluster(SgdArgs A) {
             SGD_TRACE(0);
             while (!mbar_try_wait(mb, phase)) {
             }
+            // re-arm this barrier for sample s+2 (peers cannot send s+2 before
+            // they have this CTA's partials of s+1, which are sent below)
+            if (lane == 0 && s + 2 < n) mbar_arrive_expect_tx(mb, xbytes);
             SGD_TRACE(1);
             const float* tc = trow(s);
             float zk = -INFINITY, e = 0.0f, dk = 0.0f;
@@ -742,6 +767,8 @@ __global__ void __launch_bounds__(kClThreads, 1) k_sgd_cluster(SgdArgs A) {
                     }
                     pk[lane] = P0 + P1;
                     b1s[lane] = sadd(b1s[lane], smul(neg_eta, dk));
+                } else if (lane < L.Cp) {
+                    pk[lane] = 0.0f;
                 }
                 __syncwarp();
                 for (int j = lane; j < nloc; j += 32) acur[j] = anxt[j];
@@ -750,8 +777,9 @@ __global__ void __launch_bounds__(kClThreads, 1) k_sgd_cluster(SgdArgs A) {
                 if (lane < CS) {
                     const uint32_t off = (uint32_t)(((size_t)(pn * CS + rank) * L.Cp) * sizeof(float));
                     const uint32_t dst = mapa_shared(gat_base + off, lane);
-                    for (int k = 0; k < C; ++k) st_cluster_f32(dst + 4 * k, pk[k]);
-                    mbar_arrive_remote(mapa_shared(mbar0 + 8 * pn, lane));
+                    const uint32_t rb = mapa_shared(mbar0 + 8 * pn, lane);
+                    for (int q = 0; q < L.Cp; q += 4)
+                        st_async_v4(dst + 4 * q, pk[q], pk[q + 1], pk[q + 2], pk[q + 3], rb);
                 }
                 __syncwarp();
                 SGD_TRACE(7);
