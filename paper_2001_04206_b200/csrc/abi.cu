@@ -291,13 +291,22 @@ int next_pow2(int v) {
     return p;
 }
 
-bool cluster_fits(int CS, size_t smem) {
+using SgdKernel = void (*)(SgdArgs);
+
+SgdKernel cluster_kernel(int C) {
+    // the reference's benchmark topologies are 10-class; other class counts
+    // use the runtime-C instantiation
+    return C == 10 ? k_sgd_cluster<10> : C == 3 ? k_sgd_cluster<3> : k_sgd_cluster<0>;
+}
+
+bool cluster_fits(SgdKernel kern, int CS, size_t smem) {
+    static SgdKernel cached_k = nullptr;
     static int cached_cs = 0;
     static size_t cached_smem = 0;
     static bool cached_ok = false;
-    if (CS == cached_cs && smem == cached_smem) return cached_ok;
-    LANE_CUDA(cudaFuncSetAttribute(k_sgd_cluster, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
-    LANE_CUDA(cudaFuncSetAttribute(k_sgd_cluster, cudaFuncAttributeMaxDynamicSharedMemorySize,
+    if (kern == cached_k && CS == cached_cs && smem == cached_smem) return cached_ok;
+    LANE_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
+    LANE_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                    static_cast<int>(smem)));
     cudaLaunchConfig_t cfg{};
     cfg.gridDim = dim3(CS);
@@ -311,8 +320,9 @@ bool cluster_fits(int CS, size_t smem) {
     cfg.attrs = at;
     cfg.numAttrs = 1;
     int n = 0;
-    const cudaError_t e = cudaOccupancyMaxActiveClusters(&n, k_sgd_cluster, &cfg);
+    const cudaError_t e = cudaOccupancyMaxActiveClusters(&n, kern, &cfg);
     cudaGetLastError();
+    cached_k = kern;
     cached_cs = CS;
     cached_smem = smem;
     cached_ok = e == cudaSuccess && n >= 1;
@@ -335,7 +345,7 @@ SgdPlan plan_persistent(lane_b200_net* net) {
         CS = (H + npc - 1) / npc;
         const int wpn = npc >= kClBulkWarps ? 1 : kClBulkWarps / next_pow2(npc);
         const ClSmem L(I, C, npc, wpn, CS);
-        if (C <= kClMaxC && L.total <= c->max_smem_optin && cluster_fits(CS, L.total)) {
+        if (C <= kClMaxC && L.total <= c->max_smem_optin && cluster_fits(cluster_kernel(C), CS, L.total)) {
             p.ok = p.cluster = true;
             p.G = CS;
             p.npc = npc;
@@ -413,7 +423,8 @@ void launch_persistent(lane_b200_net* net, const SgdPlan& P, const float* X, con
     }
     A.trace = trace;
     if (P.cluster) {
-        cluster_fits(P.G, P.smem);  // sets the function attributes
+        const SgdKernel kern = cluster_kernel(A.C);
+        cluster_fits(kern, P.G, P.smem);  // sets the function attributes
         cudaLaunchConfig_t cfg{};
         cfg.gridDim = dim3(P.G);
         cfg.blockDim = dim3(kClThreads);
@@ -426,7 +437,7 @@ void launch_persistent(lane_b200_net* net, const SgdPlan& P, const float* X, con
         at[0].val.clusterDim.z = 1;
         cfg.attrs = at;
         cfg.numAttrs = 1;
-        LANE_CUDA(cudaLaunchKernelEx(&cfg, k_sgd_cluster, A));
+        LANE_CUDA(cudaLaunchKernelEx(&cfg, kern, A));
     } else {
         static size_t configured = 0;
         if (P.smem > configured) {
@@ -512,8 +523,19 @@ void sgd_stream_impl(lane_b200_net* net, const float* X, const float* T, size_t 
     if (!X || !T) throw Error(LANE_ERR_CONFIG, "sgd_stream: null data");
     if (n_steps == 0) return;
     const SgdPlan P = plan_persistent(net);
-    if (P.ok)
-        launch_persistent(net, P, X, T, n, order, n_steps, eta, loss_sum, correct);
+    if (P.ok) {
+        // the persistent kernels index samples with 32-bit counters
+        const size_t chunk = size_t(1) << 30;
+        for (size_t done = 0; done < n_steps; done += chunk) {
+            const size_t m = std::min(chunk, n_steps - done);
+            if (order) {
+                launch_persistent(net, P, X, T, n, order + done, m, eta, loss_sum, correct);
+            } else {
+                if (done % n != 0) throw Error(LANE_ERR_CONFIG, "sgd_stream: stream too long for one call");
+                launch_persistent(net, P, X, T, n, nullptr, m, eta, loss_sum, correct);
+            }
+        }
+    }
     else
         stream_layer_path(net, X, T, n, order, n_steps, eta, loss_sum, correct, true);
 }

@@ -434,14 +434,12 @@ __global__ void __launch_bounds__(kSgdThreads, 1) k_sgd_persistent(SgdArgs A) {
 constexpr int kClBulkWarps = 16;
 constexpr int kClWarps = 1 + kClBulkWarps;
 constexpr int kClThreads = 32 * kClWarps;
-constexpr int kClMaxC = 32;     // classes handled by warp 0 lanes
-constexpr int kClMaxNpc = 128;  // neurons per CTA handled by warp 0 (4 per lane)
-constexpr int kBarDelta = 1, kBarPass = 2;  // named barriers (0 is __syncthreads)
+constexpr int kClMaxC = 32;  // classes handled by the critical warp's lanes
+constexpr int kBarDelta = 1, kBarPass = 2, kBarBulk = 3;  // named barriers (0 = __syncthreads)
 
 struct ClSmem {
     int I, C, Ip, Cp, npc, wpn, CS;
-    size_t w0s, w1s, xb, tb, b0s, acur, anxt, zcur, d0, b1s, zl, pl, dl, pk, gat, red, qred, mbar,
-        total;
+    size_t w0s, w1s, xb, tb, b0s, abuf, zcur, d0, zl, pl, dl, gat, red, qred, mbar, total;
     __host__ __device__ ClSmem(int I_, int C_, int npc_, int wpn_, int CS_)
         : I(I_), C(C_), npc(npc_), wpn(wpn_), CS(CS_) {
         Ip = (I + 3) & ~3;
@@ -452,24 +450,21 @@ struct ClSmem {
             o += (n + 3) & ~size_t(3);
             return at;
         };
-        w0s = take((size_t)npc * I);
-        w1s = take((size_t)npc * C);
-        xb = take(4 * (size_t)Ip);
-        tb = take(4 * (size_t)Cp);
+        w0s = take((size_t)npc * Ip);          // [j][i], rows zero-padded to Ip
+        w1s = take((size_t)npc * C);           // [j][k]
+        xb = take(4 * (size_t)Ip);             // x(s) ring, zero tails
+        tb = take(4 * (size_t)Cp);             // t(s) ring
         b0s = take(npc);
-        acur = take(npc);
-        anxt = take(npc);
+        abuf = take(2 * (size_t)npc);          // a(s) by parity
         zcur = take(npc);
-        d0 = take(npc);
-        b1s = take(Cp);
+        d0 = take(2 * (size_t)npc);            // d0(s) by parity
         zl = take(Cp);
-        pl = take(Cp);
+        pl = take(2 * (size_t)Cp);             // p(s) by parity
         dl = take(Cp);
-        pk = take(Cp);
-        gat = take(2 * (size_t)CS * Cp);          // [parity][rank][k]
-        red = take(2 * (size_t)npc * wpn);        // [parity][j][part]
-        qred = take(2 * (size_t)wpn);             // [parity][part]
-        mbar = take(4);                           // 2 x u64 mbarriers
+        gat = take(2 * (size_t)CS * Cp);       // [parity][rank][k]
+        red = take(2 * (size_t)npc * wpn);     // [parity][j][part]
+        qred = take(2 * (size_t)wpn);          // [parity][part]
+        mbar = take(4);                        // 2 x u64 mbarriers
         total = o * sizeof(float);
     }
 };
@@ -484,9 +479,6 @@ __device__ __forceinline__ uint32_t mapa_shared(uint32_t addr, uint32_t rank) {
     asm volatile("mapa.shared::cluster.u32 %0, %1, %2;\n" : "=r"(r) : "r"(addr), "r"(rank));
     return r;
 }
-__device__ __forceinline__ void st_cluster_f32(uint32_t addr, float v) {
-    asm volatile("st.shared::cluster.f32 [%0], %1;\n" ::"r"(addr), "f"(v) : "memory");
-}
 __device__ __forceinline__ void cluster_sync_all() {
     asm volatile("barrier.cluster.arrive.release.aligned;\n"
                  "barrier.cluster.wait.acquire.aligned;\n" ::: "memory");
@@ -494,26 +486,18 @@ __device__ __forceinline__ void cluster_sync_all() {
 __device__ __forceinline__ void mbar_init(uint32_t addr, uint32_t count) {
     asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;\n" ::"r"(addr), "r"(count) : "memory");
 }
-// remote arrive with release at cluster scope: orders this thread's prior
-// st.shared::cluster stores before the arrival is observed
-__device__ __forceinline__ void mbar_arrive_remote(uint32_t cluster_addr) {
-    asm volatile("mbarrier.arrive.release.cluster.shared::cluster.b64 _, [%0];\n" ::"r"(cluster_addr)
-                 : "memory");
-}
 // local arrive that also raises the expected transaction bytes of the phase
 __device__ __forceinline__ void mbar_arrive_expect_tx(uint32_t addr, uint32_t bytes) {
     asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;\n" ::"r"(addr), "r"(bytes)
                  : "memory");
 }
-// asynchronous remote store that completes `16 bytes` of the remote mbarrier's
+// asynchronous remote store that completes 4 bytes of the remote mbarrier's
 // transaction count on arrival: no fence, no separate arrive
-__device__ __forceinline__ void st_async_v4(uint32_t remote_addr, float a, float b, float c, float d,
-                                            uint32_t remote_mbar) {
-    asm volatile(
-        "st.async.shared::cluster.mbarrier::complete_tx::bytes.v4.f32 [%0], {%1, %2, %3, %4}, [%5];\n" ::"r"(
-            remote_addr),
-        "f"(a), "f"(b), "f"(c), "f"(d), "r"(remote_mbar)
-        : "memory");
+__device__ __forceinline__ void st_async_f32(uint32_t remote_addr, float v, uint32_t remote_mbar) {
+    asm volatile("st.async.shared::cluster.mbarrier::complete_tx::bytes.b32 [%0], %1, [%2];\n" ::"r"(
+                     remote_addr),
+                 "r"(__float_as_uint(v)), "r"(remote_mbar)
+                 : "memory");
 }
 __device__ __forceinline__ bool mbar_try_wait(uint32_t addr, uint32_t parity) {
     uint32_t ok;
@@ -533,15 +517,12 @@ __device__ __forceinline__ void named_arrive(int id, int n) {
     asm volatile("bar.arrive %0, %1;\n" ::"r"(id), "r"(n) : "memory");
 }
 
-// cp.async of sample row k into an smem slot, issued by `nthreads` threads
-// starting at thread index `t0`.
-__device__ __forceinline__ void prefetch_row(const SgdArgs& A, long long s, float* xdst, float* tdst,
-                                             int t, int nthreads) {
-    const long long k = A.order ? (long long)A.order[s] : s % A.n;
+// cp.async of sample row k into an smem slot, issued by `nthreads` threads.
+__device__ __forceinline__ void prefetch_row_k(const SgdArgs& A, long long k, float* xdst, float* tdst,
+                                               int t, int nthreads) {
     const float* xs = A.X + k * A.I;
     const float* ts = A.T + k * A.C;
-    const bool vec = ((A.I & 3) == 0) && ((reinterpret_cast<uintptr_t>(xs) & 15) == 0);
-    if (vec) {
+    if (((A.I & 3) == 0) && ((reinterpret_cast<uintptr_t>(xs) & 15) == 0)) {
         for (int q = t; q < (A.I >> 2); q += nthreads) cp_async16(xdst + 4 * q, xs + 4 * q);
     } else {
         for (int i = t; i < A.I; i += nthreads) cp_async4(xdst + i, xs + i);
@@ -549,53 +530,63 @@ __device__ __forceinline__ void prefetch_row(const SgdArgs& A, long long s, floa
     for (int c = t; c < A.C; c += nthreads) cp_async4(tdst + c, ts + c);
 }
 
+__device__ __forceinline__ float4 sgd_apply4(float4 w, float neg_eta, float d, float4 x) {
+    w.x = sgd_apply(w.x, neg_eta, d, x.x);
+    w.y = sgd_apply(w.y, neg_eta, d, x.y);
+    w.z = sgd_apply(w.z, neg_eta, d, x.z);
+    w.w = sgd_apply(w.w, neg_eta, d, x.w);
+    return w;
+}
+__device__ __forceinline__ float dot4(float4 a, float4 b, float acc) {
+    acc = fmaf(a.x, b.x, acc);
+    acc = fmaf(a.y, b.y, acc);
+    acc = fmaf(a.z, b.z, acc);
+    return fmaf(a.w, b.w, acc);
+}
+
+// CT: the class count as a compile-time constant (fully unrolled class loops),
+// or 0 for a runtime C <= 32.
+template <int CT>
 __global__ void __launch_bounds__(kClThreads, 1) k_sgd_cluster(SgdArgs A) {
     extern __shared__ __align__(16) float sm[];
     const ClSmem L(A.I, A.C, A.npc, A.wpn, A.G);
     float* w0s = sm + L.w0s;
     float* w1s = sm + L.w1s;
     float* b0s = sm + L.b0s;
-    float* acur = sm + L.acur;
-    float* anxt = sm + L.anxt;
+    float* abuf = sm + L.abuf;
     float* zcur = sm + L.zcur;
-    float* d0 = sm + L.d0;
-    float* b1s = sm + L.b1s;
+    float* d0b = sm + L.d0;
     float* zl = sm + L.zl;
-    float* pl = sm + L.pl;
+    float* plb = sm + L.pl;
     float* dl = sm + L.dl;
-    float* pk = sm + L.pk;
     float* gat = sm + L.gat;
     float* red = sm + L.red;
     float* qred = sm + L.qred;
     const uint32_t mbar0 = smem_u32(sm + L.mbar);  // mbar[b] at mbar0 + 8*b
 
     const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
-    const int I = A.I, H = A.H, C = A.C, CS = A.G;
+    const int I = A.I, H = A.H, CS = A.G, Ip = L.Ip, Cp = L.Cp;
+    const int C = CT > 0 ? CT : A.C;
     const int rank = (int)cluster_ctarank();
     const int h0 = min(H, rank * A.npc), h1 = min(H, h0 + A.npc), nloc = h1 - h0;
     const float neg_eta = A.neg_eta;
     const int wpn = A.wpn, nper = kClBulkWarps / wpn;
-    const long long n = A.n_steps;
-    auto xrow = [&](long long s) { return sm + L.xb + (size_t)(s & 3) * L.Ip; };
-    auto trow = [&](long long s) { return sm + L.tb + (size_t)(s & 3) * L.Cp; };
-    // The critical warp is the LAST warp: the SM's warp arbiter favours the
-    // highest warp id, so the serial chain wins issue slots over the bulk pass.
+    const int n = (int)A.n_steps;
+    auto xrow = [&](int s) { return sm + L.xb + (size_t)(s & 3) * Ip; };
+    auto trow = [&](int s) { return sm + L.tb + (size_t)(s & 3) * Cp; };
+    // The critical warp is the LAST warp: the warp arbiter favours the highest
+    // warp id, so the serial chain wins issue slots over the bulk pass.
     const bool critical = warp == kClWarps - 1;
-    const int bw = warp;  // bulk warp index (warps 0..kClBulkWarps-1)
-    const int bt = tid;   // bulk thread index
 
     // ---------------- prologue ----------------
-    for (int e = tid; e < nloc * I; e += kClThreads) {
-        const int j = e / I, i = e - j * I;
-        w0s[e] = A.W0[(size_t)i * H + h0 + j];
+    for (int e = tid; e < 4 * Ip; e += kClThreads) sm[L.xb + e] = 0.0f;  // zero tails
+    for (int e = tid; e < nloc * Ip; e += kClThreads) {
+        const int j = e / Ip, i = e - j * Ip;
+        w0s[e] = i < I ? A.W0[(size_t)i * H + h0 + j] : 0.0f;
     }
     for (int e = tid; e < nloc * C; e += kClThreads) w1s[e] = A.W1[(size_t)h0 * C + e];
     for (int j = tid; j < nloc; j += kClThreads) b0s[j] = A.b0[h0 + j];
-    for (int k = tid; k < C; k += kClThreads) b1s[k] = A.b1[k];
-    // Exchange protocol: each sample's partial logits arrive as st.async
-    // transactions (CS peers x Cp floats) completing the receiver's mbarrier
-    // (arrival count 1 = the local expect_tx arm).
-    const uint32_t xbytes = (uint32_t)(CS * L.Cp * sizeof(float));
+    const uint32_t xbytes = (uint32_t)(CS * Cp * sizeof(float));
     if (tid == 0) {
         mbar_init(mbar0, 1);
         mbar_init(mbar0 + 8, 1);
@@ -603,28 +594,30 @@ __global__ void __launch_bounds__(kClThreads, 1) k_sgd_cluster(SgdArgs A) {
         if (n > 0) mbar_arrive_expect_tx(mbar0, xbytes);
         if (n > 1) mbar_arrive_expect_tx(mbar0 + 8, xbytes);
     }
-    for (long long s = 0; s < 3 && s < n; ++s) prefetch_row(A, s, xrow(s), trow(s), tid, kClThreads);
+    __syncthreads();
+    for (int s = 0; s < 3 && s < n; ++s) {
+        const long long k = A.order ? (long long)A.order[s] : s % A.n;
+        prefetch_row_k(A, k, xrow(s), trow(s), tid, kClThreads);
+    }
     cp_async_commit();
     cp_async_wait<0>();
     __syncthreads();
     // z(0) = x0.W0 -> red[0], y(1) = x1.W0 -> red[1], q(1) = x1.x0 (bulk warps)
     if (!critical) {
-        const float* x0 = xrow(0);
-        const float* x1 = xrow(1);
-        const bool has1 = n > 1;
+        const float4* x0 = reinterpret_cast<const float4*>(xrow(0));
+        const float4* x1 = reinterpret_cast<const float4*>(xrow(1));
+        const int Ip4 = Ip >> 2;
         for (int r = 0; r * nper < nloc; ++r) {
-            const int jl = r * nper + bw / wpn, part = bw % wpn;
+            const int jl = r * nper + warp / wpn, part = warp % wpn;
             if (jl >= nloc) continue;
-            const int i0 = part * I / wpn, i1 = (part + 1) * I / wpn;
-            const float* wrow = w0s + (size_t)jl * I;
+            const int q0 = part * Ip4 / wpn, q1 = (part + 1) * Ip4 / wpn;
+            const float4* wrow = reinterpret_cast<const float4*>(w0s + (size_t)jl * Ip);
             float a0 = 0.0f, a1 = 0.0f, aq = 0.0f;
-            for (int i = i0 + lane; i < i1; i += 32) {
-                const float w = wrow[i];
-                a0 = fmaf(x0[i], w, a0);
-                if (has1) {
-                    a1 = fmaf(x1[i], w, a1);
-                    if (jl == 0) aq = fmaf(x1[i], x0[i], aq);
-                }
+            for (int q = q0 + lane; q < q1; q += 32) {
+                const float4 w = wrow[q], u = x0[q], v = x1[q];
+                a0 = dot4(u, w, a0);
+                a1 = dot4(v, w, a1);
+                if (jl == 0) aq = dot4(v, u, aq);
             }
             a0 = warp_sum(a0);
             a1 = warp_sum(a1);
@@ -637,99 +630,110 @@ __global__ void __launch_bounds__(kClThreads, 1) k_sgd_cluster(SgdArgs A) {
         }
     }
     __syncthreads();
-    double loss_acc = 0.0;
-    unsigned long long correct_acc = 0;
-    const bool stats = critical && rank == 0 && lane == 0;
-    if (stats && A.loss_sum) loss_acc = *A.loss_sum;
     const uint32_t gat_base = smem_u32(gat);
-    if (critical && n > 0) {
-        for (int j = lane; j < nloc; j += 32) {
-            float z = red[(size_t)j * wpn];
-            for (int p = 1; p < wpn; ++p) z += red[(size_t)j * wpn + p];
-            z = sadd(z, b0s[j]);
-            zcur[j] = z;
-            acur[j] = tanhf(z);
-        }
-        __syncwarp();
-        if (lane < L.Cp) {
-            float P = 0.0f;
+    // critical-warp registers: lane k owns class k, lane j owns neuron j (< 32)
+    float b1k = 0.0f, Pk = 0.0f;
+    if (critical) {
+        if (lane < C) b1k = A.b1[lane];
+        if (n > 0) {
+            for (int j = lane; j < nloc; j += 32) {
+                float z = red[(size_t)j * wpn];
+                for (int p = 1; p < wpn; ++p) z += red[(size_t)j * wpn + p];
+                z = sadd(z, b0s[j]);
+                zcur[j] = z;
+                abuf[j] = tanhf(z);
+            }
+            __syncwarp();
             if (lane < C)
-                for (int j = 0; j < nloc; ++j) P = fmaf(acur[j], w1s[(size_t)j * C + lane], P);
-            pk[lane] = P;
+                for (int j = 0; j < nloc; ++j) Pk = fmaf(abuf[j], w1s[(size_t)j * C + lane], Pk);
         }
-        __syncwarp();
     }
     cluster_sync_all();  // every CTA initialised (mbarriers, smem) before remote traffic
-    if (critical && n > 0 && lane < CS) {
-        const uint32_t dst = mapa_shared(gat_base + (uint32_t)(rank * L.Cp * sizeof(float)), lane);
-        const uint32_t rb = mapa_shared(mbar0, lane);
-        for (int q = 0; q < L.Cp; q += 4) st_async_v4(dst + 4 * q, pk[q], pk[q + 1], pk[q + 2], pk[q + 3], rb);
+    if (critical && n > 0 && lane < Cp) {
+        const uint32_t off = gat_base + (uint32_t)((rank * Cp + lane) * sizeof(float));
+        for (int p = 0; p < CS; ++p) st_async_f32(mapa_shared(off, p), Pk, mapa_shared(mbar0, p));
     }
     if (!critical) {
         __threadfence_block();
         named_arrive(kBarPass, kClThreads);  // "pass(-1) done": y(1), q(1) ready
     }
-    // bulk: sample index of the next prefetch, tracked without 64-bit division
-    long long kpre = A.n > 0 ? 3 % A.n : 0;
+    long long kpre = A.n > 0 ? 3 % A.n : 0;  // bulk: row of the next prefetch
+    double loss_acc = 0.0;
+    unsigned long long correct_acc = 0;
+    const bool stats = rank == 0 && tid == 32 * (kClBulkWarps - 1);  // last bulk warp, lane 0
+    if (stats && A.loss_sum) loss_acc = *A.loss_sum;
 
     // ---------------- the sample stream ----------------
-    for (long long s = 0; s < n; ++s) {
-        const int par = (int)(s & 1);
+    for (int s = 0; s < n; ++s) {
+        const int par = s & 1;
+        float* pl = plb + par * Cp;
+        float* d0 = d0b + par * L.npc;
         if (critical) {
-            // -- wait for every CTA's partial logits of sample s
+            const float* acur = abuf + par * L.npc;
+            float* anxt = abuf + (par ^ 1) * L.npc;
             const uint32_t mb = mbar0 + 8 * par;
-            const uint32_t phase = (uint32_t)((s >> 1) & 1);
             SGD_TRACE(0);
-            while (!mbar_try_wait(mb, phase)) {
+            while (!mbar_try_wait(mb, (uint32_t)((s >> 1) & 1))) {
             }
-            // re-arm this barrier for sample s+2 (peers cannot send s+2 before
-            // they have this CTA's partials of s+1, which are sent below)
+            // re-arm for sample s+2 (peers cannot send s+2 before they hold
+            // this CTA's partials of s+1, which are sent below)
             if (lane == 0 && s + 2 < n) mbar_arrive_expect_tx(mb, xbytes);
             SGD_TRACE(1);
+            // -- logits, softmax, output deltas
             const float* tc = trow(s);
             float zk = -INFINITY, e = 0.0f, dk = 0.0f;
             if (lane < C) {
-                const float* g = gat + (size_t)par * CS * L.Cp + lane;
+                const float* g = gat + (size_t)par * CS * Cp + lane;
                 float v0 = 0.0f, v1 = 0.0f, v2 = 0.0f, v3 = 0.0f;
                 int c = 0;
                 for (; c + 4 <= CS; c += 4) {
-                    v0 += g[(size_t)(c + 0) * L.Cp];
-                    v1 += g[(size_t)(c + 1) * L.Cp];
-                    v2 += g[(size_t)(c + 2) * L.Cp];
-                    v3 += g[(size_t)(c + 3) * L.Cp];
+                    v0 += g[(size_t)(c + 0) * Cp];
+                    v1 += g[(size_t)(c + 1) * Cp];
+                    v2 += g[(size_t)(c + 2) * Cp];
+                    v3 += g[(size_t)(c + 3) * Cp];
                 }
-                for (; c < CS; ++c) v0 += g[(size_t)c * L.Cp];
-                zk = sadd((v0 + v1) + (v2 + v3), b1s[lane]);
+                for (; c < CS; ++c) v0 += g[(size_t)c * Cp];
+                zk = sadd((v0 + v1) + (v2 + v3), b1k);
             }
             const float m = warp_max(zk);
             if (lane < C) e = expf(zk - m);
             const float sum = warp_sum(e);
             if (lane < C) {
-                const float p = __fdiv_rn(e, sum);
-                dk = ssub(p, tc[lane]);
+                const float pk = __fdiv_rn(e, sum);
+                dk = ssub(pk, tc[lane]);
                 zl[lane] = zk;
-                pl[lane] = p;
+                pl[lane] = pk;
                 dl[lane] = dk;
             }
+            __syncwarp();
             SGD_TRACE(2);
-            // -- hidden deltas with W1(s): d1 broadcast by shuffles, sequential
-            //    k in reference rounding
-            for (int j0 = 0; j0 < nloc; j0 += 32) {
-                const int j = j0 + lane;
-                const float* wrow = w1s + (size_t)min(j, nloc - 1) * C;
+            // -- hidden deltas with W1(s) (sequential k, reference rounding)
+            for (int j = lane; j < nloc; j += 32) {
+                const float* wrow = w1s + (size_t)j * C;
                 float acc = 0.0f;
-                for (int k = 0; k < C; ++k) acc = sadd(acc, smul(__shfl_sync(0xffffffffu, dk, k), wrow[k]));
-                if (j < nloc) d0[j] = tanh_grad(acur[j], acc);
+                if constexpr (CT > 0) {
+                    float wv[CT], dv[CT];
+#pragma unroll
+                    for (int k = 0; k < CT; ++k) {
+                        wv[k] = wrow[k];
+                        dv[k] = dl[k];
+                    }
+#pragma unroll
+                    for (int k = 0; k < CT; ++k) acc = sadd(acc, smul(dv[k], wv[k]));
+                } else {
+                    for (int k = 0; k < C; ++k) acc = sadd(acc, smul(dl[k], wrow[k]));
+                }
+                d0[j] = tanh_grad(acur[j], acc);
             }
             __syncwarp();
             SGD_TRACE(3);
-            named_sync(kBarPass, kClThreads);  // pass(s-1) done: y(s+1), q(s+1), t(s+1) visible
+            named_sync(kBarPass, kClThreads);  // pass(s-1) done: y(s+1), q(s+1), t(s+1)
             SGD_TRACE(4);
             __threadfence_block();
-            named_arrive(kBarDelta, kClThreads);  // release d0(s) to the bulk warps
+            named_arrive(kBarDelta, kClThreads);  // release d0(s), p(s)
             if (s + 1 < n) {
-                // -- z(s+1), a(s+1)
-                const int pn = (int)((s + 1) & 1);
+                // -- z(s+1) = y(s+1) + (-eta d0(s)) q(s+1) + b0(s+1);  a(s+1) = tanh
+                const int pn = par ^ 1;
                 float qv = 0.0f;
                 for (int p = 0; p < wpn; ++p) qv += qred[pn * wpn + p];
                 for (int j = lane; j < nloc; j += 32) {
@@ -746,47 +750,45 @@ __global__ void __launch_bounds__(kClThreads, 1) k_sgd_cluster(SgdArgs A) {
                 __syncwarp();
                 SGD_TRACE(5);
                 // -- W1 update of sample s fused with the partial logits of s+1
+                Pk = 0.0f;
                 if (lane < C) {
-                    float P0 = 0.0f, P1 = 0.0f;
+                    float P1 = 0.0f;
                     int j = 0;
                     for (; j + 2 <= nloc; j += 2) {
-                        float* w0p = w1s + (size_t)j * C + lane;
-                        float* w1p = w0p + C;
-                        const float wa = sgd_apply(*w0p, neg_eta, dk, acur[j]);
-                        const float wb = sgd_apply(*w1p, neg_eta, dk, acur[j + 1]);
-                        *w0p = wa;
-                        *w1p = wb;
-                        P0 = fmaf(anxt[j], wa, P0);
-                        P1 = fmaf(anxt[j + 1], wb, P1);
+                        float* wa = w1s + (size_t)j * C + lane;
+                        float* wb = wa + C;
+                        const float na = sgd_apply(*wa, neg_eta, dk, acur[j]);
+                        const float nb = sgd_apply(*wb, neg_eta, dk, acur[j + 1]);
+                        *wa = na;
+                        *wb = nb;
+                        Pk = fmaf(anxt[j], na, Pk);
+                        P1 = fmaf(anxt[j + 1], nb, P1);
                     }
                     if (j < nloc) {
-                        float* w0p = w1s + (size_t)j * C + lane;
-                        const float wa = sgd_apply(*w0p, neg_eta, dk, acur[j]);
-                        *w0p = wa;
-                        P0 = fmaf(anxt[j], wa, P0);
+                        float* wa = w1s + (size_t)j * C + lane;
+                        const float na = sgd_apply(*wa, neg_eta, dk, acur[j]);
+                        *wa = na;
+                        Pk = fmaf(anxt[j], na, Pk);
                     }
-                    pk[lane] = P0 + P1;
-                    b1s[lane] = sadd(b1s[lane], smul(neg_eta, dk));
-                } else if (lane < L.Cp) {
-                    pk[lane] = 0.0f;
+                    Pk += P1;
+                    b1k = sadd(b1k, smul(neg_eta, dk));
                 }
-                __syncwarp();
-                for (int j = lane; j < nloc; j += 32) acur[j] = anxt[j];
                 SGD_TRACE(6);
-                // -- push partials(s+1) into every peer, then arrive on its mbarrier
-                if (lane < CS) {
-                    const uint32_t off = (uint32_t)(((size_t)(pn * CS + rank) * L.Cp) * sizeof(float));
-                    const uint32_t dst = mapa_shared(gat_base + off, lane);
-                    const uint32_t rb = mapa_shared(mbar0 + 8 * pn, lane);
-                    for (int q = 0; q < L.Cp; q += 4)
-                        st_async_v4(dst + 4 * q, pk[q], pk[q + 1], pk[q + 2], pk[q + 3], rb);
+                // -- push partial(s+1, k) to every peer (lane k sends its class)
+                if (lane < Cp) {
+                    const uint32_t off = gat_base + (uint32_t)(((pn * CS + rank) * Cp + lane) * sizeof(float));
+                    const uint32_t mbn = mbar0 + 8 * pn;
+                    for (int p = 0; p < CS; ++p) st_async_f32(mapa_shared(off, p), Pk, mapa_shared(mbn, p));
                 }
                 __syncwarp();
                 SGD_TRACE(7);
             }
+        } else {
+            named_sync(kBarDelta, kClThreads);  // d0(s), p(s) visible
+            SGD_TRACE(8);
             if (stats) {
-                // loss / accuracy of sample s (network.cpp:165-168) while the
-                // exchange of s+1 is in flight
+                // loss / accuracy of sample s (network.cpp:165-168)
+                const float* tc = trow(s);
                 float loss = 0.0f;
                 int bp = 0, btg = 0;
                 for (int o = 0; o < C; ++o) {
@@ -800,71 +802,58 @@ __global__ void __launch_bounds__(kClThreads, 1) k_sgd_cluster(SgdArgs A) {
                 loss_acc = __dadd_rn(loss_acc, (double)loss);
                 correct_acc += bp == btg;
             }
-            __syncwarp();
-        } else {
-            named_sync(kBarDelta, kClThreads);  // d0(s) visible
-            SGD_TRACE(8);
             // prefetch x/t(s+3); make x(s+2) resident
             if (s + 3 < n) {
                 const long long kk = A.order ? (long long)A.order[s + 3] : kpre;
-                const float* xs = A.X + kk * A.I;
-                const float* ts = A.T + kk * A.C;
-                float* xd = xrow(s + 3);
-                float* td = trow(s + 3);
-                if (((A.I & 3) == 0) && ((reinterpret_cast<uintptr_t>(xs) & 15) == 0)) {
-                    for (int q = bt; q < (I >> 2); q += 32 * kClBulkWarps) cp_async16(xd + 4 * q, xs + 4 * q);
-                } else {
-                    for (int i = bt; i < I; i += 32 * kClBulkWarps) cp_async4(xd + i, xs + i);
-                }
-                for (int c = bt; c < C; c += 32 * kClBulkWarps) cp_async4(td + c, ts + c);
+                prefetch_row_k(A, kk, xrow(s + 3), trow(s + 3), tid, 32 * kClBulkWarps);
                 if (++kpre == A.n) kpre = 0;
             }
             cp_async_commit();
             cp_async_wait<1>();
-            named_sync(3, 32 * kClBulkWarps);  // bulk-only barrier: cp.async data visible
+            named_sync(kBarBulk, 32 * kClBulkWarps);  // cp.async data visible to all bulk warps
             SGD_TRACE(9);
-            // -- pass(s): W0 update of sample s fused with y(s+2), q(s+2)
-            const float* xs = xrow(s);
-            const float* x1 = xrow(s + 1);
-            const float* x2 = xrow(s + 2);
+            // -- pass(s): W0 update of sample s fused with y(s+2), q(s+2);
+            //    128-bit shared-memory traffic (4 weights per access)
+            const float4* xs = reinterpret_cast<const float4*>(xrow(s));
+            const float4* x1 = reinterpret_cast<const float4*>(xrow(s + 1));
+            const float4* x2 = reinterpret_cast<const float4*>(xrow(s + 2));
             const bool do_y = s + 2 < n;
-            const int py = par;  // y(s+2) has the parity of s
+            const int Ip4 = Ip >> 2;
             for (int r = 0; r * nper < nloc; ++r) {
-                const int jl = r * nper + bw / wpn, part = bw % wpn;
+                const int jl = r * nper + warp / wpn, part = warp % wpn;
                 if (jl >= nloc) continue;
-                const int i0 = part * I / wpn, i1 = (part + 1) * I / wpn;
-                float* wrow = w0s + (size_t)jl * I;
+                const int q0 = part * Ip4 / wpn, q1 = (part + 1) * Ip4 / wpn;
+                float4* wrow = reinterpret_cast<float4*>(w0s + (size_t)jl * Ip);
                 const float dj = d0[jl];
-                float acc0 = 0.0f, acc1 = 0.0f, aq0 = 0.0f, aq1 = 0.0f;
-                int i = i0 + lane;
                 if (do_y) {
+                    float acc0 = 0.0f, acc1 = 0.0f, aq = 0.0f;
                     const bool qrow = jl == 0;
-                    for (; i + 32 < i1; i += 64) {
-                        const float wa = sgd_apply(wrow[i], neg_eta, dj, xs[i]);
-                        const float wb = sgd_apply(wrow[i + 32], neg_eta, dj, xs[i + 32]);
-                        wrow[i] = wa;
-                        wrow[i + 32] = wb;
-                        acc0 = fmaf(x2[i], wa, acc0);
-                        acc1 = fmaf(x2[i + 32], wb, acc1);
-                        if (qrow) {
-                            aq0 = fmaf(x2[i], x1[i], aq0);
-                            aq1 = fmaf(x2[i + 32], x1[i + 32], aq1);
-                        }
+                    int q = q0 + lane;
+                    for (; q + 32 < q1; q += 64) {
+                        const float4 wa = sgd_apply4(wrow[q], neg_eta, dj, xs[q]);
+                        const float4 wb = sgd_apply4(wrow[q + 32], neg_eta, dj, xs[q + 32]);
+                        wrow[q] = wa;
+                        wrow[q + 32] = wb;
+                        const float4 ua = x2[q], ub = x2[q + 32];
+                        acc0 = dot4(ua, wa, acc0);
+                        acc1 = dot4(ub, wb, acc1);
+                        if (qrow) aq = dot4(ua, x1[q], dot4(ub, x1[q + 32], aq));
                     }
-                    if (i < i1) {
-                        const float wa = sgd_apply(wrow[i], neg_eta, dj, xs[i]);
-                        wrow[i] = wa;
-                        acc0 = fmaf(x2[i], wa, acc0);
-                        if (qrow) aq0 = fmaf(x2[i], x1[i], aq0);
+                    if (q < q1) {
+                        const float4 wa = sgd_apply4(wrow[q], neg_eta, dj, xs[q]);
+                        wrow[q] = wa;
+                        const float4 ua = x2[q];
+                        acc0 = dot4(ua, wa, acc0);
+                        if (qrow) aq = dot4(ua, x1[q], aq);
                     }
                     const float acc = warp_sum(acc0 + acc1);
-                    const float aq = qrow ? warp_sum(aq0 + aq1) : 0.0f;
+                    if (qrow) aq = warp_sum(aq);
                     if (lane == 0) {
-                        red[(size_t)py * L.npc * wpn + (size_t)jl * wpn + part] = acc;
-                        if (qrow) qred[py * wpn + part] = aq;
+                        red[(size_t)par * L.npc * wpn + (size_t)jl * wpn + part] = acc;
+                        if (qrow) qred[par * wpn + part] = aq;
                     }
                 } else {
-                    for (; i < i1; i += 32) wrow[i] = sgd_apply(wrow[i], neg_eta, dj, xs[i]);
+                    for (int q = q0 + lane; q < q1; q += 32) wrow[q] = sgd_apply4(wrow[q], neg_eta, dj, xs[q]);
                 }
             }
             SGD_TRACE(10);
@@ -878,35 +867,37 @@ __global__ void __launch_bounds__(kClThreads, 1) k_sgd_cluster(SgdArgs A) {
 
     // ---------------- write back (W0 already final; W1/biases: last update) ----------------
     if (n > 0) {
+        const int lp = (n - 1) & 1;
         const float* xl = xrow(n - 1);
+        const float* al = abuf + lp * L.npc;
+        const float* dlast = d0b + lp * L.npc;
         for (int e = tid; e < nloc * I; e += kClThreads) {
             const int j = e / I, i = e - j * I;
-            A.W0[(size_t)i * H + h0 + j] = w0s[e];
+            A.W0[(size_t)i * H + h0 + j] = w0s[(size_t)j * Ip + i];
         }
         for (int e = tid; e < nloc * C; e += kClThreads) {
             const int j = e / C, k = e - j * C;
-            A.W1[(size_t)h0 * C + e] = sgd_apply(w1s[e], neg_eta, dl[k], acur[j]);
+            A.W1[(size_t)h0 * C + e] = sgd_apply(w1s[e], neg_eta, dl[k], al[j]);
         }
         for (int j = tid; j < nloc; j += kClThreads) {
-            const float db = smul(neg_eta, d0[j]);
+            const float db = smul(neg_eta, dlast[j]);
             A.b0[h0 + j] = sadd(b0s[j], db);
             A.z0[h0 + j] = zcur[j];
-            A.a0[h0 + j] = acur[j];
-            A.d0[h0 + j] = d0[j];
+            A.a0[h0 + j] = al[j];
+            A.d0[h0 + j] = dlast[j];
             A.db0[h0 + j] = db;
-            A.x1[h0 + j] = acur[j];
+            A.x1[h0 + j] = al[j];
         }
-        if (rank == 0) {
+        if (critical && rank == 0 && lane < C) {
+            const float db = smul(neg_eta, dl[lane]);
+            A.b1[lane] = sadd(b1k, db);
+            A.z1[lane] = zl[lane];
+            A.a1[lane] = plb[lp * Cp + lane];
+            A.d1[lane] = dl[lane];
+            A.db1[lane] = db;
+        }
+        if (rank == 0)
             for (int i = tid; i < I; i += kClThreads) A.x0[i] = xl[i];
-            for (int k = tid; k < C; k += kClThreads) {
-                const float db = smul(neg_eta, dl[k]);
-                A.b1[k] = sadd(b1s[k], db);
-                A.z1[k] = zl[k];
-                A.a1[k] = pl[k];
-                A.d1[k] = dl[k];
-                A.db1[k] = db;
-            }
-        }
         if (stats) {
             if (A.loss_sum) *A.loss_sum = loss_acc;
             if (A.correct) *A.correct += correct_acc;
