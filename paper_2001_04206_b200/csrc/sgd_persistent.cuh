@@ -572,8 +572,10 @@ __global__ void __launch_bounds__(kClThreads, 1) k_sgd_cluster(SgdArgs A) {
     const float neg_eta = A.neg_eta;
     const int wpn = A.wpn, nper = kClBulkWarps / wpn;
     const int n = (int)A.n_steps;
-    auto xrow = [&](int s) { return sm + L.xb + (size_t)(s & 3) * Ip; };
-    auto trow = [&](int s) { return sm + L.tb + (size_t)(s & 3) * Cp; };
+    float* const xb0 = sm + L.xb;
+    float* const tb0 = sm + L.tb;
+    auto xrow = [&](int s) { return xb0 + (s & 3) * Ip; };
+    auto trow = [&](int s) { return tb0 + (s & 3) * Cp; };
     // The critical warp is the LAST warp: the warp arbiter favours the highest
     // warp id, so the serial chain wins issue slots over the bulk pass.
     const bool critical = warp == kClWarps - 1;
@@ -662,6 +664,10 @@ __global__ void __launch_bounds__(kClThreads, 1) k_sgd_cluster(SgdArgs A) {
     unsigned long long correct_acc = 0;
     const bool stats = rank == 0 && tid == 32 * (kClBulkWarps - 1);  // last bulk warp, lane 0
     if (stats && A.loss_sum) loss_acc = *A.loss_sum;
+
+    // bulk warp geometry (loop-invariant): neuron slot, K part, float4 range
+    const int jw = warp / wpn, part = warp % wpn, nrounds = (nloc + nper - 1) / nper;
+    const int q0 = part * (Ip >> 2) / wpn, q1 = (part + 1) * (Ip >> 2) / wpn;
 
     // ---------------- the sample stream ----------------
     for (int s = 0; s < n; ++s) {
@@ -818,11 +824,9 @@ __global__ void __launch_bounds__(kClThreads, 1) k_sgd_cluster(SgdArgs A) {
             const float4* x1 = reinterpret_cast<const float4*>(xrow(s + 1));
             const float4* x2 = reinterpret_cast<const float4*>(xrow(s + 2));
             const bool do_y = s + 2 < n;
-            const int Ip4 = Ip >> 2;
-            for (int r = 0; r * nper < nloc; ++r) {
-                const int jl = r * nper + warp / wpn, part = warp % wpn;
+            for (int r = 0; r < nrounds; ++r) {
+                const int jl = r * nper + jw;
                 if (jl >= nloc) continue;
-                const int q0 = part * Ip4 / wpn, q1 = (part + 1) * Ip4 / wpn;
                 float4* wrow = reinterpret_cast<float4*>(w0s + (size_t)jl * Ip);
                 const float dj = d0[jl];
                 if (do_y) {
