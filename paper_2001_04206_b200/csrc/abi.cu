@@ -281,6 +281,7 @@ void run_forward_chain(lane_b200_net* net) {
 struct SgdPlan {
     bool ok = false;
     bool cluster = false;  // single thread-block cluster, DSMEM exchange
+    bool w0_smem = true;   // grid plan: W0 slices resident in shared memory
     int G = 0, npc = 0, wpn = 1;
     size_t smem = 0;
 };
@@ -329,23 +330,28 @@ bool cluster_fits(SgdKernel kern, int CS, size_t smem) {
     return cached_ok;
 }
 
+SgdKernel grid_kernel(int C, bool w0_smem) {
+    if (w0_smem) return C == 10 ? k_sgd_grid<10, true> : k_sgd_grid<0, true>;
+    return C == 10 ? k_sgd_grid<10, false> : k_sgd_grid<0, false>;
+}
+
 SgdPlan plan_persistent(lane_b200_net* net) {
     SgdPlan p;
     lane_b200_ctx* c = net->ctx;
     if (net->n_hidden != 1 || c->numerics != LANE_NUMERICS_FAST) return p;
     const int I = static_cast<int>(net->input_width), H = static_cast<int>(net->L(0).O),
               C = static_cast<int>(net->classes);
-    if (C > kSgdMaxC) return p;
+    if (C > kClMaxC) return p;
     const char* mode = std::getenv("LANE_B200_SGD_MODE");
-    if (!mode || std::strcmp(mode, "grid") != 0) {
-        // single-cluster plan: the whole hidden layer on <= 16 SMs
+    if (!mode || std::strcmp(mode, "cluster") == 0) {
+        // single-cluster plan: the whole hidden layer on <= 16 SMs, DSMEM exchange
         int CS = std::min(16, H);
         if (const char* e = std::getenv("LANE_B200_SGD_CLUSTER")) CS = std::max(1, std::min(std::atoi(e), std::min(16, H)));
         const int npc = (H + CS - 1) / CS;
         CS = (H + npc - 1) / npc;
         const int wpn = npc >= kClBulkWarps ? 1 : kClBulkWarps / next_pow2(npc);
         const ClSmem L(I, C, npc, wpn, CS);
-        if (C <= kClMaxC && L.total <= c->max_smem_optin && cluster_fits(cluster_kernel(C), CS, L.total)) {
+        if (L.total <= c->max_smem_optin && cluster_fits(cluster_kernel(C), CS, L.total)) {
             p.ok = p.cluster = true;
             p.G = CS;
             p.npc = npc;
@@ -353,20 +359,28 @@ SgdPlan plan_persistent(lane_b200_net* net) {
             p.smem = L.total;
             return p;
         }
-        if (mode && std::strcmp(mode, "cluster") == 0) return p;
+        if (mode) return p;
     }
+    // grid plan: every SM, L2 exchange; W0 in shared memory when it fits,
+    // otherwise streamed from HBM each sample
     int G = std::min(c->sm_count, H);
     if (const char* e = std::getenv("LANE_B200_SGD_CTAS")) G = std::max(1, std::min(std::atoi(e), std::min(c->sm_count, H)));
     const int npc = (H + G - 1) / G;
     G = (H + npc - 1) / npc;
-    const int wpn = npc >= kSgdWarps ? 1 : kSgdWarps / next_pow2(npc);
-    const SgdSmem L(I, C, npc, wpn, G);
-    if (L.total > c->max_smem_optin) return p;
+    const GrSmem Ls(I, C, npc, G, true), Lg(I, C, npc, G, false);
+    const bool force_stream = std::getenv("LANE_B200_SGD_STREAM") != nullptr;
+    if (!force_stream && Ls.total <= c->max_smem_optin) {
+        p.w0_smem = true;
+        p.smem = Ls.total;
+    } else if (Lg.total <= c->max_smem_optin) {
+        p.w0_smem = false;
+        p.smem = Lg.total;
+    } else {
+        return p;
+    }
     p.ok = true;
     p.G = G;
     p.npc = npc;
-    p.wpn = wpn;
-    p.smem = L.total;
     return p;
 }
 
@@ -439,15 +453,16 @@ void launch_persistent(lane_b200_net* net, const SgdPlan& P, const float* X, con
         cfg.numAttrs = 1;
         LANE_CUDA(cudaLaunchKernelEx(&cfg, kern, A));
     } else {
-        static size_t configured = 0;
-        if (P.smem > configured) {
-            LANE_CUDA(cudaFuncSetAttribute(k_sgd_persistent, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                           static_cast<int>(P.smem)));
-            configured = P.smem;
-        }
+        const SgdKernel kern = grid_kernel(A.C, P.w0_smem);
+        LANE_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                       static_cast<int>(P.smem)));
+        int per_sm = 0;
+        LANE_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, kClThreads, P.smem));
+        if (per_sm < 1 || P.G > per_sm * c->sm_count)
+            throw Error(LANE_ERR_CUDA, "grid SGD kernel cannot be co-resident");
         void* args[] = {&A};
-        LANE_CUDA(cudaLaunchCooperativeKernel(reinterpret_cast<void*>(k_sgd_persistent), dim3(P.G),
-                                              dim3(kSgdThreads), args, P.smem, c->stream));
+        LANE_CUDA(cudaLaunchCooperativeKernel(reinterpret_cast<void*>(kern), dim3(P.G), dim3(kClThreads), args,
+                                              P.smem, c->stream));
     }
     c->count();
     if (trace) {  // debug: per-phase cycle stamps of CTA 0

@@ -34,9 +34,6 @@
 
 namespace lane_b200 {
 
-constexpr int kSgdThreads = 256;
-constexpr int kSgdWarps = kSgdThreads / 32;
-constexpr int kSgdMaxC = 128;  // logits per lane: kSgdMaxC / 32
 
 struct SgdArgs {
     int I, H, C;
@@ -67,39 +64,6 @@ constexpr int kTraceSamples = 64, kTracePhases = 12;
             A.trace[s * kTracePhases + (ph)] = clock64();                                 \
     } while (0)
 
-struct SgdSmem {
-    int I, C, Ip, Cp, npc, wpn, G;
-    size_t w0s, w1s, xb, tb, b0s, z0s, a0s, ap, dp, b1s, zl, pl, dl, gat, red, red1, total;
-    __host__ __device__ SgdSmem(int I_, int C_, int npc_, int wpn_, int G_)
-        : I(I_), C(C_), npc(npc_), wpn(wpn_), G(G_) {
-        Ip = (I + 3) & ~3;
-        Cp = (C + 3) & ~3;
-        size_t o = 0;
-        auto take = [&](size_t n) {
-            size_t at = o;
-            o += (n + 3) & ~size_t(3);  // 16-byte aligned pieces
-            return at;
-        };
-        w0s = take((size_t)npc * I);
-        w1s = take((size_t)npc * C);
-        xb = take(3 * (size_t)Ip);
-        tb = take(3 * (size_t)Cp);
-        b0s = take(npc);
-        z0s = take(npc);
-        a0s = take(npc);
-        ap = take(npc);
-        dp = take(npc);
-        b1s = take(Cp);
-        zl = take(Cp);
-        pl = take(Cp);
-        dl = take(Cp);
-        gat = take((size_t)G * C);
-        red = take((size_t)npc * 8);
-        red1 = take((size_t)kSgdWarps * Cp);
-        total = o * sizeof(float);
-    }
-};
-
 __device__ __forceinline__ uint32_t smem_u32(const void* p) {
     return static_cast<uint32_t>(__cvta_generic_to_shared(p));
 }
@@ -127,288 +91,6 @@ __device__ __forceinline__ unsigned long long globaltimer_ns() {
     asm volatile("mov.u64 %0, %%globaltimer;\n" : "=l"(t));
     return t;
 }
-
-// Issue the cp.async copies of sample row k into the smem slot.
-__device__ __forceinline__ void prefetch_sample(const SgdArgs& A, long long s, float* xdst,
-                                                float* tdst) {
-    const long long k = A.order ? (long long)A.order[s] : s % A.n;
-    const float* xs = A.X + k * A.I;
-    const float* ts = A.T + k * A.C;
-    const bool vec = ((A.I & 3) == 0) && ((reinterpret_cast<uintptr_t>(xs) & 15) == 0);
-    if (vec) {
-        for (int q = threadIdx.x; q < (A.I >> 2); q += kSgdThreads) cp_async16(xdst + 4 * q, xs + 4 * q);
-    } else {
-        for (int i = threadIdx.x; i < A.I; i += kSgdThreads) cp_async4(xdst + i, xs + i);
-    }
-    for (int c = threadIdx.x; c < A.C; c += kSgdThreads) cp_async4(tdst + c, ts + c);
-}
-
-__global__ void __launch_bounds__(kSgdThreads, 1) k_sgd_persistent(SgdArgs A) {
-    extern __shared__ __align__(16) float sm[];
-    const SgdSmem L(A.I, A.C, A.npc, A.wpn, A.G);
-    float* w0s = sm + L.w0s;
-    float* w1s = sm + L.w1s;
-    float* b0s = sm + L.b0s;
-    float* z0s = sm + L.z0s;
-    float* a0s = sm + L.a0s;
-    float* ap = sm + L.ap;
-    float* dp = sm + L.dp;
-    float* b1s = sm + L.b1s;
-    float* zl = sm + L.zl;
-    float* pl = sm + L.pl;
-    float* dl = sm + L.dl;
-    float* gat = sm + L.gat;
-    float* red = sm + L.red;
-    float* red1 = sm + L.red1;
-    __shared__ int s_abort;
-
-    const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
-    const int I = A.I, H = A.H, C = A.C, G = A.G, cta = blockIdx.x;
-    const int h0 = min(H, cta * A.npc), h1 = min(H, h0 + A.npc), nloc = h1 - h0;
-    const float neg_eta = A.neg_eta;
-    const int wpn = A.wpn, nper = kSgdWarps / wpn;
-
-    // ---- stage this CTA's weight slices into shared memory (once) ----
-    for (int e = tid; e < nloc * I; e += kSgdThreads) {
-        const int j = e / I, i = e - j * I;
-        w0s[e] = A.W0[(size_t)i * H + h0 + j];
-    }
-    for (int e = tid; e < nloc * C; e += kSgdThreads) w1s[e] = A.W1[(size_t)h0 * C + e];
-    for (int j = tid; j < nloc; j += kSgdThreads) b0s[j] = A.b0[h0 + j];
-    for (int k = tid; k < C; k += kSgdThreads) b1s[k] = A.b1[k];
-    if (tid == 0) s_abort = 0;
-    double loss_acc = 0.0;
-    unsigned long long correct_acc = 0;
-    if (cta == 0 && tid == 0 && A.loss_sum) loss_acc = *A.loss_sum;
-
-    if (A.n_steps > 0) prefetch_sample(A, 0, sm + L.xb, sm + L.tb);
-    cp_async_commit();
-    __syncthreads();
-
-    long long s = 0;
-    for (; s < A.n_steps; ++s) {
-        const int cur = (int)(s % 3), prv = (int)((s + 2) % 3), nxt = (int)((s + 1) % 3);
-        const float* xc = sm + L.xb + (size_t)cur * L.Ip;
-        const float* xp = sm + L.xb + (size_t)prv * L.Ip;
-        const float* tc = sm + L.tb + (size_t)cur * L.Cp;
-        const bool lazy = s > 0;
-        if (s + 1 < A.n_steps)
-            prefetch_sample(A, s + 1, sm + L.xb + (size_t)nxt * L.Ip, sm + L.tb + (size_t)nxt * L.Cp);
-        cp_async_commit();
-        cp_async_wait<1>();
-        __syncthreads();
-
-        // ---- hidden forward with the lazy W0 update of sample s-1 ----
-        for (int r = 0; r * nper < nloc; ++r) {
-            const int jl = r * nper + warp / wpn, part = warp % wpn;
-            if (jl < nloc) {
-                const int i0 = (int)((long long)part * I / wpn), i1 = (int)((long long)(part + 1) * I / wpn);
-                float* wrow = w0s + (size_t)jl * I;
-                float acc = 0.0f;
-                if (lazy) {
-                    const float dj = dp[jl];
-                    for (int i = i0 + lane; i < i1; i += 32) {
-                        const float w = sgd_apply(wrow[i], neg_eta, dj, xp[i]);
-                        wrow[i] = w;
-                        acc = fmaf(xc[i], w, acc);
-                    }
-                } else {
-                    for (int i = i0 + lane; i < i1; i += 32) acc = fmaf(xc[i], wrow[i], acc);
-                }
-                acc = warp_sum(acc);
-                if (lane == 0) red[jl * wpn + part] = acc;
-            }
-        }
-        __syncthreads();
-        for (int j = tid; j < nloc; j += kSgdThreads) {
-            if (lazy) b0s[j] = sadd(b0s[j], smul(neg_eta, dp[j]));
-            float z = red[j * wpn];
-            for (int p = 1; p < wpn; ++p) z += red[j * wpn + p];
-            z = sadd(z, b0s[j]);
-            z0s[j] = z;
-            a0s[j] = lane_libm::tanhf(z);
-        }
-        __syncthreads();
-
-        // ---- partial logits with the lazy W1 update of sample s-1 ----
-        {
-            float acc[kSgdMaxC / 32];
-#pragma unroll
-            for (int m = 0; m < kSgdMaxC / 32; ++m) acc[m] = 0.0f;
-            for (int j = warp; j < nloc; j += kSgdWarps) {
-                const float aj = a0s[j], apj = ap[j];
-                float* wrow = w1s + (size_t)j * C;
-#pragma unroll
-                for (int m = 0; m < kSgdMaxC / 32; ++m) {
-                    const int k = lane + 32 * m;
-                    if (k < C) {
-                        float w = wrow[k];
-                        if (lazy) {
-                            w = sgd_apply(w, neg_eta, dl[k], apj);
-                            wrow[k] = w;
-                        }
-                        acc[m] = fmaf(aj, w, acc[m]);
-                    }
-                }
-            }
-#pragma unroll
-            for (int m = 0; m < kSgdMaxC / 32; ++m) {
-                const int k = lane + 32 * m;
-                if (k < C) red1[warp * L.Cp + k] = acc[m];
-            }
-        }
-        __syncthreads();
-        const uint32_t tag = (uint32_t)(s + 1);
-        unsigned long long* slot = A.slots + (size_t)(s & 1) * G * C;
-        for (int k = tid; k < C; k += kSgdThreads) {
-            float P = red1[k];
-            for (int w = 1; w < kSgdWarps; ++w) P += red1[w * L.Cp + k];
-            st_relaxed_u64(slot + (size_t)cta * C + k,
-                           ((unsigned long long)tag << 32) | __float_as_uint(P));
-            if (lazy) b1s[k] = sadd(b1s[k], smul(neg_eta, dl[k]));
-        }
-
-        // ---- exchange: gather every CTA's partial logits (tag == arrival) ----
-        // Up to 8 independent L2 loads in flight per thread; re-poll only the
-        // words whose tag has not arrived yet.
-        {
-            const unsigned long long t0 = globaltimer_ns();
-            const int GC = G * C;
-            for (int base = tid; base < GC; base += kSgdThreads * 8) {
-                unsigned long long v[8];
-#pragma unroll
-                for (int u = 0; u < 8; ++u) {
-                    const int e = base + u * kSgdThreads;
-                    v[u] = e < GC ? ld_relaxed_u64(slot + e) : ((unsigned long long)tag << 32);
-                }
-#pragma unroll
-                for (int u = 0; u < 8; ++u) {
-                    const int e = base + u * kSgdThreads;
-                    if (e < GC) {
-                        while ((uint32_t)(v[u] >> 32) != tag) {
-                            if (globaltimer_ns() - t0 > 5000000000ull) {  // 5 s: a bug, not a wait
-                                s_abort = 1;
-                                break;
-                            }
-                            v[u] = ld_relaxed_u64(slot + e);
-                        }
-                        gat[e] = __uint_as_float((uint32_t)v[u]);
-                    }
-                }
-            }
-        }
-        __syncthreads();
-        if (s_abort) break;
-        for (int k = warp; k < C; k += kSgdWarps) {
-            float v = 0.0f;
-            for (int c = lane; c < G; c += 32) v += gat[c * C + k];
-            v = warp_sum(v);
-            if (lane == 0) zl[k] = sadd(v, b1s[k]);
-        }
-        __syncthreads();
-
-        // ---- softmax, output deltas, loss (warp 0; identical in every CTA) ----
-        if (warp == 0) {
-            float e[kSgdMaxC / 32];
-            float m = -INFINITY;
-#pragma unroll
-            for (int q = 0; q < kSgdMaxC / 32; ++q) {
-                const int k = lane + 32 * q;
-                if (k < C) m = fmaxf(m, zl[k]);
-            }
-            m = warp_max(m);
-            float sum = 0.0f;
-#pragma unroll
-            for (int q = 0; q < kSgdMaxC / 32; ++q) {
-                const int k = lane + 32 * q;
-                e[q] = k < C ? lane_libm::expf(ssub(zl[k], m)) : 0.0f;
-                sum += e[q];
-            }
-            sum = warp_sum(sum);
-#pragma unroll
-            for (int q = 0; q < kSgdMaxC / 32; ++q) {
-                const int k = lane + 32 * q;
-                if (k < C) {
-                    const float p = __fdiv_rn(e[q], sum);
-                    pl[k] = p;
-                    dl[k] = ssub(p, tc[k]);
-                }
-            }
-            __syncwarp();
-            if (cta == 0 && lane == 0) {
-                float loss = 0.0f;
-                int bp = 0, bt = 0;
-                for (int o = 0; o < C; ++o) {
-                    if (tc[o] != 0.0f) {
-                        const float q = pl[o] < 1e-12f ? 1e-12f : pl[o];
-                        loss = ssub(loss, smul(tc[o], lane_libm::logf(q)));
-                    }
-                    if (pl[o] > pl[bp]) bp = o;
-                    if (tc[o] > tc[bt]) bt = o;
-                }
-                loss_acc = __dadd_rn(loss_acc, (double)loss);
-                correct_acc += bp == bt;
-            }
-        }
-        __syncthreads();
-
-        // ---- hidden deltas with pre-update W1 (already holds W1(s)) ----
-        for (int j = tid; j < nloc; j += kSgdThreads) {
-            const float* wrow = w1s + (size_t)j * C;
-            // sequential k, separately rounded: exactly fc_backward_tuple's sum
-            float acc = 0.0f;
-            for (int k = 0; k < C; ++k) acc = sadd(acc, smul(dl[k], wrow[k]));
-            dp[j] = tanh_grad(a0s[j], acc);
-            ap[j] = a0s[j];
-        }
-        __syncthreads();
-    }
-
-    if (s_abort) {
-        if (tid == 0) atomicExch(A.error, 1);
-        return;
-    }
-    cp_async_wait<0>();
-
-    // ---- apply the last pending update and write everything back ----
-    if (A.n_steps > 0) {
-        const int last = (int)((A.n_steps - 1) % 3);
-        const float* xl = sm + L.xb + (size_t)last * L.Ip;
-        for (int e = tid; e < nloc * I; e += kSgdThreads) {
-            const int j = e / I, i = e - j * I;
-            A.W0[(size_t)i * H + h0 + j] = sgd_apply(w0s[e], neg_eta, dp[j], xl[i]);
-        }
-        for (int e = tid; e < nloc * C; e += kSgdThreads) {
-            const int j = e / C, k = e - j * C;
-            A.W1[(size_t)h0 * C + e] = sgd_apply(w1s[e], neg_eta, dl[k], ap[j]);
-        }
-        for (int j = tid; j < nloc; j += kSgdThreads) {
-            const float db = smul(neg_eta, dp[j]);
-            A.b0[h0 + j] = sadd(b0s[j], db);
-            A.z0[h0 + j] = z0s[j];
-            A.a0[h0 + j] = ap[j];
-            A.d0[h0 + j] = dp[j];
-            A.db0[h0 + j] = db;
-            A.x1[h0 + j] = ap[j];
-        }
-        if (cta == 0) {
-            for (int i = tid; i < I; i += kSgdThreads) A.x0[i] = xl[i];
-            for (int k = tid; k < C; k += kSgdThreads) {
-                const float db = smul(neg_eta, dl[k]);
-                A.b1[k] = sadd(b1s[k], db);
-                A.z1[k] = zl[k];
-                A.a1[k] = pl[k];
-                A.d1[k] = dl[k];
-                A.db1[k] = db;
-            }
-            if (tid == 0) {
-                if (A.loss_sum) *A.loss_sum = loss_acc;
-                if (A.correct) *A.correct += correct_acc;
-            }
-        }
-    }
-}
-
 
 // ===========================================================================
 // Cluster variant (the B=1 flagship): the whole hidden layer lives in ONE
@@ -908,6 +590,447 @@ __global__ void __launch_bounds__(kClThreads, 1) k_sgd_cluster(SgdArgs A) {
         }
     }
     cluster_sync_all();  // no CTA exits while a peer may still address its shared memory
+}
+
+// ===========================================================================
+// Grid variant (large widths, e.g. 340-16384-10 and the paper's 340-100000-10):
+// the same warp specialisation as k_sgd_cluster, over ALL SMs (cooperative
+// launch, one CTA per SM).  The per-sample exchange of partial logits goes
+// through L2 as 64-bit {value, sample tag} words (single-copy atomic, the tag
+// doubles as the arrival flag).  W0 is either resident in shared memory
+// (W0_SMEM, slices up to ~200 KB per SM) or streamed from HBM every sample in
+// its native row-major layout with coalesced column access (the paper shape:
+// 8 B per weight per sample, the algorithmic minimum -- HBM-bound).
+// ===========================================================================
+
+constexpr int kGrChunks = 4;  // K chunks per column in the streamed pass
+
+struct GrSmem {
+    int I, C, Ip, Cp, npc, G;
+    bool w0_smem;
+    size_t w0s, w1s, xb, tb, b0s, abuf, zcur, d0, zl, pl, dl, gat, red, qred, total;
+    __host__ __device__ GrSmem(int I_, int C_, int npc_, int G_, bool w0_smem_)
+        : I(I_), C(C_), npc(npc_), G(G_), w0_smem(w0_smem_) {
+        Ip = (I + 3) & ~3;
+        Cp = (C + 3) & ~3;
+        size_t o = 0;
+        auto take = [&](size_t n) {
+            size_t at = o;
+            o += (n + 3) & ~size_t(3);
+            return at;
+        };
+        w0s = take(w0_smem ? (size_t)npc * Ip : 0);
+        w1s = take((size_t)npc * C);
+        xb = take(4 * (size_t)Ip);
+        tb = take(4 * (size_t)Cp);
+        b0s = take(npc);
+        abuf = take(2 * (size_t)npc);
+        zcur = take(npc);
+        d0 = take(2 * (size_t)npc);
+        zl = take(Cp);
+        pl = take(2 * (size_t)Cp);
+        dl = take(Cp);
+        gat = take((size_t)G * Cp);
+        red = take(2 * (size_t)npc * kGrChunks);  // [parity][j][chunk] (smem mode: chunk 0 only)
+        qred = take(2 * 4);
+        total = o * sizeof(float);
+    }
+};
+
+template <int CT, bool W0_SMEM>
+__global__ void __launch_bounds__(kClThreads, 1) k_sgd_grid(SgdArgs A) {
+    extern __shared__ __align__(16) float sm[];
+    const GrSmem L(A.I, A.C, A.npc, A.G, W0_SMEM);
+    float* w0s = sm + L.w0s;
+    float* w1s = sm + L.w1s;
+    float* b0s = sm + L.b0s;
+    float* abuf = sm + L.abuf;
+    float* zcur = sm + L.zcur;
+    float* d0b = sm + L.d0;
+    float* zl = sm + L.zl;
+    float* plb = sm + L.pl;
+    float* dl = sm + L.dl;
+    float* gat = sm + L.gat;
+    float* red = sm + L.red;
+    float* qred = sm + L.qred;
+
+    const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+    const int I = A.I, H = A.H, G = A.G, Ip = L.Ip, Cp = L.Cp;
+    const int C = CT > 0 ? CT : A.C;
+    const int cta = blockIdx.x;
+    const int h0 = min(H, cta * A.npc), h1 = min(H, h0 + A.npc), nloc = h1 - h0;
+    const float neg_eta = A.neg_eta;
+    const int n = (int)A.n_steps;
+    const int npc = L.npc;
+    float* const xb0 = sm + L.xb;
+    float* const tb0 = sm + L.tb;
+    auto xrow = [&](int s) { return xb0 + (s & 3) * Ip; };
+    auto trow = [&](int s) { return tb0 + (s & 3) * Cp; };
+    const bool critical = warp == kClWarps - 1;
+    constexpr int NB = 32 * kClBulkWarps;  // bulk threads
+    // reductions per neuron: smem mode -> 1 (a warp owns a whole row);
+    // streamed mode -> kGrChunks K-chunks per column
+    constexpr int NR = W0_SMEM ? 1 : kGrChunks;
+
+    // ---------------- prologue ----------------
+    for (int e = tid; e < 4 * Ip; e += kClThreads) xb0[e] = 0.0f;
+    if constexpr (W0_SMEM) {
+        for (int e = tid; e < nloc * Ip; e += kClThreads) {
+            const int j = e / Ip, i = e - j * Ip;
+            w0s[e] = i < I ? A.W0[(size_t)i * H + h0 + j] : 0.0f;
+        }
+    }
+    for (int e = tid; e < nloc * C; e += kClThreads) w1s[e] = A.W1[(size_t)h0 * C + e];
+    for (int j = tid; j < nloc; j += kClThreads) b0s[j] = A.b0[h0 + j];
+    __syncthreads();
+    for (int s = 0; s < 3 && s < n; ++s) {
+        const long long k = A.order ? (long long)A.order[s] : s % A.n;
+        prefetch_row_k(A, k, xrow(s), trow(s), tid, kClThreads);
+    }
+    cp_async_commit();
+    cp_async_wait<0>();
+    __syncthreads();
+
+    // The bulk pass.  mode 0 (prologue): z(0) -> red[0], y(1) -> red[1], q(1);
+    // mode 1 (sample s): W0 update of s, y(s+2) -> red[par], q(s+2) -> qred[par].
+    auto bulk_pass = [&](int mode, int s) {
+        const float* xs = mode ? xrow(s) : xrow(0);
+        const float* x1 = mode ? xrow(s + 1) : xrow(1);
+        const float* x2 = mode ? xrow(s + 2) : xrow(1);
+        const bool do_y = mode ? (s + 2 < n) : true;
+        const int py = mode ? (s & 1) : 1;
+        const float* d0 = d0b + (s & 1) * npc;
+        // q = x2 . x1 (prologue: x1 . x0), one warp
+        if (warp == kClBulkWarps - 1 && do_y) {
+            const float* qa = mode ? x1 : xrow(0);
+            float aq = 0.0f;
+            for (int i = lane; i < I; i += 32) aq = fmaf(x2[i], qa[i], aq);
+            aq = warp_sum(aq);
+            if (lane == 0) qred[py * 4] = aq;
+        }
+        if constexpr (W0_SMEM) {
+            const int Ip4 = Ip >> 2;
+            for (int jl = warp; jl < nloc; jl += kClBulkWarps) {
+                float4* wrow = reinterpret_cast<float4*>(w0s + (size_t)jl * Ip);
+                const float4* xs4 = reinterpret_cast<const float4*>(xs);
+                const float4* x24 = reinterpret_cast<const float4*>(x2);
+                const float4* x04 = reinterpret_cast<const float4*>(xrow(0));
+                float acc0 = 0.0f, acc1 = 0.0f;
+                if (mode == 0) {
+                    for (int q = lane; q < Ip4; q += 32) {
+                        const float4 w = wrow[q];
+                        acc0 = dot4(x04[q], w, acc0);
+                        acc1 = dot4(x24[q], w, acc1);
+                    }
+                    acc0 = warp_sum(acc0);
+                    acc1 = warp_sum(acc1);
+                    if (lane == 0) {
+                        red[(size_t)jl * NR] = acc0;
+                        red[(size_t)npc * NR + (size_t)jl * NR] = acc1;
+                    }
+                } else if (do_y) {
+                    const float dj = d0[jl];
+                    for (int q = lane; q < Ip4; q += 32) {
+                        const float4 w = sgd_apply4(wrow[q], neg_eta, dj, xs4[q]);
+                        wrow[q] = w;
+                        acc0 = dot4(x24[q], w, acc0);
+                    }
+                    acc0 = warp_sum(acc0);
+                    if (lane == 0) red[(size_t)py * npc * NR + (size_t)jl * NR] = acc0;
+                } else {
+                    const float dj = d0[jl];
+                    for (int q = lane; q < Ip4; q += 32) wrow[q] = sgd_apply4(wrow[q], neg_eta, dj, xs4[q]);
+                }
+            }
+        } else {
+            // streamed: items (chunk c, column j), consecutive threads ->
+            // consecutive columns of one W0 row (coalesced 128 B segments)
+            const int items = nloc * kGrChunks;
+            for (int it = tid; it < items; it += NB) {
+                const int c = it / nloc, jl = it - c * nloc;
+                const int i0 = c * I / kGrChunks, i1 = (c + 1) * I / kGrChunks;
+                float* col = A.W0 + (size_t)(h0 + jl);
+                float acc0 = 0.0f, acc1 = 0.0f;
+                if (mode == 0) {
+                    const float* x0 = xrow(0);
+                    int i = i0;
+                    for (; i + 4 <= i1; i += 4) {
+                        float w[4];
+#pragma unroll
+                        for (int u = 0; u < 4; ++u) w[u] = __ldcg(col + (size_t)(i + u) * H);
+#pragma unroll
+                        for (int u = 0; u < 4; ++u) {
+                            acc0 = fmaf(x0[i + u], w[u], acc0);
+                            acc1 = fmaf(x2[i + u], w[u], acc1);
+                        }
+                    }
+                    for (; i < i1; ++i) {
+                        const float w = __ldcg(col + (size_t)i * H);
+                        acc0 = fmaf(x0[i], w, acc0);
+                        acc1 = fmaf(x2[i], w, acc1);
+                    }
+                    red[(size_t)jl * NR + c] = acc0;
+                    red[(size_t)npc * NR + (size_t)jl * NR + c] = acc1;
+                } else {
+                    const float dj = d0[jl];
+                    int i = i0;
+                    for (; i + 8 <= i1; i += 8) {
+                        float w[8];
+#pragma unroll
+                        for (int u = 0; u < 8; ++u) w[u] = __ldcg(col + (size_t)(i + u) * H);
+#pragma unroll
+                        for (int u = 0; u < 8; ++u) {
+                            w[u] = sgd_apply(w[u], neg_eta, dj, xs[i + u]);
+                            __stcg(col + (size_t)(i + u) * H, w[u]);
+                            acc0 = fmaf(x2[i + u], w[u], acc0);
+                        }
+                    }
+                    for (; i < i1; ++i) {
+                        const float w = sgd_apply(__ldcg(col + (size_t)i * H), neg_eta, dj, xs[i]);
+                        __stcg(col + (size_t)i * H, w);
+                        acc0 = fmaf(x2[i], w, acc0);
+                    }
+                    if (do_y) red[(size_t)py * npc * NR + (size_t)jl * NR + c] = acc0;
+                }
+            }
+        }
+    };
+
+    if (!critical) bulk_pass(0, 0);
+    __syncthreads();
+    float b1k = 0.0f, Pk = 0.0f;
+    if (critical) {
+        if (lane < C) b1k = A.b1[lane];
+        if (n > 0) {
+            for (int j = lane; j < nloc; j += 32) {
+                float z = red[(size_t)j * NR];
+                for (int p = 1; p < NR; ++p) z += red[(size_t)j * NR + p];
+                z = sadd(z, b0s[j]);
+                zcur[j] = z;
+                abuf[j] = tanhf(z);
+            }
+            __syncwarp();
+            if (lane < C) {
+                float P0 = 0.0f, P1 = 0.0f;
+                int j = 0;
+                for (; j + 2 <= nloc; j += 2) {
+                    P0 = fmaf(abuf[j], w1s[(size_t)j * C + lane], P0);
+                    P1 = fmaf(abuf[j + 1], w1s[(size_t)(j + 1) * C + lane], P1);
+                }
+                if (j < nloc) P0 = fmaf(abuf[j], w1s[(size_t)j * C + lane], P0);
+                Pk = P0 + P1;
+                st_relaxed_u64(A.slots + (size_t)cta * C + lane,
+                               (1ull << 32) | __float_as_uint(Pk));
+            }
+        }
+    } else {
+        __threadfence_block();
+        named_arrive(kBarPass, kClThreads);
+    }
+    long long kpre = A.n > 0 ? 3 % A.n : 0;
+    double loss_acc = 0.0;
+    unsigned long long correct_acc = 0;
+    const bool stats = cta == 0 && tid == 32 * (kClBulkWarps - 1);
+    if (stats && A.loss_sum) loss_acc = *A.loss_sum;
+    const int GC = G * C;
+
+    for (int s = 0; s < n; ++s) {
+        const int par = s & 1;
+        float* pl = plb + par * Cp;
+        float* d0 = d0b + par * npc;
+        if (critical) {
+            const float* acur = abuf + par * npc;
+            float* anxt = abuf + (par ^ 1) * npc;
+            // -- gather every CTA's partial logits of sample s from L2
+            const uint32_t tag = (uint32_t)(s + 1);
+            const unsigned long long* slot = A.slots + (size_t)par * GC;
+            const unsigned long long t0 = globaltimer_ns();
+            for (int base = lane; base < GC; base += 32 * 8) {
+                unsigned long long v[8];
+#pragma unroll
+                for (int u = 0; u < 8; ++u) {
+                    const int e = base + 32 * u;
+                    v[u] = e < GC ? ld_relaxed_u64(slot + e) : ((unsigned long long)tag << 32);
+                }
+#pragma unroll
+                for (int u = 0; u < 8; ++u) {
+                    const int e = base + 32 * u;
+                    if (e < GC) {
+                        while ((uint32_t)(v[u] >> 32) != tag) {
+                            if (globaltimer_ns() - t0 > 5000000000ull) {  // a bug, not a wait
+                                atomicExch(A.error, 1);
+                                __trap();
+                            }
+                            v[u] = ld_relaxed_u64(slot + e);
+                        }
+                        const int c = e / C, k = e - c * C;
+                        gat[(size_t)c * Cp + k] = __uint_as_float((uint32_t)v[u]);
+                    }
+                }
+            }
+            __syncwarp();
+            const float* tc = trow(s);
+            float zk = -INFINITY, e = 0.0f, dk = 0.0f;
+            if (lane < C) {
+                const float* g = gat + lane;
+                float v0 = 0.0f, v1 = 0.0f, v2 = 0.0f, v3 = 0.0f;
+                int c = 0;
+                for (; c + 4 <= G; c += 4) {
+                    v0 += g[(size_t)(c + 0) * Cp];
+                    v1 += g[(size_t)(c + 1) * Cp];
+                    v2 += g[(size_t)(c + 2) * Cp];
+                    v3 += g[(size_t)(c + 3) * Cp];
+                }
+                for (; c < G; ++c) v0 += g[(size_t)c * Cp];
+                zk = sadd((v0 + v1) + (v2 + v3), b1k);
+            }
+            const float m = warp_max(zk);
+            if (lane < C) e = expf(zk - m);
+            const float sum = warp_sum(e);
+            if (lane < C) {
+                const float pk = __fdiv_rn(e, sum);
+                dk = ssub(pk, tc[lane]);
+                zl[lane] = zk;
+                pl[lane] = pk;
+                dl[lane] = dk;
+            }
+            __syncwarp();
+            // -- hidden deltas with W1(s)
+            for (int j = lane; j < nloc; j += 32) {
+                const float* wrow = w1s + (size_t)j * C;
+                float acc = 0.0f;
+                if constexpr (CT > 0) {
+                    float wv[CT], dv[CT];
+#pragma unroll
+                    for (int k = 0; k < CT; ++k) {
+                        wv[k] = wrow[k];
+                        dv[k] = dl[k];
+                    }
+#pragma unroll
+                    for (int k = 0; k < CT; ++k) acc = sadd(acc, smul(dv[k], wv[k]));
+                } else {
+                    for (int k = 0; k < C; ++k) acc = sadd(acc, smul(dl[k], wrow[k]));
+                }
+                d0[j] = tanh_grad(acur[j], acc);
+            }
+            __syncwarp();
+            named_sync(kBarPass, kClThreads);
+            __threadfence_block();
+            named_arrive(kBarDelta, kClThreads);
+            if (s + 1 < n) {
+                const int pn = par ^ 1;
+                const float qv = qred[pn * 4];
+                for (int j = lane; j < nloc; j += 32) {
+                    const float dj = d0[j];
+                    const float b = sadd(b0s[j], smul(neg_eta, dj));
+                    b0s[j] = b;
+                    const float* ry = red + (size_t)pn * npc * NR + (size_t)j * NR;
+                    float y = ry[0];
+                    for (int p = 1; p < NR; ++p) y += ry[p];
+                    const float z = sadd(fmaf(neg_eta * dj, qv, y), b);
+                    anxt[j] = tanhf(z);
+                    zcur[j] = z;
+                }
+                __syncwarp();
+                if (lane < C) {
+                    float P0 = 0.0f, P1 = 0.0f;
+                    int j = 0;
+                    for (; j + 2 <= nloc; j += 2) {
+                        float* wa = w1s + (size_t)j * C + lane;
+                        float* wb = wa + C;
+                        const float na = sgd_apply(*wa, neg_eta, dk, acur[j]);
+                        const float nb = sgd_apply(*wb, neg_eta, dk, acur[j + 1]);
+                        *wa = na;
+                        *wb = nb;
+                        P0 = fmaf(anxt[j], na, P0);
+                        P1 = fmaf(anxt[j + 1], nb, P1);
+                    }
+                    if (j < nloc) {
+                        float* wa = w1s + (size_t)j * C + lane;
+                        const float na = sgd_apply(*wa, neg_eta, dk, acur[j]);
+                        *wa = na;
+                        P0 = fmaf(anxt[j], na, P0);
+                    }
+                    Pk = P0 + P1;
+                    b1k = sadd(b1k, smul(neg_eta, dk));
+                    st_relaxed_u64(A.slots + (size_t)pn * GC + (size_t)cta * C + lane,
+                                   ((unsigned long long)(s + 2) << 32) | __float_as_uint(Pk));
+                }
+                __syncwarp();
+            }
+        } else {
+            named_sync(kBarDelta, kClThreads);
+            if (stats) {
+                const float* tc = trow(s);
+                float loss = 0.0f;
+                int bp = 0, btg = 0;
+                for (int o = 0; o < C; ++o) {
+                    if (tc[o] != 0.0f) {
+                        const float q = pl[o] < 1e-12f ? 1e-12f : pl[o];
+                        loss = ssub(loss, smul(tc[o], logf(q)));
+                    }
+                    if (pl[o] > pl[bp]) bp = o;
+                    if (tc[o] > tc[btg]) btg = o;
+                }
+                loss_acc = __dadd_rn(loss_acc, (double)loss);
+                correct_acc += bp == btg;
+            }
+            if (s + 3 < n) {
+                const long long kk = A.order ? (long long)A.order[s + 3] : kpre;
+                prefetch_row_k(A, kk, xrow(s + 3), trow(s + 3), tid, NB);
+                if (++kpre == A.n) kpre = 0;
+            }
+            cp_async_commit();
+            cp_async_wait<1>();
+            named_sync(kBarBulk, NB);
+            bulk_pass(1, s);
+            __threadfence_block();
+            named_arrive(kBarPass, kClThreads);
+        }
+    }
+    if (critical && n > 0) named_sync(kBarPass, kClThreads);
+    cp_async_wait<0>();
+    __syncthreads();
+
+    if (n > 0) {
+        const int lp = (n - 1) & 1;
+        const float* xl = xrow(n - 1);
+        const float* al = abuf + lp * npc;
+        const float* dlast = d0b + lp * npc;
+        if constexpr (W0_SMEM) {
+            for (int e = tid; e < nloc * I; e += kClThreads) {
+                const int j = e / I, i = e - j * I;
+                A.W0[(size_t)i * H + h0 + j] = w0s[(size_t)j * Ip + i];
+            }
+        }
+        for (int e = tid; e < nloc * C; e += kClThreads) {
+            const int j = e / C, k = e - j * C;
+            A.W1[(size_t)h0 * C + e] = sgd_apply(w1s[e], neg_eta, dl[k], al[j]);
+        }
+        for (int j = tid; j < nloc; j += kClThreads) {
+            const float db = smul(neg_eta, dlast[j]);
+            A.b0[h0 + j] = sadd(b0s[j], db);
+            A.z0[h0 + j] = zcur[j];
+            A.a0[h0 + j] = al[j];
+            A.d0[h0 + j] = dlast[j];
+            A.db0[h0 + j] = db;
+            A.x1[h0 + j] = al[j];
+        }
+        if (critical && cta == 0 && lane < C) {
+            const float db = smul(neg_eta, dl[lane]);
+            A.b1[lane] = sadd(b1k, db);
+            A.z1[lane] = zl[lane];
+            A.a1[lane] = plb[lp * Cp + lane];
+            A.d1[lane] = dl[lane];
+            A.db1[lane] = db;
+        }
+        if (cta == 0)
+            for (int i = tid; i < I; i += kClThreads) A.x0[i] = xl[i];
+        if (stats) {
+            if (A.loss_sum) *A.loss_sum = loss_acc;
+            if (A.correct) *A.correct += correct_acc;
+        }
+    }
 }
 
 }  // namespace lane_b200

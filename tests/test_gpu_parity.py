@@ -295,12 +295,15 @@ def upload(dev, a, dtype=np.float32):
     (6, [3], 2, 5, 17, 0.2, None),           # H < 8 warps, C == 2
     (784, [128], 10, 64, 1, 0.01, 16),       # a single step
 ])
-@pytest.mark.parametrize("mode", ["cluster", "grid"])
+@pytest.mark.parametrize("mode", ["cluster", "grid", "stream"])
 def test_sgd_stream_fast_vs_oracle(lane, fast, monkeypatch, mode, F, H, C, n, steps, eta, ctas):
-    # cluster: one thread-block cluster, DSMEM exchange; grid: all SMs, L2 exchange
-    monkeypatch.setenv("LANE_B200_SGD_MODE", mode)
+    # cluster: one thread-block cluster, DSMEM exchange; grid: all SMs, L2
+    # exchange, W0 in shared memory; stream: grid with W0 streamed from HBM
+    monkeypatch.setenv("LANE_B200_SGD_MODE", "cluster" if mode == "cluster" else "grid")
+    if mode == "stream":
+        monkeypatch.setenv("LANE_B200_SGD_STREAM", "1")
     if ctas:
-        monkeypatch.setenv("LANE_B200_SGD_CTAS" if mode == "grid" else "LANE_B200_SGD_CLUSTER",
+        monkeypatch.setenv("LANE_B200_SGD_CLUSTER" if mode == "cluster" else "LANE_B200_SGD_CTAS",
                            str(min(ctas, 16)))
     X, T = po.synthetic_dataset(F, C, n, 9)
     order = np.random.default_rng(1).integers(0, n, steps).astype(np.uint32)
@@ -312,7 +315,7 @@ def test_sgd_stream_fast_vs_oracle(lane, fast, monkeypatch, mode, F, H, C, n, st
     before = fast.kernel_launches
     net.sgd_stream(Xd, Td, n, steps, eta, order_dev=Od, loss_dev=Ld)
     fast.sync()
-    if mode == "grid" or C <= 32:  # persistent plan: one kernel (+ G/DW materialisation)
+    if C <= 32:  # persistent plan: one kernel (+ G/DW materialisation)
         assert fast.kernel_launches - before <= 3
     loss = np.zeros(1, np.float64)
     fast.d2h(loss, Ld)

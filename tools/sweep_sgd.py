@@ -34,12 +34,15 @@ def main():
         dev.h2d(td, T)
         for mode in args.modes.split(","):
           for g in args.ctas.split(","):
-            for k in ("LANE_B200_SGD_CTAS", "LANE_B200_SGD_CLUSTER", "LANE_B200_SGD_MODE"):
+            for k in ("LANE_B200_SGD_CTAS", "LANE_B200_SGD_CLUSTER", "LANE_B200_SGD_MODE",
+                      "LANE_B200_SGD_STREAM"):
                 os.environ.pop(k, None)
             if mode != "auto":
-                os.environ["LANE_B200_SGD_MODE"] = mode
+                os.environ["LANE_B200_SGD_MODE"] = "grid" if mode == "stream" else mode
+            if mode == "stream":
+                os.environ["LANE_B200_SGD_STREAM"] = "1"
             if g != "0":
-                os.environ["LANE_B200_SGD_CTAS" if mode == "grid" else "LANE_B200_SGD_CLUSTER"] = g
+                os.environ["LANE_B200_SGD_CLUSTER" if mode == "cluster" else "LANE_B200_SGD_CTAS"] = g
             net = lane.build_network(F, [H], C, seed=42, device=dev)
             net.sgd_stream(xd, td, len(X), 2000, 0.01)
             dev.sync()
