@@ -282,6 +282,8 @@ struct SgdPlan {
     bool ok = false;
     bool cluster = false;  // single thread-block cluster, DSMEM exchange
     bool w0_smem = true;   // grid plan: W0 slices resident in shared memory
+    bool col4 = false;     // grid streamed plan: 128-bit column quads
+    int chunks = 1;        // grid streamed plan: K chunks per column group
     int G = 0, npc = 0, wpn = 1;
     size_t smem = 0;
 };
@@ -365,7 +367,8 @@ SgdPlan plan_persistent(lane_b200_net* net) {
     // otherwise streamed from HBM each sample
     int G = std::min(c->sm_count, H);
     if (const char* e = std::getenv("LANE_B200_SGD_CTAS")) G = std::max(1, std::min(std::atoi(e), std::min(c->sm_count, H)));
-    const int npc = (H + G - 1) / G;
+    int npc = (H + G - 1) / G;
+    if (H % 4 == 0) npc = (npc + 3) & ~3;  // 128-bit column quads in the streamed pass
     G = (H + npc - 1) / npc;
     const GrSmem Ls(I, C, npc, G, true), Lg(I, C, npc, G, false);
     const bool force_stream = std::getenv("LANE_B200_SGD_STREAM") != nullptr;
@@ -381,6 +384,11 @@ SgdPlan plan_persistent(lane_b200_net* net) {
     p.ok = true;
     p.G = G;
     p.npc = npc;
+    // streamed pass: enough (column group, K chunk) items for ~2 rounds of
+    // the 512 bulk threads
+    p.col4 = H % 4 == 0;
+    const int groups = p.col4 ? npc / 4 : npc;
+    p.chunks = std::max(1, std::min(kGrChunks, (2 * 32 * kClBulkWarps + groups / 2) / std::max(1, groups)));
     return p;
 }
 
@@ -436,6 +444,8 @@ void launch_persistent(lane_b200_net* net, const SgdPlan& P, const float* X, con
         LANE_CUDA(cudaMemsetAsync(trace, 0, trace_n * 8, c->stream));
     }
     A.trace = trace;
+    A.chunks = P.chunks;
+    A.col4 = P.col4 ? 1 : 0;
     if (P.cluster) {
         const SgdKernel kern = cluster_kernel(A.C);
         cluster_fits(kern, P.G, P.smem);  // sets the function attributes

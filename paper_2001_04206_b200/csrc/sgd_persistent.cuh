@@ -54,6 +54,8 @@ struct SgdArgs {
     unsigned long long* correct;
     int* error;  // set to 1 when an exchange times out (bug guard, never hangs)
     unsigned long long* trace;  // debug: per-phase clock64 of CTA 0 for the first kTraceSamples
+    int chunks;                 // grid/streamed: K chunks per column group (<= kGrChunks)
+    int col4;                   // grid/streamed: 128-bit column quads (H % 4 == 0, npc % 4 == 0)
 };
 
 constexpr int kTraceSamples = 64, kTracePhases = 12;
@@ -603,7 +605,7 @@ __global__ void __launch_bounds__(kClThreads, 1) k_sgd_cluster(SgdArgs A) {
 // 8 B per weight per sample, the algorithmic minimum -- HBM-bound).
 // ===========================================================================
 
-constexpr int kGrChunks = 4;  // K chunks per column in the streamed pass
+constexpr int kGrChunks = 8;  // max K chunks per column group in the streamed pass
 
 struct GrSmem {
     int I, C, Ip, Cp, npc, G;
@@ -670,7 +672,7 @@ __global__ void __launch_bounds__(kClThreads, 1) k_sgd_grid(SgdArgs A) {
     constexpr int NB = 32 * kClBulkWarps;  // bulk threads
     // reductions per neuron: smem mode -> 1 (a warp owns a whole row);
     // streamed mode -> kGrChunks K-chunks per column
-    constexpr int NR = W0_SMEM ? 1 : kGrChunks;
+    const int NR = W0_SMEM ? 1 : A.chunks;
 
     // ---------------- prologue ----------------
     for (int e = tid; e < 4 * Ip; e += kClThreads) xb0[e] = 0.0f;
@@ -742,29 +744,79 @@ __global__ void __launch_bounds__(kClThreads, 1) k_sgd_grid(SgdArgs A) {
                     for (int q = lane; q < Ip4; q += 32) wrow[q] = sgd_apply4(wrow[q], neg_eta, dj, xs4[q]);
                 }
             }
+        } else if (A.col4) {
+            // streamed, 128-bit: items (chunk c, column quad jq); consecutive
+            // threads -> consecutive 16-byte segments of one W0 row (coalesced);
+            // 8 rows x 16 B in flight per thread
+            const int quads = nloc >> 2, nch = A.chunks;
+            const int items = quads * nch;
+            for (int it = tid; it < items; it += NB) {
+                const int c = it / quads, jq = it - c * quads;
+                const int i0 = c * I / nch, i1 = (c + 1) * I / nch;
+                float4* col = reinterpret_cast<float4*>(A.W0 + (size_t)(h0 + 4 * jq));
+                const size_t H4 = (size_t)H >> 2;
+                float4 a0 = make_float4(0.f, 0.f, 0.f, 0.f), a1 = a0;
+                if (mode == 0) {
+                    const float* x0 = xrow(0);
+                    for (int i = i0; i < i1; ++i) {
+                        const float4 w = __ldcg(col + (size_t)i * H4);
+                        a0.x = fmaf(x0[i], w.x, a0.x); a0.y = fmaf(x0[i], w.y, a0.y);
+                        a0.z = fmaf(x0[i], w.z, a0.z); a0.w = fmaf(x0[i], w.w, a0.w);
+                        a1.x = fmaf(x2[i], w.x, a1.x); a1.y = fmaf(x2[i], w.y, a1.y);
+                        a1.z = fmaf(x2[i], w.z, a1.z); a1.w = fmaf(x2[i], w.w, a1.w);
+                    }
+                    float* r0 = red + (size_t)(4 * jq) * NR + c;
+                    float* r1 = red + (size_t)npc * NR + (size_t)(4 * jq) * NR + c;
+                    r0[0] = a0.x; r0[NR] = a0.y; r0[2 * NR] = a0.z; r0[3 * NR] = a0.w;
+                    r1[0] = a1.x; r1[NR] = a1.y; r1[2 * NR] = a1.z; r1[3 * NR] = a1.w;
+                } else {
+                    const float4 dq = *reinterpret_cast<const float4*>(d0 + 4 * jq);
+                    int i = i0;
+                    for (; i + 8 <= i1; i += 8) {
+                        float4 w[8];
+#pragma unroll
+                        for (int u = 0; u < 8; ++u) w[u] = __ldcg(col + (size_t)(i + u) * H4);
+#pragma unroll
+                        for (int u = 0; u < 8; ++u) {
+                            const float xv = xs[i + u], yv = x2[i + u];
+                            w[u].x = sgd_apply(w[u].x, neg_eta, dq.x, xv);
+                            w[u].y = sgd_apply(w[u].y, neg_eta, dq.y, xv);
+                            w[u].z = sgd_apply(w[u].z, neg_eta, dq.z, xv);
+                            w[u].w = sgd_apply(w[u].w, neg_eta, dq.w, xv);
+                            __stcg(col + (size_t)(i + u) * H4, w[u]);
+                            a0.x = fmaf(yv, w[u].x, a0.x); a0.y = fmaf(yv, w[u].y, a0.y);
+                            a0.z = fmaf(yv, w[u].z, a0.z); a0.w = fmaf(yv, w[u].w, a0.w);
+                        }
+                    }
+                    for (; i < i1; ++i) {
+                        float4 w = __ldcg(col + (size_t)i * H4);
+                        const float xv = xs[i], yv = x2[i];
+                        w.x = sgd_apply(w.x, neg_eta, dq.x, xv);
+                        w.y = sgd_apply(w.y, neg_eta, dq.y, xv);
+                        w.z = sgd_apply(w.z, neg_eta, dq.z, xv);
+                        w.w = sgd_apply(w.w, neg_eta, dq.w, xv);
+                        __stcg(col + (size_t)i * H4, w);
+                        a0.x = fmaf(yv, w.x, a0.x); a0.y = fmaf(yv, w.y, a0.y);
+                        a0.z = fmaf(yv, w.z, a0.z); a0.w = fmaf(yv, w.w, a0.w);
+                    }
+                    if (do_y) {
+                        float* r0 = red + (size_t)py * npc * NR + (size_t)(4 * jq) * NR + c;
+                        r0[0] = a0.x; r0[NR] = a0.y; r0[2 * NR] = a0.z; r0[3 * NR] = a0.w;
+                    }
+                }
+            }
         } else {
-            // streamed: items (chunk c, column j), consecutive threads ->
-            // consecutive columns of one W0 row (coalesced 128 B segments)
-            const int items = nloc * kGrChunks;
+            // streamed, scalar (H % 4 != 0): items (chunk c, column j)
+            const int nch = A.chunks;
+            const int items = nloc * nch;
             for (int it = tid; it < items; it += NB) {
                 const int c = it / nloc, jl = it - c * nloc;
-                const int i0 = c * I / kGrChunks, i1 = (c + 1) * I / kGrChunks;
+                const int i0 = c * I / nch, i1 = (c + 1) * I / nch;
                 float* col = A.W0 + (size_t)(h0 + jl);
                 float acc0 = 0.0f, acc1 = 0.0f;
                 if (mode == 0) {
                     const float* x0 = xrow(0);
-                    int i = i0;
-                    for (; i + 4 <= i1; i += 4) {
-                        float w[4];
-#pragma unroll
-                        for (int u = 0; u < 4; ++u) w[u] = __ldcg(col + (size_t)(i + u) * H);
-#pragma unroll
-                        for (int u = 0; u < 4; ++u) {
-                            acc0 = fmaf(x0[i + u], w[u], acc0);
-                            acc1 = fmaf(x2[i + u], w[u], acc1);
-                        }
-                    }
-                    for (; i < i1; ++i) {
+                    for (int i = i0; i < i1; ++i) {
                         const float w = __ldcg(col + (size_t)i * H);
                         acc0 = fmaf(x0[i], w, acc0);
                         acc1 = fmaf(x2[i], w, acc1);
