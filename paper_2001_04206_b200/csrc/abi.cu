@@ -370,25 +370,29 @@ SgdPlan plan_persistent(lane_b200_net* net) {
     int npc = (H + G - 1) / G;
     if (H % 4 == 0) npc = (npc + 3) & ~3;  // 128-bit column quads in the streamed pass
     G = (H + npc - 1) / npc;
-    const GrSmem Ls(I, C, npc, G, true), Lg(I, C, npc, G, false);
+    // streamed pass: enough (column group, K chunk) items for ~2 rounds of
+    // the 512 bulk threads, as far as shared memory allows
+    p.col4 = H % 4 == 0;
+    const int groups = p.col4 ? npc / 4 : npc;
+    int chunks = std::max(1, std::min(kGrChunks, (2 * 32 * kClBulkWarps + groups / 2) / std::max(1, groups)));
+    chunks = std::min(chunks, std::max(1, I / 8));
+    while (chunks > 1 && GrSmem(I, C, npc, G, false, chunks).total > c->max_smem_optin) --chunks;
+    const GrSmem Ls(I, C, npc, G, true), Lg(I, C, npc, G, false, chunks);
     const bool force_stream = std::getenv("LANE_B200_SGD_STREAM") != nullptr;
     if (!force_stream && Ls.total <= c->max_smem_optin) {
         p.w0_smem = true;
         p.smem = Ls.total;
+        p.chunks = 1;
     } else if (Lg.total <= c->max_smem_optin) {
         p.w0_smem = false;
         p.smem = Lg.total;
+        p.chunks = chunks;
     } else {
         return p;
     }
     p.ok = true;
     p.G = G;
     p.npc = npc;
-    // streamed pass: enough (column group, K chunk) items for ~2 rounds of
-    // the 512 bulk threads
-    p.col4 = H % 4 == 0;
-    const int groups = p.col4 ? npc / 4 : npc;
-    p.chunks = std::max(1, std::min(kGrChunks, (2 * 32 * kClBulkWarps + groups / 2) / std::max(1, groups)));
     return p;
 }
 

@@ -605,13 +605,13 @@ __global__ void __launch_bounds__(kClThreads, 1) k_sgd_cluster(SgdArgs A) {
 // 8 B per weight per sample, the algorithmic minimum -- HBM-bound).
 // ===========================================================================
 
-constexpr int kGrChunks = 8;  // max K chunks per column group in the streamed pass
+constexpr int kGrChunks = 32;  // max K chunks per column group in the streamed pass
 
 struct GrSmem {
     int I, C, Ip, Cp, npc, G;
     bool w0_smem;
     size_t w0s, w1s, xb, tb, b0s, abuf, zcur, d0, zl, pl, dl, gat, red, qred, total;
-    __host__ __device__ GrSmem(int I_, int C_, int npc_, int G_, bool w0_smem_)
+    __host__ __device__ GrSmem(int I_, int C_, int npc_, int G_, bool w0_smem_, int chunks = 1)
         : I(I_), C(C_), npc(npc_), G(G_), w0_smem(w0_smem_) {
         Ip = (I + 3) & ~3;
         Cp = (C + 3) & ~3;
@@ -633,7 +633,7 @@ struct GrSmem {
         pl = take(2 * (size_t)Cp);
         dl = take(Cp);
         gat = take((size_t)G * Cp);
-        red = take(2 * (size_t)npc * kGrChunks);  // [parity][j][chunk] (smem mode: chunk 0 only)
+        red = take(2 * (size_t)npc * (w0_smem ? 1 : chunks));  // [parity][j][chunk]
         qred = take(2 * 4);
         total = o * sizeof(float);
     }
@@ -642,7 +642,7 @@ struct GrSmem {
 template <int CT, bool W0_SMEM>
 __global__ void __launch_bounds__(kClThreads, 1) k_sgd_grid(SgdArgs A) {
     extern __shared__ __align__(16) float sm[];
-    const GrSmem L(A.I, A.C, A.npc, A.G, W0_SMEM);
+    const GrSmem L(A.I, A.C, A.npc, A.G, W0_SMEM, A.chunks);
     float* w0s = sm + L.w0s;
     float* w1s = sm + L.w1s;
     float* b0s = sm + L.b0s;
