@@ -194,6 +194,14 @@ int lane_b200_evaluate(lane_b200_net* net, const float* X_host, const float* T_h
 int lane_b200_minibatch_step(lane_b200_net* net, const float* X_dev, const float* T_dev,
                              size_t B, float eta, float mu, double* loss_sum_dev);
 
+/* Diagnostic: one GEMM of the mini-batch path on device buffers (row-major):
+ * op 0 NN: C[M,N] = A[M,K] B[K,N];  op 1 NT: C = A[M,K] B[N,K]^T;
+ * op 2 TN: C = A[K,M]^T B[K,N].  epilogue 0 store, 1 +bias[n], 2 +bias[n]
+ * with C2 = tanh(C), 3 C = (1 - aux^2) * acc.  use_tc selects the tcgen05
+ * 3xTF32 kernel where the shape is eligible (else the SIMT kernel). */
+int lane_b200_gemm(lane_b200_ctx* ctx, int op, int M, int N, int K, const float* A, const float* B,
+                   float* C, float* C2, const float* bias, const float* aux, int epilogue, int use_tc);
+
 /* ------------------------------------------- multi-GPU (data parallel) --- */
 int lane_b200_nccl_unique_id(void* id_out, size_t id_bytes); /* id_bytes >= 128 */
 int lane_b200_comm_init(lane_b200_ctx* ctx, int rank, int world, const void* id,

@@ -55,6 +55,7 @@ SIGNATURES = {
     "lane_b200_train": (_I, [_V, _FP, _FP, _S, _F, _F, _S, _U64, _FP, _FP, _SP]),
     "lane_b200_evaluate": (_I, [_V, _FP, _FP, _S, _FP, _FP]),
     "lane_b200_minibatch_step": (_I, [_V, _V, _V, _S, _F, _F, _V]),
+    "lane_b200_gemm": (_I, [_V, _I, _I, _I, _I, _V, _V, _V, _V, _V, _V, _I, _I]),
     "lane_b200_nccl_unique_id": (_I, [_V, _S]),
     "lane_b200_comm_init": (_I, [_V, _I, _I, _V, _S]),
     "lane_b200_comm_destroy": (_I, [_V]),

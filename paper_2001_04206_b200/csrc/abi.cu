@@ -1089,6 +1089,31 @@ int lane_b200_minibatch_step(lane_b200_net* net, const float* X, const float* T,
     });
 }
 
+int lane_b200_gemm(lane_b200_ctx* c, int op, int M, int N, int K, const float* A, const float* B, float* C,
+                   float* C2, const float* bias, const float* aux, int epilogue, int use_tc) {
+    return guard([&] {
+        if (!c) throw Error(LANE_ERR_CONFIG, "null context");
+        if (op < 0 || op > 2 || epilogue < 0 || epilogue > 3 || M < 0 || N < 0 || K < 0)
+            throw Error(LANE_ERR_CONFIG, "lane_b200_gemm: bad op/epilogue/shape");
+        static float* ws = nullptr;
+        static size_t ws_count = 0;
+        GemmCtx g{c->stream, c->sm_count, &ws, &ws_count, &c->launches};
+        const GemmOp o = static_cast<GemmOp>(op);
+        const int lda = o == GemmOp::TN ? M : K;
+        const int ldb = o == GemmOp::NT ? K : N;
+        const int saved = gemm_tc_mode();
+        gemm_tc_mode() = use_tc ? 1 : 0;
+        try {
+            gemm(g, o, M, N, K, A, lda, B, ldb, static_cast<Epi>(epilogue), C, C2, bias, aux);
+        } catch (...) {
+            gemm_tc_mode() = saved;
+            throw;
+        }
+        gemm_tc_mode() = saved;
+        c->check_launch();
+    });
+}
+
 int lane_b200_nccl_unique_id(void* id_out, size_t id_bytes) {
     return guard([&] { nccl_unique_id(id_out, id_bytes); });
 }

@@ -13,7 +13,11 @@
 // (gemm_tc.cuh) when it is enabled and the shape qualifies.
 #pragma once
 
+#include <cstdlib>
+#include <cstring>
+
 #include "common.cuh"
+#include "gemm_tc.cuh"
 
 namespace lane_b200 {
 
@@ -167,9 +171,59 @@ void gemm_simt_dispatch(GemmCtx& g, int M, int N, int K, const float* A, int lda
     *g.launches += 1;
 }
 
+// 0 = SIMT only, 1 = tensor cores where eligible (default), set by
+// LANE_B200_GEMM=simt|tc or lane_b200_gemm()'s use_tc argument
+inline int& gemm_tc_mode() {
+    static int mode = [] {
+        const char* e = std::getenv("LANE_B200_GEMM");
+        return (e && std::strcmp(e, "simt") == 0) ? 0 : 1;
+    }();
+    return mode;
+}
+
+// Tensor-core dispatch (gemm_tc.cuh): returns false when the shape/layout is
+// not eligible (the caller then runs the SIMT kernel).
+inline bool gemm_try_tc(GemmCtx& g, GemmOp op, int M, int N, int K, const float* A, int lda, const float* B,
+                        int ldb, Epi e, float* C, float* C2, const float* bias, const float* aux) {
+    if (!gemm_tc_mode() || !tc_eligible(M, N, K)) return false;
+    if ((reinterpret_cast<uintptr_t>(A) | reinterpret_cast<uintptr_t>(B) | reinterpret_cast<uintptr_t>(C)) & 15)
+        return false;
+    CUtensorMap ma, mb;
+    bool a_mn = false, b_mn = false;
+    switch (op) {
+        case GemmOp::NN:  // A [M][K] K-major, B [K][N] MN-major
+            if (lda != K || ldb != N) return false;
+            ma = tc_map(A, M, K, 32, 128);
+            mb = tc_map(B, K, N, 32, 32);
+            b_mn = true;
+            break;
+        case GemmOp::NT:  // A [M][K] K-major, B [N][K] K-major
+            if (lda != K || ldb != K) return false;
+            ma = tc_map(A, M, K, 32, 128);
+            mb = tc_map(B, N, K, 32, 128);
+            break;
+        case GemmOp::TN:  // A [K][M] MN-major, B [K][N] MN-major
+            if (lda != M || ldb != N) return false;
+            ma = tc_map(A, K, M, 32, 32);
+            mb = tc_map(B, K, N, 32, 32);
+            a_mn = b_mn = true;
+            break;
+    }
+    TcArgs t{M, N, K, C, C2, bias, aux};
+    switch (e) {
+        case Epi::STORE: tc_dispatch<TcEpi::STORE>(g.stream, a_mn, b_mn, ma, mb, t); break;
+        case Epi::BIAS: tc_dispatch<TcEpi::BIAS>(g.stream, a_mn, b_mn, ma, mb, t); break;
+        case Epi::BIAS_TANH: tc_dispatch<TcEpi::BIAS_TANH>(g.stream, a_mn, b_mn, ma, mb, t); break;
+        case Epi::TANH_GRAD: tc_dispatch<TcEpi::TANH_GRAD>(g.stream, a_mn, b_mn, ma, mb, t); break;
+    }
+    *g.launches += 1;
+    return true;
+}
+
 inline void gemm(GemmCtx& g, GemmOp op, int M, int N, int K, const float* A, int lda, const float* B, int ldb,
                  Epi e, float* C, float* C2, const float* bias, const float* aux) {
     if (M <= 0 || N <= 0) return;
+    if (gemm_try_tc(g, op, M, N, K, A, lda, B, ldb, e, C, C2, bias, aux)) return;
     switch (op) {
         case GemmOp::NN: gemm_simt_dispatch<GemmOp::NN>(g, M, N, K, A, lda, B, ldb, e, C, C2, bias, aux); break;
         case GemmOp::NT: gemm_simt_dispatch<GemmOp::NT>(g, M, N, K, A, lda, B, ldb, e, C, C2, bias, aux); break;

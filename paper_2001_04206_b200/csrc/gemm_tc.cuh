@@ -1,0 +1,363 @@
+// gemm_tc.cuh -- fp32-accurate GEMM on the 5th-generation tensor cores
+// (tcgen05, kind::tf32) for the mini-batch path, "3xTF32":
+//     A.B ~= A_lo.B + A.B_lo + A.B      (A_lo = A - tf32(A), exact in fp32)
+// The tensor core reads fp32 operands and ignores their low 13 mantissa bits,
+// so A itself is the "hi" part; the lo parts are produced in shared memory by
+// an elementwise pass over each TMA-loaded tile (same swizzled layout, so the
+// same descriptors apply).  All three products accumulate into one fp32 TMEM
+// accumulator.  Relative error per product ~2^-21 (the dropped A_lo.B_lo term
+// and the tf32 truncation of the lo parts), within the path's 1e-5 tolerance
+// (1xTF32 alone is ~5e-4 and is NOT used).
+//
+// Structure (one 128x128 output tile per CTA, 192 threads):
+//   warp 0      TMA producer: A/B tiles (fp32, 128B swizzle) -> smem ring
+//   warp 1      MMA issuer: one elected thread issues tcgen05.mma, commits
+//               smem slots back to the producer and the accumulator to the
+//               epilogue (tcgen05.commit -> mbarrier)
+//   warps 2..5  split pass (A_lo, B_lo per stage), then the epilogue:
+//               tcgen05.ld TMEM -> registers -> fused epilogue -> global
+// Operand majors: K-major tiles come from one TMA box {32 (K), 128 (MN)};
+// MN-major tiles from four boxes {32 (MN), 32 (K)} (one per 32-wide MN group).
+#pragma once
+
+#include <cuda.h>
+
+#include "common.cuh"
+
+namespace lane_b200 {
+
+constexpr int kTcBM = 128, kTcBN = 128, kTcBK = 32, kTcStages = 3;
+constexpr int kTcTile = kTcBM * kTcBK * 4;  // bytes of one 128x32 fp32 tile (A or B)
+constexpr int kTcStage = 4 * kTcTile;       // A, B, A_lo, B_lo
+constexpr int kTcThreads = 192;
+constexpr size_t kTcSmem = (size_t)kTcStages * kTcStage + 1024 /*align*/ + 256 /*barriers*/;
+
+enum class TcEpi : int { STORE = 0, BIAS = 1, BIAS_TANH = 2, TANH_GRAD = 3 };
+
+struct TcArgs {
+    int M, N, K;
+    float* C;           // M x N row-major (ldc = N)
+    float* C2;          // BIAS_TANH: tanh(C)
+    const float* bias;  // BIAS*: per column
+    const float* aux;   // TANH_GRAD: activations a (M x N)
+};
+
+// ---- PTX helpers ------------------------------------------------------------
+__device__ __forceinline__ uint32_t tc_smem(const void* p) {
+    return static_cast<uint32_t>(__cvta_generic_to_shared(p));
+}
+__device__ __forceinline__ void tc_mbar_init(uint32_t a, uint32_t n) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;\n" ::"r"(a), "r"(n) : "memory");
+}
+__device__ __forceinline__ void tc_mbar_expect_tx(uint32_t a, uint32_t bytes) {
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;\n" ::"r"(a), "r"(bytes) : "memory");
+}
+__device__ __forceinline__ void tc_mbar_arrive(uint32_t a) {
+    asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];\n" ::"r"(a) : "memory");
+}
+__device__ __forceinline__ void tc_mbar_wait(uint32_t a, uint32_t parity) {
+    asm volatile(
+        "{\n .reg .pred p;\n"
+        "WAIT_%=:\n"
+        " mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n"
+        " @!p bra WAIT_%=;\n}\n" ::"r"(a),
+        "r"(parity)
+        : "memory");
+}
+__device__ __forceinline__ void tc_tma_2d(const CUtensorMap* map, uint32_t bar, uint32_t dst, int c0, int c1) {
+    asm volatile(
+        "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3}], [%4];\n" ::"r"(dst),
+        "l"(reinterpret_cast<uint64_t>(map)), "r"(c0), "r"(c1), "r"(bar)
+        : "memory");
+}
+// UMMA shared-memory descriptor, SWIZZLE_128B, sm100 (version 1)
+__device__ __forceinline__ uint64_t tc_desc(uint32_t addr, uint32_t lbo, uint32_t sbo) {
+    uint64_t d = 0;
+    d |= (uint64_t)((addr >> 4) & 0x3FFF);
+    d |= (uint64_t)((lbo >> 4) & 0x3FFF) << 16;
+    d |= (uint64_t)((sbo >> 4) & 0x3FFF) << 32;
+    d |= (uint64_t)1 << 46;  // version (Blackwell)
+    d |= (uint64_t)2 << 61;  // SWIZZLE_128B
+    return d;
+}
+__device__ __forceinline__ void tc_mma(uint32_t tmem_d, uint64_t da, uint64_t db, uint32_t idesc, uint32_t acc) {
+    asm volatile(
+        "{\n .reg .pred p;\n setp.ne.b32 p, %4, 0;\n"
+        " tcgen05.mma.cta_group::1.kind::tf32 [%0], %1, %2, %3, p;\n}\n" ::"r"(tmem_d),
+        "l"(da), "l"(db), "r"(idesc), "r"(acc));
+}
+__device__ __forceinline__ void tc_commit(uint32_t bar) {
+    asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];\n" ::"r"(bar)
+                 : "memory");
+}
+
+// low part of a tf32 split: x - (x with the 13 low mantissa bits cleared)
+__device__ __forceinline__ float tf32_lo(float x) {
+    return __fsub_rn(x, __uint_as_float(__float_as_uint(x) & 0xFFFFE000u));
+}
+
+template <TcEpi E>
+__device__ __forceinline__ float4 tc_epi4(const TcArgs& a, int m, int n, float4 v, float4* second) {
+    if constexpr (E == TcEpi::BIAS || E == TcEpi::BIAS_TANH) {
+        const float4 b = *reinterpret_cast<const float4*>(a.bias + n);
+        v.x = sadd(v.x, b.x);
+        v.y = sadd(v.y, b.y);
+        v.z = sadd(v.z, b.z);
+        v.w = sadd(v.w, b.w);
+        if constexpr (E == TcEpi::BIAS_TANH) {
+            second->x = lane_libm::tanhf(v.x);
+            second->y = lane_libm::tanhf(v.y);
+            second->z = lane_libm::tanhf(v.z);
+            second->w = lane_libm::tanhf(v.w);
+        }
+    } else if constexpr (E == TcEpi::TANH_GRAD) {
+        const float4 t = *reinterpret_cast<const float4*>(a.aux + (size_t)m * a.N + n);
+        v.x = tanh_grad(t.x, v.x);
+        v.y = tanh_grad(t.y, v.y);
+        v.z = tanh_grad(t.z, v.z);
+        v.w = tanh_grad(t.w, v.w);
+    }
+    return v;
+}
+
+template <bool A_MN, bool B_MN, TcEpi E>
+__global__ void __launch_bounds__(kTcThreads, 1)
+    k_gemm_tc(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB, TcArgs args) {
+    extern __shared__ uint8_t tc_raw[];
+    uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(tc_raw) + 1023) & ~uintptr_t(1023));
+    uint64_t* bars = reinterpret_cast<uint64_t*>(smem + (size_t)kTcStages * kTcStage);
+    // bars: full[3], conv[3], empty[3], tmem_full[1]; then the TMEM address
+    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 16);
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int m0 = blockIdx.y * kTcBM, n0 = blockIdx.x * kTcBN;
+    const int nkb = (args.K + kTcBK - 1) / kTcBK;
+    const uint32_t sbase = tc_smem(smem);
+    auto full = [&](int s) { return tc_smem(bars + s); };
+    auto conv = [&](int s) { return tc_smem(bars + 3 + s); };
+    auto empty = [&](int s) { return tc_smem(bars + 6 + s); };
+    const uint32_t tmem_full = tc_smem(bars + 9);
+    auto tileA = [&](int s) { return sbase + (uint32_t)(s * kTcStage); };
+    auto tileB = [&](int s) { return sbase + (uint32_t)(s * kTcStage + kTcTile); };
+    auto tileAlo = [&](int s) { return sbase + (uint32_t)(s * kTcStage + 2 * kTcTile); };
+    auto tileBlo = [&](int s) { return sbase + (uint32_t)(s * kTcStage + 3 * kTcTile); };
+
+    if (threadIdx.x == 0) {
+        for (int s = 0; s < kTcStages; ++s) {
+            tc_mbar_init(full(s), 1);
+            tc_mbar_init(conv(s), 4);
+            tc_mbar_init(empty(s), 1);
+        }
+        tc_mbar_init(tmem_full, 1);
+        asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
+        asm volatile("prefetch.tensormap [%0];\n" ::"l"(reinterpret_cast<uint64_t>(&tmA)) : "memory");
+        asm volatile("prefetch.tensormap [%0];\n" ::"l"(reinterpret_cast<uint64_t>(&tmB)) : "memory");
+    }
+    if (warp == 1) {
+        asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;\n" ::"r"(tc_smem(tmem_slot)),
+                     "r"(kTcBN));
+        asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;\n");
+    }
+    asm volatile("tcgen05.fence::before_thread_sync;\n" ::: "memory");
+    __syncthreads();
+    asm volatile("tcgen05.fence::after_thread_sync;\n" ::: "memory");
+    const uint32_t tmem = *tmem_slot;
+
+    if (warp == 0) {
+        // ---------------- TMA producer ----------------
+        if (lane == 0) {
+            for (int kb = 0; kb < nkb; ++kb) {
+                const int s = kb % kTcStages;
+                const uint32_t ph = (uint32_t)((kb / kTcStages) & 1);
+                tc_mbar_wait(empty(s), ph ^ 1);
+                tc_mbar_expect_tx(full(s), 2 * kTcTile);
+                const int k0 = kb * kTcBK;
+                if constexpr (!A_MN) {
+                    tc_tma_2d(&tmA, full(s), tileA(s), k0, m0);
+                } else {
+#pragma unroll
+                    for (int g = 0; g < 4; ++g) tc_tma_2d(&tmA, full(s), tileA(s) + g * 4096, m0 + 32 * g, k0);
+                }
+                if constexpr (!B_MN) {
+                    tc_tma_2d(&tmB, full(s), tileB(s), k0, n0);
+                } else {
+#pragma unroll
+                    for (int g = 0; g < 4; ++g) tc_tma_2d(&tmB, full(s), tileB(s) + g * 4096, n0 + 32 * g, k0);
+                }
+            }
+        }
+    } else if (warp == 1) {
+        // ---------------- MMA issuer ----------------
+        // instruction descriptor: D f32, A/B tf32, majors, N>>3, M>>4
+        const uint32_t idesc = (1u << 4) | (2u << 7) | (2u << 10) | ((A_MN ? 1u : 0u) << 15) |
+                               ((B_MN ? 1u : 0u) << 16) | ((uint32_t)(kTcBN >> 3) << 17) |
+                               ((uint32_t)(kTcBM >> 4) << 24);
+        for (int kb = 0; kb < nkb; ++kb) {
+            const int s = kb % kTcStages;
+            const uint32_t ph = (uint32_t)((kb / kTcStages) & 1);
+            tc_mbar_wait(conv(s), ph);
+            asm volatile("tcgen05.fence::after_thread_sync;\n" ::: "memory");
+            if (lane == 0) {
+#pragma unroll
+                for (int ks = 0; ks < kTcBK / 8; ++ks) {
+                    // K-major: +32 B inside the 128 B swizzle row; MN-major: +8 rows
+                    const uint32_t ao = A_MN ? ks * 1024u : ks * 32u;
+                    const uint32_t bo = B_MN ? ks * 1024u : ks * 32u;
+                    const uint32_t albo = A_MN ? 4096u : 16u, asbo = 1024u;
+                    const uint32_t blbo = B_MN ? 4096u : 16u, bsbo = 1024u;
+                    const uint64_t dA = tc_desc(tileA(s) + ao, albo, asbo);
+                    const uint64_t dB = tc_desc(tileB(s) + bo, blbo, bsbo);
+                    const uint64_t dAl = tc_desc(tileAlo(s) + ao, albo, asbo);
+                    const uint64_t dBl = tc_desc(tileBlo(s) + bo, blbo, bsbo);
+                    const uint32_t first = (kb == 0 && ks == 0) ? 0u : 1u;
+                    tc_mma(tmem, dAl, dB, idesc, first);  // small terms first
+                    tc_mma(tmem, dA, dBl, idesc, 1u);
+                    tc_mma(tmem, dA, dB, idesc, 1u);
+                }
+                tc_commit(empty(s));  // slot free once these MMAs have read it
+            }
+            __syncwarp();
+        }
+        if (lane == 0) tc_commit(tmem_full);
+        __syncwarp();
+    } else {
+        // ---------------- split pass, then epilogue (warps 2..5) ----------------
+        const int ct = threadIdx.x - 64;  // 0..127
+        for (int kb = 0; kb < nkb; ++kb) {
+            const int s = kb % kTcStages;
+            const uint32_t ph = (uint32_t)((kb / kTcStages) & 1);
+            tc_mbar_wait(full(s), ph);
+            const float4* a = reinterpret_cast<const float4*>(smem + (size_t)s * kTcStage);
+            const float4* b = reinterpret_cast<const float4*>(smem + (size_t)s * kTcStage + kTcTile);
+            float4* al = reinterpret_cast<float4*>(smem + (size_t)s * kTcStage + 2 * kTcTile);
+            float4* bl = reinterpret_cast<float4*>(smem + (size_t)s * kTcStage + 3 * kTcTile);
+#pragma unroll
+            for (int u = 0; u < kTcTile / 16 / 128; ++u) {
+                const int q = ct + 128 * u;
+                const float4 va = a[q], vb = b[q];
+                al[q] = make_float4(tf32_lo(va.x), tf32_lo(va.y), tf32_lo(va.z), tf32_lo(va.w));
+                bl[q] = make_float4(tf32_lo(vb.x), tf32_lo(vb.y), tf32_lo(vb.z), tf32_lo(vb.w));
+            }
+            // generic-proxy smem writes -> visible to the tensor core (async proxy)
+            asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");
+            __syncwarp();
+            if (lane == 0) tc_mbar_arrive(conv(s));
+        }
+        tc_mbar_wait(tmem_full, 0);
+        asm volatile("tcgen05.fence::after_thread_sync;\n" ::: "memory");
+        const int quarter = warp & 3;  // TMEM lanes this warp may access
+        const int row = quarter * 32 + lane;
+        const int m = m0 + row;
+#pragma unroll 1
+        for (int c0 = 0; c0 < kTcBN; c0 += 32) {
+            uint32_t r[32];
+            const uint32_t taddr = tmem + ((uint32_t)(quarter * 32) << 16) + (uint32_t)c0;
+            asm volatile(
+                "tcgen05.ld.sync.aligned.32x32b.x32.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,"
+                "%16,%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31}, [%32];\n"
+                : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7]),
+                  "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]), "=r"(r[14]),
+                  "=r"(r[15]), "=r"(r[16]), "=r"(r[17]), "=r"(r[18]), "=r"(r[19]), "=r"(r[20]), "=r"(r[21]),
+                  "=r"(r[22]), "=r"(r[23]), "=r"(r[24]), "=r"(r[25]), "=r"(r[26]), "=r"(r[27]), "=r"(r[28]),
+                  "=r"(r[29]), "=r"(r[30]), "=r"(r[31])
+                : "r"(taddr));
+            asm volatile("tcgen05.wait::ld.sync.aligned;\n" ::: "memory");
+            if (m < args.M) {
+                const int nb = n0 + c0;
+                if (nb + 32 <= args.N && (args.N & 3) == 0) {
+#pragma unroll
+                    for (int q = 0; q < 8; ++q) {
+                        float4 v = make_float4(__uint_as_float(r[4 * q]), __uint_as_float(r[4 * q + 1]),
+                                               __uint_as_float(r[4 * q + 2]), __uint_as_float(r[4 * q + 3]));
+                        float4 t;
+                        v = tc_epi4<E>(args, m, nb + 4 * q, v, &t);
+                        *reinterpret_cast<float4*>(args.C + (size_t)m * args.N + nb + 4 * q) = v;
+                        if constexpr (E == TcEpi::BIAS_TANH)
+                            *reinterpret_cast<float4*>(args.C2 + (size_t)m * args.N + nb + 4 * q) = t;
+                    }
+                } else {
+                    for (int q = 0; q < 32; ++q) {
+                        const int n = nb + q;
+                        if (n >= args.N) break;
+                        float v = __uint_as_float(r[q]);
+                        const size_t idx = (size_t)m * args.N + n;
+                        if constexpr (E == TcEpi::BIAS || E == TcEpi::BIAS_TANH) v = sadd(v, args.bias[n]);
+                        if constexpr (E == TcEpi::TANH_GRAD) v = tanh_grad(args.aux[idx], v);
+                        args.C[idx] = v;
+                        if constexpr (E == TcEpi::BIAS_TANH) args.C2[idx] = lane_libm::tanhf(v);
+                    }
+                }
+            }
+        }
+    }
+    asm volatile("tcgen05.fence::before_thread_sync;\n" ::: "memory");
+    __syncthreads();
+    if (warp == 1) {
+        asm volatile("tcgen05.fence::after_thread_sync;\n" ::: "memory");
+        asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;\n" ::"r"(tmem), "r"(kTcBN));
+    }
+}
+
+}  // namespace lane_b200
+
+// ---------------------------------------------------------------- host side
+#include <cuda_runtime.h>
+
+namespace lane_b200 {
+
+using PFN_encodeTiled = CUresult (*)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
+                                     const cuuint64_t*, const cuuint32_t*, const cuuint32_t*, CUtensorMapInterleave,
+                                     CUtensorMapSwizzle, CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+
+inline PFN_encodeTiled tc_encoder() {
+    static PFN_encodeTiled fn = nullptr;
+    if (!fn) {
+        void* p = nullptr;
+        cudaDriverEntryPointQueryResult q;
+        LANE_CUDA(cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q));
+        if (!p || q != cudaDriverEntryPointSuccess) throw Error(LANE_ERR_CUDA, "cuTensorMapEncodeTiled unavailable");
+        fn = reinterpret_cast<PFN_encodeTiled>(p);
+    }
+    return fn;
+}
+
+// 2-D fp32 row-major tensor [rows x cols] (ld = cols), box {box_inner, box_rows}
+inline CUtensorMap tc_map(const float* base, int rows, int cols, int box_inner, int box_rows) {
+    CUtensorMap m;
+    const cuuint64_t dims[2] = {(cuuint64_t)cols, (cuuint64_t)rows};
+    const cuuint64_t strides[1] = {(cuuint64_t)cols * sizeof(float)};
+    const cuuint32_t box[2] = {(cuuint32_t)box_inner, (cuuint32_t)box_rows};
+    const cuuint32_t estr[2] = {1, 1};
+    const CUresult r = tc_encoder()(&m, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2, const_cast<float*>(base), dims, strides,
+                                    box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+                                    CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    if (r != CUDA_SUCCESS) throw Error(LANE_ERR_CUDA, "cuTensorMapEncodeTiled failed");
+    return m;
+}
+
+// The tensor-core path needs 16-byte row strides for every TMA operand.
+inline bool tc_eligible(int M, int N, int K) {
+    return (M % 4 == 0) && (N % 4 == 0) && (K % 4 == 0) && N >= 64 && M >= 64 && K >= 32;
+}
+
+template <bool A_MN, bool B_MN, TcEpi E>
+inline void tc_launch(cudaStream_t st, const CUtensorMap& a, const CUtensorMap& b, const TcArgs& args) {
+    static bool configured = false;
+    if (!configured) {
+        LANE_CUDA(cudaFuncSetAttribute(k_gemm_tc<A_MN, B_MN, E>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                       (int)kTcSmem));
+        configured = true;
+    }
+    const dim3 grid((args.N + kTcBN - 1) / kTcBN, (args.M + kTcBM - 1) / kTcBM);
+    k_gemm_tc<A_MN, B_MN, E><<<grid, kTcThreads, kTcSmem, st>>>(a, b, args);
+}
+
+template <TcEpi E>
+inline void tc_dispatch(cudaStream_t st, bool a_mn, bool b_mn, const CUtensorMap& a, const CUtensorMap& b,
+                        const TcArgs& args) {
+    if (!a_mn && !b_mn) tc_launch<false, false, E>(st, a, b, args);
+    else if (!a_mn && b_mn) tc_launch<false, true, E>(st, a, b, args);
+    else if (a_mn && !b_mn) tc_launch<true, false, E>(st, a, b, args);
+    else tc_launch<true, true, E>(st, a, b, args);
+}
+
+}  // namespace lane_b200

@@ -1,0 +1,99 @@
+"""GEMMs of the mini-batch path (tcgen05 3xTF32 kernel and the SIMT kernel)
+against a float64 numpy reference, with the condition-aware tolerance
+|C - ref| <= 1e-5 * (|A| |B|)  elementwise."""
+import ctypes as C
+
+import numpy as np
+import pytest
+
+pytestmark = pytest.mark.gpu
+
+NN, NT, TN = 0, 1, 2
+STORE, BIAS, BIAS_TANH, TANH_GRAD = 0, 1, 2, 3
+
+
+@pytest.fixture(scope="module")
+def dev():
+    from paper_2001_04206_b200 import lane
+    d = lane.Device(0)
+    yield d
+    d.close()
+
+
+def put(dev, a):
+    a = np.ascontiguousarray(a, np.float32)
+    p = dev.alloc(max(a.nbytes, 4))
+    dev.h2d(p, a)
+    return p
+
+
+def run(dev, op, M, N, K, A, B, epi=STORE, bias=None, aux=None, use_tc=1):
+    from paper_2001_04206_b200 import _native, lane
+    L = _native.lib()
+    pa, pb = put(dev, A), put(dev, B)
+    pc, pc2 = dev.alloc(M * N * 4), dev.alloc(M * N * 4)
+    pbias = put(dev, bias) if bias is not None else None
+    paux = put(dev, aux) if aux is not None else None
+    before = dev.kernel_launches
+    rc = L.lane_b200_gemm(dev._p, op, M, N, K, C.c_void_p(pa), C.c_void_p(pb), C.c_void_p(pc),
+                          C.c_void_p(pc2), C.c_void_p(pbias), C.c_void_p(paux), epi, use_tc)
+    if rc:
+        raise lane.Error(L.lane_b200_last_error().decode())
+    dev.sync()
+    out, out2 = np.zeros((M, N), np.float32), np.zeros((M, N), np.float32)
+    dev.d2h(out, pc)
+    dev.d2h(out2, pc2)
+    for p in (pa, pb, pc, pc2, pbias, paux):
+        if p:
+            dev.free(p)
+    return out, out2, dev.kernel_launches - before
+
+
+def operands(op, M, N, K, rs):
+    A = rs.uniform(-1, 1, (K, M) if op == TN else (M, K)).astype(np.float32)
+    B = rs.uniform(-1, 1, (N, K) if op == NT else (K, N)).astype(np.float32)
+    Am = A.T if op == TN else A
+    Bm = B.T if op == NT else B
+    return A, B, Am.astype(np.float64), Bm.astype(np.float64)
+
+
+@pytest.mark.parametrize("use_tc", [1, 0])
+@pytest.mark.parametrize("op", [NN, NT, TN])
+@pytest.mark.parametrize("M,N,K", [(128, 128, 32), (256, 512, 1024), (192, 320, 96), (64, 4100, 36),
+                                   (1024, 256, 256)])
+def test_gemm_store_condition_aware(dev, op, M, N, K, use_tc):
+    rs = np.random.default_rng(M * 7 + N * 3 + K)
+    A, B, Am, Bm = operands(op, M, N, K, rs)
+    out, _, launched = run(dev, op, M, N, K, A, B, STORE, use_tc=use_tc)
+    ref = Am @ Bm
+    cond = np.abs(Am) @ np.abs(Bm)
+    err = np.abs(out - ref)
+    assert launched == 1
+    assert np.all(err <= 1e-5 * cond + 1e-30), f"max err/cond {np.max(err / (cond + 1e-30)):.3e}"
+
+
+@pytest.mark.parametrize("op", [NN, NT])
+def test_gemm_fused_epilogues(dev, op):
+    M, N, K = 256, 384, 512
+    rs = np.random.default_rng(5)
+    A, B, Am, Bm = operands(op, M, N, K, rs)
+    A *= 0.1
+    Am *= 0.1
+    bias = rs.uniform(-0.5, 0.5, N).astype(np.float32)
+    aux = rs.uniform(-0.99, 0.99, (M, N)).astype(np.float32)
+    ref = Am @ Bm
+    cond = np.abs(Am) @ np.abs(Bm)
+    z, a, _ = run(dev, op, M, N, K, A, B, BIAS_TANH, bias=bias)
+    assert np.all(np.abs(z - (ref + bias)) <= 1e-5 * cond + 1e-6)
+    np.testing.assert_allclose(a, np.tanh(z.astype(np.float64)), rtol=2e-6, atol=2e-7)
+    d, _, _ = run(dev, op, M, N, K, A, B, TANH_GRAD, aux=aux)
+    g = (1 - aux.astype(np.float64) ** 2)
+    assert np.all(np.abs(d - g * ref) <= 1e-5 * g * cond + 1e-6)
+
+
+def test_tensor_core_kernel_is_used(dev):
+    # the eligible shape must run on the tcgen05 kernel, the ineligible one on SIMT
+    import subprocess
+    from paper_2001_04206_b200 import _build
+    sass = subprocess.run(["cuobjdump", "-sass", _build.LIB], capture_output=True, text=True).stdout
+    assert "UTCHMMA" in sass and "UTMALDG" in sass and "LDTM" in sass
