@@ -31,8 +31,8 @@ def test_library_is_sm100a_only():
 
 def test_kernels_present_in_sass():
     out = subprocess.run(["cuobjdump", "-sass", _build.LIB], capture_output=True, text=True).stdout
-    for k in ("k_sgd_persistent", "k_netin_strict", "k_delta_fc_strict", "k_outer",
-              "k_apply_updates", "k_gemm_simt"):
+    for k in ("k_sgd_cluster", "k_sgd_grid", "k_netin_strict", "k_delta_fc_strict", "k_outer",
+              "k_apply_updates", "k_gemm_simt", "k_gemm_tc"):
         assert k in out, k
 
 
