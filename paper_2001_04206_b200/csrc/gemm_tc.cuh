@@ -70,14 +70,17 @@ __device__ __forceinline__ void tc_tma_2d(const CUtensorMap* map, uint32_t bar, 
         "l"(reinterpret_cast<uint64_t>(map)), "r"(c0), "r"(c1), "r"(bar)
         : "memory");
 }
-// UMMA shared-memory descriptor, SWIZZLE_128B, sm100 (version 1)
-__device__ __forceinline__ uint64_t tc_desc(uint32_t addr, uint32_t lbo, uint32_t sbo) {
+// UMMA shared-memory descriptor (sm100, version 1).  layout 2 = SWIZZLE_128B
+// (K-major tiles); layout 1 = SWIZZLE_128B_BASE32B, the only smem layout the
+// tensor core accepts for MN-major tf32 operands (32-byte swizzle atoms,
+// 4-row groups; TMA side: CU_TENSOR_MAP_SWIZZLE_128B_ATOM_32B).
+__device__ __forceinline__ uint64_t tc_desc(uint32_t addr, uint32_t lbo, uint32_t sbo, uint32_t layout) {
     uint64_t d = 0;
     d |= (uint64_t)((addr >> 4) & 0x3FFF);
     d |= (uint64_t)((lbo >> 4) & 0x3FFF) << 16;
     d |= (uint64_t)((sbo >> 4) & 0x3FFF) << 32;
     d |= (uint64_t)1 << 46;  // version (Blackwell)
-    d |= (uint64_t)2 << 61;  // SWIZZLE_128B
+    d |= (uint64_t)layout << 61;
     return d;
 }
 __device__ __forceinline__ void tc_mma(uint32_t tmem_d, uint64_t da, uint64_t db, uint32_t idesc, uint32_t acc) {
@@ -202,12 +205,14 @@ __global__ void __launch_bounds__(kTcThreads, 1)
                     // K-major: +32 B inside the 128 B swizzle row; MN-major: +8 rows
                     const uint32_t ao = A_MN ? ks * 1024u : ks * 32u;
                     const uint32_t bo = B_MN ? ks * 1024u : ks * 32u;
-                    const uint32_t albo = A_MN ? 4096u : 16u, asbo = 1024u;
-                    const uint32_t blbo = B_MN ? 4096u : 16u, bsbo = 1024u;
-                    const uint64_t dA = tc_desc(tileA(s) + ao, albo, asbo);
-                    const uint64_t dB = tc_desc(tileB(s) + bo, blbo, bsbo);
-                    const uint64_t dAl = tc_desc(tileAlo(s) + ao, albo, asbo);
-                    const uint64_t dBl = tc_desc(tileBlo(s) + bo, blbo, bsbo);
+                    // K-major SW128: SBO = 8 rows x 128 B; MN-major SW128_BASE32B:
+                    // LBO = 32-wide MN group (one TMA box), SBO = 4 K-rows x 128 B
+                    const uint32_t albo = A_MN ? 4096u : 16u, asbo = A_MN ? 512u : 1024u, alay = A_MN ? 1u : 2u;
+                    const uint32_t blbo = B_MN ? 4096u : 16u, bsbo = B_MN ? 512u : 1024u, blay = B_MN ? 1u : 2u;
+                    const uint64_t dA = tc_desc(tileA(s) + ao, albo, asbo, alay);
+                    const uint64_t dB = tc_desc(tileB(s) + bo, blbo, bsbo, blay);
+                    const uint64_t dAl = tc_desc(tileAlo(s) + ao, albo, asbo, alay);
+                    const uint64_t dBl = tc_desc(tileBlo(s) + bo, blbo, bsbo, blay);
                     const uint32_t first = (kb == 0 && ks == 0) ? 0u : 1u;
                     tc_mma(tmem, dAl, dB, idesc, first);  // small terms first
                     tc_mma(tmem, dA, dBl, idesc, 1u);
@@ -320,15 +325,17 @@ inline PFN_encodeTiled tc_encoder() {
     return fn;
 }
 
-// 2-D fp32 row-major tensor [rows x cols] (ld = cols), box {box_inner, box_rows}
-inline CUtensorMap tc_map(const float* base, int rows, int cols, int box_inner, int box_rows) {
+// 2-D fp32 row-major tensor [rows x cols] (ld = cols), box {box_inner, box_rows};
+// mn_major selects the 32-byte-atom 128B swizzle the MN-major tf32 layout needs
+inline CUtensorMap tc_map(const float* base, int rows, int cols, int box_inner, int box_rows, bool mn_major) {
     CUtensorMap m;
     const cuuint64_t dims[2] = {(cuuint64_t)cols, (cuuint64_t)rows};
     const cuuint64_t strides[1] = {(cuuint64_t)cols * sizeof(float)};
     const cuuint32_t box[2] = {(cuuint32_t)box_inner, (cuuint32_t)box_rows};
     const cuuint32_t estr[2] = {1, 1};
     const CUresult r = tc_encoder()(&m, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2, const_cast<float*>(base), dims, strides,
-                                    box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+                                    box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
+                                    mn_major ? CU_TENSOR_MAP_SWIZZLE_128B_ATOM_32B : CU_TENSOR_MAP_SWIZZLE_128B,
                                     CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
     if (r != CUDA_SUCCESS) throw Error(LANE_ERR_CUDA, "cuTensorMapEncodeTiled failed");
     return m;
