@@ -42,6 +42,14 @@ WORKLOADS = {
 for _h in (256, 512, 1024, 2048, 4096, 8192, 16384, 100000):
     WORKLOADS[f"c4-{_h}"] = (340, [_h], 10, 1e-4, 10000 if _h <= 16384 else 1000,
                              f"340-{_h}-10 width sweep, online SGD (B=1)")
+# mini-batch extension: name -> (input, hidden, classes, eta,
+# global batch, momentum, batches resident, description)
+MINIBATCH = {
+    "c3": (1024, [4096, 4096], 10, 0.01, 256, 0.9, 16,
+           "1024-4096-4096-10 wide MLP, mini-batch 256, momentum 0.9"),
+    "c5": (4096, [4096] * 8, 10, 1e-3, 4096, 0.0, 4,
+           "4096-[4096x8]-10 deep MLP, mini-batch 4096 (data-parallel over ranks)"),
+}
 
 
 def load_peaks():
@@ -131,17 +139,25 @@ def run_reference_arm(args, wl):
     rank, world, _ = dist_env()
     if rank != 0:
         return
-    F, H, C, eta, n_epoch, desc = WORKLOADS[wl]
     from oracle import pyoracle as po
-    X, T = po.synthetic_dataset(F, C, min(n_epoch, 4096), 9)
-    per_ms = {"c1": 0.003, "c2": 1.0}.get(wl, 0.6 * (F * H[0] + H[0] * C) / 1e5)
-    per_step = max(10, int(4000.0 / per_ms / max(1, args.steps + args.warmup)))  # ~4 s of CPU
-    per_step = min(per_step, 100000)
+    if wl in MINIBATCH:
+        # the reference has no mini-batch mode: its per-sample online SGD on the
+        # same network, one sample per step (seconds each on the host cores)
+        F, H, C, eta, _, _, _, desc = MINIBATCH[wl]
+        X, T = po.synthetic_dataset(F, C, 4, 9)
+        per_step = 1
+    else:
+        F, H, C, eta, n_epoch, desc = WORKLOADS[wl]
+        X, T = po.synthetic_dataset(F, C, min(n_epoch, 4096), 9)
+        per_ms = {"c1": 0.003, "c2": 1.0}.get(wl, 0.6 * (F * H[0] + H[0] * C) / 1e5)
+        per_step = max(10, int(4000.0 / per_ms / max(1, args.steps + args.warmup)))  # ~4 s of CPU
+        per_step = min(per_step, 100000)
     cores = os.cpu_count() or 1
     rates = []
     kind = "port"
     for s in range(args.warmup + args.steps):
-        r, kind, used = cpu_reference(F, H, C, eta, X, T, per_step, 2, parallel=True)
+        r, kind, used = cpu_reference(F, H, C, eta, X, T, per_step, 0 if wl in MINIBATCH else 2,
+                                      parallel=True)
         if s >= args.warmup:
             rates.append(r)
     value = float(np.mean(rates))
@@ -149,8 +165,8 @@ def run_reference_arm(args, wl):
             "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
             "ms_per_step": 1000.0 * per_step / value, "higher_is_better": True,
             "scaling": "weak", "vs_baseline": None, "dtype": "f32", "data": "synthetic",
-            "config": {"workload": wl, "description": desc, "layers": [F] + H + [C], "batch": 1,
-                       "samples_per_step": per_step, "eta": eta},
+            "config": {"workload": wl, "description": desc, "layers": [F] + H + [C],
+                       "batch": 1, "samples_per_step": per_step, "eta": eta},
             "cpu_baseline": {"value": value, "unit": "samples/s", "cores": cores, "kind": kind,
                              "sample": f"{per_step} online-SGD samples per step through the "
                                        f"reference's forward + BackwardPlan::run on ParallelHost "
@@ -160,19 +176,133 @@ def run_reference_arm(args, wl):
     print(json.dumps(line), flush=True)
 
 
+def run_minibatch(args, wl):
+    """Mini-batch workloads (C3, C5): one step = one global batch through
+    forward, dgrad, wgrad (tcgen05 3xTF32 GEMMs) and the SGD/momentum update;
+    at N>1 each rank steps its shard and the library all-reduces the gradient
+    sums once per step over NCCL."""
+    import torch
+    rank, world, local = dist_env()
+    torch.cuda.set_device(local)
+    if world > 1:
+        import torch.distributed as dist
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    from oracle import pyoracle as po  # synthetic data generator + cpu_baseline only
+    from paper_2001_04206_b200 import lane, parallel
+
+    F, H, C, eta, BG, mu, nb, desc = MINIBATCH[wl]
+    dev = lane.Device(local)
+    if world > 1:
+        parallel.init_comm(dev, rank, world)
+    rows = BG // world
+    net = lane.build_network(F, H, C, seed=42, device=dev, max_batch=rows)
+    trainer = parallel.DataParallelTrainer(net, eta, mu, BG, rank, world)
+    X, T = po.synthetic_dataset(F, C, nb * BG, 9)
+    xd, td = dev.alloc(X.nbytes), dev.alloc(T.nbytes)
+    dev.h2d(xd, X)
+    dev.h2d(td, T)
+    flush = torch.empty(64 << 20, dtype=torch.float32, device="cuda")  # 256 MB > L2
+    stream = torch.cuda.ExternalStream(dev.stream, device=torch.device("cuda", local))
+    for s in range(args.warmup):
+        trainer.step(xd, td, s % nb, F, C)
+    dev.sync()
+    if world > 1:
+        torch.distributed.barrier()
+    torch.cuda.synchronize()
+    launches0 = dev.kernel_launches
+    evs = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
+           for _ in range(args.steps)]
+    with ClockSampler(local) as clk:
+        for s in range(args.steps):
+            with torch.cuda.stream(stream):
+                flush.zero_()  # L2 flush between timed steps (outside the events)
+            evs[s][0].record(stream)
+            trainer.step(xd, td, s % nb, F, C)
+            evs[s][1].record(stream)
+        torch.cuda.synchronize()
+    launches = dev.kernel_launches - launches0
+    ms = sum(a.elapsed_time(b) for a, b in evs)
+    if world > 1:
+        t = torch.tensor([ms], device="cuda")
+        torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
+        ms = float(t.item())
+    value = BG * args.steps / (ms / 1000.0)
+
+    # e2e: pinned host batch -> device, step, loss back to the host, per step
+    Xh = torch.from_numpy(X[: nb * BG]).pin_memory()
+    Th = torch.from_numpy(T[: nb * BG]).pin_memory()
+    bx, bt = dev.alloc(rows * F * 4), dev.alloc(rows * C * 4)
+    ld = dev.alloc(8)
+    loss_h = torch.zeros(1, dtype=torch.float64).pin_memory()
+    sh = trainer.shard
+    e2e_steps = max(1, min(args.steps, 5))
+    if world > 1:
+        torch.distributed.barrier()
+    torch.cuda.synchronize()
+    t0 = time.perf_counter()
+    for s in range(e2e_steps):
+        r0 = (s % nb) * BG + sh.begin
+        dev.h2d(bx, Xh[r0:r0 + rows].numpy())
+        dev.h2d(bt, Th[r0:r0 + rows].numpy())
+        net.minibatch_step(bx, bt, rows, eta, mu, ld)
+        dev.d2h(loss_h.numpy(), ld)
+    e2e_s = time.perf_counter() - t0
+    if world > 1:
+        t = torch.tensor([e2e_s], device="cuda")
+        torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
+        e2e_s = float(t.item())
+    e2e = BG * e2e_steps / e2e_s
+
+    widths = [F] + H + [C]
+    P = sum(a * b for a, b in zip(widths[:-1], widths[1:]))
+    P0 = widths[0] * widths[1]
+    flops = (6 * P - 2 * P0) * BG  # fwd 2P + wgrad 2P + dgrad 2(P - P0) per sample
+    achieved = flops / (ms / args.steps / 1000.0) / 1e12
+    peaks = json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json"))) if os.path.exists(
+        os.path.join(ROOT, "MEASURED_PEAKS.json")) else {"bf16_tflops": 1590.0}
+    peak = float(peaks.get("bf16_tflops", 1590.0)) / 2.0 / 3.0  # tf32 = bf16/2; 3 MMAs per product
+    line = {"metric": METRIC, "value": value, "unit": "samples/s", "n_gpus": world,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms / args.steps,
+            "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f32",
+            "data": "synthetic",
+            "config": {"workload": wl, "description": desc, "layers": widths, "global_batch": BG,
+                       "momentum": mu, "eta": eta, "parallelism": f"dp{world}",
+                       "gemm": "tcgen05 kind::tf32, 3xTF32 (fp32-accurate)",
+                       "l2": "256 MB buffer written between timed steps"},
+            "roofline": {"bound": "tensor", "achieved": achieved, "peak": peak, "unit": "TFLOP/s",
+                         "frac": achieved / peak, "traffic": None,
+                         "peak_kind": "derived: measured bf16 dense / 2 (tf32) / 3 (3xTF32 MMAs)",
+                         "algorithmic_flops_per_step": flops},
+            "e2e": {"value": e2e, "unit": "samples/s", "h2d_bytes_per_step": rows * (F + C) * 4,
+                    "d2h_bytes_per_step": 8},
+            "gpu_launches": int(launches), "clocks": clk.summary()}
+    if rank == 0 and not args.no_cpu:
+        v, kind, cores = cpu_reference(F, H, C, eta, X[:4], T[:4], 1, 0, parallel=True)
+        line["cpu_baseline"] = {"value": v, "unit": "samples/s", "cores": cores, "kind": kind,
+                                "sample": "1 sample of per-sample online SGD through the reference "
+                                          "(it has no mini-batch mode), ParallelHost"}
+    if rank == 0:
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        torch.distributed.destroy_process_group()
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
     ap.add_argument("--steps", type=int, default=10)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
-    ap.add_argument("--workload", default="c2", choices=sorted(WORKLOADS))
+    ap.add_argument("--workload", default="c2", choices=sorted(WORKLOADS) + sorted(MINIBATCH))
     ap.add_argument("--epoch", type=int, default=0, help="override samples per step")
     ap.add_argument("--no-cpu", action="store_true", help="skip the cpu_baseline leg")
     args = ap.parse_args()
     wl = args.workload
     if args.impl == "reference":
         run_reference_arm(args, wl)
+        return
+    if wl in MINIBATCH:
+        run_minibatch(args, wl)
         return
 
     import torch

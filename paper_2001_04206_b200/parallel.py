@@ -1,0 +1,74 @@
+"""Data-parallel mini-batch training -- host-side driver.
+
+One process per GPU (torchrun), ``torch.distributed`` for the plumbing only:
+rank 0 creates the NCCL unique id inside liblane_b200 and broadcasts it; every
+rank binds its lane context to the communicator (``lane_b200_comm_init``).
+Each step a rank runs forward/dgrad/wgrad on its shard of the global batch
+and the library performs ONE fp32 allreduce (sum) of the flat gradient buffer
+(G and bias gradients of every layer, contiguous in HBM) before the identical
+update on every rank, with 1/B_global folded into the step:
+
+    G = (1/B_global) * sum_{ranks} sum_{b in shard} delta_b (x) x_b
+    DW = mu*DW + (-eta)*G ;  W += DW
+
+Batch-1 online SGD (configs C1, C2, C4) has a strict sample-to-sample
+dependency and does not shard: N GPUs run N independent replicas.
+"""
+from __future__ import annotations
+
+from dataclasses import dataclass
+
+
+@dataclass(frozen=True)
+class Shard:
+    rank: int
+    world: int
+    begin: int  # first row of the global batch owned by this rank
+    rows: int   # rows owned by this rank
+
+
+def shard_batch(global_batch: int, rank: int, world: int) -> Shard:
+    """Contiguous, balanced split of a global batch (rows differ by at most 1).
+    Ranks own consecutive row ranges in rank order, so the union over ranks is
+    the global batch in its original order."""
+    if world < 1 or not (0 <= rank < world):
+        raise ValueError("bad rank/world")
+    if global_batch < world:
+        raise ValueError("global batch smaller than the number of ranks")
+    base, extra = divmod(global_batch, world)
+    rows = base + (1 if rank < extra else 0)
+    begin = rank * base + min(rank, extra)
+    return Shard(rank, world, begin, rows)
+
+
+def init_comm(device, rank: int, world: int, group=None) -> None:
+    """Bind ``device`` (a lane.Device) to an NCCL communicator of ``world``
+    ranks.  Uses torch.distributed (any backend) only to broadcast the id."""
+    import torch.distributed as dist
+    uid = [device.nccl_unique_id() if rank == 0 else None]
+    if world > 1:
+        dist.broadcast_object_list(uid, src=0, group=group)
+    device.comm_init(rank, world, uid[0])
+
+
+class DataParallelTrainer:
+    """Mini-batch SGD/momentum over a device-resident dataset, sharded by rank."""
+
+    def __init__(self, net, eta, mu: float, global_batch: int, rank: int = 0, world: int = 1):
+        if global_batch % world != 0:
+            # unequal shards would weight ranks differently under a single
+            # 1/B_global scale applied per rank-local B
+            raise ValueError("global batch must be divisible by the number of ranks")
+        self.net, self.eta, self.mu = net, eta, mu
+        self.shard = shard_batch(global_batch, rank, world)
+        if net.max_batch < self.shard.rows:
+            raise ValueError("network max_batch smaller than the per-rank shard")
+
+    def step(self, X_dev: int, T_dev: int, batch_index: int, input_width: int, classes: int,
+             loss_dev: int = 0) -> None:
+        """One global step on rows [batch_index*B_global, ...) of the resident
+        dataset; this rank processes its shard."""
+        s = self.shard
+        row0 = batch_index * s.rows * s.world + s.begin
+        self.net.minibatch_step(X_dev + 4 * row0 * input_width, T_dev + 4 * row0 * classes, s.rows,
+                                self.eta, self.mu, loss_dev)
