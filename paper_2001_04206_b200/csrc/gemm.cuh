@@ -50,7 +50,7 @@ __device__ __forceinline__ void epilogue_store(int m, int n, int N, float acc, f
     } else if constexpr (E == Epi::BIAS_TANH) {
         const float z = sadd(acc, bias[n]);
         C[idx] = z;
-        C2[idx] = lane_libm::tanhf(z);
+        C2[idx] = tanhf(z);
     } else {
         C[idx] = tanh_grad(aux[idx], acc);
     }
@@ -171,6 +171,130 @@ void gemm_simt_dispatch(GemmCtx& g, int M, int N, int K, const float* A, int lda
     *g.launches += 1;
 }
 
+// ---- skinny GEMMs (N <= 32: the 10-class output layer) --------------------
+// NN: C[M,N] = A[M,K] B[K,N].  One warp per row, lanes split K (coalesced A
+// row), N partial sums per lane in registers, shuffle-reduced.
+template <Epi E>
+__global__ void __launch_bounds__(256) k_gemm_skinny_nn(int M, int N, int K, const float* __restrict__ A,
+                                                        const float* __restrict__ B, float* __restrict__ C,
+                                                        float* __restrict__ C2, const float* __restrict__ bias) {
+    const int warp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5, lane = threadIdx.x & 31;
+    const int nw = (gridDim.x * blockDim.x) >> 5;
+    for (int m = warp; m < M; m += nw) {
+        float acc[32];
+#pragma unroll
+        for (int n = 0; n < 32; ++n) acc[n] = 0.0f;
+        const float* arow = A + (size_t)m * K;
+        for (int k = lane; k < K; k += 32) {
+            const float a = arow[k];
+            const float* brow = B + (size_t)k * N;
+#pragma unroll
+            for (int n = 0; n < 32; ++n)
+                if (n < N) acc[n] = fmaf(a, __ldg(brow + n), acc[n]);
+        }
+#pragma unroll
+        for (int n = 0; n < 32; ++n)
+            if (n < N) acc[n] = warp_sum(acc[n]);
+        if (lane < N) {
+            float v = 0.0f;
+#pragma unroll
+            for (int n = 0; n < 32; ++n)
+                if (n == lane) v = acc[n];
+            const size_t idx = (size_t)m * N + lane;
+            if constexpr (E == Epi::BIAS || E == Epi::BIAS_TANH) v = sadd(v, bias[lane]);
+            C[idx] = v;
+            if constexpr (E == Epi::BIAS_TANH) C2[idx] = tanhf(v);
+        }
+    }
+}
+
+// TN: C[M,N] = A[K,M]^T B[K,N] (wgrad of the output layer): thread per m
+// (coalesced A rows), K split over blockIdx.y; B rows staged in shared memory;
+// partial sums part[y][m][n] are reduced in a fixed order by k_sum_partials.
+constexpr int kSkinnyKChunk = 256;
+__global__ void __launch_bounds__(256) k_gemm_skinny_tn(int M, int N, int K, const float* __restrict__ A,
+                                                        const float* __restrict__ B, float* __restrict__ part) {
+    __shared__ float bs[kSkinnyKChunk * 32];
+    const int k0 = blockIdx.y * kSkinnyKChunk, k1 = min(K, k0 + kSkinnyKChunk);
+    for (int e = threadIdx.x; e < (k1 - k0) * N; e += blockDim.x) bs[e] = B[(size_t)k0 * N + e];
+    __syncthreads();
+    const int m = blockIdx.x * blockDim.x + threadIdx.x;
+    if (m >= M) return;
+    float acc[32];
+#pragma unroll
+    for (int n = 0; n < 32; ++n) acc[n] = 0.0f;
+    for (int k = k0; k < k1; ++k) {
+        const float a = A[(size_t)k * M + m];
+        const float* brow = bs + (k - k0) * N;
+#pragma unroll
+        for (int n = 0; n < 32; ++n)
+            if (n < N) acc[n] = fmaf(a, brow[n], acc[n]);
+    }
+    float* out = part + ((size_t)blockIdx.y * M + m) * N;
+#pragma unroll
+    for (int n = 0; n < 32; ++n)
+        if (n < N) out[n] = acc[n];
+}
+
+// out[e] = sum_{s < S} part[s*count + e]  (fixed order: deterministic)
+__global__ void k_sum_partials(const float* __restrict__ part, int S, size_t count, float* __restrict__ out) {
+    for (size_t e = (size_t)blockIdx.x * blockDim.x + threadIdx.x; e < count; e += (size_t)gridDim.x * blockDim.x) {
+        float v = part[e];
+        for (int s = 1; s < S; ++s) v += part[(size_t)s * count + e];
+        out[e] = v;
+    }
+}
+
+// Column sums gb[o] = sum_b D[b][o], two passes (row chunks, then fixed-order
+// reduction) so tall batches keep every SM busy.
+constexpr int kColChunk = 128;
+__global__ void k_colsum_part(const float* __restrict__ D, int B, int O, float* __restrict__ part) {
+    const int o = blockIdx.x * blockDim.x + threadIdx.x;
+    if (o >= O) return;
+    const int b0 = blockIdx.y * kColChunk, b1 = min(B, b0 + kColChunk);
+    float v0 = 0.0f, v1 = 0.0f;
+    int b = b0;
+    for (; b + 2 <= b1; b += 2) {
+        v0 += D[(size_t)b * O + o];
+        v1 += D[(size_t)(b + 1) * O + o];
+    }
+    if (b < b1) v0 += D[(size_t)b * O + o];
+    part[(size_t)blockIdx.y * O + o] = v0 + v1;
+}
+
+inline void colsum(GemmCtx& g, const float* D, int B, int O, float* gb) {
+    const int S = (B + kColChunk - 1) / kColChunk;
+    ensure_ws(g, (size_t)S * O);
+    k_colsum_part<<<dim3((O + 127) / 128, S), 128, 0, g.stream>>>(D, B, O, *g.ws);
+    k_sum_partials<<<std::max(1, std::min(4 * g.sm_count, (O + 255) / 256)), 256, 0, g.stream>>>(*g.ws, S, O, gb);
+    *g.launches += 2;
+}
+
+inline bool gemm_try_skinny(GemmCtx& g, GemmOp op, int M, int N, int K, const float* A, int lda, const float* B,
+                            int ldb, Epi e, float* C, float* C2, const float* bias) {
+    if (N > 32) return false;
+    if (op == GemmOp::NN && lda == K && ldb == N && e != Epi::TANH_GRAD) {
+        const int blocks = std::max(1, std::min(8 * g.sm_count, (M + 7) / 8));
+        switch (e) {
+            case Epi::STORE: k_gemm_skinny_nn<Epi::STORE><<<blocks, 256, 0, g.stream>>>(M, N, K, A, B, C, C2, bias); break;
+            case Epi::BIAS: k_gemm_skinny_nn<Epi::BIAS><<<blocks, 256, 0, g.stream>>>(M, N, K, A, B, C, C2, bias); break;
+            default: k_gemm_skinny_nn<Epi::BIAS_TANH><<<blocks, 256, 0, g.stream>>>(M, N, K, A, B, C, C2, bias); break;
+        }
+        *g.launches += 1;
+        return true;
+    }
+    if (op == GemmOp::TN && lda == M && ldb == N && e == Epi::STORE) {
+        const int S = (K + kSkinnyKChunk - 1) / kSkinnyKChunk;
+        ensure_ws(g, (size_t)S * M * N);
+        k_gemm_skinny_tn<<<dim3((M + 255) / 256, S), 256, 0, g.stream>>>(M, N, K, A, B, *g.ws);
+        k_sum_partials<<<std::max(1, std::min(4 * g.sm_count, (M * N + 255) / 256)), 256, 0, g.stream>>>(
+            *g.ws, S, (size_t)M * N, C);
+        *g.launches += 2;
+        return true;
+    }
+    return false;
+}
+
 // 0 = SIMT only, 1 = tensor cores where eligible (default), set by
 // LANE_B200_GEMM=simt|tc or lane_b200_gemm()'s use_tc argument
 inline int& gemm_tc_mode() {
@@ -224,6 +348,7 @@ inline void gemm(GemmCtx& g, GemmOp op, int M, int N, int K, const float* A, int
                  Epi e, float* C, float* C2, const float* bias, const float* aux) {
     if (M <= 0 || N <= 0) return;
     if (gemm_try_tc(g, op, M, N, K, A, lda, B, ldb, e, C, C2, bias, aux)) return;
+    if (gemm_try_skinny(g, op, M, N, K, A, lda, B, ldb, e, C, C2, bias)) return;
     switch (op) {
         case GemmOp::NN: gemm_simt_dispatch<GemmOp::NN>(g, M, N, K, A, lda, B, ldb, e, C, C2, bias, aux); break;
         case GemmOp::NT: gemm_simt_dispatch<GemmOp::NT>(g, M, N, K, A, lda, B, ldb, e, C, C2, bias, aux); break;

@@ -108,10 +108,10 @@ __device__ __forceinline__ float4 tc_epi4(const TcArgs& a, int m, int n, float4 
         v.z = sadd(v.z, b.z);
         v.w = sadd(v.w, b.w);
         if constexpr (E == TcEpi::BIAS_TANH) {
-            second->x = lane_libm::tanhf(v.x);
-            second->y = lane_libm::tanhf(v.y);
-            second->z = lane_libm::tanhf(v.z);
-            second->w = lane_libm::tanhf(v.w);
+            second->x = tanhf(v.x);  // FAST numerics: libdevice tanhf (<= 2 ulp)
+            second->y = tanhf(v.y);
+            second->z = tanhf(v.z);
+            second->w = tanhf(v.w);
         }
     } else if constexpr (E == TcEpi::TANH_GRAD) {
         const float4 t = *reinterpret_cast<const float4*>(a.aux + (size_t)m * a.N + n);
@@ -288,7 +288,7 @@ __global__ void __launch_bounds__(kTcThreads, 1)
                         if constexpr (E == TcEpi::BIAS || E == TcEpi::BIAS_TANH) v = sadd(v, args.bias[n]);
                         if constexpr (E == TcEpi::TANH_GRAD) v = tanh_grad(args.aux[idx], v);
                         args.C[idx] = v;
-                        if constexpr (E == TcEpi::BIAS_TANH) args.C2[idx] = lane_libm::tanhf(v);
+                        if constexpr (E == TcEpi::BIAS_TANH) args.C2[idx] = tanhf(v);
                     }
                 }
             }

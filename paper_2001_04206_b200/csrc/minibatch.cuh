@@ -128,15 +128,6 @@ __global__ void k_loss_rows(const float* __restrict__ row_loss, int B, double* l
     *loss_sum = s;
 }
 
-// Column sums of D (B x O): gb[o] = sum_b D[b][o]  (bias-gradient sums).
-__global__ void k_colsum(const float* __restrict__ D, float* __restrict__ gb, int B, int O) {
-    const int o = blockIdx.x * blockDim.x + threadIdx.x;
-    if (o >= O) return;
-    float s = 0.0f;
-    for (int b = 0; b < B; ++b) s += D[(size_t)b * O + o];
-    gb[o] = s;
-}
-
 // Momentum SGD on a flat range: g = gsum * invB; DW = mu*DW + (-eta)*g;
 // W += DW.  Writes the mean gradient back to gsum (LANE_BUF_G semantics).
 __global__ void k_momentum_update(float* __restrict__ W, float* __restrict__ DW,
@@ -198,9 +189,7 @@ void minibatch_step(Ctx& c, Net& net, const float* X, const float* T, size_t Bsz
         const float* in = l == 0 ? net.L(0).buf[LANE_BUF_INPUTS] : net.L(l - 1).buf[LANE_BUF_OUTPUTS];
         gemm(g, GemmOp::TN, (int)Ly.I, (int)Ly.O, B, in, (int)Ly.I,
              Ly.buf[LANE_BUF_DELTAS], (int)Ly.O, Epi::STORE, Ly.buf[LANE_BUF_G], nullptr, nullptr, nullptr);
-        k_colsum<<<((int)Ly.O + 127) / 128, 128, 0, st>>>(Ly.buf[LANE_BUF_DELTAS], Ly.buf[LANE_BUF_BIAS_GRAD],
-                                                          B, (int)Ly.O);
-        c.launches += 1;
+        colsum(g, Ly.buf[LANE_BUF_DELTAS], B, (int)Ly.O, Ly.buf[LANE_BUF_BIAS_GRAD]);
     }
     // data parallel: one allreduce of the flat gradient-sum buffer
     allreduce_grads(c.comm, net.grads, net.grads_count, st);
