@@ -1,0 +1,285 @@
+// lane_b200/lane.hpp -- C++ facade over the C ABI (include/lane_b200.h) that
+// restores the reference's layer/network API (namespace lane, proj/include/
+// lane/{error,layers,network}.hpp) on B200-resident state.  Header-only; link
+// against paper_2001_04206_b200/lib/liblane_b200.so.
+//
+//   reference                                   here
+//   lane::Device(Kind, workers)                 lane_b200::Device(gpu)
+//   lane::build_network(in, hidden, C, rng)     lane_b200::build_network(dev, in, hidden, C, seed)
+//   FullyConnectedLayer::forward / backward     same names (device buffers behind them)
+//   SoftmaxOutputLayer::forward / backward      same names
+//   LayerState::apply_updates                   same name
+//   BackwardPlan(net, eta, dev).run(target)     BackwardPlan(net, eta).run(target)
+//   train(net, set, cfg, dev) / evaluate        train(net, set, cfg) / evaluate(net, set)
+//   lane::ShapeError, ConfigError, ...          lane_b200::ShapeError, ConfigError, ...
+//
+// Buffers are read/written through LayerState::read()/write() (host vectors),
+// the device-resident analogue of the reference's public std::vector members.
+#pragma once
+
+#include <cstddef>
+#include <cstdint>
+#include <memory>
+#include <stdexcept>
+#include <string>
+#include <vector>
+
+#include "../lane_b200.h"
+
+namespace lane_b200 {
+
+struct Error : std::runtime_error {
+    using std::runtime_error::runtime_error;
+};
+struct ShapeError : Error {
+    using Error::Error;
+};
+struct ConfigError : Error {
+    using Error::Error;
+};
+struct ScheduleError : Error {
+    using Error::Error;
+};
+struct TrainingError : Error {
+    using Error::Error;
+};
+struct IoError : Error {
+    using Error::Error;
+};
+struct ParseError : Error {
+    using Error::Error;
+};
+struct DeviceError : Error {
+    using Error::Error;
+};
+
+inline void check(int rc) {
+    if (rc == LANE_OK) return;
+    const std::string msg = lane_b200_last_error();
+    switch (rc) {
+        case LANE_ERR_SHAPE: throw ShapeError(msg);
+        case LANE_ERR_CONFIG: throw ConfigError(msg);
+        case LANE_ERR_SCHEDULE: throw ScheduleError(msg);
+        case LANE_ERR_TRAINING: throw TrainingError(msg);
+        case LANE_ERR_IO: throw IoError(msg);
+        case LANE_ERR_PARSE: throw ParseError(msg);
+        default: throw DeviceError(msg);
+    }
+}
+
+// layers.hpp:11-19
+struct LearningRate {
+    float eta;
+    explicit LearningRate(float e) : eta(e) {
+        if (!(eta > 0.0f)) throw ConfigError("LearningRate: eta must be positive");
+    }
+};
+
+enum class Numerics { Strict = LANE_NUMERICS_STRICT, Fast = LANE_NUMERICS_FAST };
+
+class Device {
+public:
+    explicit Device(int gpu = 0, Numerics mode = Numerics::Fast) {
+        check(lane_b200_ctx_create(gpu, &ctx_));
+        check(lane_b200_ctx_set_numerics(ctx_, static_cast<int>(mode)));
+    }
+    ~Device() { lane_b200_ctx_destroy(ctx_); }
+    Device(const Device&) = delete;
+    Device& operator=(const Device&) = delete;
+    void set_numerics(Numerics m) { check(lane_b200_ctx_set_numerics(ctx_, static_cast<int>(m))); }
+    void sync() { check(lane_b200_sync(ctx_)); }
+    lane_b200_ctx* handle() const { return ctx_; }
+
+private:
+    lane_b200_ctx* ctx_ = nullptr;
+};
+
+class FeedForwardNetwork;
+
+// layers.hpp:68-92 -- the buffers live in HBM; read()/write() copy them.
+class LayerState {
+public:
+    std::size_t cols_input() const { return in_; }
+    std::size_t cols_out() const { return out_; }
+    std::vector<float> read(int buf) const {
+        std::vector<float> v(count(buf));
+        check(lane_b200_buf_read(net_, index_, buf, v.data(), v.size()));
+        return v;
+    }
+    void write(int buf, const std::vector<float>& v) {
+        if (v.size() != count(buf)) throw ShapeError("LayerState::write: size mismatch");
+        check(lane_b200_buf_write(net_, index_, buf, v.data(), v.size()));
+    }
+    std::vector<float> weights() const { return read(LANE_BUF_W); }
+    std::vector<float> gradients() const { return read(LANE_BUF_G); }
+    std::vector<float> delta_weights() const { return read(LANE_BUF_DW); }
+    std::vector<float> biases() const { return read(LANE_BUF_B); }
+    std::vector<float> inputs() const { return read(LANE_BUF_INPUTS); }
+    std::vector<float> netin() const { return read(LANE_BUF_NETIN); }
+    std::vector<float> outputs() const { return read(LANE_BUF_OUTPUTS); }
+    std::vector<float> deltas() const { return read(LANE_BUF_DELTAS); }
+    std::vector<float> delta_biases() const { return read(LANE_BUF_DELTA_BIASES); }
+
+    // layers.cpp:18-25
+    void apply_updates() { check(lane_b200_apply_updates(net_, index_)); }
+
+    // layers.cpp:27-49 / :71-87
+    std::vector<float> forward(const std::vector<float>& input) {
+        check(lane_b200_layer_forward(net_, index_, input.data(), input.size()));
+        return outputs();
+    }
+
+protected:
+    friend class FeedForwardNetwork;
+    LayerState(lane_b200_net* net, std::size_t index) : net_(net), index_(index) {
+        check(lane_b200_net_shape(net, index, &in_, &out_));
+    }
+    std::size_t count(int buf) const {
+        return (buf == LANE_BUF_W || buf == LANE_BUF_G || buf == LANE_BUF_DW) ? in_ * out_
+               : buf == LANE_BUF_INPUTS                                       ? in_
+                                                                              : out_;
+    }
+    lane_b200_net* net_;
+    std::size_t index_, in_ = 0, out_ = 0;
+};
+
+struct FullyConnectedLayer : LayerState {
+    // layers.cpp:51-69: next_weights is cols_out x next_cols_out, row-major
+    void backward(const std::vector<float>& next_weights, std::size_t next_rows,
+                  std::size_t next_cols, const std::vector<float>& next_deltas, LearningRate eta) {
+        if (next_weights.size() != next_rows * next_cols)
+            throw ShapeError("fc backward: next_weights storage != rows*cols");
+        check(lane_b200_fc_backward(net_, index_, next_weights.data(), next_rows, next_cols,
+                                    next_deltas.data(), next_deltas.size(), eta.eta));
+    }
+    // in-network form: uses the next layer's device weights and deltas
+    void backward(LearningRate eta) {
+        check(lane_b200_fc_backward(net_, index_, nullptr, 0, 0, nullptr, 0, eta.eta));
+    }
+
+private:
+    friend class FeedForwardNetwork;
+    FullyConnectedLayer(lane_b200_net* n, std::size_t i) : LayerState(n, i) {}
+};
+
+struct SoftmaxOutputLayer : LayerState {
+    // layers.cpp:89-102
+    void backward(const std::vector<float>& target, LearningRate eta) {
+        check(lane_b200_softmax_backward(net_, target.data(), target.size(), eta.eta));
+    }
+
+private:
+    friend class FeedForwardNetwork;
+    SoftmaxOutputLayer(lane_b200_net* n, std::size_t i) : LayerState(n, i) {}
+};
+
+struct EpochStats {
+    std::size_t epoch = 0;
+    float mean_loss = 0.0f;
+    float accuracy = 0.0f;
+};
+
+struct TrainerConfig {
+    LearningRate eta{0.01f};
+    float max_error = 0.0f;
+    std::size_t max_epochs = 1;
+    std::uint64_t seed = 0;
+};
+
+// features: n x feature_width, labels: n x classes (one-hot), row-major
+struct DataSet {
+    std::size_t feature_width = 0, class_count = 0;
+    std::vector<float> features, labels;
+    std::size_t size() const { return feature_width ? features.size() / feature_width : 0; }
+};
+
+// network.hpp:14-30
+class FeedForwardNetwork {
+public:
+    FeedForwardNetwork(Device& dev, std::size_t input_width, const std::vector<std::size_t>& hidden,
+                       std::size_t classes, std::size_t max_batch = 1)
+        : input_width_(input_width) {
+        check(lane_b200_net_create(dev.handle(), input_width, hidden.data(), hidden.size(), classes,
+                                   max_batch, &net_));
+        for (std::size_t l = 0; l < hidden.size(); ++l) this->hidden.push_back(FullyConnectedLayer(net_, l));
+        output_.reset(new SoftmaxOutputLayer(net_, hidden.size()));
+    }
+    ~FeedForwardNetwork() { lane_b200_net_destroy(net_); }
+    FeedForwardNetwork(const FeedForwardNetwork&) = delete;
+    FeedForwardNetwork& operator=(const FeedForwardNetwork&) = delete;
+
+    std::size_t input_width() const { return input_width_; }
+    std::size_t class_count() const { return output_->cols_out(); }
+    SoftmaxOutputLayer& output() { return *output_; }
+
+    // network.cpp:47-53
+    std::vector<float> forward(const std::vector<float>& input) {
+        if (input.size() != input_width_) throw ShapeError("forward: input length != cols_input");
+        std::vector<float> p(class_count());
+        check(lane_b200_forward(net_, input.data(), p.data()));
+        return p;
+    }
+    void init_seeded(std::uint64_t seed) { check(lane_b200_net_init_seeded(net_, seed)); }
+    std::uint64_t hash() const {
+        std::uint64_t h = 0;
+        check(lane_b200_net_hash(net_, &h));
+        return h;
+    }
+    lane_b200_net* handle() const { return net_; }
+
+    std::vector<FullyConnectedLayer> hidden;
+
+private:
+    lane_b200_net* net_ = nullptr;
+    std::size_t input_width_;
+    std::unique_ptr<SoftmaxOutputLayer> output_;
+};
+
+// network.cpp:55-66 with SeededRng(seed)
+inline std::unique_ptr<FeedForwardNetwork> build_network(Device& dev, std::size_t input_width,
+                                                         const std::vector<std::size_t>& hidden,
+                                                         std::size_t classes, std::uint64_t seed,
+                                                         std::size_t max_batch = 1) {
+    auto net = std::make_unique<FeedForwardNetwork>(dev, input_width, hidden, classes, max_batch);
+    net->init_seeded(seed);
+    return net;
+}
+
+// network.hpp:58-75
+class BackwardPlan {
+public:
+    BackwardPlan(FeedForwardNetwork& net, LearningRate eta) : net_(net), eta_(eta) {}
+    void run(const std::vector<float>& target) {
+        if (target.size() != net_.class_count()) throw ShapeError("backward: target length != class count");
+        check(lane_b200_backward_plan_run(net_.handle(), target.data(), eta_.eta));
+    }
+
+private:
+    FeedForwardNetwork& net_;
+    LearningRate eta_;
+};
+
+// network.cpp:140-182
+inline std::vector<EpochStats> train(FeedForwardNetwork& net, const DataSet& set, const TrainerConfig& cfg) {
+    if (set.size() == 0) throw TrainingError("train: empty training set");
+    if (set.feature_width != net.input_width()) throw ShapeError("train: dataset feature width != network input width");
+    if (set.class_count != net.class_count()) throw ShapeError("train: dataset class count != network class count");
+    std::vector<float> loss(cfg.max_epochs), acc(cfg.max_epochs);
+    std::size_t ran = 0;
+    check(lane_b200_train(net.handle(), set.features.data(), set.labels.data(), set.size(), cfg.eta.eta,
+                          cfg.max_error, cfg.max_epochs, cfg.seed, loss.data(), acc.data(), &ran));
+    std::vector<EpochStats> out;
+    for (std::size_t e = 0; e < ran; ++e) out.push_back({e + 1, loss[e], acc[e]});
+    return out;
+}
+
+// network.cpp:184-204
+inline EpochStats evaluate(FeedForwardNetwork& net, const DataSet& set) {
+    if (set.size() == 0) throw TrainingError("evaluate: empty test set");
+    EpochStats es;
+    check(lane_b200_evaluate(net.handle(), set.features.data(), set.labels.data(), set.size(), &es.mean_loss,
+                             &es.accuracy));
+    return es;
+}
+
+}  // namespace lane_b200
