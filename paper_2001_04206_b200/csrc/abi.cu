@@ -449,6 +449,7 @@ void launch_persistent(lane_b200_net* net, const SgdPlan& P, const float* X, con
     }
     A.trace = trace;
     A.chunks = P.chunks;
+    A.debug = std::getenv("LANE_B200_SGD_DEBUG") ? std::atoi(std::getenv("LANE_B200_SGD_DEBUG")) : 0;
     A.col4 = P.col4 ? 1 : 0;
     if (P.cluster) {
         const SgdKernel kern = cluster_kernel(A.C);

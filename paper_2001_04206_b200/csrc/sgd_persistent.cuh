@@ -56,6 +56,7 @@ struct SgdArgs {
     unsigned long long* trace;  // debug: per-phase clock64 of CTA 0 for the first kTraceSamples
     int chunks;                 // grid/streamed: K chunks per column group (<= kGrChunks)
     int col4;                   // grid/streamed: 128-bit column quads (H % 4 == 0, npc % 4 == 0)
+    int debug;                  // diagnostics only: bit 0 = skip the bulk weight pass (timing probe)
 };
 
 constexpr int kTraceSamples = 64, kTracePhases = 12;
@@ -502,6 +503,11 @@ __global__ void __launch_bounds__(kClThreads, 1) k_sgd_cluster(SgdArgs A) {
             cp_async_wait<1>();
             named_sync(kBarBulk, 32 * kClBulkWarps);  // cp.async data visible to all bulk warps
             SGD_TRACE(9);
+            if (A.debug & 1) {  // timing probe: critical chain alone
+                __threadfence_block();
+                named_arrive(kBarPass, kClThreads);
+                continue;
+            }
             // -- pass(s): W0 update of sample s fused with y(s+2), q(s+2);
             //    128-bit shared-memory traffic (4 weights per access)
             const float4* xs = reinterpret_cast<const float4*>(xrow(s));
