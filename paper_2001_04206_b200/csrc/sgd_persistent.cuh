@@ -448,42 +448,43 @@ __global__ void __launch_bounds__(kClThreads, 1) k_sgd_cluster(SgdArgs A) {
                 const float an = tanhf(z);
                 SGD_TRACE(5);
                 // -- W1 update of sample s fused with the partial logits of s+1
-                float P0 = 0.0f, P1 = 0.0f;
-                float* wcol = w1s + (lane < C ? lane : 0);
-                int j = 0;
-                for (; j + 2 <= nloc; j += 2) {
-                    const float as0 = __shfl_sync(0xffffffffu, ra, j), as1 = __shfl_sync(0xffffffffu, ra, j + 1);
-                    const float an0 = __shfl_sync(0xffffffffu, an, j), an1 = __shfl_sync(0xffffffffu, an, j + 1);
-                    if (lane < C) {
-                        const float na = sgd_apply(wcol[(size_t)j * C], neg_eta, dk, as0);
-                        const float nb = sgd_apply(wcol[(size_t)(j + 1) * C], neg_eta, dk, as1);
+                //    (a(s), a(s+1) broadcast through shared memory)
+                float* as_s = abuf + par * L.npc;
+                float* an_s = abuf + (par ^ 1) * L.npc;
+                if (lane < nloc) {
+                    as_s[lane] = ra;
+                    an_s[lane] = an;
+                }
+                __syncwarp();
+                float Pk = 0.0f;
+                if (lane < C) {
+                    float P1 = 0.0f;
+                    float* wcol = w1s + lane;
+                    int j = 0;
+                    for (; j + 2 <= nloc; j += 2) {
+                        const float na = sgd_apply(wcol[(size_t)j * C], neg_eta, dk, as_s[j]);
+                        const float nb = sgd_apply(wcol[(size_t)(j + 1) * C], neg_eta, dk, as_s[j + 1]);
                         wcol[(size_t)j * C] = na;
                         wcol[(size_t)(j + 1) * C] = nb;
-                        P0 = fmaf(an0, na, P0);
-                        P1 = fmaf(an1, nb, P1);
+                        Pk = fmaf(an_s[j], na, Pk);
+                        P1 = fmaf(an_s[j + 1], nb, P1);
                     }
-                }
-                if (j < nloc) {
-                    const float as0 = __shfl_sync(0xffffffffu, ra, j), an0 = __shfl_sync(0xffffffffu, an, j);
-                    if (lane < C) {
-                        const float na = sgd_apply(wcol[(size_t)j * C], neg_eta, dk, as0);
+                    if (j < nloc) {
+                        const float na = sgd_apply(wcol[(size_t)j * C], neg_eta, dk, as_s[j]);
                         wcol[(size_t)j * C] = na;
-                        P0 = fmaf(an0, na, P0);
+                        Pk = fmaf(an_s[j], na, Pk);
                     }
+                    Pk += P1;
+                    b1k = sadd(b1k, smul(neg_eta, dk));
                 }
-                const float Pk = lane < C ? P0 + P1 : 0.0f;
-                if (lane < C) b1k = sadd(b1k, smul(neg_eta, dk));
                 ra = an;
                 rz = z;
                 SGD_TRACE(6);
-                // -- push partial(s+1): CS x Cp st.async spread over all 32 lanes
-                const uint32_t gbase = gat_base + (uint32_t)((pn * CS + rank) * Cp * sizeof(float));
-                const uint32_t mbn = mbar0 + 8 * pn;
-                for (int base = 0; base < CS * Cp; base += 32) {
-                    const int idx = base + lane;
-                    const int peer = idx / Cp, k = idx - peer * Cp;
-                    const float v = __shfl_sync(0xffffffffu, Pk, k);  // all lanes take part
-                    if (idx < CS * Cp) st_async_f32(mapa_shared(gbase + 4u * k, peer), v, mapa_shared(mbn, peer));
+                // -- push partial(s+1, k): lane k writes its class into every peer
+                if (lane < Cp) {
+                    const uint32_t off = gat_base + (uint32_t)(((pn * CS + rank) * Cp + lane) * sizeof(float));
+                    const uint32_t mbn = mbar0 + 8 * pn;
+                    for (int p = 0; p < CS; ++p) st_async_f32(mapa_shared(off, p), Pk, mapa_shared(mbn, p));
                 }
                 __syncwarp();
                 SGD_TRACE(7);
