@@ -350,14 +350,6 @@ __global__ void __launch_bounds__(kClThreads, 1) k_sgd_cluster(SgdArgs A) {
     const bool stats = rank == 0 && tid == 32 * (kClBulkWarps - 1);  // last bulk warp, lane 0
     if (stats && A.loss_sum) loss_acc = *A.loss_sum;
 
-    // critical-warp register state for the fast path (lane j owns neuron j)
-    const bool reg_path = L.npc <= 32;
-    float ra = 0.0f, rz = 0.0f, rd = 0.0f, rb0 = 0.0f;  // a(s), z(s), d0(s), b0(s)
-    if (critical && reg_path && lane < nloc) {
-        ra = abuf[lane];
-        rz = zcur[lane];
-        rb0 = b0s[lane];
-    }
     // bulk warp geometry (loop-invariant): neuron slot, K part, float4 range
     const int jw = warp / wpn, part = warp % wpn, nrounds = (nloc + nper - 1) / nper;
     const int q0 = part * (Ip >> 2) / wpn, q1 = (part + 1) * (Ip >> 2) / wpn;
@@ -367,129 +359,7 @@ __global__ void __launch_bounds__(kClThreads, 1) k_sgd_cluster(SgdArgs A) {
         const int par = s & 1;
         float* pl = plb + par * Cp;
         float* d0 = d0b + par * L.npc;
-        if (critical && reg_path) {
-            // ---- register-resident critical chain (npc <= 32, C <= 32) ----
-            const uint32_t mb = mbar0 + 8 * par;
-            SGD_TRACE(0);
-            while (!mbar_try_wait(mb, (uint32_t)((s >> 1) & 1))) {
-            }
-            if (lane == 0 && s + 2 < n) mbar_arrive_expect_tx(mb, xbytes);
-            SGD_TRACE(1);
-            const float* tc = trow(s);
-            float zk = -INFINITY, dk = 0.0f, tk = 0.0f;
-            if (lane < C) {
-                const float* g = gat + (size_t)par * CS * Cp + lane;
-                float v0 = 0.0f, v1 = 0.0f, v2 = 0.0f, v3 = 0.0f;
-                int c = 0;
-                for (; c + 4 <= CS; c += 4) {
-                    v0 += g[(size_t)(c + 0) * Cp];
-                    v1 += g[(size_t)(c + 1) * Cp];
-                    v2 += g[(size_t)(c + 2) * Cp];
-                    v3 += g[(size_t)(c + 3) * Cp];
-                }
-                for (; c < CS; ++c) v0 += g[(size_t)c * Cp];
-                tk = tc[lane];
-                zk = sadd((v0 + v1) + (v2 + v3), b1k);
-            }
-            float m = zk;
-            if (C <= 16) {
-#pragma unroll
-                for (int o = 8; o > 0; o >>= 1) m = fmaxf(m, __shfl_xor_sync(0xffffffffu, m, o, 16));
-            } else {
-                m = warp_max(m);
-            }
-            float e = lane < C ? expf(zk - m) : 0.0f;
-            float sum = e;
-            if (C <= 16) {
-#pragma unroll
-                for (int o = 8; o > 0; o >>= 1) sum += __shfl_xor_sync(0xffffffffu, sum, o, 16);
-            } else {
-                sum = warp_sum(sum);
-            }
-            const float pk = e * __frcp_rn(sum);
-            if (lane < C) {
-                dk = ssub(pk, tk);
-                zl[lane] = zk;
-                pl[lane] = pk;
-                dl[lane] = dk;
-            }
-            SGD_TRACE(2);
-            // -- d0(s) with W1(s): lane j, sequential k (reference rounding)
-            {
-                const float* wrow = w1s + (size_t)min(lane, nloc - 1) * C;
-                float acc = 0.0f;
-                if constexpr (CT > 0) {
-                    float wv[CT];
-#pragma unroll
-                    for (int k = 0; k < CT; ++k) wv[k] = wrow[k];
-#pragma unroll
-                    for (int k = 0; k < CT; ++k) acc = sadd(acc, smul(__shfl_sync(0xffffffffu, dk, k), wv[k]));
-                } else {
-                    for (int k = 0; k < C; ++k) acc = sadd(acc, smul(__shfl_sync(0xffffffffu, dk, k), wrow[k]));
-                }
-                rd = tanh_grad(ra, acc);
-                if (lane < nloc) d0[lane] = rd;
-            }
-            SGD_TRACE(3);
-            named_sync(kBarPass, kClThreads);  // pass(s-1) done: y(s+1), q(s+1), t(s+1)
-            SGD_TRACE(4);
-            __threadfence_block();
-            named_arrive(kBarDelta, kClThreads);  // release d0(s), p(s)
-            if (s + 1 < n) {
-                const int pn = par ^ 1;
-                // -- z(s+1) = y(s+1) + (-eta d0(s)) q(s+1) + b0(s+1);  a(s+1) = tanh
-                float qv = qred[pn * wpn];
-                for (int p = 1; p < wpn; ++p) qv += qred[pn * wpn + p];
-                const float* ry = red + (size_t)pn * L.npc * wpn + (size_t)min(lane, nloc - 1) * wpn;
-                float y = ry[0];
-                for (int p = 1; p < wpn; ++p) y += ry[p];
-                rb0 = sadd(rb0, smul(neg_eta, rd));
-                const float z = sadd(fmaf(neg_eta * rd, qv, y), rb0);
-                const float an = tanhf(z);
-                SGD_TRACE(5);
-                // -- W1 update of sample s fused with the partial logits of s+1
-                //    (a(s), a(s+1) broadcast through shared memory)
-                float* as_s = abuf + par * L.npc;
-                float* an_s = abuf + (par ^ 1) * L.npc;
-                if (lane < nloc) {
-                    as_s[lane] = ra;
-                    an_s[lane] = an;
-                }
-                __syncwarp();
-                float Pk = 0.0f;
-                if (lane < C) {
-                    float P1 = 0.0f;
-                    float* wcol = w1s + lane;
-                    int j = 0;
-                    for (; j + 2 <= nloc; j += 2) {
-                        const float na = sgd_apply(wcol[(size_t)j * C], neg_eta, dk, as_s[j]);
-                        const float nb = sgd_apply(wcol[(size_t)(j + 1) * C], neg_eta, dk, as_s[j + 1]);
-                        wcol[(size_t)j * C] = na;
-                        wcol[(size_t)(j + 1) * C] = nb;
-                        Pk = fmaf(an_s[j], na, Pk);
-                        P1 = fmaf(an_s[j + 1], nb, P1);
-                    }
-                    if (j < nloc) {
-                        const float na = sgd_apply(wcol[(size_t)j * C], neg_eta, dk, as_s[j]);
-                        wcol[(size_t)j * C] = na;
-                        Pk = fmaf(an_s[j], na, Pk);
-                    }
-                    Pk += P1;
-                    b1k = sadd(b1k, smul(neg_eta, dk));
-                }
-                ra = an;
-                rz = z;
-                SGD_TRACE(6);
-                // -- push partial(s+1, k): lane k writes its class into every peer
-                if (lane < Cp) {
-                    const uint32_t off = gat_base + (uint32_t)(((pn * CS + rank) * Cp + lane) * sizeof(float));
-                    const uint32_t mbn = mbar0 + 8 * pn;
-                    for (int p = 0; p < CS; ++p) st_async_f32(mapa_shared(off, p), Pk, mapa_shared(mbn, p));
-                }
-                __syncwarp();
-                SGD_TRACE(7);
-            }
-        } else if (critical) {
+        if (critical) {
             const float* acur = abuf + par * L.npc;
             float* anxt = abuf + (par ^ 1) * L.npc;
             const uint32_t mb = mbar0 + 8 * par;
@@ -686,11 +556,6 @@ __global__ void __launch_bounds__(kClThreads, 1) k_sgd_cluster(SgdArgs A) {
         }
     }
     if (critical && n > 0) named_sync(kBarPass, kClThreads);  // consume pass(n-1)'s arrival
-    if (critical && reg_path && n > 0 && lane < nloc) {
-        abuf[((n - 1) & 1) * L.npc + lane] = ra;
-        zcur[lane] = rz;
-        b0s[lane] = rb0;
-    }
     cp_async_wait<0>();
     __syncthreads();
 
