@@ -18,6 +18,7 @@
 #include "layer_kernels.cuh"
 #include "minibatch.cuh"
 #include "sgd_persistent.cuh"
+#include "sgd_window.cuh"
 
 using namespace lane_b200;
 
@@ -140,6 +141,11 @@ struct lane_b200_net {
     unsigned long long* correct_dev = nullptr;
     unsigned long long* slots = nullptr;
     size_t slots_count = 0;
+    // windowed online-SGD scratch (sgd_window.cuh): banded Gram, Y/d0 rings, counters
+    float* win_coef = nullptr;
+    size_t win_coef_count = 0;
+    float* win_ring = nullptr;
+    size_t win_ring_count = 0;
     // dataset staging for train()/evaluate() (uploaded once per call)
     float* data = nullptr;
     size_t data_count = 0;
@@ -280,6 +286,8 @@ void run_forward_chain(lane_b200_net* net) {
 
 struct SgdPlan {
     bool ok = false;
+    bool window = false;   // delayed-base windowed kernel (chain CTA + W0 producers)
+    int jpl = 4, D = 3;    // window plan: hidden units per chain lane, lag in blocks
     bool cluster = false;  // single thread-block cluster, DSMEM exchange
     bool w0_smem = true;   // grid plan: W0 slices resident in shared memory
     bool col4 = false;     // grid streamed plan: 128-bit column quads
@@ -345,6 +353,23 @@ SgdPlan plan_persistent(lane_b200_net* net) {
               C = static_cast<int>(net->classes);
     if (C > kClMaxC) return p;
     const char* mode = std::getenv("LANE_B200_SGD_MODE");
+    if (!mode || std::strcmp(mode, "window") == 0) {
+        // windowed plan: the chain on one CTA, W0 on H/4 producer CTAs
+        int D = 3;
+        if (const char* e = std::getenv("LANE_B200_SGD_WIN_D")) D = std::max(2, std::min(std::atoi(e), kWinMaxD));
+        const int jpl = H <= 128 ? 4 : 8;
+        const WinSmem L(32 * jpl, D);
+        if (H % 4 == 0 && H <= 256 && C <= kWinCP && I <= kWinMaxNR * kWinThreads &&
+            1 + H / 4 <= c->sm_count && L.total <= c->max_smem_optin) {
+            p.ok = p.window = true;
+            p.jpl = jpl;
+            p.D = D;
+            p.G = 1 + H / 4;
+            p.smem = L.total;
+            return p;
+        }
+        if (mode) return p;
+    }
     if (!mode || std::strcmp(mode, "cluster") == 0) {
         // single-cluster plan: the whole hidden layer on <= 16 SMs, DSMEM exchange
         int CS = std::min(16, H);
@@ -505,6 +530,102 @@ void launch_persistent(lane_b200_net* net, const SgdPlan& P, const float* X, con
     c->check_launch();
 }
 
+using WinKernel = void (*)(WinArgs);
+
+WinKernel window_kernel(int jpl, int C) {
+    if (jpl == 4) return C == 10 ? k_sgd_window<4, 10> : C == 3 ? k_sgd_window<4, 3> : k_sgd_window<4, 0>;
+    return C == 10 ? k_sgd_window<8, 10> : k_sgd_window<8, 0>;
+}
+
+void launch_window(lane_b200_net* net, const SgdPlan& P, const float* X, const float* T, size_t n,
+                   const uint32_t* order, size_t n_steps, long long base, float eta, double* loss_sum,
+                   unsigned long long* correct) {
+    lane_b200_ctx* c = net->ctx;
+    LayerBufs& L0 = net->L(0);
+    LayerBufs& L1 = net->L(1);
+    const int H = static_cast<int>(L0.O);
+    const int QW = P.D * kWinS;
+    ensure(net->win_coef, net->win_coef_count, n_steps * QW);
+    const size_t ring = 2ull * (P.D + 1) * kWinS * H;
+    const size_t cnt_words = 64;  // ycnt[D+1] | dcnt (32-bit), padded
+    ensure(net->win_ring, net->win_ring_count, ring + cnt_words);
+    unsigned* cnt = reinterpret_cast<unsigned*>(net->win_ring + ring);
+    LANE_CUDA(cudaMemsetAsync(cnt, 0, cnt_words * sizeof(float), c->stream));
+    WinArgs A{};
+    A.I = static_cast<int>(net->input_width);
+    A.H = H;
+    A.C = static_cast<int>(net->classes);
+    A.D = P.D;
+    A.P = H / 4;
+    A.QW = QW;
+    A.X = X;
+    A.T = T;
+    A.order = order;
+    A.n = static_cast<long long>(n);
+    A.n_steps = static_cast<long long>(n_steps);
+    A.base = base;
+    A.neg_eta = -eta;
+    A.W0 = L0.buf[LANE_BUF_W];
+    A.b0 = L0.buf[LANE_BUF_B];
+    A.W1 = L1.buf[LANE_BUF_W];
+    A.b1 = L1.buf[LANE_BUF_B];
+    A.coef = net->win_coef;
+    A.yring = net->win_ring;
+    A.dring = net->win_ring + ring / 2;
+    A.ycnt = cnt;
+    A.dcnt = cnt + 32;
+    A.x0 = L0.buf[LANE_BUF_INPUTS];
+    A.z0 = L0.buf[LANE_BUF_NETIN];
+    A.a0 = L0.buf[LANE_BUF_OUTPUTS];
+    A.d0 = L0.buf[LANE_BUF_DELTAS];
+    A.db0 = L0.buf[LANE_BUF_DELTA_BIASES];
+    A.x1 = L1.buf[LANE_BUF_INPUTS];
+    A.z1 = L1.buf[LANE_BUF_NETIN];
+    A.a1 = L1.buf[LANE_BUF_OUTPUTS];
+    A.d1 = L1.buf[LANE_BUF_DELTAS];
+    A.db1 = L1.buf[LANE_BUF_DELTA_BIASES];
+    A.loss_sum = loss_sum;
+    A.correct = correct;
+    A.error = c->error_flag;
+    const char* trace_path = std::getenv("LANE_B200_SGD_TRACE");
+    const size_t trace_n = static_cast<size_t>(kTraceSamples) * kTracePhases;
+    if (trace_path) {
+        A.trace = static_cast<unsigned long long*>(dev_alloc(trace_n * 8));
+        LANE_CUDA(cudaMemsetAsync(A.trace, 0, trace_n * 8, c->stream));
+    }
+    // banded Gram pre-pass
+    k_gram_band<<<static_cast<unsigned>((n_steps + kGramTS - 1) / kGramTS), 256, 0, c->stream>>>(A);
+    c->count();
+    const WinKernel kern = window_kernel(P.jpl, A.C);
+    LANE_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(P.smem)));
+    void* args[] = {&A};
+    LANE_CUDA(cudaLaunchCooperativeKernel(reinterpret_cast<void*>(kern), dim3(P.G), dim3(kWinThreads), args,
+                                          P.smem, c->stream));
+    c->count();
+    if (A.trace) {
+        std::vector<unsigned long long> h(trace_n);
+        LANE_CUDA(cudaMemcpyAsync(h.data(), A.trace, trace_n * 8, cudaMemcpyDeviceToHost, c->stream));
+        LANE_CUDA(cudaStreamSynchronize(c->stream));
+        LANE_CUDA(cudaFree(A.trace));
+        if (FILE* f = std::fopen(trace_path, "a")) {
+            std::fprintf(f, "# plan window G=%d jpl=%d D=%d\n", P.G, P.jpl, P.D);
+            for (int s = 0; s < kTraceSamples; ++s) {
+                for (int ph = 0; ph < kTracePhases; ++ph) std::fprintf(f, "%llu ", h[s * kTracePhases + ph]);
+                std::fprintf(f, "\n");
+            }
+            std::fclose(f);
+        }
+    }
+    for (size_t l = 0; l < 2; ++l) {
+        LayerBufs& Ly = net->L(l);
+        k_outer<<<blocks_for(Ly.I * Ly.O, 256, 8 * c->sm_count), 256, 0, c->stream>>>(
+            Ly.buf[LANE_BUF_DELTAS], Ly.buf[LANE_BUF_INPUTS], Ly.buf[LANE_BUF_G], Ly.buf[LANE_BUF_DW],
+            -eta, static_cast<int>(Ly.I), static_cast<int>(Ly.O));
+        c->count();
+    }
+    c->check_launch();
+}
+
 // Per-sample layer-kernel stream (STRICT numerics, deep nets, C > 128 or
 // slices that do not fit on chip): one captured CUDA graph per step.
 void stream_layer_path(lane_b200_net* net, const float* X, const float* T, size_t n,
@@ -553,7 +674,15 @@ void sgd_stream_impl(lane_b200_net* net, const float* X, const float* T, size_t 
     if (!X || !T) throw Error(LANE_ERR_CONFIG, "sgd_stream: null data");
     if (n_steps == 0) return;
     const SgdPlan P = plan_persistent(net);
-    if (P.ok) {
+    if (P.ok && P.window) {
+        // the banded Gram scratch is sized per launch: stream in chunks
+        const size_t chunk = size_t(1) << 18;
+        for (size_t done = 0; done < n_steps; done += chunk) {
+            const size_t m = std::min(chunk, n_steps - done);
+            launch_window(net, P, X, T, n, order ? order + done : nullptr, m, static_cast<long long>(done % n),
+                          eta, loss_sum, correct);
+        }
+    } else if (P.ok) {
         // the persistent kernels index samples with 32-bit counters
         const size_t chunk = size_t(1) << 30;
         for (size_t done = 0; done < n_steps; done += chunk) {
@@ -818,6 +947,8 @@ int lane_b200_net_destroy(lane_b200_net* net) {
         cudaFree(net->loss_dev);
         cudaFree(net->correct_dev);
         cudaFree(net->slots);
+        cudaFree(net->win_coef);
+        cudaFree(net->win_ring);
         cudaFree(net->data);
         cudaFree(net->order);
         lane_b200_ctx* c = net->ctx;

@@ -329,6 +329,64 @@ def test_sgd_stream_fast_vs_oracle(lane, fast, monkeypatch, mode, F, H, C, n, st
         fast.free(p)
 
 
+@pytest.mark.parametrize("F,H,C,n,steps,eta,D", [
+    (784, [128], 10, 64, 200, 0.01, 3),     # C2 shape, partial last block
+    (784, [128], 10, 64, 200, 0.01, 2),     # shortest lag
+    (784, [128], 10, 64, 203, 0.01, 6),     # longest lag (window 95 rows)
+    (340, [256], 10, 32, 70, 1e-3, 3),      # C4 H=256: 8 hidden units per chain lane
+    (4, [8], 3, 12, 60, 0.1, 3),            # C1 shape: 2 producers, mostly idle lanes
+    (20, [64], 16, 9, 45, 0.05, 3),         # 16 classes (the transpose-reduce limit)
+    (33, [4], 7, 5, 33, 0.1, 3),            # one producer, I % 4 != 0
+    (784, [128], 10, 64, 1, 0.01, 3),       # a single step
+    (784, [128], 10, 64, 17, 0.01, 3),      # shorter than the window
+])
+def test_sgd_window_fast_vs_oracle(lane, fast, monkeypatch, F, H, C, n, steps, eta, D):
+    # delayed-base windowed kernel: chain CTA + W0 producer CTAs + banded Gram
+    monkeypatch.setenv("LANE_B200_SGD_MODE", "window")
+    monkeypatch.setenv("LANE_B200_SGD_WIN_D", str(D))
+    X, T = po.synthetic_dataset(F, C, n, 9)
+    order = np.random.default_rng(2).integers(0, n, steps).astype(np.uint32)
+    net = lane.build_network(F, H, C, seed=42, device=fast)
+    orc = po.OracleNet(F, H, C, seed=42)
+    want_loss = orc.sgd_run(X, T, steps, eta, order=order)
+    Xd, Td, Od = upload(fast, X), upload(fast, T), upload(fast, order, np.uint32)
+    Ld = upload(fast, np.zeros(1, np.float64), np.float64)
+    Cd = upload(fast, np.zeros(1, np.uint64), np.uint64)
+    before = fast.kernel_launches
+    net.sgd_stream(Xd, Td, n, steps, eta, order_dev=Od, loss_dev=Ld, correct_dev=Cd)
+    fast.sync()
+    assert fast.kernel_launches - before == 4  # Gram pre-pass, window kernel, G/DW x2
+    loss = np.zeros(1, np.float64)
+    fast.d2h(loss, Ld)
+    assert abs(loss[0] - want_loss) <= 1e-4 * abs(want_loss)
+    for l, layer in enumerate(net.layers):
+        got, want = layer_arrays(layer), oracle_arrays(orc, l)
+        for b in BUFS:
+            rtol = 1e-5 if steps == 1 else 2e-4
+            assert_close(got[b], want[b], rtol, f"layer {l} {b}")
+    for p in (Xd, Td, Od, Ld, Cd):
+        fast.free(p)
+
+
+def test_sgd_window_no_order_wraps_dataset(lane, fast, monkeypatch):
+    # no order array: sample s is row s % n (stream longer than the dataset)
+    monkeypatch.setenv("LANE_B200_SGD_MODE", "window")
+    F, H, C, n, steps, eta = 50, [32], 10, 7, 40, 0.05
+    X, T = po.synthetic_dataset(F, C, n, 9)
+    net = lane.build_network(F, H, C, seed=42, device=fast)
+    orc = po.OracleNet(F, H, C, seed=42)
+    orc.sgd_run(X, T, steps, eta, order=(np.arange(steps) % n).astype(np.uint32))
+    Xd, Td = upload(fast, X), upload(fast, T)
+    net.sgd_stream(Xd, Td, n, steps, eta)
+    fast.sync()
+    for l, layer in enumerate(net.layers):
+        got, want = layer_arrays(layer), oracle_arrays(orc, l)
+        for b in BUFS:
+            assert_close(got[b], want[b], 2e-4, f"layer {l} {b}")
+    for p in (Xd, Td):
+        fast.free(p)
+
+
 # ----------------------------------------------------- train / evaluate -----
 
 def iris():
