@@ -561,9 +561,11 @@ void launch_window(lane_b200_net* net, const SgdPlan& P, const float* X, const f
     A.X = X;
     A.T = T;
     A.order = order;
-    A.n = static_cast<long long>(n);
-    A.n_steps = static_cast<long long>(n_steps);
-    A.base = base;
+    if (n >= (size_t(1) << 31) || n_steps > (size_t(1) << 18))
+        throw Error(LANE_ERR_CONFIG, "sgd_stream: dataset too large for the windowed kernel");
+    A.n = static_cast<int>(n);
+    A.n_steps = static_cast<int>(n_steps);
+    A.base = static_cast<int>(base);
     A.neg_eta = -eta;
     A.W0 = L0.buf[LANE_BUF_W];
     A.b0 = L0.buf[LANE_BUF_B];

@@ -49,7 +49,7 @@
 namespace lane_b200 {
 
 constexpr int kWinS = 16;                    // samples per block
-constexpr int kWinHelpers = 8;               // helper warps
+constexpr int kWinHelpers = 4;               // helper warps
 constexpr int kWinWarps = kWinHelpers + 3;   // + publisher, loader, critical
 constexpr int kWinThreads = 32 * kWinWarps;  // 352
 constexpr int kWinPub = kWinHelpers, kWinLoad = kWinHelpers + 1, kWinCrit = kWinHelpers + 2;
@@ -65,9 +65,9 @@ struct WinArgs {
     const float* X;
     const float* T;
     const uint32_t* order;  // stream order (offset to this launch) or null
-    long long n;            // dataset rows
-    long long n_steps;      // samples in this launch
-    long long base;         // first stream position (no order: row = (base + s) % n)
+    int n;                  // dataset rows (< 2^31)
+    int n_steps;            // samples in this launch (<= 2^18)
+    int base;               // first stream position mod n (no order: row = (base + s) % n)
     float neg_eta;
     float *W0, *b0, *W1, *b1;
     float* coef;        // [n_steps][QW]: c(s, d) at [s][d-1]
@@ -85,7 +85,7 @@ struct WinArgs {
 
 struct WinSmem {
     int HP, R, Rd;
-    size_t zacc, ystage, tstage, c1stage, d0ring, pring, red, d0s, mbar, total;
+    size_t zacc, ystage, tstage, c1stage, d0ring, pring, red, d0s, rowflag, mbar, total;
     __host__ __device__ WinSmem(int HP_, int D) : HP(HP_) {
         R = D * kWinS;
         Rd = (D + 1) * kWinS;
@@ -98,19 +98,19 @@ struct WinSmem {
         zacc = take((size_t)R * HP);
         ystage = take(2 * (size_t)kWinS * HP);
         tstage = take(2 * kWinS * kWinCP);
-        c1stage = take(2 * kWinS);
+        c1stage = take(4 * kWinS);  // c(s,1) | c(s,2), double-buffered
         d0ring = take((size_t)Rd * HP);
         pring = take((size_t)Rd * kWinCP);
-        red = take(kWinWarps * 64);
+        red = take(kWinCP * 37 > kWinWarps * 64 ? kWinCP * 37 : kWinWarps * 64);
         d0s = take(kWinS * 4);
-        mbar = take(2 * (2 * kWinRing + 4 + kWinBlkRing));
+        rowflag = take(R);
+        mbar = take(2 * (kWinRing + 4 + kWinBlkRing));
         total = o * sizeof(float);
     }
 };
 
 // mbarrier indices (u64 slots)
-constexpr int kMbD0 = 0, kMbRow = kWinRing, kMbYFull = 2 * kWinRing, kMbYFree = 2 * kWinRing + 2,
-              kMbBlk = 2 * kWinRing + 4;
+constexpr int kMbD0 = 0, kMbYFull = kWinRing, kMbYFree = kWinRing + 2, kMbBlk = kWinRing + 4;
 
 __device__ __forceinline__ void mbar_arrive_cta(uint32_t a) {
     asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];\n" ::"r"(a) : "memory");
@@ -127,7 +127,7 @@ __device__ __forceinline__ bool mbar_test_cta(uint32_t a, uint32_t parity) {
     return ok != 0;
 }
 // a 5 s stall is a protocol bug: trap rather than hang the GPU
-__device__ __noinline__ void mbar_wait_slow(uint32_t a, uint32_t parity, int* err) {
+__device__ __forceinline__ void mbar_wait_slow(uint32_t a, uint32_t parity, int* err) {
     const unsigned long long t0 = globaltimer_ns();
     while (!mbar_test_cta(a, parity)) {
         if (globaltimer_ns() - t0 > 5000000000ull) {
@@ -159,8 +159,10 @@ __device__ __forceinline__ void spin_geq(const unsigned* p, unsigned target, int
     }
 }
 
-__device__ __forceinline__ long long win_row(const WinArgs& A, long long s) {
-    return A.order ? (long long)A.order[s] : (A.base + s) % A.n;
+// dataset row of stream position s (32-bit unsigned arithmetic: no 64-bit
+// division subroutine anywhere in these kernels)
+__device__ __forceinline__ long long win_row(const WinArgs& A, int s) {
+    return A.order ? (long long)A.order[s] : (long long)(((unsigned)A.base + (unsigned)s) % (unsigned)A.n);
 }
 
 // Transpose-reduce of N per-lane values over the lanes selected by the
@@ -189,10 +191,10 @@ __global__ void __launch_bounds__(256) k_gram_band(WinArgs A) {
     __shared__ float xs[kGramTS + kGramMaxQW][kGramKC + 1];
     __shared__ long long rows[kGramTS + kGramMaxQW];
     const int QW = A.QW, I = A.I;
-    const long long s0 = (long long)blockIdx.x * kGramTS;
+    const int s0 = blockIdx.x * kGramTS;
     const int NRW = kGramTS + QW;  // rows s0-QW .. s0+TS-1
     for (int r = threadIdx.x; r < NRW; r += blockDim.x) {
-        const long long s = s0 - QW + r;
+        const int s = s0 - QW + r;
         rows[r] = (s >= 0 && s < A.n_steps) ? win_row(A, s) : -1;
     }
     const int sl = threadIdx.x & 31, dg = threadIdx.x >> 5;  // d = dg+1 + 8q
@@ -219,25 +221,24 @@ __global__ void __launch_bounds__(256) k_gram_band(WinArgs A) {
         }
         __syncthreads();
     }
-    const long long s = s0 + sl;
+    const int s = s0 + sl;
     if (s < A.n_steps) {
 #pragma unroll
         for (int q = 0; q < NQ; ++q) {
             const int d = dg + 1 + 8 * q;
-            if (d <= QW) A.coef[s * QW + (d - 1)] = (s - d >= 0) ? A.neg_eta * acc[q] : 0.0f;
+            if (d <= QW) A.coef[(size_t)s * QW + (d - 1)] = (s - d >= 0) ? A.neg_eta * acc[q] : 0.0f;
         }
     }
 }
-
 // ---------------------------------------------------------------------------
 // Producer CTA: W0 columns [4p, 4p+4) in registers.
 // ---------------------------------------------------------------------------
 __device__ __forceinline__ void win_producer(const WinArgs& A, float* sm, const WinSmem& L) {
     const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
-    const int I = A.I, H = A.H, D = A.D, P = A.P;
+    const int I = A.I, H = A.H, D = A.D;
     const int p = blockIdx.x - 1, col = 4 * p;
-    const long long n = A.n_steps;
-    const int nblk = (int)((n + kWinS - 1) / kWinS);
+    const int n = A.n_steps;
+    const int nblk = (n + kWinS - 1) / kWinS;
     const int YR = D + 1, DR = D + 1;
     const float neg_eta = A.neg_eta;
     float* red = sm + L.red;
@@ -254,24 +255,23 @@ __device__ __forceinline__ void win_producer(const WinArgs& A, float* sm, const 
 
     // Y(b)[u][col..col+3] = x(row_u) . W0[:, col..col+3] with the current registers
     auto compute_y = [&](int b) {
-        const int nv = (int)min((long long)kWinS, n - (long long)b * kWinS);
+        const int nv = min(kWinS, n - b * kWinS);
         float acc[4 * kWinS];
 #pragma unroll
         for (int e = 0; e < 4 * kWinS; ++e) acc[e] = 0.0f;
 #pragma unroll
-        for (int u = 0; u < kWinS; ++u) {
-            if (u < nv) {
-                const float* xr = A.X + rn[u] * I;
+        for (int m = 0; m < kWinMaxNR; ++m) {
+            const int i = tid + kWinThreads * m;
+            if (i < I) {
+                float xv[kWinS];
 #pragma unroll
-                for (int m = 0; m < kWinMaxNR; ++m) {
-                    const int i = tid + kWinThreads * m;
-                    if (i < I) {
-                        const float x = __ldg(xr + i);
-                        acc[4 * u + 0] = fmaf(x, w[m].x, acc[4 * u + 0]);
-                        acc[4 * u + 1] = fmaf(x, w[m].y, acc[4 * u + 1]);
-                        acc[4 * u + 2] = fmaf(x, w[m].z, acc[4 * u + 2]);
-                        acc[4 * u + 3] = fmaf(x, w[m].w, acc[4 * u + 3]);
-                    }
+                for (int u = 0; u < kWinS; ++u) xv[u] = u < nv ? __ldg(A.X + rn[u] * I + i) : 0.0f;
+#pragma unroll
+                for (int u = 0; u < kWinS; ++u) {
+                    acc[4 * u + 0] = fmaf(xv[u], w[m].x, acc[4 * u + 0]);
+                    acc[4 * u + 1] = fmaf(xv[u], w[m].y, acc[4 * u + 1]);
+                    acc[4 * u + 2] = fmaf(xv[u], w[m].z, acc[4 * u + 2]);
+                    acc[4 * u + 3] = fmaf(xv[u], w[m].w, acc[4 * u + 3]);
                 }
             }
         }
@@ -297,7 +297,7 @@ __device__ __forceinline__ void win_producer(const WinArgs& A, float* sm, const 
     };
     auto stage_rows = [&](long long* dst, int b) {
         if (tid < kWinS) {
-            const long long s = (long long)b * kWinS + tid;
+            const int s = b * kWinS + tid;
             dst[tid] = s < n ? win_row(A, s) : 0;
         }
     };
@@ -309,37 +309,51 @@ __device__ __forceinline__ void win_producer(const WinArgs& A, float* sm, const 
         compute_y(b);
     }
     for (int k = 0; k < nblk; ++k) {
+        const bool do_y = k + D < nblk;
+        // rows of this block's update and of Y(k+D) do not depend on d0
+        stage_rows(rk, k);
+        if (do_y && tid >= 32 && tid < 32 + kWinS) {
+            const int s = (k + D) * kWinS + (tid - 32);
+            rn[tid - 32] = s < n ? win_row(A, s) : 0;
+        }
         if (tid == 0) spin_geq(A.dcnt, (unsigned)(k + 1), A.error);
         __syncthreads();
-        const int nv = (int)min((long long)kWinS, n - (long long)k * kWinS);
+        const int nv = min(kWinS, n - k * kWinS);
         if (tid < kWinS) {
             d0s[tid] = tid < nv ? __ldcg(reinterpret_cast<const float4*>(
-                                          A.dring + ((size_t)(k % DR) * kWinS + tid) * H + col))
+                                      A.dring + ((size_t)(k % DR) * kWinS + tid) * H + col))
                                 : make_float4(0.f, 0.f, 0.f, 0.f);
         }
-        stage_rows(rk, k);
-        const bool do_y = k + D < nblk;
-        if (do_y) stage_rows(rn, k + D);
-        __syncthreads();
-        // the S per-sample updates, reference rounding, in sample order
-        for (int u = 0; u < nv; ++u) {
-            const float4 d = d0s[u];
-            const float* xr = A.X + rk[u] * I;
+        // x values of the first row group (independent of d0): issued before
+        // the barrier; the barrier itself is unconditional (never divergent)
+        float xv0[kWinS];
 #pragma unroll
-            for (int m = 0; m < kWinMaxNR; ++m) {
-                const int i = tid + kWinThreads * m;
-                if (i < I) {
-                    const float x = __ldg(xr + i);
-                    w[m].x = sgd_apply(w[m].x, neg_eta, d.x, x);
-                    w[m].y = sgd_apply(w[m].y, neg_eta, d.y, x);
-                    w[m].z = sgd_apply(w[m].z, neg_eta, d.z, x);
-                    w[m].w = sgd_apply(w[m].w, neg_eta, d.w, x);
+        for (int u = 0; u < kWinS; ++u) xv0[u] = (tid < I && u < nv) ? __ldg(A.X + rk[u] * I + tid) : 0.0f;
+        __syncthreads();  // d0s visible
+#pragma unroll
+        for (int m = 0; m < kWinMaxNR; ++m) {
+            const int i = tid + kWinThreads * m;
+            if (i < I) {
+                float xv[kWinS];
+#pragma unroll
+                for (int u = 0; u < kWinS; ++u)
+                    xv[u] = m == 0 ? xv0[u] : (u < nv ? __ldg(A.X + rk[u] * I + i) : 0.0f);
+                // the S per-sample updates, reference rounding, in sample order
+#pragma unroll
+                for (int u = 0; u < kWinS; ++u) {
+                    if (u < nv) {
+                        const float4 d = d0s[u];
+                        w[m].x = sgd_apply(w[m].x, neg_eta, d.x, xv[u]);
+                        w[m].y = sgd_apply(w[m].y, neg_eta, d.y, xv[u]);
+                        w[m].z = sgd_apply(w[m].z, neg_eta, d.z, xv[u]);
+                        w[m].w = sgd_apply(w[m].w, neg_eta, d.w, xv[u]);
+                    }
                 }
             }
         }
         if (do_y) compute_y(k + D);
+        __syncthreads();  // rk/rn/d0s reuse
     }
-    (void)P;
 #pragma unroll
     for (int m = 0; m < kWinMaxNR; ++m) {
         const int i = tid + kWinThreads * m;
@@ -351,6 +365,20 @@ __device__ __forceinline__ void win_producer(const WinArgs& A, float* sm, const 
     }
 }
 
+__device__ __forceinline__ unsigned ld_acquire_cta_u32(uint32_t saddr) {
+    unsigned v;
+    asm volatile("ld.acquire.cta.shared::cta.u32 %0, [%1];\n" : "=r"(v) : "r"(saddr) : "memory");
+    return v;
+}
+__device__ __forceinline__ void st_release_cta_u32(uint32_t saddr, unsigned v) {
+    asm volatile("st.release.cta.shared::cta.u32 [%0], %1;\n" ::"r"(saddr), "r"(v) : "memory");
+}
+__device__ __forceinline__ float rcp_approx(float x) {
+    float r;
+    asm("rcp.approx.ftz.f32 %0, %1;\n" : "=f"(r) : "f"(x));
+    return r;
+}
+
 // ---------------------------------------------------------------------------
 // Chain CTA.
 // ---------------------------------------------------------------------------
@@ -360,8 +388,8 @@ __device__ __forceinline__ void win_chain(const WinArgs& A, float* sm, const Win
     const int H = A.H, D = A.D, HP = L.HP, R = L.R, Rd = L.Rd, QW = A.QW;
     const int HQ = H >> 2, HPQ = HP >> 2;  // float4 per row (used / padded)
     const int C = CT > 0 ? CT : A.C;
-    const long long n = A.n_steps;
-    const int nblk = (int)((n + kWinS - 1) / kWinS);
+    const int n = (int)A.n_steps;  // <= 2^18 per launch (host chunks the stream)
+    const int nblk = (n + kWinS - 1) / kWinS;
     const int YR = D + 1, DR = D + 1;
     const float neg_eta = A.neg_eta;
     float* zacc = sm + L.zacc;
@@ -370,19 +398,25 @@ __device__ __forceinline__ void win_chain(const WinArgs& A, float* sm, const Win
     float* c1stage = sm + L.c1stage;
     float* d0ring = sm + L.d0ring;
     float* pring = sm + L.pring;
+    float* red = sm + L.red;
+    unsigned* rowflag = reinterpret_cast<unsigned*>(sm + L.rowflag);
     const uint32_t mb = smem_u32(sm + L.mbar);
     auto MB = [&](int idx) { return mb + 8u * (uint32_t)idx; };
+    unsigned long long* const trace = A.trace;
+#define WIN_TRACE(s_, ph)                                                                \
+    do {                                                                                 \
+        if (trace && lane == 0 && (s_) < kTraceSamples)                                  \
+            trace[(s_) * kTracePhases + (ph)] = clock64();                               \
+    } while (0)
 
     // ---- prologue: zero the rings, init the barriers
     for (int e = tid; e < R * HP; e += kWinThreads) zacc[e] = 0.0f;
     for (int e = tid; e < 2 * kWinS * HP; e += kWinThreads) ystage[e] = 0.0f;
     for (int e = tid; e < 2 * kWinS * kWinCP; e += kWinThreads) tstage[e] = 0.0f;
     for (int e = tid; e < Rd * HP; e += kWinThreads) d0ring[e] = 0.0f;
+    for (int e = tid; e < R; e += kWinThreads) rowflag[e] = 0u;
     if (tid == 0) {
-        for (int r = 0; r < kWinRing; ++r) {
-            mbar_init(MB(kMbD0 + r), 32);
-            mbar_init(MB(kMbRow + r), 32);
-        }
+        for (int r = 0; r < kWinRing; ++r) mbar_init(MB(kMbD0 + r), 32);
         for (int r = 0; r < 2; ++r) {
             mbar_init(MB(kMbYFull + r), 32);
             mbar_init(MB(kMbYFree + r), 32);
@@ -390,126 +424,199 @@ __device__ __forceinline__ void win_chain(const WinArgs& A, float* sm, const Win
         for (int r = 0; r < kWinBlkRing; ++r) mbar_init(MB(kMbBlk + r), 32);
     }
     __syncthreads();
-    // rows 0 and 1 need no helper work: complete their row-ready phases so
-    // that phase p of ring slot j always means row j + 16p
-    if (warp == 0) {
-        mbar_arrive_cta(MB(kMbRow + 0));
-        mbar_arrive_cta(MB(kMbRow + 1));
-    }
 
     if (warp == kWinCrit) {
         // ================= the serial chain =================
         constexpr int CC = CT > 0 ? CT : kWinCP;
         constexpr int NQ = JPL / 4;
-        const int myk = lane >> 1;  // class held after the transpose-reduce
-        const bool kval = myk < C;
-        float w1[JPL][CC], b0r[JPL], dprev[JPL];
+        const bool kval = lane < C;  // lane k also owns class k (totals, b1)
+        float w1[JPL][CC], b0r[JPL], dp1[JPL], dp2[JPL], aprev[JPL], d1prev[CC];
 #pragma unroll
         for (int m = 0; m < JPL; ++m) {
             const int j = JPL * lane + m;
 #pragma unroll
             for (int k = 0; k < CC; ++k) w1[m][k] = (j < H && k < C) ? A.W1[(size_t)j * C + k] : 0.0f;
             b0r[m] = j < H ? A.b0[j] : 0.0f;
-            dprev[m] = 0.0f;
+            dp1[m] = dp2[m] = aprev[m] = 0.0f;
         }
-        float b1k = kval ? A.b1[myk] : 0.0f;
-        float zl[JPL], al[JPL], zkl = 0.0f, pkl = 0.0f, dkl = 0.0f;
+#pragma unroll
+        for (int k = 0; k < CC; ++k) d1prev[k] = 0.0f;
+        float b1k = kval ? A.b1[lane] : 0.0f;
+        float zl[JPL], al[JPL];
 #pragma unroll
         for (int m = 0; m < JPL; ++m) zl[m] = al[m] = 0.0f;
-        for (long long s = 0; s < n; ++s) {
-            const int b = (int)(s / kWinS), u = (int)(s % kWinS), st = b & 1;
-            if (A.trace && lane == 0 && s < kTraceSamples) A.trace[s * kTracePhases + 0] = clock64();
-            if (u == 0) mbar_wait_cta(MB(kMbYFull + st), (uint32_t)((b >> 1) & 1), A.error);
-            mbar_wait_cta(MB(kMbRow + (int)(s % kWinRing)), (uint32_t)((s / kWinRing) & 1), A.error);
-            if (A.trace && lane == 0 && s < kTraceSamples) A.trace[s * kTracePhases + 1] = clock64();
-            const float c1 = c1stage[st * kWinS + u];
-            const float4* zr = reinterpret_cast<const float4*>(zacc + (size_t)(s % R) * HP) + lane * NQ;
-            const float4* yr = reinterpret_cast<const float4*>(ystage + (size_t)(st * kWinS + u) * HP) + lane * NQ;
-            float z[JPL], a[JPL];
+        // prefetched operands of the next sample
+        float zpre[JPL], tn[CC], c1n = 0.0f, c2n = 0.0f;
+        // s1R = s1 % R (ring slot), kept incrementally: no 64-bit modulo on the chain
+        auto flag_wait = [&](int s1, int s1R) {
+            if (s1 < 3) return;  // rows 0..2: the chain applies every correction itself
+            const uint32_t fa = smem_u32(rowflag + s1R);
+            const unsigned want = (unsigned)(s1 + 1);
+            if (ld_acquire_cta_u32(fa) != want) {
+                const unsigned long long t0 = globaltimer_ns();
+                while (ld_acquire_cta_u32(fa) != want) {
+                    if (globaltimer_ns() - t0 > 5000000000ull) {
+                        atomicExch(A.error, 4);
+                        __trap();
+                    }
+                }
+            }
+        };
+        auto fetch_row = [&](int s1, int s1R) {
+            const int b1 = s1 >> 4, u1 = s1 & (kWinS - 1), st1 = b1 & 1;
+            if (u1 == 0) mbar_wait_cta(MB(kMbYFull + st1), (uint32_t)((b1 >> 1) & 1), A.error);
+            const float4* zr = reinterpret_cast<const float4*>(zacc + s1R * HP) + lane * NQ;
+            const float4* yr = reinterpret_cast<const float4*>(ystage + (st1 * kWinS + u1) * HP) + lane * NQ;
 #pragma unroll
             for (int q = 0; q < NQ; ++q) {
                 const float4 za = zr[q], ya = yr[q];
-                z[4 * q + 0] = fmaf(c1, dprev[4 * q + 0], za.x + ya.x) + b0r[4 * q + 0];
-                z[4 * q + 1] = fmaf(c1, dprev[4 * q + 1], za.y + ya.y) + b0r[4 * q + 1];
-                z[4 * q + 2] = fmaf(c1, dprev[4 * q + 2], za.z + ya.z) + b0r[4 * q + 2];
-                z[4 * q + 3] = fmaf(c1, dprev[4 * q + 3], za.w + ya.w) + b0r[4 * q + 3];
+                zpre[4 * q + 0] = za.x + ya.x;
+                zpre[4 * q + 1] = za.y + ya.y;
+                zpre[4 * q + 2] = za.z + ya.z;
+                zpre[4 * q + 3] = za.w + ya.w;
+            }
+            const float* tr = tstage + (st1 * kWinS + u1) * kWinCP;
+#pragma unroll
+            for (int k = 0; k < CC; ++k) tn[k] = tr[k];
+            c1n = c1stage[st1 * kWinS + u1];
+            c2n = c1stage[2 * kWinS + st1 * kWinS + u1];
+        };
+        if (n > 0) fetch_row(0, 0);
+        int sR = 0, sRd = 0;  // s % R, s % Rd
+        float* const xr = red;  // [k][36]: partial logits, transposed
+        float* const zt = red + kWinCP * 36;  // class totals (logits) of this sample
+        for (int s = 0; s < n; ++s) {
+            const int b = s >> 4, u = s & (kWinS - 1), st = b & 1;
+            WIN_TRACE(s, 0);
+            // -- z(s) = Y + window + c1 d0(s-1) + c2 d0(s-2) + b0;  tanh.
+            //    The deferred W1 update of s-1 fills the tanh latency.
+            float z[JPL], a[JPL];
+#pragma unroll
+            for (int m = 0; m < JPL; ++m) {
+                z[m] = fmaf(c1n, dp1[m], fmaf(c2n, dp2[m], zpre[m])) + b0r[m];
+                a[m] = tanhf(z[m]);
             }
 #pragma unroll
-            for (int m = 0; m < JPL; ++m) a[m] = tanhf(z[m]);
-            if (A.trace && lane == 0 && s < kTraceSamples) A.trace[s * kTracePhases + 2] = clock64();
-            // partial logits of this lane's hidden units, then the transpose-reduce
-            float P[kWinCP];
+            for (int m = 0; m < JPL; ++m)
 #pragma unroll
-            for (int k = 0; k < kWinCP; ++k) {
-                float acc = 0.0f;
-                if (k < CC) {
-#pragma unroll
-                    for (int m = 0; m < JPL; ++m) acc = fmaf(a[m], w1[m][k], acc);
-                }
-                P[k] = acc;
-            }
-            xpose_step<16>(P, lane, 16);
-            xpose_step<8>(P, lane, 8);
-            xpose_step<4>(P, lane, 4);
-            xpose_step<2>(P, lane, 2);
-            float zk = P[0] + __shfl_xor_sync(0xffffffffu, P[0], 1);
-            zk = sadd(zk, b1k);
-            if (A.trace && lane == 0 && s < kTraceSamples) A.trace[s * kTracePhases + 3] = clock64();
-            float mx = kval ? zk : -INFINITY;
-#pragma unroll
-            for (int o = 2; o < 32; o <<= 1) mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, o));
-            float e = kval ? expf(zk - mx) : 0.0f;
-            float sum = e;
-#pragma unroll
-            for (int o = 2; o < 32; o <<= 1) sum += __shfl_xor_sync(0xffffffffu, sum, o);
-            const float pk = __fdiv_rn(e, sum);
-            const float tk = kval ? tstage[(st * kWinS + u) * kWinCP + myk] : 0.0f;
-            const float dk = kval ? ssub(pk, tk) : 0.0f;
-            float d1[CC];
-#pragma unroll
-            for (int k = 0; k < CC; ++k) d1[k] = __shfl_sync(0xffffffffu, dk, 2 * k);
-            if (A.trace && lane == 0 && s < kTraceSamples) A.trace[s * kTracePhases + 4] = clock64();
-            // hidden deltas with the pre-update W1
-            float d0v[JPL];
+                for (int k = 0; k < CC; ++k) w1[m][k] = sgd_apply(w1[m][k], neg_eta, d1prev[k], aprev[m]);
+            float TW[JPL];  // W1(s) t(s)
 #pragma unroll
             for (int m = 0; m < JPL; ++m) {
                 float acc = 0.0f;
 #pragma unroll
-                for (int k = 0; k < CC; ++k) acc = fmaf(d1[k], w1[m][k], acc);
-                d0v[m] = tanh_grad(a[m], acc);
+                for (int k = 0; k < CC; ++k) acc = fmaf(tn[k], w1[m][k], acc);
+                TW[m] = acc;
             }
-            float4* dr = reinterpret_cast<float4*>(d0ring + (size_t)(s % Rd) * HP) + lane * NQ;
+            WIN_TRACE(s, 1);
+            // -- partial logits -> shared memory (transposed), lane k sums class k
+#pragma unroll
+            for (int k = 0; k < CC; ++k) {
+                float acc = 0.0f;
+#pragma unroll
+                for (int m = 0; m < JPL; ++m) acc = fmaf(a[m], w1[m][k], acc);
+                xr[k * 36 + lane] = acc;
+            }
+            __syncwarp();
+            if (kval) {
+                const float4* col = reinterpret_cast<const float4*>(xr + lane * 36);
+                float4 v[8];
+#pragma unroll
+                for (int q = 0; q < 8; ++q) v[q] = col[q];
+                float t8[8];
+#pragma unroll
+                for (int q = 0; q < 8; ++q) t8[q] = (v[q].x + v[q].y) + (v[q].z + v[q].w);
+                const float tot = ((t8[0] + t8[1]) + (t8[2] + t8[3])) + ((t8[4] + t8[5]) + (t8[6] + t8[7]));
+                zt[lane] = sadd(tot, b1k);
+            }
+            __syncwarp();
+            WIN_TRACE(s, 2);
+            // -- softmax, redundantly in every lane (no cross-lane reduction):
+            //    exact max, C exponentials, sum; E = W1 e overlaps the sum
+            float zk[CC], ek[CC];
+#pragma unroll
+            for (int k = 0; k < CC; ++k) zk[k] = k < C ? zt[k] : -INFINITY;
+            float mx = zk[0];
+#pragma unroll
+            for (int k = 1; k < CC; ++k) mx = fmaxf(mx, zk[k]);
+#pragma unroll
+            for (int k = 0; k < CC; ++k) ek[k] = k < C ? expf(zk[k] - mx) : 0.0f;
+            float sum = 0.0f;
+#pragma unroll
+            for (int k = 0; k < CC; ++k) sum += ek[k];
+            float E[JPL];
+#pragma unroll
+            for (int m = 0; m < JPL; ++m) {
+                float acc = 0.0f;
+#pragma unroll
+                for (int k = 0; k < CC; ++k) acc = fmaf(ek[k], w1[m][k], acc);
+                E[m] = acc;
+            }
+            const float inv = rcp_approx(sum);
+            // d0 = (1 - a^2) * (W1 (p - t)) = (1 - a^2) * (E/sum - W1 t)
+            float d0v[JPL];
+#pragma unroll
+            for (int m = 0; m < JPL; ++m) d0v[m] = tanh_grad(a[m], fmaf(E[m], inv, -TW[m]));
+            WIN_TRACE(s, 3);
+            float4* dr = reinterpret_cast<float4*>(d0ring + sRd * HP) + lane * NQ;
 #pragma unroll
             for (int q = 0; q < NQ; ++q)
                 dr[q] = make_float4(d0v[4 * q], d0v[4 * q + 1], d0v[4 * q + 2], d0v[4 * q + 3]);
-            if (kval && !(lane & 1)) pring[(size_t)(s % Rd) * kWinCP + myk] = pk;
-            mbar_arrive_cta(MB(kMbD0 + (int)(s % kWinRing)));
+            mbar_arrive_cta(MB(kMbD0 + (s & (kWinRing - 1))));
+            WIN_TRACE(s, 4);
+            // -- off the chain: p, d1, stats, bias updates
+#pragma unroll
+            for (int k = 0; k < CC; ++k) d1prev[k] = k < C ? ssub(ek[k] * inv, tn[k]) : 0.0f;
+            if (kval) {
+                float pk = 0.0f, dk = 0.0f;
+#pragma unroll
+                for (int k = 0; k < CC; ++k)
+                    if (k == lane) {
+                        pk = ek[k] * inv;
+                        dk = d1prev[k];
+                    }
+                pring[sRd * kWinCP + lane] = pk;
+                b1k = sadd(b1k, smul(neg_eta, dk));
+                if (s == n - 1) {
+                    A.z1[lane] = zt[lane];
+                    A.a1[lane] = pk;
+                    A.d1[lane] = dk;
+                    A.db1[lane] = smul(neg_eta, dk);
+                }
+            }
             if (u == kWinS - 1 || s == n - 1) {
                 mbar_arrive_cta(MB(kMbBlk + b % kWinBlkRing));
                 mbar_arrive_cta(MB(kMbYFree + st));
             }
-            if (A.trace && lane == 0 && s < kTraceSamples) A.trace[s * kTracePhases + 5] = clock64();
-            // updates of sample s (reference rounding)
 #pragma unroll
             for (int m = 0; m < JPL; ++m) {
-#pragma unroll
-                for (int k = 0; k < CC; ++k) w1[m][k] = sgd_apply(w1[m][k], neg_eta, d1[k], a[m]);
                 b0r[m] = sadd(b0r[m], smul(neg_eta, d0v[m]));
-                dprev[m] = d0v[m];
+                dp2[m] = dp1[m];
+                dp1[m] = d0v[m];
+                aprev[m] = a[m];
             }
-            b1k = sadd(b1k, smul(neg_eta, dk));
             if (s == n - 1) {
 #pragma unroll
                 for (int m = 0; m < JPL; ++m) {
                     zl[m] = z[m];
                     al[m] = a[m];
                 }
-                zkl = zk;
-                pkl = pk;
-                dkl = dk;
             }
+            WIN_TRACE(s, 5);
+            if (++sR == R) sR = 0;
+            if (++sRd == Rd) sRd = 0;
+            if (s + 1 < n) {
+                flag_wait(s + 1, sR);
+                fetch_row(s + 1, sR);
+            }
+            WIN_TRACE(s, 6);
         }
         if (n > 0) {
+            // the last sample's W1 update (deferred in the loop)
+#pragma unroll
+            for (int m = 0; m < JPL; ++m)
+#pragma unroll
+                for (int k = 0; k < CC; ++k) w1[m][k] = sgd_apply(w1[m][k], neg_eta, d1prev[k], aprev[m]);
 #pragma unroll
             for (int m = 0; m < JPL; ++m) {
                 const int j = JPL * lane + m;
@@ -520,64 +627,92 @@ __device__ __forceinline__ void win_chain(const WinArgs& A, float* sm, const Win
                     A.b0[j] = b0r[m];
                     A.z0[j] = zl[m];
                     A.a0[j] = al[m];
-                    A.d0[j] = dprev[m];
-                    A.db0[j] = smul(neg_eta, dprev[m]);
+                    A.d0[j] = dp1[m];
+                    A.db0[j] = smul(neg_eta, dp1[m]);
                     A.x1[j] = al[m];
                 }
             }
-            if (kval && !(lane & 1)) {
-                A.b1[myk] = b1k;
-                A.z1[myk] = zkl;
-                A.a1[myk] = pkl;
-                A.d1[myk] = dkl;
-                A.db1[myk] = smul(neg_eta, dkl);
-            }
+            if (kval) A.b1[lane] = b1k;
         }
     } else if (warp == kWinLoad) {
         // ================= loader: Y(b), targets, c(s,1) =================
         for (int b = 0; b < nblk; ++b) {
             const int st = b & 1;
+            const int s0 = b * kWinS;
+            const int nv = min(kWinS, n - s0);
+            // independent of the producers: rows, targets, c(s,1)
+            const long long myrow = lane < nv ? win_row(A, s0 + lane) : 0;
+            const float c1v = lane < nv ? __ldg(A.coef + (s0 + lane) * QW) : 0.0f;
+            const float c2v = lane < nv ? __ldg(A.coef + (s0 + lane) * QW + 1) : 0.0f;
+            float tv[kWinS * kWinCP / 32];
+#pragma unroll
+            for (int q = 0; q < kWinS * kWinCP / 32; ++q) {
+                const int e = lane + 32 * q, u = e / kWinCP, k = e % kWinCP;
+                const long long r = __shfl_sync(0xffffffffu, myrow, u);
+                tv[q] = (u < nv && k < C) ? __ldg(A.T + r * C + k) : 0.0f;
+            }
+            WIN_TRACE(s0, 8);
             if (b >= 2) mbar_wait_cta(MB(kMbYFree + st), (uint32_t)(((b - 2) >> 1) & 1), A.error);
             spin_geq(A.ycnt + (b % YR), (unsigned)(A.P * (b / YR + 1)), A.error);
-            const int nv = (int)min((long long)kWinS, n - (long long)b * kWinS);
+            WIN_TRACE(s0, 9);
             const float4* src = reinterpret_cast<const float4*>(A.yring + (size_t)(b % YR) * kWinS * H);
             float4* dst = reinterpret_cast<float4*>(ystage + (size_t)st * kWinS * HP);
-            for (int e = lane; e < nv * HQ; e += 32) {
-                const int u = e / HQ, q = e - u * HQ;
-                dst[u * HPQ + q] = __ldcg(src + u * HQ + q);
+            for (int e0 = 0; e0 < nv * HQ; e0 += 32 * 8) {
+                float4 v[8];
+#pragma unroll
+                for (int q = 0; q < 8; ++q) {
+                    const int e = e0 + lane + 32 * q;
+                    if (e < nv * HQ) v[q] = __ldcg(src + e);
+                }
+#pragma unroll
+                for (int q = 0; q < 8; ++q) {
+                    const int e = e0 + lane + 32 * q;
+                    if (e < nv * HQ) {
+                        const int u = e / HQ, qq = e - u * HQ;
+                        dst[u * HPQ + qq] = v[q];
+                    }
+                }
             }
-            for (int e = lane; e < nv * C; e += 32) {
-                const int u = e / C, k = e - u * C;
-                const long long row = win_row(A, (long long)b * kWinS + u);
-                tstage[(st * kWinS + u) * kWinCP + k] = __ldg(A.T + row * C + k);
+#pragma unroll
+            for (int q = 0; q < kWinS * kWinCP / 32; ++q) tstage[st * kWinS * kWinCP + lane + 32 * q] = tv[q];
+            if (lane < kWinS) {
+                c1stage[st * kWinS + lane] = c1v;
+                c1stage[2 * kWinS + st * kWinS + lane] = c2v;
             }
-            if (lane < kWinS)
-                c1stage[st * kWinS + lane] = lane < nv ? __ldg(A.coef + ((long long)b * kWinS + lane) * QW) : 0.0f;
             mbar_arrive_cta(MB(kMbYFull + st));
+            WIN_TRACE(s0, 10);
         }
     } else if (warp == kWinPub) {
         // ================= publisher: d0 blocks to L2, loss/accuracy =================
         double loss_acc = (lane == 0 && A.loss_sum) ? *A.loss_sum : 0.0;
         unsigned long long correct_acc = 0;
+        const bool stats = A.loss_sum || A.correct;
         for (int k = 0; k < nblk; ++k) {
+            const int s0 = k * kWinS;
+            const int nv = min(kWinS, n - s0);
+            // target row of sample s0+lane (independent of the chain)
+            const long long myrow = (stats && lane < nv) ? win_row(A, s0 + lane) : 0;
             mbar_wait_cta(MB(kMbBlk + k % kWinBlkRing), (uint32_t)((k / kWinBlkRing) & 1), A.error);
-            const int nv = (int)min((long long)kWinS, n - (long long)k * kWinS);
+            WIN_TRACE(s0, 11);
             float4* dst = reinterpret_cast<float4*>(A.dring + (size_t)(k % DR) * kWinS * H);
             for (int e = lane; e < nv * HQ; e += 32) {
                 const int u = e / HQ, q = e - u * HQ;
-                const long long s = (long long)k * kWinS + u;
-                __stcg(dst + u * HQ + q, reinterpret_cast<const float4*>(d0ring + (size_t)(s % Rd) * HP)[q]);
+                __stcg(dst + e, reinterpret_cast<const float4*>(d0ring + ((s0 + u) % Rd) * HP)[q]);
             }
             __threadfence();
             __syncwarp();
             if (lane == 0) red_release_add(A.dcnt, 1u);
-            if (lane == 0 && (A.loss_sum || A.correct)) {
-                for (int u = 0; u < nv; ++u) {
-                    const long long s = (long long)k * kWinS + u;
-                    const float* tc = A.T + win_row(A, s) * C;
-                    const float* pl = pring + (size_t)(s % Rd) * kWinCP;
-                    float loss = 0.0f;
+            WIN_TRACE(s0 + 1, 11);
+            if (stats) {
+                // lane u: loss / hit of sample s0+u (network.cpp:165-168), then
+                // lane 0 accumulates in sample order
+                float loss = 0.0f;
+                unsigned hit = 0;
+                if (lane < nv) {
+                    const float* tc = A.T + myrow * C;
+                    const float* pl = pring + ((s0 + lane) % Rd) * kWinCP;
                     int bp = 0, btg = 0;
+                    float tb = __ldg(tc);
                     for (int o = 0; o < C; ++o) {
                         const float to = __ldg(tc + o);
                         if (to != 0.0f) {
@@ -585,12 +720,20 @@ __device__ __forceinline__ void win_chain(const WinArgs& A, float* sm, const Win
                             loss = ssub(loss, smul(to, logf(q)));
                         }
                         if (pl[o] > pl[bp]) bp = o;
-                        if (to > __ldg(tc + btg)) btg = o;
+                        if (to > tb) {
+                            btg = o;
+                            tb = to;
+                        }
                     }
-                    loss_acc = __dadd_rn(loss_acc, (double)loss);
-                    correct_acc += bp == btg;
+                    hit = bp == btg;
                 }
+                for (int u = 0; u < nv; ++u) {
+                    const float lu = __shfl_sync(0xffffffffu, loss, u);
+                    loss_acc = __dadd_rn(loss_acc, (double)lu);
+                }
+                correct_acc += __popc(__ballot_sync(0xffffffffu, hit != 0));
             }
+            WIN_TRACE(s0 + 2, 11);
         }
         if (lane == 0) {
             if (A.loss_sum) *A.loss_sum = loss_acc;
@@ -600,22 +743,28 @@ __device__ __forceinline__ void win_chain(const WinArgs& A, float* sm, const Win
         // ================= helpers: window corrections =================
         const int w = warp;
         float cf[kWinMaxMine];
-        for (long long s = 0; s < n; ++s) {
-            const long long b = s / kWinS;
-            const long long last = min(n - 1, (b + D) * kWinS - 1);
-            // first owned row >= s+2
-            const long long f0 = s + 2;
-            const long long first = f0 + ((w - (int)(f0 % kWinHelpers)) + kWinHelpers) % kWinHelpers;
+        int sR = 0, sRd = 0;  // s % R, s % Rd
+        auto slot = [&](int r, int s) {  // r % R for s < r < s + R
+            const int x = sR + (r - s);
+            return x >= R ? x - R : x;
+        };
+        for (int s = 0; s < n; ++s) {
+            const int b = s >> 4;
+            const int last = min(n - 1, (b + D) * kWinS - 1);
+            // first owned row >= s+3 (the chain applies d0(s) to rows s+1, s+2)
+            const int f0 = s + 3;
+            const int first = f0 + ((w - (f0 & (kWinHelpers - 1))) & (kWinHelpers - 1));
 #pragma unroll
             for (int i = 0; i < kWinMaxMine; ++i) {
-                const long long r = first + (long long)i * kWinHelpers;
-                cf[i] = r <= last ? __ldg(A.coef + r * QW + (r - s - 1)) : 0.0f;
+                const int r = first + i * kWinHelpers;
+                cf[i] = r <= last ? __ldg(A.coef + (size_t)r * QW + (r - s - 1)) : 0.0f;
             }
-            mbar_wait_cta(MB(kMbD0 + (int)(s % kWinRing)), (uint32_t)((s / kWinRing) & 1), A.error);
-            const float4* dv = reinterpret_cast<const float4*>(d0ring + (size_t)(s % Rd) * HP);
-            // urgent row s+2 first (if owned), then signal it
-            if (first == f0 && f0 <= last) {
-                float4* zr = reinterpret_cast<float4*>(zacc + (size_t)(f0 % R) * HP);
+            mbar_wait_cta(MB(kMbD0 + (s & (kWinRing - 1))), (uint32_t)((s >> 4) & 1), A.error);
+            const float4* dv = reinterpret_cast<const float4*>(d0ring + sRd * HP);
+            // urgent row s+3 first (if owned), then flag it ready
+            const bool urgent = first == f0 && f0 <= last;
+            if (urgent) {
+                float4* zr = reinterpret_cast<float4*>(zacc + slot(f0, s) * HP);
                 for (int q = lane; q < HQ; q += 32) {
                     const float4 d = dv[q];
                     float4 z = zr[q];
@@ -625,16 +774,18 @@ __device__ __forceinline__ void win_chain(const WinArgs& A, float* sm, const Win
                     z.w = fmaf(cf[0], d.w, z.w);
                     zr[q] = z;
                 }
+                __syncwarp();
+                if (lane == 0) st_release_cta_u32(smem_u32(rowflag + slot(f0, s)), (unsigned)(f0 + 1));
+                WIN_TRACE(f0, 7);
             }
-            if (first == f0 && f0 < n) mbar_arrive_cta(MB(kMbRow + (int)(f0 % kWinRing)));
-            const int i0 = first == f0 ? 1 : 0;
+            const int i0 = urgent ? 1 : 0;
             for (int q = lane; q < HQ; q += 32) {
                 const float4 d = dv[q];
 #pragma unroll
                 for (int i = 0; i < kWinMaxMine; ++i) {
-                    const long long r = first + (long long)i * kWinHelpers;
+                    const int r = first + i * kWinHelpers;
                     if (i >= i0 && r <= last) {
-                        float4* zr = reinterpret_cast<float4*>(zacc + (size_t)(r % R) * HP) + q;
+                        float4* zr = reinterpret_cast<float4*>(zacc + slot(r, s) * HP) + q;
                         float4 z = *zr;
                         z.x = fmaf(cf[i], d.x, z.x);
                         z.y = fmaf(cf[i], d.y, z.y);
@@ -644,13 +795,17 @@ __device__ __forceinline__ void win_chain(const WinArgs& A, float* sm, const Win
                     }
                 }
             }
-            // row s has been consumed: its slot now belongs to row s + R
-            if ((int)(s % kWinHelpers) == w) {
-                float4* zr = reinterpret_cast<float4*>(zacc + (size_t)(s % R) * HP);
+            // the chain read row s before publishing d0(s): its slot now
+            // belongs to row s + R (first corrected by block(s)+1's d0)
+            if ((s & (kWinHelpers - 1)) == w) {
+                float4* zr = reinterpret_cast<float4*>(zacc + sR * HP);
                 for (int q = lane; q < HQ; q += 32) zr[q] = make_float4(0.f, 0.f, 0.f, 0.f);
             }
+            if (++sR == R) sR = 0;
+            if (++sRd == Rd) sRd = 0;
         }
     }
+#undef WIN_TRACE
 }
 
 template <int JPL, int CT>

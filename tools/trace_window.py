@@ -1,4 +1,4 @@
-"""Per-phase cycle breakdown of the windowed SGD kernel's critical warp
+"""Per-phase cycle breakdown of the windowed SGD kernel's chain CTA
 (first 64 samples of a 512-sample stream; the second call is measured).
 
     python tools/trace_window.py 784x128x10 [D]
@@ -10,8 +10,8 @@ import numpy as np
 
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 
-PH = ["waits (Y block, row ready)", "z + tanh", "partial logits + reduce", "softmax + d1 bcast",
-      "d0 + publish"]
+PH = ["z + tanh + W1 update(s-1) + W1.t", "partial logits + reduce", "softmax/E + d0",
+      "publish d0", "off-chain (p, d1, biases, shift)", "fetch row s+1"]
 
 
 def main():
@@ -35,13 +35,25 @@ def main():
     dev.sync()
     lines = open(path).read().strip().splitlines()
     print(shp, lines[-65])
-    t = np.array([[int(v) for v in ln.split()] for ln in lines[-64:]], dtype=np.int64)[8:]
+    T_ = np.array([[int(v) for v in ln.split()] for ln in lines[-64:]], dtype=np.int64)
+    t = T_[8:]
+
     def row(name, d):
-        print(f"  {name:28s} median {np.median(d):7.0f}  mean {np.mean(d):7.0f}  max {np.max(d):7.0f}")
+        d = np.asarray(d)
+        print(f"  {name:34s} median {np.median(d):7.0f}  mean {np.mean(d):7.0f}  max {np.max(d):7.0f}")
     for k in range(len(PH)):
         row(PH[k], t[:, k + 1] - t[:, k])
-    row("tail + loop back", t[1:, 0] - t[:-1, len(PH)])
+    row("loop back", t[1:, 0] - t[:-1, 6])
     row("per sample", t[1:, 0] - t[:-1, 0])
+    # helper slack: flag of row r set at T_[r,7]; chain fetches row r at T_[r-1,5]
+    r = np.arange(9, 64)
+    row("helper slack (flag before fetch)", T_[r - 1, 5] - T_[r, 7])
+    for b in (1, 2, 3):
+        s0 = 16 * b
+        print(f"  block {b}: loader wait {T_[s0, 9] - T_[s0, 8]:6d}  stage {T_[s0, 10] - T_[s0, 9]:6d}  "
+              f"ready-before-need {T_[s0 - 1, 5] - T_[s0, 10]:7d}  | publisher: after block end "
+              f"{T_[s0, 11] - T_[s0 + 15, 4]:6d}  publish {T_[s0 + 1, 11] - T_[s0, 11]:6d}  "
+              f"stats {T_[s0 + 2, 11] - T_[s0 + 1, 11]:6d}")
 
 
 if __name__ == "__main__":
