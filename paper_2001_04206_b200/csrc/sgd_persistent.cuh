@@ -59,7 +59,7 @@ struct SgdArgs {
     int debug;                  // diagnostics only: bit 0 = skip the bulk weight pass (timing probe)
 };
 
-constexpr int kTraceSamples = 64, kTracePhases = 12;
+constexpr int kTraceSamples = 64, kTracePhases = 16;
 #define SGD_TRACE(ph)                                                                     \
     do {                                                                                  \
         if (A.trace && (tid == 0 || tid == 32 * (kClWarps - 1)) && rank == 0 &&          \

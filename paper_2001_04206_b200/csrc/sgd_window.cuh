@@ -38,6 +38,7 @@
 //    updated weights and release it.  The weights never leave the chip until
 //    the final write-back.
 // c(s,d) comes from a banded-Gram pre-pass (k_gram_band) over the same stream.
+// (stored forward: c(r, r-s) = coef[s][r-s-1], contiguous for one source s)
 //
 // Numerics: FAST (the forward dot products are reassociated); the weights
 // receive exactly the reference's per-sample update sequence given d0.
@@ -58,7 +59,6 @@ constexpr int kWinRing = 16;                 // d0-ready / row-ready mbarrier ri
 constexpr int kWinBlkRing = 8;               // block-done mbarrier ring (> D)
 constexpr int kWinMaxNR = 4;                 // producer: W0 rows per thread (I <= 4 * 352)
 constexpr int kWinCP = 16;                   // classes padded for the transpose-reduce
-constexpr int kWinMaxMine = (kWinMaxD * kWinS + kWinHelpers - 1) / kWinHelpers;
 
 struct WinArgs {
     int I, H, C, D, P, QW;
@@ -70,7 +70,7 @@ struct WinArgs {
     int base;               // first stream position mod n (no order: row = (base + s) % n)
     float neg_eta;
     float *W0, *b0, *W1, *b1;
-    float* coef;        // [n_steps][QW]: c(s, d) at [s][d-1]
+    float* coef;        // [n_steps][QW]: -eta x(s).x(s+d) at [s][d-1] (forward band)
     float* yring;       // [D+1][S][H]
     float* dring;       // [D+1][S][H]
     unsigned* ycnt;     // [D+1] monotonic producer arrivals per Y slot
@@ -85,7 +85,7 @@ struct WinArgs {
 
 struct WinSmem {
     int HP, R, Rd;
-    size_t zacc, ystage, tstage, c1stage, d0ring, pring, red, d0s, rowflag, mbar, total;
+    size_t zacc, ystage, tstage, coefs, d0ring, pring, red, d0s, rowflag, mbar, total;
     __host__ __device__ WinSmem(int HP_, int D) : HP(HP_) {
         R = D * kWinS;
         Rd = (D + 1) * kWinS;
@@ -98,7 +98,7 @@ struct WinSmem {
         zacc = take((size_t)R * HP);
         ystage = take(2 * (size_t)kWinS * HP);
         tstage = take(2 * kWinS * kWinCP);
-        c1stage = take(4 * kWinS);  // c(s,1) | c(s,2), double-buffered
+        coefs = take((size_t)Rd * D * kWinS);  // forward band rows of source s, slot s % Rd
         d0ring = take((size_t)Rd * HP);
         pring = take((size_t)Rd * kWinCP);
         red = take(kWinCP * 37 > kWinWarps * 64 ? kWinCP * 37 : kWinWarps * 64);
@@ -181,9 +181,10 @@ __device__ __forceinline__ void xpose_step(float* v, int lane, int o) {
 }
 
 // ---------------------------------------------------------------------------
-// Banded Gram pre-pass: coef[s][d-1] = -eta * (x(s) . x(s-d)), d = 1..QW
-// (0 when s-d < 0).  One CTA per 32 stream positions; K streamed through
-// shared memory in 32-float chunks; thread (s, d-group) accumulates QW/8 dots.
+// Banded Gram pre-pass (forward band): coef[s][d-1] = -eta * (x(s) . x(s+d)),
+// d = 1..QW (0 past the end of the stream), so that the coefficients a new
+// d0(s) needs for every later row r = s+d are contiguous.  One CTA per 32
+// stream positions; K streamed through shared memory in 32-float chunks.
 // ---------------------------------------------------------------------------
 constexpr int kGramTS = 32, kGramKC = 32, kGramMaxQW = 96;
 
@@ -192,10 +193,10 @@ __global__ void __launch_bounds__(256) k_gram_band(WinArgs A) {
     __shared__ long long rows[kGramTS + kGramMaxQW];
     const int QW = A.QW, I = A.I;
     const int s0 = blockIdx.x * kGramTS;
-    const int NRW = kGramTS + QW;  // rows s0-QW .. s0+TS-1
+    const int NRW = kGramTS + QW;  // rows s0 .. s0+TS+QW-1
     for (int r = threadIdx.x; r < NRW; r += blockDim.x) {
-        const int s = s0 - QW + r;
-        rows[r] = (s >= 0 && s < A.n_steps) ? win_row(A, s) : -1;
+        const int s = s0 + r;
+        rows[r] = s < A.n_steps ? win_row(A, s) : -1;
     }
     const int sl = threadIdx.x & 31, dg = threadIdx.x >> 5;  // d = dg+1 + 8q
     constexpr int NQ = kGramMaxQW / 8;
@@ -212,11 +213,11 @@ __global__ void __launch_bounds__(256) k_gram_band(WinArgs A) {
         __syncthreads();
 #pragma unroll 4
         for (int kk = 0; kk < kGramKC; ++kk) {
-            const float xv = xs[QW + sl][kk];
+            const float xv = xs[sl][kk];
 #pragma unroll
             for (int q = 0; q < NQ; ++q) {
                 const int d = dg + 1 + 8 * q;
-                if (d <= QW) acc[q] = fmaf(xv, xs[QW + sl - d][kk], acc[q]);
+                if (d <= QW) acc[q] = fmaf(xv, xs[sl + d][kk], acc[q]);
             }
         }
         __syncthreads();
@@ -226,10 +227,11 @@ __global__ void __launch_bounds__(256) k_gram_band(WinArgs A) {
 #pragma unroll
         for (int q = 0; q < NQ; ++q) {
             const int d = dg + 1 + 8 * q;
-            if (d <= QW) A.coef[(size_t)s * QW + (d - 1)] = (s - d >= 0) ? A.neg_eta * acc[q] : 0.0f;
+            if (d <= QW) A.coef[(size_t)s * QW + (d - 1)] = (s + d < A.n_steps) ? A.neg_eta * acc[q] : 0.0f;
         }
     }
 }
+
 // ---------------------------------------------------------------------------
 // Producer CTA: W0 columns [4p, 4p+4) in registers.
 // ---------------------------------------------------------------------------
@@ -395,7 +397,7 @@ __device__ __forceinline__ void win_chain(const WinArgs& A, float* sm, const Win
     float* zacc = sm + L.zacc;
     float* ystage = sm + L.ystage;
     float* tstage = sm + L.tstage;
-    float* c1stage = sm + L.c1stage;
+    float* coefs = sm + L.coefs;
     float* d0ring = sm + L.d0ring;
     float* pring = sm + L.pring;
     float* red = sm + L.red;
@@ -430,7 +432,7 @@ __device__ __forceinline__ void win_chain(const WinArgs& A, float* sm, const Win
         constexpr int CC = CT > 0 ? CT : kWinCP;
         constexpr int NQ = JPL / 4;
         const bool kval = lane < C;  // lane k also owns class k (totals, b1)
-        float w1[JPL][CC], b0r[JPL], dp1[JPL], dp2[JPL], aprev[JPL], d1prev[CC];
+        float w1[JPL][CC], b0r[JPL], dp1[JPL], dp2[JPL], aprev[JPL], ndkp[CC];
 #pragma unroll
         for (int m = 0; m < JPL; ++m) {
             const int j = JPL * lane + m;
@@ -440,14 +442,13 @@ __device__ __forceinline__ void win_chain(const WinArgs& A, float* sm, const Win
             dp1[m] = dp2[m] = aprev[m] = 0.0f;
         }
 #pragma unroll
-        for (int k = 0; k < CC; ++k) d1prev[k] = 0.0f;
+        for (int k = 0; k < CC; ++k) ndkp[k] = 0.0f;
         float b1k = kval ? A.b1[lane] : 0.0f;
         float zl[JPL], al[JPL];
 #pragma unroll
         for (int m = 0; m < JPL; ++m) zl[m] = al[m] = 0.0f;
         // prefetched operands of the next sample
-        float zpre[JPL], tn[CC], c1n = 0.0f, c2n = 0.0f;
-        // s1R = s1 % R (ring slot), kept incrementally: no 64-bit modulo on the chain
+        float zpre[JPL], tn[CC], c1n = 0.0f, c2n = 0.0f, town = 0.0f;
         auto flag_wait = [&](int s1, int s1R) {
             if (s1 < 3) return;  // rows 0..2: the chain applies every correction itself
             const uint32_t fa = smem_u32(rowflag + s1R);
@@ -462,7 +463,8 @@ __device__ __forceinline__ void win_chain(const WinArgs& A, float* sm, const Win
                 }
             }
         };
-        auto fetch_row = [&](int s1, int s1R) {
+        // s1R = s1 % R, s1Rd = s1 % Rd (ring slots), kept incrementally
+        auto fetch_row = [&](int s1, int s1R, int s1Rd) {
             const int b1 = s1 >> 4, u1 = s1 & (kWinS - 1), st1 = b1 & 1;
             if (u1 == 0) mbar_wait_cta(MB(kMbYFull + st1), (uint32_t)((b1 >> 1) & 1), A.error);
             const float4* zr = reinterpret_cast<const float4*>(zacc + s1R * HP) + lane * NQ;
@@ -478,13 +480,15 @@ __device__ __forceinline__ void win_chain(const WinArgs& A, float* sm, const Win
             const float* tr = tstage + (st1 * kWinS + u1) * kWinCP;
 #pragma unroll
             for (int k = 0; k < CC; ++k) tn[k] = tr[k];
-            c1n = c1stage[st1 * kWinS + u1];
-            c2n = c1stage[2 * kWinS + st1 * kWinS + u1];
+            town = kval ? tr[lane] : 0.0f;
+            const int p1 = s1Rd == 0 ? Rd - 1 : s1Rd - 1, p2 = p1 == 0 ? Rd - 1 : p1 - 1;
+            c1n = s1 >= 1 ? coefs[p1 * QW + 0] : 0.0f;  // c(s1, 1) = coef[s1-1][0]
+            c2n = s1 >= 2 ? coefs[p2 * QW + 1] : 0.0f;  // c(s1, 2) = coef[s1-2][1]
         };
-        if (n > 0) fetch_row(0, 0);
+        if (n > 0) fetch_row(0, 0, 0);
         int sR = 0, sRd = 0;  // s % R, s % Rd
-        float* const xr = red;  // [k][36]: partial logits, transposed
-        float* const zt = red + kWinCP * 36;  // class totals (logits) of this sample
+        float* const xr = red;                // [k][36]: partial logits, transposed
+        float* const zt = red + kWinCP * 36;  // class logits of this sample
         for (int s = 0; s < n; ++s) {
             const int b = s >> 4, u = s & (kWinS - 1), st = b & 1;
             WIN_TRACE(s, 0);
@@ -496,18 +500,11 @@ __device__ __forceinline__ void win_chain(const WinArgs& A, float* sm, const Win
                 z[m] = fmaf(c1n, dp1[m], fmaf(c2n, dp2[m], zpre[m])) + b0r[m];
                 a[m] = tanhf(z[m]);
             }
+            // FAST numerics: the W1 update as one FMA, w + (-eta d1) a
 #pragma unroll
             for (int m = 0; m < JPL; ++m)
 #pragma unroll
-                for (int k = 0; k < CC; ++k) w1[m][k] = sgd_apply(w1[m][k], neg_eta, d1prev[k], aprev[m]);
-            float TW[JPL];  // W1(s) t(s)
-#pragma unroll
-            for (int m = 0; m < JPL; ++m) {
-                float acc = 0.0f;
-#pragma unroll
-                for (int k = 0; k < CC; ++k) acc = fmaf(tn[k], w1[m][k], acc);
-                TW[m] = acc;
-            }
+                for (int k = 0; k < CC; ++k) w1[m][k] = fmaf(ndkp[k], aprev[m], w1[m][k]);
             WIN_TRACE(s, 1);
             // -- partial logits -> shared memory (transposed), lane k sums class k
 #pragma unroll
@@ -518,6 +515,7 @@ __device__ __forceinline__ void win_chain(const WinArgs& A, float* sm, const Win
                 xr[k * 36 + lane] = acc;
             }
             __syncwarp();
+            float zown = 0.0f;
             if (kval) {
                 const float4* col = reinterpret_cast<const float4*>(xr + lane * 36);
                 float4 v[8];
@@ -527,36 +525,36 @@ __device__ __forceinline__ void win_chain(const WinArgs& A, float* sm, const Win
 #pragma unroll
                 for (int q = 0; q < 8; ++q) t8[q] = (v[q].x + v[q].y) + (v[q].z + v[q].w);
                 const float tot = ((t8[0] + t8[1]) + (t8[2] + t8[3])) + ((t8[4] + t8[5]) + (t8[6] + t8[7]));
-                zt[lane] = sadd(tot, b1k);
+                zown = sadd(tot, b1k);
+                zt[lane] = zown;
             }
             __syncwarp();
             WIN_TRACE(s, 2);
-            // -- softmax, redundantly in every lane (no cross-lane reduction):
-            //    exact max, C exponentials, sum; E = W1 e overlaps the sum
-            float zk[CC], ek[CC];
+            // -- softmax redundantly in every lane: exact max, C exponentials;
+            //    d1 = p - t;  d0 = (1 - a^2) * (W1 d1) with the pre-update W1
+            float ek[CC];
+            float mx = zt[0];
 #pragma unroll
-            for (int k = 0; k < CC; ++k) zk[k] = k < C ? zt[k] : -INFINITY;
-            float mx = zk[0];
-#pragma unroll
-            for (int k = 1; k < CC; ++k) mx = fmaxf(mx, zk[k]);
-#pragma unroll
-            for (int k = 0; k < CC; ++k) ek[k] = k < C ? expf(zk[k] - mx) : 0.0f;
+            for (int k = 1; k < CC; ++k)
+                if (k < C) mx = fmaxf(mx, zt[k]);
             float sum = 0.0f;
 #pragma unroll
-            for (int k = 0; k < CC; ++k) sum += ek[k];
-            float E[JPL];
+            for (int k = 0; k < CC; ++k) {
+                ek[k] = k < C ? expf(zt[k] - mx) : 0.0f;
+                sum += ek[k];
+            }
+            const float inv = rcp_approx(sum);
+            float d1[CC];
+#pragma unroll
+            for (int k = 0; k < CC; ++k) d1[k] = k < C ? ssub(ek[k] * inv, tn[k]) : 0.0f;
+            float d0v[JPL];
 #pragma unroll
             for (int m = 0; m < JPL; ++m) {
                 float acc = 0.0f;
 #pragma unroll
-                for (int k = 0; k < CC; ++k) acc = fmaf(ek[k], w1[m][k], acc);
-                E[m] = acc;
+                for (int k = 0; k < CC; ++k) acc = fmaf(d1[k], w1[m][k], acc);
+                d0v[m] = tanh_grad(a[m], acc);
             }
-            const float inv = rcp_approx(sum);
-            // d0 = (1 - a^2) * (W1 (p - t)) = (1 - a^2) * (E/sum - W1 t)
-            float d0v[JPL];
-#pragma unroll
-            for (int m = 0; m < JPL; ++m) d0v[m] = tanh_grad(a[m], fmaf(E[m], inv, -TW[m]));
             WIN_TRACE(s, 3);
             float4* dr = reinterpret_cast<float4*>(d0ring + sRd * HP) + lane * NQ;
 #pragma unroll
@@ -564,21 +562,16 @@ __device__ __forceinline__ void win_chain(const WinArgs& A, float* sm, const Win
                 dr[q] = make_float4(d0v[4 * q], d0v[4 * q + 1], d0v[4 * q + 2], d0v[4 * q + 3]);
             mbar_arrive_cta(MB(kMbD0 + (s & (kWinRing - 1))));
             WIN_TRACE(s, 4);
-            // -- off the chain: p, d1, stats, bias updates
+            // -- off the chain: p and d1 of the lane's own class, stats, biases
 #pragma unroll
-            for (int k = 0; k < CC; ++k) d1prev[k] = k < C ? ssub(ek[k] * inv, tn[k]) : 0.0f;
+            for (int k = 0; k < CC; ++k) ndkp[k] = neg_eta * d1[k];
             if (kval) {
-                float pk = 0.0f, dk = 0.0f;
-#pragma unroll
-                for (int k = 0; k < CC; ++k)
-                    if (k == lane) {
-                        pk = ek[k] * inv;
-                        dk = d1prev[k];
-                    }
+                const float pk = expf(zown - mx) * inv;
+                const float dk = ssub(pk, town);
                 pring[sRd * kWinCP + lane] = pk;
-                b1k = sadd(b1k, smul(neg_eta, dk));
+                b1k = fmaf(neg_eta, dk, b1k);
                 if (s == n - 1) {
-                    A.z1[lane] = zt[lane];
+                    A.z1[lane] = zown;
                     A.a1[lane] = pk;
                     A.d1[lane] = dk;
                     A.db1[lane] = smul(neg_eta, dk);
@@ -590,7 +583,7 @@ __device__ __forceinline__ void win_chain(const WinArgs& A, float* sm, const Win
             }
 #pragma unroll
             for (int m = 0; m < JPL; ++m) {
-                b0r[m] = sadd(b0r[m], smul(neg_eta, d0v[m]));
+                b0r[m] = fmaf(neg_eta, d0v[m], b0r[m]);
                 dp2[m] = dp1[m];
                 dp1[m] = d0v[m];
                 aprev[m] = a[m];
@@ -607,7 +600,7 @@ __device__ __forceinline__ void win_chain(const WinArgs& A, float* sm, const Win
             if (++sRd == Rd) sRd = 0;
             if (s + 1 < n) {
                 flag_wait(s + 1, sR);
-                fetch_row(s + 1, sR);
+                fetch_row(s + 1, sR, sRd);
             }
             WIN_TRACE(s, 6);
         }
@@ -616,7 +609,7 @@ __device__ __forceinline__ void win_chain(const WinArgs& A, float* sm, const Win
 #pragma unroll
             for (int m = 0; m < JPL; ++m)
 #pragma unroll
-                for (int k = 0; k < CC; ++k) w1[m][k] = sgd_apply(w1[m][k], neg_eta, d1prev[k], aprev[m]);
+                for (int k = 0; k < CC; ++k) w1[m][k] = fmaf(ndkp[k], aprev[m], w1[m][k]);
 #pragma unroll
             for (int m = 0; m < JPL; ++m) {
                 const int j = JPL * lane + m;
@@ -635,15 +628,41 @@ __device__ __forceinline__ void win_chain(const WinArgs& A, float* sm, const Win
             if (kval) A.b1[lane] = b1k;
         }
     } else if (warp == kWinLoad) {
-        // ================= loader: Y(b), targets, c(s,1) =================
+        // ================= loader: Y(b), targets, coefficient rows =================
+        // Forward band rows of block b (its own sources) go to ring slots
+        // s % Rd with Y(b): block b-D-1's slots, long retired.
+        constexpr int kCoefMax = kWinS * kWinMaxD * kWinS / 4 / 32;  // float4 per lane
+        const int QW4 = QW >> 2;
+        auto coef_load = [&](int blk, float4* v) {
+            const int r0 = blk * kWinS, rows = max(0, min(kWinS, n - r0));
+#pragma unroll
+            for (int q = 0; q < kCoefMax; ++q) {
+                const int e = lane + 32 * q;
+                if (e < rows * QW4) {
+                    const int u = e / QW4, c = e - u * QW4;
+                    v[q] = __ldg(reinterpret_cast<const float4*>(A.coef + (size_t)(r0 + u) * QW) + c);
+                }
+            }
+        };
+        auto coef_store = [&](int blk, const float4* v) {
+            const int r0 = blk * kWinS, rows = max(0, min(kWinS, n - r0));
+#pragma unroll
+            for (int q = 0; q < kCoefMax; ++q) {
+                const int e = lane + 32 * q;
+                if (e < rows * QW4) {
+                    const int u = e / QW4, c = e - u * QW4;
+                    reinterpret_cast<float4*>(coefs + ((r0 + u) % Rd) * QW)[c] = v[q];
+                }
+            }
+        };
         for (int b = 0; b < nblk; ++b) {
             const int st = b & 1;
             const int s0 = b * kWinS;
             const int nv = min(kWinS, n - s0);
-            // independent of the producers: rows, targets, c(s,1)
+            // independent of the producers: rows, targets, coefficient rows
             const long long myrow = lane < nv ? win_row(A, s0 + lane) : 0;
-            const float c1v = lane < nv ? __ldg(A.coef + (s0 + lane) * QW) : 0.0f;
-            const float c2v = lane < nv ? __ldg(A.coef + (s0 + lane) * QW + 1) : 0.0f;
+            float4 cv[kCoefMax];
+            coef_load(b, cv);
             float tv[kWinS * kWinCP / 32];
 #pragma unroll
             for (int q = 0; q < kWinS * kWinCP / 32; ++q) {
@@ -655,6 +674,7 @@ __device__ __forceinline__ void win_chain(const WinArgs& A, float* sm, const Win
             if (b >= 2) mbar_wait_cta(MB(kMbYFree + st), (uint32_t)(((b - 2) >> 1) & 1), A.error);
             spin_geq(A.ycnt + (b % YR), (unsigned)(A.P * (b / YR + 1)), A.error);
             WIN_TRACE(s0, 9);
+            coef_store(b, cv);
             const float4* src = reinterpret_cast<const float4*>(A.yring + (size_t)(b % YR) * kWinS * H);
             float4* dst = reinterpret_cast<float4*>(ystage + (size_t)st * kWinS * HP);
             for (int e0 = 0; e0 < nv * HQ; e0 += 32 * 8) {
@@ -675,10 +695,6 @@ __device__ __forceinline__ void win_chain(const WinArgs& A, float* sm, const Win
             }
 #pragma unroll
             for (int q = 0; q < kWinS * kWinCP / 32; ++q) tstage[st * kWinS * kWinCP + lane + 32 * q] = tv[q];
-            if (lane < kWinS) {
-                c1stage[st * kWinS + lane] = c1v;
-                c1stage[2 * kWinS + st * kWinS + lane] = c2v;
-            }
             mbar_arrive_cta(MB(kMbYFull + st));
             WIN_TRACE(s0, 10);
         }
@@ -741,57 +757,84 @@ __device__ __forceinline__ void win_chain(const WinArgs& A, float* sm, const Win
         }
     } else {
         // ================= helpers: window corrections =================
+        // d0(s) goes to every pending row r in [s+3, last] owned by this warp
+        // (r = w mod NH): z(r) += c(r, r-s) d0(s), c from the forward band row
+        // of source s.  Rows are visited in ascending order, so an owned row
+        // s+3 (the next one the chain fetches) is flagged first.
         const int w = warp;
-        float cf[kWinMaxMine];
         int sR = 0, sRd = 0;  // s % R, s % Rd
-        auto slot = [&](int r, int s) {  // r % R for s < r < s + R
-            const int x = sR + (r - s);
-            return x >= R ? x - R : x;
-        };
         for (int s = 0; s < n; ++s) {
             const int b = s >> 4;
             const int last = min(n - 1, (b + D) * kWinS - 1);
-            // first owned row >= s+3 (the chain applies d0(s) to rows s+1, s+2)
             const int f0 = s + 3;
             const int first = f0 + ((w - (f0 & (kWinHelpers - 1))) & (kWinHelpers - 1));
-#pragma unroll
-            for (int i = 0; i < kWinMaxMine; ++i) {
-                const int r = first + i * kWinHelpers;
-                cf[i] = r <= last ? __ldg(A.coef + (size_t)r * QW + (r - s - 1)) : 0.0f;
-            }
             mbar_wait_cta(MB(kMbD0 + (s & (kWinRing - 1))), (uint32_t)((s >> 4) & 1), A.error);
+            if ((s & (kWinHelpers - 1)) == w) WIN_TRACE(s, 12);
             const float4* dv = reinterpret_cast<const float4*>(d0ring + sRd * HP);
-            // urgent row s+3 first (if owned), then flag it ready
-            const bool urgent = first == f0 && f0 <= last;
-            if (urgent) {
-                float4* zr = reinterpret_cast<float4*>(zacc + slot(f0, s) * HP);
-                for (int q = lane; q < HQ; q += 32) {
-                    const float4 d = dv[q];
-                    float4 z = zr[q];
-                    z.x = fmaf(cf[0], d.x, z.x);
-                    z.y = fmaf(cf[0], d.y, z.y);
-                    z.z = fmaf(cf[0], d.z, z.z);
-                    z.w = fmaf(cf[0], d.w, z.w);
-                    zr[q] = z;
-                }
-                __syncwarp();
-                if (lane == 0) st_release_cta_u32(smem_u32(rowflag + slot(f0, s)), (unsigned)(f0 + 1));
-                WIN_TRACE(f0, 7);
-            }
-            const int i0 = urgent ? 1 : 0;
-            for (int q = lane; q < HQ; q += 32) {
-                const float4 d = dv[q];
+            const float* cs = coefs + sRd * QW - s - 1;  // cs[r] = c(r, r-s)
+            // this lane's d0 quads, once per sample
+            constexpr int NQH = JPL / 4;  // float4 per lane per row (HP = 128 JPL / 4 ... )
+            float4 dq[NQH];
 #pragma unroll
-                for (int i = 0; i < kWinMaxMine; ++i) {
-                    const int r = first + i * kWinHelpers;
-                    if (i >= i0 && r <= last) {
-                        float4* zr = reinterpret_cast<float4*>(zacc + slot(r, s) * HP) + q;
-                        float4 z = *zr;
-                        z.x = fmaf(cf[i], d.x, z.x);
-                        z.y = fmaf(cf[i], d.y, z.y);
-                        z.z = fmaf(cf[i], d.z, z.z);
-                        z.w = fmaf(cf[i], d.w, z.w);
-                        *zr = z;
+            for (int i = 0; i < NQH; ++i) {
+                const int q = lane + 32 * i;
+                dq[i] = q < HQ ? dv[q] : make_float4(0.f, 0.f, 0.f, 0.f);
+            }
+            auto upd = [&](float4* zr, float c) {
+#pragma unroll
+                for (int i = 0; i < NQH; ++i) {
+                    const int q = lane + 32 * i;
+                    if (q < HQ) {
+                        float4 z = zr[q];
+                        z.x = fmaf(c, dq[i].x, z.x);
+                        z.y = fmaf(c, dq[i].y, z.y);
+                        z.z = fmaf(c, dq[i].z, z.z);
+                        z.w = fmaf(c, dq[i].w, z.w);
+                        zr[q] = z;
+                    }
+                }
+            };
+            int slot = sR + (first - s);
+            if (slot >= R) slot -= R;
+            int r = first;
+            if (r == f0 && r <= last) {  // the next row the chain fetches: flag it first
+                upd(reinterpret_cast<float4*>(zacc + slot * HP), cs[r]);
+                __syncwarp();
+                if (lane == 0) st_release_cta_u32(smem_u32(rowflag + slot), (unsigned)(f0 + 1));
+                WIN_TRACE(f0, 7);
+                r += kWinHelpers;
+                slot += kWinHelpers;
+                if (slot >= R) slot -= R;
+            }
+            // the rest, 4 independent rows per batch
+            for (; r <= last; r += 4 * kWinHelpers) {
+                int sl[4];
+                float c[4];
+#pragma unroll
+                for (int k = 0; k < 4; ++k) {
+                    sl[k] = slot;
+                    c[k] = r + k * kWinHelpers <= last ? cs[r + k * kWinHelpers] : 0.0f;
+                    slot += kWinHelpers;
+                    if (slot >= R) slot -= R;
+                }
+#pragma unroll
+                for (int i = 0; i < NQH; ++i) {
+                    const int q = lane + 32 * i;
+                    if (q < HQ) {
+                        float4 z[4];
+#pragma unroll
+                        for (int k = 0; k < 4; ++k)
+                            if (r + k * kWinHelpers <= last) z[k] = reinterpret_cast<const float4*>(zacc + sl[k] * HP)[q];
+#pragma unroll
+                        for (int k = 0; k < 4; ++k) {
+                            if (r + k * kWinHelpers <= last) {
+                                z[k].x = fmaf(c[k], dq[i].x, z[k].x);
+                                z[k].y = fmaf(c[k], dq[i].y, z[k].y);
+                                z[k].z = fmaf(c[k], dq[i].z, z[k].z);
+                                z[k].w = fmaf(c[k], dq[i].w, z[k].w);
+                                reinterpret_cast<float4*>(zacc + sl[k] * HP)[q] = z[k];
+                            }
+                        }
                     }
                 }
             }
@@ -801,6 +844,7 @@ __device__ __forceinline__ void win_chain(const WinArgs& A, float* sm, const Win
                 float4* zr = reinterpret_cast<float4*>(zacc + sR * HP);
                 for (int q = lane; q < HQ; q += 32) zr[q] = make_float4(0.f, 0.f, 0.f, 0.f);
             }
+            if ((s & (kWinHelpers - 1)) == w) WIN_TRACE(s, 13);
             if (++sR == R) sR = 0;
             if (++sRd == Rd) sRd = 0;
         }

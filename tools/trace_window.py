@@ -48,6 +48,9 @@ def main():
     # helper slack: flag of row r set at T_[r,7]; chain fetches row r at T_[r-1,5]
     r = np.arange(9, 64)
     row("helper slack (flag before fetch)", T_[r - 1, 5] - T_[r, 7])
+    row("helper wake after publish", t[:, 12] - t[:, 4])
+    row("helper rows pass", t[:, 13] - t[:, 12])
+    row("helper done before next publish", t[1:, 4] - t[:-1, 13])
     for b in (1, 2, 3):
         s0 = 16 * b
         print(f"  block {b}: loader wait {T_[s0, 9] - T_[s0, 8]:6d}  stage {T_[s0, 10] - T_[s0, 9]:6d}  "
