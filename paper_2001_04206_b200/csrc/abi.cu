@@ -288,6 +288,7 @@ struct SgdPlan {
     bool ok = false;
     bool window = false;   // delayed-base windowed kernel (chain CTA + W0 producers)
     int jpl = 4, D = 3;    // window plan: hidden units per chain lane, lag in blocks
+    int ks = 1, rpc = 0;   // window plan: producer row splits per column quad, rows per split
     bool cluster = false;  // single thread-block cluster, DSMEM exchange
     bool w0_smem = true;   // grid plan: W0 slices resident in shared memory
     bool col4 = false;     // grid streamed plan: 128-bit column quads
@@ -358,14 +359,25 @@ SgdPlan plan_persistent(lane_b200_net* net) {
         int D = 3;
         if (const char* e = std::getenv("LANE_B200_SGD_WIN_D")) D = std::max(2, std::min(std::atoi(e), kWinMaxD));
         const int jpl = H <= 128 ? 4 : 8;
-        const WinSmem L(32 * jpl, D);
-        if (H % 4 == 0 && H <= 256 && C <= kWinCP && I <= kWinMaxNR * kWinThreads &&
-            1 + H / 4 <= c->sm_count && L.total <= c->max_smem_optin) {
+        // producers: H/4 column quads x KS row splits, as many SMs as fit (<= 4
+        // splits, >= 32 rows each); rows per split a multiple of 4 (cp.async 16 B)
+        const int quads = std::max(1, H / 4);
+        int ks = std::max(1, std::min({4, (c->sm_count - 1) / quads, std::max(1, I / 32)}));
+        if (const char* e = std::getenv("LANE_B200_SGD_WIN_KS")) ks = std::max(1, std::min(std::atoi(e), 4));
+        const int rpc = (((I + ks - 1) / ks) + 3) & ~3;
+        ks = (I + rpc - 1) / rpc;
+        const WinSmem L(32 * jpl, D, ks, H);
+        const ProdSmem PL(rpc, D);
+        const size_t smem = std::max(L.total, PL.total);
+        if (H % 4 == 0 && H <= 256 && C <= kWinCP && rpc <= kWinMaxNR * kWinThreads &&
+            1 + quads * ks <= c->sm_count && smem <= c->max_smem_optin) {
             p.ok = p.window = true;
             p.jpl = jpl;
             p.D = D;
-            p.G = 1 + H / 4;
-            p.smem = L.total;
+            p.ks = ks;
+            p.rpc = rpc;
+            p.G = 1 + quads * ks;
+            p.smem = smem;
             return p;
         }
         if (mode) return p;
@@ -546,17 +558,20 @@ void launch_window(lane_b200_net* net, const SgdPlan& P, const float* X, const f
     const int H = static_cast<int>(L0.O);
     const int QW = P.D * kWinS;
     ensure(net->win_coef, net->win_coef_count, n_steps * QW);
-    const size_t ring = 2ull * (P.D + 1) * kWinS * H;
+    const size_t yring = static_cast<size_t>(P.D + 1) * P.ks * kWinS * H;  // partial Y per row split
+    const size_t dring = static_cast<size_t>(P.D + 1) * kWinS * H;
     const size_t cnt_words = 64;  // ycnt[D+1] | dcnt (32-bit), padded
-    ensure(net->win_ring, net->win_ring_count, ring + cnt_words);
-    unsigned* cnt = reinterpret_cast<unsigned*>(net->win_ring + ring);
+    ensure(net->win_ring, net->win_ring_count, yring + dring + cnt_words);
+    unsigned* cnt = reinterpret_cast<unsigned*>(net->win_ring + yring + dring);
     LANE_CUDA(cudaMemsetAsync(cnt, 0, cnt_words * sizeof(float), c->stream));
     WinArgs A{};
     A.I = static_cast<int>(net->input_width);
     A.H = H;
     A.C = static_cast<int>(net->classes);
     A.D = P.D;
-    A.P = H / 4;
+    A.KS = P.ks;
+    A.RPC = P.rpc;
+    A.P = (H / 4) * P.ks;
     A.QW = QW;
     A.X = X;
     A.T = T;
@@ -573,7 +588,7 @@ void launch_window(lane_b200_net* net, const SgdPlan& P, const float* X, const f
     A.b1 = L1.buf[LANE_BUF_B];
     A.coef = net->win_coef;
     A.yring = net->win_ring;
-    A.dring = net->win_ring + ring / 2;
+    A.dring = net->win_ring + yring;
     A.ycnt = cnt;
     A.dcnt = cnt + 32;
     A.x0 = L0.buf[LANE_BUF_INPUTS];
@@ -594,6 +609,7 @@ void launch_window(lane_b200_net* net, const SgdPlan& P, const float* X, const f
     if (trace_path) {
         A.trace = static_cast<unsigned long long*>(dev_alloc(trace_n * 8));
         LANE_CUDA(cudaMemsetAsync(A.trace, 0, trace_n * 8, c->stream));
+        if (const char* e = std::getenv("LANE_B200_SGD_TRACE_BASE")) A.trace_base = std::atoi(e);
     }
     // banded Gram pre-pass
     k_gram_band<<<static_cast<unsigned>((n_steps + kGramTS - 1) / kGramTS), 256, 0, c->stream>>>(A);

@@ -53,7 +53,10 @@ constexpr int kWinS = 16;                    // samples per block
 constexpr int kWinHelpers = 4;               // helper warps
 constexpr int kWinWarps = kWinHelpers + 3;   // + publisher, loader, critical
 constexpr int kWinThreads = 32 * kWinWarps;  // 352
-constexpr int kWinPub = kWinHelpers, kWinLoad = kWinHelpers + 1, kWinCrit = kWinHelpers + 2;
+// Warp roles.  Warps share a sub-partition (SMSP) when their ids are equal mod
+// 4; the critical warp is warp 3, alone on its SMSP (7 warps: 3 | 0,4 | 1,5 | 2,6).
+constexpr int kWinCrit = 3, kWinPub = 5, kWinLoad = 6;
+__device__ __forceinline__ int win_helper_index(int warp) { return warp < 3 ? warp : 3; }  // warps 0,1,2,4
 constexpr int kWinMaxD = 6;
 constexpr int kWinRing = 16;                 // d0-ready / row-ready mbarrier rings
 constexpr int kWinBlkRing = 8;               // block-done mbarrier ring (> D)
@@ -62,6 +65,7 @@ constexpr int kWinCP = 16;                   // classes padded for the transpose
 
 struct WinArgs {
     int I, H, C, D, P, QW;
+    int KS, RPC;  // producers: row splits per column quad, rows per split (P = H/4 * KS)
     const float* X;
     const float* T;
     const uint32_t* order;  // stream order (offset to this launch) or null
@@ -71,7 +75,7 @@ struct WinArgs {
     float neg_eta;
     float *W0, *b0, *W1, *b1;
     float* coef;        // [n_steps][QW]: -eta x(s).x(s+d) at [s][d-1] (forward band)
-    float* yring;       // [D+1][S][H]
+    float* yring;       // [D+1][KS][S][H] partial Y per row split
     float* dring;       // [D+1][S][H]
     unsigned* ycnt;     // [D+1] monotonic producer arrivals per Y slot
     unsigned* dcnt;     // published d0 blocks
@@ -81,12 +85,13 @@ struct WinArgs {
     unsigned long long* correct;
     int* error;
     unsigned long long* trace;
+    int trace_base;  // first traced stream position
 };
 
 struct WinSmem {
     int HP, R, Rd;
     size_t zacc, ystage, tstage, coefs, d0ring, pring, red, d0s, rowflag, mbar, total;
-    __host__ __device__ WinSmem(int HP_, int D) : HP(HP_) {
+    __host__ __device__ WinSmem(int HP_, int D, int KS, int H) : HP(HP_) {
         R = D * kWinS;
         Rd = (D + 1) * kWinS;
         size_t o = 0;
@@ -96,7 +101,7 @@ struct WinSmem {
             return at;
         };
         zacc = take((size_t)R * HP);
-        ystage = take(2 * (size_t)kWinS * HP);
+        ystage = take(2 * (size_t)KS * kWinS * H);  // [buffer][ks][u][H] (TMA bulk copies)
         tstage = take(2 * kWinS * kWinCP);
         coefs = take((size_t)Rd * D * kWinS);  // forward band rows of source s, slot s % Rd
         d0ring = take((size_t)Rd * HP);
@@ -233,47 +238,94 @@ __global__ void __launch_bounds__(256) k_gram_band(WinArgs A) {
 }
 
 // ---------------------------------------------------------------------------
-// Producer CTA: W0 columns [4p, 4p+4) in registers.
+// Producer CTAs.  CTA (pc, ks) owns W0 columns [4pc, 4pc+4) x rows
+// [ks*RPC, ks*RPC + RPC) in registers for the whole stream.  The X rows of
+// the last D+2 blocks of its row range sit in a shared-memory ring, filled by
+// cp.async one iteration ahead: block k's rows arrive for Y(k) (iteration
+// k-D) and are reused for block k's weight update (iteration k).  Per block
+// k: acquire d0 of block k, apply its S per-sample updates with the
+// reference's exact rounding (w + (-eta * (d0 * x)), sample by sample), then
+// publish the partial Y(k+D) of this row range; the chain sums the KS
+// partials of a column quad in a fixed order.
 // ---------------------------------------------------------------------------
-__device__ __forceinline__ void win_producer(const WinArgs& A, float* sm, const WinSmem& L) {
+struct ProdSmem {
+    int RPCp, NB;
+    size_t xr, d0s, red, total;
+    __host__ __device__ ProdSmem(int RPC, int D) {
+        RPCp = (RPC + 3) & ~3;
+        NB = D + 2;
+        size_t o = 0;
+        auto take = [&](size_t nf) {
+            size_t at = o;
+            o += (nf + 3) & ~size_t(3);
+            return at;
+        };
+        xr = take((size_t)NB * kWinS * RPCp);
+        d0s = take(kWinS * 4);
+        red = take(kWinWarps * 64);
+        total = o * sizeof(float);
+    }
+};
+
+__device__ __forceinline__ void win_producer(const WinArgs& A, float* sm) {
     const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
-    const int I = A.I, H = A.H, D = A.D;
-    const int p = blockIdx.x - 1, col = 4 * p;
+    const int I = A.I, H = A.H, D = A.D, KS = A.KS, RPC = A.RPC;
+    const int pc = (blockIdx.x - 1) / KS, ks = (blockIdx.x - 1) - pc * KS;
+    const int col = 4 * pc, i0 = ks * RPC, nr = max(0, min(I, i0 + RPC) - i0);
     const int n = A.n_steps;
     const int nblk = (n + kWinS - 1) / kWinS;
     const int YR = D + 1, DR = D + 1;
     const float neg_eta = A.neg_eta;
+    const ProdSmem L(RPC, D);
+    const int RPCp = L.RPCp, NB = L.NB;
+    float* xr = sm + L.xr;
     float* red = sm + L.red;
     float4* d0s = reinterpret_cast<float4*>(sm + L.d0s);
-    __shared__ long long rk[kWinS], rn[kWinS];  // dataset rows of the update / Y blocks
+    const bool vec = ((I & 3) == 0) && ((i0 & 3) == 0) && ((nr & 3) == 0) &&
+                     ((reinterpret_cast<uintptr_t>(A.X) & 15) == 0);
 
     float4 w[kWinMaxNR];
 #pragma unroll
     for (int m = 0; m < kWinMaxNR; ++m) {
-        const int i = tid + kWinThreads * m;
-        w[m] = i < I ? *reinterpret_cast<const float4*>(A.W0 + (size_t)i * H + col)
-                     : make_float4(0.f, 0.f, 0.f, 0.f);
+        const int li = tid + kWinThreads * m;
+        w[m] = li < nr ? *reinterpret_cast<const float4*>(A.W0 + (size_t)(i0 + li) * H + col)
+                       : make_float4(0.f, 0.f, 0.f, 0.f);
     }
-
-    // Y(b)[u][col..col+3] = x(row_u) . W0[:, col..col+3] with the current registers
-    auto compute_y = [&](int b) {
-        const int nv = min(kWinS, n - b * kWinS);
+    // X rows [i0, i0+nr) of block blk -> ring slot blk % NB (cp.async, no wait)
+    auto prefetch = [&](int blk) {
+        float* dst = xr + (size_t)(blk % NB) * kWinS * RPCp;
+        const int s0 = blk * kWinS, nv = min(kWinS, n - s0);
+        if (vec) {
+            const int nq = nr >> 2;
+            for (int e = tid; e < nv * nq; e += kWinThreads) {
+                const int u = e / nq, q = e - u * nq;
+                cp_async16(dst + u * RPCp + 4 * q, A.X + win_row(A, s0 + u) * I + i0 + 4 * q);
+            }
+        } else {
+            for (int e = tid; e < nv * nr; e += kWinThreads) {
+                const int u = e / nr, q = e - u * nr;
+                cp_async4(dst + u * RPCp + q, A.X + win_row(A, s0 + u) * I + i0 + q);
+            }
+        }
+    };
+    // partial Y(blk)[u][col..col+3] over this row range, from the current registers
+    auto compute_y = [&](int blk) {
+        const float* xb = xr + (size_t)(blk % NB) * kWinS * RPCp;
+        const int nv = min(kWinS, n - blk * kWinS);
         float acc[4 * kWinS];
 #pragma unroll
         for (int e = 0; e < 4 * kWinS; ++e) acc[e] = 0.0f;
 #pragma unroll
         for (int m = 0; m < kWinMaxNR; ++m) {
-            const int i = tid + kWinThreads * m;
-            if (i < I) {
-                float xv[kWinS];
-#pragma unroll
-                for (int u = 0; u < kWinS; ++u) xv[u] = u < nv ? __ldg(A.X + rn[u] * I + i) : 0.0f;
+            const int li = tid + kWinThreads * m;
+            if (li < nr) {
 #pragma unroll
                 for (int u = 0; u < kWinS; ++u) {
-                    acc[4 * u + 0] = fmaf(xv[u], w[m].x, acc[4 * u + 0]);
-                    acc[4 * u + 1] = fmaf(xv[u], w[m].y, acc[4 * u + 1]);
-                    acc[4 * u + 2] = fmaf(xv[u], w[m].z, acc[4 * u + 2]);
-                    acc[4 * u + 3] = fmaf(xv[u], w[m].w, acc[4 * u + 3]);
+                    const float x = u < nv ? xb[u * RPCp + li] : 0.0f;
+                    acc[4 * u + 0] = fmaf(x, w[m].x, acc[4 * u + 0]);
+                    acc[4 * u + 1] = fmaf(x, w[m].y, acc[4 * u + 1]);
+                    acc[4 * u + 2] = fmaf(x, w[m].z, acc[4 * u + 2]);
+                    acc[4 * u + 3] = fmaf(x, w[m].w, acc[4 * u + 3]);
                 }
             }
         }
@@ -291,77 +343,63 @@ __device__ __forceinline__ void win_producer(const WinArgs& A, float* sm, const 
 #pragma unroll
             for (int q = 0; q < kWinWarps; ++q) y += red[q * 64 + tid];
             const int u = tid >> 2, c = tid & 3;
-            if (u < nv) __stcg(A.yring + ((size_t)(b % YR) * kWinS + u) * H + col + c, y);
-            __threadfence();
-        }
-        __syncthreads();
-        if (tid == 0) red_release_add(A.ycnt + (b % YR), 1u);
-    };
-    auto stage_rows = [&](long long* dst, int b) {
-        if (tid < kWinS) {
-            const int s = b * kWinS + tid;
-            dst[tid] = s < n ? win_row(A, s) : 0;
+            if (u < nv) __stcg(A.yring + (((size_t)(blk % YR) * KS + ks) * kWinS + u) * H + col + c, y);
+            // each of the two writer warps releases its own stores
+            __syncwarp();
+            if (lane == 0) red_release_add(A.ycnt + (blk % YR), 1u);
         }
     };
 
     const int npro = min(D, nblk);
-    for (int b = 0; b < npro; ++b) {
-        stage_rows(rn, b);
-        __syncthreads();
-        compute_y(b);
+    for (int blk = 0; blk <= npro && blk < nblk; ++blk) prefetch(blk);
+    cp_async_commit();
+    cp_async_wait<0>();
+    __syncthreads();
+    for (int blk = 0; blk < npro; ++blk) {
+        compute_y(blk);
+        __syncthreads();  // red reuse
     }
     for (int k = 0; k < nblk; ++k) {
-        const bool do_y = k + D < nblk;
-        // rows of this block's update and of Y(k+D) do not depend on d0
-        stage_rows(rk, k);
-        if (do_y && tid >= 32 && tid < 32 + kWinS) {
-            const int s = (k + D) * kWinS + (tid - 32);
-            rn[tid - 32] = s < n ? win_row(A, s) : 0;
-        }
+        const int nv = min(kWinS, n - k * kWinS);
+        if (k + D + 1 < nblk) prefetch(k + D + 1);  // slot of block k-1: retired
+        cp_async_commit();
         if (tid == 0) spin_geq(A.dcnt, (unsigned)(k + 1), A.error);
         __syncthreads();
-        const int nv = min(kWinS, n - k * kWinS);
-        if (tid < kWinS) {
+        if (tid < kWinS)
             d0s[tid] = tid < nv ? __ldcg(reinterpret_cast<const float4*>(
                                       A.dring + ((size_t)(k % DR) * kWinS + tid) * H + col))
                                 : make_float4(0.f, 0.f, 0.f, 0.f);
-        }
-        // x values of the first row group (independent of d0): issued before
-        // the barrier; the barrier itself is unconditional (never divergent)
-        float xv0[kWinS];
-#pragma unroll
-        for (int u = 0; u < kWinS; ++u) xv0[u] = (tid < I && u < nv) ? __ldg(A.X + rk[u] * I + tid) : 0.0f;
-        __syncthreads();  // d0s visible
+        cp_async_wait<1>();  // block k+D's rows (prefetched last iteration) have landed
+        __syncthreads();
+        // the S per-sample updates, reference rounding, in sample order
+        const float* xb = xr + (size_t)(k % NB) * kWinS * RPCp;
 #pragma unroll
         for (int m = 0; m < kWinMaxNR; ++m) {
-            const int i = tid + kWinThreads * m;
-            if (i < I) {
-                float xv[kWinS];
-#pragma unroll
-                for (int u = 0; u < kWinS; ++u)
-                    xv[u] = m == 0 ? xv0[u] : (u < nv ? __ldg(A.X + rk[u] * I + i) : 0.0f);
-                // the S per-sample updates, reference rounding, in sample order
+            const int li = tid + kWinThreads * m;
+            if (li < nr) {
 #pragma unroll
                 for (int u = 0; u < kWinS; ++u) {
                     if (u < nv) {
                         const float4 d = d0s[u];
-                        w[m].x = sgd_apply(w[m].x, neg_eta, d.x, xv[u]);
-                        w[m].y = sgd_apply(w[m].y, neg_eta, d.y, xv[u]);
-                        w[m].z = sgd_apply(w[m].z, neg_eta, d.z, xv[u]);
-                        w[m].w = sgd_apply(w[m].w, neg_eta, d.w, xv[u]);
+                        const float x = xb[u * RPCp + li];
+                        w[m].x = sgd_apply(w[m].x, neg_eta, d.x, x);
+                        w[m].y = sgd_apply(w[m].y, neg_eta, d.y, x);
+                        w[m].z = sgd_apply(w[m].z, neg_eta, d.z, x);
+                        w[m].w = sgd_apply(w[m].w, neg_eta, d.w, x);
                     }
                 }
             }
         }
-        if (do_y) compute_y(k + D);
-        __syncthreads();  // rk/rn/d0s reuse
+        if (k + D < nblk) compute_y(k + D);
+        __syncthreads();  // ring slot / d0s / red reuse
     }
+    cp_async_wait<0>();
 #pragma unroll
     for (int m = 0; m < kWinMaxNR; ++m) {
-        const int i = tid + kWinThreads * m;
-        if (i < I) *reinterpret_cast<float4*>(A.W0 + (size_t)i * H + col) = w[m];
+        const int li = tid + kWinThreads * m;
+        if (li < nr) *reinterpret_cast<float4*>(A.W0 + (size_t)(i0 + li) * H + col) = w[m];
     }
-    if (p == 0 && n > 0) {
+    if (blockIdx.x == 1 && n > 0) {
         const float* xl = A.X + win_row(A, n - 1) * I;
         for (int i = tid; i < I; i += kWinThreads) A.x0[i] = xl[i];
     }
@@ -387,8 +425,8 @@ __device__ __forceinline__ float rcp_approx(float x) {
 template <int JPL, int CT>
 __device__ __forceinline__ void win_chain(const WinArgs& A, float* sm, const WinSmem& L) {
     const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
-    const int H = A.H, D = A.D, HP = L.HP, R = L.R, Rd = L.Rd, QW = A.QW;
-    const int HQ = H >> 2, HPQ = HP >> 2;  // float4 per row (used / padded)
+    const int H = A.H, D = A.D, HP = L.HP, R = L.R, Rd = L.Rd, QW = A.QW, KS = A.KS;
+    const int HQ = H >> 2;  // float4 per row
     const int C = CT > 0 ? CT : A.C;
     const int n = (int)A.n_steps;  // <= 2^18 per launch (host chunks the stream)
     const int nblk = (n + kWinS - 1) / kWinS;
@@ -407,13 +445,13 @@ __device__ __forceinline__ void win_chain(const WinArgs& A, float* sm, const Win
     unsigned long long* const trace = A.trace;
 #define WIN_TRACE(s_, ph)                                                                \
     do {                                                                                 \
-        if (trace && lane == 0 && (s_) < kTraceSamples)                                  \
-            trace[(s_) * kTracePhases + (ph)] = clock64();                               \
+        if (trace && lane == 0 && (unsigned)((s_) - A.trace_base) < kTraceSamples)       \
+            trace[((s_) - A.trace_base) * kTracePhases + (ph)] = clock64();              \
     } while (0)
 
     // ---- prologue: zero the rings, init the barriers
     for (int e = tid; e < R * HP; e += kWinThreads) zacc[e] = 0.0f;
-    for (int e = tid; e < 2 * kWinS * HP; e += kWinThreads) ystage[e] = 0.0f;
+    for (int e = tid; e < 2 * A.KS * kWinS * H; e += kWinThreads) ystage[e] = 0.0f;
     for (int e = tid; e < 2 * kWinS * kWinCP; e += kWinThreads) tstage[e] = 0.0f;
     for (int e = tid; e < Rd * HP; e += kWinThreads) d0ring[e] = 0.0f;
     for (int e = tid; e < R; e += kWinThreads) rowflag[e] = 0u;
@@ -448,7 +486,9 @@ __device__ __forceinline__ void win_chain(const WinArgs& A, float* sm, const Win
 #pragma unroll
         for (int m = 0; m < JPL; ++m) zl[m] = al[m] = 0.0f;
         // prefetched operands of the next sample
-        float zpre[JPL], tn[CC], c1n = 0.0f, c2n = 0.0f, town = 0.0f;
+        constexpr int kMaxKS = 4;
+        float4 zraw[NQ], yraw[kMaxKS][NQ];  // row s+1: window sums and the KS partial Y quads
+        float tn[CC], c1n = 0.0f, c2n = 0.0f, town = 0.0f;
         auto flag_wait = [&](int s1, int s1R) {
             if (s1 < 3) return;  // rows 0..2: the chain applies every correction itself
             const uint32_t fa = smem_u32(rowflag + s1R);
@@ -467,15 +507,17 @@ __device__ __forceinline__ void win_chain(const WinArgs& A, float* sm, const Win
         auto fetch_row = [&](int s1, int s1R, int s1Rd) {
             const int b1 = s1 >> 4, u1 = s1 & (kWinS - 1), st1 = b1 & 1;
             if (u1 == 0) mbar_wait_cta(MB(kMbYFull + st1), (uint32_t)((b1 >> 1) & 1), A.error);
+            // raw loads only: the sums happen at first use (next iteration), so
+            // nothing here waits on shared-memory latency
             const float4* zr = reinterpret_cast<const float4*>(zacc + s1R * HP) + lane * NQ;
-            const float4* yr = reinterpret_cast<const float4*>(ystage + (st1 * kWinS + u1) * HP) + lane * NQ;
+            const float4* yr = reinterpret_cast<const float4*>(ystage + ((size_t)st1 * KS * kWinS + u1) * H) + lane * NQ;
 #pragma unroll
             for (int q = 0; q < NQ; ++q) {
-                const float4 za = zr[q], ya = yr[q];
-                zpre[4 * q + 0] = za.x + ya.x;
-                zpre[4 * q + 1] = za.y + ya.y;
-                zpre[4 * q + 2] = za.z + ya.z;
-                zpre[4 * q + 3] = za.w + ya.w;
+                zraw[q] = zr[q];
+                const bool qv = 4 * (lane * NQ + q) < H;
+#pragma unroll
+                for (int p = 0; p < kMaxKS; ++p)
+                    yraw[p][q] = (qv && p < KS) ? yr[q + p * kWinS * (H >> 2)] : make_float4(0.f, 0.f, 0.f, 0.f);
             }
             const float* tr = tstage + (st1 * kWinS + u1) * kWinCP;
 #pragma unroll
@@ -486,7 +528,8 @@ __device__ __forceinline__ void win_chain(const WinArgs& A, float* sm, const Win
             c2n = s1 >= 2 ? coefs[p2 * QW + 1] : 0.0f;  // c(s1, 2) = coef[s1-2][1]
         };
         if (n > 0) fetch_row(0, 0, 0);
-        int sR = 0, sRd = 0;  // s % R, s % Rd
+        int sR = 0, sRd = 0;    // s % R, s % Rd
+        int nR = 1 % R, nRd = 1;  // (s+1) % R, (s+1) % Rd
         float* const xr = red;                // [k][36]: partial logits, transposed
         float* const zt = red + kWinCP * 36;  // class logits of this sample
         for (int s = 0; s < n; ++s) {
@@ -494,11 +537,31 @@ __device__ __forceinline__ void win_chain(const WinArgs& A, float* sm, const Win
             WIN_TRACE(s, 0);
             // -- z(s) = Y + window + c1 d0(s-1) + c2 d0(s-2) + b0;  tanh.
             //    The deferred W1 update of s-1 fills the tanh latency.
-            float z[JPL], a[JPL];
+            float z[JPL], a[JPL], t[CC], zpre[JPL];
+            const float tow = town;
+#pragma unroll
+            for (int q = 0; q < NQ; ++q) {  // Y = fixed-order sum of the KS partials
+                const float4 y01 = make_float4(yraw[0][q].x + yraw[1][q].x, yraw[0][q].y + yraw[1][q].y,
+                                               yraw[0][q].z + yraw[1][q].z, yraw[0][q].w + yraw[1][q].w);
+                const float4 y23 = make_float4(yraw[2][q].x + yraw[3][q].x, yraw[2][q].y + yraw[3][q].y,
+                                               yraw[2][q].z + yraw[3][q].z, yraw[2][q].w + yraw[3][q].w);
+                zpre[4 * q + 0] = zraw[q].x + (y01.x + y23.x);
+                zpre[4 * q + 1] = zraw[q].y + (y01.y + y23.y);
+                zpre[4 * q + 2] = zraw[q].z + (y01.z + y23.z);
+                zpre[4 * q + 3] = zraw[q].w + (y01.w + y23.w);
+            }
 #pragma unroll
             for (int m = 0; m < JPL; ++m) {
                 z[m] = fmaf(c1n, dp1[m], fmaf(c2n, dp2[m], zpre[m])) + b0r[m];
                 a[m] = tanhf(z[m]);
+            }
+#pragma unroll
+            for (int k = 0; k < CC; ++k) t[k] = tn[k];
+            // row s+1 was flagged by its helper ~2 samples ago: fetch it now so
+            // the shared-memory latency hides under this sample's chain
+            if (s + 1 < n) {
+                flag_wait(s + 1, nR);
+                fetch_row(s + 1, nR, nRd);
             }
             // FAST numerics: the W1 update as one FMA, w + (-eta d1) a
 #pragma unroll
@@ -546,7 +609,7 @@ __device__ __forceinline__ void win_chain(const WinArgs& A, float* sm, const Win
             const float inv = rcp_approx(sum);
             float d1[CC];
 #pragma unroll
-            for (int k = 0; k < CC; ++k) d1[k] = k < C ? ssub(ek[k] * inv, tn[k]) : 0.0f;
+            for (int k = 0; k < CC; ++k) d1[k] = k < C ? ssub(ek[k] * inv, t[k]) : 0.0f;
             float d0v[JPL];
 #pragma unroll
             for (int m = 0; m < JPL; ++m) {
@@ -567,7 +630,7 @@ __device__ __forceinline__ void win_chain(const WinArgs& A, float* sm, const Win
             for (int k = 0; k < CC; ++k) ndkp[k] = neg_eta * d1[k];
             if (kval) {
                 const float pk = expf(zown - mx) * inv;
-                const float dk = ssub(pk, town);
+                const float dk = ssub(pk, tow);
                 pring[sRd * kWinCP + lane] = pk;
                 b1k = fmaf(neg_eta, dk, b1k);
                 if (s == n - 1) {
@@ -596,12 +659,10 @@ __device__ __forceinline__ void win_chain(const WinArgs& A, float* sm, const Win
                 }
             }
             WIN_TRACE(s, 5);
-            if (++sR == R) sR = 0;
-            if (++sRd == Rd) sRd = 0;
-            if (s + 1 < n) {
-                flag_wait(s + 1, sR);
-                fetch_row(s + 1, sR, sRd);
-            }
+            sR = nR;
+            sRd = nRd;
+            if (++nR == R) nR = 0;
+            if (++nRd == Rd) nRd = 0;
             WIN_TRACE(s, 6);
         }
         if (n > 0) {
@@ -672,30 +733,28 @@ __device__ __forceinline__ void win_chain(const WinArgs& A, float* sm, const Win
             }
             WIN_TRACE(s0, 8);
             if (b >= 2) mbar_wait_cta(MB(kMbYFree + st), (uint32_t)(((b - 2) >> 1) & 1), A.error);
-            spin_geq(A.ycnt + (b % YR), (unsigned)(A.P * (b / YR + 1)), A.error);
+            spin_geq(A.ycnt + (b % YR), (unsigned)(2 * A.P * (b / YR + 1)), A.error);  // 2 writer warps per producer
             WIN_TRACE(s0, 9);
             coef_store(b, cv);
-            const float4* src = reinterpret_cast<const float4*>(A.yring + (size_t)(b % YR) * kWinS * H);
-            float4* dst = reinterpret_cast<float4*>(ystage + (size_t)st * kWinS * HP);
-            for (int e0 = 0; e0 < nv * HQ; e0 += 32 * 8) {
-                float4 v[8];
-#pragma unroll
-                for (int q = 0; q < 8; ++q) {
-                    const int e = e0 + lane + 32 * q;
-                    if (e < nv * HQ) v[q] = __ldcg(src + e);
-                }
-#pragma unroll
-                for (int q = 0; q < 8; ++q) {
-                    const int e = e0 + lane + 32 * q;
-                    if (e < nv * HQ) {
-                        const int u = e / HQ, qq = e - u * HQ;
-                        dst[u * HPQ + qq] = v[q];
-                    }
+            // Y(b): KS partial slabs by TMA bulk copy, completing yfull's tx count
+            if (lane == 0) {
+                asm volatile("fence.proxy.async.global;\n" ::: "memory");  // generic writes -> async proxy
+                const uint32_t bytes = (uint32_t)(nv * H * sizeof(float));
+                const uint32_t mbar = MB(kMbYFull + st);
+                mbar_arrive_expect_tx(mbar, bytes * KS);
+                for (int p = 0; p < KS; ++p) {
+                    const float* src = A.yring + (((size_t)(b % YR) * KS + p) * kWinS) * H;
+                    float* dst = ystage + ((size_t)st * KS + p) * kWinS * H;
+                    asm volatile(
+                        "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];\n" ::"r"(
+                            smem_u32(dst)),
+                        "l"(src), "r"(bytes), "r"(mbar)
+                        : "memory");
                 }
             }
 #pragma unroll
             for (int q = 0; q < kWinS * kWinCP / 32; ++q) tstage[st * kWinS * kWinCP + lane + 32 * q] = tv[q];
-            mbar_arrive_cta(MB(kMbYFull + st));
+            if (lane != 0) mbar_arrive_cta(MB(kMbYFull + st));  // lane 0 arrived with expect_tx
             WIN_TRACE(s0, 10);
         }
     } else if (warp == kWinPub) {
@@ -761,7 +820,7 @@ __device__ __forceinline__ void win_chain(const WinArgs& A, float* sm, const Win
         // (r = w mod NH): z(r) += c(r, r-s) d0(s), c from the forward band row
         // of source s.  Rows are visited in ascending order, so an owned row
         // s+3 (the next one the chain fetches) is flagged first.
-        const int w = warp;
+        const int w = win_helper_index(warp);
         int sR = 0, sRd = 0;  // s % R, s % Rd
         for (int s = 0; s < n; ++s) {
             const int b = s >> 4;
@@ -855,11 +914,10 @@ __device__ __forceinline__ void win_chain(const WinArgs& A, float* sm, const Win
 template <int JPL, int CT>
 __global__ void __launch_bounds__(kWinThreads, 1) k_sgd_window(WinArgs A) {
     extern __shared__ __align__(16) float sm[];
-    const WinSmem L(32 * JPL, A.D);
     if (blockIdx.x == 0)
-        win_chain<JPL, CT>(A, sm, L);
+        win_chain<JPL, CT>(A, sm, WinSmem(32 * JPL, A.D, A.KS, A.H));
     else
-        win_producer(A, sm, L);
+        win_producer(A, sm);
 }
 
 }  // namespace lane_b200

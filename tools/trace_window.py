@@ -25,13 +25,15 @@ def main():
     from oracle import pyoracle as po
     from paper_2001_04206_b200 import lane
     dev = lane.Device(0)
-    X, T = po.synthetic_dataset(F, C, 512, 9)
+    rows = int(os.environ.get("TRACE_ROWS", "512"))
+    steps = int(os.environ.get("TRACE_STEPS", "512"))
+    X, T = po.synthetic_dataset(F, C, rows, 9)
     xd, td = dev.alloc(X.nbytes), dev.alloc(T.nbytes)
     dev.h2d(xd, X)
     dev.h2d(td, T)
     net = lane.build_network(F, [H], C, seed=42, device=dev)
-    net.sgd_stream(xd, td, 512, 512, 0.01)
-    net.sgd_stream(xd, td, 512, 512, 0.01)
+    net.sgd_stream(xd, td, rows, steps, 0.01)
+    net.sgd_stream(xd, td, rows, steps, 0.01)
     dev.sync()
     lines = open(path).read().strip().splitlines()
     print(shp, lines[-65])
