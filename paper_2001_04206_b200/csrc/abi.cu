@@ -614,7 +614,7 @@ void launch_window(lane_b200_net* net, const SgdPlan& P, const float* X, const f
     // banded Gram pre-pass
     k_gram_band<<<static_cast<unsigned>((n_steps + kGramTS - 1) / kGramTS), 256, 0, c->stream>>>(A);
     c->count();
-    const WinKernel kern = window_kernel(P.jpl, A.C);
+    const WinKernel kern = (A.trace && P.jpl == 4 && A.C == 10) ? k_sgd_window<4, 10, true> : window_kernel(P.jpl, A.C);
     LANE_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(P.smem)));
     void* args[] = {&A};
     LANE_CUDA(cudaLaunchCooperativeKernel(reinterpret_cast<void*>(kern), dim3(P.G), dim3(kWinThreads), args,

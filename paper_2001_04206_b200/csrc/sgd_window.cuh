@@ -106,7 +106,7 @@ struct WinSmem {
         coefs = take((size_t)Rd * D * kWinS);  // forward band rows of source s, slot s % Rd
         d0ring = take((size_t)Rd * HP);
         pring = take((size_t)Rd * kWinCP);
-        red = take(kWinCP * 37 > kWinWarps * 64 ? kWinCP * 37 : kWinWarps * 64);
+        red = take(kWinCP * 38 > kWinWarps * 64 ? kWinCP * 38 : kWinWarps * 64);
         d0s = take(kWinS * 4);
         rowflag = take(R);
         mbar = take(2 * (kWinRing + 4 + kWinBlkRing));
@@ -422,7 +422,7 @@ __device__ __forceinline__ float rcp_approx(float x) {
 // ---------------------------------------------------------------------------
 // Chain CTA.
 // ---------------------------------------------------------------------------
-template <int JPL, int CT>
+template <int JPL, int CT, bool TR>
 __device__ __forceinline__ void win_chain(const WinArgs& A, float* sm, const WinSmem& L) {
     const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
     const int H = A.H, D = A.D, HP = L.HP, R = L.R, Rd = L.Rd, QW = A.QW, KS = A.KS;
@@ -445,7 +445,7 @@ __device__ __forceinline__ void win_chain(const WinArgs& A, float* sm, const Win
     unsigned long long* const trace = A.trace;
 #define WIN_TRACE(s_, ph)                                                                \
     do {                                                                                 \
-        if (trace && lane == 0 && (unsigned)((s_) - A.trace_base) < kTraceSamples)       \
+        if (TR && trace && lane == 0 && (unsigned)((s_) - A.trace_base) < kTraceSamples)       \
             trace[((s_) - A.trace_base) * kTracePhases + (ph)] = clock64();              \
     } while (0)
 
@@ -521,7 +521,13 @@ __device__ __forceinline__ void win_chain(const WinArgs& A, float* sm, const Win
             }
             const float* tr = tstage + (st1 * kWinS + u1) * kWinCP;
 #pragma unroll
-            for (int k = 0; k < CC; ++k) tn[k] = tr[k];
+            for (int k4 = 0; k4 < (CC + 3) / 4; ++k4) {
+                const float4 t4 = reinterpret_cast<const float4*>(tr)[k4];
+                if (4 * k4 + 0 < CC) tn[4 * k4 + 0] = t4.x;
+                if (4 * k4 + 1 < CC) tn[4 * k4 + 1] = t4.y;
+                if (4 * k4 + 2 < CC) tn[4 * k4 + 2] = t4.z;
+                if (4 * k4 + 3 < CC) tn[4 * k4 + 3] = t4.w;
+            }
             town = kval ? tr[lane] : 0.0f;
             const int p1 = s1Rd == 0 ? Rd - 1 : s1Rd - 1, p2 = p1 == 0 ? Rd - 1 : p1 - 1;
             c1n = s1 >= 1 ? coefs[p1 * QW + 0] : 0.0f;  // c(s1, 1) = coef[s1-1][0]
@@ -532,6 +538,7 @@ __device__ __forceinline__ void win_chain(const WinArgs& A, float* sm, const Win
         int nR = 1 % R, nRd = 1;  // (s+1) % R, (s+1) % Rd
         float* const xr = red;                // [k][36]: partial logits, transposed
         float* const zt = red + kWinCP * 36;  // class logits of this sample
+        float* const es = zt + kWinCP;        // exp(z_k - max) of this sample
         for (int s = 0; s < n; ++s) {
             const int b = s >> 4, u = s & (kWinS - 1), st = b & 1;
             WIN_TRACE(s, 0);
@@ -593,19 +600,53 @@ __device__ __forceinline__ void win_chain(const WinArgs& A, float* sm, const Win
             }
             __syncwarp();
             WIN_TRACE(s, 2);
-            // -- softmax redundantly in every lane: exact max, C exponentials;
-            //    d1 = p - t;  d0 = (1 - a^2) * (W1 d1) with the pre-update W1
-            float ek[CC];
-            float mx = zt[0];
+            // -- softmax: every lane reads the C logits (exact max); lane k
+            //    computes exp(z_k - max) once and shares it through shared memory
+            constexpr int CV = (CC + 3) / 4;  // float4 loads of a class vector
+            float zk[4 * CV];
+#pragma unroll
+            for (int k4 = 0; k4 < CV; ++k4) {
+                const float4 v = reinterpret_cast<const float4*>(zt)[k4];
+                zk[4 * k4 + 0] = v.x;
+                zk[4 * k4 + 1] = v.y;
+                zk[4 * k4 + 2] = v.z;
+                zk[4 * k4 + 3] = v.w;
+            }
+            float mx = zk[0];
 #pragma unroll
             for (int k = 1; k < CC; ++k)
-                if (k < C) mx = fmaxf(mx, zt[k]);
-            float sum = 0.0f;
-#pragma unroll
-            for (int k = 0; k < CC; ++k) {
-                ek[k] = k < C ? expf(zt[k] - mx) : 0.0f;
-                sum += ek[k];
+                if (k < C) mx = fmaxf(mx, zk[k]);
+            float eown = 0.0f;
+            if (kval) {
+                eown = expf(zown - mx);
+                es[lane] = eown;
             }
+            __syncwarp();
+            float ek[4 * CV];
+#pragma unroll
+            for (int k4 = 0; k4 < CV; ++k4) {
+                const float4 v = reinterpret_cast<const float4*>(es)[k4];
+                ek[4 * k4 + 0] = v.x;
+                ek[4 * k4 + 1] = v.y;
+                ek[4 * k4 + 2] = v.z;
+                ek[4 * k4 + 3] = v.w;
+            }
+#pragma unroll
+            for (int k = CC; k < 4 * CV; ++k) ek[k] = 0.0f;
+            if (CT == 0) {
+#pragma unroll
+                for (int k = 0; k < 4 * CV; ++k)
+                    if (k >= C) ek[k] = 0.0f;
+            }
+            // tree sum (fixed order)
+            float sp[4 * CV];
+#pragma unroll
+            for (int k = 0; k < 4 * CV; ++k) sp[k] = ek[k];
+#pragma unroll
+            for (int wdt = 1; wdt < 4 * CV; wdt <<= 1)
+#pragma unroll
+                for (int k = 0; k + wdt < 4 * CV; k += 2 * wdt) sp[k] += sp[k + wdt];
+            const float sum = sp[0];
             const float inv = rcp_approx(sum);
             float d1[CC];
 #pragma unroll
@@ -629,7 +670,7 @@ __device__ __forceinline__ void win_chain(const WinArgs& A, float* sm, const Win
 #pragma unroll
             for (int k = 0; k < CC; ++k) ndkp[k] = neg_eta * d1[k];
             if (kval) {
-                const float pk = expf(zown - mx) * inv;
+                const float pk = eown * inv;
                 const float dk = ssub(pk, tow);
                 pring[sRd * kWinCP + lane] = pk;
                 b1k = fmaf(neg_eta, dk, b1k);
@@ -911,11 +952,12 @@ __device__ __forceinline__ void win_chain(const WinArgs& A, float* sm, const Win
 #undef WIN_TRACE
 }
 
-template <int JPL, int CT>
+// TR: per-phase clock64 trace of the chain CTA (diagnostics build only)
+template <int JPL, int CT, bool TR = false>
 __global__ void __launch_bounds__(kWinThreads, 1) k_sgd_window(WinArgs A) {
     extern __shared__ __align__(16) float sm[];
     if (blockIdx.x == 0)
-        win_chain<JPL, CT>(A, sm, WinSmem(32 * JPL, A.D, A.KS, A.H));
+        win_chain<JPL, CT, TR>(A, sm, WinSmem(32 * JPL, A.D, A.KS, A.H));
     else
         win_producer(A, sm);
 }
