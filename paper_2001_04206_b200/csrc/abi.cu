@@ -356,13 +356,13 @@ SgdPlan plan_persistent(lane_b200_net* net) {
     const char* mode = std::getenv("LANE_B200_SGD_MODE");
     if (!mode || std::strcmp(mode, "window") == 0) {
         // windowed plan: the chain on one CTA, W0 on H/4 producer CTAs
-        int D = 3;
+        int D = 2;  // measured best at C2 (producers keep up with one block of lag)
         if (const char* e = std::getenv("LANE_B200_SGD_WIN_D")) D = std::max(2, std::min(std::atoi(e), kWinMaxD));
         const int jpl = H <= 128 ? 4 : 8;
-        // producers: H/4 column quads x KS row splits, as many SMs as fit (<= 4
-        // splits, >= 32 rows each); rows per split a multiple of 4 (cp.async 16 B)
+        // producers: H/4 column quads x KS row splits (<= 2 splits, >= 32 rows
+        // each, as SMs allow); rows per split a multiple of 4 (cp.async 16 B)
         const int quads = std::max(1, H / 4);
-        int ks = std::max(1, std::min({4, (c->sm_count - 1) / quads, std::max(1, I / 32)}));
+        int ks = std::max(1, std::min({2, (c->sm_count - 1) / quads, std::max(1, I / 32)}));
         if (const char* e = std::getenv("LANE_B200_SGD_WIN_KS")) ks = std::max(1, std::min(std::atoi(e), 4));
         const int rpc = (((I + ks - 1) / ks) + 3) & ~3;
         ks = (I + rpc - 1) / rpc;

@@ -482,9 +482,9 @@ __device__ __forceinline__ void win_chain(const WinArgs& A, float* sm, const Win
 #pragma unroll
         for (int k = 0; k < CC; ++k) ndkp[k] = 0.0f;
         float b1k = kval ? A.b1[lane] : 0.0f;
-        float zl[JPL], al[JPL];
+        float zl[JPL], zkl = 0.0f, pkl = 0.0f, dkl = 0.0f;  // last sample's z0, z1, p, d1
 #pragma unroll
-        for (int m = 0; m < JPL; ++m) zl[m] = al[m] = 0.0f;
+        for (int m = 0; m < JPL; ++m) zl[m] = 0.0f;
         // prefetched operands of the next sample
         constexpr int kMaxKS = 4;
         float4 zraw[NQ], yraw[kMaxKS][NQ];  // row s+1: window sums and the KS partial Y quads
@@ -585,9 +585,11 @@ __device__ __forceinline__ void win_chain(const WinArgs& A, float* sm, const Win
                 xr[k * 36 + lane] = acc;
             }
             __syncwarp();
-            float zown = 0.0f;
-            if (kval) {
-                const float4* col = reinterpret_cast<const float4*>(xr + lane * 36);
+            // every lane sums a class row (lanes >= 16 repeat rows 0..15: no
+            // branch); lanes k < C publish theirs
+            float zown;
+            {
+                const float4* col = reinterpret_cast<const float4*>(xr + (lane & (kWinCP - 1)) * 36);
                 float4 v[8];
 #pragma unroll
                 for (int q = 0; q < 8; ++q) v[q] = col[q];
@@ -596,7 +598,7 @@ __device__ __forceinline__ void win_chain(const WinArgs& A, float* sm, const Win
                 for (int q = 0; q < 8; ++q) t8[q] = (v[q].x + v[q].y) + (v[q].z + v[q].w);
                 const float tot = ((t8[0] + t8[1]) + (t8[2] + t8[3])) + ((t8[4] + t8[5]) + (t8[6] + t8[7]));
                 zown = sadd(tot, b1k);
-                zt[lane] = zown;
+                if (kval) zt[lane] = zown;
             }
             __syncwarp();
             WIN_TRACE(s, 2);
@@ -616,11 +618,8 @@ __device__ __forceinline__ void win_chain(const WinArgs& A, float* sm, const Win
 #pragma unroll
             for (int k = 1; k < CC; ++k)
                 if (k < C) mx = fmaxf(mx, zk[k]);
-            float eown = 0.0f;
-            if (kval) {
-                eown = expf(zown - mx);
-                es[lane] = eown;
-            }
+            const float eown = expf(zown - mx);
+            if (kval) es[lane] = eown;
             __syncwarp();
             float ek[4 * CV];
 #pragma unroll
@@ -669,18 +668,13 @@ __device__ __forceinline__ void win_chain(const WinArgs& A, float* sm, const Win
             // -- off the chain: p and d1 of the lane's own class, stats, biases
 #pragma unroll
             for (int k = 0; k < CC; ++k) ndkp[k] = neg_eta * d1[k];
-            if (kval) {
-                const float pk = eown * inv;
-                const float dk = ssub(pk, tow);
-                pring[sRd * kWinCP + lane] = pk;
-                b1k = fmaf(neg_eta, dk, b1k);
-                if (s == n - 1) {
-                    A.z1[lane] = zown;
-                    A.a1[lane] = pk;
-                    A.d1[lane] = dk;
-                    A.db1[lane] = smul(neg_eta, dk);
-                }
-            }
+            const float pk = eown * inv;
+            const float dk = kval ? ssub(pk, tow) : 0.0f;
+            if (kval) pring[sRd * kWinCP + lane] = pk;
+            b1k = fmaf(neg_eta, dk, b1k);
+            zkl = zown;
+            pkl = pk;
+            dkl = dk;
             if (u == kWinS - 1 || s == n - 1) {
                 mbar_arrive_cta(MB(kMbBlk + b % kWinBlkRing));
                 mbar_arrive_cta(MB(kMbYFree + st));
@@ -692,13 +686,8 @@ __device__ __forceinline__ void win_chain(const WinArgs& A, float* sm, const Win
                 dp1[m] = d0v[m];
                 aprev[m] = a[m];
             }
-            if (s == n - 1) {
 #pragma unroll
-                for (int m = 0; m < JPL; ++m) {
-                    zl[m] = z[m];
-                    al[m] = a[m];
-                }
-            }
+            for (int m = 0; m < JPL; ++m) zl[m] = z[m];
             WIN_TRACE(s, 5);
             sR = nR;
             sRd = nRd;
@@ -721,13 +710,19 @@ __device__ __forceinline__ void win_chain(const WinArgs& A, float* sm, const Win
                         if (k < C) A.W1[(size_t)j * C + k] = w1[m][k];
                     A.b0[j] = b0r[m];
                     A.z0[j] = zl[m];
-                    A.a0[j] = al[m];
+                    A.a0[j] = aprev[m];
                     A.d0[j] = dp1[m];
                     A.db0[j] = smul(neg_eta, dp1[m]);
-                    A.x1[j] = al[m];
+                    A.x1[j] = aprev[m];
                 }
             }
-            if (kval) A.b1[lane] = b1k;
+            if (kval) {
+                A.b1[lane] = b1k;
+                A.z1[lane] = zkl;
+                A.a1[lane] = pkl;
+                A.d1[lane] = dkl;
+                A.db1[lane] = smul(neg_eta, dkl);
+            }
         }
     } else if (warp == kWinLoad) {
         // ================= loader: Y(b), targets, coefficient rows =================
