@@ -380,7 +380,8 @@ def main():
         e2e_s = float(t.item())
     e2e = world * n * e2e_steps / e2e_s
 
-    # ---- roofline of the dominant kernel (k_sgd_persistent) ----
+    # ---- roofline of the dominant kernel (the fused online-SGD plan) ----
+    plan = net.sgd_plan()
     peak, peak_kind = load_peaks()
     P = sum(a * b + b for a, b in zip([F] + H, H + [C]))
     bytes_per_sample = 8 * P + 4 * (F + C)  # every weight read+written once, + the sample
@@ -398,12 +399,16 @@ def main():
                        if X.nbytes + T.nbytes > 126e6 else "inputs fit in L2"},
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                          "frac": achieved / peak, "traffic": None, "peak_kind": peak_kind,
-                         "kernel": "k_sgd_cluster",
+                         "kernel": {"window": "k_sgd_window", "cluster": "k_sgd_cluster",
+                                    "grid": "k_sgd_grid"}.get(plan.split()[0], "layer kernels"),
+                         "plan": plan,
                          "algorithmic_bytes_per_sample": bytes_per_sample,
                          "note": "algorithmic bytes = every weight read+written once per sample "
-                                 "(8 B/param) + the sample; the kernel keeps the weights in shared "
-                                 "memory (measured DRAM traffic is the inputs only) and is bound by "
-                                 "the per-sample dependency chain, see DESIGN.md section 4"},
+                                 "(8 B/param) + the sample, i.e. the HBM floor of a design that "
+                                 "streams the weights; this kernel keeps them on chip (DRAM traffic "
+                                 "is the inputs only) and is bound by the serial per-sample chain "
+                                 "(DESIGN.md section 4); achieved uses the whole step (pre-pass + "
+                                 "kernel + G/DW), CUDA events on the library stream"},
             "e2e": {"value": e2e, "unit": "samples/s",
                     "h2d_bytes_per_step": int(X.nbytes + T.nbytes),
                     "d2h_bytes_per_step": 8 * 2},

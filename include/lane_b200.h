@@ -169,6 +169,11 @@ int lane_b200_backward_plan_run(lane_b200_net* net, const float* target_host, fl
 int lane_b200_sgd_stream(lane_b200_net* net, const float* X_dev, const float* T_dev, size_t n,
                          const uint32_t* order_dev, size_t n_steps, float eta,
                          double* loss_sum_dev, uint64_t* correct_dev);
+/* Which fused plan lane_b200_sgd_stream runs for this network under the
+ * context's current numerics/environment: writes a NUL-terminated description
+ * ("window D=2 KS=2 ctas=65", "cluster ctas=16", "grid ...", or "layer" for the
+ * per-sample layer-kernel path) into buf (len >= 64 recommended). */
+int lane_b200_sgd_stream_plan(lane_b200_net* net, char* buf, size_t len);
 /* train (network.hpp:77-82, network.cpp:140-182): per epoch the reference's
  * SplitMix64 Fisher-Yates shuffle (order not reset between epochs), one fused
  * sgd_stream over the epoch, EpochStats readback, early stop when

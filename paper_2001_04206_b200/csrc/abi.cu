@@ -1153,6 +1153,23 @@ int lane_b200_sgd_stream(lane_b200_net* net, const float* X, const float* T, siz
     });
 }
 
+int lane_b200_sgd_stream_plan(lane_b200_net* net, char* buf, size_t len) {
+    return guard([&] {
+        if (!net || !buf || len == 0) throw Error(LANE_ERR_CONFIG, "null argument");
+        const SgdPlan P = plan_persistent(net);
+        char tmp[128];
+        if (!P.ok)
+            std::snprintf(tmp, sizeof tmp, "layer");
+        else if (P.window)
+            std::snprintf(tmp, sizeof tmp, "window D=%d KS=%d ctas=%d smem=%zu", P.D, P.ks, P.G, P.smem);
+        else if (P.cluster)
+            std::snprintf(tmp, sizeof tmp, "cluster ctas=%d smem=%zu", P.G, P.smem);
+        else
+            std::snprintf(tmp, sizeof tmp, "grid ctas=%d w0=%s smem=%zu", P.G, P.w0_smem ? "smem" : "hbm", P.smem);
+        std::snprintf(buf, len, "%s", tmp);
+    });
+}
+
 int lane_b200_train(lane_b200_net* net, const float* X_host, const float* T_host, size_t n, float eta,
                     float max_error, size_t max_epochs, uint64_t seed, float* mean_loss_out,
                     float* accuracy_out, size_t* epochs_run) {

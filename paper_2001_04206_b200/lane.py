@@ -356,6 +356,13 @@ class FeedForwardNetwork:
             n_steps, C.c_float(_eta(eta)), C.c_void_p(loss_dev or None),
             C.c_void_p(correct_dev or None)))
 
+    def sgd_plan(self) -> str:
+        """The fused plan sgd_stream runs for this network ("window ...",
+        "cluster ...", "grid ..." or "layer")."""
+        buf = C.create_string_buffer(128)
+        _check(_native.lib().lane_b200_sgd_stream_plan(self._p, buf, 128))
+        return buf.value.decode()
+
     # -- mini-batch extension --------------------------------------------
     def minibatch_step(self, X_dev: int, T_dev: int, batch: int, eta, mu: float = 0.0,
                        loss_dev: int = 0) -> None:

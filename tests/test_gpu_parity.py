@@ -501,3 +501,11 @@ def test_minibatch_momentum_vs_oracle(lane, fast, F, H, C, B, mu):
         assert_close(layer.weights, orc.get(l, po.W), 1e-5, f"W{l}")
     fast.free(Xd)
     fast.free(Td)
+
+
+@pytest.mark.parametrize("F,H,C,want", [(784, [128], 10, "window"), (4, [8], 3, "window"),
+                                        (340, [256], 10, "window"), (340, [1024], 10, "cluster")])
+def test_sgd_plan_selection(lane, fast, F, H, C, want):
+    # the fused plan the headline shapes run (no silent fallback to layer kernels)
+    net = lane.build_network(F, H, C, seed=42, device=fast)
+    assert net.sgd_plan().split()[0] == want, net.sgd_plan()
