@@ -288,6 +288,7 @@ struct SgdPlan {
     bool ok = false;
     bool window = false;   // delayed-base windowed kernel (chain CTA + W0 producers)
     int jpl = 4, D = 3;    // window plan: hidden units per chain lane, lag in blocks
+    int ncw = 1;           // window plan: chain warps
     int ks = 1, rpc = 0;   // window plan: producer row splits per column quad, rows per split
     bool cluster = false;  // single thread-block cluster, DSMEM exchange
     bool w0_smem = true;   // grid plan: W0 slices resident in shared memory
@@ -358,7 +359,13 @@ SgdPlan plan_persistent(lane_b200_net* net) {
         // windowed plan: the chain on one CTA, W0 on H/4 producer CTAs
         int D = 2;  // measured best at C2 (producers keep up with one block of lag)
         if (const char* e = std::getenv("LANE_B200_SGD_WIN_D")) D = std::max(2, std::min(std::atoi(e), kWinMaxD));
-        const int jpl = H <= 128 ? 4 : 8;
+        // chain geometry: H <= 64 -> 1 warp x 4 units/lane; <= 128 -> 2 warps x 2;
+        // <= 256 -> 2 warps x 4
+        // (measured at C2: one chain warp 1.83M samples/s, two 1.68M -- the
+        // barrier and the duplicated softmax outweigh the halved H work)
+        int ncw = H <= 128 ? 1 : 2;
+        if (const char* e = std::getenv("LANE_B200_SGD_WIN_NCW")) ncw = (std::atoi(e) == 1 && H <= 128) ? 1 : 2;
+        const int jpl = ncw == 1 ? 4 : (H <= 128 ? 2 : 4);
         // producers: H/4 column quads x KS row splits (<= 2 splits, >= 32 rows
         // each, as SMs allow); rows per split a multiple of 4 (cp.async 16 B)
         const int quads = std::max(1, H / 4);
@@ -366,13 +373,14 @@ SgdPlan plan_persistent(lane_b200_net* net) {
         if (const char* e = std::getenv("LANE_B200_SGD_WIN_KS")) ks = std::max(1, std::min(std::atoi(e), 4));
         const int rpc = (((I + ks - 1) / ks) + 3) & ~3;
         ks = (I + rpc - 1) / rpc;
-        const WinSmem L(32 * jpl, D, ks, H);
+        const WinSmem L(32 * jpl * ncw, D, ks, H, ncw);
         const ProdSmem PL(rpc, D);
         const size_t smem = std::max(L.total, PL.total);
-        if (H % 4 == 0 && H <= 256 && C <= kWinCP && rpc <= kWinMaxNR * kWinThreads &&
+        if (H % 4 == 0 && H <= 256 && C <= kWinCP && rpc <= kWinMaxNR * 224 &&
             1 + quads * ks <= c->sm_count && smem <= c->max_smem_optin) {
             p.ok = p.window = true;
             p.jpl = jpl;
+            p.ncw = ncw;
             p.D = D;
             p.ks = ks;
             p.rpc = rpc;
@@ -544,9 +552,10 @@ void launch_persistent(lane_b200_net* net, const SgdPlan& P, const float* X, con
 
 using WinKernel = void (*)(WinArgs);
 
-WinKernel window_kernel(int jpl, int C) {
-    if (jpl == 4) return C == 10 ? k_sgd_window<4, 10> : C == 3 ? k_sgd_window<4, 3> : k_sgd_window<4, 0>;
-    return C == 10 ? k_sgd_window<8, 10> : k_sgd_window<8, 0>;
+WinKernel window_kernel(int jpl, int ncw, int C) {
+    if (ncw == 1) return C == 10 ? k_sgd_window<4, 10, 1> : C == 3 ? k_sgd_window<4, 3, 1> : k_sgd_window<4, 0, 1>;
+    if (jpl == 2) return C == 10 ? k_sgd_window<2, 10, 2> : k_sgd_window<2, 0, 2>;
+    return C == 10 ? k_sgd_window<4, 10, 2> : k_sgd_window<4, 0, 2>;
 }
 
 void launch_window(lane_b200_net* net, const SgdPlan& P, const float* X, const float* T, size_t n,
@@ -614,10 +623,13 @@ void launch_window(lane_b200_net* net, const SgdPlan& P, const float* X, const f
     // banded Gram pre-pass
     k_gram_band<<<static_cast<unsigned>((n_steps + kGramTS - 1) / kGramTS), 256, 0, c->stream>>>(A);
     c->count();
-    const WinKernel kern = (A.trace && P.jpl == 4 && A.C == 10) ? k_sgd_window<4, 10, true> : window_kernel(P.jpl, A.C);
+    const WinKernel kern = (A.trace && P.jpl == 2 && P.ncw == 2 && A.C == 10) ? k_sgd_window<2, 10, 2, true>
+                           : (A.trace && P.jpl == 4 && P.ncw == 1 && A.C == 10) ? k_sgd_window<4, 10, 1, true>
+                                                                                 : window_kernel(P.jpl, P.ncw, A.C);
     LANE_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(P.smem)));
     void* args[] = {&A};
-    LANE_CUDA(cudaLaunchCooperativeKernel(reinterpret_cast<void*>(kern), dim3(P.G), dim3(kWinThreads), args,
+    const int nthreads = P.ncw == 2 ? win_threads<2>() : win_threads<1>();
+    LANE_CUDA(cudaLaunchCooperativeKernel(reinterpret_cast<void*>(kern), dim3(P.G), dim3(nthreads), args,
                                           P.smem, c->stream));
     c->count();
     if (A.trace) {
@@ -1161,7 +1173,8 @@ int lane_b200_sgd_stream_plan(lane_b200_net* net, char* buf, size_t len) {
         if (!P.ok)
             std::snprintf(tmp, sizeof tmp, "layer");
         else if (P.window)
-            std::snprintf(tmp, sizeof tmp, "window D=%d KS=%d ctas=%d smem=%zu", P.D, P.ks, P.G, P.smem);
+            std::snprintf(tmp, sizeof tmp, "window D=%d KS=%d chain=%dx%d ctas=%d smem=%zu", P.D, P.ks, P.ncw,
+                          32 * P.jpl, P.G, P.smem);
         else if (P.cluster)
             std::snprintf(tmp, sizeof tmp, "cluster ctas=%d smem=%zu", P.G, P.smem);
         else

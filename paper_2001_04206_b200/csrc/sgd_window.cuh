@@ -51,12 +51,58 @@ namespace lane_b200 {
 
 constexpr int kWinS = 16;                    // samples per block
 constexpr int kWinHelpers = 4;               // helper warps
-constexpr int kWinWarps = kWinHelpers + 3;   // + publisher, loader, critical
-constexpr int kWinThreads = 32 * kWinWarps;  // 352
+constexpr int kWinWarps = 8;                 // max warps per CTA (two chain warps)
+constexpr int kWinThreads = 32 * kWinWarps;  // 256
+// CTA size: 7 warps with one chain warp, 8 with two
+template <int NCW>
+constexpr int win_threads() { return NCW == 2 ? 256 : 224; }
 // Warp roles.  Warps share a sub-partition (SMSP) when their ids are equal mod
-// 4; the critical warp is warp 3, alone on its SMSP (7 warps: 3 | 0,4 | 1,5 | 2,6).
-constexpr int kWinCrit = 3, kWinPub = 5, kWinLoad = 6;
-__device__ __forceinline__ int win_helper_index(int warp) { return warp < 3 ? warp : 3; }  // warps 0,1,2,4
+// 4: SMSP0 = helper 0 + helper 2 (warp 4), SMSP1 = helper 1 + helper 3 (warp
+// 5), SMSP2 = chain warp 2 + publisher (6), SMSP3 = chain warp 3 + loader (7).
+// The publisher and loader mostly sleep on mbarriers / spin on L2 counters.
+// NCW = 1 (7 warps): helpers 0,1,2,4; chain 3 (alone on SMSP3); publisher 5;
+//   loader 6.
+// NCW = 2 (8 warps): helpers 0,1,4,5; chain 2,3; publisher 6; loader 7.
+template <int NCW>
+__device__ __forceinline__ int win_loader_warp() { return NCW == 2 ? 7 : 6; }
+template <int NCW>
+__device__ __forceinline__ int win_pub_warp() { return NCW == 2 ? 6 : 5; }
+// helper index 0..3, or -1
+template <int NCW>
+__device__ __forceinline__ int win_helper_index(int warp) {
+    if (NCW == 2) return (warp == 0 || warp == 1) ? warp : (warp == 4 || warp == 5) ? warp - 2 : -1;
+    return warp < 3 ? warp : warp == 4 ? 3 : -1;
+}
+// chain warp index (0..NCW-1) or -1: NCW = 1 uses warp 3 (warp 2 idles)
+template <int NCW>
+__device__ __forceinline__ int win_chain_index(int warp) {
+    return NCW == 2 ? ((warp == 2 || warp == 3) ? warp - 2 : -1) : (warp == 3 ? 0 : -1);
+}
+// vector load/store of JPL consecutive floats (JPL = 2 or 4)
+template <int JPL>
+__device__ __forceinline__ void vld(const float* p, float* v) {
+    if constexpr (JPL % 4 == 0) {
+#pragma unroll
+        for (int i = 0; i < JPL / 4; ++i) {
+            const float4 q = reinterpret_cast<const float4*>(p)[i];
+            v[4 * i] = q.x; v[4 * i + 1] = q.y; v[4 * i + 2] = q.z; v[4 * i + 3] = q.w;
+        }
+    } else {
+        static_assert(JPL == 2, "JPL must be 2 or a multiple of 4");
+        const float2 q = *reinterpret_cast<const float2*>(p);
+        v[0] = q.x; v[1] = q.y;
+    }
+}
+template <int JPL>
+__device__ __forceinline__ void vst(float* p, const float* v) {
+    if constexpr (JPL % 4 == 0) {
+#pragma unroll
+        for (int i = 0; i < JPL / 4; ++i)
+            reinterpret_cast<float4*>(p)[i] = make_float4(v[4 * i], v[4 * i + 1], v[4 * i + 2], v[4 * i + 3]);
+    } else {
+        *reinterpret_cast<float2*>(p) = make_float2(v[0], v[1]);
+    }
+}
 constexpr int kWinMaxD = 6;
 constexpr int kWinRing = 16;                 // d0-ready / row-ready mbarrier rings
 constexpr int kWinBlkRing = 8;               // block-done mbarrier ring (> D)
@@ -91,7 +137,7 @@ struct WinArgs {
 struct WinSmem {
     int HP, R, Rd;
     size_t zacc, ystage, tstage, coefs, d0ring, pring, red, d0s, rowflag, mbar, total;
-    __host__ __device__ WinSmem(int HP_, int D, int KS, int H) : HP(HP_) {
+    __host__ __device__ WinSmem(int HP_, int D, int KS, int H, int NCW) : HP(HP_) {
         R = D * kWinS;
         Rd = (D + 1) * kWinS;
         size_t o = 0;
@@ -106,7 +152,7 @@ struct WinSmem {
         coefs = take((size_t)Rd * D * kWinS);  // forward band rows of source s, slot s % Rd
         d0ring = take((size_t)Rd * HP);
         pring = take((size_t)Rd * kWinCP);
-        red = take(kWinCP * 38 > kWinWarps * 64 ? kWinCP * 38 : kWinWarps * 64);
+        red = take(kWinCP * (32 * NCW + 4) + 4 * NCW * kWinCP);  // partials, halves x2, logits, exps
         d0s = take(kWinS * 4);
         rowflag = take(R);
         mbar = take(2 * (kWinRing + 4 + kWinBlkRing));
@@ -267,6 +313,7 @@ struct ProdSmem {
     }
 };
 
+template <int NT>
 __device__ __forceinline__ void win_producer(const WinArgs& A, float* sm) {
     const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
     const int I = A.I, H = A.H, D = A.D, KS = A.KS, RPC = A.RPC;
@@ -287,7 +334,7 @@ __device__ __forceinline__ void win_producer(const WinArgs& A, float* sm) {
     float4 w[kWinMaxNR];
 #pragma unroll
     for (int m = 0; m < kWinMaxNR; ++m) {
-        const int li = tid + kWinThreads * m;
+        const int li = tid + NT * m;
         w[m] = li < nr ? *reinterpret_cast<const float4*>(A.W0 + (size_t)(i0 + li) * H + col)
                        : make_float4(0.f, 0.f, 0.f, 0.f);
     }
@@ -297,12 +344,12 @@ __device__ __forceinline__ void win_producer(const WinArgs& A, float* sm) {
         const int s0 = blk * kWinS, nv = min(kWinS, n - s0);
         if (vec) {
             const int nq = nr >> 2;
-            for (int e = tid; e < nv * nq; e += kWinThreads) {
+            for (int e = tid; e < nv * nq; e += NT) {
                 const int u = e / nq, q = e - u * nq;
                 cp_async16(dst + u * RPCp + 4 * q, A.X + win_row(A, s0 + u) * I + i0 + 4 * q);
             }
         } else {
-            for (int e = tid; e < nv * nr; e += kWinThreads) {
+            for (int e = tid; e < nv * nr; e += NT) {
                 const int u = e / nr, q = e - u * nr;
                 cp_async4(dst + u * RPCp + q, A.X + win_row(A, s0 + u) * I + i0 + q);
             }
@@ -317,7 +364,7 @@ __device__ __forceinline__ void win_producer(const WinArgs& A, float* sm) {
         for (int e = 0; e < 4 * kWinS; ++e) acc[e] = 0.0f;
 #pragma unroll
         for (int m = 0; m < kWinMaxNR; ++m) {
-            const int li = tid + kWinThreads * m;
+            const int li = tid + NT * m;
             if (li < nr) {
 #pragma unroll
                 for (int u = 0; u < kWinS; ++u) {
@@ -341,7 +388,7 @@ __device__ __forceinline__ void win_producer(const WinArgs& A, float* sm) {
         if (tid < 4 * kWinS) {
             float y = 0.0f;
 #pragma unroll
-            for (int q = 0; q < kWinWarps; ++q) y += red[q * 64 + tid];
+            for (int q = 0; q < NT / 32; ++q) y += red[q * 64 + tid];
             const int u = tid >> 2, c = tid & 3;
             if (u < nv) __stcg(A.yring + (((size_t)(blk % YR) * KS + ks) * kWinS + u) * H + col + c, y);
             // each of the two writer warps releases its own stores
@@ -375,7 +422,7 @@ __device__ __forceinline__ void win_producer(const WinArgs& A, float* sm) {
         const float* xb = xr + (size_t)(k % NB) * kWinS * RPCp;
 #pragma unroll
         for (int m = 0; m < kWinMaxNR; ++m) {
-            const int li = tid + kWinThreads * m;
+            const int li = tid + NT * m;
             if (li < nr) {
 #pragma unroll
                 for (int u = 0; u < kWinS; ++u) {
@@ -396,12 +443,12 @@ __device__ __forceinline__ void win_producer(const WinArgs& A, float* sm) {
     cp_async_wait<0>();
 #pragma unroll
     for (int m = 0; m < kWinMaxNR; ++m) {
-        const int li = tid + kWinThreads * m;
+        const int li = tid + NT * m;
         if (li < nr) *reinterpret_cast<float4*>(A.W0 + (size_t)(i0 + li) * H + col) = w[m];
     }
     if (blockIdx.x == 1 && n > 0) {
         const float* xl = A.X + win_row(A, n - 1) * I;
-        for (int i = tid; i < I; i += kWinThreads) A.x0[i] = xl[i];
+        for (int i = tid; i < I; i += NT) A.x0[i] = xl[i];
     }
 }
 
@@ -422,7 +469,7 @@ __device__ __forceinline__ float rcp_approx(float x) {
 // ---------------------------------------------------------------------------
 // Chain CTA.
 // ---------------------------------------------------------------------------
-template <int JPL, int CT, bool TR>
+template <int JPL, int CT, int NCW, bool TR>
 __device__ __forceinline__ void win_chain(const WinArgs& A, float* sm, const WinSmem& L) {
     const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
     const int H = A.H, D = A.D, HP = L.HP, R = L.R, Rd = L.Rd, QW = A.QW, KS = A.KS;
@@ -450,30 +497,36 @@ __device__ __forceinline__ void win_chain(const WinArgs& A, float* sm, const Win
     } while (0)
 
     // ---- prologue: zero the rings, init the barriers
-    for (int e = tid; e < R * HP; e += kWinThreads) zacc[e] = 0.0f;
-    for (int e = tid; e < 2 * A.KS * kWinS * H; e += kWinThreads) ystage[e] = 0.0f;
-    for (int e = tid; e < 2 * kWinS * kWinCP; e += kWinThreads) tstage[e] = 0.0f;
-    for (int e = tid; e < Rd * HP; e += kWinThreads) d0ring[e] = 0.0f;
-    for (int e = tid; e < R; e += kWinThreads) rowflag[e] = 0u;
+    for (int e = tid; e < R * HP; e += win_threads<NCW>()) zacc[e] = 0.0f;
+    for (int e = tid; e < 2 * A.KS * kWinS * H; e += win_threads<NCW>()) ystage[e] = 0.0f;
+    for (int e = tid; e < 2 * kWinS * kWinCP; e += win_threads<NCW>()) tstage[e] = 0.0f;
+    for (int e = tid; e < Rd * HP; e += win_threads<NCW>()) d0ring[e] = 0.0f;
+    for (int e = tid; e < R; e += win_threads<NCW>()) rowflag[e] = 0u;
     if (tid == 0) {
-        for (int r = 0; r < kWinRing; ++r) mbar_init(MB(kMbD0 + r), 32);
+        for (int r = 0; r < kWinRing; ++r) mbar_init(MB(kMbD0 + r), 32 * NCW);
         for (int r = 0; r < 2; ++r) {
             mbar_init(MB(kMbYFull + r), 32);
-            mbar_init(MB(kMbYFree + r), 32);
+            mbar_init(MB(kMbYFree + r), 32 * NCW);
         }
-        for (int r = 0; r < kWinBlkRing; ++r) mbar_init(MB(kMbBlk + r), 32);
+        for (int r = 0; r < kWinBlkRing; ++r) mbar_init(MB(kMbBlk + r), 32 * NCW);
     }
     __syncthreads();
 
-    if (warp == kWinCrit) {
-        // ================= the serial chain =================
+    if (win_chain_index<NCW>(warp) >= 0) {
+        // ================= the serial chain (NCW warps) =================
+        // chain warp cw owns hidden units [cw*32*JPL + JPL*lane, +JPL); the
+        // partial logits of the NCW warps meet in shared memory once per sample
         constexpr int CC = CT > 0 ? CT : kWinCP;
-        constexpr int NQ = JPL / 4;
-        const bool kval = lane < C;  // lane k also owns class k (totals, b1)
+        constexpr int XS = 32 * NCW + 4;  // row stride of the transposed partials
+        const int cw = win_chain_index<NCW>(warp);
+        const int j0 = cw * 32 * JPL + JPL * lane;  // first owned hidden unit
+        const bool jval = j0 < H;                   // H % 4 == 0: all JPL units valid or none
+        const bool kval = lane < C;                 // lane k also owns class k (totals, b1)
+        const int kr = lane & (kWinCP - 1);         // class row summed by this lane
         float w1[JPL][CC], b0r[JPL], dp1[JPL], dp2[JPL], aprev[JPL], ndkp[CC];
 #pragma unroll
         for (int m = 0; m < JPL; ++m) {
-            const int j = JPL * lane + m;
+            const int j = j0 + m;
 #pragma unroll
             for (int k = 0; k < CC; ++k) w1[m][k] = (j < H && k < C) ? A.W1[(size_t)j * C + k] : 0.0f;
             b0r[m] = j < H ? A.b0[j] : 0.0f;
@@ -481,13 +534,17 @@ __device__ __forceinline__ void win_chain(const WinArgs& A, float* sm, const Win
         }
 #pragma unroll
         for (int k = 0; k < CC; ++k) ndkp[k] = 0.0f;
-        float b1k = kval ? A.b1[lane] : 0.0f;
+        float b1k = kval ? A.b1[lane] : 0.0f;  // every chain warp keeps an identical copy
         float zl[JPL], zkl = 0.0f, pkl = 0.0f, dkl = 0.0f;  // last sample's z0, z1, p, d1
 #pragma unroll
         for (int m = 0; m < JPL; ++m) zl[m] = 0.0f;
-        // prefetched operands of the next sample
+        float* const xr = red;                                // [16][XS] partial logits
+        float* const half0 = red + kWinCP * XS;                   // [2][NCW][16] per-warp class sums
+        float* const zt = half0 + 2 * NCW * kWinCP + cw * kWinCP;  // this warp's logits copy
+        float* const es = zt + NCW * kWinCP;                       // this warp's exponentials copy
+        // prefetched operands of the next sample (raw: sums at first use)
         constexpr int kMaxKS = 4;
-        float4 zraw[NQ], yraw[kMaxKS][NQ];  // row s+1: window sums and the KS partial Y quads
+        float zraw[JPL], yraw[kMaxKS][JPL];
         float tn[CC], c1n = 0.0f, c2n = 0.0f, town = 0.0f;
         auto flag_wait = [&](int s1, int s1R) {
             if (s1 < 3) return;  // rows 0..2: the chain applies every correction itself
@@ -507,17 +564,15 @@ __device__ __forceinline__ void win_chain(const WinArgs& A, float* sm, const Win
         auto fetch_row = [&](int s1, int s1R, int s1Rd) {
             const int b1 = s1 >> 4, u1 = s1 & (kWinS - 1), st1 = b1 & 1;
             if (u1 == 0) mbar_wait_cta(MB(kMbYFull + st1), (uint32_t)((b1 >> 1) & 1), A.error);
-            // raw loads only: the sums happen at first use (next iteration), so
-            // nothing here waits on shared-memory latency
-            const float4* zr = reinterpret_cast<const float4*>(zacc + s1R * HP) + lane * NQ;
-            const float4* yr = reinterpret_cast<const float4*>(ystage + ((size_t)st1 * KS * kWinS + u1) * H) + lane * NQ;
+            vld<JPL>(zacc + s1R * HP + j0, zraw);
+            const float* yr = ystage + ((size_t)st1 * KS * kWinS + u1) * H + j0;
 #pragma unroll
-            for (int q = 0; q < NQ; ++q) {
-                zraw[q] = zr[q];
-                const bool qv = 4 * (lane * NQ + q) < H;
+            for (int p = 0; p < kMaxKS; ++p) {
+                if (jval && p < KS)
+                    vld<JPL>(yr + p * kWinS * H, yraw[p]);
+                else
 #pragma unroll
-                for (int p = 0; p < kMaxKS; ++p)
-                    yraw[p][q] = (qv && p < KS) ? yr[q + p * kWinS * (H >> 2)] : make_float4(0.f, 0.f, 0.f, 0.f);
+                    for (int m = 0; m < JPL; ++m) yraw[p][m] = 0.0f;
             }
             const float* tr = tstage + (st1 * kWinS + u1) * kWinCP;
 #pragma unroll
@@ -534,32 +589,19 @@ __device__ __forceinline__ void win_chain(const WinArgs& A, float* sm, const Win
             c2n = s1 >= 2 ? coefs[p2 * QW + 1] : 0.0f;  // c(s1, 2) = coef[s1-2][1]
         };
         if (n > 0) fetch_row(0, 0, 0);
-        int sR = 0, sRd = 0;    // s % R, s % Rd
+        int sR = 0, sRd = 0;      // s % R, s % Rd
         int nR = 1 % R, nRd = 1;  // (s+1) % R, (s+1) % Rd
-        float* const xr = red;                // [k][36]: partial logits, transposed
-        float* const zt = red + kWinCP * 36;  // class logits of this sample
-        float* const es = zt + kWinCP;        // exp(z_k - max) of this sample
         for (int s = 0; s < n; ++s) {
             const int b = s >> 4, u = s & (kWinS - 1), st = b & 1;
             WIN_TRACE(s, 0);
             // -- z(s) = Y + window + c1 d0(s-1) + c2 d0(s-2) + b0;  tanh.
             //    The deferred W1 update of s-1 fills the tanh latency.
-            float z[JPL], a[JPL], t[CC], zpre[JPL];
+            float z[JPL], a[JPL], t[CC];
             const float tow = town;
 #pragma unroll
-            for (int q = 0; q < NQ; ++q) {  // Y = fixed-order sum of the KS partials
-                const float4 y01 = make_float4(yraw[0][q].x + yraw[1][q].x, yraw[0][q].y + yraw[1][q].y,
-                                               yraw[0][q].z + yraw[1][q].z, yraw[0][q].w + yraw[1][q].w);
-                const float4 y23 = make_float4(yraw[2][q].x + yraw[3][q].x, yraw[2][q].y + yraw[3][q].y,
-                                               yraw[2][q].z + yraw[3][q].z, yraw[2][q].w + yraw[3][q].w);
-                zpre[4 * q + 0] = zraw[q].x + (y01.x + y23.x);
-                zpre[4 * q + 1] = zraw[q].y + (y01.y + y23.y);
-                zpre[4 * q + 2] = zraw[q].z + (y01.z + y23.z);
-                zpre[4 * q + 3] = zraw[q].w + (y01.w + y23.w);
-            }
-#pragma unroll
             for (int m = 0; m < JPL; ++m) {
-                z[m] = fmaf(c1n, dp1[m], fmaf(c2n, dp2[m], zpre[m])) + b0r[m];
+                const float y = zraw[m] + ((yraw[0][m] + yraw[1][m]) + (yraw[2][m] + yraw[3][m]));
+                z[m] = fmaf(c1n, dp1[m], fmaf(c2n, dp2[m], y)) + b0r[m];
                 a[m] = tanhf(z[m]);
             }
 #pragma unroll
@@ -576,28 +618,44 @@ __device__ __forceinline__ void win_chain(const WinArgs& A, float* sm, const Win
 #pragma unroll
                 for (int k = 0; k < CC; ++k) w1[m][k] = fmaf(ndkp[k], aprev[m], w1[m][k]);
             WIN_TRACE(s, 1);
-            // -- partial logits -> shared memory (transposed), lane k sums class k
+            // -- partial logits -> shared memory (transposed); each warp sums its
+            //    own 32 columns per class, then one barrier joins the NCW warps
 #pragma unroll
             for (int k = 0; k < CC; ++k) {
                 float acc = 0.0f;
 #pragma unroll
                 for (int m = 0; m < JPL; ++m) acc = fmaf(a[m], w1[m][k], acc);
-                xr[k * 36 + lane] = acc;
+                xr[k * XS + cw * 32 + lane] = acc;
             }
             __syncwarp();
-            // every lane sums a class row (lanes >= 16 repeat rows 0..15: no
-            // branch); lanes k < C publish theirs
-            float zown;
+            float zown1 = 0.0f;
             {
-                const float4* col = reinterpret_cast<const float4*>(xr + (lane & (kWinCP - 1)) * 36);
+                const float4* col = reinterpret_cast<const float4*>(xr + kr * XS + cw * 32);
                 float4 v[8];
 #pragma unroll
                 for (int q = 0; q < 8; ++q) v[q] = col[q];
                 float t8[8];
 #pragma unroll
                 for (int q = 0; q < 8; ++q) t8[q] = (v[q].x + v[q].y) + (v[q].z + v[q].w);
-                const float tot = ((t8[0] + t8[1]) + (t8[2] + t8[3])) + ((t8[4] + t8[5]) + (t8[6] + t8[7]));
-                zown = sadd(tot, b1k);
+                const float hs = ((t8[0] + t8[1]) + (t8[2] + t8[3])) + ((t8[4] + t8[5]) + (t8[6] + t8[7]));
+                // halves are double-buffered by sample parity: a warp can run one
+                // sample ahead of its peer past the barrier, never two
+                float* const half = half0 + (s & 1) * NCW * kWinCP;
+                if (NCW > 1) {
+                    if (kval) half[cw * kWinCP + lane] = hs;
+                } else {
+                    zown1 = sadd(hs, b1k);
+                    if (kval) zt[lane] = zown1;
+                }
+            }
+            float zown = zown1;
+            if (NCW > 1) {
+                named_sync(1, 32 * NCW);
+                const float* const half = half0 + (s & 1) * NCW * kWinCP;
+                float hsum = half[kr];
+#pragma unroll
+                for (int c = 1; c < NCW; ++c) hsum += half[c * kWinCP + kr];
+                zown = sadd(hsum, b1k);
                 if (kval) zt[lane] = zown;
             }
             __syncwarp();
@@ -631,12 +689,8 @@ __device__ __forceinline__ void win_chain(const WinArgs& A, float* sm, const Win
                 ek[4 * k4 + 3] = v.w;
             }
 #pragma unroll
-            for (int k = CC; k < 4 * CV; ++k) ek[k] = 0.0f;
-            if (CT == 0) {
-#pragma unroll
-                for (int k = 0; k < 4 * CV; ++k)
-                    if (k >= C) ek[k] = 0.0f;
-            }
+            for (int k = 0; k < 4 * CV; ++k)
+                if (k >= CC || (CT == 0 && k >= C)) ek[k] = 0.0f;
             // tree sum (fixed order)
             float sp[4 * CV];
 #pragma unroll
@@ -645,11 +699,11 @@ __device__ __forceinline__ void win_chain(const WinArgs& A, float* sm, const Win
             for (int wdt = 1; wdt < 4 * CV; wdt <<= 1)
 #pragma unroll
                 for (int k = 0; k + wdt < 4 * CV; k += 2 * wdt) sp[k] += sp[k + wdt];
-            const float sum = sp[0];
-            const float inv = rcp_approx(sum);
+            const float inv = rcp_approx(sp[0]);
             float d1[CC];
 #pragma unroll
             for (int k = 0; k < CC; ++k) d1[k] = k < C ? ssub(ek[k] * inv, t[k]) : 0.0f;
+            // d0 = (1 - a^2) * (W1 d1) with the pre-update W1
             float d0v[JPL];
 #pragma unroll
             for (int m = 0; m < JPL; ++m) {
@@ -659,10 +713,7 @@ __device__ __forceinline__ void win_chain(const WinArgs& A, float* sm, const Win
                 d0v[m] = tanh_grad(a[m], acc);
             }
             WIN_TRACE(s, 3);
-            float4* dr = reinterpret_cast<float4*>(d0ring + sRd * HP) + lane * NQ;
-#pragma unroll
-            for (int q = 0; q < NQ; ++q)
-                dr[q] = make_float4(d0v[4 * q], d0v[4 * q + 1], d0v[4 * q + 2], d0v[4 * q + 3]);
+            vst<JPL>(d0ring + sRd * HP + j0, d0v);
             mbar_arrive_cta(MB(kMbD0 + (s & (kWinRing - 1))));
             WIN_TRACE(s, 4);
             // -- off the chain: p and d1 of the lane's own class, stats, biases
@@ -670,7 +721,7 @@ __device__ __forceinline__ void win_chain(const WinArgs& A, float* sm, const Win
             for (int k = 0; k < CC; ++k) ndkp[k] = neg_eta * d1[k];
             const float pk = eown * inv;
             const float dk = kval ? ssub(pk, tow) : 0.0f;
-            if (kval) pring[sRd * kWinCP + lane] = pk;
+            if (cw == 0 && kval) pring[sRd * kWinCP + lane] = pk;
             b1k = fmaf(neg_eta, dk, b1k);
             zkl = zown;
             pkl = pk;
@@ -685,9 +736,8 @@ __device__ __forceinline__ void win_chain(const WinArgs& A, float* sm, const Win
                 dp2[m] = dp1[m];
                 dp1[m] = d0v[m];
                 aprev[m] = a[m];
+                zl[m] = z[m];
             }
-#pragma unroll
-            for (int m = 0; m < JPL; ++m) zl[m] = z[m];
             WIN_TRACE(s, 5);
             sR = nR;
             sRd = nRd;
@@ -703,7 +753,7 @@ __device__ __forceinline__ void win_chain(const WinArgs& A, float* sm, const Win
                 for (int k = 0; k < CC; ++k) w1[m][k] = fmaf(ndkp[k], aprev[m], w1[m][k]);
 #pragma unroll
             for (int m = 0; m < JPL; ++m) {
-                const int j = JPL * lane + m;
+                const int j = j0 + m;
                 if (j < H) {
 #pragma unroll
                     for (int k = 0; k < CC; ++k)
@@ -716,7 +766,7 @@ __device__ __forceinline__ void win_chain(const WinArgs& A, float* sm, const Win
                     A.x1[j] = aprev[m];
                 }
             }
-            if (kval) {
+            if (cw == 0 && kval) {
                 A.b1[lane] = b1k;
                 A.z1[lane] = zkl;
                 A.a1[lane] = pkl;
@@ -724,7 +774,7 @@ __device__ __forceinline__ void win_chain(const WinArgs& A, float* sm, const Win
                 A.db1[lane] = smul(neg_eta, dkl);
             }
         }
-    } else if (warp == kWinLoad) {
+    } else if (warp == win_loader_warp<NCW>()) {
         // ================= loader: Y(b), targets, coefficient rows =================
         // Forward band rows of block b (its own sources) go to ring slots
         // s % Rd with Y(b): block b-D-1's slots, long retired.
@@ -793,7 +843,7 @@ __device__ __forceinline__ void win_chain(const WinArgs& A, float* sm, const Win
             if (lane != 0) mbar_arrive_cta(MB(kMbYFull + st));  // lane 0 arrived with expect_tx
             WIN_TRACE(s0, 10);
         }
-    } else if (warp == kWinPub) {
+    } else if (warp == win_pub_warp<NCW>()) {
         // ================= publisher: d0 blocks to L2, loss/accuracy =================
         double loss_acc = (lane == 0 && A.loss_sum) ? *A.loss_sum : 0.0;
         unsigned long long correct_acc = 0;
@@ -850,13 +900,13 @@ __device__ __forceinline__ void win_chain(const WinArgs& A, float* sm, const Win
             if (A.loss_sum) *A.loss_sum = loss_acc;
             if (A.correct) *A.correct += correct_acc;
         }
-    } else {
+    } else if (win_helper_index<NCW>(warp) >= 0) {
         // ================= helpers: window corrections =================
         // d0(s) goes to every pending row r in [s+3, last] owned by this warp
         // (r = w mod NH): z(r) += c(r, r-s) d0(s), c from the forward band row
         // of source s.  Rows are visited in ascending order, so an owned row
         // s+3 (the next one the chain fetches) is flagged first.
-        const int w = win_helper_index(warp);
+        const int w = win_helper_index<NCW>(warp);
         int sR = 0, sRd = 0;  // s % R, s % Rd
         for (int s = 0; s < n; ++s) {
             const int b = s >> 4;
@@ -868,7 +918,7 @@ __device__ __forceinline__ void win_chain(const WinArgs& A, float* sm, const Win
             const float4* dv = reinterpret_cast<const float4*>(d0ring + sRd * HP);
             const float* cs = coefs + sRd * QW - s - 1;  // cs[r] = c(r, r-s)
             // this lane's d0 quads, once per sample
-            constexpr int NQH = JPL / 4;  // float4 per lane per row (HP = 128 JPL / 4 ... )
+            constexpr int NQH = JPL * NCW / 4;  // float4 per lane per row (HP = 32 JPL NCW)
             float4 dq[NQH];
 #pragma unroll
             for (int i = 0; i < NQH; ++i) {
@@ -947,14 +997,15 @@ __device__ __forceinline__ void win_chain(const WinArgs& A, float* sm, const Win
 #undef WIN_TRACE
 }
 
-// TR: per-phase clock64 trace of the chain CTA (diagnostics build only)
-template <int JPL, int CT, bool TR = false>
-__global__ void __launch_bounds__(kWinThreads, 1) k_sgd_window(WinArgs A) {
+// JPL hidden units per chain lane, CT classes (0 = runtime <= 16), NCW chain
+// warps; TR: per-phase clock64 trace of the chain CTA (diagnostics build only)
+template <int JPL, int CT, int NCW, bool TR = false>
+__global__ void __launch_bounds__(win_threads<NCW>(), 1) k_sgd_window(WinArgs A) {
     extern __shared__ __align__(16) float sm[];
     if (blockIdx.x == 0)
-        win_chain<JPL, CT, TR>(A, sm, WinSmem(32 * JPL, A.D, A.KS, A.H));
+        win_chain<JPL, CT, NCW, TR>(A, sm, WinSmem(32 * JPL * NCW, A.D, A.KS, A.H, NCW));
     else
-        win_producer(A, sm);
+        win_producer<win_threads<NCW>()>(A, sm);
 }
 
 }  // namespace lane_b200

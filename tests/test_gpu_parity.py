@@ -339,11 +339,16 @@ def test_sgd_stream_fast_vs_oracle(lane, fast, monkeypatch, mode, F, H, C, n, st
     (33, [4], 7, 5, 33, 0.1, 3),            # one producer, I % 4 != 0
     (784, [128], 10, 64, 1, 0.01, 3),       # a single step
     (784, [128], 10, 64, 17, 0.01, 3),      # shorter than the window
+    (784, [128], 10, 64, 150, 0.01, -2),    # two chain warps (2 units/lane) instead of one
+    (100, [96], 10, 20, 90, 0.02, -3),      # two chain warps, H % 64 != 0
 ])
 def test_sgd_window_fast_vs_oracle(lane, fast, monkeypatch, F, H, C, n, steps, eta, D):
     # delayed-base windowed kernel: chain CTA + W0 producer CTAs + banded Gram
+    # (D < 0: lag |D| with the chain split over two warps)
     monkeypatch.setenv("LANE_B200_SGD_MODE", "window")
-    monkeypatch.setenv("LANE_B200_SGD_WIN_D", str(D))
+    monkeypatch.setenv("LANE_B200_SGD_WIN_D", str(abs(D)))
+    if D < 0:
+        monkeypatch.setenv("LANE_B200_SGD_WIN_NCW", "2")
     X, T = po.synthetic_dataset(F, C, n, 9)
     order = np.random.default_rng(2).integers(0, n, steps).astype(np.uint32)
     net = lane.build_network(F, H, C, seed=42, device=fast)
