@@ -384,7 +384,9 @@ def main():
     plan = net.sgd_plan()
     peak, peak_kind = load_peaks()
     P = sum(a * b + b for a, b in zip([F] + H, H + [C]))
-    bytes_per_sample = 8 * P + 4 * (F + C)  # every weight read+written once, + the sample
+    # per sample 4P (forward read of W) + 8P (update read+write
+    # of W) + 12 B per activation of every width (x, z, a / delta)
+    bytes_per_sample = 12 * P + 12 * (F + sum(H) + C)
     kernel_ms = float(np.mean(step_ms))
     achieved = bytes_per_sample * n / (kernel_ms / 1000.0) / 1e9
 
@@ -403,12 +405,13 @@ def main():
                                     "grid": "k_sgd_grid"}.get(plan.split()[0], "layer kernels"),
                          "plan": plan,
                          "algorithmic_bytes_per_sample": bytes_per_sample,
-                         "note": "algorithmic bytes = every weight read+written once per sample "
-                                 "(8 B/param) + the sample, i.e. the HBM floor of a design that "
-                                 "streams the weights; this kernel keeps them on chip (DRAM traffic "
-                                 "is the inputs only) and is bound by the serial per-sample chain "
-                                 "(DESIGN.md section 4); achieved uses the whole step (pre-pass + "
-                                 "kernel + G/DW), CUDA events on the library stream"},
+                         "note": "algorithmic bytes per sample = SURVEY 8(d): 12 B/param (forward "
+                                 "read + update read/write of W) + 12 B/activation, the HBM floor of "
+                                 "a design that streams the weights; this kernel keeps them on chip "
+                                 "(DRAM traffic is the inputs only) and is bound by the serial "
+                                 "per-sample chain (DESIGN.md section 4.1); achieved uses the whole "
+                                 "step (Gram pre-pass + kernel + G/DW), CUDA events on the library "
+                                 "stream"},
             "e2e": {"value": e2e, "unit": "samples/s",
                     "h2d_bytes_per_step": int(X.nbytes + T.nbytes),
                     "d2h_bytes_per_step": 8 * 2},
