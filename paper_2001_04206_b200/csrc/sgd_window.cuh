@@ -523,17 +523,17 @@ __device__ __forceinline__ void win_chain(const WinArgs& A, float* sm, const Win
         const bool jval = j0 < H;                   // H % 4 == 0: all JPL units valid or none
         const bool kval = lane < C;                 // lane k also owns class k (totals, b1)
         const int kr = lane & (kWinCP - 1);         // class row summed by this lane
-        float w1[JPL][CC], b0r[JPL], dp1[JPL], dp2[JPL], aprev[JPL], ndkp[CC];
+        float w1[JPL][CC], b0r[JPL], dp1[JPL], dp2[JPL], aprev[JPL], naprev[JPL], d1p[CC];
 #pragma unroll
         for (int m = 0; m < JPL; ++m) {
             const int j = j0 + m;
 #pragma unroll
             for (int k = 0; k < CC; ++k) w1[m][k] = (j < H && k < C) ? A.W1[(size_t)j * C + k] : 0.0f;
             b0r[m] = j < H ? A.b0[j] : 0.0f;
-            dp1[m] = dp2[m] = aprev[m] = 0.0f;
+            dp1[m] = dp2[m] = aprev[m] = naprev[m] = 0.0f;
         }
 #pragma unroll
-        for (int k = 0; k < CC; ++k) ndkp[k] = 0.0f;
+        for (int k = 0; k < CC; ++k) d1p[k] = 0.0f;
         float b1k = kval ? A.b1[lane] : 0.0f;  // every chain warp keeps an identical copy
         float zl[JPL], zkl = 0.0f, pkl = 0.0f, dkl = 0.0f;  // last sample's z0, z1, p, d1
 #pragma unroll
@@ -543,7 +543,7 @@ __device__ __forceinline__ void win_chain(const WinArgs& A, float* sm, const Win
         float* const zt = half0 + 2 * NCW * kWinCP + cw * kWinCP;  // this warp's logits copy
         float* const es = zt + NCW * kWinCP;                       // this warp's exponentials copy
         // prefetched operands of the next sample (raw: sums at first use)
-        constexpr int kMaxKS = 4;
+        constexpr int kMaxKS = 2;  // the plan uses at most 2 row splits
         float zraw[JPL], yraw[kMaxKS][JPL];
         float tn[CC], c1n = 0.0f, c2n = 0.0f, town = 0.0f;
         auto flag_wait = [&](int s1, int s1R) {
@@ -600,7 +600,7 @@ __device__ __forceinline__ void win_chain(const WinArgs& A, float* sm, const Win
             const float tow = town;
 #pragma unroll
             for (int m = 0; m < JPL; ++m) {
-                const float y = zraw[m] + ((yraw[0][m] + yraw[1][m]) + (yraw[2][m] + yraw[3][m]));
+                const float y = zraw[m] + (yraw[0][m] + yraw[1][m]);
                 z[m] = fmaf(c1n, dp1[m], fmaf(c2n, dp2[m], y)) + b0r[m];
                 a[m] = tanhf(z[m]);
             }
@@ -612,11 +612,11 @@ __device__ __forceinline__ void win_chain(const WinArgs& A, float* sm, const Win
                 flag_wait(s + 1, nR);
                 fetch_row(s + 1, nR, nRd);
             }
-            // FAST numerics: the W1 update as one FMA, w + (-eta d1) a
+            // FAST numerics: the W1 update as one FMA, w + d1 (-eta a)
 #pragma unroll
             for (int m = 0; m < JPL; ++m)
 #pragma unroll
-                for (int k = 0; k < CC; ++k) w1[m][k] = fmaf(ndkp[k], aprev[m], w1[m][k]);
+                for (int k = 0; k < CC; ++k) w1[m][k] = fmaf(d1p[k], naprev[m], w1[m][k]);
             WIN_TRACE(s, 1);
             // -- partial logits -> shared memory (transposed); each warp sums its
             //    own 32 columns per class, then one barrier joins the NCW warps
@@ -702,7 +702,7 @@ __device__ __forceinline__ void win_chain(const WinArgs& A, float* sm, const Win
             const float inv = rcp_approx(sp[0]);
             float d1[CC];
 #pragma unroll
-            for (int k = 0; k < CC; ++k) d1[k] = k < C ? ssub(ek[k] * inv, t[k]) : 0.0f;
+            for (int k = 0; k < CC; ++k) d1[k] = k < C ? fmaf(ek[k], inv, -t[k]) : 0.0f;  // p - t
             // d0 = (1 - a^2) * (W1 d1) with the pre-update W1
             float d0v[JPL];
 #pragma unroll
@@ -710,7 +710,7 @@ __device__ __forceinline__ void win_chain(const WinArgs& A, float* sm, const Win
                 float acc = 0.0f;
 #pragma unroll
                 for (int k = 0; k < CC; ++k) acc = fmaf(d1[k], w1[m][k], acc);
-                d0v[m] = tanh_grad(a[m], acc);
+                d0v[m] = fmaf(-a[m], a[m], 1.0f) * acc;  // (1 - a^2) W1 d1
             }
             WIN_TRACE(s, 3);
             vst<JPL>(d0ring + sRd * HP + j0, d0v);
@@ -718,7 +718,7 @@ __device__ __forceinline__ void win_chain(const WinArgs& A, float* sm, const Win
             WIN_TRACE(s, 4);
             // -- off the chain: p and d1 of the lane's own class, stats, biases
 #pragma unroll
-            for (int k = 0; k < CC; ++k) ndkp[k] = neg_eta * d1[k];
+            for (int k = 0; k < CC; ++k) d1p[k] = d1[k];
             const float pk = eown * inv;
             const float dk = kval ? ssub(pk, tow) : 0.0f;
             if (cw == 0 && kval) pring[sRd * kWinCP + lane] = pk;
@@ -736,6 +736,7 @@ __device__ __forceinline__ void win_chain(const WinArgs& A, float* sm, const Win
                 dp2[m] = dp1[m];
                 dp1[m] = d0v[m];
                 aprev[m] = a[m];
+                naprev[m] = neg_eta * a[m];
                 zl[m] = z[m];
             }
             WIN_TRACE(s, 5);
@@ -750,7 +751,7 @@ __device__ __forceinline__ void win_chain(const WinArgs& A, float* sm, const Win
 #pragma unroll
             for (int m = 0; m < JPL; ++m)
 #pragma unroll
-                for (int k = 0; k < CC; ++k) w1[m][k] = fmaf(ndkp[k], aprev[m], w1[m][k]);
+                for (int k = 0; k < CC; ++k) w1[m][k] = fmaf(d1p[k], naprev[m], w1[m][k]);
 #pragma unroll
             for (int m = 0; m < JPL; ++m) {
                 const int j = j0 + m;
