@@ -172,21 +172,26 @@ void gemm_simt_dispatch(GemmCtx& g, int M, int N, int K, const float* A, int lda
 }
 
 // ---- skinny GEMMs (N <= 32: the 10-class output layer) --------------------
-// NN: C[M,N] = A[M,K] B[K,N].  One warp per row, lanes split K (coalesced A
-// row), N partial sums per lane in registers, shuffle-reduced.
+// NN: C[M,N] = A[M,K] B[K,N].  A CTA of kSkNW warps owns one row m; warp w
+// takes the K range [w K/kSkNW, (w+1) K/kSkNW) with lanes striding it
+// (coalesced A row), N partial sums per lane in registers; shuffle reduction
+// per warp, then the kSkNW warp sums in a fixed order (deterministic).
+constexpr int kSkNW = 4;
 template <Epi E>
-__global__ void __launch_bounds__(256) k_gemm_skinny_nn(int M, int N, int K, const float* __restrict__ A,
-                                                        const float* __restrict__ B, float* __restrict__ C,
-                                                        float* __restrict__ C2, const float* __restrict__ bias) {
-    const int warp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5, lane = threadIdx.x & 31;
-    const int nw = (gridDim.x * blockDim.x) >> 5;
-    for (int m = warp; m < M; m += nw) {
+__global__ void __launch_bounds__(32 * kSkNW) k_gemm_skinny_nn(int M, int N, int K, const float* __restrict__ A,
+                                                               const float* __restrict__ B, float* __restrict__ C,
+                                                               float* __restrict__ C2, const float* __restrict__ bias) {
+    __shared__ float part[kSkNW][32];
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int k0 = warp * K / kSkNW, k1 = (warp + 1) * K / kSkNW;
+    for (int m = blockIdx.x; m < M; m += gridDim.x) {
         float acc[32];
 #pragma unroll
         for (int n = 0; n < 32; ++n) acc[n] = 0.0f;
         const float* arow = A + (size_t)m * K;
-        for (int k = lane; k < K; k += 32) {
-            const float a = arow[k];
+#pragma unroll 4
+        for (int k = k0 + lane; k < k1; k += 32) {
+            const float a = __ldg(arow + k);
             const float* brow = B + (size_t)k * N;
 #pragma unroll
             for (int n = 0; n < 32; ++n)
@@ -195,45 +200,70 @@ __global__ void __launch_bounds__(256) k_gemm_skinny_nn(int M, int N, int K, con
 #pragma unroll
         for (int n = 0; n < 32; ++n)
             if (n < N) acc[n] = warp_sum(acc[n]);
-        if (lane < N) {
-            float v = 0.0f;
+        if (lane == 0) {
 #pragma unroll
             for (int n = 0; n < 32; ++n)
-                if (n == lane) v = acc[n];
-            const size_t idx = (size_t)m * N + lane;
-            if constexpr (E == Epi::BIAS || E == Epi::BIAS_TANH) v = sadd(v, bias[lane]);
+                if (n < N) part[warp][n] = acc[n];
+        }
+        __syncthreads();
+        if (threadIdx.x < N) {
+            const int n = threadIdx.x;
+            float v = part[0][n];
+#pragma unroll
+            for (int w = 1; w < kSkNW; ++w) v += part[w][n];
+            const size_t idx = (size_t)m * N + n;
+            if constexpr (E == Epi::BIAS || E == Epi::BIAS_TANH) v = sadd(v, bias[n]);
             C[idx] = v;
             if constexpr (E == Epi::BIAS_TANH) C2[idx] = tanhf(v);
         }
+        __syncthreads();
     }
 }
 
-// TN: C[M,N] = A[K,M]^T B[K,N] (wgrad of the output layer): thread per m
-// (coalesced A rows), K split over blockIdx.y; B rows staged in shared memory;
-// partial sums part[y][m][n] are reduced in a fixed order by k_sum_partials.
-constexpr int kSkinnyKChunk = 256;
-__global__ void __launch_bounds__(256) k_gemm_skinny_tn(int M, int N, int K, const float* __restrict__ A,
-                                                        const float* __restrict__ B, float* __restrict__ part) {
+// TN: C[M,N] = A^T B with A [K][M] (lda = M), B [K][N]; K is the batch.  A CTA
+// owns 32 columns m x one K chunk of kSkinnyKChunk; its 4 warps split the
+// chunk (warp w: k = k0 + w, k0 + w + 4, ...), lanes take consecutive m
+// (coalesced A rows), N accumulators per thread; the 4 partials meet in
+// shared memory (fixed order) and the per-chunk partial sums part[y][m][n]
+// are reduced in a fixed order by k_sum_partials.
+constexpr int kSkinnyKChunk = 128;
+constexpr int kSkTnW = 4;
+__global__ void __launch_bounds__(32 * kSkTnW) k_gemm_skinny_tn(int M, int N, int K, const float* __restrict__ A,
+                                                               const float* __restrict__ B, float* __restrict__ part) {
     __shared__ float bs[kSkinnyKChunk * 32];
+    __shared__ float red[kSkTnW][32][33];
     const int k0 = blockIdx.y * kSkinnyKChunk, k1 = min(K, k0 + kSkinnyKChunk);
     for (int e = threadIdx.x; e < (k1 - k0) * N; e += blockDim.x) bs[e] = B[(size_t)k0 * N + e];
     __syncthreads();
-    const int m = blockIdx.x * blockDim.x + threadIdx.x;
-    if (m >= M) return;
+    const int tx = threadIdx.x & 31, ty = threadIdx.x >> 5;
+    const int m = blockIdx.x * 32 + tx;
     float acc[32];
 #pragma unroll
     for (int n = 0; n < 32; ++n) acc[n] = 0.0f;
-    for (int k = k0; k < k1; ++k) {
-        const float a = A[(size_t)k * M + m];
-        const float* brow = bs + (k - k0) * N;
+    if (m < M) {
+#pragma unroll 4
+        for (int k = k0 + ty; k < k1; k += kSkTnW) {
+            const float a = __ldg(A + (size_t)k * M + m);
+            const float* brow = bs + (k - k0) * N;
 #pragma unroll
-        for (int n = 0; n < 32; ++n)
-            if (n < N) acc[n] = fmaf(a, brow[n], acc[n]);
+            for (int n = 0; n < 32; ++n)
+                if (n < N) acc[n] = fmaf(a, brow[n], acc[n]);
+        }
     }
-    float* out = part + ((size_t)blockIdx.y * M + m) * N;
 #pragma unroll
     for (int n = 0; n < 32; ++n)
-        if (n < N) out[n] = acc[n];
+        if (n < N) red[ty][tx][n] = acc[n];
+    __syncthreads();
+    // thread (tx, ty): outputs n = ty, ty + kSkTnW, ... of column m
+    if (m < M) {
+        float* out = part + ((size_t)blockIdx.y * M + m) * N;
+        for (int n = ty; n < N; n += kSkTnW) {
+            float v = red[0][tx][n];
+#pragma unroll
+            for (int w = 1; w < kSkTnW; ++w) v += red[w][tx][n];
+            out[n] = v;
+        }
+    }
 }
 
 // out[e] = sum_{s < S} part[s*count + e]  (fixed order: deterministic)
@@ -247,19 +277,19 @@ __global__ void k_sum_partials(const float* __restrict__ part, int S, size_t cou
 
 // Column sums gb[o] = sum_b D[b][o], two passes (row chunks, then fixed-order
 // reduction) so tall batches keep every SM busy.
-constexpr int kColChunk = 128;
+constexpr int kColChunk = 32;
 __global__ void k_colsum_part(const float* __restrict__ D, int B, int O, float* __restrict__ part) {
     const int o = blockIdx.x * blockDim.x + threadIdx.x;
     if (o >= O) return;
     const int b0 = blockIdx.y * kColChunk, b1 = min(B, b0 + kColChunk);
-    float v0 = 0.0f, v1 = 0.0f;
+    float v[4] = {0.0f, 0.0f, 0.0f, 0.0f};  // 4 independent chains: loads in flight
     int b = b0;
-    for (; b + 2 <= b1; b += 2) {
-        v0 += D[(size_t)b * O + o];
-        v1 += D[(size_t)(b + 1) * O + o];
+    for (; b + 4 <= b1; b += 4) {
+#pragma unroll
+        for (int u = 0; u < 4; ++u) v[u] += __ldg(D + (size_t)(b + u) * O + o);
     }
-    if (b < b1) v0 += D[(size_t)b * O + o];
-    part[(size_t)blockIdx.y * O + o] = v0 + v1;
+    for (; b < b1; ++b) v[0] += __ldg(D + (size_t)b * O + o);
+    part[(size_t)blockIdx.y * O + o] = (v[0] + v[1]) + (v[2] + v[3]);
 }
 
 inline void colsum(GemmCtx& g, const float* D, int B, int O, float* gb) {
@@ -274,11 +304,12 @@ inline bool gemm_try_skinny(GemmCtx& g, GemmOp op, int M, int N, int K, const fl
                             int ldb, Epi e, float* C, float* C2, const float* bias) {
     if (N > 32) return false;
     if (op == GemmOp::NN && lda == K && ldb == N && e != Epi::TANH_GRAD) {
-        const int blocks = std::max(1, std::min(8 * g.sm_count, (M + 7) / 8));
+        const int blocks = std::max(1, std::min(16 * g.sm_count, M));
+        constexpr int T = 32 * kSkNW;
         switch (e) {
-            case Epi::STORE: k_gemm_skinny_nn<Epi::STORE><<<blocks, 256, 0, g.stream>>>(M, N, K, A, B, C, C2, bias); break;
-            case Epi::BIAS: k_gemm_skinny_nn<Epi::BIAS><<<blocks, 256, 0, g.stream>>>(M, N, K, A, B, C, C2, bias); break;
-            default: k_gemm_skinny_nn<Epi::BIAS_TANH><<<blocks, 256, 0, g.stream>>>(M, N, K, A, B, C, C2, bias); break;
+            case Epi::STORE: k_gemm_skinny_nn<Epi::STORE><<<blocks, T, 0, g.stream>>>(M, N, K, A, B, C, C2, bias); break;
+            case Epi::BIAS: k_gemm_skinny_nn<Epi::BIAS><<<blocks, T, 0, g.stream>>>(M, N, K, A, B, C, C2, bias); break;
+            default: k_gemm_skinny_nn<Epi::BIAS_TANH><<<blocks, T, 0, g.stream>>>(M, N, K, A, B, C, C2, bias); break;
         }
         *g.launches += 1;
         return true;
@@ -286,7 +317,7 @@ inline bool gemm_try_skinny(GemmCtx& g, GemmOp op, int M, int N, int K, const fl
     if (op == GemmOp::TN && lda == M && ldb == N && e == Epi::STORE) {
         const int S = (K + kSkinnyKChunk - 1) / kSkinnyKChunk;
         ensure_ws(g, (size_t)S * M * N);
-        k_gemm_skinny_tn<<<dim3((M + 255) / 256, S), 256, 0, g.stream>>>(M, N, K, A, B, *g.ws);
+        k_gemm_skinny_tn<<<dim3((M + 31) / 32, S), 32 * kSkTnW, 0, g.stream>>>(M, N, K, A, B, *g.ws);
         k_sum_partials<<<std::max(1, std::min(4 * g.sm_count, (M * N + 255) / 256)), 256, 0, g.stream>>>(
             *g.ws, S, (size_t)M * N, C);
         *g.launches += 2;

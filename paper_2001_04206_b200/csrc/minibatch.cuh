@@ -130,6 +130,32 @@ __global__ void k_loss_rows(const float* __restrict__ row_loss, int B, double* l
 
 // Momentum SGD on a flat range: g = gsum * invB; DW = mu*DW + (-eta)*g;
 // W += DW.  Writes the mean gradient back to gsum (LANE_BUF_G semantics).
+// the whole parameter set in one pass: params, grads and velocities share one
+// arena layout (W_0 | b_0 | W_1 | ...; 256-byte pieces, zero padding), so
+// element e of each region belongs to the same parameter.  16-byte accesses.
+__global__ void k_momentum_update_all(float4* __restrict__ W, float4* __restrict__ DW,
+                                      float4* __restrict__ gsum, size_t n4, float invB, float neg_eta,
+                                      float mu) {
+    for (size_t e = (size_t)blockIdx.x * blockDim.x + threadIdx.x; e < n4;
+         e += (size_t)gridDim.x * blockDim.x) {
+        float4 g = gsum[e], v = DW[e], w = W[e];
+        float* gp = &g.x;
+        float* vp = &v.x;
+        float* wp = &w.x;
+#pragma unroll
+        for (int i = 0; i < 4; ++i) {
+            const float gi = smul(gp[i], invB);
+            gp[i] = gi;
+            const float step = smul(neg_eta, gi);
+            vp[i] = mu == 0.0f ? step : sadd(smul(mu, vp[i]), step);
+            wp[i] = sadd(wp[i], vp[i]);
+        }
+        gsum[e] = g;
+        DW[e] = v;
+        W[e] = w;
+    }
+}
+
 __global__ void k_momentum_update(float* __restrict__ W, float* __restrict__ DW,
                                   float* __restrict__ gsum, size_t n, float invB, float neg_eta,
                                   float mu) {
@@ -194,16 +220,16 @@ void minibatch_step(Ctx& c, Net& net, const float* X, const float* T, size_t Bsz
     // data parallel: one allreduce of the flat gradient-sum buffer
     allreduce_grads(c.comm, net.grads, net.grads_count, st);
     const float invB = 1.0f / static_cast<float>(Bsz * static_cast<size_t>(c.comm.world));
-    for (int l = 0; l < nl; ++l) {
-        auto& Ly = net.L(l);
-        const size_t n = Ly.I * Ly.O;
-        k_momentum_update<<<std::min<size_t>(8 * c.sm_count, (n + 255) / 256), 256, 0, st>>>(
-            Ly.buf[LANE_BUF_W], Ly.buf[LANE_BUF_DW], Ly.buf[LANE_BUF_G], n, invB, -eta, mu);
-        k_momentum_update<<<((int)Ly.O + 255) / 256, 256, 0, st>>>(Ly.buf[LANE_BUF_B],
-                                                                   Ly.buf[LANE_BUF_DELTA_BIASES],
-                                                                   Ly.buf[LANE_BUF_BIAS_GRAD], Ly.O, invB,
-                                                                   -eta, mu);
-        c.launches += 2;
+    {
+        // params | grads | velocities are three equal-layout regions (abi.cu arena)
+        float* W = net.params;
+        float* G = net.grads;
+        float* V = net.grads + net.grads_count;
+        const size_t n4 = net.params_count / 4;
+        k_momentum_update_all<<<std::max<size_t>(1, std::min<size_t>(4 * c.sm_count, (n4 + 255) / 256)), 256, 0,
+                                st>>>(reinterpret_cast<float4*>(W), reinterpret_cast<float4*>(V),
+                                      reinterpret_cast<float4*>(G), n4, invB, -eta, mu);
+        c.launches += 1;
     }
     c.check_launch();
 }
