@@ -364,7 +364,20 @@ inline bool gemm_try_tc(GemmCtx& g, GemmOp op, int M, int N, int K, const float*
             a_mn = b_mn = true;
             break;
     }
-    TcArgs t{M, N, K, C, C2, bias, aux};
+    TcArgs t{M, N, K, 0, nullptr, C, C2, bias, aux};
+    // split-K when the 128x128 tiles fill less than half the SMs (the M = batch
+    // GEMMs at B = 256): S splits of >= 8 K blocks each, <= 4, one wave
+    const int tiles = ((M + kTcBM - 1) / kTcBM) * ((N + kTcBN - 1) / kTcBN);
+    const int nkb = K / kTcBK;
+    int S = std::min({4, g.sm_count / std::max(1, tiles), nkb / 8});
+    if (K % kTcBK != 0 || (N & 3) != 0) S = 1;
+    if (S > 1) {
+        t.kbs = (nkb + S - 1) / S;
+        S = (nkb + t.kbs - 1) / t.kbs;
+        ensure_ws(g, (size_t)S * M * N);
+        t.part = *g.ws;
+        *g.launches += 1;  // the split-K reduce
+    }
     switch (e) {
         case Epi::STORE: tc_dispatch<TcEpi::STORE>(g.stream, a_mn, b_mn, ma, mb, t); break;
         case Epi::BIAS: tc_dispatch<TcEpi::BIAS>(g.stream, a_mn, b_mn, ma, mb, t); break;

@@ -36,6 +36,8 @@ enum class TcEpi : int { STORE = 0, BIAS = 1, BIAS_TANH = 2, TANH_GRAD = 3 };
 
 struct TcArgs {
     int M, N, K;
+    int kbs;            // split-K: K blocks per split (gridDim.z splits); 0 = no split
+    float* part;        // split-K: raw partial tiles [split][M][N] (epilogue runs in the reduce)
     float* C;           // M x N row-major (ldc = N)
     float* C2;          // BIAS_TANH: tanh(C)
     const float* bias;  // BIAS*: per column
@@ -133,7 +135,12 @@ __global__ void __launch_bounds__(kTcThreads, 1)
     uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 16);
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const int m0 = blockIdx.y * kTcBM, n0 = blockIdx.x * kTcBN;
-    const int nkb = (args.K + kTcBK - 1) / kTcBK;
+    // split-K: this CTA accumulates K blocks [kb0, kb1)
+    const int nkb_all = (args.K + kTcBK - 1) / kTcBK;
+    const int kb0 = gridDim.z > 1 ? blockIdx.z * args.kbs : 0;
+    const int kb1 = gridDim.z > 1 ? min(nkb_all, kb0 + args.kbs) : nkb_all;
+    const int nkb = kb1 - kb0;
+    const bool split = gridDim.z > 1;
     const uint32_t sbase = tc_smem(smem);
     auto full = [&](int s) { return tc_smem(bars + s); };
     auto conv = [&](int s) { return tc_smem(bars + 3 + s); };
@@ -173,7 +180,7 @@ __global__ void __launch_bounds__(kTcThreads, 1)
                 const uint32_t ph = (uint32_t)((kb / kTcStages) & 1);
                 tc_mbar_wait(empty(s), ph ^ 1);
                 tc_mbar_expect_tx(full(s), 2 * kTcTile);
-                const int k0 = kb * kTcBK;
+                const int k0 = (kb0 + kb) * kTcBK;
                 if constexpr (!A_MN) {
                     tc_tma_2d(&tmA, full(s), tileA(s), k0, m0);
                 } else {
@@ -266,7 +273,13 @@ __global__ void __launch_bounds__(kTcThreads, 1)
                   "=r"(r[29]), "=r"(r[30]), "=r"(r[31])
                 : "r"(taddr));
             asm volatile("tcgen05.wait::ld.sync.aligned;\n" ::: "memory");
-            if (m < args.M) {
+            if (m < args.M && split) {
+                // raw partial; bias/activation are applied by k_tc_splitk_reduce
+                float* P = args.part + (size_t)blockIdx.z * args.M * args.N + (size_t)m * args.N;
+                const int nb = n0 + c0;
+                for (int q = 0; q < 32; ++q)
+                    if (nb + q < args.N) P[nb + q] = __uint_as_float(r[q]);
+            } else if (m < args.M) {
                 const int nb = n0 + c0;
                 if (nb + 32 <= args.N && (args.N & 3) == 0) {
 #pragma unroll
@@ -299,6 +312,28 @@ __global__ void __launch_bounds__(kTcThreads, 1)
     if (warp == 1) {
         asm volatile("tcgen05.fence::after_thread_sync;\n" ::: "memory");
         asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;\n" ::"r"(tmem), "r"(kTcBN));
+    }
+}
+
+// C = epilogue(sum_z part[z]) in a fixed split order (deterministic); N % 4 == 0
+template <TcEpi E>
+__global__ void __launch_bounds__(256) k_tc_splitk_reduce(TcArgs a, int S) {
+    const size_t n4 = (size_t)a.M * a.N / 4;
+    const float4* P = reinterpret_cast<const float4*>(a.part);
+    for (size_t e = (size_t)blockIdx.x * blockDim.x + threadIdx.x; e < n4; e += (size_t)gridDim.x * blockDim.x) {
+        float4 v = P[e];
+        for (int z = 1; z < S; ++z) {
+            const float4 p = P[(size_t)z * n4 + e];
+            v.x += p.x;
+            v.y += p.y;
+            v.z += p.z;
+            v.w += p.w;
+        }
+        const int m = (int)((4 * e) / a.N), n = (int)((4 * e) % a.N);
+        float4 t;
+        v = tc_epi4<E>(a, m, n, v, &t);
+        reinterpret_cast<float4*>(a.C)[e] = v;
+        if constexpr (E == TcEpi::BIAS_TANH) reinterpret_cast<float4*>(a.C2)[e] = t;
     }
 }
 
@@ -354,8 +389,13 @@ inline void tc_launch(cudaStream_t st, const CUtensorMap& a, const CUtensorMap& 
                                        (int)kTcSmem));
         configured = true;
     }
-    const dim3 grid((args.N + kTcBN - 1) / kTcBN, (args.M + kTcBM - 1) / kTcBM);
+    const int S = args.kbs > 0 ? (args.K / kTcBK + args.kbs - 1) / args.kbs : 1;
+    const dim3 grid((args.N + kTcBN - 1) / kTcBN, (args.M + kTcBM - 1) / kTcBM, S);
     k_gemm_tc<A_MN, B_MN, E><<<grid, kTcThreads, kTcSmem, st>>>(a, b, args);
+    if (S > 1) {
+        const size_t n4 = (size_t)args.M * args.N / 4;
+        k_tc_splitk_reduce<E><<<(unsigned)std::min<size_t>(1184, (n4 + 255) / 256), 256, 0, st>>>(args, S);
+    }
 }
 
 template <TcEpi E>
