@@ -117,6 +117,29 @@ struct lane_b200_ctx {
     }
 };
 
+// The captured mini-batch step graph and the configuration it was captured for.
+struct MbGraph {
+    struct Key {
+        size_t B = 0;
+        float eta = 0, mu = 0;
+        double* loss = nullptr;
+        int world = 0, numerics = 0, tc = 0;
+        const void* comm = nullptr;
+        bool operator==(const Key& o) const {
+            return B == o.B && eta == o.eta && mu == o.mu && loss == o.loss && world == o.world &&
+                   numerics == o.numerics && tc == o.tc && comm == o.comm;
+        }
+    } key;
+    bool warm = false;
+    cudaGraphExec_t exec = nullptr;
+    uint64_t launches = 0;
+    void reset() {
+        if (exec) cudaGraphExecDestroy(exec);
+        exec = nullptr;
+        warm = false;
+    }
+};
+
 struct LayerBufs {
     size_t I = 0, O = 0;
     float* buf[LANE_BUF_COUNT] = {};
@@ -152,6 +175,7 @@ struct lane_b200_net {
     uint32_t* order = nullptr;
     size_t order_count = 0;
     MinibatchState mb;  // activations + workspaces of the mini-batch path
+    MbGraph mb_graph;   // captured mini-batch step (per configuration)
 
     LayerBufs& L(size_t l) { return layers.at(l); }
     size_t out_layer() const { return n_hidden; }
@@ -979,6 +1003,7 @@ int lane_b200_net_destroy(lane_b200_net* net) {
         cudaFree(net->slots);
         cudaFree(net->win_coef);
         cudaFree(net->win_ring);
+        net->mb_graph.reset();
         cudaFree(net->data);
         cudaFree(net->order);
         lane_b200_ctx* c = net->ctx;
@@ -1265,7 +1290,44 @@ int lane_b200_minibatch_step(lane_b200_net* net, const float* X, const float* T,
         if (!net) throw Error(LANE_ERR_CONFIG, "null network");
         check_eta(eta);
         if (B == 0 || B > net->max_batch) throw Error(LANE_ERR_SHAPE, "minibatch: B must be in [1, max_batch]");
-        minibatch_step(*net->ctx, *net, X, T, B, eta, mu, loss_sum);
+        lane_b200_ctx* c = net->ctx;
+        minibatch_stage(*c, *net, X, T, B);
+        // The step body runs eagerly once per configuration (sizing every
+        // workspace), then as a captured CUDA graph: ~20 launches -> one.
+        MbGraph& gr = net->mb_graph;
+        const MbGraph::Key key{B, eta, mu, loss_sum, c->comm.world, c->numerics, gemm_tc_mode(),
+                               static_cast<const void*>(c->comm.comm)};
+        const bool use_graph = !std::getenv("LANE_B200_MB_NOGRAPH");
+        if (use_graph && gr.exec && gr.key == key) {
+            LANE_CUDA(cudaGraphLaunch(gr.exec, c->stream));
+            c->count(static_cast<int>(gr.launches));
+        } else if (use_graph && gr.warm && gr.key == key) {
+            gr.reset();
+            cudaGraph_t graph = nullptr;
+            const uint64_t before = c->launches;
+            LANE_CUDA(cudaStreamBeginCapture(c->stream, cudaStreamCaptureModeThreadLocal));
+            try {
+                minibatch_body(*c, *net, B, eta, mu, loss_sum);
+            } catch (...) {
+                cudaStreamEndCapture(c->stream, &graph);
+                if (graph) cudaGraphDestroy(graph);
+                throw;
+            }
+            LANE_CUDA(cudaStreamEndCapture(c->stream, &graph));
+            gr.launches = c->launches - before;
+            c->launches = before;
+            LANE_CUDA(cudaGraphInstantiate(&gr.exec, graph, 0));
+            LANE_CUDA(cudaGraphDestroy(graph));
+            gr.key = key;
+            LANE_CUDA(cudaGraphLaunch(gr.exec, c->stream));
+            c->count(static_cast<int>(gr.launches));
+        } else {
+            gr.reset();
+            minibatch_body(*c, *net, B, eta, mu, loss_sum);
+            gr.key = key;
+            gr.warm = true;
+        }
+        c->check_launch();
     });
 }
 

@@ -172,18 +172,27 @@ __global__ void k_momentum_update(float* __restrict__ W, float* __restrict__ DW,
 
 // --------------------------------------------------------------- driver ---
 
+// Stage a batch: the first layer's inputs (LayerState::inputs) and the
+// targets, device to device.  Kept out of the captured step graph so the graph
+// only ever touches the network's own buffers.
 template <class Ctx, class Net>
-void minibatch_step(Ctx& c, Net& net, const float* X, const float* T, size_t Bsz, float eta,
-                    float mu, double* loss_sum) {
+void minibatch_stage(Ctx& c, Net& net, const float* X, const float* T, size_t Bsz) {
+    if (net.classes > 128) throw Error(LANE_ERR_CONFIG, "minibatch: classes must be <= 128");
+    LANE_CUDA(cudaMemcpyAsync(net.L(0).buf[LANE_BUF_INPUTS], X, Bsz * net.input_width * sizeof(float),
+                              cudaMemcpyDeviceToDevice, c.stream));
+    LANE_CUDA(cudaMemcpyAsync(net.target_stage, T, Bsz * net.classes * sizeof(float), cudaMemcpyDeviceToDevice,
+                              c.stream));
+}
+
+// The step on the staged batch: forward, softmax/CE, dgrad, wgrad, one
+// allreduce (DP), the fused momentum update.  Capturable in a CUDA graph.
+template <class Ctx, class Net>
+void minibatch_body(Ctx& c, Net& net, size_t Bsz, float eta, float mu, double* loss_sum) {
     const int B = static_cast<int>(Bsz);
     const int nl = static_cast<int>(net.layers.size());
     const int C = static_cast<int>(net.classes);
-    if (C > 128) throw Error(LANE_ERR_CONFIG, "minibatch: classes must be <= 128");
     cudaStream_t st = c.stream;
     GemmCtx g{c.stream, c.sm_count, &net.mb.ws, &net.mb.ws_count, &c.launches};
-    // cache the batch as the first layer's inputs (LayerState::inputs)
-    LANE_CUDA(cudaMemcpyAsync(net.L(0).buf[LANE_BUF_INPUTS], X, Bsz * net.input_width * sizeof(float),
-                              cudaMemcpyDeviceToDevice, st));
     // forward
     for (int l = 0; l < nl; ++l) {
         auto& Ly = net.L(l);
@@ -195,7 +204,6 @@ void minibatch_step(Ctx& c, Net& net, const float* X, const float* T, size_t Bsz
              Ly.buf[LANE_BUF_B], nullptr);
     }
     auto& out = net.L(nl - 1);
-    LANE_CUDA(cudaMemcpyAsync(net.target_stage, T, Bsz * C * sizeof(float), cudaMemcpyDeviceToDevice, st));
     ensure_ws(g, (size_t)B);  // per-row losses live in the GEMM workspace between GEMMs
     k_softmax_rows<<<(B * 32 + 255) / 256, 256, 0, st>>>(out.buf[LANE_BUF_NETIN], out.buf[LANE_BUF_OUTPUTS],
                                                           net.target_stage, out.buf[LANE_BUF_DELTAS],

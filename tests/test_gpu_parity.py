@@ -493,11 +493,12 @@ def test_minibatch_b1_mu0_reduces_to_backward_plan(lane, fast):
 @pytest.mark.parametrize("F,H,C,B,mu", [(64, [96, 80], 10, 32, 0.9), (130, [200], 7, 17, 0.0),
                                         (1024, [512, 512], 10, 64, 0.9)])
 def test_minibatch_momentum_vs_oracle(lane, fast, F, H, C, B, mu):
-    X, T = po.synthetic_dataset(F, C, 3 * B, 4)
+    # 4 steps: eager (sizes the workspaces), graph capture, two graph replays
+    X, T = po.synthetic_dataset(F, C, 4 * B, 4)
     net = lane.build_network(F, H, C, seed=1, device=fast, max_batch=B)
     orc = po.OracleNet(F, H, C, seed=1)
     Xd, Td = upload(fast, X), upload(fast, T)
-    for s in range(3):
+    for s in range(4):
         net.minibatch_step(Xd + s * B * F * 4, Td + s * B * C * 4, B, 0.05, mu)
         orc.minibatch_step(X[s * B:(s + 1) * B], T[s * B:(s + 1) * B], 0.05, mu)
     for l, layer in enumerate(net.layers):
