@@ -313,6 +313,7 @@ struct SgdPlan {
     bool window = false;   // delayed-base windowed kernel (chain CTA + W0 producers)
     int jpl = 4, D = 3;    // window plan: hidden units per chain lane, lag in blocks
     int ncw = 1;           // window plan: chain warps
+    int cs = 1, qpc = 1;   // window plan: chain CTAs (cluster), column quads per producer
     int ks = 1, rpc = 0;   // window plan: producer row splits per column quad, rows per split
     bool cluster = false;  // single thread-block cluster, DSMEM exchange
     bool w0_smem = true;   // grid plan: W0 slices resident in shared memory
@@ -371,6 +372,37 @@ SgdKernel grid_kernel(int C, bool w0_smem) {
     return C == 10 ? k_sgd_grid<10, false> : k_sgd_grid<0, false>;
 }
 
+using WinKernel = void (*)(WinArgs);
+constexpr int kWinWideQPC = 8;  // wide producers: 8 column quads x 2 W0 rows per thread
+
+// co-resident CTAs of a cluster launch of the windowed kernel (cluster size cs)
+int window_cluster_capacity(int cs, size_t smem) {
+    static int cached_cs = 0, cached = 0;
+    static size_t cached_smem = 0;
+    if (cs == cached_cs && smem == cached_smem) return cached;
+    const WinKernel kern = k_sgd_window<4, 10, 1, true, kWinMaxQPC>;
+    cudaFuncSetAttribute(kern, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
+    cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
+    cudaLaunchConfig_t cfg{};
+    cfg.gridDim = dim3(cs);
+    cfg.blockDim = dim3(win_threads<1>());
+    cfg.dynamicSmemBytes = smem;
+    cudaLaunchAttribute at[1];
+    at[0].id = cudaLaunchAttributeClusterDimension;
+    at[0].val.clusterDim.x = cs;
+    at[0].val.clusterDim.y = 1;
+    at[0].val.clusterDim.z = 1;
+    cfg.attrs = at;
+    cfg.numAttrs = 1;
+    int nclusters = 0;
+    if (cudaOccupancyMaxActiveClusters(&nclusters, kern, &cfg) != cudaSuccess) nclusters = 0;
+    cudaGetLastError();
+    cached_cs = cs;
+    cached_smem = smem;
+    cached = nclusters * cs;
+    return cached;
+}
+
 SgdPlan plan_persistent(lane_b200_net* net) {
     SgdPlan p;
     lane_b200_ctx* c = net->ctx;
@@ -383,32 +415,49 @@ SgdPlan plan_persistent(lane_b200_net* net) {
         // windowed plan: the chain on one CTA, W0 on H/4 producer CTAs
         int D = 2;  // measured best at C2 (producers keep up with one block of lag)
         if (const char* e = std::getenv("LANE_B200_SGD_WIN_D")) D = std::max(2, std::min(std::atoi(e), kWinMaxD));
-        // chain geometry: H <= 64 -> 1 warp x 4 units/lane; <= 128 -> 2 warps x 2;
-        // <= 256 -> 2 warps x 4
-        // (measured at C2: one chain warp 1.83M samples/s, two 1.68M -- the
-        // barrier and the duplicated softmax outweigh the halved H work)
-        int ncw = H <= 128 ? 1 : 2;
-        if (const char* e = std::getenv("LANE_B200_SGD_WIN_NCW")) ncw = (std::atoi(e) == 1 && H <= 128) ? 1 : 2;
+        // chain geometry: H <= 128 -> one chain warp x 4 units/lane; <= 256 ->
+        // two warps x 4 (measured at C2: one warp 1.83M samples/s, two 1.68M --
+        // the barrier and the duplicated softmax outweigh the halved H work);
+        // wider -> CS = H/128 chain CTAs in one cluster, one warp each, with a
+        // DSMEM exchange of the slice partial logits per sample
+        int cs = 1;
+        if (H > 256) cs = next_pow2((H + 127) / 128);
+        int ncw = (H <= 128 || cs > 1) ? 1 : 2;
+        if (const char* e = std::getenv("LANE_B200_SGD_WIN_NCW"))
+            if (cs == 1) ncw = (std::atoi(e) == 1 && H <= 128) ? 1 : 2;
         const int jpl = ncw == 1 ? 4 : (H <= 128 ? 2 : 4);
-        // producers: H/4 column quads x KS row splits (<= 2 splits, >= 32 rows
-        // each, as SMs allow); rows per split a multiple of 4 (cp.async 16 B)
+        const int Hs = H / cs;
+        // producers: H/4 column quads (QPC per CTA) x KS row splits (<= 2
+        // splits, >= 32 rows each); rows per split a multiple of 4 (cp.async 16 B)
         const int quads = std::max(1, H / 4);
-        int ks = std::max(1, std::min({2, (c->sm_count - 1) / quads, std::max(1, I / 32)}));
-        if (const char* e = std::getenv("LANE_B200_SGD_WIN_KS")) ks = std::max(1, std::min(std::atoi(e), 4));
+        int pmax = c->sm_count - cs;
+        int ks = std::max(1, std::min({2, pmax / quads, std::max(1, I / 32)}));
+        if (const char* e = std::getenv("LANE_B200_SGD_WIN_KS")) ks = std::max(1, std::min(std::atoi(e), 2));
         const int rpc = (((I + ks - 1) / ks) + 3) & ~3;
         ks = (I + rpc - 1) / rpc;
-        const WinSmem L(32 * jpl * ncw, D, ks, H, ncw);
+        const WinSmem L(32 * jpl * ncw, D, ks, Hs, ncw);
         const ProdSmem PL(rpc, D);
         const size_t smem = std::max(L.total, PL.total);
-        if (H % 4 == 0 && H <= 256 && C <= kWinCP && rpc <= kWinMaxNR * 224 &&
-            1 + quads * ks <= c->sm_count && smem <= c->max_smem_optin) {
+        // co-resident CTAs: one per SM; clusters of cs must also fit the GPCs
+        int max_ctas = c->sm_count;
+        if (cs > 1 && cs <= kWinMaxCS && smem <= c->max_smem_optin)
+            max_ctas = std::min(max_ctas, window_cluster_capacity(cs, smem));
+        pmax = std::max(1, max_ctas - cs);
+        const int qpc = std::max(1, (quads * ks + pmax - 1) / pmax);
+        const int producers = ((quads + qpc - 1) / qpc) * ks;
+        const int grid = ((cs + producers + cs - 1) / cs) * cs;  // a whole number of clusters
+        if (H % (4 * cs) == 0 && Hs <= 32 * jpl * ncw && cs <= kWinMaxCS && C <= kWinCP &&
+            rpc <= (qpc > kWinMaxQPC ? 2 : kWinMaxNR) * 224 && qpc <= (cs > 1 ? kWinWideQPC : 1) &&
+            grid <= max_ctas && smem <= c->max_smem_optin) {
             p.ok = p.window = true;
             p.jpl = jpl;
             p.ncw = ncw;
+            p.cs = cs;
+            p.qpc = qpc;
             p.D = D;
             p.ks = ks;
             p.rpc = rpc;
-            p.G = 1 + quads * ks;
+            p.G = grid;
             p.smem = smem;
             return p;
         }
@@ -574,9 +623,12 @@ void launch_persistent(lane_b200_net* net, const SgdPlan& P, const float* X, con
     c->check_launch();
 }
 
-using WinKernel = void (*)(WinArgs);
-
-WinKernel window_kernel(int jpl, int ncw, int C) {
+// cluster chains: producers with up to 4 quads x 4 rows/thread, or 8 quads x 2 rows
+WinKernel window_kernel(int jpl, int ncw, int C, int cs, int qpc) {
+    if (cs > 1 && qpc > kWinMaxQPC)
+        return C == 10 ? k_sgd_window<4, 10, 1, true, kWinWideQPC, 2> : k_sgd_window<4, 0, 1, true, kWinWideQPC, 2>;
+    if (cs > 1)
+        return C == 10 ? k_sgd_window<4, 10, 1, true, kWinMaxQPC> : k_sgd_window<4, 0, 1, true, kWinMaxQPC>;
     if (ncw == 1) return C == 10 ? k_sgd_window<4, 10, 1> : C == 3 ? k_sgd_window<4, 3, 1> : k_sgd_window<4, 0, 1>;
     if (jpl == 2) return C == 10 ? k_sgd_window<2, 10, 2> : k_sgd_window<2, 0, 2>;
     return C == 10 ? k_sgd_window<4, 10, 2> : k_sgd_window<4, 0, 2>;
@@ -604,7 +656,9 @@ void launch_window(lane_b200_net* net, const SgdPlan& P, const float* X, const f
     A.D = P.D;
     A.KS = P.ks;
     A.RPC = P.rpc;
-    A.P = (H / 4) * P.ks;
+    A.QPC = P.qpc;
+    A.CS = P.cs;
+    A.P = ((H / 4 + P.qpc - 1) / P.qpc) * P.ks;  // active producers
     A.QW = QW;
     A.X = X;
     A.T = T;
@@ -647,14 +701,34 @@ void launch_window(lane_b200_net* net, const SgdPlan& P, const float* X, const f
     // banded Gram pre-pass
     k_gram_band<<<static_cast<unsigned>((n_steps + kGramTS - 1) / kGramTS), 256, 0, c->stream>>>(A);
     c->count();
-    const WinKernel kern = (A.trace && P.jpl == 2 && P.ncw == 2 && A.C == 10) ? k_sgd_window<2, 10, 2, true>
-                           : (A.trace && P.jpl == 4 && P.ncw == 1 && A.C == 10) ? k_sgd_window<4, 10, 1, true>
-                                                                                 : window_kernel(P.jpl, P.ncw, A.C);
+    const WinKernel kern = (A.trace && P.jpl == 4 && P.ncw == 1 && P.cs == 1 && A.C == 10)
+                               ? k_sgd_window<4, 10, 1, false, 1, kWinMaxNR, true>
+                               : window_kernel(P.jpl, P.ncw, A.C, P.cs, P.qpc);
     LANE_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(P.smem)));
     void* args[] = {&A};
     const int nthreads = P.ncw == 2 ? win_threads<2>() : win_threads<1>();
-    LANE_CUDA(cudaLaunchCooperativeKernel(reinterpret_cast<void*>(kern), dim3(P.G), dim3(nthreads), args,
-                                          P.smem, c->stream));
+    if (P.cs == 1) {
+        LANE_CUDA(cudaLaunchCooperativeKernel(reinterpret_cast<void*>(kern), dim3(P.G), dim3(nthreads), args,
+                                              P.smem, c->stream));
+    } else {
+        // chain CTAs form one cluster (CTAs 0..CS-1); every CTA co-resident
+        LANE_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
+        cudaLaunchConfig_t cfg{};
+        cfg.gridDim = dim3(P.G);
+        cfg.blockDim = dim3(nthreads);
+        cfg.dynamicSmemBytes = P.smem;
+        cfg.stream = c->stream;
+        cudaLaunchAttribute at[2];
+        at[0].id = cudaLaunchAttributeClusterDimension;
+        at[0].val.clusterDim.x = P.cs;
+        at[0].val.clusterDim.y = 1;
+        at[0].val.clusterDim.z = 1;
+        at[1].id = cudaLaunchAttributeCooperative;
+        at[1].val.cooperative = 1;
+        cfg.attrs = at;
+        cfg.numAttrs = 2;
+        LANE_CUDA(cudaLaunchKernelEx(&cfg, kern, A));
+    }
     c->count();
     if (A.trace) {
         std::vector<unsigned long long> h(trace_n);
@@ -1198,8 +1272,8 @@ int lane_b200_sgd_stream_plan(lane_b200_net* net, char* buf, size_t len) {
         if (!P.ok)
             std::snprintf(tmp, sizeof tmp, "layer");
         else if (P.window)
-            std::snprintf(tmp, sizeof tmp, "window D=%d KS=%d chain=%dx%d ctas=%d smem=%zu", P.D, P.ks, P.ncw,
-                          32 * P.jpl, P.G, P.smem);
+            std::snprintf(tmp, sizeof tmp, "window D=%d KS=%d QPC=%d chain=%dx%dx%d ctas=%d smem=%zu", P.D, P.ks,
+                          P.qpc, P.cs, P.ncw, 32 * P.jpl, P.G, P.smem);
         else if (P.cluster)
             std::snprintf(tmp, sizeof tmp, "cluster ctas=%d smem=%zu", P.G, P.smem);
         else

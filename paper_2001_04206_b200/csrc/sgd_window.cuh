@@ -108,10 +108,13 @@ constexpr int kWinRing = 16;                 // d0-ready / row-ready mbarrier ri
 constexpr int kWinBlkRing = 8;               // block-done mbarrier ring (> D)
 constexpr int kWinMaxNR = 4;                 // producer: W0 rows per thread (I <= 4 * 352)
 constexpr int kWinCP = 16;                   // classes padded for the transpose-reduce
+constexpr int kWinMaxCS = 16;                // chain CTAs per cluster
 
 struct WinArgs {
     int I, H, C, D, P, QW;
-    int KS, RPC;  // producers: row splits per column quad, rows per split (P = H/4 * KS)
+    int KS, RPC;  // producers: row splits per column group, rows per split
+    int QPC;      // producers: column quads per CTA (P = ceil(H/4 / QPC) * KS active producers)
+    int CS;       // chain CTAs (one thread-block cluster); producers are CTAs CS..
     const float* X;
     const float* T;
     const uint32_t* order;  // stream order (offset to this launch) or null
@@ -136,8 +139,9 @@ struct WinArgs {
 
 struct WinSmem {
     int HP, R, Rd;
-    size_t zacc, ystage, tstage, coefs, d0ring, pring, red, d0s, rowflag, mbar, total;
-    __host__ __device__ WinSmem(int HP_, int D, int KS, int H, int NCW) : HP(HP_) {
+    size_t zacc, ystage, tstage, coefs, d0ring, pring, red, d0s, rowflag, gat, mbar, total;
+    // HP_: padded hidden slice per chain CTA; Hs: the slice width (H / CS)
+    __host__ __device__ WinSmem(int HP_, int D, int KS, int Hs, int NCW) : HP(HP_) {
         R = D * kWinS;
         Rd = (D + 1) * kWinS;
         size_t o = 0;
@@ -147,7 +151,7 @@ struct WinSmem {
             return at;
         };
         zacc = take((size_t)R * HP);
-        ystage = take(2 * (size_t)KS * kWinS * H);  // [buffer][ks][u][H] (TMA bulk copies)
+        ystage = take(2 * (size_t)KS * kWinS * Hs);  // [buffer][ks][u][Hs] (TMA bulk copies)
         tstage = take(2 * kWinS * kWinCP);
         coefs = take((size_t)Rd * D * kWinS);  // forward band rows of source s, slot s % Rd
         d0ring = take((size_t)Rd * HP);
@@ -155,13 +159,15 @@ struct WinSmem {
         red = take(kWinCP * (32 * NCW + 4) + 4 * NCW * kWinCP);  // partials, halves x2, logits, exps
         d0s = take(kWinS * 4);
         rowflag = take(R);
-        mbar = take(2 * (kWinRing + 4 + kWinBlkRing));
+        gat = take(2 * kWinMaxCS * kWinCP);  // [parity][rank][class]: cluster logit exchange
+        mbar = take(2 * (kWinRing + 6 + kWinBlkRing));
         total = o * sizeof(float);
     }
 };
 
 // mbarrier indices (u64 slots)
-constexpr int kMbD0 = 0, kMbYFull = kWinRing, kMbYFree = kWinRing + 2, kMbBlk = kWinRing + 4;
+constexpr int kMbD0 = 0, kMbYFull = kWinRing, kMbYFree = kWinRing + 2, kMbBlk = kWinRing + 4,
+              kMbXch = kWinRing + 4 + kWinBlkRing;  // 2 exchange barriers (by sample parity)
 
 __device__ __forceinline__ void mbar_arrive_cta(uint32_t a) {
     asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];\n" ::"r"(a) : "memory");
@@ -284,16 +290,19 @@ __global__ void __launch_bounds__(256) k_gram_band(WinArgs A) {
 }
 
 // ---------------------------------------------------------------------------
-// Producer CTAs.  CTA (pc, ks) owns W0 columns [4pc, 4pc+4) x rows
-// [ks*RPC, ks*RPC + RPC) in registers for the whole stream.  The X rows of
-// the last D+2 blocks of its row range sit in a shared-memory ring, filled by
-// cp.async one iteration ahead: block k's rows arrive for Y(k) (iteration
-// k-D) and are reused for block k's weight update (iteration k).  Per block
-// k: acquire d0 of block k, apply its S per-sample updates with the
-// reference's exact rounding (w + (-eta * (d0 * x)), sample by sample), then
-// publish the partial Y(k+D) of this row range; the chain sums the KS
-// partials of a column quad in a fixed order.
+// Producer CTAs.  Producer (pc, ks) owns W0 columns [4 pc QPC, 4 (pc+1) QPC)
+// (QPC column quads) x rows [ks*RPC, ks*RPC + RPC) in registers for the whole
+// stream.  The X rows of the last D+2 blocks of its row range sit in a
+// shared-memory ring, filled by cp.async one iteration ahead: block k's rows
+// arrive for Y(k) (iteration k-D) and are reused for block k's weight update
+// (iteration k).  Per block k: acquire d0 of block k (all CS chain CTAs), apply
+// its S per-sample updates with the reference's exact rounding
+// (w + (-eta * (d0 * x)), sample by sample), then publish the partial Y(k+D)
+// of this row range; the chain sums the KS partials of a column in a fixed
+// order.
 // ---------------------------------------------------------------------------
+constexpr int kWinMaxQPC = 4;  // column quads per producer CTA
+
 struct ProdSmem {
     int RPCp, NB;
     size_t xr, d0s, red, total;
@@ -307,18 +316,21 @@ struct ProdSmem {
             return at;
         };
         xr = take((size_t)NB * kWinS * RPCp);
-        d0s = take(kWinS * 4);
+        d0s = take(kWinS * 8 * 4);  // [u][quad] float4, up to 8 quads
         red = take(kWinWarps * 64);
         total = o * sizeof(float);
     }
 };
 
-template <int NT>
+template <int NT, int MQ, int NR>
 __device__ __forceinline__ void win_producer(const WinArgs& A, float* sm) {
     const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
-    const int I = A.I, H = A.H, D = A.D, KS = A.KS, RPC = A.RPC;
-    const int pc = (blockIdx.x - 1) / KS, ks = (blockIdx.x - 1) - pc * KS;
-    const int col = 4 * pc, i0 = ks * RPC, nr = max(0, min(I, i0 + RPC) - i0);
+    const int I = A.I, H = A.H, D = A.D, KS = A.KS, RPC = A.RPC, QPC = A.QPC;
+    const int pid = blockIdx.x - A.CS;
+    const int pc = pid / KS, ks = pid - pc * KS;
+    const int q0 = pc * QPC, nq = max(0, min(QPC, (H >> 2) - q0));  // this CTA's column quads
+    if (nq == 0) return;                                           // padding CTA of the cluster grid
+    const int i0 = ks * RPC, nr = max(0, min(I, i0 + RPC) - i0);
     const int n = A.n_steps;
     const int nblk = (n + kWinS - 1) / kWinS;
     const int YR = D + 1, DR = D + 1;
@@ -327,25 +339,28 @@ __device__ __forceinline__ void win_producer(const WinArgs& A, float* sm) {
     const int RPCp = L.RPCp, NB = L.NB;
     float* xr = sm + L.xr;
     float* red = sm + L.red;
-    float4* d0s = reinterpret_cast<float4*>(sm + L.d0s);
+    float4* d0s = reinterpret_cast<float4*>(sm + L.d0s);  // [u][quad]
     const bool vec = ((I & 3) == 0) && ((i0 & 3) == 0) && ((nr & 3) == 0) &&
                      ((reinterpret_cast<uintptr_t>(A.X) & 15) == 0);
 
-    float4 w[kWinMaxNR];
+    float4 w[MQ][NR];
 #pragma unroll
-    for (int m = 0; m < kWinMaxNR; ++m) {
-        const int li = tid + NT * m;
-        w[m] = li < nr ? *reinterpret_cast<const float4*>(A.W0 + (size_t)(i0 + li) * H + col)
-                       : make_float4(0.f, 0.f, 0.f, 0.f);
-    }
+    for (int qi = 0; qi < MQ; ++qi)
+#pragma unroll
+        for (int m = 0; m < NR; ++m) {
+            const int li = tid + NT * m;
+            w[qi][m] = (qi < nq && li < nr)
+                           ? *reinterpret_cast<const float4*>(A.W0 + (size_t)(i0 + li) * H + 4 * (q0 + qi))
+                           : make_float4(0.f, 0.f, 0.f, 0.f);
+        }
     // X rows [i0, i0+nr) of block blk -> ring slot blk % NB (cp.async, no wait)
     auto prefetch = [&](int blk) {
         float* dst = xr + (size_t)(blk % NB) * kWinS * RPCp;
         const int s0 = blk * kWinS, nv = min(kWinS, n - s0);
         if (vec) {
-            const int nq = nr >> 2;
-            for (int e = tid; e < nv * nq; e += NT) {
-                const int u = e / nq, q = e - u * nq;
+            const int nq4 = nr >> 2;
+            for (int e = tid; e < nv * nq4; e += NT) {
+                const int u = e / nq4, q = e - u * nq4;
                 cp_async16(dst + u * RPCp + 4 * q, A.X + win_row(A, s0 + u) * I + i0 + 4 * q);
             }
         } else {
@@ -355,43 +370,52 @@ __device__ __forceinline__ void win_producer(const WinArgs& A, float* sm) {
             }
         }
     };
-    // partial Y(blk)[u][col..col+3] over this row range, from the current registers
+    // partial Y(blk)[u][cols] over this row range from the current registers,
+    // one column quad at a time (64 accumulators per thread)
     auto compute_y = [&](int blk) {
         const float* xb = xr + (size_t)(blk % NB) * kWinS * RPCp;
         const int nv = min(kWinS, n - blk * kWinS);
-        float acc[4 * kWinS];
 #pragma unroll
-        for (int e = 0; e < 4 * kWinS; ++e) acc[e] = 0.0f;
+        for (int qi = 0; qi < MQ; ++qi) {
+            if (qi >= nq) break;
+            float acc[4 * kWinS];
 #pragma unroll
-        for (int m = 0; m < kWinMaxNR; ++m) {
-            const int li = tid + NT * m;
-            if (li < nr) {
+            for (int e = 0; e < 4 * kWinS; ++e) acc[e] = 0.0f;
 #pragma unroll
-                for (int u = 0; u < kWinS; ++u) {
-                    const float x = u < nv ? xb[u * RPCp + li] : 0.0f;
-                    acc[4 * u + 0] = fmaf(x, w[m].x, acc[4 * u + 0]);
-                    acc[4 * u + 1] = fmaf(x, w[m].y, acc[4 * u + 1]);
-                    acc[4 * u + 2] = fmaf(x, w[m].z, acc[4 * u + 2]);
-                    acc[4 * u + 3] = fmaf(x, w[m].w, acc[4 * u + 3]);
+            for (int m = 0; m < NR; ++m) {
+                const int li = tid + NT * m;
+                if (li < nr) {
+#pragma unroll
+                    for (int u = 0; u < kWinS; ++u) {
+                        const float x = u < nv ? xb[u * RPCp + li] : 0.0f;
+                        acc[4 * u + 0] = fmaf(x, w[qi][m].x, acc[4 * u + 0]);
+                        acc[4 * u + 1] = fmaf(x, w[qi][m].y, acc[4 * u + 1]);
+                        acc[4 * u + 2] = fmaf(x, w[qi][m].z, acc[4 * u + 2]);
+                        acc[4 * u + 3] = fmaf(x, w[qi][m].w, acc[4 * u + 3]);
+                    }
                 }
             }
-        }
-        // 64 values -> 2 per lane (indices 2*lane, 2*lane+1)
-        xpose_step<64>(acc, lane, 16);
-        xpose_step<32>(acc, lane, 8);
-        xpose_step<16>(acc, lane, 4);
-        xpose_step<8>(acc, lane, 2);
-        xpose_step<4>(acc, lane, 1);
-        red[warp * 64 + 2 * lane] = acc[0];
-        red[warp * 64 + 2 * lane + 1] = acc[1];
-        __syncthreads();
-        if (tid < 4 * kWinS) {
-            float y = 0.0f;
+            // 64 values -> 2 per lane (indices 2*lane, 2*lane+1)
+            xpose_step<64>(acc, lane, 16);
+            xpose_step<32>(acc, lane, 8);
+            xpose_step<16>(acc, lane, 4);
+            xpose_step<8>(acc, lane, 2);
+            xpose_step<4>(acc, lane, 1);
+            red[warp * 64 + 2 * lane] = acc[0];
+            red[warp * 64 + 2 * lane + 1] = acc[1];
+            __syncthreads();
+            if (tid < 4 * kWinS) {
+                float y = 0.0f;
 #pragma unroll
-            for (int q = 0; q < NT / 32; ++q) y += red[q * 64 + tid];
-            const int u = tid >> 2, c = tid & 3;
-            if (u < nv) __stcg(A.yring + (((size_t)(blk % YR) * KS + ks) * kWinS + u) * H + col + c, y);
-            // each of the two writer warps releases its own stores
+                for (int q = 0; q < NT / 32; ++q) y += red[q * 64 + tid];
+                const int u = tid >> 2, c = tid & 3;
+                if (u < nv)
+                    __stcg(A.yring + (((size_t)(blk % YR) * KS + ks) * kWinS + u) * H + 4 * (q0 + qi) + c, y);
+            }
+            __syncthreads();  // red reuse
+        }
+        // each of the two writer warps releases its own stores
+        if (tid < 4 * kWinS) {
             __syncwarp();
             if (lane == 0) red_release_add(A.ycnt + (blk % YR), 1u);
         }
@@ -402,37 +426,41 @@ __device__ __forceinline__ void win_producer(const WinArgs& A, float* sm) {
     cp_async_commit();
     cp_async_wait<0>();
     __syncthreads();
-    for (int blk = 0; blk < npro; ++blk) {
-        compute_y(blk);
-        __syncthreads();  // red reuse
-    }
+    for (int blk = 0; blk < npro; ++blk) compute_y(blk);
     for (int k = 0; k < nblk; ++k) {
         const int nv = min(kWinS, n - k * kWinS);
         if (k + D + 1 < nblk) prefetch(k + D + 1);  // slot of block k-1: retired
         cp_async_commit();
-        if (tid == 0) spin_geq(A.dcnt, (unsigned)(k + 1), A.error);
+        if (tid == 0) spin_geq(A.dcnt, (unsigned)(A.CS * (k + 1)), A.error);
         __syncthreads();
-        if (tid < kWinS)
-            d0s[tid] = tid < nv ? __ldcg(reinterpret_cast<const float4*>(
-                                      A.dring + ((size_t)(k % DR) * kWinS + tid) * H + col))
-                                : make_float4(0.f, 0.f, 0.f, 0.f);
+        if (tid < kWinS * MQ) {
+            const int u = tid / MQ, qi = tid - u * MQ;
+            d0s[tid] = (u < nv && qi < nq) ? __ldcg(reinterpret_cast<const float4*>(
+                                                 A.dring + ((size_t)(k % DR) * kWinS + u) * H + 4 * (q0 + qi)))
+                                           : make_float4(0.f, 0.f, 0.f, 0.f);
+        }
         cp_async_wait<1>();  // block k+D's rows (prefetched last iteration) have landed
         __syncthreads();
         // the S per-sample updates, reference rounding, in sample order
         const float* xb = xr + (size_t)(k % NB) * kWinS * RPCp;
 #pragma unroll
-        for (int m = 0; m < kWinMaxNR; ++m) {
+        for (int m = 0; m < NR; ++m) {
             const int li = tid + NT * m;
             if (li < nr) {
 #pragma unroll
                 for (int u = 0; u < kWinS; ++u) {
                     if (u < nv) {
-                        const float4 d = d0s[u];
                         const float x = xb[u * RPCp + li];
-                        w[m].x = sgd_apply(w[m].x, neg_eta, d.x, x);
-                        w[m].y = sgd_apply(w[m].y, neg_eta, d.y, x);
-                        w[m].z = sgd_apply(w[m].z, neg_eta, d.z, x);
-                        w[m].w = sgd_apply(w[m].w, neg_eta, d.w, x);
+#pragma unroll
+                        for (int qi = 0; qi < MQ; ++qi) {
+                            if (qi < nq) {
+                                const float4 d = d0s[u * MQ + qi];
+                                w[qi][m].x = sgd_apply(w[qi][m].x, neg_eta, d.x, x);
+                                w[qi][m].y = sgd_apply(w[qi][m].y, neg_eta, d.y, x);
+                                w[qi][m].z = sgd_apply(w[qi][m].z, neg_eta, d.z, x);
+                                w[qi][m].w = sgd_apply(w[qi][m].w, neg_eta, d.w, x);
+                            }
+                        }
                     }
                 }
             }
@@ -442,11 +470,14 @@ __device__ __forceinline__ void win_producer(const WinArgs& A, float* sm) {
     }
     cp_async_wait<0>();
 #pragma unroll
-    for (int m = 0; m < kWinMaxNR; ++m) {
-        const int li = tid + NT * m;
-        if (li < nr) *reinterpret_cast<float4*>(A.W0 + (size_t)(i0 + li) * H + col) = w[m];
-    }
-    if (blockIdx.x == 1 && n > 0) {
+    for (int qi = 0; qi < MQ; ++qi)
+#pragma unroll
+        for (int m = 0; m < NR; ++m) {
+            const int li = tid + NT * m;
+            if (qi < nq && li < nr)
+                *reinterpret_cast<float4*>(A.W0 + (size_t)(i0 + li) * H + 4 * (q0 + qi)) = w[qi][m];
+        }
+    if (pid == 0 && n > 0) {
         const float* xl = A.X + win_row(A, n - 1) * I;
         for (int i = tid; i < I; i += NT) A.x0[i] = xl[i];
     }
@@ -469,11 +500,15 @@ __device__ __forceinline__ float rcp_approx(float x) {
 // ---------------------------------------------------------------------------
 // Chain CTA.
 // ---------------------------------------------------------------------------
-template <int JPL, int CT, int NCW, bool TR>
+template <int JPL, int CT, int NCW, bool CLU, bool TR>
 __device__ __forceinline__ void win_chain(const WinArgs& A, float* sm, const WinSmem& L) {
     const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
-    const int H = A.H, D = A.D, HP = L.HP, R = L.R, Rd = L.Rd, QW = A.QW, KS = A.KS;
-    const int HQ = H >> 2;  // float4 per row
+    // CS chain CTAs (one cluster) split the hidden layer: rank r owns units
+    // [h0, h0 + Hs); everything H-wide in this CTA is slice-local
+    const int CS = CLU ? A.CS : 1, rank = CLU ? (int)cluster_ctarank() : 0;
+    const int H = A.H, Hs = H / CS, h0 = rank * Hs;
+    const int D = A.D, HP = L.HP, R = L.R, Rd = L.Rd, QW = A.QW, KS = A.KS;
+    const int HQ = Hs >> 2;  // float4 per slice row
     const int C = CT > 0 ? CT : A.C;
     const int n = (int)A.n_steps;  // <= 2^18 per launch (host chunks the stream)
     const int nblk = (n + kWinS - 1) / kWinS;
@@ -487,6 +522,7 @@ __device__ __forceinline__ void win_chain(const WinArgs& A, float* sm, const Win
     float* pring = sm + L.pring;
     float* red = sm + L.red;
     unsigned* rowflag = reinterpret_cast<unsigned*>(sm + L.rowflag);
+    float* gat = sm + L.gat;
     const uint32_t mb = smem_u32(sm + L.mbar);
     auto MB = [&](int idx) { return mb + 8u * (uint32_t)idx; };
     unsigned long long* const trace = A.trace;
@@ -498,7 +534,7 @@ __device__ __forceinline__ void win_chain(const WinArgs& A, float* sm, const Win
 
     // ---- prologue: zero the rings, init the barriers
     for (int e = tid; e < R * HP; e += win_threads<NCW>()) zacc[e] = 0.0f;
-    for (int e = tid; e < 2 * A.KS * kWinS * H; e += win_threads<NCW>()) ystage[e] = 0.0f;
+    for (int e = tid; e < 2 * A.KS * kWinS * Hs; e += win_threads<NCW>()) ystage[e] = 0.0f;
     for (int e = tid; e < 2 * kWinS * kWinCP; e += win_threads<NCW>()) tstage[e] = 0.0f;
     for (int e = tid; e < Rd * HP; e += win_threads<NCW>()) d0ring[e] = 0.0f;
     for (int e = tid; e < R; e += win_threads<NCW>()) rowflag[e] = 0u;
@@ -509,8 +545,17 @@ __device__ __forceinline__ void win_chain(const WinArgs& A, float* sm, const Win
             mbar_init(MB(kMbYFree + r), 32 * NCW);
         }
         for (int r = 0; r < kWinBlkRing; ++r) mbar_init(MB(kMbBlk + r), 32 * NCW);
+        if (CS > 1) {
+            // one local arrival (with the expected bytes) + CS*C st.async completions
+            mbar_init(MB(kMbXch + 0), 1);
+            mbar_init(MB(kMbXch + 1), 1);
+            asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
+            if (n > 0) mbar_arrive_expect_tx(MB(kMbXch + 0), (uint32_t)(CS * C * sizeof(float)));
+            if (n > 1) mbar_arrive_expect_tx(MB(kMbXch + 1), (uint32_t)(CS * C * sizeof(float)));
+        }
     }
     __syncthreads();
+    if (CS > 1) cluster_sync_all();  // every chain CTA initialised before remote traffic
 
     if (win_chain_index<NCW>(warp) >= 0) {
         // ================= the serial chain (NCW warps) =================
@@ -519,8 +564,8 @@ __device__ __forceinline__ void win_chain(const WinArgs& A, float* sm, const Win
         constexpr int CC = CT > 0 ? CT : kWinCP;
         constexpr int XS = 32 * NCW + 4;  // row stride of the transposed partials
         const int cw = win_chain_index<NCW>(warp);
-        const int j0 = cw * 32 * JPL + JPL * lane;  // first owned hidden unit
-        const bool jval = j0 < H;                   // H % 4 == 0: all JPL units valid or none
+        const int j0 = cw * 32 * JPL + JPL * lane;  // first owned hidden unit (slice-local)
+        const bool jval = j0 < Hs;                  // Hs % 4 == 0: all JPL units valid or none
         const bool kval = lane < C;                 // lane k also owns class k (totals, b1)
         const int kr = lane & (kWinCP - 1);         // class row summed by this lane
         float w1[JPL][CC], b0r[JPL], dp1[JPL], dp2[JPL], aprev[JPL], naprev[JPL], d1p[CC];
@@ -528,8 +573,8 @@ __device__ __forceinline__ void win_chain(const WinArgs& A, float* sm, const Win
         for (int m = 0; m < JPL; ++m) {
             const int j = j0 + m;
 #pragma unroll
-            for (int k = 0; k < CC; ++k) w1[m][k] = (j < H && k < C) ? A.W1[(size_t)j * C + k] : 0.0f;
-            b0r[m] = j < H ? A.b0[j] : 0.0f;
+            for (int k = 0; k < CC; ++k) w1[m][k] = (j < Hs && k < C) ? A.W1[(size_t)(h0 + j) * C + k] : 0.0f;
+            b0r[m] = j < Hs ? A.b0[h0 + j] : 0.0f;
             dp1[m] = dp2[m] = aprev[m] = naprev[m] = 0.0f;
         }
 #pragma unroll
@@ -565,11 +610,11 @@ __device__ __forceinline__ void win_chain(const WinArgs& A, float* sm, const Win
             const int b1 = s1 >> 4, u1 = s1 & (kWinS - 1), st1 = b1 & 1;
             if (u1 == 0) mbar_wait_cta(MB(kMbYFull + st1), (uint32_t)((b1 >> 1) & 1), A.error);
             vld<JPL>(zacc + s1R * HP + j0, zraw);
-            const float* yr = ystage + ((size_t)st1 * KS * kWinS + u1) * H + j0;
+            const float* yr = ystage + ((size_t)st1 * KS * kWinS + u1) * Hs + j0;
 #pragma unroll
             for (int p = 0; p < kMaxKS; ++p) {
                 if (jval && p < KS)
-                    vld<JPL>(yr + p * kWinS * H, yraw[p]);
+                    vld<JPL>(yr + p * kWinS * Hs, yraw[p]);
                 else
 #pragma unroll
                     for (int m = 0; m < JPL; ++m) yraw[p][m] = 0.0f;
@@ -643,6 +688,32 @@ __device__ __forceinline__ void win_chain(const WinArgs& A, float* sm, const Win
                 float* const half = half0 + (s & 1) * NCW * kWinCP;
                 if (NCW > 1) {
                     if (kval) half[cw * kWinCP + lane] = hs;
+                } else if (CS > 1) {
+                    // cluster: every chain CTA pushes its C slice partials to all
+                    // peers (st.async completes the peer's exchange barrier), then
+                    // sums the CS partials in rank order: identical logits in all
+                    const int par = s & 1;
+                    const uint32_t slot = smem_u32(gat + (par * kWinMaxCS + rank) * kWinCP + lane);
+                    const uint32_t xb = MB(kMbXch + par);
+                    if (kval)
+                        for (int p = 0; p < CS; ++p) st_async_f32(mapa_shared(slot, p), hs, mapa_shared(xb, p));
+                    {
+                        const unsigned long long t0 = globaltimer_ns();
+                        while (!mbar_try_wait(xb, (uint32_t)((s >> 1) & 1))) {
+                            if (globaltimer_ns() - t0 > 5000000000ull) {
+                                atomicExch(A.error, 5);
+                                __trap();
+                            }
+                        }
+                    }
+                    // re-arm for sample s+2: no peer sends s+2 before it holds this
+                    // CTA's partials of s+1, which are sent after this point
+                    if (lane == 0 && s + 2 < n) mbar_arrive_expect_tx(xb, (uint32_t)(CS * C * sizeof(float)));
+                    const float* g = gat + par * kWinMaxCS * kWinCP + kr;
+                    float tot = g[0];
+                    for (int p = 1; p < CS; ++p) tot += g[p * kWinCP];
+                    zown1 = sadd(tot, b1k);
+                    if (kval) zt[lane] = zown1;
                 } else {
                     zown1 = sadd(hs, b1k);
                     if (kval) zt[lane] = zown1;
@@ -721,7 +792,7 @@ __device__ __forceinline__ void win_chain(const WinArgs& A, float* sm, const Win
             for (int k = 0; k < CC; ++k) d1p[k] = d1[k];
             const float pk = eown * inv;
             const float dk = kval ? ssub(pk, tow) : 0.0f;
-            if (cw == 0 && kval) pring[sRd * kWinCP + lane] = pk;
+            if (cw == 0 && rank == 0 && kval) pring[sRd * kWinCP + lane] = pk;
             b1k = fmaf(neg_eta, dk, b1k);
             zkl = zown;
             pkl = pk;
@@ -755,19 +826,20 @@ __device__ __forceinline__ void win_chain(const WinArgs& A, float* sm, const Win
 #pragma unroll
             for (int m = 0; m < JPL; ++m) {
                 const int j = j0 + m;
-                if (j < H) {
+                if (j < Hs) {
+                    const int jg = h0 + j;
 #pragma unroll
                     for (int k = 0; k < CC; ++k)
-                        if (k < C) A.W1[(size_t)j * C + k] = w1[m][k];
-                    A.b0[j] = b0r[m];
-                    A.z0[j] = zl[m];
-                    A.a0[j] = aprev[m];
-                    A.d0[j] = dp1[m];
-                    A.db0[j] = smul(neg_eta, dp1[m]);
-                    A.x1[j] = aprev[m];
+                        if (k < C) A.W1[(size_t)jg * C + k] = w1[m][k];
+                    A.b0[jg] = b0r[m];
+                    A.z0[jg] = zl[m];
+                    A.a0[jg] = aprev[m];
+                    A.d0[jg] = dp1[m];
+                    A.db0[jg] = smul(neg_eta, dp1[m]);
+                    A.x1[jg] = aprev[m];
                 }
             }
-            if (cw == 0 && kval) {
+            if (cw == 0 && rank == 0 && kval) {
                 A.b1[lane] = b1k;
                 A.z1[lane] = zkl;
                 A.a1[lane] = pkl;
@@ -823,20 +895,24 @@ __device__ __forceinline__ void win_chain(const WinArgs& A, float* sm, const Win
             spin_geq(A.ycnt + (b % YR), (unsigned)(2 * A.P * (b / YR + 1)), A.error);  // 2 writer warps per producer
             WIN_TRACE(s0, 9);
             coef_store(b, cv);
-            // Y(b): KS partial slabs by TMA bulk copy, completing yfull's tx count
+            // Y(b): the KS partial slabs of this CTA's slice by TMA bulk copy
+            // (whole rows at once when the slice is the full layer), completing
+            // yfull's transaction count
             if (lane == 0) {
                 asm volatile("fence.proxy.async.global;\n" ::: "memory");  // generic writes -> async proxy
-                const uint32_t bytes = (uint32_t)(nv * H * sizeof(float));
                 const uint32_t mbar = MB(kMbYFull + st);
-                mbar_arrive_expect_tx(mbar, bytes * KS);
+                mbar_arrive_expect_tx(mbar, (uint32_t)(KS * nv * Hs * sizeof(float)));
                 for (int p = 0; p < KS; ++p) {
-                    const float* src = A.yring + (((size_t)(b % YR) * KS + p) * kWinS) * H;
-                    float* dst = ystage + ((size_t)st * KS + p) * kWinS * H;
-                    asm volatile(
-                        "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];\n" ::"r"(
-                            smem_u32(dst)),
-                        "l"(src), "r"(bytes), "r"(mbar)
-                        : "memory");
+                    const float* src = A.yring + (((size_t)(b % YR) * KS + p) * kWinS) * H + h0;
+                    float* dst = ystage + ((size_t)st * KS + p) * kWinS * Hs;
+                    const int nrow = CS == 1 ? 1 : nv;
+                    const uint32_t bytes = (uint32_t)((CS == 1 ? nv * H : Hs) * sizeof(float));
+                    for (int u = 0; u < nrow; ++u)
+                        asm volatile(
+                            "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];\n" ::"r"(
+                                smem_u32(dst + (size_t)u * Hs)),
+                            "l"(src + (size_t)u * H), "r"(bytes), "r"(mbar)
+                            : "memory");
                 }
             }
 #pragma unroll
@@ -848,7 +924,7 @@ __device__ __forceinline__ void win_chain(const WinArgs& A, float* sm, const Win
         // ================= publisher: d0 blocks to L2, loss/accuracy =================
         double loss_acc = (lane == 0 && A.loss_sum) ? *A.loss_sum : 0.0;
         unsigned long long correct_acc = 0;
-        const bool stats = A.loss_sum || A.correct;
+        const bool stats = (A.loss_sum || A.correct) && rank == 0;
         for (int k = 0; k < nblk; ++k) {
             const int s0 = k * kWinS;
             const int nv = min(kWinS, n - s0);
@@ -856,10 +932,12 @@ __device__ __forceinline__ void win_chain(const WinArgs& A, float* sm, const Win
             const long long myrow = (stats && lane < nv) ? win_row(A, s0 + lane) : 0;
             mbar_wait_cta(MB(kMbBlk + k % kWinBlkRing), (uint32_t)((k / kWinBlkRing) & 1), A.error);
             WIN_TRACE(s0, 11);
-            float4* dst = reinterpret_cast<float4*>(A.dring + (size_t)(k % DR) * kWinS * H);
+            // this CTA's slice of the block's d0 rows (dring rows are H wide)
+            float* dst = A.dring + (size_t)(k % DR) * kWinS * H + h0;
             for (int e = lane; e < nv * HQ; e += 32) {
                 const int u = e / HQ, q = e - u * HQ;
-                __stcg(dst + e, reinterpret_cast<const float4*>(d0ring + ((s0 + u) % Rd) * HP)[q]);
+                __stcg(reinterpret_cast<float4*>(dst + (size_t)u * H) + q,
+                       reinterpret_cast<const float4*>(d0ring + ((s0 + u) % Rd) * HP)[q]);
             }
             __threadfence();
             __syncwarp();
@@ -897,7 +975,7 @@ __device__ __forceinline__ void win_chain(const WinArgs& A, float* sm, const Win
             }
             WIN_TRACE(s0 + 2, 11);
         }
-        if (lane == 0) {
+        if (lane == 0 && rank == 0) {
             if (A.loss_sum) *A.loss_sum = loss_acc;
             if (A.correct) *A.correct += correct_acc;
         }
@@ -996,17 +1074,20 @@ __device__ __forceinline__ void win_chain(const WinArgs& A, float* sm, const Win
         }
     }
 #undef WIN_TRACE
+    if (CS > 1) cluster_sync_all();  // no chain CTA exits while a peer may still address it
 }
 
 // JPL hidden units per chain lane, CT classes (0 = runtime <= 16), NCW chain
-// warps; TR: per-phase clock64 trace of the chain CTA (diagnostics build only)
-template <int JPL, int CT, int NCW, bool TR = false>
+// warps, CLU: the chain is split over a cluster of A.CS CTAs (else one CTA),
+// MQ/NR: max column quads per producer CTA / W0 rows per producer thread;
+// TR: per-phase clock64 trace of the chain CTA (diagnostics build only)
+template <int JPL, int CT, int NCW, bool CLU = false, int MQ = 1, int NR = kWinMaxNR, bool TR = false>
 __global__ void __launch_bounds__(win_threads<NCW>(), 1) k_sgd_window(WinArgs A) {
     extern __shared__ __align__(16) float sm[];
-    if (blockIdx.x == 0)
-        win_chain<JPL, CT, NCW, TR>(A, sm, WinSmem(32 * JPL * NCW, A.D, A.KS, A.H, NCW));
+    if ((int)blockIdx.x < (CLU ? A.CS : 1))
+        win_chain<JPL, CT, NCW, CLU, TR>(A, sm, WinSmem(32 * JPL * NCW, A.D, A.KS, A.H / (CLU ? A.CS : 1), NCW));
     else
-        win_producer<win_threads<NCW>()>(A, sm);
+        win_producer<win_threads<NCW>(), MQ, NR>(A, sm);
 }
 
 }  // namespace lane_b200
