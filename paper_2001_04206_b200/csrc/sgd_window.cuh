@@ -483,6 +483,148 @@ __device__ __forceinline__ void win_producer(const WinArgs& A, float* sm) {
     }
 }
 
+// Producer for the single-CTA chain (H <= 256): one column quad per CTA.
+// (The multi-quad producer above costs ~3% at C2: an extra barrier per quad
+// and a later Y release.)
+template <int NT>
+__device__ __forceinline__ void win_producer_v1(const WinArgs& A, float* sm) {
+    const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+    const int I = A.I, H = A.H, D = A.D, KS = A.KS, RPC = A.RPC;
+    const int pc = (blockIdx.x - 1) / KS, ks = (blockIdx.x - 1) - pc * KS;
+    const int col = 4 * pc, i0 = ks * RPC, nr = max(0, min(I, i0 + RPC) - i0);
+    const int n = A.n_steps;
+    const int nblk = (n + kWinS - 1) / kWinS;
+    const int YR = D + 1, DR = D + 1;
+    const float neg_eta = A.neg_eta;
+    const ProdSmem L(RPC, D);
+    const int RPCp = L.RPCp, NB = L.NB;
+    float* xr = sm + L.xr;
+    float* red = sm + L.red;
+    float4* d0s = reinterpret_cast<float4*>(sm + L.d0s);
+    const bool vec = ((I & 3) == 0) && ((i0 & 3) == 0) && ((nr & 3) == 0) &&
+                     ((reinterpret_cast<uintptr_t>(A.X) & 15) == 0);
+
+    float4 w[kWinMaxNR];
+#pragma unroll
+    for (int m = 0; m < kWinMaxNR; ++m) {
+        const int li = tid + NT * m;
+        w[m] = li < nr ? *reinterpret_cast<const float4*>(A.W0 + (size_t)(i0 + li) * H + col)
+                       : make_float4(0.f, 0.f, 0.f, 0.f);
+    }
+    // X rows [i0, i0+nr) of block blk -> ring slot blk % NB (cp.async, no wait)
+    auto prefetch = [&](int blk) {
+        float* dst = xr + (size_t)(blk % NB) * kWinS * RPCp;
+        const int s0 = blk * kWinS, nv = min(kWinS, n - s0);
+        if (vec) {
+            const int nq = nr >> 2;
+            for (int e = tid; e < nv * nq; e += NT) {
+                const int u = e / nq, q = e - u * nq;
+                cp_async16(dst + u * RPCp + 4 * q, A.X + win_row(A, s0 + u) * I + i0 + 4 * q);
+            }
+        } else {
+            for (int e = tid; e < nv * nr; e += NT) {
+                const int u = e / nr, q = e - u * nr;
+                cp_async4(dst + u * RPCp + q, A.X + win_row(A, s0 + u) * I + i0 + q);
+            }
+        }
+    };
+    // partial Y(blk)[u][col..col+3] over this row range, from the current registers
+    auto compute_y = [&](int blk) {
+        const float* xb = xr + (size_t)(blk % NB) * kWinS * RPCp;
+        const int nv = min(kWinS, n - blk * kWinS);
+        float acc[4 * kWinS];
+#pragma unroll
+        for (int e = 0; e < 4 * kWinS; ++e) acc[e] = 0.0f;
+#pragma unroll
+        for (int m = 0; m < kWinMaxNR; ++m) {
+            const int li = tid + NT * m;
+            if (li < nr) {
+#pragma unroll
+                for (int u = 0; u < kWinS; ++u) {
+                    const float x = u < nv ? xb[u * RPCp + li] : 0.0f;
+                    acc[4 * u + 0] = fmaf(x, w[m].x, acc[4 * u + 0]);
+                    acc[4 * u + 1] = fmaf(x, w[m].y, acc[4 * u + 1]);
+                    acc[4 * u + 2] = fmaf(x, w[m].z, acc[4 * u + 2]);
+                    acc[4 * u + 3] = fmaf(x, w[m].w, acc[4 * u + 3]);
+                }
+            }
+        }
+        // 64 values -> 2 per lane (indices 2*lane, 2*lane+1)
+        xpose_step<64>(acc, lane, 16);
+        xpose_step<32>(acc, lane, 8);
+        xpose_step<16>(acc, lane, 4);
+        xpose_step<8>(acc, lane, 2);
+        xpose_step<4>(acc, lane, 1);
+        red[warp * 64 + 2 * lane] = acc[0];
+        red[warp * 64 + 2 * lane + 1] = acc[1];
+        __syncthreads();
+        if (tid < 4 * kWinS) {
+            float y = 0.0f;
+#pragma unroll
+            for (int q = 0; q < NT / 32; ++q) y += red[q * 64 + tid];
+            const int u = tid >> 2, c = tid & 3;
+            if (u < nv) __stcg(A.yring + (((size_t)(blk % YR) * KS + ks) * kWinS + u) * H + col + c, y);
+            // each of the two writer warps releases its own stores
+            __syncwarp();
+            if (lane == 0) red_release_add(A.ycnt + (blk % YR), 1u);
+        }
+    };
+
+    const int npro = min(D, nblk);
+    for (int blk = 0; blk <= npro && blk < nblk; ++blk) prefetch(blk);
+    cp_async_commit();
+    cp_async_wait<0>();
+    __syncthreads();
+    for (int blk = 0; blk < npro; ++blk) {
+        compute_y(blk);
+        __syncthreads();  // red reuse
+    }
+    for (int k = 0; k < nblk; ++k) {
+        const int nv = min(kWinS, n - k * kWinS);
+        if (k + D + 1 < nblk) prefetch(k + D + 1);  // slot of block k-1: retired
+        cp_async_commit();
+        if (tid == 0) spin_geq(A.dcnt, (unsigned)(k + 1), A.error);
+        __syncthreads();
+        if (tid < kWinS)
+            d0s[tid] = tid < nv ? __ldcg(reinterpret_cast<const float4*>(
+                                      A.dring + ((size_t)(k % DR) * kWinS + tid) * H + col))
+                                : make_float4(0.f, 0.f, 0.f, 0.f);
+        cp_async_wait<1>();  // block k+D's rows (prefetched last iteration) have landed
+        __syncthreads();
+        // the S per-sample updates, reference rounding, in sample order
+        const float* xb = xr + (size_t)(k % NB) * kWinS * RPCp;
+#pragma unroll
+        for (int m = 0; m < kWinMaxNR; ++m) {
+            const int li = tid + NT * m;
+            if (li < nr) {
+#pragma unroll
+                for (int u = 0; u < kWinS; ++u) {
+                    if (u < nv) {
+                        const float4 d = d0s[u];
+                        const float x = xb[u * RPCp + li];
+                        w[m].x = sgd_apply(w[m].x, neg_eta, d.x, x);
+                        w[m].y = sgd_apply(w[m].y, neg_eta, d.y, x);
+                        w[m].z = sgd_apply(w[m].z, neg_eta, d.z, x);
+                        w[m].w = sgd_apply(w[m].w, neg_eta, d.w, x);
+                    }
+                }
+            }
+        }
+        if (k + D < nblk) compute_y(k + D);
+        __syncthreads();  // ring slot / d0s / red reuse
+    }
+    cp_async_wait<0>();
+#pragma unroll
+    for (int m = 0; m < kWinMaxNR; ++m) {
+        const int li = tid + NT * m;
+        if (li < nr) *reinterpret_cast<float4*>(A.W0 + (size_t)(i0 + li) * H + col) = w[m];
+    }
+    if (blockIdx.x == 1 && n > 0) {
+        const float* xl = A.X + win_row(A, n - 1) * I;
+        for (int i = tid; i < I; i += NT) A.x0[i] = xl[i];
+    }
+}
+
 __device__ __forceinline__ unsigned ld_acquire_cta_u32(uint32_t saddr) {
     unsigned v;
     asm volatile("ld.acquire.cta.shared::cta.u32 %0, [%1];\n" : "=r"(v) : "r"(saddr) : "memory");
@@ -1086,6 +1228,8 @@ __global__ void __launch_bounds__(win_threads<NCW>(), 1) k_sgd_window(WinArgs A)
     extern __shared__ __align__(16) float sm[];
     if ((int)blockIdx.x < (CLU ? A.CS : 1))
         win_chain<JPL, CT, NCW, CLU, TR>(A, sm, WinSmem(32 * JPL * NCW, A.D, A.KS, A.H / (CLU ? A.CS : 1), NCW));
+    else if constexpr (!CLU)
+        win_producer_v1<win_threads<NCW>()>(A, sm);
     else
         win_producer<win_threads<NCW>(), MQ, NR>(A, sm);
 }
