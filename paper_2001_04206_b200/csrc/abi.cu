@@ -744,6 +744,12 @@ void launch_window(lane_b200_net* net, const SgdPlan& P, const float* X, const f
             std::fclose(f);
         }
     }
+    c->check_launch();
+}
+
+// G and DW of the last sample, as the reference's stream_out leaves them
+void materialise_last_grads(lane_b200_net* net, float eta) {
+    lane_b200_ctx* c = net->ctx;
     for (size_t l = 0; l < 2; ++l) {
         LayerBufs& Ly = net->L(l);
         k_outer<<<blocks_for(Ly.I * Ly.O, 256, 8 * c->sm_count), 256, 0, c->stream>>>(
@@ -810,6 +816,7 @@ void sgd_stream_impl(lane_b200_net* net, const float* X, const float* T, size_t 
             launch_window(net, P, X, T, n, order ? order + done : nullptr, m, static_cast<long long>(done % n),
                           eta, loss_sum, correct);
         }
+        materialise_last_grads(net, eta);
     } else if (P.ok) {
         // the persistent kernels index samples with 32-bit counters
         const size_t chunk = size_t(1) << 30;

@@ -521,3 +521,29 @@ def test_sgd_plan_selection(lane, fast, F, H, C, want):
     # the fused plan the headline shapes run (no silent fallback to layer kernels)
     net = lane.build_network(F, H, C, seed=42, device=fast)
     assert net.sgd_plan().split()[0] == want, net.sgd_plan()
+
+
+def test_sgd_window_long_stream_chunks(lane, fast, monkeypatch):
+    # > 2^18 samples: the stream runs as several window launches (the banded
+    # Gram scratch is per launch); state, loss and accuracy carry across
+    monkeypatch.setenv("LANE_B200_SGD_MODE", "window")
+    F, H, C, n, steps, eta = 4, [8], 3, 135, (1 << 18) + 1000, 0.01
+    X, T = po.synthetic_dataset(F, C, n, 9)
+    net = lane.build_network(F, H, C, seed=42, device=fast)
+    orc = po.OracleNet(F, H, C, seed=42)
+    order = np.random.default_rng(7).integers(0, n, steps).astype(np.uint32)
+    want = orc.sgd_run(X, T, steps, eta, order=order)
+    Xd, Td, Od = upload(fast, X), upload(fast, T), upload(fast, order, np.uint32)
+    Ld = upload(fast, np.zeros(1, np.float64), np.float64)
+    before = fast.kernel_launches
+    net.sgd_stream(Xd, Td, n, steps, eta, order_dev=Od, loss_dev=Ld)
+    fast.sync()
+    assert fast.kernel_launches - before == 2 * 2 + 2  # 2 x (Gram + window) + G/DW x2
+    loss = np.zeros(1, np.float64)
+    fast.d2h(loss, Ld)
+    assert abs(loss[0] - want) <= 1e-4 * abs(want)
+    # 262k chaotic SGD steps: the weights agree loosely, the loss tightly
+    for l, layer in enumerate(net.layers):
+        assert_close(layer.weights, orc.get(l, po.W), 2e-3, f"W{l}")
+    for p in (Xd, Td, Od, Ld):
+        fast.free(p)
