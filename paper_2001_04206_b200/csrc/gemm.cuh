@@ -300,9 +300,119 @@ inline void colsum(GemmCtx& g, const float* D, int B, int O, float* gb) {
     *g.launches += 2;
 }
 
+// NN, K split into chunks with the B chunk staged in shared memory: CTA
+// (row block of 8 rows, K chunk of kSkKC) -- warp w owns row m0+w, lanes
+// stride the chunk (coalesced A row), N partial sums per lane, shuffle
+// reduction; per-chunk partials part[y][m][n] are summed in a fixed order
+// (with the epilogue) by k_sum_partials_epi.
+constexpr int kSkKC = 512;
+__global__ void __launch_bounds__(256) k_gemm_skinny_nn_kc(int M, int N, int K, const float* __restrict__ A,
+                                                           const float* __restrict__ B, float* __restrict__ part) {
+    __shared__ float bs[kSkKC * 16];
+    const int k0 = blockIdx.y * kSkKC, k1 = min(K, k0 + kSkKC);
+    for (int e = threadIdx.x; e < (k1 - k0) * N; e += blockDim.x) bs[e] = B[(size_t)k0 * N + e];
+    __syncthreads();
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int m = blockIdx.x * 8 + warp;
+    if (m >= M) return;
+    float acc[16];
+#pragma unroll
+    for (int n = 0; n < 16; ++n) acc[n] = 0.0f;
+    const float* arow = A + (size_t)m * K;
+#pragma unroll 4
+    for (int k = k0 + lane; k < k1; k += 32) {
+        const float a = __ldg(arow + k);
+        const float* brow = bs + (k - k0) * N;
+#pragma unroll
+        for (int n = 0; n < 16; ++n)
+            if (n < N) acc[n] = fmaf(a, brow[n], acc[n]);
+    }
+#pragma unroll
+    for (int n = 0; n < 16; ++n)
+        if (n < N) acc[n] = warp_sum(acc[n]);
+    if (lane < N) {
+        float v = 0.0f;
+#pragma unroll
+        for (int n = 0; n < 16; ++n)
+            if (n == lane) v = acc[n];
+        part[((size_t)blockIdx.y * M + m) * N + lane] = v;
+    }
+}
+
+// out = epilogue(sum_{s < S} part[s]) in a fixed order; bias per column
+template <Epi E>
+__global__ void k_sum_partials_epi(const float* __restrict__ part, int S, int M, int N, float* __restrict__ C,
+                                   float* __restrict__ C2, const float* __restrict__ bias) {
+    const size_t count = (size_t)M * N;
+    for (size_t e = (size_t)blockIdx.x * blockDim.x + threadIdx.x; e < count; e += (size_t)gridDim.x * blockDim.x) {
+        float v = part[e];
+        for (int s2 = 1; s2 < S; ++s2) v += part[(size_t)s2 * count + e];
+        if constexpr (E == Epi::BIAS || E == Epi::BIAS_TANH) v = sadd(v, bias[e % N]);
+        C[e] = v;
+        if constexpr (E == Epi::BIAS_TANH) C2[e] = tanhf(v);
+    }
+}
+
+// NT with a short K (the output layer's dgrad: D[M][K<=16] W[N][K]^T) and the
+// tanh' epilogue: one thread per output column n holds W[n][:] in registers,
+// 8 rows m per CTA (D rows broadcast from shared memory), sequential k.
+constexpr int kShortK = 16;
+template <Epi E>
+__global__ void __launch_bounds__(256) k_gemm_shortk_nt(int M, int N, int K, const float* __restrict__ D,
+                                                        const float* __restrict__ W, float* __restrict__ C,
+                                                        const float* __restrict__ aux) {
+    __shared__ float ds[8][kShortK];
+    const int n = blockIdx.x * blockDim.x + threadIdx.x;
+    const int m0 = blockIdx.y * 8;
+    for (int e = threadIdx.x; e < 8 * K; e += blockDim.x) {
+        const int r = e / K, k = e - r * K;
+        ds[r][k] = m0 + r < M ? D[(size_t)(m0 + r) * K + k] : 0.0f;
+    }
+    __syncthreads();
+    if (n >= N) return;
+    float w[kShortK];
+#pragma unroll
+    for (int k = 0; k < kShortK; ++k) w[k] = k < K ? __ldg(W + (size_t)n * K + k) : 0.0f;
+#pragma unroll
+    for (int r = 0; r < 8; ++r) {
+        const int m = m0 + r;
+        if (m >= M) break;
+        float acc = 0.0f;
+#pragma unroll
+        for (int k = 0; k < kShortK; ++k)
+            if (k < K) acc = fmaf(ds[r][k], w[k], acc);
+        const size_t idx = (size_t)m * N + n;
+        if constexpr (E == Epi::TANH_GRAD) acc = tanh_grad(aux[idx], acc);
+        C[idx] = acc;
+    }
+}
+
 inline bool gemm_try_skinny(GemmCtx& g, GemmOp op, int M, int N, int K, const float* A, int lda, const float* B,
-                            int ldb, Epi e, float* C, float* C2, const float* bias) {
+                            int ldb, Epi e, float* C, float* C2, const float* bias, const float* aux) {
+    if (op == GemmOp::NT && K <= kShortK && lda == K && ldb == K && (e == Epi::STORE || e == Epi::TANH_GRAD)) {
+        const dim3 grid((N + 255) / 256, (M + 7) / 8);
+        if (e == Epi::STORE)
+            k_gemm_shortk_nt<Epi::STORE><<<grid, 256, 0, g.stream>>>(M, N, K, A, B, C, nullptr);
+        else
+            k_gemm_shortk_nt<Epi::TANH_GRAD><<<grid, 256, 0, g.stream>>>(M, N, K, A, B, C, aux);
+        *g.launches += 1;
+        return true;
+    }
     if (N > 32) return false;
+    if (op == GemmOp::NN && lda == K && ldb == N && e != Epi::TANH_GRAD && N <= 16 && K >= 2 * kSkKC) {
+        // long K: chunked, B chunk in shared memory, fixed-order partial sum
+        const int S = (K + kSkKC - 1) / kSkKC;
+        ensure_ws(g, (size_t)S * M * N);
+        k_gemm_skinny_nn_kc<<<dim3((M + 7) / 8, S), 256, 0, g.stream>>>(M, N, K, A, B, *g.ws);
+        const int blocks = std::max(1, std::min(4 * g.sm_count, (M * N + 255) / 256));
+        switch (e) {
+            case Epi::STORE: k_sum_partials_epi<Epi::STORE><<<blocks, 256, 0, g.stream>>>(*g.ws, S, M, N, C, C2, bias); break;
+            case Epi::BIAS: k_sum_partials_epi<Epi::BIAS><<<blocks, 256, 0, g.stream>>>(*g.ws, S, M, N, C, C2, bias); break;
+            default: k_sum_partials_epi<Epi::BIAS_TANH><<<blocks, 256, 0, g.stream>>>(*g.ws, S, M, N, C, C2, bias); break;
+        }
+        *g.launches += 2;
+        return true;
+    }
     if (op == GemmOp::NN && lda == K && ldb == N && e != Epi::TANH_GRAD) {
         const int blocks = std::max(1, std::min(16 * g.sm_count, M));
         constexpr int T = 32 * kSkNW;
@@ -392,7 +502,7 @@ inline void gemm(GemmCtx& g, GemmOp op, int M, int N, int K, const float* A, int
                  Epi e, float* C, float* C2, const float* bias, const float* aux) {
     if (M <= 0 || N <= 0) return;
     if (gemm_try_tc(g, op, M, N, K, A, lda, B, ldb, e, C, C2, bias, aux)) return;
-    if (gemm_try_skinny(g, op, M, N, K, A, lda, B, ldb, e, C, C2, bias)) return;
+    if (gemm_try_skinny(g, op, M, N, K, A, lda, B, ldb, e, C, C2, bias, aux)) return;
     switch (op) {
         case GemmOp::NN: gemm_simt_dispatch<GemmOp::NN>(g, M, N, K, A, lda, B, ldb, e, C, C2, bias, aux); break;
         case GemmOp::NT: gemm_simt_dispatch<GemmOp::NT>(g, M, N, K, A, lda, B, ldb, e, C, C2, bias, aux); break;

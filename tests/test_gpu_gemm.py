@@ -100,3 +100,36 @@ def test_tensor_core_kernel_is_used(dev):
     from paper_2001_04206_b200 import _build
     sass = subprocess.run(["cuobjdump", "-sass", _build.LIB], capture_output=True, text=True).stdout
     assert "UTCHMMA" in sass and "UTMALDG" in sass and "LDTM" in sass
+
+
+@pytest.mark.parametrize("epi", [STORE, TANH_GRAD])
+def test_shortk_nt_output_layer_dgrad(dev, epi):
+    # D[M][K<=16] W[N][K]^T (x tanh'), the 10-class output layer's dgrad
+    M, N, K = 256, 4100, 10
+    rs = np.random.default_rng(11)
+    A, B, Am, Bm = operands(NT, M, N, K, rs)
+    aux = rs.uniform(-0.99, 0.99, (M, N)).astype(np.float32)
+    out, _, launched = run(dev, NT, M, N, K, A, B, epi, aux=aux if epi == TANH_GRAD else None)
+    ref = Am @ Bm
+    cond = np.abs(Am) @ np.abs(Bm)
+    g = (1 - aux.astype(np.float64) ** 2) if epi == TANH_GRAD else 1.0
+    assert launched == 1
+    assert np.all(np.abs(out - g * ref) <= 1e-5 * g * cond + 1e-30)
+
+
+@pytest.mark.parametrize("epi", [STORE, BIAS, BIAS_TANH])
+def test_skinny_nn_long_k(dev, epi):
+    # A[M][K] B[K][N<=16] with a long K: chunked, fixed-order partial sums
+    M, N, K = 256, 10, 4096 + 96
+    rs = np.random.default_rng(12)
+    A, B, Am, Bm = operands(NN, M, N, K, rs)
+    A *= 0.05
+    Am *= 0.05
+    bias = rs.uniform(-0.5, 0.5, N).astype(np.float32)
+    out, out2, launched = run(dev, NN, M, N, K, A, B, epi, bias=bias if epi != STORE else None)
+    ref = Am @ Bm + (bias if epi != STORE else 0.0)
+    cond = np.abs(Am) @ np.abs(Bm)
+    assert launched == 2
+    assert np.all(np.abs(out - ref) <= 1e-5 * cond + 1e-6)
+    if epi == BIAS_TANH:
+        np.testing.assert_allclose(out2, np.tanh(out.astype(np.float64)), rtol=2e-6, atol=2e-7)
