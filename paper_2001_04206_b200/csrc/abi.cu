@@ -421,12 +421,13 @@ SgdPlan plan_persistent(lane_b200_net* net) {
         // wider -> CS = H/128 chain CTAs in one cluster, one warp each, with a
         // DSMEM exchange of the slice partial logits per sample
         int cs = 1;
-        if (H > 256) cs = next_pow2((H + 127) / 128);
-        int ncw = (H <= 128 || cs > 1) ? 1 : 2;
+        if (H > 256) cs = std::min(kWinMaxCS, next_pow2((H + 127) / 128));
+        const int Hs = H / cs;
+        // one chain warp per 128-unit slice (two for 256-unit cluster slices)
+        int ncw = cs > 1 ? (Hs <= 128 ? 1 : 2) : (H <= 128 ? 1 : 2);
         if (const char* e = std::getenv("LANE_B200_SGD_WIN_NCW"))
             if (cs == 1) ncw = (std::atoi(e) == 1 && H <= 128) ? 1 : 2;
-        const int jpl = ncw == 1 ? 4 : (H <= 128 ? 2 : 4);
-        const int Hs = H / cs;
+        const int jpl = ncw == 1 ? 4 : ((cs == 1 && H <= 128) ? 2 : 4);
         // producers: H/4 column quads (QPC per CTA) x KS row splits (<= 2
         // splits, >= 32 rows each); rows per split a multiple of 4 (cp.async 16 B)
         const int quads = std::max(1, H / 4);
@@ -436,18 +437,24 @@ SgdPlan plan_persistent(lane_b200_net* net) {
         const int rpc = (((I + ks - 1) / ks) + 3) & ~3;
         ks = (I + rpc - 1) / rpc;
         const WinSmem L(32 * jpl * ncw, D, ks, Hs, ncw);
-        const ProdSmem PL(rpc, D);
-        const size_t smem = std::max(L.total, PL.total);
+        const size_t psmem_reg = ProdSmem(rpc, D).total;
+        // producers: register slices up to kWinWideQPC quads, else W0 in smem
+        // (the quad count is only known after the capacity query; size for both)
+        const size_t smem_reg = std::max(L.total, psmem_reg);
         // co-resident CTAs: one per SM; clusters of cs must also fit the GPCs
         int max_ctas = c->sm_count;
-        if (cs > 1 && cs <= kWinMaxCS && smem <= c->max_smem_optin)
-            max_ctas = std::min(max_ctas, window_cluster_capacity(cs, smem));
+        if (cs > 1 && cs <= kWinMaxCS && smem_reg <= c->max_smem_optin)
+            max_ctas = std::min(max_ctas, window_cluster_capacity(cs, smem_reg));
         pmax = std::max(1, max_ctas - cs);
         const int qpc = std::max(1, (quads * ks + pmax - 1) / pmax);
         const int producers = ((quads + qpc - 1) / qpc) * ks;
         const int grid = ((cs + producers + cs - 1) / cs) * cs;  // a whole number of clusters
+        const bool psm = qpc > kWinWideQPC;  // W0 slices in shared memory
+        const size_t smem = psm ? std::max(L.total, ProdSmemS(rpc, D, qpc).total) : smem_reg;
+        const int nthr = ncw == 2 ? 256 : 224;
         if (H % (4 * cs) == 0 && Hs <= 32 * jpl * ncw && cs <= kWinMaxCS && C <= kWinCP &&
-            rpc <= (qpc > kWinMaxQPC ? 2 : kWinMaxNR) * 224 && qpc <= (cs > 1 ? kWinWideQPC : 1) &&
+            rpc <= (qpc > kWinMaxQPC ? 2 : kWinMaxNR) * nthr &&
+            qpc <= (cs > 1 ? kWinSmemQPC : 1) && (cs == 1 || ncw == 1 || psm) &&
             grid <= max_ctas && smem <= c->max_smem_optin) {
             p.ok = p.window = true;
             p.jpl = jpl;
@@ -625,6 +632,11 @@ void launch_persistent(lane_b200_net* net, const SgdPlan& P, const float* X, con
 
 // cluster chains: producers with up to 4 quads x 4 rows/thread, or 8 quads x 2 rows
 WinKernel window_kernel(int jpl, int ncw, int C, int cs, int qpc) {
+    if (cs > 1 && qpc > kWinWideQPC) {
+        if (ncw == 2)
+            return C == 10 ? k_sgd_window<4, 10, 2, true, kWinSmemQPC, 2> : k_sgd_window<4, 0, 2, true, kWinSmemQPC, 2>;
+        return C == 10 ? k_sgd_window<4, 10, 1, true, kWinSmemQPC, 2> : k_sgd_window<4, 0, 1, true, kWinSmemQPC, 2>;
+    }
     if (cs > 1 && qpc > kWinMaxQPC)
         return C == 10 ? k_sgd_window<4, 10, 1, true, kWinWideQPC, 2> : k_sgd_window<4, 0, 1, true, kWinWideQPC, 2>;
     if (cs > 1)

@@ -483,6 +483,188 @@ __device__ __forceinline__ void win_producer(const WinArgs& A, float* sm) {
     }
 }
 
+// Producer with its W0 slice in SHARED memory (very wide layers, > 8 column
+// quads per CTA): quad-major [quad][row] float4.  Per block, one pass per
+// quad: load the thread's row-quads, apply the S updates (reference rounding),
+// store them back and, with the updated values still in registers, add this
+// quad's contribution to Y(k+D).
+constexpr int kWinSmemQPC = 16;
+struct ProdSmemS {
+    int RPCp, NB;
+    size_t xr, d0s, red, wsm, total;
+    __host__ __device__ ProdSmemS(int RPC, int D, int QPC) {
+        RPCp = (RPC + 3) & ~3;
+        NB = D + 2;
+        size_t o = 0;
+        auto take = [&](size_t nf) {
+            size_t at = o;
+            o += (nf + 3) & ~size_t(3);
+            return at;
+        };
+        xr = take((size_t)NB * kWinS * RPCp);
+        d0s = take(kWinS * kWinSmemQPC * 4);
+        red = take(kWinWarps * 64);
+        wsm = take((size_t)QPC * RPCp * 4);
+        total = o * sizeof(float);
+    }
+};
+
+template <int NT, int NR>
+__device__ __forceinline__ void win_producer_smem(const WinArgs& A, float* sm) {
+    const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+    const int I = A.I, H = A.H, D = A.D, KS = A.KS, RPC = A.RPC, QPC = A.QPC;
+    const int pid = blockIdx.x - A.CS;
+    const int pc = pid / KS, ks = pid - pc * KS;
+    const int q0 = pc * QPC, nq = max(0, min(QPC, (H >> 2) - q0));
+    if (nq == 0) return;
+    const int i0 = ks * RPC, nr = max(0, min(I, i0 + RPC) - i0);
+    const int n = A.n_steps;
+    const int nblk = (n + kWinS - 1) / kWinS;
+    const int YR = D + 1, DR = D + 1;
+    const float neg_eta = A.neg_eta;
+    const ProdSmemS L(RPC, D, QPC);
+    const int RPCp = L.RPCp, NB = L.NB;
+    float* xr = sm + L.xr;
+    float* red = sm + L.red;
+    float4* d0s = reinterpret_cast<float4*>(sm + L.d0s);  // [u][quad]
+    float4* wsm = reinterpret_cast<float4*>(sm + L.wsm);  // [quad][row]
+    const bool vec = ((I & 3) == 0) && ((i0 & 3) == 0) && ((nr & 3) == 0) &&
+                     ((reinterpret_cast<uintptr_t>(A.X) & 15) == 0);
+    for (int e = tid; e < nq * RPCp; e += NT) {
+        const int qi = e / RPCp, li = e - qi * RPCp;
+        wsm[e] = li < nr ? *reinterpret_cast<const float4*>(A.W0 + (size_t)(i0 + li) * H + 4 * (q0 + qi))
+                         : make_float4(0.f, 0.f, 0.f, 0.f);
+    }
+    auto prefetch = [&](int blk) {
+        float* dst = xr + (size_t)(blk % NB) * kWinS * RPCp;
+        const int s0 = blk * kWinS, nv = min(kWinS, n - s0);
+        if (vec) {
+            const int nq4 = nr >> 2;
+            for (int e = tid; e < nv * nq4; e += NT) {
+                const int u = e / nq4, q = e - u * nq4;
+                cp_async16(dst + u * RPCp + 4 * q, A.X + win_row(A, s0 + u) * I + i0 + 4 * q);
+            }
+        } else {
+            for (int e = tid; e < nv * nr; e += NT) {
+                const int u = e / nr, q = e - u * nr;
+                cp_async4(dst + u * RPCp + q, A.X + win_row(A, s0 + u) * I + i0 + q);
+            }
+        }
+    };
+    // one quad: optional update with block ku's d0 (nvu samples), optional
+    // Y(ky) contribution from the resulting weights
+    auto quad_pass = [&](int qi, int ku, int nvu, int ky) {
+        float4 w[NR];
+#pragma unroll
+        for (int m = 0; m < NR; ++m) {
+            const int li = tid + NT * m;
+            w[m] = li < nr ? wsm[qi * RPCp + li] : make_float4(0.f, 0.f, 0.f, 0.f);
+        }
+        if (ku >= 0) {
+            const float* xb = xr + (size_t)(ku % NB) * kWinS * RPCp;
+#pragma unroll
+            for (int m = 0; m < NR; ++m) {
+                const int li = tid + NT * m;
+                if (li < nr) {
+#pragma unroll
+                    for (int u = 0; u < kWinS; ++u) {
+                        if (u < nvu) {
+                            const float x = xb[u * RPCp + li];
+                            const float4 d = d0s[u * kWinSmemQPC + qi];
+                            w[m].x = sgd_apply(w[m].x, neg_eta, d.x, x);
+                            w[m].y = sgd_apply(w[m].y, neg_eta, d.y, x);
+                            w[m].z = sgd_apply(w[m].z, neg_eta, d.z, x);
+                            w[m].w = sgd_apply(w[m].w, neg_eta, d.w, x);
+                        }
+                    }
+                    wsm[qi * RPCp + li] = w[m];
+                }
+            }
+        }
+        if (ky < 0) return;
+        const float* xb = xr + (size_t)(ky % NB) * kWinS * RPCp;
+        const int nv = min(kWinS, n - ky * kWinS);
+        float acc[4 * kWinS];
+#pragma unroll
+        for (int e = 0; e < 4 * kWinS; ++e) acc[e] = 0.0f;
+#pragma unroll
+        for (int m = 0; m < NR; ++m) {
+            const int li = tid + NT * m;
+            if (li < nr) {
+#pragma unroll
+                for (int u = 0; u < kWinS; ++u) {
+                    const float x = u < nv ? xb[u * RPCp + li] : 0.0f;
+                    acc[4 * u + 0] = fmaf(x, w[m].x, acc[4 * u + 0]);
+                    acc[4 * u + 1] = fmaf(x, w[m].y, acc[4 * u + 1]);
+                    acc[4 * u + 2] = fmaf(x, w[m].z, acc[4 * u + 2]);
+                    acc[4 * u + 3] = fmaf(x, w[m].w, acc[4 * u + 3]);
+                }
+            }
+        }
+        xpose_step<64>(acc, lane, 16);
+        xpose_step<32>(acc, lane, 8);
+        xpose_step<16>(acc, lane, 4);
+        xpose_step<8>(acc, lane, 2);
+        xpose_step<4>(acc, lane, 1);
+        red[warp * 64 + 2 * lane] = acc[0];
+        red[warp * 64 + 2 * lane + 1] = acc[1];
+        __syncthreads();
+        if (tid < 4 * kWinS) {
+            float y = 0.0f;
+#pragma unroll
+            for (int q = 0; q < NT / 32; ++q) y += red[q * 64 + tid];
+            const int u = tid >> 2, c = tid & 3;
+            if (u < nv) __stcg(A.yring + (((size_t)(ky % YR) * KS + ks) * kWinS + u) * H + 4 * (q0 + qi) + c, y);
+        }
+        __syncthreads();  // red reuse
+    };
+    auto release_y = [&](int blk) {
+        if (tid < 4 * kWinS) {
+            __syncwarp();
+            if (lane == 0) red_release_add(A.ycnt + (blk % YR), 1u);
+        }
+    };
+
+    const int npro = min(D, nblk);
+    for (int blk = 0; blk <= npro && blk < nblk; ++blk) prefetch(blk);
+    cp_async_commit();
+    cp_async_wait<0>();
+    __syncthreads();
+    for (int blk = 0; blk < npro; ++blk) {
+        for (int qi = 0; qi < nq; ++qi) quad_pass(qi, -1, 0, blk);
+        release_y(blk);
+    }
+    for (int k = 0; k < nblk; ++k) {
+        const int nv = min(kWinS, n - k * kWinS);
+        if (k + D + 1 < nblk) prefetch(k + D + 1);  // slot of block k-1: retired
+        cp_async_commit();
+        if (tid == 0) spin_geq(A.dcnt, (unsigned)(A.CS * (k + 1)), A.error);
+        __syncthreads();
+        for (int e = tid; e < kWinS * kWinSmemQPC; e += NT) {
+            const int u = e / kWinSmemQPC, qi = e - u * kWinSmemQPC;
+            d0s[e] = (u < nv && qi < nq) ? __ldcg(reinterpret_cast<const float4*>(
+                                               A.dring + ((size_t)(k % DR) * kWinS + u) * H + 4 * (q0 + qi)))
+                                         : make_float4(0.f, 0.f, 0.f, 0.f);
+        }
+        cp_async_wait<1>();  // block k+D's rows (prefetched last iteration) have landed
+        __syncthreads();
+        const int ky = k + D < nblk ? k + D : -1;
+        for (int qi = 0; qi < nq; ++qi) quad_pass(qi, k, nv, ky);
+        if (ky >= 0) release_y(ky);
+        __syncthreads();  // ring slot / d0s reuse
+    }
+    cp_async_wait<0>();
+    __syncthreads();
+    for (int e = tid; e < nq * RPCp; e += NT) {
+        const int qi = e / RPCp, li = e - qi * RPCp;
+        if (li < nr) *reinterpret_cast<float4*>(A.W0 + (size_t)(i0 + li) * H + 4 * (q0 + qi)) = wsm[e];
+    }
+    if (pid == 0 && n > 0) {
+        const float* xl = A.X + win_row(A, n - 1) * I;
+        for (int i = tid; i < I; i += NT) A.x0[i] = xl[i];
+    }
+}
+
 // Producer for the single-CTA chain (H <= 256): one column quad per CTA.
 // (The multi-quad producer above costs ~3% at C2: an extra barrier per quad
 // and a later Y release.)
@@ -775,6 +957,33 @@ __device__ __forceinline__ void win_chain(const WinArgs& A, float* sm, const Win
             c1n = s1 >= 1 ? coefs[p1 * QW + 0] : 0.0f;  // c(s1, 1) = coef[s1-1][0]
             c2n = s1 >= 2 ? coefs[p2 * QW + 1] : 0.0f;  // c(s1, 2) = coef[s1-2][1]
         };
+        // cluster exchange of this CTA's slice partial logits (lanes k < C hold
+        // class k): st.async to every peer (completing the peer's exchange
+        // barrier), wait for all CS, sum in rank order -- identical logits in
+        // every chain CTA.  The pushing warp re-arms the barrier for sample
+        // s+2: no peer sends s+2 before it holds this CTA's s+1 partials, which
+        // are pushed after this point.
+        auto xchg = [&](int s, float part, bool push) {
+            const int par = s & 1;
+            const uint32_t slot = smem_u32(gat + (par * kWinMaxCS + rank) * kWinCP + lane);
+            const uint32_t xb = MB(kMbXch + par);
+            if (push && kval)
+                for (int p = 0; p < CS; ++p) st_async_f32(mapa_shared(slot, p), part, mapa_shared(xb, p));
+            {
+                const unsigned long long t0 = globaltimer_ns();
+                while (!mbar_try_wait(xb, (uint32_t)((s >> 1) & 1))) {
+                    if (globaltimer_ns() - t0 > 5000000000ull) {
+                        atomicExch(A.error, 5);
+                        __trap();
+                    }
+                }
+            }
+            if (push && lane == 0 && s + 2 < n) mbar_arrive_expect_tx(xb, (uint32_t)(CS * C * sizeof(float)));
+            const float* g = gat + par * kWinMaxCS * kWinCP + kr;
+            float tot = g[0];
+            for (int p = 1; p < CS; ++p) tot += g[p * kWinCP];
+            return tot;
+        };
         if (n > 0) fetch_row(0, 0, 0);
         int sR = 0, sRd = 0;      // s % R, s % Rd
         int nR = 1 % R, nRd = 1;  // (s+1) % R, (s+1) % Rd
@@ -831,30 +1040,7 @@ __device__ __forceinline__ void win_chain(const WinArgs& A, float* sm, const Win
                 if (NCW > 1) {
                     if (kval) half[cw * kWinCP + lane] = hs;
                 } else if (CS > 1) {
-                    // cluster: every chain CTA pushes its C slice partials to all
-                    // peers (st.async completes the peer's exchange barrier), then
-                    // sums the CS partials in rank order: identical logits in all
-                    const int par = s & 1;
-                    const uint32_t slot = smem_u32(gat + (par * kWinMaxCS + rank) * kWinCP + lane);
-                    const uint32_t xb = MB(kMbXch + par);
-                    if (kval)
-                        for (int p = 0; p < CS; ++p) st_async_f32(mapa_shared(slot, p), hs, mapa_shared(xb, p));
-                    {
-                        const unsigned long long t0 = globaltimer_ns();
-                        while (!mbar_try_wait(xb, (uint32_t)((s >> 1) & 1))) {
-                            if (globaltimer_ns() - t0 > 5000000000ull) {
-                                atomicExch(A.error, 5);
-                                __trap();
-                            }
-                        }
-                    }
-                    // re-arm for sample s+2: no peer sends s+2 before it holds this
-                    // CTA's partials of s+1, which are sent after this point
-                    if (lane == 0 && s + 2 < n) mbar_arrive_expect_tx(xb, (uint32_t)(CS * C * sizeof(float)));
-                    const float* g = gat + par * kWinMaxCS * kWinCP + kr;
-                    float tot = g[0];
-                    for (int p = 1; p < CS; ++p) tot += g[p * kWinCP];
-                    zown1 = sadd(tot, b1k);
+                    zown1 = sadd(xchg(s, hs, true), b1k);
                     if (kval) zt[lane] = zown1;
                 } else {
                     zown1 = sadd(hs, b1k);
@@ -868,6 +1054,7 @@ __device__ __forceinline__ void win_chain(const WinArgs& A, float* sm, const Win
                 float hsum = half[kr];
 #pragma unroll
                 for (int c = 1; c < NCW; ++c) hsum += half[c * kWinCP + kr];
+                if (CS > 1) hsum = xchg(s, hsum, cw == 0);  // chain warp 0 pushes, all wait
                 zown = sadd(hsum, b1k);
                 if (kval) zt[lane] = zown;
             }
@@ -1230,6 +1417,8 @@ __global__ void __launch_bounds__(win_threads<NCW>(), 1) k_sgd_window(WinArgs A)
         win_chain<JPL, CT, NCW, CLU, TR>(A, sm, WinSmem(32 * JPL * NCW, A.D, A.KS, A.H / (CLU ? A.CS : 1), NCW));
     else if constexpr (!CLU)
         win_producer_v1<win_threads<NCW>()>(A, sm);
+    else if constexpr (MQ == kWinSmemQPC)
+        win_producer_smem<win_threads<NCW>(), NR>(A, sm);
     else
         win_producer<win_threads<NCW>(), MQ, NR>(A, sm);
 }
