@@ -423,8 +423,8 @@ SgdPlan plan_persistent(lane_b200_net* net) {
         int cs = 1;
         if (H > 256) cs = std::min(kWinMaxCS, next_pow2((H + 127) / 128));
         const int Hs = H / cs;
-        // one chain warp per 128-unit slice (two for 256-unit cluster slices)
-        int ncw = cs > 1 ? (Hs <= 128 ? 1 : 2) : (H <= 128 ? 1 : 2);
+        // one chain warp per 128 units of a cluster slice (1, 2 or 4)
+        int ncw = cs > 1 ? (Hs <= 128 ? 1 : Hs <= 256 ? 2 : Hs <= 512 ? 4 : 8) : (H <= 128 ? 1 : 2);
         if (const char* e = std::getenv("LANE_B200_SGD_WIN_NCW"))
             if (cs == 1) ncw = (std::atoi(e) == 1 && H <= 128) ? 1 : 2;
         const int jpl = ncw == 1 ? 4 : ((cs == 1 && H <= 128) ? 2 : 4);
@@ -436,7 +436,10 @@ SgdPlan plan_persistent(lane_b200_net* net) {
         if (const char* e = std::getenv("LANE_B200_SGD_WIN_KS")) ks = std::max(1, std::min(std::atoi(e), 2));
         const int rpc = (((I + ks - 1) / ks) + 3) & ~3;
         ks = (I + rpc - 1) / rpc;
-        const WinSmem L(32 * jpl * ncw, D, ks, Hs, ncw);
+        // (the d0-direct choice needs the producer variant: wide/smem producers
+        // when the quads per producer exceed 4 -- known after the capacity query;
+        // size the chain CTA for the non-direct ring, the larger of the two)
+        const WinSmem L(32 * jpl * ncw, D, ks, Hs, ncw, cs > 1 && ncw >= 2);
         const size_t psmem_reg = ProdSmem(rpc, D).total;
         // producers: register slices up to kWinWideQPC quads, else W0 in smem
         // (the quad count is only known after the capacity query; size for both)
@@ -451,8 +454,8 @@ SgdPlan plan_persistent(lane_b200_net* net) {
         const int grid = ((cs + producers + cs - 1) / cs) * cs;  // a whole number of clusters
         const bool psm = qpc > kWinWideQPC;  // W0 slices in shared memory
         const size_t smem = psm ? std::max(L.total, ProdSmemS(rpc, D, qpc).total) : smem_reg;
-        const int nthr = ncw == 2 ? 256 : 224;
-        if (H % (4 * cs) == 0 && Hs <= 32 * jpl * ncw && cs <= kWinMaxCS && C <= kWinCP &&
+        const int nthr = ncw == 4 ? 320 : ncw == 2 ? 256 : 224;
+        if (ncw <= 4 && H % (4 * cs) == 0 && Hs <= 32 * jpl * ncw && cs <= kWinMaxCS && C <= kWinCP &&
             rpc <= (qpc > kWinMaxQPC ? 2 : kWinMaxNR) * nthr &&
             qpc <= (cs > 1 ? kWinSmemQPC : 1) && (cs == 1 || ncw == 1 || psm) &&
             grid <= max_ctas && smem <= c->max_smem_optin) {
@@ -633,6 +636,8 @@ void launch_persistent(lane_b200_net* net, const SgdPlan& P, const float* X, con
 // cluster chains: producers with up to 4 quads x 4 rows/thread, or 8 quads x 2 rows
 WinKernel window_kernel(int jpl, int ncw, int C, int cs, int qpc) {
     if (cs > 1 && qpc > kWinWideQPC) {
+        if (ncw == 4)
+            return C == 10 ? k_sgd_window<4, 10, 4, true, kWinSmemQPC, 2> : k_sgd_window<4, 0, 4, true, kWinSmemQPC, 2>;
         if (ncw == 2)
             return C == 10 ? k_sgd_window<4, 10, 2, true, kWinSmemQPC, 2> : k_sgd_window<4, 0, 2, true, kWinSmemQPC, 2>;
         return C == 10 ? k_sgd_window<4, 10, 1, true, kWinSmemQPC, 2> : k_sgd_window<4, 0, 1, true, kWinSmemQPC, 2>;
@@ -718,7 +723,7 @@ void launch_window(lane_b200_net* net, const SgdPlan& P, const float* X, const f
                                : window_kernel(P.jpl, P.ncw, A.C, P.cs, P.qpc);
     LANE_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(P.smem)));
     void* args[] = {&A};
-    const int nthreads = P.ncw == 2 ? win_threads<2>() : win_threads<1>();
+    const int nthreads = P.ncw == 4 ? win_threads<4>() : P.ncw == 2 ? win_threads<2>() : win_threads<1>();
     if (P.cs == 1) {
         LANE_CUDA(cudaLaunchCooperativeKernel(reinterpret_cast<void*>(kern), dim3(P.G), dim3(nthreads), args,
                                               P.smem, c->stream));

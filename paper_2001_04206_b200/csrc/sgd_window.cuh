@@ -51,11 +51,11 @@ namespace lane_b200 {
 
 constexpr int kWinS = 16;                    // samples per block
 constexpr int kWinHelpers = 4;               // helper warps
-constexpr int kWinWarps = 8;                 // max warps per CTA (two chain warps)
+constexpr int kWinWarps = 10;                // max warps per CTA (four chain warps)
 constexpr int kWinThreads = 32 * kWinWarps;  // 256
 // CTA size: 7 warps with one chain warp, 8 with two
 template <int NCW>
-constexpr int win_threads() { return NCW == 2 ? 256 : 224; }
+constexpr int win_threads() { return NCW == 4 ? 320 : NCW == 2 ? 256 : 224; }
 // Warp roles.  Warps share a sub-partition (SMSP) when their ids are equal mod
 // 4: SMSP0 = helper 0 + helper 2 (warp 4), SMSP1 = helper 1 + helper 3 (warp
 // 5), SMSP2 = chain warp 2 + publisher (6), SMSP3 = chain warp 3 + loader (7).
@@ -63,19 +63,23 @@ constexpr int win_threads() { return NCW == 2 ? 256 : 224; }
 // NCW = 1 (7 warps): helpers 0,1,2,4; chain 3 (alone on SMSP3); publisher 5;
 //   loader 6.
 // NCW = 2 (8 warps): helpers 0,1,4,5; chain 2,3; publisher 6; loader 7.
+// NCW = 4 (10 warps): chain 0..3 (one per SMSP); helpers 4..7; publisher 8;
+//   loader 9.
 template <int NCW>
-__device__ __forceinline__ int win_loader_warp() { return NCW == 2 ? 7 : 6; }
+__device__ __forceinline__ int win_loader_warp() { return NCW == 4 ? 9 : NCW == 2 ? 7 : 6; }
 template <int NCW>
-__device__ __forceinline__ int win_pub_warp() { return NCW == 2 ? 6 : 5; }
+__device__ __forceinline__ int win_pub_warp() { return NCW == 4 ? 8 : NCW == 2 ? 6 : 5; }
 // helper index 0..3, or -1
 template <int NCW>
 __device__ __forceinline__ int win_helper_index(int warp) {
+    if (NCW == 4) return (warp >= 4 && warp < 8) ? warp - 4 : -1;
     if (NCW == 2) return (warp == 0 || warp == 1) ? warp : (warp == 4 || warp == 5) ? warp - 2 : -1;
     return warp < 3 ? warp : warp == 4 ? 3 : -1;
 }
 // chain warp index (0..NCW-1) or -1: NCW = 1 uses warp 3 (warp 2 idles)
 template <int NCW>
 __device__ __forceinline__ int win_chain_index(int warp) {
+    if (NCW == 4) return warp < 4 ? warp : -1;
     return NCW == 2 ? ((warp == 2 || warp == 3) ? warp - 2 : -1) : (warp == 3 ? 0 : -1);
 }
 // vector load/store of JPL consecutive floats (JPL = 2 or 4)
@@ -138,12 +142,15 @@ struct WinArgs {
 };
 
 struct WinSmem {
-    int HP, R, Rd;
+    int HP, R, Rd, Rdh;  // Rdh: rows of the shared-memory d0 ring (helpers, publisher)
     size_t zacc, ystage, tstage, coefs, d0ring, pring, red, d0s, rowflag, gat, mbar, total;
     // HP_: padded hidden slice per chain CTA; Hs: the slice width (H / CS)
-    __host__ __device__ WinSmem(int HP_, int D, int KS, int Hs, int NCW) : HP(HP_) {
+    // direct: the chain also writes d0 rows straight to the L2 ring (cluster
+    // chains), so the shared ring only covers the helpers' lag (16 rows)
+    __host__ __device__ WinSmem(int HP_, int D, int KS, int Hs, int NCW, bool direct = false) : HP(HP_) {
         R = D * kWinS;
         Rd = (D + 1) * kWinS;
+        Rdh = direct ? kWinS : Rd;
         size_t o = 0;
         auto take = [&](size_t nf) {
             size_t at = o;
@@ -154,7 +161,7 @@ struct WinSmem {
         ystage = take(2 * (size_t)KS * kWinS * Hs);  // [buffer][ks][u][Hs] (TMA bulk copies)
         tstage = take(2 * kWinS * kWinCP);
         coefs = take((size_t)Rd * D * kWinS);  // forward band rows of source s, slot s % Rd
-        d0ring = take((size_t)Rd * HP);
+        d0ring = take((size_t)Rdh * HP);
         pring = take((size_t)Rd * kWinCP);
         red = take(kWinCP * (32 * NCW + 4) + 4 * NCW * kWinCP);  // partials, halves x2, logits, exps
         d0s = take(kWinS * 4);
@@ -488,7 +495,7 @@ __device__ __forceinline__ void win_producer(const WinArgs& A, float* sm) {
 // quad: load the thread's row-quads, apply the S updates (reference rounding),
 // store them back and, with the updated values still in registers, add this
 // quad's contribution to Y(k+D).
-constexpr int kWinSmemQPC = 16;
+constexpr int kWinSmemQPC = 32;
 struct ProdSmemS {
     int RPCp, NB;
     size_t xr, d0s, red, wsm, total;
@@ -824,7 +831,7 @@ __device__ __forceinline__ float rcp_approx(float x) {
 // ---------------------------------------------------------------------------
 // Chain CTA.
 // ---------------------------------------------------------------------------
-template <int JPL, int CT, int NCW, bool CLU, bool TR>
+template <int JPL, int CT, int NCW, bool CLU, bool DIR, bool TR>
 __device__ __forceinline__ void win_chain(const WinArgs& A, float* sm, const WinSmem& L) {
     const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
     // CS chain CTAs (one cluster) split the hidden layer: rank r owns units
@@ -860,7 +867,7 @@ __device__ __forceinline__ void win_chain(const WinArgs& A, float* sm, const Win
     for (int e = tid; e < R * HP; e += win_threads<NCW>()) zacc[e] = 0.0f;
     for (int e = tid; e < 2 * A.KS * kWinS * Hs; e += win_threads<NCW>()) ystage[e] = 0.0f;
     for (int e = tid; e < 2 * kWinS * kWinCP; e += win_threads<NCW>()) tstage[e] = 0.0f;
-    for (int e = tid; e < Rd * HP; e += win_threads<NCW>()) d0ring[e] = 0.0f;
+    for (int e = tid; e < L.Rdh * HP; e += win_threads<NCW>()) d0ring[e] = 0.0f;
     for (int e = tid; e < R; e += win_threads<NCW>()) rowflag[e] = 0u;
     if (tid == 0) {
         for (int r = 0; r < kWinRing; ++r) mbar_init(MB(kMbD0 + r), 32 * NCW);
@@ -1113,7 +1120,14 @@ __device__ __forceinline__ void win_chain(const WinArgs& A, float* sm, const Win
                 d0v[m] = fmaf(-a[m], a[m], 1.0f) * acc;  // (1 - a^2) W1 d1
             }
             WIN_TRACE(s, 3);
-            vst<JPL>(d0ring + sRd * HP + j0, d0v);
+            if constexpr (DIR) {
+                // helpers read the short smem ring; producers read the L2 ring
+                // (the publisher releases it per block, cumulatively)
+                vst<JPL>(d0ring + (s & (kWinS - 1)) * HP + j0, d0v);
+                if (jval) vst<JPL>(A.dring + ((size_t)(b % (D + 1)) * kWinS + u) * H + h0 + j0, d0v);
+            } else {
+                vst<JPL>(d0ring + sRd * HP + j0, d0v);
+            }
             mbar_arrive_cta(MB(kMbD0 + (s & (kWinRing - 1))));
             WIN_TRACE(s, 4);
             // -- off the chain: p and d1 of the lane's own class, stats, biases
@@ -1261,12 +1275,17 @@ __device__ __forceinline__ void win_chain(const WinArgs& A, float* sm, const Win
             const long long myrow = (stats && lane < nv) ? win_row(A, s0 + lane) : 0;
             mbar_wait_cta(MB(kMbBlk + k % kWinBlkRing), (uint32_t)((k / kWinBlkRing) & 1), A.error);
             WIN_TRACE(s0, 11);
-            // this CTA's slice of the block's d0 rows (dring rows are H wide)
-            float* dst = A.dring + (size_t)(k % DR) * kWinS * H + h0;
-            for (int e = lane; e < nv * HQ; e += 32) {
-                const int u = e / HQ, q = e - u * HQ;
-                __stcg(reinterpret_cast<float4*>(dst + (size_t)u * H) + q,
-                       reinterpret_cast<const float4*>(d0ring + ((s0 + u) % Rd) * HP)[q]);
+            // this CTA's slice of the block's d0 rows (dring rows are H wide);
+            // multi-warp cluster chains wrote them directly (the fence below makes
+            // the chain warps' stores, ordered before blkdone, visible with the
+            // release)
+            if constexpr (!DIR) {
+                float* dst = A.dring + (size_t)(k % DR) * kWinS * H + h0;
+                for (int e = lane; e < nv * HQ; e += 32) {
+                    const int u = e / HQ, q = e - u * HQ;
+                    __stcg(reinterpret_cast<float4*>(dst + (size_t)u * H) + q,
+                           reinterpret_cast<const float4*>(d0ring + ((s0 + u) % Rd) * HP)[q]);
+                }
             }
             __threadfence();
             __syncwarp();
@@ -1323,7 +1342,8 @@ __device__ __forceinline__ void win_chain(const WinArgs& A, float* sm, const Win
             const int first = f0 + ((w - (f0 & (kWinHelpers - 1))) & (kWinHelpers - 1));
             mbar_wait_cta(MB(kMbD0 + (s & (kWinRing - 1))), (uint32_t)((s >> 4) & 1), A.error);
             if ((s & (kWinHelpers - 1)) == w) WIN_TRACE(s, 12);
-            const float4* dv = reinterpret_cast<const float4*>(d0ring + sRd * HP);
+            const float4* dv =
+                reinterpret_cast<const float4*>(d0ring + (DIR ? (s & (kWinS - 1)) : sRd) * HP);
             const float* cs = coefs + sRd * QW - s - 1;  // cs[r] = c(r, r-s)
             // this lane's d0 quads, once per sample
             constexpr int NQH = JPL * NCW / 4;  // float4 per lane per row (HP = 32 JPL NCW)
@@ -1414,7 +1434,10 @@ template <int JPL, int CT, int NCW, bool CLU = false, int MQ = 1, int NR = kWinM
 __global__ void __launch_bounds__(win_threads<NCW>(), 1) k_sgd_window(WinArgs A) {
     extern __shared__ __align__(16) float sm[];
     if ((int)blockIdx.x < (CLU ? A.CS : 1))
-        win_chain<JPL, CT, NCW, CLU, TR>(A, sm, WinSmem(32 * JPL * NCW, A.D, A.KS, A.H / (CLU ? A.CS : 1), NCW));
+        // DIR: d0 straight to the L2 ring (multi-warp or 16-CTA cluster chains,
+        // where it measured faster and saves shared memory)
+        win_chain<JPL, CT, NCW, CLU, CLU && (NCW >= 2 || MQ >= 8), TR>(
+            A, sm, WinSmem(32 * JPL * NCW, A.D, A.KS, A.H / (CLU ? A.CS : 1), NCW, CLU && (NCW >= 2 || MQ >= 8)));
     else if constexpr (!CLU)
         win_producer_v1<win_threads<NCW>()>(A, sm);
     else if constexpr (MQ == kWinSmemQPC)

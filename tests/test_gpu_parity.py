@@ -343,6 +343,7 @@ def test_sgd_stream_fast_vs_oracle(lane, fast, monkeypatch, mode, F, H, C, n, st
     (340, [1024], 10, 32, 60, 1e-3, 2),     # 8 chain CTAs, 2 column quads per producer
     (340, [2048], 10, 32, 45, 1e-3, 3),     # 16 chain CTAs (non-portable cluster), 4 quads per producer
     (340, [4096], 10, 32, 40, 1e-3, 2),     # 16 chain CTAs x 2 warps, W0 slices in producer smem
+    (340, [8192], 10, 32, 40, 1e-3, 2),     # 16 chain CTAs x 4 warps, d0 straight to L2, 19 quads/producer
     (64, [384], 7, 16, 50, 0.02, 2),        # 4 chain CTAs x 96 units (partial slices)
     (784, [128], 10, 64, 150, 0.01, -2),    # two chain warps (2 units/lane) instead of one
     (100, [96], 10, 20, 90, 0.02, -3),      # two chain warps, H % 64 != 0
@@ -517,7 +518,8 @@ def test_minibatch_momentum_vs_oracle(lane, fast, F, H, C, B, mu):
 @pytest.mark.parametrize("F,H,C,want", [(784, [128], 10, "window"), (4, [8], 3, "window"),
                                         (340, [256], 10, "window"), (340, [1024], 10, "window"),
                                         (340, [2048], 10, "window"), (340, [1000], 10, "cluster"),
-                                        (340, [4096], 10, "window"), (340, [8192], 10, "grid")])
+                                        (340, [4096], 10, "window"), (340, [8192], 10, "window"),
+                                        (340, [16384], 10, "grid")])
 def test_sgd_plan_selection(lane, fast, F, H, C, want):
     # the fused plan the headline shapes run (no silent fallback to layer kernels)
     net = lane.build_network(F, H, C, seed=42, device=fast)
