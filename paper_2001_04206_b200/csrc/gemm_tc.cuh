@@ -14,7 +14,8 @@
 //   warp 1      MMA issuer: one elected thread issues tcgen05.mma, commits
 //               smem slots back to the producer and the accumulator to the
 //               epilogue (tcgen05.commit -> mbarrier)
-//   warps 2..5  split pass (A_lo, B_lo per stage), then the epilogue:
+//   warps 2..9  split pass (A_lo, B_lo per stage), then the epilogue (two
+//               warps per TMEM lane quarter, 64 columns each):
 //               tcgen05.ld TMEM -> registers -> fused epilogue -> global
 // Operand majors: K-major tiles come from one TMA box {32 (K), 128 (MN)};
 // MN-major tiles from four boxes {32 (MN), 32 (K)} (one per 32-wide MN group).
@@ -29,7 +30,8 @@ namespace lane_b200 {
 constexpr int kTcBM = 128, kTcBN = 128, kTcBK = 32, kTcStages = 3;
 constexpr int kTcTile = kTcBM * kTcBK * 4;  // bytes of one 128x32 fp32 tile (A or B)
 constexpr int kTcStage = 4 * kTcTile;       // A, B, A_lo, B_lo
-constexpr int kTcThreads = 192;
+constexpr int kTcSplitWarps = 8;  // the split pass is the busiest role (3xTF32)
+constexpr int kTcThreads = 64 + 32 * kTcSplitWarps;
 constexpr size_t kTcSmem = (size_t)kTcStages * kTcStage + 1024 /*align*/ + 256 /*barriers*/;
 
 enum class TcEpi : int { STORE = 0, BIAS = 1, BIAS_TANH = 2, TANH_GRAD = 3 };
@@ -154,7 +156,7 @@ __global__ void __launch_bounds__(kTcThreads, 1)
     if (threadIdx.x == 0) {
         for (int s = 0; s < kTcStages; ++s) {
             tc_mbar_init(full(s), 1);
-            tc_mbar_init(conv(s), 4);
+            tc_mbar_init(conv(s), kTcSplitWarps);
             tc_mbar_init(empty(s), 1);
         }
         tc_mbar_init(tmem_full, 1);
@@ -232,8 +234,8 @@ __global__ void __launch_bounds__(kTcThreads, 1)
         if (lane == 0) tc_commit(tmem_full);
         __syncwarp();
     } else {
-        // ---------------- split pass, then epilogue (warps 2..5) ----------------
-        const int ct = threadIdx.x - 64;  // 0..127
+        // ---------------- split pass, then epilogue (warps 2..9) ----------------
+        const int ct = threadIdx.x - 64;  // 0..32*kTcSplitWarps-1
         for (int kb = 0; kb < nkb; ++kb) {
             const int s = kb % kTcStages;
             const uint32_t ph = (uint32_t)((kb / kTcStages) & 1);
@@ -243,8 +245,8 @@ __global__ void __launch_bounds__(kTcThreads, 1)
             float4* al = reinterpret_cast<float4*>(smem + (size_t)s * kTcStage + 2 * kTcTile);
             float4* bl = reinterpret_cast<float4*>(smem + (size_t)s * kTcStage + 3 * kTcTile);
 #pragma unroll
-            for (int u = 0; u < kTcTile / 16 / 128; ++u) {
-                const int q = ct + 128 * u;
+            for (int u = 0; u < kTcTile / 16 / (32 * kTcSplitWarps); ++u) {
+                const int q = ct + 32 * kTcSplitWarps * u;
                 const float4 va = a[q], vb = b[q];
                 al[q] = make_float4(tf32_lo(va.x), tf32_lo(va.y), tf32_lo(va.z), tf32_lo(va.w));
                 bl[q] = make_float4(tf32_lo(vb.x), tf32_lo(vb.y), tf32_lo(vb.z), tf32_lo(vb.w));
@@ -258,9 +260,10 @@ __global__ void __launch_bounds__(kTcThreads, 1)
         asm volatile("tcgen05.fence::after_thread_sync;\n" ::: "memory");
         const int quarter = warp & 3;  // TMEM lanes this warp may access
         const int row = quarter * 32 + lane;
+        const int cbeg = ((warp - 2) >> 2) * (kTcBN / 2);  // this warp's 64 columns
         const int m = m0 + row;
 #pragma unroll 1
-        for (int c0 = 0; c0 < kTcBN; c0 += 32) {
+        for (int c0 = cbeg; c0 < cbeg + kTcBN / 2; c0 += 32) {
             uint32_t r[32];
             const uint32_t taddr = tmem + ((uint32_t)(quarter * 32) << 16) + (uint32_t)c0;
             asm volatile(
