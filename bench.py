@@ -228,24 +228,22 @@ def run_minibatch(args, wl):
         ms = float(t.item())
     value = BG * args.steps / (ms / 1000.0)
 
-    # e2e: pinned host batch -> device, step, loss back to the host, per step
-    Xh = torch.from_numpy(X[: nb * BG]).pin_memory()
-    Th = torch.from_numpy(T[: nb * BG]).pin_memory()
-    bx, bt = dev.alloc(rows * F * 4), dev.alloc(rows * C * 4)
-    ld = dev.alloc(8)
-    loss_h = torch.zeros(1, dtype=torch.float64).pin_memory()
-    sh = trainer.shard
-    e2e_steps = max(1, min(args.steps, 5))
+    # e2e: through the public trainer (lane.train_minibatch) over pinned host
+    # arrays: every step's rows are gathered into a page-locked slot and copied
+    # H2D on the library's copy stream (overlapping the previous steps), and
+    # every step's loss is read back D2H (async, 8 bytes)
+    Xh = torch.from_numpy(X).pin_memory().numpy()
+    Th = torch.from_numpy(T).pin_memory().numpy()
+    ds = lane.DataSet(Xh, Th)
+    epochs = max(1, -(-min(args.steps, 10) // nb))
+    lane.train_minibatch(net, ds, rows, eta, mu, epochs=1, shuffle=False)  # warm: staging + graph
+    e2e_steps = epochs * nb
     if world > 1:
         torch.distributed.barrier()
     torch.cuda.synchronize()
     t0 = time.perf_counter()
-    for s in range(e2e_steps):
-        r0 = (s % nb) * BG + sh.begin
-        dev.h2d(bx, Xh[r0:r0 + rows].numpy())
-        dev.h2d(bt, Th[r0:r0 + rows].numpy())
-        net.minibatch_step(bx, bt, rows, eta, mu, ld)
-        dev.d2h(loss_h.numpy(), ld)
+    lane.train_minibatch(net, ds, rows, eta, mu, epochs=epochs, shuffle=False)
+    torch.cuda.synchronize()
     e2e_s = time.perf_counter() - t0
     if world > 1:
         t = torch.tensor([e2e_s], device="cuda")

@@ -84,6 +84,7 @@ enum { LANE_NUMERICS_STRICT = 0, LANE_NUMERICS_FAST = 1 };
 
 typedef struct lane_b200_ctx lane_b200_ctx;
 typedef struct lane_b200_net lane_b200_net;
+typedef struct lane_b200_dataset lane_b200_dataset;
 
 /* ----------------------------------------------------------- context --- */
 int lane_b200_abi_version(void);
@@ -199,6 +200,23 @@ int lane_b200_evaluate(lane_b200_net* net, const float* X_host, const float* T_h
 int lane_b200_minibatch_step(lane_b200_net* net, const float* X_dev, const float* T_dev,
                              size_t B, float eta, float mu, double* loss_sum_dev);
 
+/* Mini-batch training over a host dataset (the input side of the
+ * path).  X_host [n][input_width], T_host [n][classes] (pageable or pinned).
+ * Each epoch permutes the sample order with SplitMix64(seed) when shuffle != 0
+ * (one generator for the whole run, continuing the previous epoch's order, as
+ * train does, network.cpp:153-161), then runs n / (batch * world) steps of
+ * lane_b200_minibatch_step; rank r of a communicator takes rows
+ * [r*batch, (r+1)*batch) of every global batch.  With world == 1 and
+ * drop_last == 0 a final short step takes the n % batch remaining rows.
+ * Input pipeline: the rows of a step are gathered on the host into one of 3
+ * page-locked slots and copied on a second stream while earlier steps run;
+ * each step's running loss is read back asynchronously.  mean_loss_out
+ * [epochs] (local samples) and step_loss_out [epochs * steps] (mean loss of
+ * each step) may be NULL; steps_run = steps executed over all epochs. */
+int lane_b200_train_minibatch(lane_b200_net* net, const float* X_host, const float* T_host, size_t n,
+                              size_t batch, float eta, float mu, size_t epochs, uint64_t seed, int shuffle,
+                              int drop_last, float* mean_loss_out, float* step_loss_out, size_t* steps_run);
+
 /* Diagnostic: one GEMM of the mini-batch path on device buffers (row-major):
  * op 0 NN: C[M,N] = A[M,K] B[K,N];  op 1 NT: C = A[M,K] B[N,K]^T;
  * op 2 TN: C = A[K,M]^T B[K,N].  epilogue 0 store, 1 +bias[n], 2 +bias[n]
@@ -206,6 +224,34 @@ int lane_b200_minibatch_step(lane_b200_net* net, const float* X_dev, const float
  * 3xTF32 kernel where the shape is eligible (else the SIMT kernel). */
 int lane_b200_gemm(lane_b200_ctx* ctx, int op, int M, int N, int K, const float* A, const float* B,
                    float* C, float* C2, const float* bias, const float* aux, int epilogue, int use_tc);
+
+/* ---------------------------------------------- datasets --- */
+/* DataSet (include/lane/dataset.hpp:16-23) held by the library in page-locked
+ * host memory (plain memory when no GPU is present): X [n][features] then
+ * T [n][classes], row-major -- pass the pointers from dataset_info straight
+ * to lane_b200_train / _train_minibatch / _evaluate. */
+int lane_b200_dataset_create(size_t features, size_t classes, size_t n, const float* X, const float* T,
+                             lane_b200_dataset** out);
+/* load_dataset (dataset.hpp:25-30, dataset.cpp:31-83): CSV, features then a
+ * one-hot label per line; IoError when the file cannot be opened, ParseError
+ * with the line number for a bad field count, a non-numeric field (parsed as
+ * std::from_chars), a label field other than 0/1 or a label that is not
+ * one-hot.  Empty lines are skipped. */
+int lane_b200_dataset_load(const char* path, size_t features, size_t classes, lane_b200_dataset** out);
+/* save_dataset (dataset.hpp:32-33, dataset.cpp:85-103): %.9g features. */
+int lane_b200_dataset_save(const lane_b200_dataset* d, const char* path);
+int lane_b200_dataset_info(const lane_b200_dataset* d, size_t* features, size_t* classes, size_t* n, float** X,
+                           float** T, int* pinned);
+/* split (dataset.hpp:35-37, dataset.cpp:105-124): ConfigError unless
+ * 0 < train_fraction < 1. */
+int lane_b200_dataset_split(const lane_b200_dataset* d, double train_fraction, uint64_t seed,
+                            lane_b200_dataset** train, lane_b200_dataset** test);
+/* enlarge (dataset.hpp:39-41, dataset.cpp:126-148); *rng_state is the
+ * SeededRng state (tensor.hpp:13-44), advanced in place.  ConfigError for
+ * factor == 0 or noise < 0. */
+int lane_b200_dataset_enlarge(const lane_b200_dataset* d, size_t factor, float noise, uint64_t* rng_state,
+                              lane_b200_dataset** out);
+int lane_b200_dataset_destroy(lane_b200_dataset* d);
 
 /* ------------------------------------------- multi-GPU (data parallel) --- */
 int lane_b200_nccl_unique_id(void* id_out, size_t id_bytes); /* id_bytes >= 128 */

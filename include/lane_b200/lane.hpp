@@ -22,6 +22,7 @@
 #include <memory>
 #include <stdexcept>
 #include <string>
+#include <utility>
 #include <vector>
 
 #include "../lane_b200.h"
@@ -280,6 +281,75 @@ inline EpochStats evaluate(FeedForwardNetwork& net, const DataSet& set) {
     check(lane_b200_evaluate(net.handle(), set.features.data(), set.labels.data(), set.size(), &es.mean_loss,
                              &es.accuracy));
     return es;
+}
+
+// ---------------------------------------------------------------- datasets
+// dataset.hpp:25-41 over the library's loader (csrc/dataset.cuh); the
+// library's page-locked rows are copied into the value-type DataSet.
+struct SeededRng {  // tensor.hpp:13-44, only the state crosses the ABI
+    std::uint64_t state;
+    explicit SeededRng(std::uint64_t seed) : state(seed) {}
+};
+
+namespace detail {
+struct NativeSet {
+    lane_b200_dataset* h = nullptr;
+    ~NativeSet() { lane_b200_dataset_destroy(h); }
+    DataSet take() const {
+        std::size_t F = 0, C = 0, n = 0;
+        float *X = nullptr, *T = nullptr;
+        check(lane_b200_dataset_info(h, &F, &C, &n, &X, &T, nullptr));
+        DataSet d;
+        d.feature_width = F;
+        d.class_count = C;
+        d.features.assign(X, X + n * F);
+        d.labels.assign(T, T + n * C);
+        return d;
+    }
+};
+inline NativeSet to_native(const DataSet& d) {
+    NativeSet s;
+    check(lane_b200_dataset_create(d.feature_width, d.class_count, d.size(), d.features.data(), d.labels.data(),
+                                   &s.h));
+    return s;
+}
+}  // namespace detail
+
+inline DataSet load_dataset(const std::string& path, std::size_t feature_width, std::size_t class_count) {
+    detail::NativeSet s;
+    check(lane_b200_dataset_load(path.c_str(), feature_width, class_count, &s.h));
+    return s.take();
+}
+
+inline void save_dataset(const DataSet& d, const std::string& path) {
+    check(lane_b200_dataset_save(detail::to_native(d).h, path.c_str()));
+}
+
+inline std::pair<DataSet, DataSet> split(const DataSet& d, double train_fraction, std::uint64_t seed) {
+    detail::NativeSet a, b;
+    check(lane_b200_dataset_split(detail::to_native(d).h, train_fraction, seed, &a.h, &b.h));
+    return {a.take(), b.take()};
+}
+
+inline DataSet enlarge(const DataSet& d, std::size_t factor, float noise, SeededRng& rng) {
+    detail::NativeSet e;
+    check(lane_b200_dataset_enlarge(detail::to_native(d).h, factor, noise, &rng.state, &e.h));
+    return e.take();
+}
+
+// Mini-batch extension over a host dataset with the pipelined input path
+// (lane_b200_train_minibatch); returns the per-epoch mean losses.
+inline std::vector<float> train_minibatch(FeedForwardNetwork& net, const DataSet& set, std::size_t batch,
+                                          LearningRate eta, float momentum, std::size_t epochs,
+                                          std::uint64_t seed, bool shuffle = true, bool drop_last = true) {
+    if (set.size() == 0) throw TrainingError("train: empty training set");
+    if (set.feature_width != net.input_width()) throw ShapeError("train: dataset feature width != network input width");
+    if (set.class_count != net.class_count()) throw ShapeError("train: dataset class count != network class count");
+    std::vector<float> loss(epochs);
+    check(lane_b200_train_minibatch(net.handle(), set.features.data(), set.labels.data(), set.size(), batch,
+                                    eta.eta, momentum, epochs, seed, shuffle ? 1 : 0, drop_last ? 1 : 0,
+                                    loss.data(), nullptr, nullptr));
+    return loss;
 }
 
 }  // namespace lane_b200

@@ -56,6 +56,14 @@ SIGNATURES = {
     "lane_b200_train": (_I, [_V, _FP, _FP, _S, _F, _F, _S, _U64, _FP, _FP, _SP]),
     "lane_b200_evaluate": (_I, [_V, _FP, _FP, _S, _FP, _FP]),
     "lane_b200_minibatch_step": (_I, [_V, _V, _V, _S, _F, _F, _V]),
+    "lane_b200_train_minibatch": (_I, [_V, _FP, _FP, _S, _S, _F, _F, _S, _U64, _I, _I, _FP, _FP, _SP]),
+    "lane_b200_dataset_create": (_I, [_S, _S, _S, _FP, _FP, C.POINTER(_V)]),
+    "lane_b200_dataset_load": (_I, [C.c_char_p, _S, _S, C.POINTER(_V)]),
+    "lane_b200_dataset_save": (_I, [_V, C.c_char_p]),
+    "lane_b200_dataset_info": (_I, [_V, _SP, _SP, _SP, C.POINTER(_FP), C.POINTER(_FP), C.POINTER(_I)]),
+    "lane_b200_dataset_split": (_I, [_V, C.c_double, _U64, C.POINTER(_V), C.POINTER(_V)]),
+    "lane_b200_dataset_enlarge": (_I, [_V, _S, _F, C.POINTER(_U64), C.POINTER(_V)]),
+    "lane_b200_dataset_destroy": (_I, [_V]),
     "lane_b200_gemm": (_I, [_V, _I, _I, _I, _I, _V, _V, _V, _V, _V, _V, _I, _I]),
     "lane_b200_nccl_unique_id": (_I, [_V, _S]),
     "lane_b200_comm_init": (_I, [_V, _I, _I, _V, _S]),

@@ -11,12 +11,14 @@
 #include <cstdlib>
 #include <cstdio>
 #include <cstring>
+#include <memory>
 #include <string>
 #include <vector>
 
 #include "common.cuh"
 #include "layer_kernels.cuh"
 #include "minibatch.cuh"
+#include "pipeline.cuh"
 #include "sgd_persistent.cuh"
 #include "sgd_window.cuh"
 
@@ -82,6 +84,8 @@ int blocks_for(size_t n, int threads, int cap) {
 }
 
 }  // namespace
+
+#include "dataset.cuh"
 
 // ============================================================== objects ===
 
@@ -176,6 +180,7 @@ struct lane_b200_net {
     size_t order_count = 0;
     MinibatchState mb;  // activations + workspaces of the mini-batch path
     MbGraph mb_graph;   // captured mini-batch step (per configuration)
+    InputPipeline pipe;  // pinned staging + copy stream of train_minibatch
 
     LayerBufs& L(size_t l) { return layers.at(l); }
     size_t out_layer() const { return n_hidden; }
@@ -1102,6 +1107,7 @@ int lane_b200_net_destroy(lane_b200_net* net) {
         cudaFree(net->win_coef);
         cudaFree(net->win_ring);
         net->mb_graph.reset();
+        net->pipe.release();
         cudaFree(net->data);
         cudaFree(net->order);
         lane_b200_ctx* c = net->ctx;
@@ -1382,53 +1388,200 @@ int lane_b200_evaluate(lane_b200_net* net, const float* X_host, const float* T_h
 
 // ------------------------------------------------- mini-batch + comms ---
 
+namespace {
+
+void minibatch_step_impl(lane_b200_net* net, const float* X, const float* T, size_t B, float eta, float mu,
+                         double* loss_sum) {
+    lane_b200_ctx* c = net->ctx;
+    minibatch_stage(*c, *net, X, T, B);
+    // The step body runs eagerly once per configuration (sizing every
+    // workspace), then as a captured CUDA graph: ~20 launches -> one.
+    MbGraph& gr = net->mb_graph;
+    const MbGraph::Key key{B, eta, mu, loss_sum, c->comm.world, c->numerics, gemm_tc_mode(),
+                           static_cast<const void*>(c->comm.comm)};
+    const bool use_graph = !std::getenv("LANE_B200_MB_NOGRAPH");
+    if (use_graph && gr.exec && gr.key == key) {
+        LANE_CUDA(cudaGraphLaunch(gr.exec, c->stream));
+        c->count(static_cast<int>(gr.launches));
+    } else if (use_graph && gr.warm && gr.key == key) {
+        gr.reset();
+        cudaGraph_t graph = nullptr;
+        const uint64_t before = c->launches;
+        LANE_CUDA(cudaStreamBeginCapture(c->stream, cudaStreamCaptureModeThreadLocal));
+        try {
+            minibatch_body(*c, *net, B, eta, mu, loss_sum);
+        } catch (...) {
+            cudaStreamEndCapture(c->stream, &graph);
+            if (graph) cudaGraphDestroy(graph);
+            throw;
+        }
+        LANE_CUDA(cudaStreamEndCapture(c->stream, &graph));
+        gr.launches = c->launches - before;
+        c->launches = before;
+        LANE_CUDA(cudaGraphInstantiate(&gr.exec, graph, 0));
+        LANE_CUDA(cudaGraphDestroy(graph));
+        gr.key = key;
+        LANE_CUDA(cudaGraphLaunch(gr.exec, c->stream));
+        c->count(static_cast<int>(gr.launches));
+    } else {
+        gr.reset();
+        minibatch_body(*c, *net, B, eta, mu, loss_sum);
+        gr.key = key;
+        gr.warm = true;
+    }
+    c->check_launch();
+}
+
+}  // namespace
+
 int lane_b200_minibatch_step(lane_b200_net* net, const float* X, const float* T, size_t B, float eta, float mu,
                              double* loss_sum) {
     return guard([&] {
         if (!net) throw Error(LANE_ERR_CONFIG, "null network");
         check_eta(eta);
         if (B == 0 || B > net->max_batch) throw Error(LANE_ERR_SHAPE, "minibatch: B must be in [1, max_batch]");
-        lane_b200_ctx* c = net->ctx;
-        minibatch_stage(*c, *net, X, T, B);
-        // The step body runs eagerly once per configuration (sizing every
-        // workspace), then as a captured CUDA graph: ~20 launches -> one.
-        MbGraph& gr = net->mb_graph;
-        const MbGraph::Key key{B, eta, mu, loss_sum, c->comm.world, c->numerics, gemm_tc_mode(),
-                               static_cast<const void*>(c->comm.comm)};
-        const bool use_graph = !std::getenv("LANE_B200_MB_NOGRAPH");
-        if (use_graph && gr.exec && gr.key == key) {
-            LANE_CUDA(cudaGraphLaunch(gr.exec, c->stream));
-            c->count(static_cast<int>(gr.launches));
-        } else if (use_graph && gr.warm && gr.key == key) {
-            gr.reset();
-            cudaGraph_t graph = nullptr;
-            const uint64_t before = c->launches;
-            LANE_CUDA(cudaStreamBeginCapture(c->stream, cudaStreamCaptureModeThreadLocal));
-            try {
-                minibatch_body(*c, *net, B, eta, mu, loss_sum);
-            } catch (...) {
-                cudaStreamEndCapture(c->stream, &graph);
-                if (graph) cudaGraphDestroy(graph);
-                throw;
-            }
-            LANE_CUDA(cudaStreamEndCapture(c->stream, &graph));
-            gr.launches = c->launches - before;
-            c->launches = before;
-            LANE_CUDA(cudaGraphInstantiate(&gr.exec, graph, 0));
-            LANE_CUDA(cudaGraphDestroy(graph));
-            gr.key = key;
-            LANE_CUDA(cudaGraphLaunch(gr.exec, c->stream));
-            c->count(static_cast<int>(gr.launches));
-        } else {
-            gr.reset();
-            minibatch_body(*c, *net, B, eta, mu, loss_sum);
-            gr.key = key;
-            gr.warm = true;
-        }
-        c->check_launch();
+        minibatch_step_impl(net, X, T, B, eta, mu, loss_sum);
     });
 }
 
+int lane_b200_train_minibatch(lane_b200_net* net, const float* X_host, const float* T_host, size_t n,
+                              size_t batch, float eta, float mu, size_t epochs, uint64_t seed, int shuffle,
+                              int drop_last, float* mean_loss_out, float* step_loss_out, size_t* steps_run) {
+    return guard([&] {
+        if (!net) throw Error(LANE_ERR_CONFIG, "null network");
+        check_eta(eta);
+        if (!X_host || !T_host) throw Error(LANE_ERR_CONFIG, "train_minibatch: null dataset");
+        if (n == 0) throw Error(LANE_ERR_TRAINING, "train_minibatch: empty training set");
+        if (batch == 0 || batch > net->max_batch)
+            throw Error(LANE_ERR_SHAPE, "train_minibatch: batch must be in [1, max_batch]");
+        if (n > 0xffffffffull) throw Error(LANE_ERR_SHAPE, "train_minibatch: more than 2^32 samples");
+        lane_b200_ctx* c = net->ctx;
+        const size_t I = net->input_width, C = net->classes;
+        const int world = std::max(1, c->comm.world), rank = c->comm.rank;
+        // rank r takes rows [r*batch, (r+1)*batch) of every global batch
+        const size_t BG = batch * static_cast<size_t>(world);
+        const size_t full = n / BG;
+        const size_t tail = (world == 1 && !drop_last) ? n % BG : 0;
+        const size_t steps = full + (tail ? 1 : 0);
+        if (steps == 0) throw Error(LANE_ERR_TRAINING, "train_minibatch: fewer samples than one global batch");
+        InputPipeline& P = net->pipe;
+        P.reserve(batch * (I + C), steps);
+        std::vector<uint32_t> order(n);
+        for (size_t k = 0; k < n; ++k) order[k] = static_cast<uint32_t>(k);
+        SplitMix64 rng(seed);  // one generator for the whole run, like train (network.cpp:153)
+        size_t done = 0;
+        for (size_t epoch = 0; epoch < epochs; ++epoch) {
+            // the permutation continues from the previous epoch's (network.cpp:154-161)
+            if (shuffle)
+                for (size_t i = n; i > 1; --i) std::swap(order[i - 1], order[rng.below(i)]);
+            LANE_CUDA(cudaMemsetAsync(net->loss_dev, 0, sizeof(double), c->stream));
+            size_t local = 0;
+            for (size_t s = 0; s < steps; ++s) {
+                const size_t rows = s < full ? batch : tail;
+                const int k = static_cast<int>(done % InputPipeline::kSlots);
+                if (P.pending[k]) LANE_CUDA(cudaEventSynchronize(P.copied[k]));  // pinned slot free
+                gather_rows(X_host, T_host, I, C, order.data() + s * BG + (s < full ? rank * batch : 0), rows,
+                            P.host[k]);
+                LANE_CUDA(cudaStreamWaitEvent(P.copy, P.consumed[k], 0));  // device slot free
+                LANE_CUDA(cudaMemcpyAsync(P.dev[k], P.host[k], rows * (I + C) * sizeof(float),
+                                          cudaMemcpyHostToDevice, P.copy));
+                LANE_CUDA(cudaEventRecord(P.copied[k], P.copy));
+                LANE_CUDA(cudaStreamWaitEvent(c->stream, P.copied[k], 0));
+                minibatch_step_impl(net, P.dev[k], P.dev[k] + rows * I, rows, eta, mu, net->loss_dev);
+                LANE_CUDA(cudaEventRecord(P.consumed[k], c->stream));
+                P.pending[k] = true;
+                // the step's result back to the host: the running loss sum (8 bytes, async)
+                LANE_CUDA(cudaMemcpyAsync(P.cum_loss_host + s, net->loss_dev, sizeof(double),
+                                          cudaMemcpyDeviceToHost, c->stream));
+                local += rows;
+                ++done;
+            }
+            LANE_CUDA(cudaStreamSynchronize(c->stream));
+            c->check_device_error();
+            if (mean_loss_out)
+                mean_loss_out[epoch] = static_cast<float>(P.cum_loss_host[steps - 1] / static_cast<double>(local));
+            if (step_loss_out)
+                for (size_t s = 0; s < steps; ++s) {
+                    const double prev = s ? P.cum_loss_host[s - 1] : 0.0;
+                    const size_t rows = s < full ? batch : tail;
+                    step_loss_out[epoch * steps + s] =
+                        static_cast<float>((P.cum_loss_host[s] - prev) / static_cast<double>(rows));
+                }
+        }
+        if (steps_run) *steps_run = done;
+    });
+}
+
+// ------------------------------------------------------------ datasets ---
+
+int lane_b200_dataset_create(size_t features, size_t classes, size_t n, const float* X, const float* T,
+                             lane_b200_dataset** out) {
+    return guard([&] {
+        if (!out || (n && (!X || !T))) throw Error(LANE_ERR_CONFIG, "null argument");
+        auto d = std::make_unique<lane_b200_dataset>();
+        d->allocate(features, classes, n);
+        if (n) {
+            std::memcpy(d->X, X, n * features * sizeof(float));
+            std::memcpy(d->T, T, n * classes * sizeof(float));
+        }
+        *out = d.release();
+    });
+}
+
+int lane_b200_dataset_load(const char* path, size_t features, size_t classes, lane_b200_dataset** out) {
+    return guard([&] {
+        if (!path || !out) throw Error(LANE_ERR_CONFIG, "null argument");
+        auto d = std::make_unique<lane_b200_dataset>();
+        lane_b200::dataset::load(path, features, classes, *d);
+        *out = d.release();
+    });
+}
+
+int lane_b200_dataset_save(const lane_b200_dataset* d, const char* path) {
+    return guard([&] {
+        if (!d || !path) throw Error(LANE_ERR_CONFIG, "null argument");
+        lane_b200::dataset::save(*d, path);
+    });
+}
+
+int lane_b200_dataset_info(const lane_b200_dataset* d, size_t* features, size_t* classes, size_t* n, float** X,
+                           float** T, int* pinned) {
+    return guard([&] {
+        if (!d) throw Error(LANE_ERR_CONFIG, "null dataset");
+        if (features) *features = d->features;
+        if (classes) *classes = d->classes;
+        if (n) *n = d->n;
+        if (X) *X = d->X;
+        if (T) *T = d->T;
+        if (pinned) *pinned = d->pinned ? 1 : 0;
+    });
+}
+
+int lane_b200_dataset_split(const lane_b200_dataset* d, double train_fraction, uint64_t seed,
+                            lane_b200_dataset** train, lane_b200_dataset** test) {
+    return guard([&] {
+        if (!d || !train || !test) throw Error(LANE_ERR_CONFIG, "null argument");
+        auto a = std::make_unique<lane_b200_dataset>();
+        auto b = std::make_unique<lane_b200_dataset>();
+        lane_b200::dataset::split(*d, train_fraction, seed, *a, *b);
+        *train = a.release();
+        *test = b.release();
+    });
+}
+
+int lane_b200_dataset_enlarge(const lane_b200_dataset* d, size_t factor, float noise, uint64_t* rng_state,
+                              lane_b200_dataset** out) {
+    return guard([&] {
+        if (!d || !rng_state || !out) throw Error(LANE_ERR_CONFIG, "null argument");
+        auto e = std::make_unique<lane_b200_dataset>();
+        lane_b200::dataset::enlarge(*d, factor, noise, *rng_state, *e);
+        *out = e.release();
+    });
+}
+
+int lane_b200_dataset_destroy(lane_b200_dataset* d) {
+    return guard([&] { delete d; });
+}
 int lane_b200_gemm(lane_b200_ctx* c, int op, int M, int N, int K, const float* A, const float* B, float* C,
                    float* C2, const float* bias, const float* aux, int epilogue, int use_tc) {
     return guard([&] {

@@ -16,7 +16,7 @@ from __future__ import annotations
 
 import ctypes as C
 import os
-from dataclasses import dataclass
+from dataclasses import dataclass, field
 
 import numpy as np
 
@@ -90,6 +90,7 @@ class Device:
         self._p = C.c_void_p()
         _check(L.lane_b200_ctx_create(index, C.byref(self._p)))
         self.index = index
+        self.world = 1
         if numerics is not None:
             self.numerics = numerics
 
@@ -156,9 +157,11 @@ class Device:
     def comm_init(self, rank: int, world: int, uid: bytes):
         buf = C.create_string_buffer(bytes(uid), 128)
         _check(_native.lib().lane_b200_comm_init(self._p, rank, world, buf, 128))
+        self.world = int(world)
 
     def comm_destroy(self):
         _check(_native.lib().lane_b200_comm_destroy(self._p))
+        self.world = 1
 
 
 _default_device: Device | None = None
@@ -416,9 +419,12 @@ class EpochStats:
 
 @dataclass
 class DataSet:
-    """dataset.hpp: features (n x feature_width), labels one-hot (n x classes)."""
+    """dataset.hpp:16-23: features (n x feature_width), labels one-hot (n x
+    classes).  Sets made by load_dataset / split / enlarge are views of the
+    library's page-locked rows (``_owner`` keeps them alive)."""
     features: np.ndarray
     labels: np.ndarray
+    _owner: object = field(default=None, repr=False, compare=False)
 
     @property
     def feature_width(self) -> int:
@@ -464,3 +470,109 @@ def evaluate(net: FeedForwardNetwork, test_set: DataSet) -> EpochStats:
     _check(_native.lib().lane_b200_evaluate(net._p, _ptr(X), _ptr(T), test_set.size(),
                                             C.byref(lo), C.byref(ac)))
     return EpochStats(0, lo.value, ac.value)
+
+
+# ------------------------------------------------------------------ datasets
+class _NativeSet:
+    """Owns a lane_b200_dataset handle (page-locked rows)."""
+
+    def __init__(self, handle):
+        self._h = handle
+
+    def __del__(self):
+        h, self._h = getattr(self, "_h", None), None
+        if h:
+            _native.lib().lane_b200_dataset_destroy(h)
+
+
+def _wrap_native(handle) -> DataSet:
+    L = _native.lib()
+    F, Cn, n = C.c_size_t(), C.c_size_t(), C.c_size_t()
+    xp, tp = C.POINTER(C.c_float)(), C.POINTER(C.c_float)()
+    pinned = C.c_int()
+    _check(L.lane_b200_dataset_info(handle, C.byref(F), C.byref(Cn), C.byref(n), C.byref(xp), C.byref(tp),
+                                    C.byref(pinned)))
+    owner = _NativeSet(handle)
+    if n.value == 0:
+        return DataSet(np.zeros((0, F.value), np.float32), np.zeros((0, Cn.value), np.float32), owner)
+    X = np.ctypeslib.as_array(xp, shape=(n.value, F.value))
+    T = np.ctypeslib.as_array(tp, shape=(n.value, Cn.value))
+    return DataSet(X, T, owner)
+
+
+def _to_native(d: DataSet):
+    """A native handle for d (reuses d's own when it has one)."""
+    if isinstance(d._owner, _NativeSet):
+        return d._owner._h, None
+    X, T = _f32(d.features), _f32(d.labels)
+    h = C.c_void_p()
+    _check(_native.lib().lane_b200_dataset_create(X.shape[1], T.shape[1], X.shape[0], _ptr(X), _ptr(T),
+                                                  C.byref(h)))
+    tmp = _NativeSet(h)
+    return h, tmp
+
+
+class SeededRng:
+    """SplitMix64 state (tensor.hpp:13-44) for enlarge(); advanced in place."""
+
+    def __init__(self, seed: int = 0):
+        self.state = int(seed) & 0xFFFFFFFFFFFFFFFF
+
+
+def load_dataset(path, feature_width: int, class_count: int) -> DataSet:
+    """load_dataset (dataset.hpp:25-30, dataset.cpp:31-83)."""
+    h = C.c_void_p()
+    _check(_native.lib().lane_b200_dataset_load(os.fsencode(path), feature_width, class_count, C.byref(h)))
+    return _wrap_native(h)
+
+
+def save_dataset(d: DataSet, path) -> None:
+    """save_dataset (dataset.hpp:32-33, dataset.cpp:85-103)."""
+    h, _tmp = _to_native(d)
+    _check(_native.lib().lane_b200_dataset_save(h, os.fsencode(path)))
+
+
+def split(d: DataSet, train_fraction: float, seed: int) -> tuple[DataSet, DataSet]:
+    """split (dataset.hpp:35-37, dataset.cpp:105-124)."""
+    h, _tmp = _to_native(d)
+    a, b = C.c_void_p(), C.c_void_p()
+    _check(_native.lib().lane_b200_dataset_split(h, float(train_fraction), C.c_uint64(seed), C.byref(a),
+                                                 C.byref(b)))
+    return _wrap_native(a), _wrap_native(b)
+
+
+def enlarge(d: DataSet, factor: int, noise: float, rng: SeededRng) -> DataSet:
+    """enlarge (dataset.hpp:39-41, dataset.cpp:126-148)."""
+    if factor < 0:
+        raise ConfigError("enlarge: factor must be >= 1")
+    h, _tmp = _to_native(d)
+    st = C.c_uint64(rng.state)
+    out = C.c_void_p()
+    _check(_native.lib().lane_b200_dataset_enlarge(h, factor, C.c_float(noise), C.byref(st), C.byref(out)))
+    rng.state = st.value
+    return _wrap_native(out)
+
+
+def train_minibatch(net: FeedForwardNetwork, train_set: DataSet, batch: int, eta, mu: float = 0.0,
+                    epochs: int = 1, seed: int = 0, shuffle: bool = True, drop_last: bool = True,
+                    step_losses: bool = False):
+    """Mini-batch training over a host dataset through the pipelined input
+    path (lane_b200_train_minibatch).  Returns the per-epoch mean losses, and
+    with step_losses=True also the per-step mean losses [epochs, steps]."""
+    _check_set(net, train_set, "train")
+    X, T = _f32(train_set.features), _f32(train_set.labels)
+    n = train_set.size()
+    world = getattr(net.device, "world", 1)
+    bg = batch * world
+    steps = n // bg + (1 if (world == 1 and not drop_last and n % bg) else 0)
+    E = int(epochs)
+    ml = np.zeros(max(1, E), np.float32)
+    sl = np.zeros(max(1, E * max(1, steps)), np.float32) if step_losses else None
+    ran = C.c_size_t()
+    _check(_native.lib().lane_b200_train_minibatch(
+        net._p, _ptr(X), _ptr(T), n, batch, C.c_float(_eta(eta)), C.c_float(mu), E, C.c_uint64(seed),
+        int(bool(shuffle)), int(bool(drop_last)), _ptr(ml), _ptr(sl) if sl is not None else None,
+        C.byref(ran)))
+    if step_losses:
+        return [float(v) for v in ml[:E]], sl[:E * steps].reshape(E, steps)
+    return [float(v) for v in ml[:E]]

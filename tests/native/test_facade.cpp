@@ -31,7 +31,7 @@ static int failures = 0;
 
 static bool approx(float a, float b, float rel = 1e-6f) { return std::fabs(a - b) <= rel * std::fabs(b); }
 
-int main() {
+int main(int argc, char** argv) {
     Device dev(0, Numerics::Strict);
     {
         // test_layers.cpp:125-142 softmax backward hand example
@@ -103,6 +103,33 @@ int main() {
         empty.feature_width = 2;
         empty.class_count = 2;
         CHECK_THROWS_AS(train(*net, empty, cfg), TrainingError);
+    }
+    if (argc > 1) {
+        // dataset.hpp over the library loader: Iris, split(0.9, 42) -> 135/15
+        // (acceptance.cpp:443-469), enlarge, save/load round trip, errors
+        DataSet iris = load_dataset(argv[1], 4, 3);
+        CHECK(iris.size() == 150);
+        auto tt = split(iris, 0.9, 42);
+        CHECK(tt.first.size() == 135 && tt.second.size() == 15);
+        SeededRng rng(7);
+        DataSet big = enlarge(tt.first, 3, 0.02f, rng);
+        CHECK(big.size() == 405 && rng.state != 7);
+        bool in_range = true;
+        for (float v : big.features) in_range = in_range && v >= 0.0f && v <= 1.0f;
+        CHECK(in_range);
+        CHECK_THROWS_AS(split(iris, 1.0, 1), ConfigError);
+        CHECK_THROWS_AS(enlarge(iris, 0, 0.1f, rng), ConfigError);
+        CHECK_THROWS_AS(load_dataset("/nonexistent/iris.csv", 4, 3), IoError);
+        CHECK_THROWS_AS(load_dataset(argv[1], 4, 2), ParseError);
+        const std::string tmp = std::string(argc > 2 ? argv[2] : "/tmp") + "/facade_iris.csv";
+        save_dataset(tt.second, tmp);
+        DataSet back = load_dataset(tmp, 4, 3);
+        CHECK(back.features == tt.second.features && back.labels == tt.second.labels);
+        // mini-batch trainer over the loaded rows: the loss falls
+        auto net = build_network(dev, 4, {16}, 3, 42, 16);
+        auto losses = train_minibatch(*net, big, 16, LearningRate(0.1f), 0.9f, 20, 1);
+        CHECK(losses.size() == 20 && losses.back() < 0.5f * losses.front());
+        CHECK(evaluate(*net, tt.second).accuracy >= 0.8f);
     }
     if (failures == 0) std::printf("ALL PASSED\n");
     return failures == 0 ? 0 : 1;

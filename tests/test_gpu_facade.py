@@ -27,5 +27,6 @@ def test_facade_compiles_against_the_c_abi(tmp_path):
 def test_facade_reference_style_kats(tmp_path):
     _build.build()
     exe = build_facade_test(tmp_path)
-    out = subprocess.run([str(exe)], capture_output=True, text=True, timeout=300)
+    iris = os.path.join(HERE, "golden", "iris_normalized.txt")
+    out = subprocess.run([str(exe), iris, str(tmp_path)], capture_output=True, text=True, timeout=300)
     assert out.returncode == 0 and "ALL PASSED" in out.stdout, out.stdout + out.stderr

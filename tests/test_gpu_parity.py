@@ -515,6 +515,58 @@ def test_minibatch_momentum_vs_oracle(lane, fast, F, H, C, B, mu):
     fast.free(Td)
 
 
+@pytest.mark.parametrize("shuffle,drop_last,n", [(False, True, 200), (True, True, 200), (True, False, 203)])
+def test_train_minibatch_pipeline_matches_manual_steps(lane, fast, shuffle, drop_last, n):
+    """The pipelined trainer (host gather -> pinned slot -> copy stream) runs
+    exactly the steps a caller would run by hand on the same batches: bitwise
+    identical weights, per-step losses equal to each step's own loss sum."""
+    F, H, C, B, mu, eta, E = 40, [64, 48], 6, 16, 0.9, 0.05, 3
+    X, T = po.synthetic_dataset(F, C, n, 5)
+    a = lane.build_network(F, H, C, seed=3, device=fast, max_batch=B)
+    b = lane.build_network(F, H, C, seed=3, device=fast, max_batch=B)
+    means, steps = lane.train_minibatch(a, lane.DataSet(X, T), B, eta, mu, epochs=E, seed=42, shuffle=shuffle,
+                                        drop_last=drop_last, step_losses=True)
+    orders = po.shuffle_orders(n, E, 42) if shuffle else np.tile(np.arange(n, dtype=np.uint32), (E, 1))
+    nb = n // B + (0 if drop_last or n % B == 0 else 1)
+    assert steps.shape == (E, nb)
+    ld = fast.alloc(8)
+    Xd, Td = fast.alloc(B * F * 4), fast.alloc(B * C * 4)
+    for e in range(E):
+        for s in range(nb):
+            idx = orders[e][s * B:(s + 1) * B]
+            fast.h2d(Xd, np.ascontiguousarray(X[idx]))
+            fast.h2d(Td, np.ascontiguousarray(T[idx]))
+            fast.h2d(ld, np.zeros(1, np.float64))
+            b.minibatch_step(Xd, Td, len(idx), eta, mu, ld)
+            got = np.zeros(1, np.float64)
+            fast.d2h(got, ld)
+            np.testing.assert_allclose(steps[e, s], got[0] / len(idx), rtol=1e-5)
+        np.testing.assert_allclose(means[e], steps[e] @ np.array(
+            [min(B, n - s * B) for s in range(nb)], np.float64) / sum(min(B, n - s * B) for s in range(nb)),
+            rtol=1e-5)
+    for la, lb in zip(a.layers, b.layers):
+        np.testing.assert_array_equal(la.weights, lb.weights)
+        np.testing.assert_array_equal(la.delta_weights, lb.delta_weights)
+    for p_ in (ld, Xd, Td):
+        fast.free(p_)
+
+
+def test_train_minibatch_from_loaded_dataset(lane, fast, tmp_path):
+    """load_dataset (page-locked rows) -> split -> train_minibatch -> evaluate,
+    the loss falling over the epochs (Iris, 4-16-3)."""
+    import os
+    iris = os.path.join(os.path.dirname(__file__), "golden", "iris_normalized.txt")
+    tr, te = lane.split(lane.load_dataset(iris, 4, 3), 0.9, 42)
+    net = lane.build_network(4, [16], 3, seed=42, device=fast, max_batch=16)
+    means = lane.train_minibatch(net, tr, 16, 0.2, 0.9, epochs=60, seed=1)
+    assert means[-1] < 0.5 * means[0]
+    assert lane.evaluate(net, te).accuracy >= 0.8
+    with pytest.raises(lane.ShapeError):
+        lane.train_minibatch(net, tr, 17, 0.1)
+    with pytest.raises(lane.TrainingError):
+        lane.train_minibatch(net, lane.DataSet(tr.features[:8], tr.labels[:8]), 16, 0.1)
+
+
 @pytest.mark.parametrize("F,H,C,want", [(784, [128], 10, "window"), (4, [8], 3, "window"),
                                         (340, [256], 10, "window"), (340, [1024], 10, "window"),
                                         (340, [2048], 10, "window"), (340, [1000], 10, "cluster"),
