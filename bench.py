@@ -285,6 +285,45 @@ def run_minibatch(args, wl):
         torch.distributed.destroy_process_group()
 
 
+def run_paper_table(args):
+    """The paper's per-kernel table (340-100000-10):
+    the reference's own lane-bench (lane::run_benchmark through oracle/_ref,
+    serial and parallel on every host core) and the B200 lane-bench CLI
+    (paper_2001_04206_b200/lib/lane-bench) on the same synthetic dataset,
+    merged into one report (speedup = reference serial mean / device mean)."""
+    import ctypes as C
+    import tempfile
+    from oracle import pyoracle as po  # CPU reference leg + data generator only
+    from paper_2001_04206_b200 import _build, lane
+
+    F, Cn, H = 340, 10, args.fc_neurons
+    X, T = po.synthetic_dataset(F, Cn, 64, 9)
+    tmp = tempfile.mkdtemp()
+    data = os.path.join(tmp, "paper_340x10.csv")
+    lane.save_dataset(lane.DataSet(X, T), data)
+    warm, iters = max(1, args.warmup), max(1, args.steps)
+    ref_csv = os.path.join(tmp, "ref.csv")
+    if po.ref_available():
+        f = po.ref_lib().lr_run_benchmark
+        f.restype = C.c_long
+        f.argtypes = [C.c_char_p, C.c_size_t, C.c_size_t, C.c_size_t, C.c_float, C.c_size_t, C.c_size_t,
+                      C.c_size_t, C.c_int, C.c_uint, C.c_uint64, C.c_char_p, C.c_size_t, C.POINTER(C.c_uint64)]
+        buf, h = C.create_string_buffer(1 << 14), C.c_uint64()
+        if f(data.encode(), F, Cn, H, 1e-4, warm, iters, 1, 1, os.cpu_count() or 1, 42, buf, 1 << 14,
+             C.byref(h)) < 0:
+            raise RuntimeError(po.ref_lib().lr_last_error().decode())
+        open(ref_csv, "w").write(buf.value.decode())
+    _build.build()
+    cmd = [_build.CLI, "--dataset", data, "--features", str(F), "--classes", str(Cn), "--fc-neurons", str(H),
+           "--eta", "1e-4", "--warmup", str(max(warm, 20)), "--iters", str(max(iters, 20)), "--format", "md"]
+    if os.path.exists(ref_csv):
+        cmd += ["--baseline-csv", ref_csv]
+    out = subprocess.run(cmd, capture_output=True, text=True, check=True)
+    print(f"lane-bench {F}-{H}-{Cn}, eta 1e-4; reference: warmup {warm}, iters {iters}, "
+          f"{os.cpu_count()} host threads; b200: warmup {max(warm, 20)}, iters {max(iters, 20)}")
+    print(out.stdout, end="", flush=True)
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
@@ -294,8 +333,14 @@ def main():
     ap.add_argument("--workload", default="c2", choices=sorted(WORKLOADS) + sorted(MINIBATCH))
     ap.add_argument("--epoch", type=int, default=0, help="override samples per step")
     ap.add_argument("--no-cpu", action="store_true", help="skip the cpu_baseline leg")
+    ap.add_argument("--paper-table", action="store_true",
+                    help="the paper's per-kernel lane-bench table (reference serial/parallel + b200)")
+    ap.add_argument("--fc-neurons", type=int, default=100000, help="--paper-table hidden width")
     args = ap.parse_args()
     wl = args.workload
+    if args.paper_table:
+        run_paper_table(args)
+        return
     if args.impl == "reference":
         run_reference_arm(args, wl)
         return

@@ -157,6 +157,16 @@ int lane_b200_forward(lane_b200_net* net, const float* x_host, float* probs_host
  * hidden backward in reverse, then apply_updates on every layer; G and DW
  * are materialised exactly as the reference's stream_out leaves them. */
 int lane_b200_backward_plan_run(lane_b200_net* net, const float* target_host, float eta);
+/* The same step returning its std::vector<PhaseTiming> (network.hpp:70-72,
+ * task_runtime.hpp:53-60): phase_ms[3*k + {0,1,2}] = copy_in, kernel,
+ * copy_out milliseconds of schedule k, k = 0 the output layer then the hidden
+ * layers in reverse (the order run() executes them); n_phase >= 3 * n_layers.
+ * Times are CUDA events on the context's stream: copy_in is the target's
+ * upload (output layer) and 0 for hidden layers, whose inputs are already
+ * device-resident; copy_out is 0 (nothing leaves the device).  apply_updates
+ * runs after the schedules, untimed, as in the reference.  Blocks. */
+int lane_b200_backward_plan_run_timed(lane_b200_net* net, const float* target_host, float eta,
+                                      double* phase_ms, size_t n_phase);
 
 /* Fused online SGD over a device-resident sample stream: for s in [0, n_steps):
  * k = order[s] (order_dev == NULL => s mod n); FeedForwardNetwork::forward(X[k]);

@@ -246,11 +246,30 @@ inline std::unique_ptr<FeedForwardNetwork> build_network(Device& dev, std::size_
     return net;
 }
 
+// task_runtime.hpp:53-60
+struct PhaseTiming {
+    double copy_in_ms = 0.0;
+    double kernel_ms = 0.0;
+    double copy_out_ms = 0.0;
+    double total_ms() const { return copy_in_ms + kernel_ms + copy_out_ms; }
+};
+
 // network.hpp:58-75
 class BackwardPlan {
 public:
     BackwardPlan(FeedForwardNetwork& net, LearningRate eta) : net_(net), eta_(eta) {}
-    void run(const std::vector<float>& target) {
+    // Blocking, like the reference: one PhaseTiming per schedule, output first.
+    std::vector<PhaseTiming> run(const std::vector<float>& target) {
+        if (target.size() != net_.class_count()) throw ShapeError("backward: target length != class count");
+        const std::size_t nl = net_.hidden.size() + 1;
+        std::vector<double> ph(3 * nl);
+        check(lane_b200_backward_plan_run_timed(net_.handle(), target.data(), eta_.eta, ph.data(), ph.size()));
+        std::vector<PhaseTiming> out(nl);
+        for (std::size_t k = 0; k < nl; ++k) out[k] = {ph[3 * k], ph[3 * k + 1], ph[3 * k + 2]};
+        return out;
+    }
+    // Stream-ordered (no host sync, no timings): the production path.
+    void run_async(const std::vector<float>& target) {
         if (target.size() != net_.class_count()) throw ShapeError("backward: target length != class count");
         check(lane_b200_backward_plan_run(net_.handle(), target.data(), eta_.eta));
     }

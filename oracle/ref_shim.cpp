@@ -379,3 +379,35 @@ int lr_enlarge(const float* X, const float* T, std::size_t n, std::size_t F, std
 }
 
 }  // extern "C"
+
+// lane::run_benchmark + emit_report (bench.cpp:147-209): the reference's own
+// lane-bench report (CSV) and final weights hash, for the B200 lane-bench
+// parity test and bench.py's paper-table mode.  device: 0 serial, 1 parallel.
+extern "C" long lr_run_benchmark(const char* dataset, std::size_t features, std::size_t classes,
+                                 std::size_t fc_neurons, float eta, std::size_t warmup, std::size_t iters,
+                                 std::size_t enlarge, int device, unsigned workers, std::uint64_t seed,
+                                 char* csv, std::size_t csv_len, std::uint64_t* hash) {
+    try {
+        lane::BenchConfig cfg;
+        cfg.dataset_path = dataset;
+        cfg.features = features;
+        cfg.classes = classes;
+        cfg.fc_neurons = fc_neurons;
+        cfg.eta = eta;
+        cfg.warmup_iters = warmup;
+        cfg.timed_iters = iters;
+        cfg.enlarge_factor = enlarge;
+        cfg.device = device ? lane::Device::Kind::ParallelHost : lane::Device::Kind::SerialHost;
+        cfg.workers = workers;
+        cfg.seed = seed;
+        const lane::BenchReport rep = lane::run_benchmark(cfg);
+        const std::string text = lane::emit_report(rep, lane::BenchConfig::Format::Csv);
+        if (hash) *hash = rep.final_weights_hash;
+        if (text.size() + 1 > csv_len) return -1;
+        std::memcpy(csv, text.c_str(), text.size() + 1);
+        return static_cast<long>(text.size());
+    } catch (const std::exception& e) {
+        fail(e);
+        return -1;
+    }
+}

@@ -17,6 +17,7 @@ ROOT = os.path.dirname(PKG)
 CSRC = os.path.join(PKG, "csrc")
 LIBDIR = os.path.join(PKG, "lib")
 LIB = os.path.join(LIBDIR, "liblane_b200.so")
+CLI = os.path.join(LIBDIR, "lane-bench")
 
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
@@ -36,8 +37,21 @@ def needs_build() -> bool:
     return any(os.path.getmtime(p) > t for p in deps)
 
 
+def build_cli(force: bool = False) -> str:
+    """lane-bench for the B200 path (csrc/lane_bench.cpp over the C++ facade)."""
+    src = os.path.join(CSRC, "lane_bench.cpp")
+    deps = [src, LIB, os.path.join(ROOT, "include", "lane_b200", "lane.hpp")]
+    if not force and os.path.exists(CLI) and all(os.path.getmtime(p) <= os.path.getmtime(CLI) for p in deps):
+        return CLI
+    subprocess.run(["g++", "-std=c++17", "-O2", "-Wall", "-I", os.path.join(ROOT, "include"), src, "-o", CLI + ".tmp",
+                    "-L", LIBDIR, "-llane_b200", "-Wl,-rpath,$ORIGIN"], check=True)
+    os.replace(CLI + ".tmp", CLI)
+    return CLI
+
+
 def build(verbose: bool = False, force: bool = False) -> str:
     if not force and not needs_build():
+        build_cli()
         return LIB
     os.makedirs(LIBDIR, exist_ok=True)
     tmp = LIB + ".tmp"
@@ -48,6 +62,7 @@ def build(verbose: bool = False, force: bool = False) -> str:
         print(" ".join(cmd), flush=True)
     subprocess.run(cmd, check=True)
     os.replace(tmp, LIB)
+    build_cli(force=True)
     return LIB
 
 

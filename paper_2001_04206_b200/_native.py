@@ -51,6 +51,7 @@ SIGNATURES = {
     "lane_b200_apply_updates": (_I, [_V, _S]),
     "lane_b200_forward": (_I, [_V, _FP, _FP]),
     "lane_b200_backward_plan_run": (_I, [_V, _FP, _F]),
+    "lane_b200_backward_plan_run_timed": (_I, [_V, _FP, _F, C.POINTER(C.c_double), _S]),
     "lane_b200_sgd_stream": (_I, [_V, _V, _V, _S, _V, _S, _F, _V, _V]),
     "lane_b200_sgd_stream_plan": (_I, [_V, C.c_char_p, _S]),
     "lane_b200_train": (_I, [_V, _FP, _FP, _S, _F, _F, _S, _U64, _FP, _FP, _SP]),

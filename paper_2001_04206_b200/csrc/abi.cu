@@ -181,6 +181,7 @@ struct lane_b200_net {
     MinibatchState mb;  // activations + workspaces of the mini-batch path
     MbGraph mb_graph;   // captured mini-batch step (per configuration)
     InputPipeline pipe;  // pinned staging + copy stream of train_minibatch
+    std::vector<cudaEvent_t> plan_events;  // backward_plan_run_timed
 
     LayerBufs& L(size_t l) { return layers.at(l); }
     size_t out_layer() const { return n_hidden; }
@@ -1108,6 +1109,7 @@ int lane_b200_net_destroy(lane_b200_net* net) {
         cudaFree(net->win_ring);
         net->mb_graph.reset();
         net->pipe.release();
+        for (cudaEvent_t e : net->plan_events) cudaEventDestroy(e);
         cudaFree(net->data);
         cudaFree(net->order);
         lane_b200_ctx* c = net->ctx;
@@ -1282,6 +1284,51 @@ int lane_b200_backward_plan_run(lane_b200_net* net, const float* t_host, float e
         LANE_CUDA(cudaMemcpyAsync(net->target_stage, t_host, net->classes * sizeof(float),
                                   cudaMemcpyHostToDevice, net->ctx->stream));
         run_backward_plan(net, net->target_stage, eta);
+    });
+}
+
+int lane_b200_backward_plan_run_timed(lane_b200_net* net, const float* t_host, float eta, double* phase_ms,
+                                      size_t n_phase) {
+    return guard([&] {
+        if (!net || !t_host || !phase_ms) throw Error(LANE_ERR_CONFIG, "null argument");
+        check_eta(eta);
+        const size_t nl = net->layers.size();
+        if (n_phase < 3 * nl) throw Error(LANE_ERR_SHAPE, "backward_plan_run_timed: phase_ms too short");
+        cudaStream_t st = net->ctx->stream;
+        // events: [0] start, [1] target uploaded, [2 + k] end of schedule k
+        std::vector<cudaEvent_t>& ev = net->plan_events;
+        while (ev.size() < nl + 2) {
+            cudaEvent_t e;
+            LANE_CUDA(cudaEventCreate(&e));
+            ev.push_back(e);
+        }
+        LANE_CUDA(cudaEventRecord(ev[0], st));
+        LANE_CUDA(cudaMemcpyAsync(net->target_stage, t_host, net->classes * sizeof(float), cudaMemcpyHostToDevice,
+                                  st));
+        LANE_CUDA(cudaEventRecord(ev[1], st));
+        run_softmax_backward(net, net->target_stage, eta);
+        LANE_CUDA(cudaEventRecord(ev[2], st));
+        size_t k = 1;
+        for (size_t l = net->n_hidden; l-- > 0; ++k) {
+            LayerBufs& nx = net->L(l + 1);
+            run_fc_backward(net, l, nx.buf[LANE_BUF_W], nx.buf[LANE_BUF_DELTAS], static_cast<int>(nx.O), eta);
+            LANE_CUDA(cudaEventRecord(ev[2 + k], st));
+        }
+        for (size_t l = 0; l < nl; ++l) run_apply_updates(net, l);
+        LANE_CUDA(cudaEventSynchronize(ev[1 + nl]));
+        float ms = 0.0f;
+        LANE_CUDA(cudaEventElapsedTime(&ms, ev[0], ev[1]));
+        phase_ms[0] = ms;
+        LANE_CUDA(cudaEventElapsedTime(&ms, ev[1], ev[2]));
+        phase_ms[1] = ms;
+        phase_ms[2] = 0.0;
+        for (size_t j = 1; j < nl; ++j) {
+            LANE_CUDA(cudaEventElapsedTime(&ms, ev[1 + j], ev[2 + j]));
+            phase_ms[3 * j + 0] = 0.0;
+            phase_ms[3 * j + 1] = ms;
+            phase_ms[3 * j + 2] = 0.0;
+        }
+        LANE_CUDA(cudaStreamSynchronize(st));
     });
 }
 

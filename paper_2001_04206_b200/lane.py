@@ -399,6 +399,28 @@ class BackwardPlan:
             raise ShapeError("backward: target length != class count")
         _check(_native.lib().lane_b200_backward_plan_run(self.net._p, _ptr(t), self.eta))
 
+    def run_timed(self, target) -> list["PhaseTiming"]:
+        """run() returning one PhaseTiming per schedule, output layer first
+        (network.hpp:70-72); device-timed with CUDA events, blocking."""
+        t = _f32(target).reshape(-1)
+        if t.size != self.net.class_count():
+            raise ShapeError("backward: target length != class count")
+        nl = len(self.net.layers)
+        ph = (C.c_double * (3 * nl))()
+        _check(_native.lib().lane_b200_backward_plan_run_timed(self.net._p, _ptr(t), self.eta, ph, 3 * nl))
+        return [PhaseTiming(ph[3 * k], ph[3 * k + 1], ph[3 * k + 2]) for k in range(nl)]
+
+
+@dataclass
+class PhaseTiming:
+    """task_runtime.hpp:53-60 (milliseconds)."""
+    copy_in_ms: float = 0.0
+    kernel_ms: float = 0.0
+    copy_out_ms: float = 0.0
+
+    def total_ms(self) -> float:
+        return self.copy_in_ms + self.kernel_ms + self.copy_out_ms
+
 
 @dataclass
 class TrainerConfig:
