@@ -14,7 +14,10 @@ than the 126 MB L2, streamed from HBM each step.
 value  = samples/s with the inputs resident in HBM (device-timed, CUDA events
          on the library's stream, max over ranks).
 e2e    = samples/s through the public API (lane.train over host arrays in
-         pinned memory: H2D of the epoch, the fused kernel, D2H of EpochStats).
+         pinned memory: the epoch streams through the library's input
+         pipeline in chunks -- host gather of the shuffled rows, H2D on a copy
+         stream overlapping the fused kernel on the previous chunk -- then
+         D2H of EpochStats).
 Multi-GPU: online SGD has a strict sample-to-sample dependency, so N>1 runs N
 independent replicas (one per rank, "replicas only").
 """

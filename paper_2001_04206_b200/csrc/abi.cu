@@ -722,7 +722,18 @@ void launch_window(lane_b200_net* net, const SgdPlan& P, const float* X, const f
         if (const char* e = std::getenv("LANE_B200_SGD_TRACE_BASE")) A.trace_base = std::atoi(e);
     }
     // banded Gram pre-pass
-    k_gram_band<<<static_cast<unsigned>((n_steps + kGramTS - 1) / kGramTS), 256, 0, c->stream>>>(A);
+    {
+        const dim3 g(static_cast<unsigned>((n_steps + kGramTS - 1) / kGramTS));
+        switch ((QW + 7) / 8) {
+            case 2: k_gram_band<2><<<g, 256, 0, c->stream>>>(A); break;
+            case 4: k_gram_band<4><<<g, 256, 0, c->stream>>>(A); break;
+            case 6: k_gram_band<6><<<g, 256, 0, c->stream>>>(A); break;
+            case 8: k_gram_band<8><<<g, 256, 0, c->stream>>>(A); break;
+            case 10: k_gram_band<10><<<g, 256, 0, c->stream>>>(A); break;
+            case 12: k_gram_band<12><<<g, 256, 0, c->stream>>>(A); break;
+            default: throw Error(LANE_ERR_INTERNAL, "window: unsupported Gram band width");
+        }
+    }
     c->count();
     const WinKernel kern = (A.trace && P.jpl == 4 && P.ncw == 1 && P.cs == 1 && A.C == 10)
                                ? k_sgd_window<4, 10, 1, false, 1, kWinMaxNR, true>
@@ -1367,29 +1378,42 @@ int lane_b200_train(lane_b200_net* net, const float* X_host, const float* T_host
         check_eta(eta);
         // train (network.cpp:142-150)
         if (n == 0) throw Error(LANE_ERR_TRAINING, "train: empty training set");
+        if (n > 0xffffffffull) throw Error(LANE_ERR_SHAPE, "train: more than 2^32 samples");
         lane_b200_ctx* c = net->ctx;
         const size_t I = net->input_width, C = net->classes;
-        ensure(net->data, net->data_count, n * (I + C));
-        if (net->order_count < n) {
-            if (net->order) LANE_CUDA(cudaFree(net->order));
-            net->order = static_cast<uint32_t*>(dev_alloc(n * sizeof(uint32_t)));
-            net->order_count = n;
-        }
-        float* Xd = net->data;
-        float* Td = net->data + n * I;
-        LANE_CUDA(cudaMemcpyAsync(Xd, X_host, n * I * sizeof(float), cudaMemcpyHostToDevice, c->stream));
-        LANE_CUDA(cudaMemcpyAsync(Td, T_host, n * C * sizeof(float), cudaMemcpyHostToDevice, c->stream));
+        // The epoch streams through the input pipeline (pipeline.cuh) in
+        // chunks of consecutive stream positions: the host gathers the rows of
+        // the epoch's permutation into a page-locked slot, the copy stream
+        // uploads it, and the fused kernel runs the chunk as a contiguous
+        // stream -- the upload of chunk k+1 overlaps the kernel on chunk k.
+        // Chunks start small (little exposed copy) and double.
+        constexpr size_t kFirst = 2048, kMax = 16384;
+        InputPipeline& P = net->pipe;
+        P.reserve(std::min(n, kMax) * (I + C), 1);
         SplitMix64 shuffle(seed);  // one generator for the whole run (network.cpp:153)
         std::vector<uint32_t> order(n);
         for (size_t k = 0; k < n; ++k) order[k] = static_cast<uint32_t>(k);
-        size_t ran = 0;
+        size_t ran = 0, done = 0;
         for (size_t epoch = 1; epoch <= max_epochs; ++epoch) {
             for (size_t i = n; i > 1; --i) std::swap(order[i - 1], order[shuffle.below(i)]);
-            LANE_CUDA(cudaMemcpyAsync(net->order, order.data(), n * sizeof(uint32_t), cudaMemcpyHostToDevice,
-                                      c->stream));
             LANE_CUDA(cudaMemsetAsync(net->loss_dev, 0, sizeof(double), c->stream));
             LANE_CUDA(cudaMemsetAsync(net->correct_dev, 0, sizeof(unsigned long long), c->stream));
-            sgd_stream_impl(net, Xd, Td, n, net->order, n, eta, net->loss_dev, net->correct_dev);
+            size_t chunk = kFirst;
+            for (size_t s = 0; s < n; s += chunk, chunk = std::min(2 * chunk, kMax)) {
+                const size_t m = std::min(chunk, n - s);
+                const int k = static_cast<int>(done++ % InputPipeline::kSlots);
+                if (P.pending[k]) LANE_CUDA(cudaEventSynchronize(P.copied[k]));
+                gather_rows(X_host, T_host, I, C, order.data() + s, m, P.host[k]);
+                LANE_CUDA(cudaStreamWaitEvent(P.copy, P.consumed[k], 0));
+                LANE_CUDA(cudaMemcpyAsync(P.dev[k], P.host[k], m * (I + C) * sizeof(float), cudaMemcpyHostToDevice,
+                                          P.copy));
+                LANE_CUDA(cudaEventRecord(P.copied[k], P.copy));
+                LANE_CUDA(cudaStreamWaitEvent(c->stream, P.copied[k], 0));
+                sgd_stream_impl(net, P.dev[k], P.dev[k] + m * I, m, nullptr, m, eta, net->loss_dev,
+                                net->correct_dev);
+                LANE_CUDA(cudaEventRecord(P.consumed[k], c->stream));
+                P.pending[k] = true;
+            }
             double loss_sum = 0;
             unsigned long long correct = 0;
             LANE_CUDA(cudaMemcpyAsync(&loss_sum, net->loss_dev, sizeof(double), cudaMemcpyDeviceToHost, c->stream));

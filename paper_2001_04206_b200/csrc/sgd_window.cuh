@@ -250,39 +250,72 @@ __device__ __forceinline__ void xpose_step(float* v, int lane, int o) {
 // d0(s) needs for every later row r = s+d are contiguous.  One CTA per 32
 // stream positions; K streamed through shared memory in 32-float chunks.
 // ---------------------------------------------------------------------------
-constexpr int kGramTS = 32, kGramKC = 32, kGramMaxQW = 96;
+constexpr int kGramTS = 32, kGramKC = 64, kGramMaxQW = 96;
 
+// NQ = ceil(QW / 8): thread (sl, dg) accumulates d = dg+1, dg+9, ... <= QW.
+// K chunks of 64 floats, loaded as float4 (I % 4 == 0) one chunk ahead in
+// registers, so the global latency hides under the previous chunk's FMAs.
+template <int NQ>
 __global__ void __launch_bounds__(256) k_gram_band(WinArgs A) {
-    __shared__ float xs[kGramTS + kGramMaxQW][kGramKC + 1];
-    __shared__ long long rows[kGramTS + kGramMaxQW];
+    constexpr int kRows = kGramTS + 8 * NQ;            // rows s0 .. s0+TS+QW-1 (QW <= 8 NQ)
+    constexpr int kLd = (kRows * kGramKC / 4 + 255) / 256;  // float4 loads per thread per chunk
+    __shared__ float xs[kRows][kGramKC + 1];
+    __shared__ long long rows[kRows];
     const int QW = A.QW, I = A.I;
     const int s0 = blockIdx.x * kGramTS;
-    const int NRW = kGramTS + QW;  // rows s0 .. s0+TS+QW-1
-    for (int r = threadIdx.x; r < NRW; r += blockDim.x) {
+    const int NRW = kGramTS + QW;
+    for (int r = threadIdx.x; r < kRows; r += blockDim.x) {
         const int s = s0 + r;
-        rows[r] = s < A.n_steps ? win_row(A, s) : -1;
+        rows[r] = (r < NRW && s < A.n_steps) ? win_row(A, s) : -1;
     }
-    const int sl = threadIdx.x & 31, dg = threadIdx.x >> 5;  // d = dg+1 + 8q
-    constexpr int NQ = kGramMaxQW / 8;
+    const int sl = threadIdx.x & 31, dg = threadIdx.x >> 5;
     float acc[NQ];
 #pragma unroll
     for (int q = 0; q < NQ; ++q) acc[q] = 0.0f;
     __syncthreads();
+    const bool vec = (I & 3) == 0;
+    float4 pf[kLd];
+    auto load = [&](int k0) {
+#pragma unroll
+        for (int l = 0; l < kLd; ++l) {
+            const int e = threadIdx.x + 256 * l;  // (row, quad) = (e / 16, e % 16)
+            const int r = e >> 4, kk = (e & 15) * 4;
+            float4 v = make_float4(0.f, 0.f, 0.f, 0.f);
+            const long long row = r < kRows ? rows[r] : -1;
+            if (row >= 0) {
+                const float* src = A.X + row * I + k0 + kk;
+                if (vec && k0 + kk + 3 < I) {
+                    v = __ldg(reinterpret_cast<const float4*>(src));
+                } else {
+                    if (k0 + kk + 0 < I) v.x = __ldg(src + 0);
+                    if (k0 + kk + 1 < I) v.y = __ldg(src + 1);
+                    if (k0 + kk + 2 < I) v.z = __ldg(src + 2);
+                    if (k0 + kk + 3 < I) v.w = __ldg(src + 3);
+                }
+            }
+            pf[l] = v;
+        }
+    };
+    load(0);
     for (int k0 = 0; k0 < I; k0 += kGramKC) {
-        for (int e = threadIdx.x; e < NRW * kGramKC; e += blockDim.x) {
-            const int r = e / kGramKC, kk = e - r * kGramKC;
-            const long long row = rows[r];
-            xs[r][kk] = (row >= 0 && k0 + kk < I) ? __ldg(A.X + row * I + k0 + kk) : 0.0f;
+#pragma unroll
+        for (int l = 0; l < kLd; ++l) {
+            const int e = threadIdx.x + 256 * l;
+            const int r = e >> 4, kk = (e & 15) * 4;
+            if (r < kRows) {
+                xs[r][kk + 0] = pf[l].x;
+                xs[r][kk + 1] = pf[l].y;
+                xs[r][kk + 2] = pf[l].z;
+                xs[r][kk + 3] = pf[l].w;
+            }
         }
         __syncthreads();
-#pragma unroll 4
+        if (k0 + kGramKC < I) load(k0 + kGramKC);
+#pragma unroll 8
         for (int kk = 0; kk < kGramKC; ++kk) {
             const float xv = xs[sl][kk];
 #pragma unroll
-            for (int q = 0; q < NQ; ++q) {
-                const int d = dg + 1 + 8 * q;
-                if (d <= QW) acc[q] = fmaf(xv, xs[sl + d][kk], acc[q]);
-            }
+            for (int q = 0; q < NQ; ++q) acc[q] = fmaf(xv, xs[sl + dg + 1 + 8 * q][kk], acc[q]);
         }
         __syncthreads();
     }
