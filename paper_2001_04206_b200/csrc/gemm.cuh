@@ -458,19 +458,19 @@ inline bool gemm_try_tc(GemmCtx& g, GemmOp op, int M, int N, int K, const float*
     switch (op) {
         case GemmOp::NN:  // A [M][K] K-major, B [K][N] MN-major
             if (lda != K || ldb != N) return false;
-            ma = tc_map(A, M, K, 32, 128, false);
-            mb = tc_map(B, K, N, 32, 32, true);
+            ma = tc_map(A, M, K, 32, 128, 0);
+            mb = tc_map(B, K, N, 32, 32, 1);
             b_mn = true;
             break;
         case GemmOp::NT:  // A [M][K] K-major, B [N][K] K-major
             if (lda != K || ldb != K) return false;
-            ma = tc_map(A, M, K, 32, 128, false);
-            mb = tc_map(B, N, K, 32, 128, false);
+            ma = tc_map(A, M, K, 32, 128, 0);
+            mb = tc_map(B, N, K, 32, 128, 0);
             break;
         case GemmOp::TN:  // A [K][M] MN-major, B [K][N] MN-major
             if (lda != M || ldb != N) return false;
-            ma = tc_map(A, K, M, 32, 32, true);
-            mb = tc_map(B, K, N, 32, 32, true);
+            ma = tc_map(A, K, M, 128, 32, 2);
+            mb = tc_map(B, K, N, 32, 32, 1);
             a_mn = b_mn = true;
             break;
     }

@@ -2,23 +2,32 @@
 // (tcgen05, kind::tf32) for the mini-batch path, "3xTF32":
 //     A.B ~= A_lo.B + A.B_lo + A.B      (A_lo = A - tf32(A), exact in fp32)
 // The tensor core reads fp32 operands and ignores their low 13 mantissa bits,
-// so A itself is the "hi" part; the lo parts are produced in shared memory by
-// an elementwise pass over each TMA-loaded tile (same swizzled layout, so the
-// same descriptors apply).  All three products accumulate into one fp32 TMEM
-// accumulator.  Relative error per product ~2^-21 (the dropped A_lo.B_lo term
+// so A itself is the "hi" part.  A is staged through tensor memory: the split
+// warps read each TMA-loaded A tile once and write A and A_lo into TMEM
+// (tcgen05.st); the MMAs take A from TMEM and B / B_lo from shared memory.
+// Shared-memory traffic per 128x128x32 K block is then 128 KB (TMA 32, split
+// reads 32 + B_lo writes 16, MMA operand reads 48) instead of 192 KB with both
+// lo parts in shared memory -- the kernel was bound by the ~128 B/clk of SMEM
+// bandwidth, not by the tensor pipe.  All three products accumulate into one
+// fp32 TMEM accumulator.  Relative error per product ~2^-21 (the dropped A_lo.B_lo term
 // and the tf32 truncation of the lo parts), within the path's 1e-5 tolerance
 // (1xTF32 alone is ~5e-4 and is NOT used).
 //
-// Structure (one 128x128 output tile per CTA, 192 threads):
-//   warp 0      TMA producer: A/B tiles (fp32, 128B swizzle) -> smem ring
-//   warp 1      MMA issuer: one elected thread issues tcgen05.mma, commits
-//               smem slots back to the producer and the accumulator to the
-//               epilogue (tcgen05.commit -> mbarrier)
-//   warps 2..9  split pass (A_lo, B_lo per stage), then the epilogue (two
-//               warps per TMEM lane quarter, 64 columns each):
-//               tcgen05.ld TMEM -> registers -> fused epilogue -> global
-// Operand majors: K-major tiles come from one TMA box {32 (K), 128 (MN)};
-// MN-major tiles from four boxes {32 (MN), 32 (K)} (one per 32-wide MN group).
+// Structure (one 128x128 output tile per CTA, 320 threads, 4-stage ring):
+//   warp 0      TMA producer: A/B tiles (fp32) -> smem ring
+//   warp 1      MMA issuer: one elected thread issues tcgen05.mma (A from
+//               TMEM), commits smem/TMEM slots back to the producer and the
+//               accumulator to the epilogue (tcgen05.commit -> mbarrier)
+//   warps 2..9  split pass: rows of A -> TMEM (A, A_lo; the two warps of a
+//               TMEM lane quarter take 16 K columns each) and B_lo -> smem;
+//               then the epilogue (two warps per lane quarter, 64 columns
+//               each): tcgen05.ld TMEM -> registers -> fused epilogue -> global
+// TMEM: columns [0,128) accumulator, then per stage 32 columns of A and 32 of
+// A_lo (lane = row of A, column = k).
+// Operand majors: K-major tiles come from one TMA box {32 (K), 128 (MN)},
+// 128B swizzle; a MN-major B from four boxes {32 (MN), 32 (K)} (32-byte-atom
+// swizzle, the layout the MMA reads); a MN-major A -- read only by the split
+// warps -- from one unswizzled box {128 (MN), 32 (K)}.
 #pragma once
 
 #include <cuda.h>
@@ -27,9 +36,10 @@
 
 namespace lane_b200 {
 
-constexpr int kTcBM = 128, kTcBN = 128, kTcBK = 32, kTcStages = 3;
+constexpr int kTcBM = 128, kTcBN = 128, kTcBK = 32, kTcStages = 4;
 constexpr int kTcTile = kTcBM * kTcBK * 4;  // bytes of one 128x32 fp32 tile (A or B)
-constexpr int kTcStage = 4 * kTcTile;       // A, B, A_lo, B_lo
+constexpr int kTcStage = 3 * kTcTile;       // A, B, B_lo
+constexpr int kTcTmemCols = 512;            // accumulator (128) + kTcStages x (A, A_lo) x 32
 constexpr int kTcSplitWarps = 8;  // the split pass is the busiest role (3xTF32)
 constexpr int kTcThreads = 64 + 32 * kTcSplitWarps;
 constexpr size_t kTcSmem = (size_t)kTcStages * kTcStage + 1024 /*align*/ + 256 /*barriers*/;
@@ -93,6 +103,23 @@ __device__ __forceinline__ void tc_mma(uint32_t tmem_d, uint64_t da, uint64_t db
         " tcgen05.mma.cta_group::1.kind::tf32 [%0], %1, %2, %3, p;\n}\n" ::"r"(tmem_d),
         "l"(da), "l"(db), "r"(idesc), "r"(acc));
 }
+// A from tensor memory (K-major: lane = row, column = k), B from shared memory
+__device__ __forceinline__ void tc_mma_ts(uint32_t tmem_d, uint32_t tmem_a, uint64_t db, uint32_t idesc,
+                                          uint32_t acc) {
+    asm volatile(
+        "{\n .reg .pred p;\n setp.ne.b32 p, %4, 0;\n"
+        " tcgen05.mma.cta_group::1.kind::tf32 [%0], [%1], %2, %3, p;\n}\n" ::"r"(tmem_d),
+        "r"(tmem_a), "l"(db), "r"(idesc), "r"(acc));
+}
+// 32 lanes x 16 consecutive 32-bit TMEM columns from registers
+__device__ __forceinline__ void tc_st16(uint32_t taddr, const uint32_t (&v)[16]) {
+    asm volatile(
+        "tcgen05.st.sync.aligned.32x32b.x16.b32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,%16};\n" ::"r"(
+            taddr),
+        "r"(v[0]), "r"(v[1]), "r"(v[2]), "r"(v[3]), "r"(v[4]), "r"(v[5]), "r"(v[6]), "r"(v[7]), "r"(v[8]),
+        "r"(v[9]), "r"(v[10]), "r"(v[11]), "r"(v[12]), "r"(v[13]), "r"(v[14]), "r"(v[15])
+        : "memory");
+}
 __device__ __forceinline__ void tc_commit(uint32_t bar) {
     asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];\n" ::"r"(bar)
                  : "memory");
@@ -133,7 +160,7 @@ __global__ void __launch_bounds__(kTcThreads, 1)
     extern __shared__ uint8_t tc_raw[];
     uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(tc_raw) + 1023) & ~uintptr_t(1023));
     uint64_t* bars = reinterpret_cast<uint64_t*>(smem + (size_t)kTcStages * kTcStage);
-    // bars: full[3], conv[3], empty[3], tmem_full[1]; then the TMEM address
+    // bars: full[S], conv[S], empty[S], tmem_full[1]; then the TMEM address
     uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 16);
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const int m0 = blockIdx.y * kTcBM, n0 = blockIdx.x * kTcBN;
@@ -145,13 +172,12 @@ __global__ void __launch_bounds__(kTcThreads, 1)
     const bool split = gridDim.z > 1;
     const uint32_t sbase = tc_smem(smem);
     auto full = [&](int s) { return tc_smem(bars + s); };
-    auto conv = [&](int s) { return tc_smem(bars + 3 + s); };
-    auto empty = [&](int s) { return tc_smem(bars + 6 + s); };
-    const uint32_t tmem_full = tc_smem(bars + 9);
+    auto conv = [&](int s) { return tc_smem(bars + kTcStages + s); };
+    auto empty = [&](int s) { return tc_smem(bars + 2 * kTcStages + s); };
+    const uint32_t tmem_full = tc_smem(bars + 3 * kTcStages);
     auto tileA = [&](int s) { return sbase + (uint32_t)(s * kTcStage); };
     auto tileB = [&](int s) { return sbase + (uint32_t)(s * kTcStage + kTcTile); };
-    auto tileAlo = [&](int s) { return sbase + (uint32_t)(s * kTcStage + 2 * kTcTile); };
-    auto tileBlo = [&](int s) { return sbase + (uint32_t)(s * kTcStage + 3 * kTcTile); };
+    auto tileBlo = [&](int s) { return sbase + (uint32_t)(s * kTcStage + 2 * kTcTile); };
 
     if (threadIdx.x == 0) {
         for (int s = 0; s < kTcStages; ++s) {
@@ -166,7 +192,7 @@ __global__ void __launch_bounds__(kTcThreads, 1)
     }
     if (warp == 1) {
         asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;\n" ::"r"(tc_smem(tmem_slot)),
-                     "r"(kTcBN));
+                     "r"(kTcTmemCols));
         asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;\n");
     }
     asm volatile("tcgen05.fence::before_thread_sync;\n" ::: "memory");
@@ -183,12 +209,10 @@ __global__ void __launch_bounds__(kTcThreads, 1)
                 tc_mbar_wait(empty(s), ph ^ 1);
                 tc_mbar_expect_tx(full(s), 2 * kTcTile);
                 const int k0 = (kb0 + kb) * kTcBK;
-                if constexpr (!A_MN) {
+                if constexpr (!A_MN)
                     tc_tma_2d(&tmA, full(s), tileA(s), k0, m0);
-                } else {
-#pragma unroll
-                    for (int g = 0; g < 4; ++g) tc_tma_2d(&tmA, full(s), tileA(s) + g * 4096, m0 + 32 * g, k0);
-                }
+                else
+                    tc_tma_2d(&tmA, full(s), tileA(s), m0, k0);  // unswizzled [k][128 m]
                 if constexpr (!B_MN) {
                     tc_tma_2d(&tmB, full(s), tileB(s), k0, n0);
                 } else {
@@ -199,10 +223,9 @@ __global__ void __launch_bounds__(kTcThreads, 1)
         }
     } else if (warp == 1) {
         // ---------------- MMA issuer ----------------
-        // instruction descriptor: D f32, A/B tf32, majors, N>>3, M>>4
-        const uint32_t idesc = (1u << 4) | (2u << 7) | (2u << 10) | ((A_MN ? 1u : 0u) << 15) |
-                               ((B_MN ? 1u : 0u) << 16) | ((uint32_t)(kTcBN >> 3) << 17) |
-                               ((uint32_t)(kTcBM >> 4) << 24);
+        // instruction descriptor: D f32, A/B tf32, A K-major (TMEM), B major, N>>3, M>>4
+        const uint32_t idesc = (1u << 4) | (2u << 7) | (2u << 10) | ((B_MN ? 1u : 0u) << 16) |
+                               ((uint32_t)(kTcBN >> 3) << 17) | ((uint32_t)(kTcBM >> 4) << 24);
         for (int kb = 0; kb < nkb; ++kb) {
             const int s = kb % kTcStages;
             const uint32_t ph = (uint32_t)((kb / kTcStages) & 1);
@@ -211,21 +234,18 @@ __global__ void __launch_bounds__(kTcThreads, 1)
             if (lane == 0) {
 #pragma unroll
                 for (int ks = 0; ks < kTcBK / 8; ++ks) {
-                    // K-major: +32 B inside the 128 B swizzle row; MN-major: +8 rows
-                    const uint32_t ao = A_MN ? ks * 1024u : ks * 32u;
+                    // B: K-major +32 B inside the 128 B swizzle row (SBO = 8 rows x
+                    // 128 B); MN-major SW128_BASE32B +8 K-rows (LBO = 32-wide MN
+                    // group, one TMA box; SBO = 4 K-rows x 128 B)
                     const uint32_t bo = B_MN ? ks * 1024u : ks * 32u;
-                    // K-major SW128: SBO = 8 rows x 128 B; MN-major SW128_BASE32B:
-                    // LBO = 32-wide MN group (one TMA box), SBO = 4 K-rows x 128 B
-                    const uint32_t albo = A_MN ? 4096u : 16u, asbo = A_MN ? 512u : 1024u, alay = A_MN ? 1u : 2u;
                     const uint32_t blbo = B_MN ? 4096u : 16u, bsbo = B_MN ? 512u : 1024u, blay = B_MN ? 1u : 2u;
-                    const uint64_t dA = tc_desc(tileA(s) + ao, albo, asbo, alay);
                     const uint64_t dB = tc_desc(tileB(s) + bo, blbo, bsbo, blay);
-                    const uint64_t dAl = tc_desc(tileAlo(s) + ao, albo, asbo, alay);
                     const uint64_t dBl = tc_desc(tileBlo(s) + bo, blbo, bsbo, blay);
+                    const uint32_t tA = tmem + (uint32_t)(kTcBN + 64 * s + 8 * ks);  // A; A_lo at +32
                     const uint32_t first = (kb == 0 && ks == 0) ? 0u : 1u;
-                    tc_mma(tmem, dAl, dB, idesc, first);  // small terms first
-                    tc_mma(tmem, dA, dBl, idesc, 1u);
-                    tc_mma(tmem, dA, dB, idesc, 1u);
+                    tc_mma_ts(tmem, tA + 32u, dB, idesc, first);  // small terms first
+                    tc_mma_ts(tmem, tA, dBl, idesc, 1u);
+                    tc_mma_ts(tmem, tA, dB, idesc, 1u);
                 }
                 tc_commit(empty(s));  // slot free once these MMAs have read it
             }
@@ -236,23 +256,52 @@ __global__ void __launch_bounds__(kTcThreads, 1)
     } else {
         // ---------------- split pass, then epilogue (warps 2..9) ----------------
         const int ct = threadIdx.x - 64;  // 0..32*kTcSplitWarps-1
+        const int quarter_s = warp & 3;   // TMEM lanes this warp may access
+        const int rowA = quarter_s * 32 + lane;
+        const int khalf = (warp - 2) >> 2;  // K columns [16 khalf, 16 khalf + 16) of the block
         for (int kb = 0; kb < nkb; ++kb) {
             const int s = kb % kTcStages;
             const uint32_t ph = (uint32_t)((kb / kTcStages) & 1);
             tc_mbar_wait(full(s), ph);
-            const float4* a = reinterpret_cast<const float4*>(smem + (size_t)s * kTcStage);
+            const uint8_t* a = smem + (size_t)s * kTcStage;
             const float4* b = reinterpret_cast<const float4*>(smem + (size_t)s * kTcStage + kTcTile);
-            float4* al = reinterpret_cast<float4*>(smem + (size_t)s * kTcStage + 2 * kTcTile);
-            float4* bl = reinterpret_cast<float4*>(smem + (size_t)s * kTcStage + 3 * kTcTile);
+            float4* bl = reinterpret_cast<float4*>(smem + (size_t)s * kTcStage + 2 * kTcTile);
+            // A row rowA, K columns [16 khalf, +16) -> TMEM (A and A_lo)
+            uint32_t hi[16], lo[16];
+            if constexpr (!A_MN) {
+                // SW128: 16-byte chunk c of row r sits at chunk c ^ (r & 7)
+#pragma unroll
+                for (int c = 0; c < 4; ++c) {
+                    const int chunk = (4 * khalf + c) ^ (rowA & 7);
+                    const float4 v = *reinterpret_cast<const float4*>(a + rowA * 128 + chunk * 16);
+                    hi[4 * c + 0] = __float_as_uint(v.x);
+                    hi[4 * c + 1] = __float_as_uint(v.y);
+                    hi[4 * c + 2] = __float_as_uint(v.z);
+                    hi[4 * c + 3] = __float_as_uint(v.w);
+                }
+            } else {
+                // unswizzled [k][128 m]
+#pragma unroll
+                for (int j = 0; j < 16; ++j)
+                    hi[j] = __float_as_uint(*reinterpret_cast<const float*>(a + (16 * khalf + j) * 512 + rowA * 4));
+            }
+#pragma unroll
+            for (int j = 0; j < 16; ++j) lo[j] = __float_as_uint(tf32_lo(__uint_as_float(hi[j])));
+            const uint32_t tA = tmem + ((uint32_t)(quarter_s * 32) << 16) + (uint32_t)(kTcBN + 64 * s + 16 * khalf);
+            tc_st16(tA, hi);
+            tc_st16(tA + 32u, lo);
+            // B_lo -> smem (same swizzled layout as B)
 #pragma unroll
             for (int u = 0; u < kTcTile / 16 / (32 * kTcSplitWarps); ++u) {
                 const int q = ct + 32 * kTcSplitWarps * u;
-                const float4 va = a[q], vb = b[q];
-                al[q] = make_float4(tf32_lo(va.x), tf32_lo(va.y), tf32_lo(va.z), tf32_lo(va.w));
+                const float4 vb = b[q];
                 bl[q] = make_float4(tf32_lo(vb.x), tf32_lo(vb.y), tf32_lo(vb.z), tf32_lo(vb.w));
             }
-            // generic-proxy smem writes -> visible to the tensor core (async proxy)
+            // TMEM stores complete + generic-proxy smem writes visible to the
+            // tensor core (async proxy) before the MMA issuer is released
+            asm volatile("tcgen05.wait::st.sync.aligned;\n" ::: "memory");
             asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");
+            asm volatile("tcgen05.fence::before_thread_sync;\n" ::: "memory");
             __syncwarp();
             if (lane == 0) tc_mbar_arrive(conv(s));
         }
@@ -314,7 +363,7 @@ __global__ void __launch_bounds__(kTcThreads, 1)
     __syncthreads();
     if (warp == 1) {
         asm volatile("tcgen05.fence::after_thread_sync;\n" ::: "memory");
-        asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;\n" ::"r"(tmem), "r"(kTcBN));
+        asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;\n" ::"r"(tmem), "r"(kTcTmemCols));
     }
 }
 
@@ -364,8 +413,9 @@ inline PFN_encodeTiled tc_encoder() {
 }
 
 // 2-D fp32 row-major tensor [rows x cols] (ld = cols), box {box_inner, box_rows};
-// mn_major selects the 32-byte-atom 128B swizzle the MN-major tf32 layout needs
-inline CUtensorMap tc_map(const float* base, int rows, int cols, int box_inner, int box_rows, bool mn_major) {
+// swizzle: 0 = 128B (K-major MMA operand), 1 = 128B with 32-byte atoms (the
+// MN-major tf32 MMA operand), 2 = none (read by the split warps only)
+inline CUtensorMap tc_map(const float* base, int rows, int cols, int box_inner, int box_rows, int swizzle) {
     CUtensorMap m;
     const cuuint64_t dims[2] = {(cuuint64_t)cols, (cuuint64_t)rows};
     const cuuint64_t strides[1] = {(cuuint64_t)cols * sizeof(float)};
@@ -373,7 +423,9 @@ inline CUtensorMap tc_map(const float* base, int rows, int cols, int box_inner, 
     const cuuint32_t estr[2] = {1, 1};
     const CUresult r = tc_encoder()(&m, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2, const_cast<float*>(base), dims, strides,
                                     box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
-                                    mn_major ? CU_TENSOR_MAP_SWIZZLE_128B_ATOM_32B : CU_TENSOR_MAP_SWIZZLE_128B,
+                                    swizzle == 1   ? CU_TENSOR_MAP_SWIZZLE_128B_ATOM_32B
+                                    : swizzle == 2 ? CU_TENSOR_MAP_SWIZZLE_NONE
+                                                   : CU_TENSOR_MAP_SWIZZLE_128B,
                                     CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
     if (r != CUDA_SUCCESS) throw Error(LANE_ERR_CUDA, "cuTensorMapEncodeTiled failed");
     return m;
