@@ -455,6 +455,11 @@ inline bool gemm_try_tc(GemmCtx& g, GemmOp op, int M, int N, int K, const float*
         return false;
     CUtensorMap ma, mb;
     bool a_mn = false, b_mn = false;
+    // CTA pairs (cta_group::2, 256 x 128 tiles) for the large square GEMMs
+    // (C5: 0.596 -> 0.578 ms at 4096^3); the M = 256 / K = 256 shapes of C3
+    // run faster on single CTAs (short K loops, split-K)
+    static const bool pair_ok = !std::getenv("LANE_B200_TC_NOPAIR");
+    const bool pair = pair_ok && M >= 4 * kTcBM && K >= 2048;
     switch (op) {
         case GemmOp::NN:  // A [M][K] K-major, B [K][N] MN-major
             if (lda != K || ldb != N) return false;
@@ -465,7 +470,7 @@ inline bool gemm_try_tc(GemmCtx& g, GemmOp op, int M, int N, int K, const float*
         case GemmOp::NT:  // A [M][K] K-major, B [N][K] K-major
             if (lda != K || ldb != K) return false;
             ma = tc_map(A, M, K, 32, 128, 0);
-            mb = tc_map(B, N, K, 32, 128, 0);
+            mb = tc_map(B, N, K, 32, pair ? kTcBN / 2 : kTcBN, 0);
             break;
         case GemmOp::TN:  // A [K][M] MN-major, B [K][N] MN-major
             if (lda != M || ldb != N) return false;
@@ -489,10 +494,22 @@ inline bool gemm_try_tc(GemmCtx& g, GemmOp op, int M, int N, int K, const float*
         *g.launches += 1;  // the split-K reduce
     }
     switch (e) {
-        case Epi::STORE: tc_dispatch<TcEpi::STORE>(g.stream, a_mn, b_mn, ma, mb, t); break;
-        case Epi::BIAS: tc_dispatch<TcEpi::BIAS>(g.stream, a_mn, b_mn, ma, mb, t); break;
-        case Epi::BIAS_TANH: tc_dispatch<TcEpi::BIAS_TANH>(g.stream, a_mn, b_mn, ma, mb, t); break;
-        case Epi::TANH_GRAD: tc_dispatch<TcEpi::TANH_GRAD>(g.stream, a_mn, b_mn, ma, mb, t); break;
+        case Epi::STORE:
+            if (pair) tc_dispatch<TcEpi::STORE, true>(g.stream, a_mn, b_mn, ma, mb, t);
+            else tc_dispatch<TcEpi::STORE, false>(g.stream, a_mn, b_mn, ma, mb, t);
+            break;
+        case Epi::BIAS:
+            if (pair) tc_dispatch<TcEpi::BIAS, true>(g.stream, a_mn, b_mn, ma, mb, t);
+            else tc_dispatch<TcEpi::BIAS, false>(g.stream, a_mn, b_mn, ma, mb, t);
+            break;
+        case Epi::BIAS_TANH:
+            if (pair) tc_dispatch<TcEpi::BIAS_TANH, true>(g.stream, a_mn, b_mn, ma, mb, t);
+            else tc_dispatch<TcEpi::BIAS_TANH, false>(g.stream, a_mn, b_mn, ma, mb, t);
+            break;
+        case Epi::TANH_GRAD:
+            if (pair) tc_dispatch<TcEpi::TANH_GRAD, true>(g.stream, a_mn, b_mn, ma, mb, t);
+            else tc_dispatch<TcEpi::TANH_GRAD, false>(g.stream, a_mn, b_mn, ma, mb, t);
+            break;
     }
     *g.launches += 1;
     return true;

@@ -36,13 +36,22 @@
 
 namespace lane_b200 {
 
-constexpr int kTcBM = 128, kTcBN = 128, kTcBK = 32, kTcStages = 4;
-constexpr int kTcTile = kTcBM * kTcBK * 4;  // bytes of one 128x32 fp32 tile (A or B)
-constexpr int kTcStage = 3 * kTcTile;       // A, B, B_lo
-constexpr int kTcTmemCols = 512;            // accumulator (128) + kTcStages x (A, A_lo) x 32
+constexpr int kTcBM = 128, kTcBN = 128, kTcBK = 32;
+constexpr int kTcTile = kTcBM * kTcBK * 4;  // bytes of one 128x32 fp32 tile (A)
+constexpr int kTcTmemCols = 512;            // accumulator (128) + stages x (A, A_lo) x 32
+// Per-CTA ring.  PAIR = a CTA pair (cluster of 2, tcgen05 cta_group::2) on a
+// 256 x 128 tile: each CTA holds its 128 rows of A and half (64 columns) of B,
+// so each SM reads half the B bytes per MMA and the ring fits 6 stages.
+template <bool PAIR>
+struct TcCfg {
+    static constexpr int kBLocal = PAIR ? kTcBN / 2 : kTcBN;  // B columns this CTA holds
+    static constexpr int kBTile = kBLocal * kTcBK * 4;
+    static constexpr int kStage = kTcTile + 2 * kBTile;  // A, B, B_lo
+    static constexpr int kStages = PAIR ? 6 : 4;         // TMEM: 128 + 64 x stages <= 512
+    static constexpr size_t kSmem = (size_t)kStages * kStage + 1024 /*align*/ + 512 /*barriers*/;
+};
 constexpr int kTcSplitWarps = 8;  // the split pass is the busiest role (3xTF32)
 constexpr int kTcThreads = 64 + 32 * kTcSplitWarps;
-constexpr size_t kTcSmem = (size_t)kTcStages * kTcStage + 1024 /*align*/ + 256 /*barriers*/;
 
 enum class TcEpi : int { STORE = 0, BIAS = 1, BIAS_TANH = 2, TANH_GRAD = 3 };
 
@@ -111,6 +120,40 @@ __device__ __forceinline__ void tc_mma_ts(uint32_t tmem_d, uint32_t tmem_a, uint
         " tcgen05.mma.cta_group::1.kind::tf32 [%0], [%1], %2, %3, p;\n}\n" ::"r"(tmem_d),
         "r"(tmem_a), "l"(db), "r"(idesc), "r"(acc));
 }
+__device__ __forceinline__ void tc_mma_ts_pair(uint32_t tmem_d, uint32_t tmem_a, uint64_t db, uint32_t idesc,
+                                               uint32_t acc) {
+    asm volatile(
+        "{\n .reg .pred p;\n setp.ne.b32 p, %4, 0;\n"
+        " tcgen05.mma.cta_group::2.kind::tf32 [%0], [%1], %2, %3, p;\n}\n" ::"r"(tmem_d),
+        "r"(tmem_a), "l"(db), "r"(idesc), "r"(acc));
+}
+// arrive on the same-offset barrier of both CTAs of the pair once the MMAs
+// issued so far have completed
+__device__ __forceinline__ void tc_commit_pair(uint32_t bar) {
+    asm volatile(
+        "tcgen05.commit.cta_group::2.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64 [%0], %1;\n" ::"r"(
+            bar),
+        "h"((unsigned short)3)
+        : "memory");
+}
+// release-arrive on the barrier at this CTA-local offset in cluster CTA `rank`
+__device__ __forceinline__ void tc_mbar_arrive_remote(uint32_t local, uint32_t rank) {
+    uint32_t remote;
+    asm volatile("mapa.shared::cluster.u32 %0, %1, %2;\n" : "=r"(remote) : "r"(local), "r"(rank));
+    asm volatile("mbarrier.arrive.release.cluster.shared::cluster.b64 _, [%0];\n" ::"r"(remote) : "memory");
+}
+__device__ __forceinline__ void tc_mbar_wait_cluster(uint32_t a, uint32_t parity) {
+    asm volatile(
+        "{\n .reg .pred p;\n"
+        "WAITC_%=:\n"
+        " mbarrier.try_wait.parity.acquire.cluster.shared::cta.b64 p, [%0], %1;\n"
+        " @!p bra WAITC_%=;\n}\n" ::"r"(a),
+        "r"(parity)
+        : "memory");
+}
+__device__ __forceinline__ void tc_cluster_sync() {
+    asm volatile("barrier.cluster.arrive.release.aligned;\nbarrier.cluster.wait.acquire.aligned;\n" ::: "memory");
+}
 // 32 lanes x 16 consecutive 32-bit TMEM columns from registers
 __device__ __forceinline__ void tc_st16(uint32_t taddr, const uint32_t (&v)[16]) {
     asm volatile(
@@ -154,16 +197,21 @@ __device__ __forceinline__ float4 tc_epi4(const TcArgs& a, int m, int n, float4 
     return v;
 }
 
-template <bool A_MN, bool B_MN, TcEpi E>
+template <bool A_MN, bool B_MN, TcEpi E, bool PAIR>
 __global__ void __launch_bounds__(kTcThreads, 1)
     k_gemm_tc(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB, TcArgs args) {
+    using Cfg = TcCfg<PAIR>;
+    constexpr int kTcStages = Cfg::kStages, kTcStage = Cfg::kStage, kBTile = Cfg::kBTile;
     extern __shared__ uint8_t tc_raw[];
     uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(tc_raw) + 1023) & ~uintptr_t(1023));
     uint64_t* bars = reinterpret_cast<uint64_t*>(smem + (size_t)kTcStages * kTcStage);
     // bars: full[S], conv[S], empty[S], tmem_full[1]; then the TMEM address
-    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 16);
+    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 32);
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    const int m0 = blockIdx.y * kTcBM, n0 = blockIdx.x * kTcBN;
+    // PAIR: cluster (2,1,1) along x = M; rank 0 issues the pair's MMAs
+    const uint32_t rank = PAIR ? (blockIdx.x & 1u) : 0u;
+    const int m0 = PAIR ? (int)(blockIdx.x >> 1) * 2 * kTcBM + (int)rank * kTcBM : (int)blockIdx.y * kTcBM;
+    const int n0 = PAIR ? (int)blockIdx.y * kTcBN : (int)blockIdx.x * kTcBN;
     // split-K: this CTA accumulates K blocks [kb0, kb1)
     const int nkb_all = (args.K + kTcBK - 1) / kTcBK;
     const int kb0 = gridDim.z > 1 ? blockIdx.z * args.kbs : 0;
@@ -177,11 +225,14 @@ __global__ void __launch_bounds__(kTcThreads, 1)
     const uint32_t tmem_full = tc_smem(bars + 3 * kTcStages);
     auto tileA = [&](int s) { return sbase + (uint32_t)(s * kTcStage); };
     auto tileB = [&](int s) { return sbase + (uint32_t)(s * kTcStage + kTcTile); };
-    auto tileBlo = [&](int s) { return sbase + (uint32_t)(s * kTcStage + 2 * kTcTile); };
+    auto tileBlo = [&](int s) { return sbase + (uint32_t)(s * kTcStage + kTcTile + kBTile); };
 
     if (threadIdx.x == 0) {
         for (int s = 0; s < kTcStages; ++s) {
             tc_mbar_init(full(s), 1);
+            // PAIR: rank 1's "split done" reaches rank 0's conv(s) as the
+            // complete_tx of a 16-byte DSMEM bulk copy (one of rank 0's split
+            // warps arms the matching expect_tx) -- no cluster-scope fence
             tc_mbar_init(conv(s), kTcSplitWarps);
             tc_mbar_init(empty(s), 1);
         }
@@ -191,12 +242,23 @@ __global__ void __launch_bounds__(kTcThreads, 1)
         asm volatile("prefetch.tensormap [%0];\n" ::"l"(reinterpret_cast<uint64_t>(&tmB)) : "memory");
     }
     if (warp == 1) {
-        asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;\n" ::"r"(tc_smem(tmem_slot)),
-                     "r"(kTcTmemCols));
-        asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;\n");
+        if constexpr (PAIR) {
+            asm volatile("tcgen05.alloc.cta_group::2.sync.aligned.shared::cta.b32 [%0], %1;\n" ::"r"(
+                             tc_smem(tmem_slot)),
+                         "r"(kTcTmemCols));
+            asm volatile("tcgen05.relinquish_alloc_permit.cta_group::2.sync.aligned;\n");
+        } else {
+            asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;\n" ::"r"(
+                             tc_smem(tmem_slot)),
+                         "r"(kTcTmemCols));
+            asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;\n");
+        }
     }
     asm volatile("tcgen05.fence::before_thread_sync;\n" ::: "memory");
-    __syncthreads();
+    if constexpr (PAIR)
+        tc_cluster_sync();  // both CTAs' barriers initialised before any remote arrive / multicast commit
+    else
+        __syncthreads();
     asm volatile("tcgen05.fence::after_thread_sync;\n" ::: "memory");
     const uint32_t tmem = *tmem_slot;
 
@@ -207,29 +269,32 @@ __global__ void __launch_bounds__(kTcThreads, 1)
                 const int s = kb % kTcStages;
                 const uint32_t ph = (uint32_t)((kb / kTcStages) & 1);
                 tc_mbar_wait(empty(s), ph ^ 1);
-                tc_mbar_expect_tx(full(s), 2 * kTcTile);
+                tc_mbar_expect_tx(full(s), kTcTile + kBTile);
                 const int k0 = (kb0 + kb) * kTcBK;
                 if constexpr (!A_MN)
                     tc_tma_2d(&tmA, full(s), tileA(s), k0, m0);
                 else
                     tc_tma_2d(&tmA, full(s), tileA(s), m0, k0);  // unswizzled [k][128 m]
+                const int nb = n0 + (int)rank * Cfg::kBLocal;  // this CTA's B columns
                 if constexpr (!B_MN) {
-                    tc_tma_2d(&tmB, full(s), tileB(s), k0, n0);
+                    tc_tma_2d(&tmB, full(s), tileB(s), k0, nb);
                 } else {
 #pragma unroll
-                    for (int g = 0; g < 4; ++g) tc_tma_2d(&tmB, full(s), tileB(s) + g * 4096, n0 + 32 * g, k0);
+                    for (int g = 0; g < Cfg::kBLocal / 32; ++g)
+                        tc_tma_2d(&tmB, full(s), tileB(s) + g * 4096, nb + 32 * g, k0);
                 }
             }
         }
-    } else if (warp == 1) {
+    } else if (warp == 1 && rank == 0) {
         // ---------------- MMA issuer ----------------
         // instruction descriptor: D f32, A/B tf32, A K-major (TMEM), B major, N>>3, M>>4
+        constexpr uint32_t kM = PAIR ? 2 * kTcBM : kTcBM;
         const uint32_t idesc = (1u << 4) | (2u << 7) | (2u << 10) | ((B_MN ? 1u : 0u) << 16) |
-                               ((uint32_t)(kTcBN >> 3) << 17) | ((uint32_t)(kTcBM >> 4) << 24);
+                               ((uint32_t)(kTcBN >> 3) << 17) | ((kM >> 4) << 24);
         for (int kb = 0; kb < nkb; ++kb) {
             const int s = kb % kTcStages;
             const uint32_t ph = (uint32_t)((kb / kTcStages) & 1);
-            tc_mbar_wait(conv(s), ph);
+            tc_mbar_wait(conv(s), ph);  // PAIR: both CTAs' split passes (rank 1's forwarded)
             asm volatile("tcgen05.fence::after_thread_sync;\n" ::: "memory");
             if (lane == 0) {
 #pragma unroll
@@ -243,15 +308,51 @@ __global__ void __launch_bounds__(kTcThreads, 1)
                     const uint64_t dBl = tc_desc(tileBlo(s) + bo, blbo, bsbo, blay);
                     const uint32_t tA = tmem + (uint32_t)(kTcBN + 64 * s + 8 * ks);  // A; A_lo at +32
                     const uint32_t first = (kb == 0 && ks == 0) ? 0u : 1u;
-                    tc_mma_ts(tmem, tA + 32u, dB, idesc, first);  // small terms first
-                    tc_mma_ts(tmem, tA, dBl, idesc, 1u);
-                    tc_mma_ts(tmem, tA, dB, idesc, 1u);
+                    if constexpr (PAIR) {
+                        tc_mma_ts_pair(tmem, tA + 32u, dB, idesc, first);  // small terms first
+                        tc_mma_ts_pair(tmem, tA, dBl, idesc, 1u);
+                        tc_mma_ts_pair(tmem, tA, dB, idesc, 1u);
+                    } else {
+                        tc_mma_ts(tmem, tA + 32u, dB, idesc, first);  // small terms first
+                        tc_mma_ts(tmem, tA, dBl, idesc, 1u);
+                        tc_mma_ts(tmem, tA, dB, idesc, 1u);
+                    }
                 }
-                tc_commit(empty(s));  // slot free once these MMAs have read it
+                // slot free (in both CTAs) once these MMAs have read it
+                if constexpr (PAIR)
+                    tc_commit_pair(empty(s));
+                else
+                    tc_commit(empty(s));
             }
             __syncwarp();
         }
-        if (lane == 0) tc_commit(tmem_full);
+        if (lane == 0) {
+            if constexpr (PAIR)
+                tc_commit_pair(tmem_full);
+            else
+                tc_commit(tmem_full);
+        }
+        __syncwarp();
+    } else if (warp == 1) {
+        // the pair's second CTA: its MMAs are issued by rank 0.  This warp
+        // forwards "stage s split done" to rank 0 as an async-proxy DSMEM bulk
+        // copy that completes rank 0's conv(s) transaction count.
+        if (lane == 0) {
+            const uint32_t src = tc_smem(reinterpret_cast<uint8_t*>(bars) + 464);
+            uint32_t dst, rbar0;
+            asm volatile("mapa.shared::cluster.u32 %0, %1, %2;\n" : "=r"(dst) : "r"(src - 16), "r"(0));
+            asm volatile("mapa.shared::cluster.u32 %0, %1, %2;\n" : "=r"(rbar0) : "r"(conv(0)), "r"(0));
+            for (int kb = 0; kb < nkb; ++kb) {
+                const int s = kb % kTcStages;
+                const uint32_t ph = (uint32_t)((kb / kTcStages) & 1);
+                tc_mbar_wait(conv(s), ph);
+                asm volatile(
+                    "cp.async.bulk.shared::cluster.shared::cta.mbarrier::complete_tx::bytes [%0], [%1], 16, [%2];\n" ::"r"(
+                        dst),
+                    "r"(src), "r"(rbar0 + 8u * (uint32_t)s)
+                    : "memory");
+            }
+        }
         __syncwarp();
     } else {
         // ---------------- split pass, then epilogue (warps 2..9) ----------------
@@ -265,7 +366,7 @@ __global__ void __launch_bounds__(kTcThreads, 1)
             tc_mbar_wait(full(s), ph);
             const uint8_t* a = smem + (size_t)s * kTcStage;
             const float4* b = reinterpret_cast<const float4*>(smem + (size_t)s * kTcStage + kTcTile);
-            float4* bl = reinterpret_cast<float4*>(smem + (size_t)s * kTcStage + 2 * kTcTile);
+            float4* bl = reinterpret_cast<float4*>(smem + (size_t)s * kTcStage + kTcTile + kBTile);
             // A row rowA, K columns [16 khalf, +16) -> TMEM (A and A_lo)
             uint32_t hi[16], lo[16];
             if constexpr (!A_MN) {
@@ -292,7 +393,7 @@ __global__ void __launch_bounds__(kTcThreads, 1)
             tc_st16(tA + 32u, lo);
             // B_lo -> smem (same swizzled layout as B)
 #pragma unroll
-            for (int u = 0; u < kTcTile / 16 / (32 * kTcSplitWarps); ++u) {
+            for (int u = 0; u < kBTile / 16 / (32 * kTcSplitWarps); ++u) {
                 const int q = ct + 32 * kTcSplitWarps * u;
                 const float4 vb = b[q];
                 bl[q] = make_float4(tf32_lo(vb.x), tf32_lo(vb.y), tf32_lo(vb.z), tf32_lo(vb.w));
@@ -303,7 +404,12 @@ __global__ void __launch_bounds__(kTcThreads, 1)
             asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");
             asm volatile("tcgen05.fence::before_thread_sync;\n" ::: "memory");
             __syncwarp();
-            if (lane == 0) tc_mbar_arrive(conv(s));
+            if (lane == 0) {
+                if (PAIR && rank == 0 && warp == 2)
+                    tc_mbar_expect_tx(conv(s), 16);  // rank 1's forward (16-byte bulk copy)
+                else
+                    tc_mbar_arrive(conv(s));
+            }
         }
         tc_mbar_wait(tmem_full, 0);
         asm volatile("tcgen05.fence::after_thread_sync;\n" ::: "memory");
@@ -360,10 +466,16 @@ __global__ void __launch_bounds__(kTcThreads, 1)
         }
     }
     asm volatile("tcgen05.fence::before_thread_sync;\n" ::: "memory");
-    __syncthreads();
+    if constexpr (PAIR)
+        tc_cluster_sync();
+    else
+        __syncthreads();
     if (warp == 1) {
         asm volatile("tcgen05.fence::after_thread_sync;\n" ::: "memory");
-        asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;\n" ::"r"(tmem), "r"(kTcTmemCols));
+        if constexpr (PAIR)
+            asm volatile("tcgen05.dealloc.cta_group::2.sync.aligned.b32 %0, %1;\n" ::"r"(tmem), "r"(kTcTmemCols));
+        else
+            asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;\n" ::"r"(tmem), "r"(kTcTmemCols));
     }
 }
 
@@ -436,30 +548,48 @@ inline bool tc_eligible(int M, int N, int K) {
     return (M % 4 == 0) && (N % 4 == 0) && (K % 4 == 0) && N >= 64 && M >= 64 && K >= 32;
 }
 
-template <bool A_MN, bool B_MN, TcEpi E>
+template <bool A_MN, bool B_MN, TcEpi E, bool PAIR>
 inline void tc_launch(cudaStream_t st, const CUtensorMap& a, const CUtensorMap& b, const TcArgs& args) {
+    constexpr size_t smem = TcCfg<PAIR>::kSmem;
     static bool configured = false;
     if (!configured) {
-        LANE_CUDA(cudaFuncSetAttribute(k_gemm_tc<A_MN, B_MN, E>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                       (int)kTcSmem));
+        LANE_CUDA(cudaFuncSetAttribute(k_gemm_tc<A_MN, B_MN, E, PAIR>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                       (int)smem));
         configured = true;
     }
     const int S = args.kbs > 0 ? (args.K / kTcBK + args.kbs - 1) / args.kbs : 1;
-    const dim3 grid((args.N + kTcBN - 1) / kTcBN, (args.M + kTcBM - 1) / kTcBM, S);
-    k_gemm_tc<A_MN, B_MN, E><<<grid, kTcThreads, kTcSmem, st>>>(a, b, args);
+    if constexpr (PAIR) {
+        // clusters of 2 along x (M): CTA 2p and 2p+1 share the 256 x 128 tile p
+        cudaLaunchConfig_t cfg = {};
+        cfg.gridDim = dim3(2 * ((args.M + 2 * kTcBM - 1) / (2 * kTcBM)), (args.N + kTcBN - 1) / kTcBN, S);
+        cfg.blockDim = dim3(kTcThreads);
+        cfg.dynamicSmemBytes = smem;
+        cfg.stream = st;
+        cudaLaunchAttribute attr[1];
+        attr[0].id = cudaLaunchAttributeClusterDimension;
+        attr[0].val.clusterDim.x = 2;
+        attr[0].val.clusterDim.y = 1;
+        attr[0].val.clusterDim.z = 1;
+        cfg.attrs = attr;
+        cfg.numAttrs = 1;
+        LANE_CUDA(cudaLaunchKernelEx(&cfg, k_gemm_tc<A_MN, B_MN, E, PAIR>, a, b, args));
+    } else {
+        const dim3 grid((args.N + kTcBN - 1) / kTcBN, (args.M + kTcBM - 1) / kTcBM, S);
+        k_gemm_tc<A_MN, B_MN, E, PAIR><<<grid, kTcThreads, smem, st>>>(a, b, args);
+    }
     if (S > 1) {
         const size_t n4 = (size_t)args.M * args.N / 4;
         k_tc_splitk_reduce<E><<<(unsigned)std::min<size_t>(1184, (n4 + 255) / 256), 256, 0, st>>>(args, S);
     }
 }
 
-template <TcEpi E>
+template <TcEpi E, bool PAIR>
 inline void tc_dispatch(cudaStream_t st, bool a_mn, bool b_mn, const CUtensorMap& a, const CUtensorMap& b,
                         const TcArgs& args) {
-    if (!a_mn && !b_mn) tc_launch<false, false, E>(st, a, b, args);
-    else if (!a_mn && b_mn) tc_launch<false, true, E>(st, a, b, args);
-    else if (a_mn && !b_mn) tc_launch<true, false, E>(st, a, b, args);
-    else tc_launch<true, true, E>(st, a, b, args);
+    if (!a_mn && !b_mn) tc_launch<false, false, E, PAIR>(st, a, b, args);
+    else if (!a_mn && b_mn) tc_launch<false, true, E, PAIR>(st, a, b, args);
+    else if (a_mn && !b_mn) tc_launch<true, false, E, PAIR>(st, a, b, args);
+    else tc_launch<true, true, E, PAIR>(st, a, b, args);
 }
 
 }  // namespace lane_b200

@@ -60,7 +60,10 @@ def operands(op, M, N, K, rs):
 @pytest.mark.parametrize("use_tc", [1, 0])
 @pytest.mark.parametrize("op", [NN, NT, TN])
 @pytest.mark.parametrize("M,N,K", [(128, 128, 32), (256, 512, 1024), (192, 320, 96), (64, 4100, 36),
-                                   (1024, 256, 256)])
+                                   (1024, 256, 256),
+                                   # CTA-pair tiles (M >= 512, K >= 2048); 640 leaves the last
+                                   # pair's second CTA entirely past M
+                                   (640, 384, 2048), (512, 128, 4096)])
 def test_gemm_store_condition_aware(dev, op, M, N, K, use_tc):
     rs = np.random.default_rng(M * 7 + N * 3 + K)
     A, B, Am, Bm = operands(op, M, N, K, rs)
@@ -76,8 +79,8 @@ def test_gemm_store_condition_aware(dev, op, M, N, K, use_tc):
 
 
 @pytest.mark.parametrize("op", [NN, NT])
-def test_gemm_fused_epilogues(dev, op):
-    M, N, K = 256, 384, 512
+@pytest.mark.parametrize("M,N,K", [(256, 384, 512), (512, 256, 2048)])  # single CTAs; CTA pairs
+def test_gemm_fused_epilogues(dev, op, M, N, K):
     rs = np.random.default_rng(5)
     A, B, Am, Bm = operands(op, M, N, K, rs)
     A *= 0.1
@@ -100,6 +103,8 @@ def test_tensor_core_kernel_is_used(dev):
     from paper_2001_04206_b200 import _build
     sass = subprocess.run(["cuobjdump", "-sass", _build.LIB], capture_output=True, text=True).stdout
     assert "UTCHMMA" in sass and "UTMALDG" in sass and "LDTM" in sass
+    # A staged through TMEM (STTM) and the CTA-pair variant (2-CTA MMA + multicast commit)
+    assert "STTM" in sass and "UTCHMMA.2CTA" in sass and "UTCBAR.2CTA.MULTICAST" in sass
 
 
 @pytest.mark.parametrize("epi", [STORE, TANH_GRAD])
