@@ -55,6 +55,16 @@ MINIBATCH = {
 }
 
 
+def load_traffic(wl):
+    """DRAM bytes per launch of the workload's dominant kernel from the
+    committed ncu capture (profiles/traffic.json, tools/ncu_traffic.py)."""
+    path = os.path.join(ROOT, "profiles", "traffic.json")
+    if not os.path.exists(path):
+        return None, None
+    d = json.load(open(path)).get(wl)
+    return (d["traffic_bytes_per_launch"], d["source"]) if d else (None, None)
+
+
 def load_peaks():
     p = os.path.join(ROOT, "MEASURED_PEAKS.json")
     if os.path.exists(p):
@@ -271,7 +281,8 @@ def run_minibatch(args, wl):
                        "gemm": "tcgen05 kind::tf32, 3xTF32 (fp32-accurate)",
                        "l2": "256 MB buffer written between timed steps"},
             "roofline": {"bound": "tensor", "achieved": achieved, "peak": peak, "unit": "TFLOP/s",
-                         "frac": achieved / peak, "traffic": None,
+                         "frac": achieved / peak, "traffic": load_traffic(wl)[0],
+                         "traffic_source": load_traffic(wl)[1],
                          "peak_kind": "derived: measured bf16 dense / 2 (tf32) / 3 (3xTF32 MMAs)",
                          "algorithmic_flops_per_step": flops},
             "e2e": {"value": e2e, "unit": "samples/s", "h2d_bytes_per_step": rows * (F + C) * 4,
@@ -446,7 +457,9 @@ def main():
                        "l2": f"inputs {X.nbytes + T.nbytes} B > 126 MB L2, streamed each step"
                        if X.nbytes + T.nbytes > 126e6 else "inputs fit in L2"},
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
-                         "frac": achieved / peak, "traffic": None, "peak_kind": peak_kind,
+                         "frac": achieved / peak, "traffic": load_traffic(wl)[0] if wl == "c2" else None,
+                         "traffic_source": load_traffic(wl)[1] if wl == "c2" else None,
+                         "peak_kind": peak_kind,
                          "kernel": {"window": "k_sgd_window", "cluster": "k_sgd_cluster",
                                     "grid": "k_sgd_grid"}.get(plan.split()[0], "layer kernels"),
                          "plan": plan,
