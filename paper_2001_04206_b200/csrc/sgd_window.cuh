@@ -1100,22 +1100,12 @@ __device__ __forceinline__ void win_chain(const WinArgs& A, float* sm, const Win
             }
             __syncwarp();
             WIN_TRACE(s, 2);
-            // -- softmax: every lane reads the C logits (exact max); lane k
-            //    computes exp(z_k - max) once and shares it through shared memory
+            // -- softmax: the exact max over the C logits in one warp reduction
+            //    (redux.sync.max.f32); lane k computes exp(z_k - max) once and
+            //    shares it through shared memory
             constexpr int CV = (CC + 3) / 4;  // float4 loads of a class vector
-            float zk[4 * CV];
-#pragma unroll
-            for (int k4 = 0; k4 < CV; ++k4) {
-                const float4 v = reinterpret_cast<const float4*>(zt)[k4];
-                zk[4 * k4 + 0] = v.x;
-                zk[4 * k4 + 1] = v.y;
-                zk[4 * k4 + 2] = v.z;
-                zk[4 * k4 + 3] = v.w;
-            }
-            float mx = zk[0];
-#pragma unroll
-            for (int k = 1; k < CC; ++k)
-                if (k < C) mx = fmaxf(mx, zk[k]);
+            float mx;
+            asm("redux.sync.max.f32 %0, %1, 0xffffffff;\n" : "=f"(mx) : "f"(kval ? zown : -INFINITY));
             const float eown = expf(zown - mx);
             if (kval) es[lane] = eown;
             __syncwarp();
@@ -1143,14 +1133,17 @@ __device__ __forceinline__ void win_chain(const WinArgs& A, float* sm, const Win
             float d1[CC];
 #pragma unroll
             for (int k = 0; k < CC; ++k) d1[k] = k < C ? fmaf(ek[k], inv, -t[k]) : 0.0f;  // p - t
-            // d0 = (1 - a^2) * (W1 d1) with the pre-update W1
+            // d0 = (1 - a^2) * (W1 d1) with the pre-update W1 (two half-chains:
+            // the dependent FMA latency is on the critical path)
             float d0v[JPL];
 #pragma unroll
             for (int m = 0; m < JPL; ++m) {
-                float acc = 0.0f;
+                float acc0 = 0.0f, acc1 = 0.0f;
 #pragma unroll
-                for (int k = 0; k < CC; ++k) acc = fmaf(d1[k], w1[m][k], acc);
-                d0v[m] = fmaf(-a[m], a[m], 1.0f) * acc;  // (1 - a^2) W1 d1
+                for (int k = 0; k < CC / 2; ++k) acc0 = fmaf(d1[k], w1[m][k], acc0);
+#pragma unroll
+                for (int k = CC / 2; k < CC; ++k) acc1 = fmaf(d1[k], w1[m][k], acc1);
+                d0v[m] = fmaf(-a[m], a[m], 1.0f) * (acc0 + acc1);  // (1 - a^2) W1 d1
             }
             WIN_TRACE(s, 3);
             if constexpr (DIR) {
