@@ -83,6 +83,25 @@ int blocks_for(size_t n, int threads, int cap) {
     return static_cast<int>(std::max<size_t>(1, std::min<size_t>(cap, (n + threads - 1) / threads)));
 }
 
+// G = d (x) x, DW = -eta G (the softmax/fc backward tuples' outer product)
+void launch_outer(cudaStream_t st, int sm_count, const float* d, const float* x, float* G, float* DW,
+                  float neg_eta, int I, int O) {
+    const bool vec = (O & 3) == 0 && ((reinterpret_cast<uintptr_t>(d) | reinterpret_cast<uintptr_t>(G) |
+                                       reinterpret_cast<uintptr_t>(DW)) & 15) == 0;
+    if (vec) {
+        const int Q = O / 4;
+        const unsigned gx = static_cast<unsigned>((Q + 255) / 256);
+        const unsigned gy = static_cast<unsigned>(std::min<long long>(
+            I, std::max<long long>(1, (long long)16 * sm_count / std::max(1u, gx))));
+        k_outer4<<<dim3(gx, std::max(1u, gy)), 256, 0, st>>>(
+            reinterpret_cast<const float4*>(d), x, reinterpret_cast<float4*>(G), reinterpret_cast<float4*>(DW),
+            neg_eta, I, Q);
+    } else {
+        k_outer<<<blocks_for(static_cast<size_t>(I) * O, 256, 8 * sm_count), 256, 0, st>>>(d, x, G, DW, neg_eta,
+                                                                                           I, O);
+    }
+}
+
 }  // namespace
 
 #include "dataset.cuh"
@@ -264,9 +283,8 @@ void run_fc_backward(lane_b200_net* net, size_t l, const float* nW, const float*
             Ly.buf[LANE_BUF_OUTPUTS], nW, nd, Ly.buf[LANE_BUF_DELTAS], Ly.buf[LANE_BUF_DELTA_BIASES],
             neg_eta, O, N);
     }
-    k_outer<<<blocks_for(static_cast<size_t>(I) * O, 256, 8 * c->sm_count), 256, 0, c->stream>>>(
-        Ly.buf[LANE_BUF_DELTAS], Ly.buf[LANE_BUF_INPUTS], Ly.buf[LANE_BUF_G], Ly.buf[LANE_BUF_DW],
-        neg_eta, I, O);
+    launch_outer(c->stream, c->sm_count, Ly.buf[LANE_BUF_DELTAS], Ly.buf[LANE_BUF_INPUTS], Ly.buf[LANE_BUF_G],
+                 Ly.buf[LANE_BUF_DW], neg_eta, I, O);
     c->count(2);
     c->check_launch();
 }
@@ -277,9 +295,8 @@ void run_softmax_backward(lane_b200_net* net, const float* t_dev, float eta) {
     const int I = static_cast<int>(Ly.I), O = static_cast<int>(Ly.O);
     k_delta_softmax<<<blocks_for(O, 128, 1 << 20), 128, 0, c->stream>>>(
         Ly.buf[LANE_BUF_OUTPUTS], t_dev, Ly.buf[LANE_BUF_DELTAS], Ly.buf[LANE_BUF_DELTA_BIASES], -eta, O);
-    k_outer<<<blocks_for(static_cast<size_t>(I) * O, 256, 8 * c->sm_count), 256, 0, c->stream>>>(
-        Ly.buf[LANE_BUF_DELTAS], Ly.buf[LANE_BUF_INPUTS], Ly.buf[LANE_BUF_G], Ly.buf[LANE_BUF_DW], -eta,
-        I, O);
+    launch_outer(c->stream, c->sm_count, Ly.buf[LANE_BUF_DELTAS], Ly.buf[LANE_BUF_INPUTS], Ly.buf[LANE_BUF_G],
+                 Ly.buf[LANE_BUF_DW], -eta, I, O);
     c->count(2);
     c->check_launch();
 }
@@ -631,9 +648,8 @@ void launch_persistent(lane_b200_net* net, const SgdPlan& P, const float* X, con
     // G and DW of the last sample, as the reference's stream_out leaves them
     for (size_t l = 0; l < 2; ++l) {
         LayerBufs& Ly = net->L(l);
-        k_outer<<<blocks_for(Ly.I * Ly.O, 256, 8 * c->sm_count), 256, 0, c->stream>>>(
-            Ly.buf[LANE_BUF_DELTAS], Ly.buf[LANE_BUF_INPUTS], Ly.buf[LANE_BUF_G], Ly.buf[LANE_BUF_DW],
-            -eta, static_cast<int>(Ly.I), static_cast<int>(Ly.O));
+        launch_outer(c->stream, c->sm_count, Ly.buf[LANE_BUF_DELTAS], Ly.buf[LANE_BUF_INPUTS],
+                     Ly.buf[LANE_BUF_G], Ly.buf[LANE_BUF_DW], -eta, static_cast<int>(Ly.I), static_cast<int>(Ly.O));
         c->count();
     }
     c->check_launch();
@@ -786,9 +802,8 @@ void materialise_last_grads(lane_b200_net* net, float eta) {
     lane_b200_ctx* c = net->ctx;
     for (size_t l = 0; l < 2; ++l) {
         LayerBufs& Ly = net->L(l);
-        k_outer<<<blocks_for(Ly.I * Ly.O, 256, 8 * c->sm_count), 256, 0, c->stream>>>(
-            Ly.buf[LANE_BUF_DELTAS], Ly.buf[LANE_BUF_INPUTS], Ly.buf[LANE_BUF_G], Ly.buf[LANE_BUF_DW],
-            -eta, static_cast<int>(Ly.I), static_cast<int>(Ly.O));
+        launch_outer(c->stream, c->sm_count, Ly.buf[LANE_BUF_DELTAS], Ly.buf[LANE_BUF_INPUTS],
+                     Ly.buf[LANE_BUF_G], Ly.buf[LANE_BUF_DW], -eta, static_cast<int>(Ly.I), static_cast<int>(Ly.O));
         c->count();
     }
     c->check_launch();

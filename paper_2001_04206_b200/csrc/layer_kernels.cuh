@@ -175,12 +175,44 @@ __global__ void k_outer(const float* __restrict__ d, const float* __restrict__ x
                         float* __restrict__ G, float* __restrict__ DW, float neg_eta, int I,
                         int O) {
     const size_t n = (size_t)I * O;
+    if (n <= 0xffffffffull) {  // 32-bit index math (no 64-bit division per element)
+        const unsigned un = (unsigned)n, uO = (unsigned)O;
+        for (unsigned e = blockIdx.x * blockDim.x + threadIdx.x; e < un; e += gridDim.x * blockDim.x) {
+            const unsigned i = e / uO, o = e - i * uO;
+            const float g = smul(d[o], x[i]);
+            G[e] = g;
+            DW[e] = smul(neg_eta, g);
+        }
+        return;
+    }
     for (size_t e = (size_t)blockIdx.x * blockDim.x + threadIdx.x; e < n;
          e += (size_t)gridDim.x * blockDim.x) {
         const int i = (int)(e / O), o = (int)(e - (size_t)i * O);
         const float g = smul(d[o], x[i]);
         G[e] = g;
         DW[e] = smul(neg_eta, g);
+    }
+}
+
+// Same with O % 4 == 0: threads own a column quad (the delta quad stays in
+// registers) and walk rows with stride gridDim.y; float4 streaming stores.
+// HBM-bound: 8 B written per element.
+__global__ void __launch_bounds__(256) k_outer4(const float4* __restrict__ d, const float* __restrict__ x,
+                                                float4* __restrict__ G, float4* __restrict__ DW, float neg_eta,
+                                                int I, int Q) {
+    const int q = blockIdx.x * blockDim.x + threadIdx.x;
+    if (q >= Q) return;
+    const float4 dq = d[q];
+    for (int i = blockIdx.y; i < I; i += gridDim.y) {
+        const float xi = x[i];
+        float4 g;
+        g.x = smul(dq.x, xi);
+        g.y = smul(dq.y, xi);
+        g.z = smul(dq.z, xi);
+        g.w = smul(dq.w, xi);
+        const size_t e = (size_t)i * Q + q;
+        __stcs(G + e, g);
+        __stcs(DW + e, make_float4(smul(neg_eta, g.x), smul(neg_eta, g.y), smul(neg_eta, g.z), smul(neg_eta, g.w)));
     }
 }
 
