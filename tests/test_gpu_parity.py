@@ -602,3 +602,80 @@ def test_sgd_window_long_stream_chunks(lane, fast, monkeypatch):
         assert_close(layer.weights, orc.get(l, po.W), 2e-3, f"W{l}")
     for p in (Xd, Td, Od, Ld):
         fast.free(p)
+
+
+# ------------------------------------------- finite-difference gradients ---
+
+def _ce_loss64(Ws, bs, X, T):
+    """Mean cross entropy in float64 (proj/tests/acceptance.cpp:62-98, ce_loss_double)."""
+    a = np.asarray(X, np.float64)
+    for W, b in zip(Ws[:-1], bs[:-1]):
+        a = np.tanh(a @ W + b)
+    z = a @ Ws[-1] + bs[-1]
+    z = z - z.max(axis=-1, keepdims=True)
+    logp = z - np.log(np.exp(z).sum(axis=-1, keepdims=True))
+    return float(-(np.asarray(T, np.float64) * logp).sum(axis=-1).mean())
+
+
+def _fd_check(Ws, bs, X, T, l, G, gb):
+    """acceptance.cpp:100-140: central differences, h = 1e-3 max(1, |w|), rel 1e-3."""
+    worst = 0.0
+    for P, A in ((Ws[l], G), (bs[l], gb)):
+        for idx in np.ndindex(P.shape):
+            saved = P[idx]
+            h = 1e-3 * max(1.0, abs(saved))
+            P[idx] = saved + h
+            up = _ce_loss64(Ws, bs, X, T)
+            P[idx] = saved - h
+            dn = _ce_loss64(Ws, bs, X, T)
+            P[idx] = saved
+            fd = (up - dn) / (2 * h)
+            rel = abs(A[idx] - fd) / max(1.0, abs(A[idx]), abs(fd))
+            worst = max(worst, rel)
+    assert worst <= 1e-3, worst
+    return worst
+
+
+@pytest.mark.parametrize("mode", ["strict", "fast"])
+def test_layer_gradients_vs_finite_differences(lane, dev, mode):
+    """The reference's gradient-correctness criterion (acceptance.cpp:142-162)
+    on the GPU layer API: 20 networks up to 8-8-4, every weight and bias of
+    both layers, analytic G / delta against float64 central differences."""
+    dev.numerics = lane.NUMERICS_STRICT if mode == "strict" else lane.NUMERICS_FAST
+    try:
+        rs = np.random.default_rng(4242)
+        for trial in range(20):
+            F, H, C_ = 1 + int(rs.integers(8)), 1 + int(rs.integers(8)), 2 + int(rs.integers(3))
+            net = lane.build_network(F, [H], C_, seed=int(rs.integers(1 << 30)), device=dev)
+            x = rs.uniform(-1, 1, F).astype(np.float32)
+            t = np.eye(C_, dtype=np.float32)[int(rs.integers(C_))]
+            net.forward(x)
+            net.output.backward(t, 0.01)
+            net.hidden[0].backward(eta=0.01)
+            Ws = [net.hidden[0].weights.astype(np.float64), net.output.weights.astype(np.float64)]
+            bs = [net.hidden[0].biases.astype(np.float64), net.output.biases.astype(np.float64)]
+            for l, layer in enumerate([net.hidden[0], net.output]):
+                _fd_check(Ws, bs, x[None], t[None], l, layer.gradients.astype(np.float64),
+                          layer.deltas.astype(np.float64))
+    finally:
+        dev.numerics = lane.NUMERICS_FAST
+
+
+def test_minibatch_gradients_vs_finite_differences(lane, fast):
+    """Mini-batch extension ("FD of the mean loss"): the mean
+    gradient the step applies, read back as G / BIAS_GRAD, against float64
+    central differences of the batch-mean cross entropy at the pre-update
+    weights."""
+    F, H, C_, B = 6, [7, 5], 3, 9
+    X, T = po.synthetic_dataset(F, C_, B, 3)
+    net = lane.build_network(F, H, C_, seed=11, device=fast, max_batch=B)
+    Ws = [L.weights.astype(np.float64) for L in net.layers]
+    bs = [L.biases.astype(np.float64) for L in net.layers]
+    Xd, Td = upload(fast, X), upload(fast, T)
+    net.minibatch_step(Xd, Td, B, 0.05, 0.0)
+    for l, L in enumerate(net.layers):
+        G = L.gradients.astype(np.float64)
+        gb = L.read(lane.BIAS_GRAD).astype(np.float64)
+        _fd_check(Ws, bs, X, T, l, G, gb)
+    fast.free(Xd)
+    fast.free(Td)
