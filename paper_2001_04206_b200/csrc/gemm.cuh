@@ -226,28 +226,51 @@ __global__ void __launch_bounds__(32 * kSkNW) k_gemm_skinny_nn(int M, int N, int
 // (coalesced A rows), N accumulators per thread; the 4 partials meet in
 // shared memory (fixed order) and the per-chunk partial sums part[y][m][n]
 // are reduced in a fixed order by k_sum_partials.
+// dst[0..n) = src[0..n) with every load of the loop in flight together
+// (float4 when src is 16-byte aligned; the serial load->store loop it replaces
+// cost one L2 round trip per iteration)
+__device__ __forceinline__ void stage_rows(float* dst, const float* __restrict__ src, int n) {
+    if ((reinterpret_cast<uintptr_t>(src) & 15) == 0) {
+        const int n4 = n >> 2;
+        const float4* s4 = reinterpret_cast<const float4*>(src);
+        float4* d4 = reinterpret_cast<float4*>(dst);
+#pragma unroll 4
+        for (int e = threadIdx.x; e < n4; e += blockDim.x) d4[e] = __ldg(s4 + e);
+        for (int e = 4 * n4 + threadIdx.x; e < n; e += blockDim.x) dst[e] = __ldg(src + e);
+    } else {
+#pragma unroll 4
+        for (int e = threadIdx.x; e < n; e += blockDim.x) dst[e] = __ldg(src + e);
+    }
+}
+
 constexpr int kSkinnyKChunk = 128;
 constexpr int kSkTnW = 4;
 __global__ void __launch_bounds__(32 * kSkTnW) k_gemm_skinny_tn(int M, int N, int K, const float* __restrict__ A,
-                                                               const float* __restrict__ B, float* __restrict__ part) {
-    __shared__ float bs[kSkinnyKChunk * 32];
+                                                               const float* __restrict__ B, float* __restrict__ part,
+                                                               int cpb) {
+    // this CTA: K chunks [blockIdx.y * cpb, +cpb) (cpb = chunks per block)
+    __shared__ __align__(16) float bs[kSkinnyKChunk * 32];
     __shared__ float red[kSkTnW][32][33];
-    const int k0 = blockIdx.y * kSkinnyKChunk, k1 = min(K, k0 + kSkinnyKChunk);
-    for (int e = threadIdx.x; e < (k1 - k0) * N; e += blockDim.x) bs[e] = B[(size_t)k0 * N + e];
-    __syncthreads();
     const int tx = threadIdx.x & 31, ty = threadIdx.x >> 5;
     const int m = blockIdx.x * 32 + tx;
     float acc[32];
 #pragma unroll
     for (int n = 0; n < 32; ++n) acc[n] = 0.0f;
-    if (m < M) {
+    for (int c = 0; c < cpb; ++c) {
+        const int k0 = (blockIdx.y * cpb + c) * kSkinnyKChunk, k1 = min(K, k0 + kSkinnyKChunk);
+        if (k0 >= K) break;
+        if (c) __syncthreads();
+        stage_rows(bs, B + (size_t)k0 * N, (k1 - k0) * N);
+        __syncthreads();
+        if (m < M) {
 #pragma unroll 4
-        for (int k = k0 + ty; k < k1; k += kSkTnW) {
-            const float a = __ldg(A + (size_t)k * M + m);
-            const float* brow = bs + (k - k0) * N;
+            for (int k = k0 + ty; k < k1; k += kSkTnW) {
+                const float a = __ldg(A + (size_t)k * M + m);
+                const float* brow = bs + (k - k0) * N;
 #pragma unroll
-            for (int n = 0; n < 32; ++n)
-                if (n < N) acc[n] = fmaf(a, brow[n], acc[n]);
+                for (int n = 0; n < 32; ++n)
+                    if (n < N) acc[n] = fmaf(a, brow[n], acc[n]);
+            }
         }
     }
 #pragma unroll
@@ -292,7 +315,38 @@ __global__ void k_colsum_part(const float* __restrict__ D, int B, int O, float* 
     part[(size_t)blockIdx.y * O + o] = (v[0] + v[1]) + (v[2] + v[3]);
 }
 
+// One pass: CTA = 32 columns x 8 row groups (warp w sums rows b = w mod 8,
+// four chains), the 8 group sums meet in shared memory in a fixed order.
+__global__ void __launch_bounds__(256) k_colsum(const float* __restrict__ D, int B, int O, float* __restrict__ gb) {
+    __shared__ float red[8][33];
+    const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+    const int o = blockIdx.x * 32 + lane;
+    float v[4] = {0.0f, 0.0f, 0.0f, 0.0f};
+    if (o < O) {
+        int b = w;
+        for (; b + 24 < B; b += 32) {
+#pragma unroll
+            for (int u = 0; u < 4; ++u) v[u] += __ldg(D + (size_t)(b + 8 * u) * O + o);
+        }
+        for (; b < B; b += 8) v[0] += __ldg(D + (size_t)b * O + o);
+    }
+    red[w][lane] = (v[0] + v[1]) + (v[2] + v[3]);
+    __syncthreads();
+    if (w == 0 && o < O) {
+        float t = red[0][lane];
+#pragma unroll
+        for (int q = 1; q < 8; ++q) t += red[q][lane];
+        gb[o] = t;
+    }
+}
+
 inline void colsum(GemmCtx& g, const float* D, int B, int O, float* gb) {
+    if (B <= 1024 && ((O + 31) / 32 >= g.sm_count / 2 || B <= 256)) {
+        k_colsum<<<(O + 31) / 32, 256, 0, g.stream>>>(D, B, O, gb);
+        *g.launches += 1;
+        return;
+    }
+    // narrow and tall: row chunks first so every SM streams, then a fixed-order sum
     const int S = (B + kColChunk - 1) / kColChunk;
     ensure_ws(g, (size_t)S * O);
     k_colsum_part<<<dim3((O + 127) / 128, S), 128, 0, g.stream>>>(D, B, O, *g.ws);
@@ -308,9 +362,9 @@ inline void colsum(GemmCtx& g, const float* D, int B, int O, float* gb) {
 constexpr int kSkKC = 512;
 __global__ void __launch_bounds__(256) k_gemm_skinny_nn_kc(int M, int N, int K, const float* __restrict__ A,
                                                            const float* __restrict__ B, float* __restrict__ part) {
-    __shared__ float bs[kSkKC * 16];
+    __shared__ __align__(16) float bs[kSkKC * 16];
     const int k0 = blockIdx.y * kSkKC, k1 = min(K, k0 + kSkKC);
-    for (int e = threadIdx.x; e < (k1 - k0) * N; e += blockDim.x) bs[e] = B[(size_t)k0 * N + e];
+    stage_rows(bs, B + (size_t)k0 * N, (k1 - k0) * N);
     __syncthreads();
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const int m = blockIdx.x * 8 + warp;
@@ -424,10 +478,18 @@ inline bool gemm_try_skinny(GemmCtx& g, GemmOp op, int M, int N, int K, const fl
         *g.launches += 1;
         return true;
     }
+    if (op == GemmOp::TN && lda == M && ldb == N && e == Epi::STORE && (M + 31) / 32 >= g.sm_count / 2 &&
+        K <= 4 * kSkinnyKChunk) {
+        // enough row blocks to fill the GPU: one pass over K, no partials
+        const int S = (K + kSkinnyKChunk - 1) / kSkinnyKChunk;
+        k_gemm_skinny_tn<<<dim3((M + 31) / 32, 1), 32 * kSkTnW, 0, g.stream>>>(M, N, K, A, B, C, S);
+        *g.launches += 1;
+        return true;
+    }
     if (op == GemmOp::TN && lda == M && ldb == N && e == Epi::STORE) {
         const int S = (K + kSkinnyKChunk - 1) / kSkinnyKChunk;
         ensure_ws(g, (size_t)S * M * N);
-        k_gemm_skinny_tn<<<dim3((M + 31) / 32, S), 32 * kSkTnW, 0, g.stream>>>(M, N, K, A, B, *g.ws);
+        k_gemm_skinny_tn<<<dim3((M + 31) / 32, S), 32 * kSkTnW, 0, g.stream>>>(M, N, K, A, B, *g.ws, 1);
         k_sum_partials<<<std::max(1, std::min(4 * g.sm_count, (M * N + 255) / 256)), 256, 0, g.stream>>>(
             *g.ws, S, (size_t)M * N, C);
         *g.launches += 2;

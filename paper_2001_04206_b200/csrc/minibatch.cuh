@@ -121,11 +121,15 @@ __global__ void k_softmax_rows(const float* __restrict__ Z, float* __restrict__ 
     if (lane == 0 && row_loss) row_loss[warp] = -loss;
 }
 
+// loss_sum += sum_b row_loss[b] in double: lane l sums rows l, l+32, ... in
+// order, then a fixed butterfly (deterministic, one warp)
 __global__ void k_loss_rows(const float* __restrict__ row_loss, int B, double* loss_sum) {
-    if (threadIdx.x != 0 || blockIdx.x != 0 || !loss_sum) return;
-    double s = *loss_sum;
-    for (int b = 0; b < B; ++b) s += (double)row_loss[b];
-    *loss_sum = s;
+    if (blockIdx.x != 0 || threadIdx.x >= 32 || !loss_sum) return;
+    double s = 0.0;
+    for (int b = threadIdx.x; b < B; b += 32) s += (double)row_loss[b];
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
+    if (threadIdx.x == 0) *loss_sum += s;
 }
 
 // Momentum SGD on a flat range: g = gsum * invB; DW = mu*DW + (-eta)*g;
