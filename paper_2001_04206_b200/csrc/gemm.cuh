@@ -532,7 +532,7 @@ inline bool gemm_try_tc(GemmCtx& g, GemmOp op, int M, int N, int K, const float*
         case GemmOp::NT:  // A [M][K] K-major, B [N][K] K-major
             if (lda != K || ldb != K) return false;
             ma = tc_map(A, M, K, 32, 128, 0);
-            mb = tc_map(B, N, K, 32, pair ? kTcBN / 2 : kTcBN, 0);
+            mb = tc_map(B, N, K, 32, TcCfg<false>::kBN, 0);  // 128 rows: a pair CTA's half of a 256 tile
             break;
         case GemmOp::TN:  // A [K][M] MN-major, B [K][N] MN-major
             if (lda != M || ldb != N) return false;

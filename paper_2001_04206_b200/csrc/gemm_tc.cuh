@@ -44,10 +44,11 @@ constexpr int kTcTmemCols = 512;            // accumulator (128) + stages x (A, 
 // so each SM reads half the B bytes per MMA and the ring fits 6 stages.
 template <bool PAIR>
 struct TcCfg {
-    static constexpr int kBLocal = PAIR ? kTcBN / 2 : kTcBN;  // B columns this CTA holds
+    static constexpr int kBN = PAIR ? 2 * kTcBN : kTcBN;   // tile N (pairs: 256 x 256 tiles)
+    static constexpr int kBLocal = PAIR ? kBN / 2 : kBN;   // B columns this CTA holds
     static constexpr int kBTile = kBLocal * kTcBK * 4;
     static constexpr int kStage = kTcTile + 2 * kBTile;  // A, B, B_lo
-    static constexpr int kStages = PAIR ? 6 : 4;         // TMEM: 128 + 64 x stages <= 512
+    static constexpr int kStages = 4;                    // TMEM: kBN + 64 x stages <= 512
     static constexpr size_t kSmem = (size_t)kStages * kStage + 1024 /*align*/ + 512 /*barriers*/;
 };
 constexpr int kTcSplitWarps = 8;  // the split pass is the busiest role (3xTF32)
@@ -211,7 +212,7 @@ __global__ void __launch_bounds__(kTcThreads, 1)
     // PAIR: cluster (2,1,1) along x = M; rank 0 issues the pair's MMAs
     const uint32_t rank = PAIR ? (blockIdx.x & 1u) : 0u;
     const int m0 = PAIR ? (int)(blockIdx.x >> 1) * 2 * kTcBM + (int)rank * kTcBM : (int)blockIdx.y * kTcBM;
-    const int n0 = PAIR ? (int)blockIdx.y * kTcBN : (int)blockIdx.x * kTcBN;
+    const int n0 = PAIR ? (int)blockIdx.y * Cfg::kBN : (int)blockIdx.x * kTcBN;
     // split-K: this CTA accumulates K blocks [kb0, kb1)
     const int nkb_all = (args.K + kTcBK - 1) / kTcBK;
     const int kb0 = gridDim.z > 1 ? blockIdx.z * args.kbs : 0;
@@ -290,7 +291,7 @@ __global__ void __launch_bounds__(kTcThreads, 1)
         // instruction descriptor: D f32, A/B tf32, A K-major (TMEM), B major, N>>3, M>>4
         constexpr uint32_t kM = PAIR ? 2 * kTcBM : kTcBM;
         const uint32_t idesc = (1u << 4) | (2u << 7) | (2u << 10) | ((B_MN ? 1u : 0u) << 16) |
-                               ((uint32_t)(kTcBN >> 3) << 17) | ((kM >> 4) << 24);
+                               ((uint32_t)(Cfg::kBN >> 3) << 17) | ((kM >> 4) << 24);
         for (int kb = 0; kb < nkb; ++kb) {
             const int s = kb % kTcStages;
             const uint32_t ph = (uint32_t)((kb / kTcStages) & 1);
@@ -306,7 +307,7 @@ __global__ void __launch_bounds__(kTcThreads, 1)
                     const uint32_t blbo = B_MN ? 4096u : 16u, bsbo = B_MN ? 512u : 1024u, blay = B_MN ? 1u : 2u;
                     const uint64_t dB = tc_desc(tileB(s) + bo, blbo, bsbo, blay);
                     const uint64_t dBl = tc_desc(tileBlo(s) + bo, blbo, bsbo, blay);
-                    const uint32_t tA = tmem + (uint32_t)(kTcBN + 64 * s + 8 * ks);  // A; A_lo at +32
+                    const uint32_t tA = tmem + (uint32_t)(Cfg::kBN + 64 * s + 8 * ks);  // A; A_lo at +32
                     const uint32_t first = (kb == 0 && ks == 0) ? 0u : 1u;
                     if constexpr (PAIR) {
                         tc_mma_ts_pair(tmem, tA + 32u, dB, idesc, first);  // small terms first
@@ -388,7 +389,8 @@ __global__ void __launch_bounds__(kTcThreads, 1)
             }
 #pragma unroll
             for (int j = 0; j < 16; ++j) lo[j] = __float_as_uint(tf32_lo(__uint_as_float(hi[j])));
-            const uint32_t tA = tmem + ((uint32_t)(quarter_s * 32) << 16) + (uint32_t)(kTcBN + 64 * s + 16 * khalf);
+            const uint32_t tA =
+                tmem + ((uint32_t)(quarter_s * 32) << 16) + (uint32_t)(Cfg::kBN + 64 * s + 16 * khalf);
             tc_st16(tA, hi);
             tc_st16(tA + 32u, lo);
             // B_lo -> smem (same swizzled layout as B)
@@ -415,10 +417,10 @@ __global__ void __launch_bounds__(kTcThreads, 1)
         asm volatile("tcgen05.fence::after_thread_sync;\n" ::: "memory");
         const int quarter = warp & 3;  // TMEM lanes this warp may access
         const int row = quarter * 32 + lane;
-        const int cbeg = ((warp - 2) >> 2) * (kTcBN / 2);  // this warp's 64 columns
+        const int cbeg = ((warp - 2) >> 2) * (Cfg::kBN / 2);  // this warp's half of the columns
         const int m = m0 + row;
 #pragma unroll 1
-        for (int c0 = cbeg; c0 < cbeg + kTcBN / 2; c0 += 32) {
+        for (int c0 = cbeg; c0 < cbeg + Cfg::kBN / 2; c0 += 32) {
             uint32_t r[32];
             const uint32_t taddr = tmem + ((uint32_t)(quarter * 32) << 16) + (uint32_t)c0;
             asm volatile(
@@ -561,7 +563,8 @@ inline void tc_launch(cudaStream_t st, const CUtensorMap& a, const CUtensorMap& 
     if constexpr (PAIR) {
         // clusters of 2 along x (M): CTA 2p and 2p+1 share the 256 x 128 tile p
         cudaLaunchConfig_t cfg = {};
-        cfg.gridDim = dim3(2 * ((args.M + 2 * kTcBM - 1) / (2 * kTcBM)), (args.N + kTcBN - 1) / kTcBN, S);
+        constexpr int kBN = TcCfg<true>::kBN;
+        cfg.gridDim = dim3(2 * ((args.M + 2 * kTcBM - 1) / (2 * kTcBM)), (args.N + kBN - 1) / kBN, S);
         cfg.blockDim = dim3(kTcThreads);
         cfg.dynamicSmemBytes = smem;
         cfg.stream = st;
