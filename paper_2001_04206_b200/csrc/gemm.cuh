@@ -517,11 +517,13 @@ inline bool gemm_try_tc(GemmCtx& g, GemmOp op, int M, int N, int K, const float*
         return false;
     CUtensorMap ma, mb;
     bool a_mn = false, b_mn = false;
-    // CTA pairs (cta_group::2, 256 x 128 tiles) for the large square GEMMs
-    // (C5: 0.596 -> 0.578 ms at 4096^3); the M = 256 / K = 256 shapes of C3
-    // run faster on single CTAs (short K loops, split-K)
+    // CTA pairs (cta_group::2, 256 x 256 tiles, N = 256 MMAs) for the tall
+    // GEMMs: 4096^3 0.596 -> 0.500 ms; C3's wgrads (M = 1024 / 4096, K = 256)
+    // 70.6 -> 68.7 and 23.1 -> 20.0 us.  The M = 256 GEMMs stay on single CTAs:
+    // a 256-row pair tile leaves 16 tiles for 148 SMs, and the 4-way split-K it
+    // then needs costs more than the bigger MMAs win (61.8 -> 67.2 us).
     static const bool pair_ok = !std::getenv("LANE_B200_TC_NOPAIR");
-    const bool pair = pair_ok && M >= 4 * kTcBM && K >= 2048;
+    const bool pair = pair_ok && (M >= 1024 || (M >= 512 && K >= 2048));
     switch (op) {
         case GemmOp::NN:  // A [M][K] K-major, B [K][N] MN-major
             if (lda != K || ldb != N) return false;
@@ -544,7 +546,10 @@ inline bool gemm_try_tc(GemmCtx& g, GemmOp op, int M, int N, int K, const float*
     TcArgs t{M, N, K, 0, nullptr, C, C2, bias, aux};
     // split-K when the 128x128 tiles fill less than half the SMs (the M = batch
     // GEMMs at B = 256): S splits of >= 8 K blocks each, <= 4, one wave
-    const int tiles = ((M + kTcBM - 1) / kTcBM) * ((N + kTcBN - 1) / kTcBN);
+    // CTAs per split: pairs run 256 x 256 tiles on 2 CTAs
+    constexpr int kPN = TcCfg<true>::kBN;
+    const int tiles = pair ? 2 * ((M + 2 * kTcBM - 1) / (2 * kTcBM)) * ((N + kPN - 1) / kPN)
+                           : ((M + kTcBM - 1) / kTcBM) * ((N + kTcBN - 1) / kTcBN);
     const int nkb = K / kTcBK;
     int S = std::min({4, g.sm_count / std::max(1, tiles), nkb / 8});
     if (K % kTcBK != 0 || (N & 3) != 0) S = 1;
