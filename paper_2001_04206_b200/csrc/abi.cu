@@ -1402,7 +1402,7 @@ int lane_b200_train(lane_b200_net* net, const float* X_host, const float* T_host
         // uploads it, and the fused kernel runs the chunk as a contiguous
         // stream -- the upload of chunk k+1 overlaps the kernel on chunk k.
         // Chunks start small (little exposed copy) and double.
-        constexpr size_t kFirst = 2048, kMax = 16384;
+        constexpr size_t kFirst = 512, kMax = 16384;
         InputPipeline& P = net->pipe;
         P.reserve(std::min(n, kMax) * (I + C), 1);
         SplitMix64 shuffle(seed);  // one generator for the whole run (network.cpp:153)

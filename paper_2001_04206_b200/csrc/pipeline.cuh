@@ -92,8 +92,8 @@ struct InputPipeline {
 };
 
 // Gather rows idx[0..rows) of X [*, F] and T [*, C] into dst = [rows][F] then
-// [rows][C].  Large batches split the rows over a few host threads (the
-// gather is a pageable-memory read, ~10 GB/s per thread).
+// [rows][C].  Batches over 2 MB split the rows over up to 8 host threads (the
+// gather is a memory-bound copy, a few GB/s per thread).
 inline void gather_rows(const float* X, const float* T, size_t F, size_t C, const uint32_t* idx, size_t rows,
                         float* dst) {
     auto part = [&](size_t r0, size_t r1) {
@@ -104,7 +104,7 @@ inline void gather_rows(const float* X, const float* T, size_t F, size_t C, cons
     };
     const size_t bytes = rows * (F + C) * sizeof(float);
     const unsigned hw = std::max(1u, std::thread::hardware_concurrency());
-    const size_t nt = std::min<size_t>({bytes >> 22, static_cast<size_t>(hw), 8, rows});
+    const size_t nt = std::min<size_t>({bytes >> 20, static_cast<size_t>(hw), 8, rows});
     if (nt <= 1) {
         part(0, rows);
         return;
