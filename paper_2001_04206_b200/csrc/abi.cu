@@ -201,6 +201,8 @@ struct lane_b200_net {
     MbGraph mb_graph;   // captured mini-batch step (per configuration)
     InputPipeline pipe;  // pinned staging + copy stream of train_minibatch
     std::vector<cudaEvent_t> plan_events;  // backward_plan_run_timed
+    float* eval_buf = nullptr;             // batched evaluate scratch
+    size_t eval_count = 0;
 
     LayerBufs& L(size_t l) { return layers.at(l); }
     size_t out_layer() const { return n_hidden; }
@@ -1136,6 +1138,7 @@ int lane_b200_net_destroy(lane_b200_net* net) {
         net->mb_graph.reset();
         net->pipe.release();
         for (cudaEvent_t e : net->plan_events) cudaEventDestroy(e);
+        cudaFree(net->eval_buf);
         cudaFree(net->data);
         cudaFree(net->order);
         lane_b200_ctx* c = net->ctx;
@@ -1446,6 +1449,50 @@ int lane_b200_train(lane_b200_net* net, const float* X_host, const float* T_host
     });
 }
 
+}  // extern "C"
+
+namespace {
+
+// evaluate in FAST numerics: the forward of whole row chunks as GEMMs (the
+// mini-batch path's kernels: tcgen05 3xTF32 where eligible, bias/tanh fused),
+// then per-row softmax / cross entropy / argmax and one fixed-order reduction.
+// STRICT evaluation keeps the per-sample layer path (bit-exact).
+void evaluate_batched(lane_b200_net* net, const float* Xd, const float* Td, size_t n) {
+    lane_b200_ctx* c = net->ctx;
+    const int nl = static_cast<int>(net->layers.size());
+    const int C = static_cast<int>(net->classes);
+    size_t wmax = net->classes;
+    for (auto& Ly : net->layers) wmax = std::max(wmax, Ly.O);
+    const size_t R = std::min<size_t>(n, 8192);
+    // scratch: z | a0 | a1 (R x wmax each) | row losses | row hits
+    ensure(net->eval_buf, net->eval_count, 3 * R * wmax + 2 * R + 64);
+    float* z = net->eval_buf;
+    float* act[2] = {z + R * wmax, z + 2 * R * wmax};
+    float* row_loss = z + 3 * R * wmax;
+    float* row_ok = row_loss + R;
+    GemmCtx g{c->stream, c->sm_count, &net->mb.ws, &net->mb.ws_count, &c->launches};
+    for (size_t r0 = 0; r0 < n; r0 += R) {
+        const int rows = static_cast<int>(std::min(R, n - r0));
+        const float* in = Xd + r0 * net->input_width;
+        for (int l = 0; l < nl; ++l) {
+            LayerBufs& Ly = net->L(l);
+            const bool last = l == nl - 1;
+            float* out = act[l & 1];
+            gemm(g, GemmOp::NN, rows, (int)Ly.O, (int)Ly.I, in, (int)Ly.I, Ly.buf[LANE_BUF_W], (int)Ly.O,
+                 last ? Epi::BIAS : Epi::BIAS_TANH, z, last ? nullptr : out, Ly.buf[LANE_BUF_B], nullptr);
+            in = out;
+        }
+        k_eval_rows<<<(rows + 127) / 128, 128, 0, c->stream>>>(z, Td + r0 * C, rows, C, row_loss, row_ok);
+        k_eval_reduce<<<1, 32, 0, c->stream>>>(row_loss, row_ok, rows, net->loss_dev, net->correct_dev);
+        c->count(2);
+    }
+    c->check_launch();
+}
+
+}  // namespace
+
+extern "C" {
+
 int lane_b200_evaluate(lane_b200_net* net, const float* X_host, const float* T_host, size_t n, float* mean_loss,
                        float* accuracy) {
     return guard([&] {
@@ -1461,7 +1508,10 @@ int lane_b200_evaluate(lane_b200_net* net, const float* X_host, const float* T_h
         LANE_CUDA(cudaMemcpyAsync(Td, T_host, n * C * sizeof(float), cudaMemcpyHostToDevice, c->stream));
         LANE_CUDA(cudaMemsetAsync(net->loss_dev, 0, sizeof(double), c->stream));
         LANE_CUDA(cudaMemsetAsync(net->correct_dev, 0, sizeof(unsigned long long), c->stream));
-        stream_layer_path(net, Xd, Td, n, nullptr, n, 1.0f, net->loss_dev, net->correct_dev, false);
+        if (c->numerics == LANE_NUMERICS_STRICT || n < 64 || C > 128)
+            stream_layer_path(net, Xd, Td, n, nullptr, n, 1.0f, net->loss_dev, net->correct_dev, false);
+        else
+            evaluate_batched(net, Xd, Td, n);
         double loss_sum = 0;
         unsigned long long correct = 0;
         LANE_CUDA(cudaMemcpyAsync(&loss_sum, net->loss_dev, sizeof(double), cudaMemcpyDeviceToHost, c->stream));

@@ -132,6 +132,57 @@ __global__ void k_loss_rows(const float* __restrict__ row_loss, int B, double* l
     if (threadIdx.x == 0) *loss_sum += s;
 }
 
+// evaluate() over a batch of rows (FAST numerics): thread per row, the
+// softmax of the logits Z (bias included) and k_loss_accumulate's per-sample
+// cross entropy and argmax test (ties to the lowest index, network.cpp:13-21).
+__global__ void k_eval_rows(const float* __restrict__ Z, const float* __restrict__ T, int B, int C,
+                            float* __restrict__ row_loss, float* __restrict__ row_ok) {
+    const int b = blockIdx.x * blockDim.x + threadIdx.x;
+    if (b >= B) return;
+    const float* z = Z + (size_t)b * C;
+    const float* t = T + (size_t)b * C;
+    float m = z[0];
+    for (int k = 1; k < C; ++k) m = fmaxf(m, z[k]);
+    float s = 0.0f;
+    for (int k = 0; k < C; ++k) s += lane_libm::expf(ssub(z[k], m));
+    float loss = 0.0f;
+    int bp = 0, bt = 0;
+    float pbest = -1.0f;
+    for (int k = 0; k < C; ++k) {
+        const float p = __fdiv_rn(lane_libm::expf(ssub(z[k], m)), s);
+        if (t[k] != 0.0f) loss = ssub(loss, smul(t[k], lane_libm::logf(p < 1e-12f ? 1e-12f : p)));
+        if (k == 0 || p > pbest) {
+            pbest = p;
+            bp = k;
+        }
+        if (k > 0 && t[k] > t[bt]) bt = k;
+    }
+    row_loss[b] = loss;
+    row_ok[b] = bp == bt ? 1.0f : 0.0f;
+}
+
+// loss_sum += sum_b row_loss[b] (double; lane-strided then a fixed butterfly),
+// correct += sum_b row_ok[b]
+__global__ void k_eval_reduce(const float* __restrict__ row_loss, const float* __restrict__ row_ok, int B,
+                              double* loss_sum, unsigned long long* correct) {
+    if (blockIdx.x != 0 || threadIdx.x >= 32) return;
+    double s = 0.0;
+    unsigned long long ok = 0;
+    for (int b = threadIdx.x; b < B; b += 32) {
+        s += (double)row_loss[b];
+        ok += row_ok[b] != 0.0f ? 1ull : 0ull;
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+        s += __shfl_xor_sync(0xffffffffu, s, o);
+        ok += __shfl_xor_sync(0xffffffffu, ok, o);
+    }
+    if (threadIdx.x == 0) {
+        *loss_sum += s;
+        *correct += ok;
+    }
+}
+
 // Momentum SGD on a flat range: g = gsum * invB; DW = mu*DW + (-eta)*g;
 // W += DW.  Writes the mean gradient back to gsum (LANE_BUF_G semantics).
 // the whole parameter set in one pass: params, grads and velocities share one

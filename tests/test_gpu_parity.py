@@ -679,3 +679,21 @@ def test_minibatch_gradients_vs_finite_differences(lane, fast):
         _fd_check(Ws, bs, X, T, l, G, gb)
     fast.free(Xd)
     fast.free(Td)
+
+
+@pytest.mark.parametrize("F,H,C,n", [(784, [128], 10, 3000), (64, [96, 80], 7, 500), (130, [33], 3, 257)])
+def test_evaluate_batched_fast_vs_oracle(lane, fast, F, H, C, n):
+    """FAST evaluate runs the forward of whole row chunks as GEMMs; mean loss
+    and accuracy against the oracle's per-sample evaluate (network.cpp:184-204)
+    after a short training run moved the weights off their init."""
+    X, T = po.synthetic_dataset(F, C, n, 21)
+    net = lane.build_network(F, H, C, seed=5, device=fast)
+    orc = po.OracleNet(F, H, C, seed=5)
+    lane.train(net, lane.DataSet(X, T), lane.TrainerConfig(lane.LearningRate(0.01), 0.0, 1, 3))
+    for l, layer in enumerate(net.layers):  # same weights on both sides
+        orc.set(l, po.W, layer.weights)
+        orc.set(l, po.B, layer.biases)
+    got = lane.evaluate(net, lane.DataSet(X, T))
+    loss, acc = orc.evaluate(X, T)
+    assert abs(got.mean_loss - loss) <= 1e-5 * abs(loss) + 1e-7
+    assert abs(got.accuracy - acc) <= 2.0 / n
