@@ -80,10 +80,31 @@ def header_symbols() -> list[str]:
     return sorted(set(re.findall(r"\b(lane_b200_[a-z0-9_]+)\s*\(", text)))
 
 
+def _preload_torch_nccl() -> None:
+    """PyTorch ships its own libnccl.so.2, newer than the system one that
+    liblane_b200.so is linked against.  Both are found by the soname
+    libnccl.so.2, and the first one loaded wins.  If the system copy came
+    first, a later ``import torch`` would fail on missing NCCL symbols. So the
+    bundled copy (a superset of the API this library calls) is loaded globally
+    before this library, and torch and the library share one NCCL whichever is
+    imported first."""
+    import importlib.util
+    try:
+        spec = importlib.util.find_spec("nvidia.nccl")
+    except (ImportError, ValueError):
+        return
+    for base in (spec.submodule_search_locations or []) if spec else []:
+        p = os.path.join(base, "lib", "libnccl.so.2")
+        if os.path.exists(p):
+            C.CDLL(p, mode=C.RTLD_GLOBAL)
+            return
+
+
 def load(check_gpu: bool = True):
     global _lib
     if _lib is None:
         path = _build.build()  # no-op when up to date
+        _preload_torch_nccl()
         L = C.CDLL(path)
         for name, (res, args) in SIGNATURES.items():
             f = getattr(L, name)

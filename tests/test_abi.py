@@ -2,6 +2,7 @@
 sm_100a, loads, exports every symbol include/lane_b200.h declares, and fails
 loudly (a status code + message, no crash, no CPU fallback) without a GPU."""
 import ctypes as C
+import os
 import subprocess
 
 import pytest
@@ -46,3 +47,15 @@ def test_no_gpu_is_a_loud_error_not_a_fallback():
     from paper_2001_04206_b200 import lane
     with pytest.raises(lane.Error):
         lane.Device(0)
+
+
+def test_library_then_torch_import_order():
+    """liblane_b200.so links libnccl.so.2; loading it before torch must not
+    bind the older system NCCL that torch's libtorch_cuda cannot use."""
+    import subprocess
+    import sys
+    code = ("from paper_2001_04206_b200 import _native; _native.load(check_gpu=False); "
+            "import torch; print('ok')")
+    out = subprocess.run([sys.executable, "-c", code], capture_output=True, text=True, timeout=600,
+                         cwd=os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+    assert out.returncode == 0 and "ok" in out.stdout, out.stderr[-2000:]

@@ -697,3 +697,32 @@ def test_evaluate_batched_fast_vs_oracle(lane, fast, F, H, C, n):
     loss, acc = orc.evaluate(X, T)
     assert abs(got.mean_loss - loss) <= 1e-5 * abs(loss) + 1e-7
     assert abs(got.accuracy - acc) <= 2.0 / n
+
+
+def test_nccl_communicator_single_rank(lane):
+    """The data-parallel plumbing on the one GPU available: an NCCL
+    communicator of one rank (id created in the library), mini-batch steps
+    through it, and results bitwise equal to a context without one."""
+    from paper_2001_04206_b200 import parallel
+    F, H, C_, B = 48, [64], 5, 32
+    X, T = po.synthetic_dataset(F, C_, 2 * B, 6)
+    out = []
+    for use_comm in (False, True):
+        d = lane.Device(0)
+        if use_comm:
+            parallel.init_comm(d, 0, 1)
+            assert d.world == 1
+        net = lane.build_network(F, H, C_, seed=8, device=d, max_batch=B)
+        Xd, Td = upload(d, X), upload(d, T)
+        for s in range(2):
+            net.minibatch_step(Xd + s * B * F * 4, Td + s * B * C_ * 4, B, 0.05, 0.9)
+        net.allreduce_grads()  # a no-op sum over one rank
+        out.append([layer.weights.copy() for layer in net.layers])
+        if use_comm:
+            d.comm_destroy()
+        d.free(Xd)
+        d.free(Td)
+        net.close()
+        d.close()
+    for a, b in zip(*out):
+        np.testing.assert_array_equal(a, b)
