@@ -14,7 +14,9 @@
 
 #include <nccl.h>
 
+#include <cstdlib>
 #include <cstring>
+#include <vector>
 
 #include "common.cuh"
 #include "gemm.cuh"
@@ -37,12 +39,18 @@ struct MinibatchComm {
 struct MinibatchState {
     float* ws = nullptr;  // GEMM workspace (split-K partials / 3xTF32 splits)
     size_t ws_count = 0;
+    cudaStream_t comm_stream = nullptr;  // per-layer gradient allreduces (data parallel)
+    std::vector<cudaEvent_t> ev;         // one per layer + the join
 };
 
 inline void minibatch_free(MinibatchState& s) {
     if (s.ws) cudaFree(s.ws);
     s.ws = nullptr;
     s.ws_count = 0;
+    for (cudaEvent_t e : s.ev) cudaEventDestroy(e);
+    s.ev.clear();
+    if (s.comm_stream) cudaStreamDestroy(s.comm_stream);
+    s.comm_stream = nullptr;
 }
 
 inline void nccl_unique_id(void* out, size_t bytes) {
@@ -272,6 +280,22 @@ void minibatch_body(Ctx& c, Net& net, size_t Bsz, float eta, float mu, double* l
         gemm(g, GemmOp::NT, B, (int)Ly.O, (int)nx.O, nx.buf[LANE_BUF_DELTAS], (int)nx.O, nx.buf[LANE_BUF_W],
              (int)nx.O, Epi::TANH_GRAD, Ly.buf[LANE_BUF_DELTAS], nullptr, nullptr, Ly.buf[LANE_BUF_OUTPUTS]);
     }
+    // Data parallel: each layer's gradient sums (its G and bias pieces, one
+    // contiguous span of the grads arena) are all-reduced on a communication
+    // stream as soon as its wgrad is done, overlapping the remaining wgrads;
+    // the update waits for all of them.  (LANE_B200_MB_BUCKETS=1 forces this
+    // path on a one-rank communicator, where NCCL's sum is the identity.)
+    static const bool force_buckets = std::getenv("LANE_B200_MB_BUCKETS") != nullptr;
+    const bool buckets = c.comm.comm && (c.comm.world > 1 || force_buckets);
+    auto& M = net.mb;
+    if (buckets) {
+        if (!M.comm_stream) LANE_CUDA(cudaStreamCreateWithFlags(&M.comm_stream, cudaStreamNonBlocking));
+        while ((int)M.ev.size() < nl + 1) {
+            cudaEvent_t e;
+            LANE_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+            M.ev.push_back(e);
+        }
+    }
     // wgrad sums: G_l = X_l^T D_l ; gb_l = colsum(D_l)
     for (int l = 0; l < nl; ++l) {
         auto& Ly = net.L(l);
@@ -279,9 +303,19 @@ void minibatch_body(Ctx& c, Net& net, size_t Bsz, float eta, float mu, double* l
         gemm(g, GemmOp::TN, (int)Ly.I, (int)Ly.O, B, in, (int)Ly.I,
              Ly.buf[LANE_BUF_DELTAS], (int)Ly.O, Epi::STORE, Ly.buf[LANE_BUF_G], nullptr, nullptr, nullptr);
         colsum(g, Ly.buf[LANE_BUF_DELTAS], B, (int)Ly.O, Ly.buf[LANE_BUF_BIAS_GRAD]);
+        if (buckets) {
+            float* begin = Ly.buf[LANE_BUF_G];
+            float* end = l + 1 < nl ? net.L(l + 1).buf[LANE_BUF_G] : net.grads + net.grads_count;
+            LANE_CUDA(cudaEventRecord(M.ev[l], st));
+            LANE_CUDA(cudaStreamWaitEvent(M.comm_stream, M.ev[l], 0));
+            LANE_NCCL(ncclAllReduce(begin, begin, static_cast<size_t>(end - begin), ncclFloat32, ncclSum,
+                                    c.comm.comm, M.comm_stream));
+        }
     }
-    // data parallel: one allreduce of the flat gradient-sum buffer
-    allreduce_grads(c.comm, net.grads, net.grads_count, st);
+    if (buckets) {
+        LANE_CUDA(cudaEventRecord(M.ev[nl], M.comm_stream));
+        LANE_CUDA(cudaStreamWaitEvent(st, M.ev[nl], 0));
+    }
     const float invB = 1.0f / static_cast<float>(Bsz * static_cast<size_t>(c.comm.world));
     {
         // params | grads | velocities are three equal-layout regions (abi.cu arena)

@@ -726,3 +726,39 @@ def test_nccl_communicator_single_rank(lane):
         d.close()
     for a, b in zip(*out):
         np.testing.assert_array_equal(a, b)
+
+
+def test_nccl_bucketed_allreduce_path_single_rank():
+    """The data-parallel step's per-layer allreduces on a communication stream
+    (overlapping the remaining wgrads, captured in the step graph), forced on
+    a one-rank communicator: weights bitwise equal to the plain step."""
+    import subprocess
+    import sys
+    code = r'''
+import numpy as np
+from oracle import pyoracle as po
+from paper_2001_04206_b200 import lane, parallel
+F, H, C, B = 40, [64, 48], 6, 32
+X, T = po.synthetic_dataset(F, C, 4 * B, 7)
+out = []
+for use_comm in (False, True):
+    d = lane.Device(0)
+    if use_comm:
+        parallel.init_comm(d, 0, 1)
+    net = lane.build_network(F, H, C, seed=9, device=d, max_batch=B)
+    xd, td = d.alloc(X.nbytes), d.alloc(T.nbytes)
+    d.h2d(xd, X)
+    d.h2d(td, T)
+    for s in range(4):  # eager, capture, two graph replays
+        net.minibatch_step(xd + s * B * F * 4, td + s * B * C * 4, B, 0.05, 0.9)
+    d.sync()
+    out.append([L.weights.copy() for L in net.layers] + [L.biases.copy() for L in net.layers])
+for a, b in zip(*out):
+    assert np.array_equal(a, b)
+print("BUCKETS OK")
+'''
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    env = dict(os.environ, LANE_B200_MB_BUCKETS="1")
+    r = subprocess.run([sys.executable, "-c", code], cwd=root, env=env, capture_output=True, text=True,
+                       timeout=600)
+    assert r.returncode == 0 and "BUCKETS OK" in r.stdout, r.stdout[-2000:] + r.stderr[-3000:]
