@@ -191,3 +191,44 @@ def test_enlarge_matches_reference():
     e = lane.enlarge(d, 3, 0.05, lane.SeededRng(9))
     assert_bitwise(e.features, Xr)
     assert_bitwise(e.labels, Tr)
+
+
+@needs_ref
+def test_parse_fuzz_matches_reference(tmp_path):
+    """Random near-miss CSV files (mutated fields, separators, signs, blanks,
+    line endings): the library's loader accepts exactly what the reference's
+    load_dataset accepts, with bitwise equal rows."""
+    rs = np.random.default_rng(20261017)
+    atoms = ["0", "1", "0.5", "1e-3", "2.5E+1", "-0.25", ".5", "5.", "+1", " 1", "1 ", "", "nan", "inf",
+             "-0", "1e", "0x1p-2", "1,0", "\t", "0.3333333333333333", "3.4028235e38", "1e-45", "abc"]
+    for trial in range(400):
+        lines = []
+        for _ in range(int(rs.integers(1, 6))):
+            feats = [str(np.float32(rs.uniform(0, 1))) for _ in range(4)]
+            lab = ["0", "0", "0"]
+            lab[int(rs.integers(3))] = "1"
+            fields = feats + lab
+            for _ in range(int(rs.integers(0, 3))):  # mutate a few fields
+                fields[int(rs.integers(len(fields)))] = atoms[int(rs.integers(len(atoms)))]
+            line = ",".join(fields)
+            if rs.random() < 0.2:
+                line += ","
+            if rs.random() < 0.2:
+                line += "\r"
+            lines.append(line)
+        if rs.random() < 0.3:
+            lines.insert(int(rs.integers(len(lines) + 1)), "")
+        p = tmp_path / f"fuzz{trial}.csv"
+        p.write_bytes(("\n".join(lines) + ("\n" if rs.random() < 0.5 else "")).encode())
+        Xr = np.zeros((16, 4), np.float32)
+        Tr = np.zeros((16, 3), np.float32)
+        got = po.ref_lib().lr_load_dataset(str(p).encode(), 4, 3, Xr.reshape(-1), Tr.reshape(-1), 16)
+        try:
+            d = lane.load_dataset(p, 4, 3)
+            mine = d.size()
+        except lane.ParseError:
+            mine = -1
+        assert mine == got, (trial, p.read_text())
+        if got > 0:
+            assert_bitwise(d.features, Xr[:got])
+            assert_bitwise(d.labels, Tr[:got])
