@@ -1042,12 +1042,14 @@ __device__ __forceinline__ void win_chain(const WinArgs& A, float* sm, const Win
             }
 #pragma unroll
             for (int k = 0; k < CC; ++k) t[k] = tn[k];
+            WIN_TRACE(s, 14);
             // row s+1 was flagged by its helper ~2 samples ago: fetch it now so
             // the shared-memory latency hides under this sample's chain
             if (s + 1 < n) {
                 flag_wait(s + 1, nR);
                 fetch_row(s + 1, nR, nRd);
             }
+            WIN_TRACE(s, 15);
             // FAST numerics: the W1 update as one FMA, w + d1 (-eta a)
 #pragma unroll
             for (int m = 0; m < JPL; ++m)

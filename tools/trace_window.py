@@ -43,6 +43,9 @@ def main():
     def row(name, d):
         d = np.asarray(d)
         print(f"  {name:34s} median {np.median(d):7.0f}  mean {np.mean(d):7.0f}  max {np.max(d):7.0f}")
+    row("  z + tanh (of phase 0)", t[:, 14] - t[:, 0])
+    row("  flag wait + fetch row s+1", t[:, 15] - t[:, 14])
+    row("  W1 update (s-1)", t[:, 1] - t[:, 15])
     for k in range(len(PH)):
         row(PH[k], t[:, k + 1] - t[:, k])
     row("loop back", t[1:, 0] - t[:-1, 6])
