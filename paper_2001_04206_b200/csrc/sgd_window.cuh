@@ -953,8 +953,12 @@ __device__ __forceinline__ void win_chain(const WinArgs& A, float* sm, const Win
         float* const es = zt + NCW * kWinCP;                       // this warp's exponentials copy
         // prefetched operands of the next sample (raw: sums at first use)
         constexpr int kMaxKS = 2;  // the plan uses at most 2 row splits
-        float zraw[JPL], yraw[kMaxKS][JPL];
-        float tn[CC], c1n = 0.0f, c2n = 0.0f, town = 0.0f;
+        struct Pre {
+            float zraw[JPL], yraw[kMaxKS][JPL], tn[CC];
+            float c1n, c2n, town;
+        };
+        Pre pa, pb;
+        pa.c1n = pa.c2n = pa.town = pb.c1n = pb.c2n = pb.town = 0.0f;
         auto flag_wait = [&](int s1, int s1R) {
             if (s1 < 3) return;  // rows 0..2: the chain applies every correction itself
             const uint32_t fa = smem_u32(rowflag + s1R);
@@ -970,7 +974,13 @@ __device__ __forceinline__ void win_chain(const WinArgs& A, float* sm, const Win
             }
         };
         // s1R = s1 % R, s1Rd = s1 % Rd (ring slots), kept incrementally
-        auto fetch_row = [&](int s1, int s1R, int s1Rd) {
+        auto fetch_row = [&](int s1, int s1R, int s1Rd, Pre& dst) {
+            float(&zraw)[JPL] = dst.zraw;
+            float(&yraw)[kMaxKS][JPL] = dst.yraw;
+            float(&tn)[CC] = dst.tn;
+            float& c1n = dst.c1n;
+            float& c2n = dst.c2n;
+            float& town = dst.town;
             const int b1 = s1 >> 4, u1 = s1 & (kWinS - 1), st1 = b1 & 1;
             if (u1 == 0) mbar_wait_cta(MB(kMbYFull + st1), (uint32_t)((b1 >> 1) & 1), A.error);
             vld<JPL>(zacc + s1R * HP + j0, zraw);
@@ -1024,30 +1034,30 @@ __device__ __forceinline__ void win_chain(const WinArgs& A, float* sm, const Win
             for (int p = 1; p < CS; ++p) tot += g[p * kWinCP];
             return tot;
         };
-        if (n > 0) fetch_row(0, 0, 0);
+        if (n > 0) fetch_row(0, 0, 0, pa);
         int sR = 0, sRd = 0;      // s % R, s % Rd
         int nR = 1 % R, nRd = 1;  // (s+1) % R, (s+1) % Rd
-        for (int s = 0; s < n; ++s) {
+        auto body = [&](const int s, Pre& cur, Pre& nxt) {
             const int b = s >> 4, u = s & (kWinS - 1), st = b & 1;
             WIN_TRACE(s, 0);
             // -- z(s) = Y + window + c1 d0(s-1) + c2 d0(s-2) + b0;  tanh.
             //    The deferred W1 update of s-1 fills the tanh latency.
             float z[JPL], a[JPL], t[CC];
-            const float tow = town;
+            const float tow = cur.town;
 #pragma unroll
             for (int m = 0; m < JPL; ++m) {
-                const float y = zraw[m] + (yraw[0][m] + yraw[1][m]);
-                z[m] = fmaf(c1n, dp1[m], fmaf(c2n, dp2[m], y)) + b0r[m];
+                const float y = cur.zraw[m] + (cur.yraw[0][m] + cur.yraw[1][m]);
+                z[m] = fmaf(cur.c1n, dp1[m], fmaf(cur.c2n, dp2[m], y)) + b0r[m];
                 a[m] = tanhf(z[m]);
             }
 #pragma unroll
-            for (int k = 0; k < CC; ++k) t[k] = tn[k];
+            for (int k = 0; k < CC; ++k) t[k] = cur.tn[k];
             WIN_TRACE(s, 14);
             // row s+1 was flagged by its helper ~2 samples ago: fetch it now so
             // the shared-memory latency hides under this sample's chain
             if (s + 1 < n) {
                 flag_wait(s + 1, nR);
-                fetch_row(s + 1, nR, nRd);
+                fetch_row(s + 1, nR, nRd, nxt);
             }
             WIN_TRACE(s, 15);
             // FAST numerics: the W1 update as one FMA, w + d1 (-eta a)
@@ -1187,6 +1197,12 @@ __device__ __forceinline__ void win_chain(const WinArgs& A, float* sm, const Win
             if (++nR == R) nR = 0;
             if (++nRd == Rd) nRd = 0;
             WIN_TRACE(s, 6);
+        };
+        // unrolled by two: the prefetch of row s+1 lands in the other register
+        // set (no copies of the prefetched row between samples)
+        for (int s = 0; s < n; s += 2) {
+            body(s, pa, pb);
+            if (s + 1 < n) body(s + 1, pb, pa);
         }
         if (n > 0) {
             // the last sample's W1 update (deferred in the loop)
