@@ -13,17 +13,19 @@
 // and the tf32 truncation of the lo parts), within the path's 1e-5 tolerance
 // (1xTF32 alone is ~5e-4 and is NOT used).
 //
-// Structure (one 128x128 output tile per CTA, 320 threads, 4-stage ring):
+// Structure (one 128x128 output tile per CTA -- or one 256x256 tile per CTA
+// pair, below -- 320 threads, 4-stage ring):
 //   warp 0      TMA producer: A/B tiles (fp32) -> smem ring
 //   warp 1      MMA issuer: one elected thread issues tcgen05.mma (A from
 //               TMEM), commits smem/TMEM slots back to the producer and the
 //               accumulator to the epilogue (tcgen05.commit -> mbarrier)
 //   warps 2..9  split pass: rows of A -> TMEM (A, A_lo; the two warps of a
 //               TMEM lane quarter take 16 K columns each) and B_lo -> smem;
-//               then the epilogue (two warps per lane quarter, 64 columns
-//               each): tcgen05.ld TMEM -> registers -> fused epilogue -> global
-// TMEM: columns [0,128) accumulator, then per stage 32 columns of A and 32 of
-// A_lo (lane = row of A, column = k).
+//               then the epilogue (two warps per lane quarter, half the
+//               tile's columns each): tcgen05.ld TMEM -> registers -> fused
+//               epilogue -> global
+// TMEM: columns [0, tile N) accumulator, then per stage 32 columns of A and 32
+// of A_lo (lane = row of A, column = k).
 // Operand majors: K-major tiles come from one TMA box {32 (K), 128 (MN)},
 // 128B swizzle; a MN-major B from four boxes {32 (MN), 32 (K)} (32-byte-atom
 // swizzle, the layout the MMA reads); a MN-major A -- read only by the split
@@ -40,8 +42,8 @@ constexpr int kTcBM = 128, kTcBN = 128, kTcBK = 32;
 constexpr int kTcTile = kTcBM * kTcBK * 4;  // bytes of one 128x32 fp32 tile (A)
 constexpr int kTcTmemCols = 512;            // accumulator (128) + stages x (A, A_lo) x 32
 // Per-CTA ring.  PAIR = a CTA pair (cluster of 2, tcgen05 cta_group::2) on a
-// 256 x 128 tile: each CTA holds its 128 rows of A and half (64 columns) of B,
-// so each SM reads half the B bytes per MMA and the ring fits 6 stages.
+// 256 x 256 tile, issued as N = 256 MMAs: each CTA holds its 128 rows of A (in
+// TMEM) and half (128 columns) of B; rank 0 issues the pair's MMAs.
 template <bool PAIR>
 struct TcCfg {
     static constexpr int kBN = PAIR ? 2 * kTcBN : kTcBN;   // tile N (pairs: 256 x 256 tiles)
