@@ -315,6 +315,13 @@ def run_minibatch(args, wl):
     peaks = json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json"))) if os.path.exists(
         os.path.join(ROOT, "MEASURED_PEAKS.json")) else {"bf16_tflops": 1590.0}
     peak = float(peaks.get("bf16_tflops", 1590.0)) / 2.0 / 3.0  # tf32 = bf16/2; 3 MMAs per product
+    # the step's two sequential phases each have a floor: the GEMMs on the tensor
+    # pipe and the update streaming W, V and G (read + write, 24 B/param) from
+    # HBM; the next step's forward needs the updated weights, so they add
+    hbm_peak, _ = load_peaks()
+    n_param = sum(a * b + b for a, b in zip(widths[:-1], widths[1:]))
+    floor_tensor_us = flops / (peak * 1e12) * 1e6
+    floor_update_us = 24.0 * n_param / (hbm_peak * 1e9) * 1e6
     line = {"metric": METRIC, "value": value, "unit": "samples/s", "n_gpus": world,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms / args.steps,
             "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f32",
@@ -327,6 +334,10 @@ def run_minibatch(args, wl):
                          "frac": achieved / peak, "traffic": load_traffic(wl)[0],
                          "traffic_source": load_traffic(wl)[1],
                          "scope": "whole step (all kernels incl. the HBM-bound update) / step time",
+                         "step_floor": {"tensor_us": floor_tensor_us, "hbm_update_us": floor_update_us,
+                                        "frac": (floor_tensor_us + floor_update_us) / (ms / args.steps * 1e3),
+                                        "how": "GEMM flops at the derived 3xTF32 peak + the update's 24 B/param "
+                                               "at the measured HBM peak, against the measured step time"},
                          "dominant_kernel": {"kernel": "k_gemm_tc", "achieved": gemm_tf, "frac": gemm_tf / peak,
                                              "flop_share_of_step": gemm_share,
                                              "how": "the step's tensor-core GEMM shapes (fwd/dgrad/wgrad of "
