@@ -545,13 +545,17 @@ inline bool gemm_try_tc(GemmCtx& g, GemmOp op, int M, int N, int K, const float*
     }
     TcArgs t{M, N, K, 0, nullptr, C, C2, bias, aux};
     // split-K when the 128x128 tiles fill less than half the SMs (the M = batch
-    // GEMMs at B = 256): S splits of >= 8 K blocks each, <= 4, one wave
+    // GEMMs at B = 256): S splits of >= 24 K blocks each, <= 4, one wave
     // CTAs per split: pairs run 256 x 256 tiles on 2 CTAs
     constexpr int kPN = TcCfg<true>::kBN;
     const int tiles = pair ? 2 * ((M + 2 * kTcBM - 1) / (2 * kTcBM)) * ((N + kPN - 1) / kPN)
                            : ((M + kTcBM - 1) / kTcBM) * ((N + kTcBN - 1) / kTcBN);
     const int nkb = K / kTcBK;
-    int S = std::min({4, g.sm_count / std::max(1, tiles), nkb / 8});
+    static const int smax = std::getenv("LANE_B200_TC_SPLITK_MAX") ? std::atoi(std::getenv("LANE_B200_TC_SPLITK_MAX")) : 4;
+    // split only when every split keeps >= 24 K blocks: C3's 256x4096x1024
+    // forward ran 29.4 us with two 16-block splits + the reduce, 26.1 us unsplit
+    static const int kbmin = std::getenv("LANE_B200_TC_SPLITK_KBMIN") ? std::atoi(std::getenv("LANE_B200_TC_SPLITK_KBMIN")) : 24;
+    int S = std::min({smax, g.sm_count / std::max(1, tiles), nkb / kbmin});
     if (K % kTcBK != 0 || (N & 3) != 0) S = 1;
     if (S > 1) {
         t.kbs = (nkb + S - 1) / S;

@@ -59,7 +59,8 @@ def operands(op, M, N, K, rs):
 
 @pytest.mark.parametrize("use_tc", [1, 0])
 @pytest.mark.parametrize("op", [NN, NT, TN])
-@pytest.mark.parametrize("M,N,K", [(128, 128, 32), (256, 512, 1024), (192, 320, 96), (64, 4100, 36),
+@pytest.mark.parametrize("M,N,K", [(128, 128, 32), (256, 512, 2048), (256, 512, 1024), (192, 320, 96),
+                                   (64, 4100, 36),
                                    (1024, 256, 256),
                                    # CTA-pair tiles (M >= 512, K >= 2048); 640 leaves the last
                                    # pair's second CTA entirely past M
@@ -72,8 +73,8 @@ def test_gemm_store_condition_aware(dev, op, M, N, K, use_tc):
     cond = np.abs(Am) @ np.abs(Bm)
     err = np.abs(out - ref)
     # tensor cores split K (+1 fixed-order reduce launch) when the tiles fill
-    # under half the SMs: (256, 512, 1024) always does
-    split = use_tc and (M, N, K) == (256, 512, 1024)
+    # under half the SMs and every split keeps >= 24 K blocks: (256, 512, 2048)
+    split = use_tc and (M, N, K) == (256, 512, 2048)
     assert launched == (2 if split else 1) or (use_tc and launched == 2)
     assert np.all(err <= 1e-5 * cond + 1e-30), f"max err/cond {np.max(err / (cond + 1e-30)):.3e}"
 
