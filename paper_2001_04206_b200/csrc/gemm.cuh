@@ -315,34 +315,35 @@ __global__ void k_colsum_part(const float* __restrict__ D, int B, int O, float* 
     part[(size_t)blockIdx.y * O + o] = (v[0] + v[1]) + (v[2] + v[3]);
 }
 
-// One pass: CTA = 32 columns x 8 row groups (warp w sums rows b = w mod 8,
-// four chains), the 8 group sums meet in shared memory in a fixed order.
-__global__ void __launch_bounds__(256) k_colsum(const float* __restrict__ D, int B, int O, float* __restrict__ gb) {
-    __shared__ float red[8][33];
+// One pass: CTA = 32 columns x 16 row groups (warp w sums rows b = w mod 16,
+// eight independent chains so a warp keeps eight loads in flight), the 16
+// group sums meet in shared memory in a fixed order.
+__global__ void __launch_bounds__(512) k_colsum(const float* __restrict__ D, int B, int O, float* __restrict__ gb) {
+    __shared__ float red[16][33];
     const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
     const int o = blockIdx.x * 32 + lane;
-    float v[4] = {0.0f, 0.0f, 0.0f, 0.0f};
+    float v[8] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
     if (o < O) {
         int b = w;
-        for (; b + 24 < B; b += 32) {
+        for (; b + 7 * 16 < B; b += 8 * 16) {
 #pragma unroll
-            for (int u = 0; u < 4; ++u) v[u] += __ldg(D + (size_t)(b + 8 * u) * O + o);
+            for (int u = 0; u < 8; ++u) v[u] += __ldg(D + (size_t)(b + 16 * u) * O + o);
         }
-        for (; b < B; b += 8) v[0] += __ldg(D + (size_t)b * O + o);
+        for (; b < B; b += 16) v[0] += __ldg(D + (size_t)b * O + o);
     }
-    red[w][lane] = (v[0] + v[1]) + (v[2] + v[3]);
+    red[w][lane] = ((v[0] + v[1]) + (v[2] + v[3])) + ((v[4] + v[5]) + (v[6] + v[7]));
     __syncthreads();
     if (w == 0 && o < O) {
         float t = red[0][lane];
 #pragma unroll
-        for (int q = 1; q < 8; ++q) t += red[q][lane];
+        for (int q = 1; q < 16; ++q) t += red[q][lane];
         gb[o] = t;
     }
 }
 
 inline void colsum(GemmCtx& g, const float* D, int B, int O, float* gb) {
     if (B <= 1024 && ((O + 31) / 32 >= g.sm_count / 2 || B <= 256)) {
-        k_colsum<<<(O + 31) / 32, 256, 0, g.stream>>>(D, B, O, gb);
+        k_colsum<<<(O + 31) / 32, 512, 0, g.stream>>>(D, B, O, gb);
         *g.launches += 1;
         return;
     }
