@@ -245,6 +245,7 @@ __device__ __forceinline__ void stage_rows(float* dst, const float* __restrict__
 
 constexpr int kSkinnyKChunk = 128;
 constexpr int kSkTnW = 4;
+template <int NM>  // N <= NM (16 or 32): accumulators and the unrolled class loop
 __global__ void __launch_bounds__(32 * kSkTnW) k_gemm_skinny_tn(int M, int N, int K, const float* __restrict__ A,
                                                                const float* __restrict__ B, float* __restrict__ part,
                                                                int cpb) {
@@ -253,9 +254,9 @@ __global__ void __launch_bounds__(32 * kSkTnW) k_gemm_skinny_tn(int M, int N, in
     __shared__ float red[kSkTnW][32][33];
     const int tx = threadIdx.x & 31, ty = threadIdx.x >> 5;
     const int m = blockIdx.x * 32 + tx;
-    float acc[32];
+    float acc[NM];
 #pragma unroll
-    for (int n = 0; n < 32; ++n) acc[n] = 0.0f;
+    for (int n = 0; n < NM; ++n) acc[n] = 0.0f;
     for (int c = 0; c < cpb; ++c) {
         const int k0 = (blockIdx.y * cpb + c) * kSkinnyKChunk, k1 = min(K, k0 + kSkinnyKChunk);
         if (k0 >= K) break;
@@ -268,13 +269,13 @@ __global__ void __launch_bounds__(32 * kSkTnW) k_gemm_skinny_tn(int M, int N, in
                 const float a = __ldg(A + (size_t)k * M + m);
                 const float* brow = bs + (k - k0) * N;
 #pragma unroll
-                for (int n = 0; n < 32; ++n)
+                for (int n = 0; n < NM; ++n)
                     if (n < N) acc[n] = fmaf(a, brow[n], acc[n]);
             }
         }
     }
 #pragma unroll
-    for (int n = 0; n < 32; ++n)
+    for (int n = 0; n < NM; ++n)
         if (n < N) red[ty][tx][n] = acc[n];
     __syncthreads();
     // thread (tx, ty): outputs n = ty, ty + kSkTnW, ... of column m
@@ -483,14 +484,20 @@ inline bool gemm_try_skinny(GemmCtx& g, GemmOp op, int M, int N, int K, const fl
         K <= 4 * kSkinnyKChunk) {
         // enough row blocks to fill the GPU: one pass over K, no partials
         const int S = (K + kSkinnyKChunk - 1) / kSkinnyKChunk;
-        k_gemm_skinny_tn<<<dim3((M + 31) / 32, 1), 32 * kSkTnW, 0, g.stream>>>(M, N, K, A, B, C, S);
+        if (N <= 16)
+            k_gemm_skinny_tn<16><<<dim3((M + 31) / 32, 1), 32 * kSkTnW, 0, g.stream>>>(M, N, K, A, B, C, S);
+        else
+            k_gemm_skinny_tn<32><<<dim3((M + 31) / 32, 1), 32 * kSkTnW, 0, g.stream>>>(M, N, K, A, B, C, S);
         *g.launches += 1;
         return true;
     }
     if (op == GemmOp::TN && lda == M && ldb == N && e == Epi::STORE) {
         const int S = (K + kSkinnyKChunk - 1) / kSkinnyKChunk;
         ensure_ws(g, (size_t)S * M * N);
-        k_gemm_skinny_tn<<<dim3((M + 31) / 32, S), 32 * kSkTnW, 0, g.stream>>>(M, N, K, A, B, *g.ws, 1);
+        if (N <= 16)
+            k_gemm_skinny_tn<16><<<dim3((M + 31) / 32, S), 32 * kSkTnW, 0, g.stream>>>(M, N, K, A, B, *g.ws, 1);
+        else
+            k_gemm_skinny_tn<32><<<dim3((M + 31) / 32, S), 32 * kSkTnW, 0, g.stream>>>(M, N, K, A, B, *g.ws, 1);
         k_sum_partials<<<std::max(1, std::min(4 * g.sm_count, (M * N + 255) / 256)), 256, 0, g.stream>>>(
             *g.ws, S, (size_t)M * N, C);
         *g.launches += 2;
