@@ -245,13 +245,19 @@ __device__ __forceinline__ void stage_rows(float* dst, const float* __restrict__
 
 constexpr int kSkinnyKChunk = 128;
 constexpr int kSkTnW = 4;
-template <int NM>  // N <= NM (16 or 32): accumulators and the unrolled class loop
-__global__ void __launch_bounds__(32 * kSkTnW) k_gemm_skinny_tn(int M, int N, int K, const float* __restrict__ A,
-                                                               const float* __restrict__ B, float* __restrict__ part,
-                                                               int cpb) {
+// N <= NM (16 or 32): accumulators and the unrolled class loop; TW k-groups
+// (warps) per CTA -- 8 for NM = 16, so more loads are in flight
+template <int NM>
+constexpr int skinny_tn_warps() { return NM == 16 ? 8 : kSkTnW; }
+template <int NM>
+__global__ void __launch_bounds__(32 * skinny_tn_warps<NM>()) k_gemm_skinny_tn(int M, int N, int K,
+                                                                              const float* __restrict__ A,
+                                                                              const float* __restrict__ B,
+                                                                              float* __restrict__ part, int cpb) {
+    constexpr int TW = skinny_tn_warps<NM>();
     // this CTA: K chunks [blockIdx.y * cpb, +cpb) (cpb = chunks per block)
     __shared__ __align__(16) float bs[kSkinnyKChunk * 32];
-    __shared__ float red[kSkTnW][32][33];
+    __shared__ float red[TW][32][NM + 1];
     const int tx = threadIdx.x & 31, ty = threadIdx.x >> 5;
     const int m = blockIdx.x * 32 + tx;
     float acc[NM];
@@ -265,7 +271,7 @@ __global__ void __launch_bounds__(32 * kSkTnW) k_gemm_skinny_tn(int M, int N, in
         __syncthreads();
         if (m < M) {
 #pragma unroll 4
-            for (int k = k0 + ty; k < k1; k += kSkTnW) {
+            for (int k = k0 + ty; k < k1; k += TW) {
                 const float a = __ldg(A + (size_t)k * M + m);
                 const float* brow = bs + (k - k0) * N;
 #pragma unroll
@@ -278,13 +284,13 @@ __global__ void __launch_bounds__(32 * kSkTnW) k_gemm_skinny_tn(int M, int N, in
     for (int n = 0; n < NM; ++n)
         if (n < N) red[ty][tx][n] = acc[n];
     __syncthreads();
-    // thread (tx, ty): outputs n = ty, ty + kSkTnW, ... of column m
+    // thread (tx, ty): outputs n = ty, ty + TW, ... of column m
     if (m < M) {
         float* out = part + ((size_t)blockIdx.y * M + m) * N;
-        for (int n = ty; n < N; n += kSkTnW) {
+        for (int n = ty; n < N; n += TW) {
             float v = red[0][tx][n];
 #pragma unroll
-            for (int w = 1; w < kSkTnW; ++w) v += red[w][tx][n];
+            for (int w = 1; w < TW; ++w) v += red[w][tx][n];
             out[n] = v;
         }
     }
@@ -485,7 +491,7 @@ inline bool gemm_try_skinny(GemmCtx& g, GemmOp op, int M, int N, int K, const fl
         // enough row blocks to fill the GPU: one pass over K, no partials
         const int S = (K + kSkinnyKChunk - 1) / kSkinnyKChunk;
         if (N <= 16)
-            k_gemm_skinny_tn<16><<<dim3((M + 31) / 32, 1), 32 * kSkTnW, 0, g.stream>>>(M, N, K, A, B, C, S);
+            k_gemm_skinny_tn<16><<<dim3((M + 31) / 32, 1), 32 * skinny_tn_warps<16>(), 0, g.stream>>>(M, N, K, A, B, C, S);
         else
             k_gemm_skinny_tn<32><<<dim3((M + 31) / 32, 1), 32 * kSkTnW, 0, g.stream>>>(M, N, K, A, B, C, S);
         *g.launches += 1;
@@ -495,7 +501,8 @@ inline bool gemm_try_skinny(GemmCtx& g, GemmOp op, int M, int N, int K, const fl
         const int S = (K + kSkinnyKChunk - 1) / kSkinnyKChunk;
         ensure_ws(g, (size_t)S * M * N);
         if (N <= 16)
-            k_gemm_skinny_tn<16><<<dim3((M + 31) / 32, S), 32 * kSkTnW, 0, g.stream>>>(M, N, K, A, B, *g.ws, 1);
+            k_gemm_skinny_tn<16><<<dim3((M + 31) / 32, S), 32 * skinny_tn_warps<16>(), 0, g.stream>>>(M, N, K, A, B,
+                                                                                                   *g.ws, 1);
         else
             k_gemm_skinny_tn<32><<<dim3((M + 31) / 32, S), 32 * kSkTnW, 0, g.stream>>>(M, N, K, A, B, *g.ws, 1);
         k_sum_partials<<<std::max(1, std::min(4 * g.sm_count, (M * N + 255) / 256)), 256, 0, g.stream>>>(
