@@ -389,16 +389,26 @@ __global__ void __launch_bounds__(256) k_gemm_skinny_nn_kc(int M, int N, int K, 
         for (int n = 0; n < 16; ++n)
             if (n < N) acc[n] = fmaf(a, brow[n], acc[n]);
     }
+    // transpose-reduce the 16 sums over the warp (fixed butterfly, 16
+    // shuffles instead of 16 x 5): after the offsets 16, 8, 4, 2 a lane holds
+    // the partial of value idx = its lane bits 4..1; offset 1 completes it
+    int nv = 16;
 #pragma unroll
-    for (int n = 0; n < 16; ++n)
-        if (n < N) acc[n] = warp_sum(acc[n]);
-    if (lane < N) {
-        float v = 0.0f;
+    for (int o = 16; o >= 2; o >>= 1) {
+        nv >>= 1;
+        const bool hi = (lane & o) != 0;
 #pragma unroll
-        for (int n = 0; n < 16; ++n)
-            if (n == lane) v = acc[n];
-        part[((size_t)blockIdx.y * M + m) * N + lane] = v;
+        for (int q = 0; q < 8; ++q) {
+            if (q < nv) {
+                const float send = hi ? acc[q] : acc[q + nv];
+                const float keep = hi ? acc[q + nv] : acc[q];
+                acc[q] = keep + __shfl_xor_sync(0xffffffffu, send, o);
+            }
+        }
     }
+    const float v = acc[0] + __shfl_xor_sync(0xffffffffu, acc[0], 1);
+    const int idx = ((lane >> 4) & 1) * 8 + ((lane >> 3) & 1) * 4 + ((lane >> 2) & 1) * 2 + ((lane >> 1) & 1);
+    if ((lane & 1) == 0 && idx < N) part[((size_t)blockIdx.y * M + m) * N + idx] = v;
 }
 
 // out = epilogue(sum_{s < S} part[s]) in a fixed order; bias per column
