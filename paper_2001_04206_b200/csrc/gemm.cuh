@@ -419,7 +419,7 @@ __global__ void k_sum_partials_epi(const float* __restrict__ part, int S, int M,
     for (size_t e = (size_t)blockIdx.x * blockDim.x + threadIdx.x; e < count; e += (size_t)gridDim.x * blockDim.x) {
         float v = part[e];
         for (int s2 = 1; s2 < S; ++s2) v += part[(size_t)s2 * count + e];
-        if constexpr (E == Epi::BIAS || E == Epi::BIAS_TANH) v = sadd(v, bias[e % N]);
+        if constexpr (E == Epi::BIAS || E == Epi::BIAS_TANH) v = sadd(v, bias[(unsigned)e % (unsigned)N]);
         C[e] = v;
         if constexpr (E == Epi::BIAS_TANH) C2[e] = tanhf(v);
     }

@@ -497,7 +497,10 @@ __global__ void __launch_bounds__(256) k_tc_splitk_reduce(TcArgs a, int S) {
             v.z += p.z;
             v.w += p.w;
         }
-        const int m = (int)((4 * e) / a.N), n = (int)((4 * e) % a.N);
+        // 32-bit index math (M * N < 2^32 for every split-K shape): no 64-bit
+        // division per element
+        const unsigned q = (unsigned)(4 * e), uN = (unsigned)a.N;
+        const int m = (int)(q / uN), n = (int)(q - (q / uN) * uN);
         float4 t;
         v = tc_epi4<E>(a, m, n, v, &t);
         reinterpret_cast<float4*>(a.C)[e] = v;
