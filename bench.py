@@ -533,7 +533,7 @@ def main():
                                  "stream"},
             "e2e": {"value": e2e, "unit": "samples/s",
                     "h2d_bytes_per_step": int(X.nbytes + T.nbytes),
-                    "d2h_bytes_per_step": 8 * 2},
+                    "d2h_bytes_per_step": 8 * 2 + 4},  # EpochStats (loss sum, hits) + the device error flag
             "gpu_launches": int(launches),
             "clocks": clk.summary()}
     if rank == 0 and not args.no_cpu:

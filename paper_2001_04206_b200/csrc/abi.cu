@@ -1091,8 +1091,9 @@ int lane_b200_net_create(lane_b200_ctx* c, size_t input_width, const size_t* hid
         net->grads = base + grads_begin;
         net->target_stage = base + stage_off;
         net->step = static_cast<long long*>(dev_alloc(sizeof(long long)));
-        net->loss_dev = static_cast<double*>(dev_alloc(sizeof(double)));
-        net->correct_dev = static_cast<unsigned long long*>(dev_alloc(sizeof(unsigned long long)));
+        // loss sum and hit count side by side: one memset and one D2H per epoch
+        net->loss_dev = static_cast<double*>(dev_alloc(2 * sizeof(double)));
+        net->correct_dev = reinterpret_cast<unsigned long long*>(net->loss_dev + 1);
         // split-K partials of the FAST forward (sized up front: the forward is
         // also captured into CUDA graphs, where allocation is not allowed)
         size_t part = 0;
@@ -1131,7 +1132,6 @@ int lane_b200_net_destroy(lane_b200_net* net) {
         cudaFree(net->scratch);
         cudaFree(net->step);
         cudaFree(net->loss_dev);
-        cudaFree(net->correct_dev);
         cudaFree(net->slots);
         cudaFree(net->win_coef);
         cudaFree(net->win_ring);
@@ -1414,30 +1414,40 @@ int lane_b200_train(lane_b200_net* net, const float* X_host, const float* T_host
         size_t ran = 0, done = 0;
         for (size_t epoch = 1; epoch <= max_epochs; ++epoch) {
             for (size_t i = n; i > 1; --i) std::swap(order[i - 1], order[shuffle.below(i)]);
-            LANE_CUDA(cudaMemsetAsync(net->loss_dev, 0, sizeof(double), c->stream));
-            LANE_CUDA(cudaMemsetAsync(net->correct_dev, 0, sizeof(unsigned long long), c->stream));
+            LANE_CUDA(cudaMemsetAsync(net->loss_dev, 0, 2 * sizeof(double), c->stream));  // loss + hits
             size_t chunk = kFirst;
             for (size_t s = 0; s < n; s += chunk, chunk = std::min(2 * chunk, kMax)) {
                 const size_t m = std::min(chunk, n - s);
                 const int k = static_cast<int>(done++ % InputPipeline::kSlots);
                 if (P.pending[k]) LANE_CUDA(cudaEventSynchronize(P.copied[k]));
                 gather_rows(X_host, T_host, I, C, order.data() + s, m, P.host[k]);
-                LANE_CUDA(cudaStreamWaitEvent(P.copy, P.consumed[k], 0));
-                LANE_CUDA(cudaMemcpyAsync(P.dev[k], P.host[k], m * (I + C) * sizeof(float), cudaMemcpyHostToDevice,
-                                          P.copy));
-                LANE_CUDA(cudaEventRecord(P.copied[k], P.copy));
-                LANE_CUDA(cudaStreamWaitEvent(c->stream, P.copied[k], 0));
+                if (m == n) {
+                    // the whole epoch in one chunk: nothing to overlap, so copy on
+                    // the compute stream (no cross-stream events on the latency path)
+                    LANE_CUDA(cudaMemcpyAsync(P.dev[k], P.host[k], m * (I + C) * sizeof(float),
+                                              cudaMemcpyHostToDevice, c->stream));
+                    LANE_CUDA(cudaEventRecord(P.copied[k], c->stream));
+                } else {
+                    LANE_CUDA(cudaStreamWaitEvent(P.copy, P.consumed[k], 0));
+                    LANE_CUDA(cudaMemcpyAsync(P.dev[k], P.host[k], m * (I + C) * sizeof(float),
+                                              cudaMemcpyHostToDevice, P.copy));
+                    LANE_CUDA(cudaEventRecord(P.copied[k], P.copy));
+                    LANE_CUDA(cudaStreamWaitEvent(c->stream, P.copied[k], 0));
+                }
                 sgd_stream_impl(net, P.dev[k], P.dev[k] + m * I, m, nullptr, m, eta, net->loss_dev,
                                 net->correct_dev);
                 LANE_CUDA(cudaEventRecord(P.consumed[k], c->stream));
                 P.pending[k] = true;
             }
-            double loss_sum = 0;
-            unsigned long long correct = 0;
-            LANE_CUDA(cudaMemcpyAsync(&loss_sum, net->loss_dev, sizeof(double), cudaMemcpyDeviceToHost, c->stream));
-            LANE_CUDA(cudaMemcpyAsync(&correct, net->correct_dev, sizeof(correct), cudaMemcpyDeviceToHost, c->stream));
+            double stats[2];  // loss sum, hit count (bit pattern)
+            int dev_err = 0;  // persistent-kernel exchange timeout flag, read in the same round trip
+            LANE_CUDA(cudaMemcpyAsync(stats, net->loss_dev, sizeof(stats), cudaMemcpyDeviceToHost, c->stream));
+            LANE_CUDA(cudaMemcpyAsync(&dev_err, c->error_flag, sizeof(int), cudaMemcpyDeviceToHost, c->stream));
             LANE_CUDA(cudaStreamSynchronize(c->stream));
-            c->check_device_error();
+            if (dev_err) c->check_device_error();  // resets the flag and throws
+            const double loss_sum = stats[0];
+            unsigned long long correct = 0;
+            std::memcpy(&correct, &stats[1], sizeof(correct));
             const float mean_loss = static_cast<float>(loss_sum / static_cast<double>(n));
             const float acc = static_cast<float>(correct) / static_cast<float>(n);
             if (mean_loss_out) mean_loss_out[ran] = mean_loss;
