@@ -762,3 +762,79 @@ print("BUCKETS OK")
     r = subprocess.run([sys.executable, "-c", code], cwd=root, env=env, capture_output=True, text=True,
                        timeout=600)
     assert r.returncode == 0 and "BUCKETS OK" in r.stdout, r.stdout[-2000:] + r.stderr[-3000:]
+
+
+def _random_window_shapes(count=10, seed=20261017):
+    rs = np.random.default_rng(seed)
+    out = []
+    for _ in range(count):
+        F = int(rs.integers(3, 900))
+        H = int(rs.choice([4, 8, 12, 16, 32, 60, 96, 124, 128]))
+        C_ = int(rs.integers(2, 17))
+        n = int(rs.integers(5, 90))
+        steps = int(rs.integers(1, 260))
+        out.append((F, H, C_, n, steps))
+    return out
+
+
+@pytest.mark.parametrize("F,H,C,n,steps", _random_window_shapes())
+def test_sgd_stream_random_shapes_vs_oracle(lane, fast, F, H, C, n, steps):
+    """Seeded random shapes through the default fused plan (the window kernel
+    for H <= 128): odd feature widths, 2..16 classes, streams shorter and
+    longer than the dataset, against the oracle's per-sample SGD."""
+    X, T = po.synthetic_dataset(F, C, n, 13)
+    eta = 0.01 if F > 100 else 0.05
+    net = lane.build_network(F, [H], C, seed=7, device=fast)
+    orc = po.OracleNet(F, [H], C, seed=7)
+    want_loss = orc.sgd_run(X, T, steps, eta)
+    Xd, Td = upload(fast, X), upload(fast, T)
+    Ld = upload(fast, np.zeros(1, np.float64), np.float64)
+    net.sgd_stream(Xd, Td, n, steps, eta, loss_dev=Ld)
+    fast.sync()
+    loss = np.zeros(1, np.float64)
+    fast.d2h(loss, Ld)
+    assert abs(loss[0] - want_loss) <= 1e-4 * abs(want_loss) + 1e-6
+    for l, layer in enumerate(net.layers):
+        assert_close(layer.weights, orc.get(l, po.W), 2e-4, f"W{l}")
+        assert_close(layer.biases, orc.get(l, po.B), 2e-4, f"b{l}")
+    fast.free(Xd)
+    fast.free(Td)
+    fast.free(Ld)
+
+
+def _random_wide_shapes(count=8, seed=777):
+    rs = np.random.default_rng(seed)
+    out = []
+    for _ in range(count):
+        F = int(rs.integers(8, 400))
+        H = int(rs.choice([200, 256, 384, 512, 1000, 1024, 2048, 3000, 4096, 8192, 12288]))
+        C_ = int(rs.integers(2, 11))
+        n = int(rs.integers(5, 40))
+        steps = int(rs.integers(20, 120))
+        out.append((F, H, C_, n, steps))
+    return out
+
+
+@pytest.mark.parametrize("F,H,C,n,steps", _random_wide_shapes())
+def test_sgd_stream_random_wide_shapes_vs_oracle(lane, fast, F, H, C, n, steps):
+    """Seeded random wide layers through whichever fused plan the library picks
+    (cluster-split window chains, the single-cluster kernel, the grid kernel)."""
+    X, T = po.synthetic_dataset(F, C, n, 17)
+    eta = 1e-3
+    net = lane.build_network(F, [H], C, seed=3, device=fast)
+    assert net.sgd_plan().split()[0] in ("window", "cluster", "grid"), net.sgd_plan()
+    orc = po.OracleNet(F, [H], C, seed=3)
+    want_loss = orc.sgd_run(X, T, steps, eta)
+    Xd, Td = upload(fast, X), upload(fast, T)
+    Ld = upload(fast, np.zeros(1, np.float64), np.float64)
+    net.sgd_stream(Xd, Td, n, steps, eta, loss_dev=Ld)
+    fast.sync()
+    loss = np.zeros(1, np.float64)
+    fast.d2h(loss, Ld)
+    assert abs(loss[0] - want_loss) <= 1e-4 * abs(want_loss) + 1e-6
+    for l, layer in enumerate(net.layers):
+        assert_close(layer.weights, orc.get(l, po.W), 2e-4, f"W{l}")
+        assert_close(layer.biases, orc.get(l, po.B), 2e-4, f"b{l}")
+    fast.free(Xd)
+    fast.free(Td)
+    fast.free(Ld)
