@@ -201,7 +201,8 @@ __global__ void k_momentum_update_all(float4* __restrict__ W, float4* __restrict
                                       float mu) {
     for (size_t e = (size_t)blockIdx.x * blockDim.x + threadIdx.x; e < n4;
          e += (size_t)gridDim.x * blockDim.x) {
-        float4 g = gsum[e], v = DW[e], w = W[e];
+        // plain SGD (mu == 0) never reads the old delta_weights
+        float4 g = gsum[e], v = mu == 0.0f ? make_float4(0.f, 0.f, 0.f, 0.f) : DW[e], w = W[e];
         float* gp = &g.x;
         float* vp = &v.x;
         float* wp = &w.x;
