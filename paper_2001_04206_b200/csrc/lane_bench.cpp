@@ -19,6 +19,7 @@
 #include <map>
 #include <sstream>
 #include <string>
+#include <type_traits>
 #include <vector>
 
 #include "lane_b200/lane.hpp"
@@ -70,6 +71,9 @@ struct ConfigError2 : std::runtime_error {
 
 template <class T>
 T parse_num(const std::string& flag, const std::string& v) {
+    // unsigned options: "-1" would wrap to a huge count (CLI11 rejects it)
+    if (std::is_unsigned<T>::value && v.find('-') != std::string::npos)
+        throw ConfigError2(flag + ": bad value '" + v + "'");
     std::istringstream is(v);
     T x{};
     is >> x;

@@ -35,6 +35,7 @@ def run(*args, timeout=300):
     (("--dataset", IRIS, "--classes", "1"), "invalid network topology"),
     (("--dataset", IRIS, "--eta", "0"), "eta must be positive"),
     (("--dataset", IRIS, "--fc-neurons", "abc"), "bad value"),
+    (("--dataset", IRIS, "--warmup", "-1"), "bad value"),
     (("--dataset", IRIS, "--bogus"), "unknown option"),
 ])
 def test_cli_configuration_errors_exit_2(args, msg):
