@@ -838,3 +838,36 @@ def test_sgd_stream_random_wide_shapes_vs_oracle(lane, fast, F, H, C, n, steps):
     fast.free(Xd)
     fast.free(Td)
     fast.free(Ld)
+
+
+def _random_minibatch_shapes(count=10, seed=4096):
+    rs = np.random.default_rng(seed)
+    out = []
+    for _ in range(count):
+        F = int(rs.choice([7, 33, 64, 130, 256, 515, 1024]))
+        H = [int(rs.choice([5, 64, 96, 129, 256, 384, 640])) for _ in range(int(rs.integers(1, 3)))]
+        C_ = int(rs.integers(2, 17))
+        B = int(rs.choice([1, 3, 16, 64, 100, 256]))
+        mu = float(rs.choice([0.0, 0.9]))
+        out.append((F, H, C_, B, mu))
+    return out
+
+
+@pytest.mark.parametrize("F,H,C,B,mu", _random_minibatch_shapes())
+def test_minibatch_random_shapes_vs_oracle(lane, fast, F, H, C, B, mu):
+    """Seeded random widths and batches through the mini-batch step (tensor-core
+    GEMMs where eligible, SIMT/skinny kernels elsewhere), three steps against
+    the oracle's mini-batch restatement."""
+    X, T = po.synthetic_dataset(F, C, 3 * B, 23)
+    net = lane.build_network(F, H, C, seed=4, device=fast, max_batch=B)
+    orc = po.OracleNet(F, H, C, seed=4)
+    Xd, Td = upload(fast, X), upload(fast, T)
+    for s in range(3):
+        net.minibatch_step(Xd + s * B * F * 4, Td + s * B * C * 4, B, 0.03, mu)
+        orc.minibatch_step(X[s * B:(s + 1) * B], T[s * B:(s + 1) * B], 0.03, mu)
+    for l, layer in enumerate(net.layers):
+        assert_close(layer.weights, orc.get(l, po.W), 1e-5, f"W{l}")
+        assert_close(layer.biases, orc.get(l, po.B), 1e-5, f"b{l}")
+        assert_close(layer.gradients, orc.get(l, po.G), 2e-4, f"G{l}")
+    fast.free(Xd)
+    fast.free(Td)
