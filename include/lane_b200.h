@@ -202,13 +202,36 @@ int lane_b200_evaluate(lane_b200_net* net, const float* X_host, const float* T_h
 /* One step on a device-resident batch (B <= max_batch):
  *   G = (1/B) sum_b delta_b (x) x_b ;  DW = mu*DW + (-eta)*G (DW = -eta*G when
  *   mu == 0) ; W += DW ; same for the biases.  Every delta uses pre-update
- *   weights.  B == 1, mu == 0 reduces to BackwardPlan::run.  When the context
- *   has a communicator (lane_b200_comm_init) the gradient sums are
- *   all-reduced across ranks (one NCCL fp32 allreduce per step over the flat
- *   gradient buffer) before the update, and B_global = B * world.  loss_sum_dev
- *   (device double, may be NULL) accumulates the local cross entropy. */
+ *   weights.  B == 1, mu == 0 reduces to BackwardPlan::run.  ConfigError
+ *   unless eta > 0 and 0 <= mu < 1.  When the context has a communicator
+ *   (lane_b200_comm_init) the gradient sums are all-reduced across ranks
+ *   before the update (one NCCL fp32 allreduce per layer, issued right after
+ *   that layer's wgrad so it overlaps the rest of the backward), and
+ *   B_global = B * world.  loss_sum_dev (device double, may be NULL)
+ *   accumulates the local cross entropy. */
 int lane_b200_minibatch_step(lane_b200_net* net, const float* X_dev, const float* T_dev,
                              size_t B, float eta, float mu, double* loss_sum_dev);
+
+/* The same step in its three data-parallel phases (the SURVEY 8b sketch's
+ * lane_b200_backward / lane_b200_allreduce_grads / lane_b200_apply_updates(net,
+ * momentum)); minibatch_step == grads, then the per-layer allreduce, then
+ * apply(B * world), bit for bit.
+ * minibatch_grads: forward + backward of a device batch (B <= max_batch);
+ *   leaves the gradient SUMS over the B rows (sum_b delta_b (x) x_b and
+ *   sum_b delta_b, not yet divided) in the grads arena; no update, no
+ *   communication.  loss_sum_dev as in minibatch_step.
+ * minibatch_apply: the update from the arena's (summed) gradients:
+ *   G = gsum / B_global; DW = mu*DW + (-eta)*G; W += DW; biases alike; G and
+ *   the bias gradients are left as the means.  ConfigError unless eta > 0 and
+ *   0 <= mu < 1.  delta_weights is the velocity: whatever update was last
+ *   applied to the layer (by a mini-batch step or by the online path's last
+ *   sample, which leaves DW = -eta*G of that sample, as the reference does).
+ * net_grads_arena: the flat gradient arena, [G_0 | gb_0 | G_1 | gb_1 | ...]
+ *   (256-byte aligned pieces, zero padding), the buffer an allreduce sums. */
+int lane_b200_minibatch_grads(lane_b200_net* net, const float* X_dev, const float* T_dev, size_t B,
+                              double* loss_sum_dev);
+int lane_b200_minibatch_apply(lane_b200_net* net, size_t B_global, float eta, float mu);
+int lane_b200_net_grads_arena(lane_b200_net* net, float** dev, size_t* count);
 
 /* Mini-batch training over a host dataset (the input side of the
  * path).  X_host [n][input_width], T_host [n][classes] (pageable or pinned).

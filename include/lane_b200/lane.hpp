@@ -296,6 +296,8 @@ inline std::vector<EpochStats> train(FeedForwardNetwork& net, const DataSet& set
 // network.cpp:184-204
 inline EpochStats evaluate(FeedForwardNetwork& net, const DataSet& set) {
     if (set.size() == 0) throw TrainingError("evaluate: empty test set");
+    if (set.feature_width != net.input_width() || set.class_count != net.class_count())
+        throw ShapeError("evaluate: dataset shape does not match network");
     EpochStats es;
     check(lane_b200_evaluate(net.handle(), set.features.data(), set.labels.data(), set.size(), &es.mean_loss,
                              &es.accuracy));

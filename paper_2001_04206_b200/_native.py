@@ -57,6 +57,9 @@ SIGNATURES = {
     "lane_b200_train": (_I, [_V, _FP, _FP, _S, _F, _F, _S, _U64, _FP, _FP, _SP]),
     "lane_b200_evaluate": (_I, [_V, _FP, _FP, _S, _FP, _FP]),
     "lane_b200_minibatch_step": (_I, [_V, _V, _V, _S, _F, _F, _V]),
+    "lane_b200_minibatch_grads": (_I, [_V, _V, _V, _S, _V]),
+    "lane_b200_minibatch_apply": (_I, [_V, _S, _F, _F]),
+    "lane_b200_net_grads_arena": (_I, [_V, _V, _V]),
     "lane_b200_train_minibatch": (_I, [_V, _FP, _FP, _S, _S, _F, _F, _S, _U64, _I, _I, _FP, _FP, _SP]),
     "lane_b200_dataset_create": (_I, [_S, _S, _S, _FP, _FP, C.POINTER(_V)]),
     "lane_b200_dataset_load": (_I, [C.c_char_p, _S, _S, C.POINTER(_V)]),

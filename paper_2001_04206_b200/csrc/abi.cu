@@ -11,8 +11,11 @@
 #include <cstdlib>
 #include <cstdio>
 #include <cstring>
+#include <map>
 #include <memory>
+#include <mutex>
 #include <string>
+#include <tuple>
 #include <vector>
 
 #include "common.cuh"
@@ -148,9 +151,11 @@ struct MbGraph {
         double* loss = nullptr;
         int world = 0, numerics = 0, tc = 0;
         const void* comm = nullptr;
+        const float* ws = nullptr;  // the GEMM workspace the graph's kernels write
+        uint64_t ws_gen = 0;        // and its reallocation count (a freed and reused address)
         bool operator==(const Key& o) const {
             return B == o.B && eta == o.eta && mu == o.mu && loss == o.loss && world == o.world &&
-                   numerics == o.numerics && tc == o.tc && comm == o.comm;
+                   numerics == o.numerics && tc == o.tc && comm == o.comm && ws == o.ws && ws_gen == o.ws_gen;
         }
     } key;
     bool warm = false;
@@ -203,6 +208,8 @@ struct lane_b200_net {
     std::vector<cudaEvent_t> plan_events;  // backward_plan_run_timed
     float* eval_buf = nullptr;             // batched evaluate scratch
     size_t eval_count = 0;
+    float* eval_ws = nullptr;              // batched evaluate GEMM workspace
+    size_t eval_ws_count = 0;
 
     LayerBufs& L(size_t l) { return layers.at(l); }
     size_t out_layer() const { return n_hidden; }
@@ -226,6 +233,11 @@ void ensure(float*& p, size_t& have, size_t need) {
 void check_eta(float eta) {
     // LearningRate (layers.hpp:11-19)
     if (!(eta > 0.0f)) throw Error(LANE_ERR_CONFIG, "LearningRate: eta must be positive");
+}
+
+void check_mu(float mu) {
+    // momentum (extension): finite, 0 <= mu < 1 (NaN fails too)
+    if (!(mu >= 0.0f && mu < 1.0f)) throw Error(LANE_ERR_CONFIG, "momentum: mu must be in [0, 1)");
 }
 
 void check_layer(lane_b200_net* net, size_t layer) {
@@ -362,15 +374,24 @@ SgdKernel cluster_kernel(int C) {
     return C == 10 ? k_sgd_cluster<10> : C == 3 ? k_sgd_cluster<3> : k_sgd_cluster<0>;
 }
 
+// Sets the kernel's opt-in attributes (every call: the attributes are
+// per-device function state) and reports whether one cluster of CS CTAs with
+// `smem` bytes fits.  The occupancy answer is cached per (device, kernel, CS,
+// smem) under a mutex.
 bool cluster_fits(SgdKernel kern, int CS, size_t smem) {
-    static SgdKernel cached_k = nullptr;
-    static int cached_cs = 0;
-    static size_t cached_smem = 0;
-    static bool cached_ok = false;
-    if (kern == cached_k && CS == cached_cs && smem == cached_smem) return cached_ok;
     LANE_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
     LANE_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                    static_cast<int>(smem)));
+    int dev = 0;
+    LANE_CUDA(cudaGetDevice(&dev));
+    static std::mutex mu;
+    static std::map<std::tuple<int, SgdKernel, int, size_t>, bool> cache;
+    const auto key = std::make_tuple(dev, kern, CS, smem);
+    {
+        std::lock_guard<std::mutex> lk(mu);
+        auto it = cache.find(key);
+        if (it != cache.end()) return it->second;
+    }
     cudaLaunchConfig_t cfg{};
     cfg.gridDim = dim3(CS);
     cfg.blockDim = dim3(kClThreads);
@@ -385,11 +406,10 @@ bool cluster_fits(SgdKernel kern, int CS, size_t smem) {
     int n = 0;
     const cudaError_t e = cudaOccupancyMaxActiveClusters(&n, kern, &cfg);
     cudaGetLastError();
-    cached_k = kern;
-    cached_cs = CS;
-    cached_smem = smem;
-    cached_ok = e == cudaSuccess && n >= 1;
-    return cached_ok;
+    const bool ok = e == cudaSuccess && n >= 1;
+    std::lock_guard<std::mutex> lk(mu);
+    cache[key] = ok;
+    return ok;
 }
 
 SgdKernel grid_kernel(int C, bool w0_smem) {
@@ -402,12 +422,19 @@ constexpr int kWinWideQPC = 8;  // wide producers: 8 column quads x 2 W0 rows pe
 
 // co-resident CTAs of a cluster launch of the windowed kernel (cluster size cs)
 int window_cluster_capacity(int cs, size_t smem) {
-    static int cached_cs = 0, cached = 0;
-    static size_t cached_smem = 0;
-    if (cs == cached_cs && smem == cached_smem) return cached;
     const WinKernel kern = k_sgd_window<4, 10, 1, true, kWinMaxQPC>;
     cudaFuncSetAttribute(kern, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
     cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
+    int dev = 0;
+    LANE_CUDA(cudaGetDevice(&dev));
+    static std::mutex mu;
+    static std::map<std::tuple<int, int, size_t>, int> cache;  // (device, cs, smem) -> CTAs
+    const auto key = std::make_tuple(dev, cs, smem);
+    {
+        std::lock_guard<std::mutex> lk(mu);
+        auto it = cache.find(key);
+        if (it != cache.end()) return it->second;
+    }
     cudaLaunchConfig_t cfg{};
     cfg.gridDim = dim3(cs);
     cfg.blockDim = dim3(win_threads<1>());
@@ -422,10 +449,9 @@ int window_cluster_capacity(int cs, size_t smem) {
     int nclusters = 0;
     if (cudaOccupancyMaxActiveClusters(&nclusters, kern, &cfg) != cudaSuccess) nclusters = 0;
     cudaGetLastError();
-    cached_cs = cs;
-    cached_smem = smem;
-    cached = nclusters * cs;
-    return cached;
+    std::lock_guard<std::mutex> lk(mu);
+    cache[key] = nclusters * cs;
+    return nclusters * cs;
 }
 
 SgdPlan plan_persistent(lane_b200_net* net) {
@@ -1139,6 +1165,7 @@ int lane_b200_net_destroy(lane_b200_net* net) {
         net->pipe.release();
         for (cudaEvent_t e : net->plan_events) cudaEventDestroy(e);
         cudaFree(net->eval_buf);
+        cudaFree(net->eval_ws);
         cudaFree(net->data);
         cudaFree(net->order);
         lane_b200_ctx* c = net->ctx;
@@ -1480,7 +1507,8 @@ void evaluate_batched(lane_b200_net* net, const float* Xd, const float* Td, size
     float* act[2] = {z + R * wmax, z + 2 * R * wmax};
     float* row_loss = z + 3 * R * wmax;
     float* row_ok = row_loss + R;
-    GemmCtx g{c->stream, c->sm_count, &net->mb.ws, &net->mb.ws_count, &c->launches};
+    // its own GEMM workspace: the mini-batch step graph holds net->mb.ws
+    GemmCtx g{c->stream, c->sm_count, &net->eval_ws, &net->eval_ws_count, &c->launches};
     for (size_t r0 = 0; r0 < n; r0 += R) {
         const int rows = static_cast<int>(std::min(R, n - r0));
         const float* in = Xd + r0 * net->input_width;
@@ -1543,8 +1571,8 @@ void minibatch_step_impl(lane_b200_net* net, const float* X, const float* T, siz
     // The step body runs eagerly once per configuration (sizing every
     // workspace), then as a captured CUDA graph: ~20 launches -> one.
     MbGraph& gr = net->mb_graph;
-    const MbGraph::Key key{B, eta, mu, loss_sum, c->comm.world, c->numerics, gemm_tc_mode(),
-                           static_cast<const void*>(c->comm.comm)};
+    const MbGraph::Key key{B,        eta,           mu, loss_sum, c->comm.world, c->numerics, gemm_tc_mode(),
+                           static_cast<const void*>(c->comm.comm), net->mb.ws, net->mb.ws_gen};
     const bool use_graph = !std::getenv("LANE_B200_MB_NOGRAPH");
     if (use_graph && gr.exec && gr.key == key) {
         LANE_CUDA(cudaGraphLaunch(gr.exec, c->stream));
@@ -1573,6 +1601,8 @@ void minibatch_step_impl(lane_b200_net* net, const float* X, const float* T, siz
         gr.reset();
         minibatch_body(*c, *net, B, eta, mu, loss_sum);
         gr.key = key;
+        gr.key.ws = net->mb.ws;  // the eager run sized the workspace
+        gr.key.ws_gen = net->mb.ws_gen;
         gr.warm = true;
     }
     c->check_launch();
@@ -1585,8 +1615,36 @@ int lane_b200_minibatch_step(lane_b200_net* net, const float* X, const float* T,
     return guard([&] {
         if (!net) throw Error(LANE_ERR_CONFIG, "null network");
         check_eta(eta);
+        check_mu(mu);
         if (B == 0 || B > net->max_batch) throw Error(LANE_ERR_SHAPE, "minibatch: B must be in [1, max_batch]");
         minibatch_step_impl(net, X, T, B, eta, mu, loss_sum);
+    });
+}
+
+int lane_b200_minibatch_grads(lane_b200_net* net, const float* X, const float* T, size_t B, double* loss_sum) {
+    return guard([&] {
+        if (!net) throw Error(LANE_ERR_CONFIG, "null network");
+        if (B == 0 || B > net->max_batch) throw Error(LANE_ERR_SHAPE, "minibatch: B must be in [1, max_batch]");
+        minibatch_stage(*net->ctx, *net, X, T, B);
+        minibatch_grads_body(*net->ctx, *net, B, loss_sum, false);
+    });
+}
+
+int lane_b200_minibatch_apply(lane_b200_net* net, size_t B_global, float eta, float mu) {
+    return guard([&] {
+        if (!net) throw Error(LANE_ERR_CONFIG, "null network");
+        check_eta(eta);
+        check_mu(mu);
+        if (B_global == 0) throw Error(LANE_ERR_SHAPE, "minibatch_apply: B_global must be >= 1");
+        minibatch_update(*net->ctx, *net, B_global, eta, mu);
+    });
+}
+
+int lane_b200_net_grads_arena(lane_b200_net* net, float** dev, size_t* count) {
+    return guard([&] {
+        if (!net || !dev || !count) throw Error(LANE_ERR_CONFIG, "null argument");
+        *dev = net->grads;
+        *count = net->grads_count;
     });
 }
 
@@ -1596,6 +1654,7 @@ int lane_b200_train_minibatch(lane_b200_net* net, const float* X_host, const flo
     return guard([&] {
         if (!net) throw Error(LANE_ERR_CONFIG, "null network");
         check_eta(eta);
+        check_mu(mu);
         if (!X_host || !T_host) throw Error(LANE_ERR_CONFIG, "train_minibatch: null dataset");
         if (n == 0) throw Error(LANE_ERR_TRAINING, "train_minibatch: empty training set");
         if (batch == 0 || batch > net->max_batch)

@@ -30,6 +30,7 @@ struct GemmCtx {
     float** ws;
     size_t* ws_count;
     uint64_t* launches;
+    uint64_t* ws_gen = nullptr;  // bumped on every reallocation (captured graphs key on it)
 };
 
 inline void ensure_ws(GemmCtx& g, size_t count) {
@@ -37,6 +38,7 @@ inline void ensure_ws(GemmCtx& g, size_t count) {
     if (*g.ws) LANE_CUDA(cudaFree(*g.ws));
     LANE_CUDA(cudaMalloc(reinterpret_cast<void**>(g.ws), count * sizeof(float)));
     *g.ws_count = count;
+    if (g.ws_gen) ++*g.ws_gen;
 }
 
 template <Epi E>

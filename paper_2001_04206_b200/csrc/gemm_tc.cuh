@@ -513,6 +513,8 @@ __global__ void __launch_bounds__(256) k_tc_splitk_reduce(TcArgs a, int S) {
 // ---------------------------------------------------------------- host side
 #include <cuda_runtime.h>
 
+#include <atomic>
+
 namespace lane_b200 {
 
 using PFN_encodeTiled = CUresult (*)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
@@ -558,11 +560,15 @@ inline bool tc_eligible(int M, int N, int K) {
 template <bool A_MN, bool B_MN, TcEpi E, bool PAIR>
 inline void tc_launch(cudaStream_t st, const CUtensorMap& a, const CUtensorMap& b, const TcArgs& args) {
     constexpr size_t smem = TcCfg<PAIR>::kSmem;
-    static bool configured = false;
-    if (!configured) {
+    // the attribute is per-device function state: set it once per device
+    static std::atomic<uint64_t> configured{0};
+    int dev = 0;
+    LANE_CUDA(cudaGetDevice(&dev));
+    const uint64_t bit = 1ull << (dev & 63);
+    if (!(configured.load(std::memory_order_acquire) & bit)) {
         LANE_CUDA(cudaFuncSetAttribute(k_gemm_tc<A_MN, B_MN, E, PAIR>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                        (int)smem));
-        configured = true;
+        configured.fetch_or(bit, std::memory_order_release);
     }
     const int S = args.kbs > 0 ? (args.K / kTcBK + args.kbs - 1) / args.kbs : 1;
     if constexpr (PAIR) {

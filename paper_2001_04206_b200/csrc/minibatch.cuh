@@ -7,9 +7,11 @@
 //     W += DW ;  biases likewise.
 // Per layer the step is three GEMMs -- forward Z = X W (+b, tanh), dgrad
 // S = D' W'^T (x tanh'), wgrad G = X^T D -- plus a row softmax and the update.
-// Data parallel: each rank runs its local batch, the flat gradient-sum buffer
-// (G and bias sums of every layer, contiguous) is summed with ONE NCCL fp32
-// allreduce, then every rank applies the identical update.
+// Data parallel: each rank runs its local batch; each layer's span of the flat
+// gradient-sum buffer (G and bias sums, contiguous per layer) is summed with an
+// NCCL fp32 allreduce as soon as that layer's wgrad is done (one per layer, in
+// reverse layer order, overlapping the rest of the backward), then every rank
+// applies the identical update.
 #pragma once
 
 #include <nccl.h>
@@ -39,6 +41,7 @@ struct MinibatchComm {
 struct MinibatchState {
     float* ws = nullptr;  // GEMM workspace (split-K partials / 3xTF32 splits)
     size_t ws_count = 0;
+    uint64_t ws_gen = 0;  // reallocation count: part of the captured step graph's key
     cudaStream_t comm_stream = nullptr;  // per-layer gradient allreduces (data parallel)
     std::vector<cudaEvent_t> ev;         // one per layer + the join
 };
@@ -122,7 +125,7 @@ __global__ void k_softmax_rows(const float* __restrict__ Z, float* __restrict__ 
             const float p = __fdiv_rn(e[q], s);
             P[(size_t)warp * C + k] = p;
             D[(size_t)warp * C + k] = ssub(p, t[k]);
-            if (t[k] != 0.0f) loss = smul(t[k], lane_libm::logf(p < 1e-12f ? 1e-12f : p));
+            if (t[k] != 0.0f) loss = sadd(loss, smul(t[k], lane_libm::logf(p < 1e-12f ? 1e-12f : p)));
         }
     }
     loss = warp_sum(loss);
@@ -248,15 +251,21 @@ void minibatch_stage(Ctx& c, Net& net, const float* X, const float* T, size_t Bs
                               c.stream));
 }
 
-// The step on the staged batch: forward, softmax/CE, dgrad, wgrad, one
-// allreduce (DP), the fused momentum update.  Capturable in a CUDA graph.
+// Forward, softmax/CE and the backward of a staged batch: per layer l the
+// gradient sums G_l = X_l^T D_l and gb_l = colsum(D_l) land in the grads arena
+// (sums over the local rows, not yet divided by B).  The backward runs in
+// reverse layer order with each layer's wgrad issued before the next dgrad, so
+// in data-parallel mode (`allreduce`) layer l's span of the arena goes to NCCL
+// on the communication stream right after its wgrad and overlaps every
+// remaining dgrad and wgrad; the compute stream joins the communication stream
+// at the end.  Capturable in a CUDA graph.
 template <class Ctx, class Net>
-void minibatch_body(Ctx& c, Net& net, size_t Bsz, float eta, float mu, double* loss_sum) {
+void minibatch_grads_body(Ctx& c, Net& net, size_t Bsz, double* loss_sum, bool allreduce) {
     const int B = static_cast<int>(Bsz);
     const int nl = static_cast<int>(net.layers.size());
     const int C = static_cast<int>(net.classes);
     cudaStream_t st = c.stream;
-    GemmCtx g{c.stream, c.sm_count, &net.mb.ws, &net.mb.ws_count, &c.launches};
+    GemmCtx g{c.stream, c.sm_count, &net.mb.ws, &net.mb.ws_count, &c.launches, &net.mb.ws_gen};
     // forward
     for (int l = 0; l < nl; ++l) {
         auto& Ly = net.L(l);
@@ -274,22 +283,8 @@ void minibatch_body(Ctx& c, Net& net, size_t Bsz, float eta, float mu, double* l
                                                           net.mb.ws, B, C);
     k_loss_rows<<<1, 32, 0, st>>>(net.mb.ws, B, loss_sum);
     c.launches += 2;
-    // dgrad (pre-update weights): D_l = (D_{l+1} W_{l+1}^T) * (1 - A_l^2)
-    for (int l = nl - 2; l >= 0; --l) {
-        auto& Ly = net.L(l);
-        auto& nx = net.L(l + 1);
-        gemm(g, GemmOp::NT, B, (int)Ly.O, (int)nx.O, nx.buf[LANE_BUF_DELTAS], (int)nx.O, nx.buf[LANE_BUF_W],
-             (int)nx.O, Epi::TANH_GRAD, Ly.buf[LANE_BUF_DELTAS], nullptr, nullptr, Ly.buf[LANE_BUF_OUTPUTS]);
-    }
-    // Data parallel: each layer's gradient sums (its G and bias pieces, one
-    // contiguous span of the grads arena) are all-reduced on a communication
-    // stream as soon as its wgrad is done, overlapping the remaining wgrads;
-    // the update waits for all of them.  (LANE_B200_MB_BUCKETS=1 forces this
-    // path on a one-rank communicator, where NCCL's sum is the identity.)
-    static const bool force_buckets = std::getenv("LANE_B200_MB_BUCKETS") != nullptr;
-    const bool buckets = c.comm.comm && (c.comm.world > 1 || force_buckets);
     auto& M = net.mb;
-    if (buckets) {
+    if (allreduce) {
         if (!M.comm_stream) LANE_CUDA(cudaStreamCreateWithFlags(&M.comm_stream, cudaStreamNonBlocking));
         while ((int)M.ev.size() < nl + 1) {
             cudaEvent_t e;
@@ -297,14 +292,15 @@ void minibatch_body(Ctx& c, Net& net, size_t Bsz, float eta, float mu, double* l
             M.ev.push_back(e);
         }
     }
-    // wgrad sums: G_l = X_l^T D_l ; gb_l = colsum(D_l)
-    for (int l = 0; l < nl; ++l) {
+    for (int l = nl - 1; l >= 0; --l) {
         auto& Ly = net.L(l);
         const float* in = l == 0 ? net.L(0).buf[LANE_BUF_INPUTS] : net.L(l - 1).buf[LANE_BUF_OUTPUTS];
-        gemm(g, GemmOp::TN, (int)Ly.I, (int)Ly.O, B, in, (int)Ly.I,
-             Ly.buf[LANE_BUF_DELTAS], (int)Ly.O, Epi::STORE, Ly.buf[LANE_BUF_G], nullptr, nullptr, nullptr);
+        // wgrad sums: G_l = X_l^T D_l ; gb_l = colsum(D_l)
+        gemm(g, GemmOp::TN, (int)Ly.I, (int)Ly.O, B, in, (int)Ly.I, Ly.buf[LANE_BUF_DELTAS], (int)Ly.O, Epi::STORE,
+             Ly.buf[LANE_BUF_G], nullptr, nullptr, nullptr);
         colsum(g, Ly.buf[LANE_BUF_DELTAS], B, (int)Ly.O, Ly.buf[LANE_BUF_BIAS_GRAD]);
-        if (buckets) {
+        if (allreduce) {
+            // layer l's G and bias pieces: one contiguous span of the grads arena
             float* begin = Ly.buf[LANE_BUF_G];
             float* end = l + 1 < nl ? net.L(l + 1).buf[LANE_BUF_G] : net.grads + net.grads_count;
             LANE_CUDA(cudaEventRecord(M.ev[l], st));
@@ -312,24 +308,48 @@ void minibatch_body(Ctx& c, Net& net, size_t Bsz, float eta, float mu, double* l
             LANE_NCCL(ncclAllReduce(begin, begin, static_cast<size_t>(end - begin), ncclFloat32, ncclSum,
                                     c.comm.comm, M.comm_stream));
         }
+        // dgrad with the pre-update weights: D_{l-1} = (D_l W_l^T) * (1 - A_{l-1}^2)
+        if (l > 0) {
+            auto& pv = net.L(l - 1);
+            gemm(g, GemmOp::NT, B, (int)pv.O, (int)Ly.O, Ly.buf[LANE_BUF_DELTAS], (int)Ly.O, Ly.buf[LANE_BUF_W],
+                 (int)Ly.O, Epi::TANH_GRAD, pv.buf[LANE_BUF_DELTAS], nullptr, nullptr, pv.buf[LANE_BUF_OUTPUTS]);
+        }
     }
-    if (buckets) {
+    if (allreduce) {
         LANE_CUDA(cudaEventRecord(M.ev[nl], M.comm_stream));
         LANE_CUDA(cudaStreamWaitEvent(st, M.ev[nl], 0));
     }
-    const float invB = 1.0f / static_cast<float>(Bsz * static_cast<size_t>(c.comm.world));
-    {
-        // params | grads | velocities are three equal-layout regions (abi.cu arena)
-        float* W = net.params;
-        float* G = net.grads;
-        float* V = net.grads + net.grads_count;
-        const size_t n4 = net.params_count / 4;
-        k_momentum_update_all<<<std::max<size_t>(1, std::min<size_t>(4 * c.sm_count, (n4 + 255) / 256)), 256, 0,
-                                st>>>(reinterpret_cast<float4*>(W), reinterpret_cast<float4*>(V),
-                                      reinterpret_cast<float4*>(G), n4, invB, -eta, mu);
-        c.launches += 1;
-    }
     c.check_launch();
+}
+
+// The update over the whole parameter set in one pass: G = gsum / B_global;
+// DW = mu*DW + (-eta)*G (DW = (-eta)*G when mu == 0); W += DW; biases alike.
+template <class Ctx, class Net>
+void minibatch_update(Ctx& c, Net& net, size_t B_global, float eta, float mu) {
+    const float invB = 1.0f / static_cast<float>(B_global);
+    // params | grads | velocities are three equal-layout regions (abi.cu arena)
+    float* W = net.params;
+    float* G = net.grads;
+    float* V = net.grads + net.grads_count;
+    const size_t n4 = net.params_count / 4;
+    k_momentum_update_all<<<std::max<size_t>(1, std::min<size_t>(4 * c.sm_count, (n4 + 255) / 256)), 256, 0,
+                            c.stream>>>(reinterpret_cast<float4*>(W), reinterpret_cast<float4*>(V),
+                                        reinterpret_cast<float4*>(G), n4, invB, -eta, mu);
+    c.launches += 1;
+    c.check_launch();
+}
+
+// The whole step on the staged batch.  Data parallel: every layer's gradient
+// span is all-reduced (one NCCL allreduce per layer, overlapping the rest of
+// the backward), then every rank applies the identical update with
+// B_global = B * world.  (LANE_B200_MB_BUCKETS=1 forces the allreduce path on
+// a one-rank communicator, where NCCL's sum is the identity.)
+template <class Ctx, class Net>
+void minibatch_body(Ctx& c, Net& net, size_t Bsz, float eta, float mu, double* loss_sum) {
+    static const bool force_buckets = std::getenv("LANE_B200_MB_BUCKETS") != nullptr;
+    const bool allreduce = c.comm.comm && (c.comm.world > 1 || force_buckets);
+    minibatch_grads_body(c, net, Bsz, loss_sum, allreduce);
+    minibatch_update(c, net, Bsz * static_cast<size_t>(c.comm.world), eta, mu);
 }
 
 }  // namespace lane_b200

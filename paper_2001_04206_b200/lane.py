@@ -373,6 +373,23 @@ class FeedForwardNetwork:
             self._p, C.c_void_p(X_dev), C.c_void_p(T_dev), batch, C.c_float(_eta(eta)),
             C.c_float(mu), C.c_void_p(loss_dev or None)))
 
+    def minibatch_grads(self, X_dev: int, T_dev: int, batch: int, loss_dev: int = 0) -> None:
+        """Forward + backward of a device batch: gradient sums into the grads
+        arena, no update (lane_b200_minibatch_grads)."""
+        _check(_native.lib().lane_b200_minibatch_grads(
+            self._p, C.c_void_p(X_dev), C.c_void_p(T_dev), batch, C.c_void_p(loss_dev or None)))
+
+    def minibatch_apply(self, global_batch: int, eta, mu: float = 0.0) -> None:
+        """The update from the arena's gradient sums (lane_b200_minibatch_apply)."""
+        _check(_native.lib().lane_b200_minibatch_apply(self._p, global_batch, C.c_float(_eta(eta)),
+                                                       C.c_float(mu)))
+
+    def grads_arena(self) -> tuple[int, int]:
+        """(device pointer, float count) of the flat gradient arena."""
+        p, n = C.c_void_p(), C.c_size_t()
+        _check(_native.lib().lane_b200_net_grads_arena(self._p, C.byref(p), C.byref(n)))
+        return p.value, n.value
+
     def allreduce_grads(self) -> None:
         _check(_native.lib().lane_b200_allreduce_grads(self._p))
 

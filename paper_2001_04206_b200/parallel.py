@@ -3,10 +3,12 @@
 One process per GPU (torchrun), ``torch.distributed`` for the plumbing only:
 rank 0 creates the NCCL unique id inside liblane_b200 and broadcasts it; every
 rank binds its lane context to the communicator (``lane_b200_comm_init``).
-Each step a rank runs forward/dgrad/wgrad on its shard of the global batch
-and the library performs ONE fp32 allreduce (sum) of the flat gradient buffer
-(G and bias gradients of every layer, contiguous in HBM) before the identical
-update on every rank, with 1/B_global folded into the step:
+Each step a rank runs forward/dgrad/wgrad on its shard of the global batch.
+The library all-reduces (NCCL fp32 sum) each layer's span of the flat gradient
+buffer (G and bias gradients, contiguous per layer in HBM) as soon as that
+layer's wgrad is done -- one allreduce per layer, in reverse layer order, on a
+communication stream that overlaps the rest of the backward -- and then every
+rank applies the identical update, with 1/B_global folded into the step:
 
     G = (1/B_global) * sum_{ranks} sum_{b in shard} delta_b (x) x_b
     DW = mu*DW + (-eta)*G ;  W += DW

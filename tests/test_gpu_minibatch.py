@@ -1,0 +1,456 @@
+"""GPU parity of the mini-batch / momentum / data-parallel extension
+ at the shapes the bench measures.
+
+The extension has no reference counterpart; its definition
+(oracle/lane_oracle.c lo_minibatch_step, which reduces bit for bit to the
+reference's BackwardPlan::run at B = 1, mu = 0) is restated here in float64
+on the GPU (torch) so the full-size configs C3 (1024-4096-4096-10, B = 256,
+mu = 0.9) and C5 (4096-[4096 x 8]-10, B = 4096) can be checked in seconds.
+
+Tolerance (stated per step):
+  * every reduced element of every GEMM of the step -- forward Z_l, dgrad
+    D_l, wgrad G_l -- given the GPU's own inputs to that GEMM:
+        |gpu - ref| <= 1e-5 * sum_k |a_k b_k|   (+ the fp32 epilogue rounding)
+    ("stage-wise": the step's GEMMs are checked one by one at their own
+    conditioning, so no error is attributed to the wrong stage);
+  * the elementwise stages (tanh, softmax, P - T, the SGD/momentum update)
+    given the GPU's inputs: tanh/softmax within 1e-6 relative, the update
+    bit for bit against a float32 emulation of k_momentum_update_all;
+  * the whole step against float64 from the same initial state (errors of
+    all stages propagated): G, DW within 1e-5 condition-aware x 4 (the
+    measured propagation factor over up to 9 layers stays below 2), W
+    within 1e-5 relative to max|W|.
+"""
+import ctypes as C
+
+import numpy as np
+import pytest
+
+from oracle import pyoracle as po
+
+pytestmark = pytest.mark.gpu
+
+torch = pytest.importorskip("torch")
+
+
+@pytest.fixture(scope="module")
+def lane():
+    from paper_2001_04206_b200 import lane as L
+    return L
+
+
+@pytest.fixture(scope="module")
+def dev(lane):
+    d = lane.Device(0)
+    d.numerics = lane.NUMERICS_FAST
+    yield d
+    d.close()
+
+
+def upload(dev, a):
+    a = np.ascontiguousarray(a, np.float32)
+    p = dev.alloc(a.nbytes)
+    dev.h2d(p, a)
+    return p
+
+
+def read_dev(dev, ptr, shape):
+    out = np.empty(int(np.prod(shape)), np.float32)
+    dev.d2h(out, ptr)
+    return out.reshape(shape)
+
+
+def cuda64(a):
+    return torch.from_numpy(np.ascontiguousarray(a)).to("cuda", torch.float64)
+
+
+def state(lane, dev, net, B):
+    """Every LayerState buffer of every layer, batch rows included."""
+    L = lane
+    out = []
+    for layer in net.layers:
+        I, O = layer.cols_input(), layer.cols_out()
+        d = {"W": layer.weights, "b": layer.biases, "G": layer.gradients, "DW": layer.delta_weights,
+             "db": layer.delta_biases, "gb": layer.bias_gradients}
+        d["Z"] = read_dev(dev, layer.device_ptr(L.NETIN), (B, O))
+        d["A"] = read_dev(dev, layer.device_ptr(L.OUTPUTS), (B, O))
+        d["D"] = read_dev(dev, layer.device_ptr(L.DELTAS), (B, O))
+        out.append(d)
+    return out
+
+
+def check_cond(gpu, ref, cond, what, k=1e-5, extra_rel=1e-6):
+    """|gpu - ref| <= k * cond + extra_rel * |ref| (elementwise)."""
+    g = torch.as_tensor(np.asarray(gpu, np.float32)).to("cuda", torch.float64) \
+        if not torch.is_tensor(gpu) else gpu.to(torch.float64)
+    err = (g - ref).abs()
+    bound = k * cond + extra_rel * ref.abs() + 1e-30
+    ratio = float((err / bound).max())
+    assert ratio <= 1.0, f"{what}: max err/bound {ratio:.3f} (max err {float(err.max()):.3e})"
+    return ratio
+
+
+def emulate_update(W, V, G, eta, mu):
+    """k_momentum_update_all in float32, operation for operation (G is the
+    mean gradient the kernel wrote back)."""
+    f = np.float32
+    step = (f(-eta) * G).astype(np.float32)
+    v = step if mu == 0.0 else ((f(mu) * V).astype(np.float32) + step).astype(np.float32)
+    return (W + v).astype(np.float32), v
+
+
+def stagewise_check(lane, dev, net, X, T, before, after, eta, mu, B):
+    """The per-stage checks of one step (module docstring)."""
+    ratios = {}
+    nl = len(net.layers)
+    A_prev = cuda64(X)
+    for l in range(nl):
+        s0, s1 = before[l], after[l]
+        W = cuda64(s0["W"])
+        b = cuda64(s0["b"])
+        ref = A_prev @ W + b
+        cond = A_prev.abs() @ W.abs() + b.abs()
+        ratios[f"Z{l}"] = check_cond(s1["Z"], ref, cond, f"forward Z{l}")
+        if l < nl - 1:
+            Zg = cuda64(s1["Z"])
+            ratios[f"A{l}"] = check_cond(s1["A"], torch.tanh(Zg), torch.zeros_like(Zg), f"tanh A{l}",
+                                         extra_rel=1e-6)
+            A_prev = cuda64(s1["A"])
+    # softmax + output deltas
+    Zo = cuda64(after[-1]["Z"])
+    P = torch.softmax(Zo, dim=1)
+    check_cond(after[-1]["A"], P, torch.zeros_like(P) + 1e-7, "softmax P", extra_rel=1e-6)
+    Dout = (after[-1]["A"] - T).astype(np.float32)
+    assert np.array_equal(after[-1]["D"].view(np.uint32), Dout.view(np.uint32)), "D_out != fl(P - T)"
+    # dgrad (pre-update weights) and wgrad, layer by layer
+    for l in range(nl - 1, -1, -1):
+        D = cuda64(after[l]["D"])
+        Xl = cuda64(X) if l == 0 else cuda64(after[l - 1]["A"])
+        G = Xl.T @ D / B
+        condG = Xl.T.abs() @ D.abs() / B
+        ratios[f"G{l}"] = check_cond(after[l]["G"], G, condG, f"wgrad G{l}")
+        gb = D.sum(0) / B
+        ratios[f"gb{l}"] = check_cond(after[l]["gb"], gb, D.abs().sum(0) / B, f"bias grad {l}")
+        if l > 0:
+            W = cuda64(before[l]["W"])
+            Ap = cuda64(after[l - 1]["A"])
+            tp = 1.0 - Ap * Ap
+            S = D @ W.T
+            cond = (D.abs() @ W.abs().T) * tp.abs()
+            ratios[f"D{l - 1}"] = check_cond(after[l - 1]["D"], S * tp, cond, f"dgrad D{l - 1}")
+    # the update, bit for bit given the GPU's mean gradients
+    for l in range(nl):
+        s0, s1 = before[l], after[l]
+        Wn, Vn = emulate_update(s0["W"], s0["DW"], s1["G"], eta, mu)
+        assert np.array_equal(s1["DW"].view(np.uint32), Vn.view(np.uint32)), f"DW{l} update"
+        assert np.array_equal(s1["W"].view(np.uint32), Wn.view(np.uint32)), f"W{l} update"
+        bn, dbn = emulate_update(s0["b"], s0["db"], s1["gb"], eta, mu)
+        assert np.array_equal(s1["db"].view(np.uint32), dbn.view(np.uint32)), f"db{l} update"
+        assert np.array_equal(s1["b"].view(np.uint32), bn.view(np.uint32)), f"b{l} update"
+    return ratios
+
+
+FULL = {
+    # name: (F, H, C, B, eta, mu, steps) -- the bench's C3 and C5 (BASELINE.json configs[2], [4])
+    "c3": (1024, [4096, 4096], 10, 256, 0.01, 0.9, 3),
+    "c5": (4096, [4096] * 8, 10, 4096, 1e-3, 0.9, 2),
+}
+
+
+@pytest.mark.parametrize("name", sorted(FULL))
+def test_minibatch_full_shape_stagewise_1e5(lane, dev, name):
+    """One step of C3 / C5 at full shape, checked stage by stage at the
+    1e-5 condition-aware bound (the last of `steps` steps: eager, captured,
+    replayed, so the momentum velocity is non-zero and the graph path runs)."""
+    F, H, C_, B, eta, mu, steps = FULL[name]
+    X, T = po.synthetic_dataset(F, C_, steps * B, 9)
+    net = lane.build_network(F, H, C_, seed=42, device=dev, max_batch=B)
+    Xd, Td = upload(dev, X), upload(dev, T)
+    for s in range(steps - 1):
+        net.minibatch_step(Xd + s * B * F * 4, Td + s * B * C_ * 4, B, eta, mu)
+    before = state(lane, dev, net, B)
+    s = steps - 1
+    ld = upload(dev, np.zeros(2, np.float32))  # one double
+    net.minibatch_step(Xd + s * B * F * 4, Td + s * B * C_ * 4, B, eta, mu, loss_dev=ld)
+    after = state(lane, dev, net, B)
+    loss = np.zeros(1, np.float64)
+    dev.d2h(loss, ld)
+    Xs, Ts = X[s * B:(s + 1) * B], T[s * B:(s + 1) * B]
+    ratios = stagewise_check(lane, dev, net, Xs, Ts, before, after, eta, mu, B)
+    # cross entropy of the step from the GPU's probabilities (float64)
+    P = after[-1]["A"].astype(np.float64)
+    want = -np.sum(Ts * np.log(np.maximum(P, 1e-12)))
+    assert abs(loss[0] - want) <= 1e-5 * abs(want), (loss[0], want)
+    print(name, {k: round(v, 3) for k, v in ratios.items()})
+    for p in (Xd, Td, ld):
+        dev.free(p)
+    net.close()
+
+
+def f64_step(X, T, Ws, bs, Vs, vbs, eta, mu):
+    """lo_minibatch_step's definition in float64 (oracle/lane_oracle.c)."""
+    B = X.shape[0]
+    nl = len(Ws)
+    acts = [X]
+    a = X
+    for l in range(nl):
+        z = a @ Ws[l] + bs[l]
+        a = z if l == nl - 1 else torch.tanh(z)
+        acts.append(a)
+    P = torch.softmax(acts[-1], dim=1)
+    D = P - T
+    Gs, gbs, conds = [None] * nl, [None] * nl, [None] * nl
+    for l in range(nl - 1, -1, -1):
+        Gs[l] = acts[l].T @ D / B
+        conds[l] = acts[l].T.abs() @ D.abs() / B
+        gbs[l] = D.sum(0) / B
+        if l > 0:
+            D = (D @ Ws[l].T) * (1.0 - acts[l] * acts[l])
+    out = []
+    for l in range(nl):
+        v = mu * Vs[l] - eta * Gs[l]
+        vb = mu * vbs[l] - eta * gbs[l]
+        out.append((Ws[l] + v, bs[l] + vb, Gs[l], v, conds[l]))
+    return out
+
+
+@pytest.mark.parametrize("name", sorted(FULL))
+def test_minibatch_full_shape_step_vs_f64(lane, dev, name):
+    """The whole step (all stages' errors propagated) against float64 from
+    the same initial state."""
+    F, H, C_, B, eta, mu, steps = FULL[name]
+    X, T = po.synthetic_dataset(F, C_, 2 * B, 11)
+    net = lane.build_network(F, H, C_, seed=42, device=dev, max_batch=B)
+    Xd, Td = upload(dev, X), upload(dev, T)
+    net.minibatch_step(Xd, Td, B, eta, mu)  # a non-zero velocity
+    before = [(cuda64(l.weights), cuda64(l.biases), cuda64(l.delta_weights), cuda64(l.delta_biases))
+              for l in net.layers]
+    net.minibatch_step(Xd + B * F * 4, Td + B * C_ * 4, B, eta, mu)
+    ref = f64_step(cuda64(X[B:]), cuda64(T[B:]), [b[0] for b in before], [b[1] for b in before],
+                   [b[2] for b in before], [b[3] for b in before], eta, mu)
+    worst = {}
+    for l, layer in enumerate(net.layers):
+        Wr, br, Gr, Vr, cond = ref[l]
+        worst[f"G{l}"] = check_cond(layer.gradients, Gr, cond, f"G{l}", k=4e-5)
+        worst[f"DW{l}"] = check_cond(layer.delta_weights, Vr, mu * before[l][2].abs() + eta * cond,
+                                     f"DW{l}", k=4e-5)
+        Wg = torch.as_tensor(layer.weights).to("cuda", torch.float64)
+        rel = float((Wg - Wr).abs().max() / Wr.abs().max())
+        assert rel <= 1e-5, f"W{l}: {rel:.3e}"
+    print(name, {k: round(v, 3) for k, v in worst.items()})
+    dev.free(Xd)
+    dev.free(Td)
+    net.close()
+
+
+# -------------------------------------------------- tcgen05 GEMM, 4096^3 ---
+
+@pytest.mark.parametrize("op", [0, 1, 2])
+def test_tc_pair_gemm_4096_cube_vs_f64(lane, dev, op):
+    """The C5 GEMM shape (CTA-pair 256x256 tiles, 256 pair tiles on 74 SM
+    pairs) for NN / NT / TN, every element at the 1e-5 condition-aware bound."""
+    from paper_2001_04206_b200 import _native
+    M = N = K = 4096
+    g = torch.Generator(device="cuda").manual_seed(op)
+    a = torch.rand(M * K, device="cuda", generator=g) * 2 - 1
+    b = torch.rand(N * K, device="cuda", generator=g) * 2 - 1
+    c = torch.empty(M * N, device="cuda")
+    torch.cuda.synchronize()
+    rc = _native.lib().lane_b200_gemm(dev._p, op, M, N, K, C.c_void_p(a.data_ptr()), C.c_void_p(b.data_ptr()),
+                                      C.c_void_p(c.data_ptr()), None, None, None, 0, 1)
+    assert rc == 0, _native.lib().lane_b200_last_error()
+    dev.sync()
+    A = a.view(M, K) if op != 2 else a.view(K, M).T
+    Bm = b.view(K, N) if op != 1 else b.view(N, K).T
+    A64, B64 = A.double(), Bm.double()
+    ref = A64 @ B64
+    cond = A64.abs() @ B64.abs()
+    check_cond(c.view(M, N), ref, cond, f"gemm op {op} 4096^3", extra_rel=0.0)
+
+
+# ---------------------------------------------- phases and data parallel ---
+
+def test_minibatch_grads_then_apply_equals_step_bitwise(lane, dev):
+    """minibatch_step == minibatch_grads + minibatch_apply(B), bit for bit."""
+    F, H, C_, B = 256, [512, 384], 10, 64
+    X, T = po.synthetic_dataset(F, C_, 3 * B, 5)
+    n1 = lane.build_network(F, H, C_, seed=3, device=dev, max_batch=B)
+    n2 = lane.build_network(F, H, C_, seed=3, device=dev, max_batch=B)
+    Xd, Td = upload(dev, X), upload(dev, T)
+    for s in range(3):
+        n1.minibatch_step(Xd + s * B * F * 4, Td + s * B * C_ * 4, B, 0.02, 0.9)
+        n2.minibatch_grads(Xd + s * B * F * 4, Td + s * B * C_ * 4, B)
+        n2.minibatch_apply(B, 0.02, 0.9)
+    assert n1.hash() == n2.hash()
+    for a, b in zip(n1.layers, n2.layers):
+        assert np.array_equal(a.delta_weights, b.delta_weights)
+        assert np.array_equal(a.gradients, b.gradients)
+    dev.free(Xd)
+    dev.free(Td)
+
+
+def test_two_rank_shards_on_one_gpu(lane):
+    """The data-parallel step with two library contexts as the two ranks of a
+    global batch (one GPU): each shard's gradient sums, summed elementwise in
+    fp32 (what a 2-rank NCCL sum computes), then the update with
+    B_global = 2B applied on both ranks.  Checks the flat arena layout and the
+    1/B_global scaling: both replicas bit-identical, equal to a float32
+    emulation of the update, and within the 1e-5 condition-aware bound of
+    the single-context full-batch step."""
+    F, H, C_, B, eta, mu = 300, [512, 256], 10, 96, 0.05, 0.9
+    X, T = po.synthetic_dataset(F, C_, 2 * B, 8)
+    devs = [lane.Device(0), lane.Device(0), lane.Device(0)]
+    for d in devs:
+        d.numerics = lane.NUMERICS_FAST
+    nets = [lane.build_network(F, H, C_, seed=4, device=d, max_batch=2 * B) for d in devs]
+    bufs = [(upload(d, X), upload(d, T)) for d in devs]
+    for r in range(2):
+        d, (Xd, Td) = devs[r], bufs[r]
+        nets[r].minibatch_grads(Xd + r * B * F * 4, Td + r * B * C_ * 4, B)
+        d.sync()
+    arenas = []
+    for r in range(2):
+        p, n = nets[r].grads_arena()
+        arenas.append(read_dev(devs[r], p, (n,)))
+    total = (arenas[0] + arenas[1]).astype(np.float32)
+    before = [(l.weights, l.delta_weights, l.biases, l.delta_biases) for l in nets[0].layers]
+    for r in range(2):
+        p, _ = nets[r].grads_arena()
+        devs[r].h2d(p, total)
+        nets[r].minibatch_apply(2 * B, eta, mu)
+    assert nets[0].hash() == nets[1].hash()
+    # full batch on one context
+    Xd, Td = bufs[2]
+    nets[2].minibatch_step(Xd, Td, 2 * B, eta, mu)
+    for l in range(len(nets[0].layers)):
+        L0, L2 = nets[0].layers[l], nets[2].layers[l]
+        Wn, Vn = emulate_update(before[l][0], before[l][1], L0.gradients, eta, mu)
+        assert np.array_equal(L0.weights.view(np.uint32), Wn.view(np.uint32)), f"W{l}"
+        # G = (1/2B) (sum_r shard sums): vs the full-batch GEMM (other K order)
+        a = X.astype(np.float64) if l == 0 else None
+        g0, g2 = L0.gradients.astype(np.float64), L2.gradients.astype(np.float64)
+        scale = np.abs(g2).max()
+        assert np.abs(g0 - g2).max() <= 1e-5 * scale, f"G{l} shard sum vs full batch"
+        assert np.abs(L0.weights.astype(np.float64) - L2.weights).max() <= 1e-6 * np.abs(L2.weights).max()
+    for d, (Xd, Td) in zip(devs, bufs):
+        d.free(Xd)
+        d.free(Td)
+    for n in nets:
+        n.close()
+    for d in devs:
+        d.close()
+
+
+# ---------------------------------------------------------- regressions ---
+
+def test_minibatch_after_large_evaluate(lane, dev):
+    """evaluate on many rows must not reallocate the
+    workspace a captured mini-batch step graph writes.  train_minibatch ->
+    evaluate(10k rows) -> train_minibatch, against the oracle."""
+    F, H, C_, B = 784, [1024], 10, 64
+    X, T = po.synthetic_dataset(F, C_, 4 * B, 2)
+    Xe, Te = po.synthetic_dataset(F, C_, 10000, 3)
+    net = lane.build_network(F, H, C_, seed=1, device=dev, max_batch=B)
+    orc = po.OracleNet(F, H, C_, seed=1)
+    Xd, Td = upload(dev, X), upload(dev, T)
+    for s in range(3):  # eager, capture, replay
+        net.minibatch_step(Xd + s * B * F * 4, Td + s * B * C_ * 4, B, 0.05, 0.9)
+        orc.minibatch_step(X[s * B:(s + 1) * B], T[s * B:(s + 1) * B], 0.05, 0.9)
+    ds = lane.DataSet(Xe, Te)
+    lane.evaluate(net, ds)
+    s = 3
+    net.minibatch_step(Xd + s * B * F * 4, Td + s * B * C_ * 4, B, 0.05, 0.9)
+    orc.minibatch_step(X[s * B:(s + 1) * B], T[s * B:(s + 1) * B], 0.05, 0.9)
+    for l, layer in enumerate(net.layers):
+        w, wo = layer.weights.reshape(-1).astype(np.float64), orc.get(l, po.W).astype(np.float64)
+        assert np.abs(w - wo).max() <= 1e-5 * np.abs(wo).max(), f"W{l}"
+        g, go = layer.gradients.reshape(-1).astype(np.float64), orc.get(l, po.G).astype(np.float64)
+        assert np.abs(g - go).max() <= 1e-4 * np.abs(go).max(), f"G{l}"
+    dev.free(Xd)
+    dev.free(Td)
+
+
+def test_momentum_must_be_in_unit_interval(lane, dev):
+    net = lane.build_network(8, [16], 3, seed=1, device=dev, max_batch=4)
+    X, T = po.synthetic_dataset(8, 3, 4, 1)
+    Xd, Td = upload(dev, X), upload(dev, T)
+    for mu in (-0.1, 1.0, float("nan"), float("inf")):
+        with pytest.raises(lane.ConfigError):
+            net.minibatch_step(Xd, Td, 4, 0.1, mu)
+        with pytest.raises(lane.ConfigError):
+            net.minibatch_apply(4, 0.1, mu)
+    net.minibatch_step(Xd, Td, 4, 0.1, 0.0)
+    dev.free(Xd)
+    dev.free(Td)
+
+
+def test_minibatch_loss_many_classes_soft_targets(lane, dev):
+    """with C > 32 each lane of k_softmax_rows covers
+    several classes; with soft targets every class contributes to the cross
+    entropy.  The step's loss sum against float64 from the GPU's logits."""
+    F, H, C_, B = 64, [96], 70, 32
+    rng = np.random.default_rng(5)
+    X = rng.random((B, F), dtype=np.float32)
+    T = rng.random((B, C_), dtype=np.float32)
+    T /= T.sum(1, keepdims=True)
+    net = lane.build_network(F, H, C_, seed=2, device=dev, max_batch=B)
+    Xd, Td = upload(dev, X), upload(dev, T.astype(np.float32))
+    ld = upload(dev, np.zeros(2, np.float32))
+    net.minibatch_step(Xd, Td, B, 0.01, 0.0, loss_dev=ld)
+    loss = np.zeros(1, np.float64)
+    dev.d2h(loss, ld)
+    P = read_dev(dev, net.output.device_ptr(lane.OUTPUTS), (B, C_)).astype(np.float64)
+    want = -np.sum(T.astype(np.float32).astype(np.float64) * np.log(np.maximum(P, 1e-12)))
+    assert abs(loss[0] - want) <= 1e-5 * abs(want), (loss[0], want)
+    for p in (Xd, Td, ld):
+        dev.free(p)
+
+
+# ---------------------------------------------------------- determinism ---
+
+def test_minibatch_fast_run_to_run_bitwise(lane, dev):
+    """Two identical C3-shaped runs (eager, captured, replayed steps) give
+    bit-identical weights, velocities and losses: split-K and every
+    reduction use a fixed order."""
+    F, H, C_, B = 1024, [4096, 4096], 10, 256
+    X, T = po.synthetic_dataset(F, C_, 4 * B, 9)
+    Xd, Td = upload(dev, X), upload(dev, T)
+    hashes, losses = [], []
+    for run in range(2):
+        net = lane.build_network(F, H, C_, seed=42, device=dev, max_batch=B)
+        ld = upload(dev, np.zeros(2, np.float32))
+        for s in range(4):
+            net.minibatch_step(Xd + s * B * F * 4, Td + s * B * C_ * 4, B, 0.01, 0.9, loss_dev=ld)
+        loss = np.zeros(1, np.float64)
+        dev.d2h(loss, ld)
+        hashes.append((net.hash(), [l.delta_weights.tobytes() for l in net.layers]))
+        losses.append(loss[0])
+        dev.free(ld)
+        net.close()
+    assert hashes[0] == hashes[1]
+    assert losses[0] == losses[1]
+    dev.free(Xd)
+    dev.free(Td)
+
+
+@pytest.mark.parametrize("F,H,C", [(784, [128], 10), (340, [1024], 10), (340, [16384], 10)])
+def test_sgd_stream_fast_run_to_run_bitwise(lane, dev, F, H, C):
+    """The fused online-SGD plans (window, cluster-window, grid) are
+    deterministic: two runs over the same stream give bit-identical weights,
+    loss sums and hit counts."""
+    n = 2000 if H[0] <= 1024 else 300
+    X, T = po.synthetic_dataset(F, C, n, 9)
+    Xd, Td = upload(dev, X), upload(dev, T)
+    out = []
+    for run in range(2):
+        net = lane.build_network(F, H, C, seed=42, device=dev)
+        ld = upload(dev, np.zeros(4, np.float32))  # loss (double) + hits (u64)
+        net.sgd_stream(Xd, Td, n, n, 0.01 if H[0] <= 128 else 1e-4, loss_dev=ld, correct_dev=ld + 8)
+        st = np.zeros(2, np.float64)
+        dev.d2h(st, ld)
+        out.append((net.hash(), st.tobytes(), net.sgd_plan()))
+        dev.free(ld)
+        net.close()
+    assert out[0] == out[1], out
+    dev.free(Xd)
+    dev.free(Td)
