@@ -2,24 +2,28 @@
 """Benchmark of the B200 FC-backprop hot path (contract: see README/DESIGN).
 
     python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
-                    [--workload c2|c1|c4-<H>|c3|c5]
+                    [--workload c5|c3|c2|c1|c4-<H>]
 
-Default workload = BASELINE.json configs[1]: MNIST-shaped MLP 784-128-10,
-online SGD (batch 1) on 1 B200.  One "step" = one pass of online SGD over a
-60,000-sample synthetic epoch (features U[0,1), uniform one-hot labels from
-SeededRng(9) exactly like proj/tests/test_support.hpp; weights from
-build_network(seed 42)); 60,000 x (784+10) x 4 B = 190 MB of inputs, larger
-than the 126 MB L2, streamed from HBM each step.
+Default workload = BASELINE.json configs[4], the config the metric's
+1/2/4/8-GPU numbers are quoted on: the deep MLP 4096-[4096 x 8]-10, mini-batch
+4096 (global), SGD.  One "step" = one global batch through forward, dgrad,
+wgrad (tcgen05 3xTF32 GEMMs) and the update; at N > 1 every rank steps its
+4096/N shard and the gradient sums are all-reduced over NCCL (strong scaling:
+the global batch is fixed).  Inputs: synthetic features U[0,1) and one-hot
+labels from SeededRng(9) exactly like proj/tests/test_support.hpp; weights
+from build_network(seed 42).
 
 value  = samples/s with the inputs resident in HBM (device-timed, CUDA events
-         on the library's stream, max over ranks).
-e2e    = samples/s through the public API (lane.train over host arrays in
-         pinned memory: the epoch streams through the library's input
-         pipeline in chunks -- host gather of the shuffled rows, H2D on a copy
-         stream overlapping the fused kernel on the previous chunk -- then
-         D2H of EpochStats).
-Multi-GPU: online SGD has a strict sample-to-sample dependency, so N>1 runs N
-independent replicas (one per rank, "replicas only").
+         on the library's stream, max over ranks, a 256 MB L2 flush between
+         timed steps).
+e2e    = samples/s through the public API (lane.train_minibatch over pinned
+         host arrays: every step's rows are gathered into a page-locked slot,
+         copied H2D on a copy stream overlapping the previous steps, and every
+         step's loss is read back D2H).
+--gpus N without torchrun re-launches itself under torch.distributed.run
+with N ranks (and fails if fewer than N GPUs are visible); under torchrun
+WORLD_SIZE must equal N.  Batch-1 online SGD (c1, c2, c4-*) has a strict
+sample-to-sample dependency, so N > 1 runs N independent replicas there.
 """
 from __future__ import annotations
 
@@ -87,7 +91,7 @@ class ClockSampler:
         try:
             self.proc = subprocess.Popen(
                 ["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.Q}",
-                 "--format=csv,noheader,nounits", "-lms", "100"],
+                 "--format=csv,noheader,nounits", "-lms", "20"],
                 stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
             self.t = threading.Thread(target=self._read, daemon=True)
             self.t.start()
@@ -149,39 +153,61 @@ def cpu_reference(F, H, C, eta, X, T, samples, warmup, parallel):
 
 
 def run_reference_arm(args, wl):
+    """The reference's own CPU implementation of the path (oracle/_ref: its
+    proj/src/*.cpp, Release flags) on every host core (ParallelHost), timed
+    with its measure() protocol (proj/src/bench.cpp:55-73: forward +
+    BackwardPlan::run per sample).  Rank 0 only under torchrun."""
     rank, world, _ = dist_env()
     if rank != 0:
         return
     from oracle import pyoracle as po
+    cores = os.cpu_count() or 1
     if wl in MINIBATCH:
         # the reference has no mini-batch mode: its per-sample online SGD on the
-        # same network, one sample per step (seconds each on the host cores)
-        F, H, C, eta, _, _, _, desc = MINIBATCH[wl]
+        # same network, one sample per step (seconds each on the host cores);
+        # the network is built once and warmed with one sample (a CPU path
+        # has no state to warm beyond the first pass over the weights)
+        F, H, C, eta, BG, mu, _, desc = MINIBATCH[wl]
         X, T = po.synthetic_dataset(F, C, 4, 9)
         per_step = 1
+        config = {"workload": wl, "description": desc, "layers": [F] + H + [C], "global_batch": BG,
+                  "momentum": mu, "eta": eta, "samples_per_step": per_step,
+                  "mode": "per-sample online SGD (the reference has no mini-batch mode)"}
+        if po.ref_available():
+            net, kind = po.RefNet(F, H, C, seed=42), "reference"
+            net.sgd_bench(X, T, 0, 1, eta, parallel=True, workers=cores)  # warm-up sample
+            rates = [1.0 / net.sgd_bench(X, T, 0, 1, eta, parallel=True, workers=cores)[0]
+                     for _ in range(args.steps)]
+        else:
+            net, kind, cores = po.OracleNet(F, H, C, seed=42), "port", 1
+            net.sgd_run(X, T, 1, eta)
+            rates = []
+            for _ in range(args.steps):
+                t0 = time.perf_counter()
+                net.sgd_run(X, T, 1, eta)
+                rates.append(1.0 / (time.perf_counter() - t0))
     else:
         F, H, C, eta, n_epoch, desc = WORKLOADS[wl]
         X, T = po.synthetic_dataset(F, C, min(n_epoch, 4096), 9)
         per_ms = {"c1": 0.003, "c2": 1.0}.get(wl, 0.6 * (F * H[0] + H[0] * C) / 1e5)
         per_step = max(10, int(4000.0 / per_ms / max(1, args.steps + args.warmup)))  # ~4 s of CPU
         per_step = min(per_step, 100000)
-    cores = os.cpu_count() or 1
-    rates = []
-    kind = "port"
-    for s in range(args.warmup + args.steps):
-        r, kind, used = cpu_reference(F, H, C, eta, X, T, per_step, 0 if wl in MINIBATCH else 2,
-                                      parallel=True)
-        if s >= args.warmup:
-            rates.append(r)
+        config = {"workload": wl, "description": desc, "layers": [F] + H + [C], "batch": 1,
+                  "samples_per_step": per_step, "eta": eta}
+        rates = []
+        kind = "port"
+        for s in range(args.warmup + args.steps):
+            r, kind, cores = cpu_reference(F, H, C, eta, X, T, per_step, 2, parallel=True)
+            if s >= args.warmup:
+                rates.append(r)
     value = float(np.mean(rates))
     line = {"impl": "reference", "metric": METRIC, "value": value, "unit": "samples/s",
             "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
             "ms_per_step": 1000.0 * per_step / value, "higher_is_better": True,
-            "scaling": "weak", "vs_baseline": None, "dtype": "f32", "data": "synthetic",
-            "config": {"workload": wl, "description": desc, "layers": [F] + H + [C],
-                       "batch": 1, "samples_per_step": per_step, "eta": eta},
+            "scaling": "strong" if wl in MINIBATCH else "weak", "vs_baseline": None, "dtype": "f32",
+            "data": "synthetic", "config": config,
             "cpu_baseline": {"value": value, "unit": "samples/s", "cores": cores, "kind": kind,
-                             "sample": f"{per_step} online-SGD samples per step through the "
+                             "sample": f"{per_step} online-SGD sample(s) per step through the "
                                        f"reference's forward + BackwardPlan::run on ParallelHost "
                                        f"({cores} workers)"},
             "e2e": {"value": value, "unit": "samples/s", "h2d_bytes_per_step": 0,
@@ -229,6 +255,33 @@ def dominant_gemm(dev, widths, rows, stream):
     P = sum(i * o for i, o in zip(widths[:-1], widths[1:]))
     step_f = (6 * P - 2 * widths[0] * widths[1]) * rows
     return (tot_f / (tot_ms / 1e3) / 1e12 if tot_ms else None), tot_f / step_f
+
+
+def measure_tf32_peak() -> float:
+    """Dense TF32 TFLOP/s of this GPU as cuBLAS reaches it: fp32 matmul with
+    TF32 tensor cores enabled at 8192^3, best of 10 (CUDA events)."""
+    import torch
+    old = torch.backends.cuda.matmul.allow_tf32
+    torch.backends.cuda.matmul.allow_tf32 = True
+    try:
+        n = 8192
+        a = torch.randn(n, n, device="cuda")
+        b = torch.randn(n, n, device="cuda")
+        c = torch.empty(n, n, device="cuda")
+        for _ in range(3):
+            torch.matmul(a, b, out=c)
+        best = float("inf")
+        for _ in range(10):
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record()
+            torch.matmul(a, b, out=c)
+            e1.record()
+            e1.synchronize()
+            best = min(best, e0.elapsed_time(e1))
+        del a, b, c
+        return 2.0 * n ** 3 / (best / 1e3) / 1e12
+    finally:
+        torch.backends.cuda.matmul.allow_tf32 = old
 
 
 def run_minibatch(args, wl):
@@ -310,45 +363,51 @@ def run_minibatch(args, wl):
     P = sum(a * b for a, b in zip(widths[:-1], widths[1:]))
     P0 = widths[0] * widths[1]
     flops = (6 * P - 2 * P0) * BG  # fwd 2P + wgrad 2P + dgrad 2(P - P0) per sample
-    achieved = flops / (ms / args.steps / 1000.0) / 1e12
+    step_tf = flops / (ms / args.steps / 1000.0) / 1e12
     gemm_tf, gemm_share = dominant_gemm(dev, widths, rows, stream)
-    peaks = json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json"))) if os.path.exists(
-        os.path.join(ROOT, "MEASURED_PEAKS.json")) else {"bf16_tflops": 1590.0}
-    peak = float(peaks.get("bf16_tflops", 1590.0)) / 2.0 / 3.0  # tf32 = bf16/2; 3 MMAs per product
+    # the denominator: this box's dense TF32 rate (cuBLAS fp32 matmul with
+    # TF32 at 8192^3, best of 10), / 3 for the 3 MMAs of a 3xTF32 product
+    tf32 = measure_tf32_peak()
+    peak = tf32 / 3.0
+    nominal = 2250.0 / 2.0 / 3.0  # NVIDIA's dense bf16 2.25 PF/s -> TF32 1.125 -> 3xTF32
     # the step's two sequential phases each have a floor: the GEMMs on the tensor
     # pipe and the update streaming W, V and G (read + write, 24 B/param) from
     # HBM; the next step's forward needs the updated weights, so they add
     hbm_peak, _ = load_peaks()
     n_param = sum(a * b + b for a, b in zip(widths[:-1], widths[1:]))
-    floor_tensor_us = flops / (peak * 1e12) * 1e6
-    floor_update_us = 24.0 * n_param / (hbm_peak * 1e9) * 1e6
+    floor_tensor_us = flops * gemm_share / (peak * 1e12) * 1e6
+    floor_update_us = (24.0 if mu else 20.0) * n_param / (hbm_peak * 1e9) * 1e6
     line = {"metric": METRIC, "value": value, "unit": "samples/s", "n_gpus": world,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms / args.steps,
             "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f32",
             "data": "synthetic",
             "config": {"workload": wl, "description": desc, "layers": widths, "global_batch": BG,
-                       "momentum": mu, "eta": eta, "parallelism": f"dp{world}",
-                       "gemm": "tcgen05 kind::tf32, 3xTF32 (fp32-accurate)",
+                       "rows_per_rank": rows, "momentum": mu, "eta": eta, "parallelism": f"dp{world}",
+                       "gemm": "tcgen05 kind::tf32, 3xTF32 (fp32-accurate, 1e-5 condition-aware)",
                        "l2": "256 MB buffer written between timed steps"},
-            "roofline": {"bound": "tensor", "achieved": achieved, "peak": peak, "unit": "TFLOP/s",
-                         "frac": achieved / peak, "traffic": load_traffic(wl)[0],
-                         "traffic_source": load_traffic(wl)[1],
-                         "scope": "whole step (all kernels incl. the HBM-bound update) / step time",
+            "roofline": {"bound": "tensor", "kernel": "k_gemm_tc", "achieved": gemm_tf, "peak": peak,
+                         "unit": "TFLOP/s", "frac": gemm_tf / peak if gemm_tf else None,
+                         "traffic": load_traffic(wl)[0], "traffic_source": load_traffic(wl)[1],
+                         "how": "the step's tensor-core GEMM shapes (fwd/dgrad/wgrad of the 4096-wide "
+                                "layers) replayed through lane_b200_gemm, CUDA events on the library "
+                                "stream, 10 reps each; algorithmic flops 2MNK per launch",
+                         "peak_kind": "measured: cuBLAS dense TF32 8192^3 on this GPU "
+                                      f"({tf32:.0f} TF/s) / 3 (3xTF32 MMAs per product)",
+                         "frac_of_nominal": gemm_tf / nominal if gemm_tf else None,
+                         "flop_share_of_step": gemm_share,
+                         "step": {"achieved": step_tf, "frac": step_tf / peak,
+                                  "scope": "whole step (every kernel incl. the HBM-bound update) / "
+                                           "step time"},
                          "step_floor": {"tensor_us": floor_tensor_us, "hbm_update_us": floor_update_us,
                                         "frac": (floor_tensor_us + floor_update_us) / (ms / args.steps * 1e3),
-                                        "how": "GEMM flops at the derived 3xTF32 peak + the update's 24 B/param "
-                                               "at the measured HBM peak, against the measured step time"},
-                         "dominant_kernel": {"kernel": "k_gemm_tc", "achieved": gemm_tf, "frac": gemm_tf / peak,
-                                             "flop_share_of_step": gemm_share,
-                                             "how": "the step's tensor-core GEMM shapes (fwd/dgrad/wgrad of "
-                                                    "the 4096-wide layers) replayed through lane_b200_gemm, "
-                                                    "CUDA events on the library stream, 10 reps each"},
-                         "peak_kind": "derived: measured bf16 dense / 2 (tf32) / 3 (3xTF32 MMAs)",
+                                        "how": "GEMM flops at the measured 3xTF32 peak + the update's "
+                                               "20 (SGD) / 24 (momentum) B/param at the measured HBM "
+                                               "peak, against the measured step time"},
                          "algorithmic_flops_per_step": flops},
             "e2e": {"value": e2e, "unit": "samples/s", "h2d_bytes_per_step": rows * (F + C) * 4,
                     "d2h_bytes_per_step": 8},
             "gpu_launches": int(launches), "clocks": clk.summary()}
-    if rank == 0 and not args.no_cpu:
+    if rank == 0 and world == 1 and not args.no_cpu:
         v, kind, cores = cpu_reference(F, H, C, eta, X[:4], T[:4], 1, 0, parallel=True)
         line["cpu_baseline"] = {"value": v, "unit": "samples/s", "cores": cores, "kind": kind,
                                 "sample": "1 sample of per-sample online SGD through the reference "
@@ -398,13 +457,31 @@ def run_paper_table(args):
     print(out.stdout, end="", flush=True)
 
 
+def self_launch(args) -> int:
+    """--gpus N outside torchrun: N ranks under torch.distributed.run on this
+    node (127.0.0.1 rendezvous).  Refuses loudly when fewer than N GPUs are
+    visible instead of silently running one rank."""
+    import socket
+    import torch
+    have = torch.cuda.device_count()
+    if have < args.gpus:
+        print(f"bench.py: --gpus {args.gpus} needs {args.gpus} visible GPUs, found {have}", file=sys.stderr)
+        return 2
+    with socket.socket() as s:
+        s.bind(("127.0.0.1", 0))
+        port = s.getsockname()[1]
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={args.gpus}",
+           "--master-addr", "127.0.0.1", "--master-port", str(port), os.path.abspath(__file__)] + sys.argv[1:]
+    return subprocess.call(cmd)
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
     ap.add_argument("--steps", type=int, default=10)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
-    ap.add_argument("--workload", default="c2", choices=sorted(WORKLOADS) + sorted(MINIBATCH))
+    ap.add_argument("--workload", default="c5", choices=sorted(WORKLOADS) + sorted(MINIBATCH))
     ap.add_argument("--epoch", type=int, default=0, help="override samples per step")
     ap.add_argument("--no-cpu", action="store_true", help="skip the cpu_baseline leg")
     ap.add_argument("--paper-table", action="store_true",
@@ -412,6 +489,12 @@ def main():
     ap.add_argument("--fc-neurons", type=int, default=100000, help="--paper-table hidden width")
     args = ap.parse_args()
     wl = args.workload
+    if args.gpus < 1:
+        raise SystemExit("--gpus must be >= 1")
+    if "WORLD_SIZE" not in os.environ and args.gpus > 1 and not args.paper_table:
+        sys.exit(self_launch(args))
+    if "WORLD_SIZE" in os.environ and int(os.environ["WORLD_SIZE"]) != args.gpus:
+        raise SystemExit(f"bench.py: WORLD_SIZE={os.environ['WORLD_SIZE']} but --gpus {args.gpus}")
     if args.paper_table:
         run_paper_table(args)
         return
@@ -536,7 +619,7 @@ def main():
                     "d2h_bytes_per_step": 8 * 2 + 4},  # EpochStats (loss sum, hits) + the device error flag
             "gpu_launches": int(launches),
             "clocks": clk.summary()}
-    if rank == 0 and not args.no_cpu:
+    if rank == 0 and world == 1 and not args.no_cpu:
         Xs, Ts = X[:2000], T[:2000]
         per_ms = {"c1": 0.003, "c2": 1.0}.get(wl, 0.6 * P / 1e5)
         samples = int(max(20, min(20000, 8000.0 / per_ms)))  # ~8 s of single-core CPU
