@@ -210,6 +210,8 @@ struct lane_b200_net {
     size_t eval_count = 0;
     float* eval_ws = nullptr;              // batched evaluate GEMM workspace
     size_t eval_ws_count = 0;
+    int* eval_counters = nullptr;          // its stream-K tile counters
+    size_t eval_counters_count = 0;
 
     LayerBufs& L(size_t l) { return layers.at(l); }
     size_t out_layer() const { return n_hidden; }
@@ -1166,6 +1168,7 @@ int lane_b200_net_destroy(lane_b200_net* net) {
         for (cudaEvent_t e : net->plan_events) cudaEventDestroy(e);
         cudaFree(net->eval_buf);
         cudaFree(net->eval_ws);
+        cudaFree(net->eval_counters);
         cudaFree(net->data);
         cudaFree(net->order);
         lane_b200_ctx* c = net->ctx;
@@ -1508,7 +1511,8 @@ void evaluate_batched(lane_b200_net* net, const float* Xd, const float* Td, size
     float* row_loss = z + 3 * R * wmax;
     float* row_ok = row_loss + R;
     // its own GEMM workspace: the mini-batch step graph holds net->mb.ws
-    GemmCtx g{c->stream, c->sm_count, &net->eval_ws, &net->eval_ws_count, &c->launches};
+    GemmCtx g{c->stream,      c->sm_count, &net->eval_ws, &net->eval_ws_count, &c->launches, nullptr,
+              &net->eval_counters, &net->eval_counters_count};
     for (size_t r0 = 0; r0 < n; r0 += R) {
         const int rows = static_cast<int>(std::min(R, n - r0));
         const float* in = Xd + r0 * net->input_width;
@@ -1795,19 +1799,25 @@ int lane_b200_gemm(lane_b200_ctx* c, int op, int M, int N, int K, const float* A
             throw Error(LANE_ERR_CONFIG, "lane_b200_gemm: bad op/epilogue/shape");
         static float* ws = nullptr;
         static size_t ws_count = 0;
-        GemmCtx g{c->stream, c->sm_count, &ws, &ws_count, &c->launches};
+        static int* counters = nullptr;
+        static size_t counters_count = 0;
+        GemmCtx g{c->stream, c->sm_count, &ws, &ws_count, &c->launches, nullptr, &counters, &counters_count};
         const GemmOp o = static_cast<GemmOp>(op);
         const int lda = o == GemmOp::TN ? M : K;
         const int ldb = o == GemmOp::NT ? K : N;
-        const int saved = gemm_tc_mode();
+        const int saved = gemm_tc_mode(), saved_p = tc_persist_mode();
         gemm_tc_mode() = use_tc ? 1 : 0;
+        if (use_tc == 2) tc_persist_mode() = 2;  // the persistent stream-K kernel for every shape
+        if (use_tc == 3) tc_persist_mode() = 0;  // never
         try {
             gemm(g, o, M, N, K, A, lda, B, ldb, static_cast<Epi>(epilogue), C, C2, bias, aux);
         } catch (...) {
             gemm_tc_mode() = saved;
+            tc_persist_mode() = saved_p;
             throw;
         }
         gemm_tc_mode() = saved;
+        tc_persist_mode() = saved_p;
         c->check_launch();
     });
 }

@@ -18,6 +18,7 @@
 
 #include "common.cuh"
 #include "gemm_tc.cuh"
+#include "gemm_tcp.cuh"
 
 namespace lane_b200 {
 
@@ -31,6 +32,8 @@ struct GemmCtx {
     size_t* ws_count;
     uint64_t* launches;
     uint64_t* ws_gen = nullptr;  // bumped on every reallocation (captured graphs key on it)
+    int** counters = nullptr;    // stream-K tile arrival counters (zero between launches)
+    size_t* counters_count = nullptr;
 };
 
 inline void ensure_ws(GemmCtx& g, size_t count) {
@@ -39,6 +42,19 @@ inline void ensure_ws(GemmCtx& g, size_t count) {
     LANE_CUDA(cudaMalloc(reinterpret_cast<void**>(g.ws), count * sizeof(float)));
     *g.ws_count = count;
     if (g.ws_gen) ++*g.ws_gen;
+}
+
+// stream-K arrival counters: zeroed once at allocation, reset to zero by the
+// kernel's last arriving piece of every tile
+inline bool ensure_counters(GemmCtx& g, size_t count) {
+    if (!g.counters || !g.counters_count) return false;
+    if (*g.counters_count >= count) return true;
+    if (*g.counters) LANE_CUDA(cudaFree(*g.counters));
+    LANE_CUDA(cudaMalloc(reinterpret_cast<void**>(g.counters), count * sizeof(int)));
+    LANE_CUDA(cudaMemsetAsync(*g.counters, 0, count * sizeof(int), g.stream));
+    *g.counters_count = count;
+    if (g.ws_gen) ++*g.ws_gen;
+    return true;
 }
 
 template <Epi E>
@@ -535,6 +551,28 @@ inline int& gemm_tc_mode() {
     return mode;
 }
 
+// 1 = the persistent stream-K kernel (gemm_tcp.cuh) serves the single-CTA
+// shapes and the short-K wgrads (default); 0 = never; 2 = every shape
+// (lane_b200_gemm's use_tc = 2 / 3 select 2 / 0 for one call)
+inline int& tc_persist_mode() {
+    static int persist = std::getenv("LANE_B200_TC_PERSIST") ? std::atoi(std::getenv("LANE_B200_TC_PERSIST")) : 1;
+    return persist;
+}
+
+// CTA pairs (cta_group::2, 256 x 256 tiles, N = 256 MMAs) for the tall
+// GEMMs: 4096^3 0.596 -> 0.500 ms.  The M = 256 GEMMs stay on single CTAs (a
+// 256-row pair tile leaves 16 tiles for 148 SMs), and the short-K wgrads
+// (K = batch <= 1024) run on the persistent kernel, whose double-buffered
+// accumulators overlap each tile's epilogue with the next tile's MMAs and
+// whose epilogue can carry the fused SGD/momentum update.
+inline bool tc_use_pair(GemmOp op, int M, int N, int K) {
+    static const bool pair_ok = !std::getenv("LANE_B200_TC_NOPAIR");
+    const int persist = tc_persist_mode();
+    if (!pair_ok || persist == 2) return false;
+    if (persist == 1 && op == GemmOp::TN && K <= 1024) return false;
+    return M >= 1024 || (M >= 512 && K >= 2048);
+}
+
 // Tensor-core dispatch (gemm_tc.cuh): returns false when the shape/layout is
 // not eligible (the caller then runs the SIMT kernel).
 inline bool gemm_try_tc(GemmCtx& g, GemmOp op, int M, int N, int K, const float* A, int lda, const float* B,
@@ -544,13 +582,7 @@ inline bool gemm_try_tc(GemmCtx& g, GemmOp op, int M, int N, int K, const float*
         return false;
     CUtensorMap ma, mb;
     bool a_mn = false, b_mn = false;
-    // CTA pairs (cta_group::2, 256 x 256 tiles, N = 256 MMAs) for the tall
-    // GEMMs: 4096^3 0.596 -> 0.500 ms; C3's wgrads (M = 1024 / 4096, K = 256)
-    // 70.6 -> 68.7 and 23.1 -> 20.0 us.  The M = 256 GEMMs stay on single CTAs:
-    // a 256-row pair tile leaves 16 tiles for 148 SMs, and the 4-way split-K it
-    // then needs costs more than the bigger MMAs win (61.8 -> 67.2 us).
-    static const bool pair_ok = !std::getenv("LANE_B200_TC_NOPAIR");
-    const bool pair = pair_ok && (M >= 1024 || (M >= 512 && K >= 2048));
+    const bool pair = tc_use_pair(op, M, N, K);
     switch (op) {
         case GemmOp::NN:  // A [M][K] K-major, B [K][N] MN-major
             if (lda != K || ldb != N) return false;
@@ -569,6 +601,36 @@ inline bool gemm_try_tc(GemmCtx& g, GemmOp op, int M, int N, int K, const float*
             mb = tc_map(B, K, N, 32, 32, 1);
             a_mn = b_mn = true;
             break;
+    }
+    // the persistent kernel (gemm_tcp.cuh) for the short-K wgrads (mode 1) or
+    // every shape (mode 2); the M = batch forward/dgrad GEMMs stay on the
+    // one-tile-per-CTA kernel with split-K, measured faster there (C3
+    // 256x4096x4096: 60.5 vs 65.6 us; 256x4096x1024: 25.5 vs 37.8 us)
+    if (tc_persist_mode() == 2 || (tc_persist_mode() == 1 && op == GemmOp::TN && K <= 1024 && !pair)) {
+        TpPlan p = tp_plan(M, N, K, g.sm_count);
+        bool ok = true;
+        if (p.a.sk) {
+            ok = ensure_counters(g, (size_t)p.tiles);
+            if (ok) {
+                ensure_ws(g, p.part_floats);
+                p.a.part = *g.ws;
+                p.a.counters = *g.counters;
+            }
+        }
+        if (ok) {
+            p.a.C = C;
+            p.a.C2 = C2;
+            p.a.bias = bias;
+            p.a.aux = aux;
+            switch (e) {
+                case Epi::STORE: tp_dispatch<TpEpi::STORE>(g.stream, a_mn, b_mn, ma, mb, p); break;
+                case Epi::BIAS: tp_dispatch<TpEpi::BIAS>(g.stream, a_mn, b_mn, ma, mb, p); break;
+                case Epi::BIAS_TANH: tp_dispatch<TpEpi::BIAS_TANH>(g.stream, a_mn, b_mn, ma, mb, p); break;
+                case Epi::TANH_GRAD: tp_dispatch<TpEpi::TANH_GRAD>(g.stream, a_mn, b_mn, ma, mb, p); break;
+            }
+            *g.launches += 1;
+            return true;
+        }
     }
     TcArgs t{M, N, K, 0, nullptr, C, C2, bias, aux};
     // split-K when the 128x128 tiles fill less than half the SMs (the M = batch
@@ -609,6 +671,37 @@ inline bool gemm_try_tc(GemmCtx& g, GemmOp op, int M, int N, int K, const float*
             else tc_dispatch<TcEpi::TANH_GRAD, false>(g.stream, a_mn, b_mn, ma, mb, t);
             break;
     }
+    *g.launches += 1;
+    return true;
+}
+
+// wgrad fused with the SGD/momentum update (TN: G[M,N] = A[K,M]^T B[K,N] / B_glob,
+// then V = mu V - eta G, W += V), on the persistent tensor-core kernel only.
+// Returns false (nothing launched) when the shape or layout is not eligible.
+inline bool gemm_wgrad_update(GemmCtx& g, int M, int N, int K, const float* A, const float* B, float* G, float* W,
+                              float* V, float inv_b, float neg_eta, float mu) {
+    static const bool fuse = !std::getenv("LANE_B200_NO_FUSED_UPDATE");
+    if (!fuse || !tc_persist_mode() || !gemm_tc_mode() || !tc_eligible(M, N, K)) return false;
+    if (tc_use_pair(GemmOp::TN, M, N, K)) return false;  // the wgrad stays on the pair kernel
+    if ((reinterpret_cast<uintptr_t>(A) | reinterpret_cast<uintptr_t>(B) | reinterpret_cast<uintptr_t>(G) |
+         reinterpret_cast<uintptr_t>(W) | reinterpret_cast<uintptr_t>(V)) & 15)
+        return false;
+    TpPlan p = tp_plan(M, N, K, g.sm_count);
+    if (p.a.sk) {
+        if (!ensure_counters(g, (size_t)p.tiles)) return false;
+        ensure_ws(g, p.part_floats);
+        p.a.part = *g.ws;
+        p.a.counters = *g.counters;
+    }
+    const CUtensorMap ma = tc_map(A, K, M, 128, 32, 2);
+    const CUtensorMap mb = tc_map(B, K, N, 32, 32, 1);
+    p.a.C = G;
+    p.a.W = W;
+    p.a.V = V;
+    p.a.inv_b = inv_b;
+    p.a.neg_eta = neg_eta;
+    p.a.mu = mu;
+    tp_dispatch<TpEpi::UPDATE>(g.stream, true, true, ma, mb, p);
     *g.launches += 1;
     return true;
 }

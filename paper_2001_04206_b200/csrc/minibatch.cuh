@@ -42,6 +42,8 @@ struct MinibatchState {
     float* ws = nullptr;  // GEMM workspace (split-K partials / 3xTF32 splits)
     size_t ws_count = 0;
     uint64_t ws_gen = 0;  // reallocation count: part of the captured step graph's key
+    int* counters = nullptr;  // stream-K tile counters of the persistent GEMM
+    size_t counters_count = 0;
     cudaStream_t comm_stream = nullptr;  // per-layer gradient allreduces (data parallel)
     std::vector<cudaEvent_t> ev;         // one per layer + the join
 };
@@ -50,6 +52,9 @@ inline void minibatch_free(MinibatchState& s) {
     if (s.ws) cudaFree(s.ws);
     s.ws = nullptr;
     s.ws_count = 0;
+    if (s.counters) cudaFree(s.counters);
+    s.counters = nullptr;
+    s.counters_count = 0;
     for (cudaEvent_t e : s.ev) cudaEventDestroy(e);
     s.ev.clear();
     if (s.comm_stream) cudaStreamDestroy(s.comm_stream);
@@ -223,6 +228,42 @@ __global__ void k_momentum_update_all(float4* __restrict__ W, float4* __restrict
     }
 }
 
+// The same update over a list of spans of the arena (float4 offsets from the
+// region bases): the pieces a fused wgrad + update epilogue did not cover.
+constexpr int kMaxUpdSpans = 32;
+struct UpdSpans {
+    int n = 0;
+    unsigned long long beg[kMaxUpdSpans], end[kMaxUpdSpans];
+};
+__global__ void k_momentum_update_spans(float4* __restrict__ W, float4* __restrict__ DW, float4* __restrict__ gsum,
+                                        UpdSpans sp, unsigned long long total, float invB, float neg_eta, float mu) {
+    for (unsigned long long t = (unsigned long long)blockIdx.x * blockDim.x + threadIdx.x; t < total;
+         t += (unsigned long long)gridDim.x * blockDim.x) {
+        unsigned long long e = t;
+        int k = 0;
+        while (k < sp.n - 1 && e >= sp.end[k] - sp.beg[k]) {
+            e -= sp.end[k] - sp.beg[k];
+            ++k;
+        }
+        e += sp.beg[k];
+        float4 g = gsum[e], v = mu == 0.0f ? make_float4(0.f, 0.f, 0.f, 0.f) : DW[e], w = W[e];
+        float* gp = &g.x;
+        float* vp = &v.x;
+        float* wp = &w.x;
+#pragma unroll
+        for (int i = 0; i < 4; ++i) {
+            const float gi = smul(gp[i], invB);
+            gp[i] = gi;
+            const float step = smul(neg_eta, gi);
+            vp[i] = mu == 0.0f ? step : sadd(smul(mu, vp[i]), step);
+            wp[i] = sadd(wp[i], vp[i]);
+        }
+        gsum[e] = g;
+        DW[e] = v;
+        W[e] = w;
+    }
+}
+
 __global__ void k_momentum_update(float* __restrict__ W, float* __restrict__ DW,
                                   float* __restrict__ gsum, size_t n, float invB, float neg_eta,
                                   float mu) {
@@ -259,13 +300,20 @@ void minibatch_stage(Ctx& c, Net& net, const float* X, const float* T, size_t Bs
 // on the communication stream right after its wgrad and overlaps every
 // remaining dgrad and wgrad; the compute stream joins the communication stream
 // at the end.  Capturable in a CUDA graph.
+struct FusedUpdate {
+    float inv_b, eta, mu;
+    bool fused_w[kMaxUpdSpans];  // out: layer l's weights were updated by its wgrad epilogue
+};
+
 template <class Ctx, class Net>
-void minibatch_grads_body(Ctx& c, Net& net, size_t Bsz, double* loss_sum, bool allreduce) {
+void minibatch_grads_body(Ctx& c, Net& net, size_t Bsz, double* loss_sum, bool allreduce,
+                          FusedUpdate* fused = nullptr) {
     const int B = static_cast<int>(Bsz);
     const int nl = static_cast<int>(net.layers.size());
     const int C = static_cast<int>(net.classes);
     cudaStream_t st = c.stream;
-    GemmCtx g{c.stream, c.sm_count, &net.mb.ws, &net.mb.ws_count, &c.launches, &net.mb.ws_gen};
+    GemmCtx g{c.stream,   c.sm_count,        &net.mb.ws,       &net.mb.ws_count, &c.launches,
+              &net.mb.ws_gen, &net.mb.counters, &net.mb.counters_count};
     // forward
     for (int l = 0; l < nl; ++l) {
         auto& Ly = net.L(l);
@@ -292,9 +340,31 @@ void minibatch_grads_body(Ctx& c, Net& net, size_t Bsz, double* loss_sum, bool a
             M.ev.push_back(e);
         }
     }
+    auto dgrad = [&](int l) {
+        // dgrad with the pre-update weights: D_{l-1} = (D_l W_l^T) * (1 - A_{l-1}^2)
+        auto& Ly = net.L(l);
+        auto& pv = net.L(l - 1);
+        gemm(g, GemmOp::NT, B, (int)pv.O, (int)Ly.O, Ly.buf[LANE_BUF_DELTAS], (int)Ly.O, Ly.buf[LANE_BUF_W],
+             (int)Ly.O, Epi::TANH_GRAD, pv.buf[LANE_BUF_DELTAS], nullptr, nullptr, pv.buf[LANE_BUF_OUTPUTS]);
+    };
     for (int l = nl - 1; l >= 0; --l) {
         auto& Ly = net.L(l);
         const float* in = l == 0 ? net.L(0).buf[LANE_BUF_INPUTS] : net.L(l - 1).buf[LANE_BUF_OUTPUTS];
+        if (fused) {
+            // one rank: the dgrad reads W_l first, then the wgrad's epilogue
+            // updates W_l in place (G_l = X_l^T D_l / B, V_l, W_l)
+            if (l > 0) dgrad(l);
+            float* W = Ly.buf[LANE_BUF_W];
+            float* V = Ly.buf[LANE_BUF_DW];
+            fused->fused_w[l] = gemm_wgrad_update(g, (int)Ly.I, (int)Ly.O, B, in, Ly.buf[LANE_BUF_DELTAS],
+                                                            Ly.buf[LANE_BUF_G], W, V, fused->inv_b, -fused->eta,
+                                                            fused->mu);
+            if (!fused->fused_w[l])
+                gemm(g, GemmOp::TN, (int)Ly.I, (int)Ly.O, B, in, (int)Ly.I, Ly.buf[LANE_BUF_DELTAS], (int)Ly.O,
+                     Epi::STORE, Ly.buf[LANE_BUF_G], nullptr, nullptr, nullptr);
+            colsum(g, Ly.buf[LANE_BUF_DELTAS], B, (int)Ly.O, Ly.buf[LANE_BUF_BIAS_GRAD]);
+            continue;
+        }
         // wgrad sums: G_l = X_l^T D_l ; gb_l = colsum(D_l)
         gemm(g, GemmOp::TN, (int)Ly.I, (int)Ly.O, B, in, (int)Ly.I, Ly.buf[LANE_BUF_DELTAS], (int)Ly.O, Epi::STORE,
              Ly.buf[LANE_BUF_G], nullptr, nullptr, nullptr);
@@ -308,12 +378,7 @@ void minibatch_grads_body(Ctx& c, Net& net, size_t Bsz, double* loss_sum, bool a
             LANE_NCCL(ncclAllReduce(begin, begin, static_cast<size_t>(end - begin), ncclFloat32, ncclSum,
                                     c.comm.comm, M.comm_stream));
         }
-        // dgrad with the pre-update weights: D_{l-1} = (D_l W_l^T) * (1 - A_{l-1}^2)
-        if (l > 0) {
-            auto& pv = net.L(l - 1);
-            gemm(g, GemmOp::NT, B, (int)pv.O, (int)Ly.O, Ly.buf[LANE_BUF_DELTAS], (int)Ly.O, Ly.buf[LANE_BUF_W],
-                 (int)Ly.O, Epi::TANH_GRAD, pv.buf[LANE_BUF_DELTAS], nullptr, nullptr, pv.buf[LANE_BUF_OUTPUTS]);
-        }
+        if (l > 0) dgrad(l);
     }
     if (allreduce) {
         LANE_CUDA(cudaEventRecord(M.ev[nl], M.comm_stream));
@@ -324,32 +389,68 @@ void minibatch_grads_body(Ctx& c, Net& net, size_t Bsz, double* loss_sum, bool a
 
 // The update over the whole parameter set in one pass: G = gsum / B_global;
 // DW = mu*DW + (-eta)*G (DW = (-eta)*G when mu == 0); W += DW; biases alike.
+// With `fused`, only the pieces the wgrad epilogues did not update: every
+// bias, and the weights of the layers whose wgrad ran unfused.
 template <class Ctx, class Net>
-void minibatch_update(Ctx& c, Net& net, size_t B_global, float eta, float mu) {
+void minibatch_update(Ctx& c, Net& net, size_t B_global, float eta, float mu, const FusedUpdate* fused = nullptr) {
     const float invB = 1.0f / static_cast<float>(B_global);
     // params | grads | velocities are three equal-layout regions (abi.cu arena)
     float* W = net.params;
     float* G = net.grads;
     float* V = net.grads + net.grads_count;
     const size_t n4 = net.params_count / 4;
-    k_momentum_update_all<<<std::max<size_t>(1, std::min<size_t>(4 * c.sm_count, (n4 + 255) / 256)), 256, 0,
-                            c.stream>>>(reinterpret_cast<float4*>(W), reinterpret_cast<float4*>(V),
-                                        reinterpret_cast<float4*>(G), n4, invB, -eta, mu);
+    const unsigned blocks_max = 4u * static_cast<unsigned>(c.sm_count);
+    UpdSpans sp;
+    unsigned long long total = 0;
+    const int nl = static_cast<int>(net.layers.size());
+    const bool spans = fused != nullptr;
+    if (spans) {
+        for (int l = 0; l < nl; ++l) {
+            auto& Ly = net.L(l);
+            // [W_l | b_l] or [b_l] alone; pieces are 256-byte aligned, so the
+            // end of layer l is the start of layer l+1 (or of the grads region)
+            const float* from = fused->fused_w[l] ? Ly.buf[LANE_BUF_B] : Ly.buf[LANE_BUF_W];
+            const float* to = l + 1 < nl ? net.L(l + 1).buf[LANE_BUF_W] : net.params + net.params_count;
+            sp.beg[sp.n] = static_cast<unsigned long long>(from - W) / 4;
+            sp.end[sp.n] = static_cast<unsigned long long>(to - W) / 4;
+            total += sp.end[sp.n] - sp.beg[sp.n];
+            ++sp.n;
+        }
+    }
+    if (spans) {
+        const unsigned blocks = static_cast<unsigned>(std::max<unsigned long long>(
+            1, std::min<unsigned long long>(blocks_max, (total + 255) / 256)));
+        k_momentum_update_spans<<<blocks, 256, 0, c.stream>>>(reinterpret_cast<float4*>(W), reinterpret_cast<float4*>(V),
+                                                              reinterpret_cast<float4*>(G), sp, total, invB, -eta, mu);
+    } else {
+        k_momentum_update_all<<<std::max<size_t>(1, std::min<size_t>(blocks_max, (n4 + 255) / 256)), 256, 0,
+                                c.stream>>>(reinterpret_cast<float4*>(W), reinterpret_cast<float4*>(V),
+                                            reinterpret_cast<float4*>(G), n4, invB, -eta, mu);
+    }
     c.launches += 1;
     c.check_launch();
 }
 
-// The whole step on the staged batch.  Data parallel: every layer's gradient
-// span is all-reduced (one NCCL allreduce per layer, overlapping the rest of
-// the backward), then every rank applies the identical update with
+// The whole step on the staged batch.  One rank: the wgrad epilogues apply
+// the update of the weights they produce (tensor-core shapes), one small
+// kernel the rest.  Data parallel: every layer's gradient span is
+// all-reduced (one NCCL allreduce per layer, overlapping the rest of the
+// backward), then every rank applies the identical update with
 // B_global = B * world.  (LANE_B200_MB_BUCKETS=1 forces the allreduce path on
 // a one-rank communicator, where NCCL's sum is the identity.)
 template <class Ctx, class Net>
 void minibatch_body(Ctx& c, Net& net, size_t Bsz, float eta, float mu, double* loss_sum) {
     static const bool force_buckets = std::getenv("LANE_B200_MB_BUCKETS") != nullptr;
     const bool allreduce = c.comm.comm && (c.comm.world > 1 || force_buckets);
-    minibatch_grads_body(c, net, Bsz, loss_sum, allreduce);
-    minibatch_update(c, net, Bsz * static_cast<size_t>(c.comm.world), eta, mu);
+    const size_t B_global = Bsz * static_cast<size_t>(c.comm.world);
+    if (allreduce || net.layers.size() > static_cast<size_t>(kMaxUpdSpans)) {
+        minibatch_grads_body(c, net, Bsz, loss_sum, allreduce);
+        minibatch_update(c, net, B_global, eta, mu);
+        return;
+    }
+    FusedUpdate f{1.0f / static_cast<float>(B_global), eta, mu, {}};
+    minibatch_grads_body(c, net, Bsz, loss_sum, false, &f);
+    minibatch_update(c, net, B_global, eta, mu, &f);
 }
 
 }  // namespace lane_b200
