@@ -570,6 +570,8 @@ inline bool tc_use_pair(GemmOp op, int M, int N, int K) {
     const int persist = tc_persist_mode();
     if (!pair_ok || persist == 2) return false;
     if (persist == 1 && op == GemmOp::TN && K <= 1024) return false;
+    static const int min_m = std::getenv("LANE_B200_TC_PAIR_MIN_M") ? std::atoi(std::getenv("LANE_B200_TC_PAIR_MIN_M")) : 0;
+    if (min_m > 0) return M >= min_m;
     return M >= 1024 || (M >= 512 && K >= 2048);
 }
 

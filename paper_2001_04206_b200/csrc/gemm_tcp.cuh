@@ -9,10 +9,13 @@
 //   * data parallel (tiles >= 2 waves): CTA c takes whole tiles c, c + grid, ...
 //     in a grouped raster (GROUP tile rows at a time, for L2 reuse of B);
 //   * stream-K (fewer tiles): the tiles x K-blocks iteration space is cut into
-//     grid equal contiguous ranges, one per CTA; a tile covered by several
-//     ranges is finished by its LAST arriving piece, which sums the pieces'
-//     raw partials in piece (= K) order -- deterministic -- and runs the fused
-//     epilogue.  No CTA ever waits for another (no co-residency assumption).
+//     grid equal contiguous ranges, one per CTA (grid <= #SMs, one CTA per SM);
+//     a tile covered by several ranges is finished by its piece 0 (the one
+//     holding K block 0, the LAST unit of its CTA's range), which waits for
+//     the later pieces' raw partials -- they open their CTAs' ranges, so they
+//     are normally long published -- and sums them in piece (= K) order,
+//     deterministically, before the fused epilogue.  The wait is bounded
+//     (5 s, then trap: a failure, never a hang).
 // Warp roles (448 threads):
 //   warp 0      TMA producer: runs ahead across units through the 4-stage ring
 //   warp 1      MMA issuer: 3xTF32 MMAs (A from TMEM) into one of TWO TMEM
@@ -118,12 +121,12 @@ __device__ __forceinline__ void tp_tile_mn(const TpArgs& a, int tile, int& mt, i
     nt = r / gm;
 }
 
-template <TpEpi E>
-__device__ __forceinline__ void tp_epi_store(const TpArgs& a, int m, int n0, const float (&v)[32]) {
-    // one row segment [n0, n0 + 32) of row m (m < M checked by the caller)
-    if (n0 + 32 <= a.N && (a.N & 3) == 0) {
+template <TpEpi E, int NV>
+__device__ __forceinline__ void tp_epi_store(const TpArgs& a, int m, int n0, const float (&v)[NV]) {
+    // one row segment [n0, n0 + NV) of row m (m < M checked by the caller)
+    if (n0 + NV <= a.N && (a.N & 3) == 0) {
 #pragma unroll
-        for (int q = 0; q < 8; ++q) {
+        for (int q = 0; q < NV / 4; ++q) {
             const int n = n0 + 4 * q;
             const size_t idx = (size_t)m * a.N + n;
             float4 x = make_float4(v[4 * q], v[4 * q + 1], v[4 * q + 2], v[4 * q + 3]);
@@ -154,7 +157,7 @@ __device__ __forceinline__ void tp_epi_store(const TpArgs& a, int m, int n0, con
             }
         }
     } else {
-        for (int q = 0; q < 32; ++q) {
+        for (int q = 0; q < NV; ++q) {
             const int n = n0 + q;
             if (n >= a.N) break;
             const size_t idx = (size_t)m * a.N + n;
@@ -191,6 +194,30 @@ __device__ __forceinline__ void tp_ld32(uint32_t taddr, float (&v)[32]) {
     for (int q = 0; q < 32; ++q) v[q] = __uint_as_float(r[q]);
 }
 
+__device__ __forceinline__ void tp_ld16(uint32_t taddr, float (&v)[16]) {
+    uint32_t r[16];
+    asm volatile(
+        "tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15}, [%16];\n"
+        : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7]),
+          "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]), "=r"(r[14]), "=r"(r[15])
+        : "r"(taddr));
+    asm volatile("tcgen05.wait::ld.sync.aligned;\n" ::: "memory");
+#pragma unroll
+    for (int q = 0; q < 16; ++q) v[q] = __uint_as_float(r[q]);
+}
+
+__device__ __forceinline__ unsigned long long tp_globaltimer() {
+    unsigned long long t;
+    asm volatile("mov.u64 %0, %%globaltimer;\n" : "=l"(t));
+    return t;
+}
+
+__device__ __forceinline__ int tp_ld_acquire(const int* p) {
+    int v;
+    asm volatile("ld.acquire.gpu.global.b32 %0, [%1];\n" : "=r"(v) : "l"(p) : "memory");
+    return v;
+}
+
 __device__ __forceinline__ void tp_epi_bar() {
     // the 4 epilogue warps only (named barrier 1)
     asm volatile("bar.sync 1, %0;\n" ::"n"(32 * kTpEpiWarps) : "memory");
@@ -216,7 +243,6 @@ __global__ void __launch_bounds__(kTpThreads, 1)
     uint64_t* bars = reinterpret_cast<uint64_t*>(smem + Cfg::kRing + Cfg::kEpi);
     // bars: full[S], conv[S], empty[S], acc_full[2], acc_empty[2]; then the TMEM address, the last-arriver flag
     uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 32);
-    volatile int* last_flag = reinterpret_cast<volatile int*>(bars + 33);
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const uint32_t sbase = tc_smem(smem);
     auto full = [&](int s) { return tc_smem(bars + s); };
@@ -511,60 +537,72 @@ __global__ void __launch_bounds__(kTpThreads, 1)
                     if (m < args.M) tp_epi_store<E>(args, m, n0 + 32 * c, v);
                 }
             } else {
-                // stream-K piece: raw partial -> workspace; the last arriving
-                // piece of the tile sums all pieces in K order and finishes it
-                float* mine = args.part + ((size_t)u.tile * args.max_pieces + u.piece) * kTpTileElems + (size_t)row * kTcBN;
-#pragma unroll 1
-                for (int c = 0; c < kTcBN / 32; ++c) {
-                    float v[32];
-                    tp_ld32(tacc + (uint32_t)(32 * c), v);
-                    if (c == kTcBN / 32 - 1) {
-                        asm volatile("tcgen05.fence::before_thread_sync;\n" ::: "memory");
-                        __syncwarp();
-                        if (lane == 0) tc_mbar_arrive(acc_empty(b));
-                    }
-#pragma unroll
-                    for (int q = 0; q < 8; ++q)
-                        __stcg(reinterpret_cast<float4*>(mine + 32 * c + 4 * q),
-                               make_float4(v[4 * q], v[4 * q + 1], v[4 * q + 2], v[4 * q + 3]));
-                }
-                __threadfence();
-                tp_epi_bar();
-                if (leader) {
-                    const int old = atomicAdd(args.counters + u.tile, 1);
-                    const int last = old == u.npieces - 1;
-                    if (last) args.counters[u.tile] = 0;  // ready for the next launch
-                    *last_flag = last;
-                }
-                tp_epi_bar();
-                const bool last = *last_flag != 0;
-                tp_epi_bar();  // everyone has read the flag before the next unit rewrites it
-                if (last) {
-                    __threadfence();
-                    const float* base = args.part + (size_t)u.tile * args.max_pieces * kTpTileElems + (size_t)row * kTcBN;
+                // stream-K: the tile's pieces in K order; piece 0 (the one
+                // holding K block 0) is its CTA's LAST unit, while the later
+                // pieces open their CTAs' ranges, so piece 0 finishes the tile:
+                // it waits until pieces 1.. have published their raw partials
+                // (normally long done), then sums acc0 + acc1 + ... in piece
+                // order (deterministic) and runs the fused epilogue.
+                if (u.piece != 0) {
+                    float* mine = args.part + ((size_t)u.tile * args.max_pieces + u.piece) * kTpTileElems +
+                                  (size_t)row * kTcBN;
 #pragma unroll 1
                     for (int c = 0; c < kTcBN / 32; ++c) {
                         float v[32];
-#pragma unroll
-                        for (int q = 0; q < 8; ++q) {
-                            const float4 x = __ldcg(reinterpret_cast<const float4*>(base + 32 * c + 4 * q));
-                            v[4 * q] = x.x;
-                            v[4 * q + 1] = x.y;
-                            v[4 * q + 2] = x.z;
-                            v[4 * q + 3] = x.w;
+                        tp_ld32(tacc + (uint32_t)(32 * c), v);
+                        if (c == kTcBN / 32 - 1) {
+                            asm volatile("tcgen05.fence::before_thread_sync;\n" ::: "memory");
+                            __syncwarp();
+                            if (lane == 0) tc_mbar_arrive(acc_empty(b));
                         }
-                        for (int p = 1; p < u.npieces; ++p) {
 #pragma unroll
-                            for (int q = 0; q < 8; ++q) {
-                                const float4 x = __ldcg(reinterpret_cast<const float4*>(
-                                    base + (size_t)p * kTpTileElems + 32 * c + 4 * q));
-                                v[4 * q] += x.x;
-                                v[4 * q + 1] += x.y;
-                                v[4 * q + 2] += x.z;
-                                v[4 * q + 3] += x.w;
-                            }
+                        for (int q = 0; q < 8; ++q)
+                            __stcg(reinterpret_cast<float4*>(mine + 32 * c + 4 * q),
+                                   make_float4(v[4 * q], v[4 * q + 1], v[4 * q + 2], v[4 * q + 3]));
+                    }
+                    __threadfence();
+                    tp_epi_bar();
+                    if (leader) atomicAdd(args.counters + u.tile, 1);
+                } else {
+                    if (leader) {
+                        const unsigned long long t0 = tp_globaltimer();
+                        while (tp_ld_acquire(args.counters + u.tile) < u.npieces - 1) {
+                            __nanosleep(100);
+                            if (tp_globaltimer() - t0 > 5000000000ull) __trap();  // a lost piece: fail, never hang
                         }
-                        if (m < args.M) tp_epi_store<E>(args, m, n0 + 32 * c, v);
+                        args.counters[u.tile] = 0;  // ready for the next launch
+                    }
+                    tp_epi_bar();
+                    const float* base = args.part + (size_t)u.tile * args.max_pieces * kTpTileElems + (size_t)row * kTcBN;
+                    constexpr int kMaxP = 4;  // tp_plan keeps every tile within 4 pieces
+#pragma unroll 1
+                    for (int c = 0; c < kTcBN / 16; ++c) {
+                        float v[16];
+                        tp_ld16(tacc + (uint32_t)(16 * c), v);
+                        if (c == kTcBN / 16 - 1) {
+                            asm volatile("tcgen05.fence::before_thread_sync;\n" ::: "memory");
+                            __syncwarp();
+                            if (lane == 0) tc_mbar_arrive(acc_empty(b));
+                        }
+                        float4 x[kMaxP - 1][4];
+#pragma unroll
+                        for (int p = 1; p < kMaxP; ++p)
+                            if (p < u.npieces)
+#pragma unroll
+                                for (int q = 0; q < 4; ++q)
+                                    x[p - 1][q] = __ldcg(reinterpret_cast<const float4*>(
+                                        base + (size_t)p * kTpTileElems + 16 * c + 4 * q));
+#pragma unroll
+                        for (int p = 1; p < kMaxP; ++p)
+                            if (p < u.npieces)
+#pragma unroll
+                                for (int q = 0; q < 4; ++q) {
+                                    v[4 * q] += x[p - 1][q].x;
+                                    v[4 * q + 1] += x[p - 1][q].y;
+                                    v[4 * q + 2] += x[p - 1][q].z;
+                                    v[4 * q + 3] += x[p - 1][q].w;
+                                }
+                        if (m < args.M) tp_epi_store<E>(args, m, n0 + 16 * c, v);
                     }
                 }
             }
@@ -615,8 +653,9 @@ inline TpPlan tp_plan(int M, int N, int K, int sms) {
     } else {
         a.sk = 1;
         a.per = (int)((total + sms - 1) / sms);
-        // pieces shorter than 4 K blocks cost more in fix-up than they balance
-        a.per = std::max(a.per, std::min(a.kbs, 4));
+        // pieces shorter than 4 K blocks cost more in fix-up than they balance,
+        // and the finishing piece sums at most 4 (per >= kbs / 3)
+        a.per = std::max({a.per, std::min(a.kbs, 4), (a.kbs + 2) / 3});
         p.grid = (int)((total + a.per - 1) / a.per);
         a.max_pieces = (a.kbs + a.per - 1) / a.per + 1;
         p.part_floats = (size_t)p.tiles * a.max_pieces * kTpTileElems;

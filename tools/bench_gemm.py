@@ -26,7 +26,7 @@ def main():
         a = torch.randn(M * K, device="cuda")
         b = torch.randn(N * K, device="cuda")
         c = torch.empty(M * N, device="cuda")
-        for use_tc in (1, 0):
+        for use_tc in [int(x) for x in os.environ.get("BENCH_TC", "1,0").split(",")]:
             def call():
                 rc = L.lane_b200_gemm(dev._p, op, M, N, K, C.c_void_p(a.data_ptr()), C.c_void_p(b.data_ptr()),
                                       C.c_void_p(c.data_ptr()), None, None, None, 0, use_tc)
