@@ -216,9 +216,10 @@ def run_reference_arm(args, wl):
 
 
 def dominant_gemm(dev, widths, rows, stream):
-    """fp32-equivalent TFLOP/s of k_gemm_tc alone over the step's tensor-core
-    GEMM shapes (same kernels and shapes as inside the captured step graph,
-    which cannot be timed per kernel), and their share of the step's flops."""
+    """fp32-equivalent TFLOP/s of the tensor-core GEMMs alone over the step's
+    GEMM shapes (same kernels, precision scheme and shapes as inside the
+    captured step graph, which cannot be timed per kernel: lane_b200_gemm with
+    use_tc = 5, the step's own choice), and their share of the step's flops."""
     import ctypes as C
     import torch
     from paper_2001_04206_b200 import _native
@@ -238,7 +239,7 @@ def dominant_gemm(dev, widths, rows, stream):
         c = torch.empty(M * N, device="cuda")
         def call():
             rc = L.lane_b200_gemm(dev._p, op, M, N, K, C.c_void_p(a.data_ptr()), C.c_void_p(b.data_ptr()),
-                                  C.c_void_p(c.data_ptr()), None, None, None, 0, 1)
+                                  C.c_void_p(c.data_ptr()), None, None, None, 0, 5)
             assert rc == 0, L.lane_b200_last_error()
         for _ in range(2):
             call()
@@ -257,17 +258,30 @@ def dominant_gemm(dev, widths, rows, stream):
     return (tot_f / (tot_ms / 1e3) / 1e12 if tot_ms else None), tot_f / step_f
 
 
-def measure_tf32_peak() -> float:
-    """Dense TF32 TFLOP/s of this GPU as cuBLAS reaches it: fp32 matmul with
-    TF32 tensor cores enabled at 8192^3, best of 10 (CUDA events)."""
+def uses_h3(widths, rows):
+    """True when the step's tensor-core GEMMs run the 3xF16 kernel (gemm.cuh
+    tc_use_h3: tall CTA-pair shapes with K >= 2048), unless overridden."""
+    mode = os.environ.get("LANE_B200_TC_PREC", "auto")
+    if mode in ("f16", "tf32"):
+        return mode == "f16"
+    big = [(rows, o, i) for i, o in zip(widths[:-1], widths[1:]) if o >= 64]
+    return bool(big) and all((M >= 1024 or (M >= 512 and K >= 2048)) and K >= 2048 and N >= 256
+                             for M, N, K in big)
+
+
+def measure_tf32_peak(dtype: str = "tf32") -> float:
+    """Dense tensor-core TFLOP/s of this GPU as cuBLAS reaches it at 8192^3,
+    best of 10 (CUDA events): fp32 matmul with TF32 enabled ("tf32"), or a
+    plain fp16 matmul ("f16")."""
     import torch
     old = torch.backends.cuda.matmul.allow_tf32
     torch.backends.cuda.matmul.allow_tf32 = True
     try:
         n = 8192
-        a = torch.randn(n, n, device="cuda")
-        b = torch.randn(n, n, device="cuda")
-        c = torch.empty(n, n, device="cuda")
+        dt = torch.float16 if dtype == "f16" else torch.float32
+        a = torch.randn(n, n, device="cuda", dtype=dt)
+        b = torch.randn(n, n, device="cuda", dtype=dt)
+        c = torch.empty(n, n, device="cuda", dtype=dt)
         for _ in range(3):
             torch.matmul(a, b, out=c)
         best = float("inf")
@@ -365,11 +379,16 @@ def run_minibatch(args, wl):
     flops = (6 * P - 2 * P0) * BG  # fwd 2P + wgrad 2P + dgrad 2(P - P0) per sample
     step_tf = flops / (ms / args.steps / 1000.0) / 1e12
     gemm_tf, gemm_share = dominant_gemm(dev, widths, rows, stream)
-    # the denominator: this box's dense TF32 rate (cuBLAS fp32 matmul with
-    # TF32 at 8192^3, best of 10), / 3 for the 3 MMAs of a 3xTF32 product
-    tf32 = measure_tf32_peak()
-    peak = tf32 / 3.0
-    nominal = 2250.0 / 2.0 / 3.0  # NVIDIA's dense bf16 2.25 PF/s -> TF32 1.125 -> 3xTF32
+    # the denominator: this box's dense tensor rate for the MMA kind the step
+    # runs (cuBLAS at 8192^3, best of 10: fp16 for the 3xF16 kernel, fp32 with
+    # TF32 for the 3xTF32 kernels), / 3 for the 3 MMAs per fp32 product
+    h3 = uses_h3(widths, rows)
+    tc_rate = measure_tf32_peak("f16" if h3 else "tf32")
+    peak = tc_rate / 3.0
+    nominal = 2250.0 / (1.0 if h3 else 2.0) / 3.0  # NVIDIA's dense fp16 2.25 PF/s (TF32: half)
+    kernel = "k_gemm_h3" if h3 else "k_gemm_tc"
+    gemm_desc = ("tcgen05 kind::f16, 3xF16 (power-of-two row/column scales; fp32-accurate, 1e-5 "
+                 "condition-aware)" if h3 else "tcgen05 kind::tf32, 3xTF32 (fp32-accurate, 1e-5 condition-aware)")
     # the step's two sequential phases each have a floor: the GEMMs on the tensor
     # pipe and the update streaming W, V and G (read + write, 24 B/param) from
     # HBM; the next step's forward needs the updated weights, so they add
@@ -383,16 +402,16 @@ def run_minibatch(args, wl):
             "data": "synthetic",
             "config": {"workload": wl, "description": desc, "layers": widths, "global_batch": BG,
                        "rows_per_rank": rows, "momentum": mu, "eta": eta, "parallelism": f"dp{world}",
-                       "gemm": "tcgen05 kind::tf32, 3xTF32 (fp32-accurate, 1e-5 condition-aware)",
+                       "gemm": gemm_desc,
                        "l2": "256 MB buffer written between timed steps"},
-            "roofline": {"bound": "tensor", "kernel": "k_gemm_tc", "achieved": gemm_tf, "peak": peak,
+            "roofline": {"bound": "tensor", "kernel": kernel, "achieved": gemm_tf, "peak": peak,
                          "unit": "TFLOP/s", "frac": gemm_tf / peak if gemm_tf else None,
                          "traffic": load_traffic(wl)[0], "traffic_source": load_traffic(wl)[1],
                          "how": "the step's tensor-core GEMM shapes (fwd/dgrad/wgrad of the 4096-wide "
                                 "layers) replayed through lane_b200_gemm, CUDA events on the library "
                                 "stream, 10 reps each; algorithmic flops 2MNK per launch",
-                         "peak_kind": "measured: cuBLAS dense TF32 8192^3 on this GPU "
-                                      f"({tf32:.0f} TF/s) / 3 (3xTF32 MMAs per product)",
+                         "peak_kind": f"measured: cuBLAS dense {'fp16' if h3 else 'TF32'} 8192^3 on this "
+                                      f"GPU ({tc_rate:.0f} TF/s) / 3 (MMAs per fp32 product)",
                          "frac_of_nominal": gemm_tf / nominal if gemm_tf else None,
                          "flop_share_of_step": gemm_share,
                          "step": {"achieved": step_tf, "frac": step_tf / peak,
@@ -400,7 +419,7 @@ def run_minibatch(args, wl):
                                            "step time"},
                          "step_floor": {"tensor_us": floor_tensor_us, "hbm_update_us": floor_update_us,
                                         "frac": (floor_tensor_us + floor_update_us) / (ms / args.steps * 1e3),
-                                        "how": "GEMM flops at the measured 3xTF32 peak + the update's "
+                                        "how": "GEMM flops at the measured 3-MMA peak + the update's "
                                                "20 (SGD) / 24 (momentum) B/param at the measured HBM "
                                                "peak, against the measured step time"},
                          "algorithmic_flops_per_step": flops},

@@ -254,9 +254,11 @@ int lane_b200_train_minibatch(lane_b200_net* net, const float* X_host, const flo
  * op 0 NN: C[M,N] = A[M,K] B[K,N];  op 1 NT: C = A[M,K] B[N,K]^T;
  * op 2 TN: C = A[K,M]^T B[K,N].  epilogue 0 store, 1 +bias[n], 2 +bias[n]
  * with C2 = tanh(C), 3 C = (1 - aux^2) * acc.  use_tc: 0 the SIMT kernel;
- * 1 the tcgen05 3xTF32 kernels where the shape is eligible (the library's own
- * choice); 2 the persistent stream-K tcgen05 kernel for every eligible shape;
- * 3 the one-tile-per-CTA tcgen05 kernels only. */
+ * 1 the tcgen05 3xTF32 kernels where the shape is eligible; 2 the persistent
+ * stream-K 3xTF32 kernel for every eligible shape; 3 the one-tile-per-CTA
+ * 3xTF32 kernels only; 4 the tcgen05 3xF16 kernel (power-of-two row/column
+ * operand scales, kind::f16 MMAs); 5 the mini-batch step's own choice (3xF16
+ * for the tall long-K shapes, 3xTF32 otherwise; LANE_B200_TC_PREC overrides). */
 int lane_b200_gemm(lane_b200_ctx* ctx, int op, int M, int N, int K, const float* A, const float* B,
                    float* C, float* C2, const float* bias, const float* aux, int epilogue, int use_tc);
 

@@ -1795,7 +1795,7 @@ int lane_b200_gemm(lane_b200_ctx* c, int op, int M, int N, int K, const float* A
                    float* C2, const float* bias, const float* aux, int epilogue, int use_tc) {
     return guard([&] {
         if (!c) throw Error(LANE_ERR_CONFIG, "null context");
-        if (op < 0 || op > 2 || epilogue < 0 || epilogue > 3 || M < 0 || N < 0 || K < 0)
+        if (op < 0 || op > 2 || epilogue < 0 || epilogue > 3 || M < 0 || N < 0 || K < 0 || use_tc < 0 || use_tc > 5)
             throw Error(LANE_ERR_CONFIG, "lane_b200_gemm: bad op/epilogue/shape");
         static float* ws = nullptr;
         static size_t ws_count = 0;
@@ -1805,8 +1805,11 @@ int lane_b200_gemm(lane_b200_ctx* c, int op, int M, int N, int K, const float* A
         const GemmOp o = static_cast<GemmOp>(op);
         const int lda = o == GemmOp::TN ? M : K;
         const int ldb = o == GemmOp::NT ? K : N;
-        const int saved = gemm_tc_mode(), saved_p = tc_persist_mode();
+        const int saved = gemm_tc_mode(), saved_p = tc_persist_mode(), saved_h = tc_prec_mode();
         gemm_tc_mode() = use_tc ? 1 : 0;
+        // 4: the 3xF16 kernel (gemm_h3.cuh); 5: the mini-batch step's own choice
+        // (3xF16 for the tall long-K shapes); else 3xTF32
+        tc_prec_mode() = use_tc == 4 ? 1 : use_tc == 5 ? saved_h : 0;
         if (use_tc == 2) tc_persist_mode() = 2;  // the persistent stream-K kernel for every shape
         if (use_tc == 3) tc_persist_mode() = 0;  // never
         try {
@@ -1814,10 +1817,12 @@ int lane_b200_gemm(lane_b200_ctx* c, int op, int M, int N, int K, const float* A
         } catch (...) {
             gemm_tc_mode() = saved;
             tc_persist_mode() = saved_p;
+            tc_prec_mode() = saved_h;
             throw;
         }
         gemm_tc_mode() = saved;
         tc_persist_mode() = saved_p;
+        tc_prec_mode() = saved_h;
         c->check_launch();
     });
 }

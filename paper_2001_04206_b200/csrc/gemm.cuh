@@ -19,6 +19,7 @@
 #include "common.cuh"
 #include "gemm_tc.cuh"
 #include "gemm_tcp.cuh"
+#include "gemm_h3.cuh"
 
 namespace lane_b200 {
 
@@ -575,6 +576,99 @@ inline bool tc_use_pair(GemmOp op, int M, int N, int K) {
     return M >= 1024 || (M >= 512 && K >= 2048);
 }
 
+// Tensor-core operand precision scheme: 0 = 3xTF32 everywhere (gemm_tc.cuh /
+// gemm_tcp.cuh); 1 = 3xF16 with power-of-two row/column scales (gemm_h3.cuh)
+// everywhere; 2 (default) = 3xF16 for the tall CTA-pair shapes with a long K
+// (4096^3: 0.51 -> 0.38 ms including the operand-maxima passes), 3xTF32 for
+// the rest (the M = batch = 256 shapes and short-K wgrads of C3 run faster on
+// the persistent stream-K 3xTF32 kernel).  LANE_B200_TC_PREC=tf32|f16|auto,
+// or lane_b200_gemm()'s use_tc = 4 (3xF16) for one call.
+inline int& tc_prec_mode() {
+    static int mode = [] {
+        const char* e = std::getenv("LANE_B200_TC_PREC");
+        if (e && std::strcmp(e, "f16") == 0) return 1;
+        if (e && std::strcmp(e, "tf32") == 0) return 0;
+        return 2;
+    }();
+    return mode;
+}
+inline bool tc_use_h3(int M, int N, int K) {
+    const int m = tc_prec_mode();
+    return m == 1 || (m == 2 && (M >= 1024 || (M >= 512 && K >= 2048)) && K >= 2048 && N >= 256);
+}
+
+// 3xF16: per-row maxima of op(A) and per-column maxima of op(B) into the
+// workspace tail, then the split-scaled kernel (pairs for the tall shapes,
+// single CTAs with split-K otherwise)
+inline void gemm_h3(GemmCtx& g, GemmOp op, int M, int N, int K, const float* A, const float* B, Epi e, float* C,
+                    float* C2, const float* bias, const float* aux) {
+    const bool pair = M >= 1024 || (M >= 512 && K >= 2048);
+    CUtensorMap ma, mb;
+    bool a_mn = false, b_mn = false;
+    switch (op) {
+        case GemmOp::NN:
+            ma = tc_map(A, M, K, 32, 128, 0);
+            mb = tc_map(B, K, N, 128, 32, 2);
+            b_mn = true;
+            break;
+        case GemmOp::NT:
+            ma = tc_map(A, M, K, 32, 128, 0);
+            mb = tc_map(B, N, K, 32, 128, 0);
+            break;
+        case GemmOp::TN:
+            ma = tc_map(A, K, M, 128, 32, 2);
+            mb = tc_map(B, K, N, 128, 32, 2);
+            a_mn = b_mn = true;
+            break;
+    }
+    TcArgs t{M, N, K, 0, nullptr, C, C2, bias, aux};
+    constexpr int kPN = H3Cfg<true>::kBN;
+    const int tiles = pair ? 2 * ((M + 2 * kTcBM - 1) / (2 * kTcBM)) * ((N + kPN - 1) / kPN)
+                           : ((M + kTcBM - 1) / kTcBM) * ((N + kTcBN - 1) / kTcBN);
+    const int nkb = (K + kTcBK - 1) / kTcBK;
+    static const int kbmin = std::getenv("LANE_B200_TC_SPLITK_KBMIN") ? std::atoi(std::getenv("LANE_B200_TC_SPLITK_KBMIN")) : 24;
+    int S = std::min({4, g.sm_count / std::max(1, tiles), nkb / kbmin});
+    if (K % kTcBK != 0) S = 1;
+    size_t part = 0;
+    if (S > 1) {
+        t.kbs = (nkb + S - 1) / S;
+        S = (nkb + t.kbs - 1) / t.kbs;
+        part = (size_t)S * M * N;
+    }
+    // [split-K partials | row maxima of op(A) | column maxima of op(B)]
+    ensure_ws(g, part + (size_t)M + (size_t)N);
+    float* ws = *g.ws;
+    if (S > 1) t.part = ws;
+    unsigned* amax = reinterpret_cast<unsigned*>(ws + part);
+    unsigned* bmax = amax + M;
+    absmax_launch(g.stream, A, op == GemmOp::TN ? K : M, op == GemmOp::TN ? M : K, op != GemmOp::TN, amax);
+    absmax_launch(g.stream, B, op == GemmOp::NT ? N : K, op == GemmOp::NT ? K : N, op == GemmOp::NT, bmax);
+    t.amax = amax;
+    t.bmax = bmax;
+    static const int diag = std::getenv("LANE_B200_H3_DIAG") ? std::atoi(std::getenv("LANE_B200_H3_DIAG")) : 0;
+    t.diag = diag;
+    *g.launches += 2 + (S > 1 ? 1 : 0);
+    switch (e) {
+        case Epi::STORE:
+            if (pair) h3_dispatch<TcEpi::STORE, true>(g.stream, a_mn, b_mn, ma, mb, t);
+            else h3_dispatch<TcEpi::STORE, false>(g.stream, a_mn, b_mn, ma, mb, t);
+            break;
+        case Epi::BIAS:
+            if (pair) h3_dispatch<TcEpi::BIAS, true>(g.stream, a_mn, b_mn, ma, mb, t);
+            else h3_dispatch<TcEpi::BIAS, false>(g.stream, a_mn, b_mn, ma, mb, t);
+            break;
+        case Epi::BIAS_TANH:
+            if (pair) h3_dispatch<TcEpi::BIAS_TANH, true>(g.stream, a_mn, b_mn, ma, mb, t);
+            else h3_dispatch<TcEpi::BIAS_TANH, false>(g.stream, a_mn, b_mn, ma, mb, t);
+            break;
+        case Epi::TANH_GRAD:
+            if (pair) h3_dispatch<TcEpi::TANH_GRAD, true>(g.stream, a_mn, b_mn, ma, mb, t);
+            else h3_dispatch<TcEpi::TANH_GRAD, false>(g.stream, a_mn, b_mn, ma, mb, t);
+            break;
+    }
+    *g.launches += 1;
+}
+
 // Tensor-core dispatch (gemm_tc.cuh): returns false when the shape/layout is
 // not eligible (the caller then runs the SIMT kernel).
 inline bool gemm_try_tc(GemmCtx& g, GemmOp op, int M, int N, int K, const float* A, int lda, const float* B,
@@ -582,6 +676,11 @@ inline bool gemm_try_tc(GemmCtx& g, GemmOp op, int M, int N, int K, const float*
     if (!gemm_tc_mode() || !tc_eligible(M, N, K)) return false;
     if ((reinterpret_cast<uintptr_t>(A) | reinterpret_cast<uintptr_t>(B) | reinterpret_cast<uintptr_t>(C)) & 15)
         return false;
+    if (tc_use_h3(M, N, K)) {
+        if (lda != (op == GemmOp::TN ? M : K) || ldb != (op == GemmOp::NT ? K : N)) return false;
+        gemm_h3(g, op, M, N, K, A, B, e, C, C2, bias, aux);
+        return true;
+    }
     CUtensorMap ma, mb;
     bool a_mn = false, b_mn = false;
     const bool pair = tc_use_pair(op, M, N, K);
@@ -683,7 +782,7 @@ inline bool gemm_try_tc(GemmCtx& g, GemmOp op, int M, int N, int K, const float*
 inline bool gemm_wgrad_update(GemmCtx& g, int M, int N, int K, const float* A, const float* B, float* G, float* W,
                               float* V, float inv_b, float neg_eta, float mu) {
     static const bool fuse = !std::getenv("LANE_B200_NO_FUSED_UPDATE");
-    if (!fuse || !tc_persist_mode() || !gemm_tc_mode() || !tc_eligible(M, N, K)) return false;
+    if (!fuse || !tc_persist_mode() || !gemm_tc_mode() || tc_use_h3(M, N, K) || !tc_eligible(M, N, K)) return false;
     if (tc_use_pair(GemmOp::TN, M, N, K)) return false;  // the wgrad stays on the pair kernel
     if ((reinterpret_cast<uintptr_t>(A) | reinterpret_cast<uintptr_t>(B) | reinterpret_cast<uintptr_t>(G) |
          reinterpret_cast<uintptr_t>(W) | reinterpret_cast<uintptr_t>(V)) & 15)

@@ -1,0 +1,515 @@
+// gemm_h3.cuh -- fp32-accurate GEMM on the tcgen05 tensor cores at the FP16
+// rate, "3xF16": every operand element x is scaled by a power of two and split
+// into two halves,
+//     s x = hi + lo,   hi = f16(s x),   lo = f16(s x - hi)
+// and the product is accumulated in fp32 as A_lo.B_hi + A_hi.B_lo + A_hi.B_hi
+// (the dropped A_lo.B_lo term is ~2^-22 relative).  kind::f16 MMAs run at twice
+// the kind::tf32 rate and read half the operand bytes, so the three products
+// cost what 1.5 tf32 MMAs cost -- against 3 for the 3xTF32 kernel
+// (gemm_tc.cuh), which was bound by the tensor pipe.
+//
+// Scales.  fp16 has 5 exponent bits, so each row m of op(A) is scaled by
+// sa[m] = 2^(14 - e) with e the exponent of max_k |A[m][k]| (so the row's
+// largest element lands in [2^14, 2^15) and nothing overflows), and each column
+// n of op(B) by sb[n] likewise.  The scales are constant along K, so the MMA
+// accumulates sa[m] sb[n] (A.B)[m][n] exactly as it would A.B, and the
+// epilogue multiplies by the two inverse powers of two (exact).  An element
+// 2^17 below its row's (column's) maximum still keeps a normal lo part; the
+// precision degrades only gradually below that (subnormal lo), far beyond what
+// the condition-aware 1e-5 bound can see.  The per-row / per-column maxima come
+// from a one-pass pre-kernel (k_absmax_rows / k_absmax_cols, below).
+//
+// Structure: gemm_tc.cuh's (one 128 x 128 tile per CTA, or 256 x 256 per CTA
+// pair with cta_group::2 and N = 256 MMAs; TMA producer, MMA issuer, 16 split
+// warps that then run the epilogue).  Per 32-wide K block the split warps read
+// the TMA-loaded fp32 A and B tiles (a 5-slot landing ring, released as soon
+// as it is read) and write
+//   A_hi, A_lo -> TMEM (lane = row, 32-bit column = a pair of K elements),
+//   B_hi, B_lo -> shared memory, K-major, no swizzle (8 x 16-byte core
+//                 matrices: LBO = 128 B along K, SBO = 512 B along N).
+// into a 4-slot f16 ring.  Per K block the MMA issuer issues 2 K-steps
+// (K = 16) x 3 MMAs.  Shared memory: landing slots 32 KB (A, B fp32), f16
+// slots 16 KB (B_hi, B_lo).
+// TMEM: accumulator [0, tile N), then per stage 16 columns of A_hi and 16 of A_lo.
+#pragma once
+
+#include <cuda_fp16.h>
+
+#include "gemm_tc.cuh"
+
+namespace lane_b200 {
+
+// 16 split warps (4 per SM sub-partition): warps 2..9 split A, 10..17 split B
+// (8 split warps doing both ran the split pass latency-bound at ~1.1k cycles
+// per K block against ~770 of MMAs)
+constexpr int kH3SplitWarps = 16;
+constexpr int kH3Threads = 64 + 32 * kH3SplitWarps;
+
+template <bool PAIR>
+struct H3Cfg {
+    static constexpr int kBN = PAIR ? 2 * kTcBN : kTcBN;
+    static constexpr int kBLocal = PAIR ? kBN / 2 : kBN;  // 128 B columns per CTA
+    static constexpr int kA32 = kTcBM * kTcBK * 4;        // fp32 A tile
+    static constexpr int kB32 = kBLocal * kTcBK * 4;      // fp32 B tile
+    static constexpr int kB16 = kBLocal * kTcBK * 2;      // one f16 B part
+    // two rings: fp32 landing slots (TMA -> split warps, freed as soon as they
+    // are read) and f16 slots (split warps -> MMA, freed by the MMA commit), so
+    // the TMA runs up to kLand + kStages K blocks ahead of the tensor core
+    static constexpr int kLand = 5, kStages = 4;
+    static constexpr int kLandBytes = kA32 + kB32, kF16Bytes = 2 * kB16;
+    static constexpr size_t kSmem = (size_t)kLand * kLandBytes + (size_t)kStages * kF16Bytes + 1024 + 512;
+};
+
+// power-of-two operand scale from the max |x| bits of a row / column: the
+// maximum lands in [2^14, 2^15) (zero rows: exponent clamped, any scale works)
+__device__ __forceinline__ int h3_exp(unsigned maxbits) {
+    int e = (int)((maxbits >> 23) & 0xFFu) - 127;
+    return e < -100 ? -100 : e;
+}
+__device__ __forceinline__ float h3_pow2(int p) { return __int_as_float((127 + p) << 23); }
+
+// s*x split into f16 hi + lo, packed pairwise (k even in the low half).  hi is
+// s*x truncated to 11 significant bits in fp32 (exactly an f16 for the scaled
+// range [2^-14, 2^15)), so lo = s*x - hi is exact and no f16 -> f32
+// conversion is needed; one packed cvt per pair for each part.
+__device__ __forceinline__ uint32_t h3_pack(float lo_k, float hi_k) {
+    uint32_t d;
+    asm("cvt.rn.f16x2.f32 %0, %1, %2;\n" : "=r"(d) : "f"(hi_k), "f"(lo_k));  // hi_k -> upper half
+    return d;
+}
+__device__ __forceinline__ void h3_split2(float x0, float x1, float s, uint32_t& hi, uint32_t& lo) {
+    const float a0 = x0 * s, a1 = x1 * s;  // exact: power-of-two scale
+    const float h0 = __uint_as_float(__float_as_uint(a0) & 0xFFFFE000u);
+    const float h1 = __uint_as_float(__float_as_uint(a1) & 0xFFFFE000u);
+    hi = h3_pack(h0, h1);
+    lo = h3_pack(__fsub_rn(a0, h0), __fsub_rn(a1, h1));
+}
+
+__device__ __forceinline__ void h3_mma(uint32_t tmem_d, uint32_t tmem_a, uint64_t db, uint32_t idesc, uint32_t acc) {
+    asm volatile(
+        "{\n .reg .pred p;\n setp.ne.b32 p, %4, 0;\n"
+        " tcgen05.mma.cta_group::1.kind::f16 [%0], [%1], %2, %3, p;\n}\n" ::"r"(tmem_d),
+        "r"(tmem_a), "l"(db), "r"(idesc), "r"(acc));
+}
+__device__ __forceinline__ void h3_mma_pair(uint32_t tmem_d, uint32_t tmem_a, uint64_t db, uint32_t idesc,
+                                            uint32_t acc) {
+    asm volatile(
+        "{\n .reg .pred p;\n setp.ne.b32 p, %4, 0;\n"
+        " tcgen05.mma.cta_group::2.kind::f16 [%0], [%1], %2, %3, p;\n}\n" ::"r"(tmem_d),
+        "r"(tmem_a), "l"(db), "r"(idesc), "r"(acc));
+}
+// 32 lanes x 8 consecutive 32-bit TMEM columns from registers
+__device__ __forceinline__ void h3_st8(uint32_t taddr, const uint32_t (&v)[8]) {
+    asm volatile("tcgen05.st.sync.aligned.32x32b.x8.b32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8};\n" ::"r"(taddr), "r"(v[0]),
+                 "r"(v[1]), "r"(v[2]), "r"(v[3]), "r"(v[4]), "r"(v[5]), "r"(v[6]), "r"(v[7])
+                 : "memory");
+}
+
+__device__ __forceinline__ void h3_sts4(uint32_t a, uint32_t x, uint32_t y, uint32_t z, uint32_t w) {
+    asm volatile("st.shared.v4.b32 [%0], {%1,%2,%3,%4};\n" ::"r"(a), "r"(x), "r"(y), "r"(z), "r"(w) : "memory");
+}
+
+// 16 consecutive K values of one row (K-major SW128 fp32 tile, 128-byte rows)
+// or of one column (MN-major unswizzled [32 k][128] fp32 tile); t is a
+// shared-window address (explicit ld.shared: no generic-address loads)
+template <bool MN>
+__device__ __forceinline__ void h3_load16(uint32_t t, int r, int khalf, float (&v)[16]) {
+    if constexpr (!MN) {
+#pragma unroll
+        for (int c = 0; c < 4; ++c) {
+            const int chunk = (4 * khalf + c) ^ (r & 7);
+            asm volatile("ld.shared.v4.f32 {%0,%1,%2,%3}, [%4];\n"
+                         : "=f"(v[4 * c]), "=f"(v[4 * c + 1]), "=f"(v[4 * c + 2]), "=f"(v[4 * c + 3])
+                         : "r"(t + (uint32_t)(r * 128 + chunk * 16)));
+        }
+    } else {
+#pragma unroll
+        for (int j = 0; j < 16; ++j)
+            asm volatile("ld.shared.f32 %0, [%1];\n" : "=f"(v[j]) : "r"(t + (uint32_t)((16 * khalf + j) * 512 + r * 4)));
+    }
+}
+
+template <bool A_MN, bool B_MN, TcEpi E, bool PAIR>
+__global__ void __launch_bounds__(kH3Threads, 1)
+    k_gemm_h3(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB, TcArgs args) {
+    using Cfg = H3Cfg<PAIR>;
+    constexpr int kS = Cfg::kStages, kL = Cfg::kLand;
+    extern __shared__ uint8_t h3_raw[];
+    uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(h3_raw) + 1023) & ~uintptr_t(1023));
+    uint64_t* bars =
+        reinterpret_cast<uint64_t*>(smem + (size_t)kL * Cfg::kLandBytes + (size_t)kS * Cfg::kF16Bytes);
+    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 32);
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const uint32_t rank = PAIR ? (blockIdx.x & 1u) : 0u;
+    const int m0 = PAIR ? (int)(blockIdx.x >> 1) * 2 * kTcBM + (int)rank * kTcBM : (int)blockIdx.y * kTcBM;
+    const int n0 = PAIR ? (int)blockIdx.y * Cfg::kBN : (int)blockIdx.x * kTcBN;
+    const int nbl = n0 + (int)rank * Cfg::kBLocal;  // this CTA's B columns
+    const int nkb_all = (args.K + kTcBK - 1) / kTcBK;
+    const int kb0 = gridDim.z > 1 ? blockIdx.z * args.kbs : 0;
+    const int kb1 = gridDim.z > 1 ? min(nkb_all, kb0 + args.kbs) : nkb_all;
+    const int nkb = kb1 - kb0;
+    const bool split = gridDim.z > 1;
+    const uint32_t sbase = tc_smem(smem);
+    // barriers: full[kL] (TMA -> split), lempty[kL] (split -> TMA), conv[kS]
+    // (split -> MMA), fempty[kS] (MMA -> split), tmem_full
+    auto full = [&](int l) { return tc_smem(bars + l); };
+    auto lempty = [&](int l) { return tc_smem(bars + kL + l); };
+    auto conv = [&](int s) { return tc_smem(bars + 2 * kL + s); };
+    auto fempty = [&](int s) { return tc_smem(bars + 2 * kL + kS + s); };
+    const uint32_t tmem_full = tc_smem(bars + 2 * kL + 2 * kS);
+    auto landA = [&](int l) { return sbase + (uint32_t)(l * Cfg::kLandBytes); };
+    auto landB = [&](int l) { return sbase + (uint32_t)(l * Cfg::kLandBytes + Cfg::kA32); };
+    const uint32_t f16base = sbase + (uint32_t)(kL * Cfg::kLandBytes);
+    auto tileBh = [&](int s) { return f16base + (uint32_t)(s * Cfg::kF16Bytes); };
+    auto tileBl = [&](int s) { return f16base + (uint32_t)(s * Cfg::kF16Bytes + Cfg::kB16); };
+
+    if (threadIdx.x == 0) {
+        for (int l = 0; l < kL; ++l) {
+            tc_mbar_init(full(l), 1);
+            tc_mbar_init(lempty(l), kH3SplitWarps);
+        }
+        for (int s = 0; s < kS; ++s) {
+            tc_mbar_init(conv(s), kH3SplitWarps);
+            tc_mbar_init(fempty(s), 1);
+        }
+        tc_mbar_init(tmem_full, 1);
+        asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
+        asm volatile("prefetch.tensormap [%0];\n" ::"l"(reinterpret_cast<uint64_t>(&tmA)) : "memory");
+        asm volatile("prefetch.tensormap [%0];\n" ::"l"(reinterpret_cast<uint64_t>(&tmB)) : "memory");
+    }
+    if (warp == 1) {
+        if constexpr (PAIR) {
+            asm volatile("tcgen05.alloc.cta_group::2.sync.aligned.shared::cta.b32 [%0], %1;\n" ::"r"(
+                             tc_smem(tmem_slot)),
+                         "r"(kTcTmemCols));
+            asm volatile("tcgen05.relinquish_alloc_permit.cta_group::2.sync.aligned;\n");
+        } else {
+            asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;\n" ::"r"(
+                             tc_smem(tmem_slot)),
+                         "r"(kTcTmemCols));
+            asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;\n");
+        }
+    }
+    asm volatile("tcgen05.fence::before_thread_sync;\n" ::: "memory");
+    if constexpr (PAIR)
+        tc_cluster_sync();
+    else
+        __syncthreads();
+    asm volatile("tcgen05.fence::after_thread_sync;\n" ::: "memory");
+    const uint32_t tmem = *tmem_slot;
+
+    if (warp == 0) {
+        // ---------------- TMA producer: fp32 A and B tiles ----------------
+        if (lane == 0) {
+            for (int kb = 0; kb < nkb; ++kb) {
+                const int l = kb % kL;
+                const uint32_t ph = (uint32_t)((kb / kL) & 1);
+                tc_mbar_wait(lempty(l), ph ^ 1);
+                tc_mbar_expect_tx(full(l), Cfg::kA32 + Cfg::kB32);
+                const int k0 = (kb0 + kb) * kTcBK;
+                if constexpr (!A_MN)
+                    tc_tma_2d(&tmA, full(l), landA(l), k0, m0);
+                else
+                    tc_tma_2d(&tmA, full(l), landA(l), m0, k0);
+                if constexpr (!B_MN)
+                    tc_tma_2d(&tmB, full(l), landB(l), k0, nbl);
+                else
+                    tc_tma_2d(&tmB, full(l), landB(l), nbl, k0);
+            }
+        }
+    } else if (warp == 1 && rank == 0) {
+        // ---------------- MMA issuer ----------------
+        // instruction descriptor: D f32, A/B f16, both K-major, N>>3, M>>4
+        constexpr uint32_t kM = PAIR ? 2 * kTcBM : kTcBM;
+        constexpr uint32_t idesc = (1u << 4) | ((uint32_t)(Cfg::kBN >> 3) << 17) | ((kM >> 4) << 24);
+        for (int kb = 0; kb < nkb; ++kb) {
+            const int s = kb % kS;
+            const uint32_t ph = (uint32_t)((kb / kS) & 1);
+            tc_mbar_wait(conv(s), ph);
+            asm volatile("tcgen05.fence::after_thread_sync;\n" ::: "memory");
+            if (lane == 0 && !(args.diag & 2)) {
+#pragma unroll
+                for (int ks = 0; ks < kTcBK / 16; ++ks) {
+                    // no swizzle, K-major: core matrices 8 rows x 16 B; the K = 16
+                    // step covers two of them (LBO = 128 B), 8-row groups at 512 B
+                    const uint64_t dBh = tc_desc(tileBh(s) + 256u * ks, 128u, 512u, 0u);
+                    const uint64_t dBl = tc_desc(tileBl(s) + 256u * ks, 128u, 512u, 0u);
+                    const uint32_t tA = tmem + (uint32_t)(Cfg::kBN + 32 * s + 8 * ks);  // A_hi; A_lo at +16
+                    const uint32_t first = (kb == 0 && ks == 0) ? 0u : 1u;
+                    if constexpr (PAIR) {
+                        h3_mma_pair(tmem, tA + 16u, dBh, idesc, first);  // small terms first
+                        h3_mma_pair(tmem, tA, dBl, idesc, 1u);
+                        h3_mma_pair(tmem, tA, dBh, idesc, 1u);
+                    } else {
+                        h3_mma(tmem, tA + 16u, dBh, idesc, first);
+                        h3_mma(tmem, tA, dBl, idesc, 1u);
+                        h3_mma(tmem, tA, dBh, idesc, 1u);
+                    }
+                }
+            }
+            if (lane == 0) {
+                if constexpr (PAIR)
+                    tc_commit_pair(fempty(s));
+                else
+                    tc_commit(fempty(s));
+            }
+            __syncwarp();
+        }
+        if (lane == 0) {
+            if constexpr (PAIR)
+                tc_commit_pair(tmem_full);
+            else
+                tc_commit(tmem_full);
+        }
+        __syncwarp();
+    } else if (warp == 1) {
+        // the pair's second CTA: forward "stage s split done" to rank 0 (see gemm_tc.cuh)
+        if (lane == 0) {
+            const uint32_t src = tc_smem(reinterpret_cast<uint8_t*>(bars) + 464);
+            uint32_t dst, rbar0;
+            asm volatile("mapa.shared::cluster.u32 %0, %1, %2;\n" : "=r"(dst) : "r"(src - 16), "r"(0));
+            asm volatile("mapa.shared::cluster.u32 %0, %1, %2;\n" : "=r"(rbar0) : "r"(conv(0)), "r"(0));
+            for (int kb = 0; kb < nkb; ++kb) {
+                const int s = kb % kS;
+                const uint32_t ph = (uint32_t)((kb / kS) & 1);
+                tc_mbar_wait(conv(s), ph);
+                asm volatile(
+                    "cp.async.bulk.shared::cluster.shared::cta.mbarrier::complete_tx::bytes [%0], [%1], 16, [%2];\n" ::"r"(
+                        dst),
+                    "r"(src), "r"(rbar0 + 8u * (uint32_t)s)
+                    : "memory");
+            }
+        }
+        __syncwarp();
+    } else {
+        // ---------------- split pass, then epilogue (warps 2..17) ----------------
+        const int quarter = warp & 3;       // TMEM lanes this warp may access
+        const int r = quarter * 32 + lane;  // A row of the tile / B column of this CTA's half
+        const bool isB = warp >= 2 + kH3SplitWarps / 2;
+        const int khalf = ((warp - 2) >> 2) & 1;  // K columns [16 khalf, +16) of the block
+        const int ma = m0 + r, nb = nbl + r;
+        const int ea = ma < args.M ? h3_exp(args.amax[ma]) : 0;
+        const int eb = nb < args.N ? h3_exp(args.bmax[nb]) : 0;
+        const float sc = isB ? h3_pow2(14 - eb) : h3_pow2(14 - ea);
+        // this thread's B column in the no-swizzle K-major f16 tiles: row r of
+        // 8-row group r/8, K core matrices 2 khalf, 2 khalf + 1
+        const uint32_t boff = (uint32_t)((r >> 3) * 512 + (2 * khalf) * 128 + (r & 7) * 16);
+        for (int kb = 0; kb < nkb; ++kb) {
+            const int l = kb % kL, s = kb % kS;
+            tc_mbar_wait(full(l), (uint32_t)((kb / kL) & 1));
+            float v[16];
+            uint32_t hi[8], lo[8];
+            if (args.diag & 1) {
+#pragma unroll
+                for (int j = 0; j < 8; ++j) hi[j] = lo[j] = 0u;
+            } else {
+                if (!isB)
+                    h3_load16<A_MN>(landA(l), r, khalf, v);
+                else
+                    h3_load16<B_MN>(landB(l), r, khalf, v);
+#pragma unroll
+                for (int j = 0; j < 8; ++j) h3_split2(v[2 * j], v[2 * j + 1], sc, hi[j], lo[j]);
+            }
+            // landing slot read (the values are consumed above): release it
+            __syncwarp();
+            if (lane == 0) tc_mbar_arrive(lempty(l));
+            // f16 slot s free once the MMAs of K block kb - kS have completed
+            tc_mbar_wait(fempty(s), (uint32_t)(((kb / kS) & 1) ^ 1));
+            asm volatile("tcgen05.fence::after_thread_sync;\n" ::: "memory");
+            if (!isB) {
+                const uint32_t tA =
+                    tmem + ((uint32_t)(quarter * 32) << 16) + (uint32_t)(Cfg::kBN + 32 * s + 8 * khalf);
+                h3_st8(tA, hi);
+                h3_st8(tA + 16u, lo);
+                asm volatile("tcgen05.wait::st.sync.aligned;\n" ::: "memory");
+                asm volatile("tcgen05.fence::before_thread_sync;\n" ::: "memory");
+            } else {
+                const uint32_t bh = tileBh(s) + boff;
+                h3_sts4(bh, hi[0], hi[1], hi[2], hi[3]);
+                h3_sts4(bh + 128, hi[4], hi[5], hi[6], hi[7]);
+                h3_sts4(bh + Cfg::kB16, lo[0], lo[1], lo[2], lo[3]);
+                h3_sts4(bh + Cfg::kB16 + 128, lo[4], lo[5], lo[6], lo[7]);
+                asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");
+            }
+            __syncwarp();
+            if (lane == 0) {
+                if (PAIR && rank == 0 && warp == 2)
+                    tc_mbar_expect_tx(conv(s), 16);  // rank 1's forward (16-byte bulk copy)
+                else
+                    tc_mbar_arrive(conv(s));
+            }
+        }
+        tc_mbar_wait(tmem_full, 0);
+        asm volatile("tcgen05.fence::after_thread_sync;\n" ::: "memory");
+        const int m = ma;
+        const float ia = h3_pow2(ea - 14);
+        constexpr int kCols = Cfg::kBN / (kH3SplitWarps / 4);  // columns per warp
+        const int cbeg = ((warp - 2) >> 2) * kCols;
+#pragma unroll 1
+        for (int c0 = cbeg; c0 < cbeg + kCols; c0 += 32) {
+            uint32_t rr[32];
+            const uint32_t taddr = tmem + ((uint32_t)(quarter * 32) << 16) + (uint32_t)c0;
+            asm volatile(
+                "tcgen05.ld.sync.aligned.32x32b.x32.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,"
+                "%16,%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31}, [%32];\n"
+                : "=r"(rr[0]), "=r"(rr[1]), "=r"(rr[2]), "=r"(rr[3]), "=r"(rr[4]), "=r"(rr[5]), "=r"(rr[6]),
+                  "=r"(rr[7]), "=r"(rr[8]), "=r"(rr[9]), "=r"(rr[10]), "=r"(rr[11]), "=r"(rr[12]), "=r"(rr[13]),
+                  "=r"(rr[14]), "=r"(rr[15]), "=r"(rr[16]), "=r"(rr[17]), "=r"(rr[18]), "=r"(rr[19]),
+                  "=r"(rr[20]), "=r"(rr[21]), "=r"(rr[22]), "=r"(rr[23]), "=r"(rr[24]), "=r"(rr[25]),
+                  "=r"(rr[26]), "=r"(rr[27]), "=r"(rr[28]), "=r"(rr[29]), "=r"(rr[30]), "=r"(rr[31])
+                : "r"(taddr));
+            asm volatile("tcgen05.wait::ld.sync.aligned;\n" ::: "memory");
+            if (m >= args.M) continue;
+            const int nb0 = n0 + c0;
+            // undo the operand scales: two exact power-of-two products
+            float x[32];
+#pragma unroll
+            for (int q = 0; q < 32; ++q) {
+                const int n = nb0 + q;
+                const float ib = n < args.N ? h3_pow2(h3_exp(__ldg(args.bmax + n)) - 14) : 0.0f;
+                x[q] = (__uint_as_float(rr[q]) * ia) * ib;
+            }
+            if (split) {
+                float* P = args.part + (size_t)blockIdx.z * args.M * args.N + (size_t)m * args.N;
+                for (int q = 0; q < 32; ++q)
+                    if (nb0 + q < args.N) P[nb0 + q] = x[q];
+            } else if (nb0 + 32 <= args.N && (args.N & 3) == 0) {
+#pragma unroll
+                for (int q = 0; q < 8; ++q) {
+                    float4 vv = make_float4(x[4 * q], x[4 * q + 1], x[4 * q + 2], x[4 * q + 3]);
+                    float4 t;
+                    vv = tc_epi4<E>(args, m, nb0 + 4 * q, vv, &t);
+                    *reinterpret_cast<float4*>(args.C + (size_t)m * args.N + nb0 + 4 * q) = vv;
+                    if constexpr (E == TcEpi::BIAS_TANH)
+                        *reinterpret_cast<float4*>(args.C2 + (size_t)m * args.N + nb0 + 4 * q) = t;
+                }
+            } else {
+                for (int q = 0; q < 32; ++q) {
+                    const int n = nb0 + q;
+                    if (n >= args.N) break;
+                    float vv = x[q];
+                    const size_t idx = (size_t)m * args.N + n;
+                    if constexpr (E == TcEpi::BIAS || E == TcEpi::BIAS_TANH) vv = sadd(vv, args.bias[n]);
+                    if constexpr (E == TcEpi::TANH_GRAD) vv = tanh_grad(args.aux[idx], vv);
+                    args.C[idx] = vv;
+                    if constexpr (E == TcEpi::BIAS_TANH) args.C2[idx] = tanhf(vv);
+                }
+            }
+        }
+    }
+    asm volatile("tcgen05.fence::before_thread_sync;\n" ::: "memory");
+    if constexpr (PAIR)
+        tc_cluster_sync();
+    else
+        __syncthreads();
+    if (warp == 1) {
+        asm volatile("tcgen05.fence::after_thread_sync;\n" ::: "memory");
+        if constexpr (PAIR)
+            asm volatile("tcgen05.dealloc.cta_group::2.sync.aligned.b32 %0, %1;\n" ::"r"(tmem), "r"(kTcTmemCols));
+        else
+            asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;\n" ::"r"(tmem), "r"(kTcTmemCols));
+    }
+}
+
+// ---- operand maxima (the scales' source) -------------------------------------
+// max |x| of every row of a row-major R x C matrix (C % 4 == 0), as float bits
+// (non-negative floats order like their bit patterns).  One warp per row.
+__global__ void __launch_bounds__(256) k_absmax_rows(const float* __restrict__ X, int R, int C, unsigned* out) {
+    const int row = (blockIdx.x * blockDim.x + threadIdx.x) >> 5, lane = threadIdx.x & 31;
+    if (row >= R) return;
+    const float4* x = reinterpret_cast<const float4*>(X + (size_t)row * C);
+    unsigned m = 0;
+    for (int q = lane; q < C / 4; q += 32) {
+        const float4 v = __ldg(x + q);
+        m = max(m, max(max(__float_as_uint(fabsf(v.x)), __float_as_uint(fabsf(v.y))),
+                       max(__float_as_uint(fabsf(v.z)), __float_as_uint(fabsf(v.w)))));
+    }
+    m = __reduce_max_sync(0xffffffffu, m);
+    if (lane == 0) out[row] = m;
+}
+
+// max |x| of every column (out zeroed beforehand): thread = 4 columns x a chunk
+// of rows, one atomicMax per column per chunk
+constexpr int kAbsmaxRows = 64;
+__global__ void __launch_bounds__(256) k_absmax_cols(const float* __restrict__ X, int R, int C, unsigned* out) {
+    const int c4 = blockIdx.x * blockDim.x + threadIdx.x;
+    if (4 * c4 >= C) return;
+    const int r0 = blockIdx.y * kAbsmaxRows, r1 = min(R, r0 + kAbsmaxRows);
+    unsigned m0 = 0, m1 = 0, m2 = 0, m3 = 0;
+    for (int r = r0; r < r1; ++r) {
+        const float4 v = __ldg(reinterpret_cast<const float4*>(X + (size_t)r * C) + c4);
+        m0 = max(m0, __float_as_uint(fabsf(v.x)));
+        m1 = max(m1, __float_as_uint(fabsf(v.y)));
+        m2 = max(m2, __float_as_uint(fabsf(v.z)));
+        m3 = max(m3, __float_as_uint(fabsf(v.w)));
+    }
+    atomicMax(out + 4 * c4 + 0, m0);
+    atomicMax(out + 4 * c4 + 1, m1);
+    atomicMax(out + 4 * c4 + 2, m2);
+    atomicMax(out + 4 * c4 + 3, m3);
+}
+
+}  // namespace lane_b200
+
+// ---------------------------------------------------------------- host side
+namespace lane_b200 {
+
+// maxima of the rows (rows = true) or columns of a row-major R x C matrix
+inline void absmax_launch(cudaStream_t st, const float* X, int R, int C, bool rows, unsigned* out) {
+    if (rows) {
+        k_absmax_rows<<<(unsigned)((R + 7) / 8), 256, 0, st>>>(X, R, C, out);
+    } else {
+        LANE_CUDA(cudaMemsetAsync(out, 0, (size_t)C * sizeof(unsigned), st));
+        k_absmax_cols<<<dim3((unsigned)((C / 4 + 255) / 256), (unsigned)((R + kAbsmaxRows - 1) / kAbsmaxRows)), 256,
+                        0, st>>>(X, R, C, out);
+    }
+}
+
+template <bool A_MN, bool B_MN, TcEpi E, bool PAIR>
+inline void h3_launch(cudaStream_t st, const CUtensorMap& a, const CUtensorMap& b, const TcArgs& args) {
+    constexpr size_t smem = H3Cfg<PAIR>::kSmem;
+    static std::atomic<uint64_t> configured{0};
+    int dev = 0;
+    LANE_CUDA(cudaGetDevice(&dev));
+    const uint64_t bit = 1ull << (dev & 63);
+    if (!(configured.load(std::memory_order_acquire) & bit)) {
+        LANE_CUDA(cudaFuncSetAttribute(k_gemm_h3<A_MN, B_MN, E, PAIR>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                       (int)smem));
+        configured.fetch_or(bit, std::memory_order_release);
+    }
+    const int S = args.kbs > 0 ? (args.K / kTcBK + args.kbs - 1) / args.kbs : 1;
+    if constexpr (PAIR) {
+        cudaLaunchConfig_t cfg = {};
+        constexpr int kBN = H3Cfg<true>::kBN;
+        cfg.gridDim = dim3(2 * ((args.M + 2 * kTcBM - 1) / (2 * kTcBM)), (args.N + kBN - 1) / kBN, S);
+        cfg.blockDim = dim3(kH3Threads);
+        cfg.dynamicSmemBytes = smem;
+        cfg.stream = st;
+        cudaLaunchAttribute attr[1];
+        attr[0].id = cudaLaunchAttributeClusterDimension;
+        attr[0].val.clusterDim.x = 2;
+        attr[0].val.clusterDim.y = 1;
+        attr[0].val.clusterDim.z = 1;
+        cfg.attrs = attr;
+        cfg.numAttrs = 1;
+        LANE_CUDA(cudaLaunchKernelEx(&cfg, k_gemm_h3<A_MN, B_MN, E, PAIR>, a, b, args));
+    } else {
+        const dim3 grid((args.N + kTcBN - 1) / kTcBN, (args.M + kTcBM - 1) / kTcBM, S);
+        k_gemm_h3<A_MN, B_MN, E, PAIR><<<grid, kH3Threads, smem, st>>>(a, b, args);
+    }
+    if (S > 1) {
+        const size_t n4 = (size_t)args.M * args.N / 4;
+        k_tc_splitk_reduce<E><<<(unsigned)std::min<size_t>(1184, (n4 + 255) / 256), 256, 0, st>>>(args, S);
+    }
+}
+
+template <TcEpi E, bool PAIR>
+inline void h3_dispatch(cudaStream_t st, bool a_mn, bool b_mn, const CUtensorMap& a, const CUtensorMap& b,
+                        const TcArgs& args) {
+    if (!a_mn && !b_mn) h3_launch<false, false, E, PAIR>(st, a, b, args);
+    else if (!a_mn && b_mn) h3_launch<false, true, E, PAIR>(st, a, b, args);
+    else if (a_mn && !b_mn) h3_launch<true, false, E, PAIR>(st, a, b, args);
+    else h3_launch<true, true, E, PAIR>(st, a, b, args);
+}
+
+}  // namespace lane_b200

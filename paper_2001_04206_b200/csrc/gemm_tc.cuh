@@ -66,6 +66,11 @@ struct TcArgs {
     float* C2;          // BIAS_TANH: tanh(C)
     const float* bias;  // BIAS*: per column
     const float* aux;   // TANH_GRAD: activations a (M x N)
+    // 3xF16 kernel (gemm_h3.cuh): max |.| bits of every row of op(A) / column
+    // of op(B), from which the power-of-two operand scales are derived
+    const unsigned* amax = nullptr;
+    const unsigned* bmax = nullptr;
+    int diag = 0;  // experiments (LANE_B200_H3_DIAG): 1 skip the split math, 2 skip the MMAs
 };
 
 // ---- PTX helpers ------------------------------------------------------------
