@@ -37,6 +37,18 @@ struct GemmCtx {
     size_t* counters_count = nullptr;
 };
 
+// 3xF16 operand maxima supplied by the caller (gemm_h3.cuh): a = rows of
+// op(A), b = columns of op(B); orow / ocol (zeroed by the caller) receive the
+// row / column maxima of the output operand the next GEMMs read (tanh(z) for
+// BIAS_TANH, C otherwise) -- fused into the 3xF16 epilogue, or one extra pass
+// when the GEMM runs another kernel.
+struct GemmMax {
+    const unsigned* a = nullptr;
+    const unsigned* b = nullptr;
+    unsigned* orow = nullptr;
+    unsigned* ocol = nullptr;
+};
+
 inline void ensure_ws(GemmCtx& g, size_t count) {
     if (*g.ws_count >= count) return;
     if (*g.ws) LANE_CUDA(cudaFree(*g.ws));
@@ -601,7 +613,7 @@ inline bool tc_use_h3(int M, int N, int K) {
 // workspace tail, then the split-scaled kernel (pairs for the tall shapes,
 // single CTAs with split-K otherwise)
 inline void gemm_h3(GemmCtx& g, GemmOp op, int M, int N, int K, const float* A, const float* B, Epi e, float* C,
-                    float* C2, const float* bias, const float* aux) {
+                    float* C2, const float* bias, const float* aux, const GemmMax* mx, bool* fused_out) {
     const bool pair = M >= 1024 || (M >= 512 && K >= 2048);
     CUtensorMap ma, mb;
     bool a_mn = false, b_mn = false;
@@ -627,7 +639,7 @@ inline void gemm_h3(GemmCtx& g, GemmOp op, int M, int N, int K, const float* A, 
                            : ((M + kTcBM - 1) / kTcBM) * ((N + kTcBN - 1) / kTcBN);
     const int nkb = (K + kTcBK - 1) / kTcBK;
     static const int kbmin = std::getenv("LANE_B200_TC_SPLITK_KBMIN") ? std::atoi(std::getenv("LANE_B200_TC_SPLITK_KBMIN")) : 24;
-    int S = std::min({4, g.sm_count / std::max(1, tiles), nkb / kbmin});
+    int S = std::max(1, std::min({4, g.sm_count / std::max(1, tiles), nkb / kbmin}));
     if (K % kTcBK != 0) S = 1;
     size_t part = 0;
     if (S > 1) {
@@ -641,13 +653,28 @@ inline void gemm_h3(GemmCtx& g, GemmOp op, int M, int N, int K, const float* A, 
     if (S > 1) t.part = ws;
     unsigned* amax = reinterpret_cast<unsigned*>(ws + part);
     unsigned* bmax = amax + M;
-    absmax_launch(g.stream, A, op == GemmOp::TN ? K : M, op == GemmOp::TN ? M : K, op != GemmOp::TN, amax);
-    absmax_launch(g.stream, B, op == GemmOp::NT ? N : K, op == GemmOp::NT ? K : N, op == GemmOp::NT, bmax);
-    t.amax = amax;
-    t.bmax = bmax;
+    if (mx && mx->a) {
+        t.amax = mx->a;
+    } else {
+        absmax_launch(g.stream, A, op == GemmOp::TN ? K : M, op == GemmOp::TN ? M : K, op != GemmOp::TN, amax);
+        t.amax = amax;
+        *g.launches += 1;
+    }
+    if (mx && mx->b) {
+        t.bmax = mx->b;
+    } else {
+        absmax_launch(g.stream, B, op == GemmOp::NT ? N : K, op == GemmOp::NT ? K : N, op == GemmOp::NT, bmax);
+        t.bmax = bmax;
+        *g.launches += 1;
+    }
+    if (mx && mx->orow && S == 1) {
+        t.omax_row = mx->orow;
+        t.omax_col = mx->ocol;
+        *fused_out = true;
+    }
     static const int diag = std::getenv("LANE_B200_H3_DIAG") ? std::atoi(std::getenv("LANE_B200_H3_DIAG")) : 0;
     t.diag = diag;
-    *g.launches += 2 + (S > 1 ? 1 : 0);
+    *g.launches += S > 1 ? 1 : 0;
     switch (e) {
         case Epi::STORE:
             if (pair) h3_dispatch<TcEpi::STORE, true>(g.stream, a_mn, b_mn, ma, mb, t);
@@ -669,16 +696,28 @@ inline void gemm_h3(GemmCtx& g, GemmOp op, int M, int N, int K, const float* A, 
     *g.launches += 1;
 }
 
+// Whether gemm() runs this call on the 3xF16 kernel (the step uses it to
+// decide which operand maxima to provide).
+inline bool gemm_will_h3(GemmOp op, int M, int N, int K, const float* A, int lda, const float* B, int ldb,
+                         const float* C) {
+    if (!gemm_tc_mode() || !tc_eligible(M, N, K) || !tc_use_h3(M, N, K)) return false;
+    if ((reinterpret_cast<uintptr_t>(A) | reinterpret_cast<uintptr_t>(B) | reinterpret_cast<uintptr_t>(C)) & 15)
+        return false;
+    return lda == (op == GemmOp::TN ? M : K) && ldb == (op == GemmOp::NT ? K : N);
+}
+
 // Tensor-core dispatch (gemm_tc.cuh): returns false when the shape/layout is
 // not eligible (the caller then runs the SIMT kernel).
 inline bool gemm_try_tc(GemmCtx& g, GemmOp op, int M, int N, int K, const float* A, int lda, const float* B,
-                        int ldb, Epi e, float* C, float* C2, const float* bias, const float* aux) {
+                        int ldb, Epi e, float* C, float* C2, const float* bias, const float* aux,
+                        const GemmMax* mx = nullptr, bool* fused = nullptr) {
     if (!gemm_tc_mode() || !tc_eligible(M, N, K)) return false;
     if ((reinterpret_cast<uintptr_t>(A) | reinterpret_cast<uintptr_t>(B) | reinterpret_cast<uintptr_t>(C)) & 15)
         return false;
-    if (tc_use_h3(M, N, K)) {
-        if (lda != (op == GemmOp::TN ? M : K) || ldb != (op == GemmOp::NT ? K : N)) return false;
-        gemm_h3(g, op, M, N, K, A, B, e, C, C2, bias, aux);
+    if (gemm_will_h3(op, M, N, K, A, lda, B, ldb, C)) {
+        bool f = false;
+        gemm_h3(g, op, M, N, K, A, B, e, C, C2, bias, aux, mx, &f);
+        if (fused) *fused = f;
         return true;
     }
     CUtensorMap ma, mb;
@@ -808,14 +847,22 @@ inline bool gemm_wgrad_update(GemmCtx& g, int M, int N, int K, const float* A, c
 }
 
 inline void gemm(GemmCtx& g, GemmOp op, int M, int N, int K, const float* A, int lda, const float* B, int ldb,
-                 Epi e, float* C, float* C2, const float* bias, const float* aux) {
+                 Epi e, float* C, float* C2, const float* bias, const float* aux, const GemmMax* mx = nullptr) {
     if (M <= 0 || N <= 0) return;
-    if (gemm_try_tc(g, op, M, N, K, A, lda, B, ldb, e, C, C2, bias, aux)) return;
-    if (gemm_try_skinny(g, op, M, N, K, A, lda, B, ldb, e, C, C2, bias, aux)) return;
-    switch (op) {
-        case GemmOp::NN: gemm_simt_dispatch<GemmOp::NN>(g, M, N, K, A, lda, B, ldb, e, C, C2, bias, aux); break;
-        case GemmOp::NT: gemm_simt_dispatch<GemmOp::NT>(g, M, N, K, A, lda, B, ldb, e, C, C2, bias, aux); break;
-        case GemmOp::TN: gemm_simt_dispatch<GemmOp::TN>(g, M, N, K, A, lda, B, ldb, e, C, C2, bias, aux); break;
+    bool fused = false;
+    if (gemm_try_tc(g, op, M, N, K, A, lda, B, ldb, e, C, C2, bias, aux, mx, &fused)) {
+    } else if (gemm_try_skinny(g, op, M, N, K, A, lda, B, ldb, e, C, C2, bias, aux)) {
+    } else {
+        switch (op) {
+            case GemmOp::NN: gemm_simt_dispatch<GemmOp::NN>(g, M, N, K, A, lda, B, ldb, e, C, C2, bias, aux); break;
+            case GemmOp::NT: gemm_simt_dispatch<GemmOp::NT>(g, M, N, K, A, lda, B, ldb, e, C, C2, bias, aux); break;
+            case GemmOp::TN: gemm_simt_dispatch<GemmOp::TN>(g, M, N, K, A, lda, B, ldb, e, C, C2, bias, aux); break;
+        }
+    }
+    if (mx && mx->orow && !fused) {
+        // the output's maxima in one extra pass (zeroed by the caller)
+        absmax_rc_launch(g.stream, e == Epi::BIAS_TANH ? C2 : C, M, N, mx->orow, mx->ocol);
+        *g.launches += 1;
     }
 }
 

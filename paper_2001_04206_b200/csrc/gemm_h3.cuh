@@ -345,6 +345,11 @@ __global__ void __launch_bounds__(kH3Threads, 1)
         const float ia = h3_pow2(ea - 14);
         constexpr int kCols = Cfg::kBN / (kH3SplitWarps / 4);  // columns per warp
         const int cbeg = ((warp - 2) >> 2) * kCols;
+        // optional maxima of the output operand the next GEMMs consume (tanh(z)
+        // for BIAS_TANH, C otherwise): per row (atomicMax once per thread) and
+        // per column (warp max over this warp's 32 rows, one atomicMax per lane)
+        const bool omax = args.omax_row != nullptr && !split;
+        unsigned rmax = 0;
 #pragma unroll 1
         for (int c0 = cbeg; c0 < cbeg + kCols; c0 += 32) {
             uint32_t rr[32];
@@ -359,8 +364,8 @@ __global__ void __launch_bounds__(kH3Threads, 1)
                   "=r"(rr[26]), "=r"(rr[27]), "=r"(rr[28]), "=r"(rr[29]), "=r"(rr[30]), "=r"(rr[31])
                 : "r"(taddr));
             asm volatile("tcgen05.wait::ld.sync.aligned;\n" ::: "memory");
-            if (m >= args.M) continue;
             const int nb0 = n0 + c0;
+            if (nb0 >= args.N) continue;  // warp-uniform
             // undo the operand scales: two exact power-of-two products
             float x[32];
 #pragma unroll
@@ -369,33 +374,64 @@ __global__ void __launch_bounds__(kH3Threads, 1)
                 const float ib = n < args.N ? h3_pow2(h3_exp(__ldg(args.bmax + n)) - 14) : 0.0f;
                 x[q] = (__uint_as_float(rr[q]) * ia) * ib;
             }
+            const bool mrow = m < args.M;
             if (split) {
-                float* P = args.part + (size_t)blockIdx.z * args.M * args.N + (size_t)m * args.N;
-                for (int q = 0; q < 32; ++q)
-                    if (nb0 + q < args.N) P[nb0 + q] = x[q];
-            } else if (nb0 + 32 <= args.N && (args.N & 3) == 0) {
+                if (mrow) {
+                    float* P = args.part + (size_t)blockIdx.z * args.M * args.N + (size_t)m * args.N;
+                    for (int q = 0; q < 32; ++q)
+                        if (nb0 + q < args.N) P[nb0 + q] = x[q];
+                }
+                continue;
+            }
+            uint32_t ob[32];  // |consumed output| bits (0 past M / N)
+            if (nb0 + 32 <= args.N && (args.N & 3) == 0) {
 #pragma unroll
                 for (int q = 0; q < 8; ++q) {
                     float4 vv = make_float4(x[4 * q], x[4 * q + 1], x[4 * q + 2], x[4 * q + 3]);
-                    float4 t;
-                    vv = tc_epi4<E>(args, m, nb0 + 4 * q, vv, &t);
-                    *reinterpret_cast<float4*>(args.C + (size_t)m * args.N + nb0 + 4 * q) = vv;
-                    if constexpr (E == TcEpi::BIAS_TANH)
-                        *reinterpret_cast<float4*>(args.C2 + (size_t)m * args.N + nb0 + 4 * q) = t;
+                    float4 t = make_float4(0.f, 0.f, 0.f, 0.f);
+                    if (mrow) {
+                        vv = tc_epi4<E>(args, m, nb0 + 4 * q, vv, &t);
+                        *reinterpret_cast<float4*>(args.C + (size_t)m * args.N + nb0 + 4 * q) = vv;
+                        if constexpr (E == TcEpi::BIAS_TANH)
+                            *reinterpret_cast<float4*>(args.C2 + (size_t)m * args.N + nb0 + 4 * q) = t;
+                    }
+                    const float4 o = E == TcEpi::BIAS_TANH ? t : vv;
+                    ob[4 * q + 0] = mrow ? __float_as_uint(fabsf(o.x)) : 0u;
+                    ob[4 * q + 1] = mrow ? __float_as_uint(fabsf(o.y)) : 0u;
+                    ob[4 * q + 2] = mrow ? __float_as_uint(fabsf(o.z)) : 0u;
+                    ob[4 * q + 3] = mrow ? __float_as_uint(fabsf(o.w)) : 0u;
                 }
             } else {
+#pragma unroll
                 for (int q = 0; q < 32; ++q) {
                     const int n = nb0 + q;
-                    if (n >= args.N) break;
+                    ob[q] = 0u;
+                    if (n >= args.N || !mrow) continue;
                     float vv = x[q];
                     const size_t idx = (size_t)m * args.N + n;
                     if constexpr (E == TcEpi::BIAS || E == TcEpi::BIAS_TANH) vv = sadd(vv, args.bias[n]);
                     if constexpr (E == TcEpi::TANH_GRAD) vv = tanh_grad(args.aux[idx], vv);
                     args.C[idx] = vv;
-                    if constexpr (E == TcEpi::BIAS_TANH) args.C2[idx] = tanhf(vv);
+                    float o = vv;
+                    if constexpr (E == TcEpi::BIAS_TANH) {
+                        o = tanhf(vv);
+                        args.C2[idx] = o;
+                    }
+                    ob[q] = __float_as_uint(fabsf(o));
                 }
             }
+            if (omax) {
+                unsigned mine = 0;
+#pragma unroll
+                for (int q = 0; q < 32; ++q) {
+                    rmax = max(rmax, ob[q]);
+                    const unsigned cm = __reduce_max_sync(0xffffffffu, ob[q]);
+                    if (lane == q) mine = cm;
+                }
+                if (nb0 + lane < args.N) atomicMax(args.omax_col + nb0 + lane, mine);
+            }
         }
+        if (omax && m < args.M) atomicMax(args.omax_row + m, rmax);
     }
     asm volatile("tcgen05.fence::before_thread_sync;\n" ::: "memory");
     if constexpr (PAIR)
@@ -449,10 +485,53 @@ __global__ void __launch_bounds__(256) k_absmax_cols(const float* __restrict__ X
     atomicMax(out + 4 * c4 + 3, m3);
 }
 
+// max |x| of every row AND every column of a row-major R x C matrix in one
+// pass (both zeroed beforehand): thread = 4 columns x kAbsmaxRows rows, rows
+// loaded 8 at a time (memory-level parallelism); a row's partial over the
+// warp's 128 columns is one redux + one atomicMax
+__global__ void __launch_bounds__(256) k_absmax_rc(const float* __restrict__ X, int R, int C, unsigned* rows,
+                                                   unsigned* cols) {
+    const int c4 = blockIdx.x * blockDim.x + threadIdx.x;
+    const bool on = 4 * c4 < C;
+    const int r0 = blockIdx.y * kAbsmaxRows, r1 = min(R, r0 + kAbsmaxRows);
+    unsigned m0 = 0, m1 = 0, m2 = 0, m3 = 0;
+    for (int rb = r0; rb < r1; rb += 8) {
+        float4 v[8];
+#pragma unroll
+        for (int j = 0; j < 8; ++j)
+            v[j] = (on && rb + j < r1) ? __ldg(reinterpret_cast<const float4*>(X + (size_t)(rb + j) * C) + c4)
+                                       : make_float4(0.f, 0.f, 0.f, 0.f);
+#pragma unroll
+        for (int j = 0; j < 8; ++j) {
+            const unsigned a = __float_as_uint(fabsf(v[j].x)), b = __float_as_uint(fabsf(v[j].y));
+            const unsigned c = __float_as_uint(fabsf(v[j].z)), d = __float_as_uint(fabsf(v[j].w));
+            m0 = max(m0, a);
+            m1 = max(m1, b);
+            m2 = max(m2, c);
+            m3 = max(m3, d);
+            const unsigned rm = __reduce_max_sync(0xffffffffu, max(max(a, b), max(c, d)));
+            if ((threadIdx.x & 31) == j && rb + j < r1 && rm) atomicMax(rows + rb + j, rm);
+        }
+    }
+    if (on) {
+        atomicMax(cols + 4 * c4 + 0, m0);
+        atomicMax(cols + 4 * c4 + 1, m1);
+        atomicMax(cols + 4 * c4 + 2, m2);
+        atomicMax(cols + 4 * c4 + 3, m3);
+    }
+}
+
 }  // namespace lane_b200
 
 // ---------------------------------------------------------------- host side
 namespace lane_b200 {
+
+// row and column maxima of a row-major R x C matrix (C % 4 == 0) into zeroed
+// `rows` / `cols`
+inline void absmax_rc_launch(cudaStream_t st, const float* X, int R, int C, unsigned* rows, unsigned* cols) {
+    k_absmax_rc<<<dim3((unsigned)((C / 4 + 255) / 256), (unsigned)((R + kAbsmaxRows - 1) / kAbsmaxRows)), 256, 0,
+                  st>>>(X, R, C, rows, cols);
+}
 
 // maxima of the rows (rows = true) or columns of a row-major R x C matrix
 inline void absmax_launch(cudaStream_t st, const float* X, int R, int C, bool rows, unsigned* out) {

@@ -71,6 +71,10 @@ struct TcArgs {
     const unsigned* amax = nullptr;
     const unsigned* bmax = nullptr;
     int diag = 0;  // experiments (LANE_B200_H3_DIAG): 1 skip the split math, 2 skip the MMAs
+    // 3xF16 epilogue (optional): max |.| bits of every row / column of the
+    // output operand the next GEMMs read (zeroed by the caller)
+    unsigned* omax_row = nullptr;
+    unsigned* omax_col = nullptr;
 };
 
 // ---- PTX helpers ------------------------------------------------------------

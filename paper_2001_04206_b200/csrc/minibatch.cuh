@@ -46,6 +46,8 @@ struct MinibatchState {
     size_t counters_count = 0;
     cudaStream_t comm_stream = nullptr;  // per-layer gradient allreduces (data parallel)
     std::vector<cudaEvent_t> ev;         // one per layer + the join
+    unsigned* stats = nullptr;           // 3xF16 operand maxima (MbStats)
+    size_t stats_count = 0;
 };
 
 inline void minibatch_free(MinibatchState& s) {
@@ -55,6 +57,9 @@ inline void minibatch_free(MinibatchState& s) {
     if (s.counters) cudaFree(s.counters);
     s.counters = nullptr;
     s.counters_count = 0;
+    if (s.stats) cudaFree(s.stats);
+    s.stats = nullptr;
+    s.stats_count = 0;
     for (cudaEvent_t e : s.ev) cudaEventDestroy(e);
     s.ev.clear();
     if (s.comm_stream) cudaStreamDestroy(s.comm_stream);
@@ -300,6 +305,43 @@ void minibatch_stage(Ctx& c, Net& net, const float* X, const float* T, size_t Bs
 // on the communication stream right after its wgrad and overlaps every
 // remaining dgrad and wgrad; the compute stream joins the communication stream
 // at the end.  Capturable in a CUDA graph.
+// Operand maxima of the 3xF16 GEMMs (gemm_h3.cuh), per layer l with input
+// width I and output width O: rows / columns of the layer input act_l (B, I),
+// of W_l (I, O) and of the layer's output deltas D_l (B, O).  Produced once per
+// step -- W_l and act_0 by one pass each, act_{l+1} and D_{l-1} by the
+// epilogues of the GEMMs that write them -- instead of two passes per GEMM.
+struct MbStats {
+    std::vector<unsigned*> act_row, act_col, w_row, w_col, d_row, d_col;
+};
+
+template <class Net>
+MbStats minibatch_stats(Net& net, size_t B, GemmCtx& g, cudaStream_t st) {
+    const int nl = static_cast<int>(net.layers.size());
+    size_t need = 0;
+    for (int l = 0; l < nl; ++l) need += 2 * B + 2 * net.L(l).I + 2 * net.L(l).O;
+    auto& M = net.mb;
+    if (M.stats_count < need) {
+        if (M.stats) LANE_CUDA(cudaFree(M.stats));
+        LANE_CUDA(cudaMalloc(reinterpret_cast<void**>(&M.stats), need * sizeof(unsigned)));
+        M.stats_count = need;
+        ++M.ws_gen;  // captured step graphs hold the old pointer
+    }
+    (void)g;
+    LANE_CUDA(cudaMemsetAsync(M.stats, 0, need * sizeof(unsigned), st));
+    MbStats S;
+    unsigned* p = M.stats;
+    for (int l = 0; l < nl; ++l) {
+        const size_t I = net.L(l).I, O = net.L(l).O;
+        S.act_row.push_back(p), p += B;
+        S.act_col.push_back(p), p += I;
+        S.w_row.push_back(p), p += I;
+        S.w_col.push_back(p), p += O;
+        S.d_row.push_back(p), p += B;
+        S.d_col.push_back(p), p += O;
+    }
+    return S;
+}
+
 struct FusedUpdate {
     float inv_b, eta, mu;
     bool fused_w[kMaxUpdSpans];  // out: layer l's weights were updated by its wgrad epilogue
@@ -314,15 +356,61 @@ void minibatch_grads_body(Ctx& c, Net& net, size_t Bsz, double* loss_sum, bool a
     cudaStream_t st = c.stream;
     GemmCtx g{c.stream,   c.sm_count,        &net.mb.ws,       &net.mb.ws_count, &c.launches,
               &net.mb.ws_gen, &net.mb.counters, &net.mb.counters_count};
+    // which GEMMs run on the 3xF16 kernel, and so which operand maxima exist
+    auto input = [&](int l) {
+        return l == 0 ? net.L(0).buf[LANE_BUF_INPUTS] : net.L(l - 1).buf[LANE_BUF_OUTPUTS];
+    };
+    auto fwd_h3 = [&](int l) {
+        auto& Ly = net.L(l);
+        return gemm_will_h3(GemmOp::NN, B, (int)Ly.O, (int)Ly.I, input(l), (int)Ly.I, Ly.buf[LANE_BUF_W], (int)Ly.O,
+                            Ly.buf[LANE_BUF_NETIN]);
+    };
+    auto dgrad_h3 = [&](int l) {  // l >= 1: D_{l-1} = D_l W_l^T
+        if (l < 1) return false;
+        auto& Ly = net.L(l);
+        auto& pv = net.L(l - 1);
+        return gemm_will_h3(GemmOp::NT, B, (int)pv.O, (int)Ly.O, Ly.buf[LANE_BUF_DELTAS], (int)Ly.O,
+                                      Ly.buf[LANE_BUF_W], (int)Ly.O, pv.buf[LANE_BUF_DELTAS]);
+    };
+    auto wgrad_h3 = [&](int l) {
+        auto& Ly = net.L(l);
+        return gemm_will_h3(GemmOp::TN, (int)Ly.I, (int)Ly.O, B, input(l), (int)Ly.I, Ly.buf[LANE_BUF_DELTAS],
+                            (int)Ly.O, Ly.buf[LANE_BUF_G]);
+    };
+    bool any_h3 = false;
+    for (int l = 0; l < nl; ++l) any_h3 = any_h3 || fwd_h3(l) || dgrad_h3(l) || wgrad_h3(l);
+    MbStats S;
+    if (any_h3) {
+        S = minibatch_stats(net, Bsz, g, st);
+        for (int l = 0; l < nl; ++l)
+            if (fwd_h3(l) || dgrad_h3(l)) {
+                absmax_rc_launch(st, net.L(l).buf[LANE_BUF_W], (int)net.L(l).I, (int)net.L(l).O, S.w_row[l],
+                                 S.w_col[l]);
+                c.launches += 1;
+            }
+        if (fwd_h3(0) || wgrad_h3(0)) {
+            absmax_rc_launch(st, input(0), B, (int)net.L(0).I, S.act_row[0], S.act_col[0]);
+            c.launches += 1;
+        }
+    }
     // forward
     for (int l = 0; l < nl; ++l) {
         auto& Ly = net.L(l);
         // layer l > 0 reads the previous layer's outputs in place (no copy)
-        const float* in = l == 0 ? net.L(0).buf[LANE_BUF_INPUTS] : net.L(l - 1).buf[LANE_BUF_OUTPUTS];
+        const float* in = input(l);
         const bool last = l == nl - 1;
+        GemmMax mx;
+        if (fwd_h3(l)) {
+            mx.a = S.act_row[l];
+            mx.b = S.w_col[l];
+        }
+        if (!last && (fwd_h3(l + 1) || wgrad_h3(l + 1))) {
+            mx.orow = S.act_row[l + 1];
+            mx.ocol = S.act_col[l + 1];
+        }
         gemm(g, GemmOp::NN, B, (int)Ly.O, (int)Ly.I, in, (int)Ly.I, Ly.buf[LANE_BUF_W], (int)Ly.O,
              last ? Epi::BIAS : Epi::BIAS_TANH, Ly.buf[LANE_BUF_NETIN], Ly.buf[LANE_BUF_OUTPUTS],
-             Ly.buf[LANE_BUF_B], nullptr);
+             Ly.buf[LANE_BUF_B], nullptr, &mx);
     }
     auto& out = net.L(nl - 1);
     ensure_ws(g, (size_t)B);  // per-row losses live in the GEMM workspace between GEMMs
@@ -344,8 +432,25 @@ void minibatch_grads_body(Ctx& c, Net& net, size_t Bsz, double* loss_sum, bool a
         // dgrad with the pre-update weights: D_{l-1} = (D_l W_l^T) * (1 - A_{l-1}^2)
         auto& Ly = net.L(l);
         auto& pv = net.L(l - 1);
+        GemmMax mx;
+        if (dgrad_h3(l)) {
+            mx.a = S.d_row[l];
+            mx.b = S.w_row[l];
+        }
+        if (dgrad_h3(l - 1) || wgrad_h3(l - 1)) {
+            mx.orow = S.d_row[l - 1];
+            mx.ocol = S.d_col[l - 1];
+        }
         gemm(g, GemmOp::NT, B, (int)pv.O, (int)Ly.O, Ly.buf[LANE_BUF_DELTAS], (int)Ly.O, Ly.buf[LANE_BUF_W],
-             (int)Ly.O, Epi::TANH_GRAD, pv.buf[LANE_BUF_DELTAS], nullptr, nullptr, pv.buf[LANE_BUF_OUTPUTS]);
+             (int)Ly.O, Epi::TANH_GRAD, pv.buf[LANE_BUF_DELTAS], nullptr, nullptr, pv.buf[LANE_BUF_OUTPUTS], &mx);
+    };
+    auto wgrad_mx = [&](int l) {
+        GemmMax mx;
+        if (wgrad_h3(l)) {
+            mx.a = S.act_col[l];
+            mx.b = S.d_col[l];
+        }
+        return mx;
     };
     for (int l = nl - 1; l >= 0; --l) {
         auto& Ly = net.L(l);
@@ -359,15 +464,18 @@ void minibatch_grads_body(Ctx& c, Net& net, size_t Bsz, double* loss_sum, bool a
             fused->fused_w[l] = gemm_wgrad_update(g, (int)Ly.I, (int)Ly.O, B, in, Ly.buf[LANE_BUF_DELTAS],
                                                             Ly.buf[LANE_BUF_G], W, V, fused->inv_b, -fused->eta,
                                                             fused->mu);
-            if (!fused->fused_w[l])
+            if (!fused->fused_w[l]) {
+                const GemmMax mx = wgrad_mx(l);
                 gemm(g, GemmOp::TN, (int)Ly.I, (int)Ly.O, B, in, (int)Ly.I, Ly.buf[LANE_BUF_DELTAS], (int)Ly.O,
-                     Epi::STORE, Ly.buf[LANE_BUF_G], nullptr, nullptr, nullptr);
+                     Epi::STORE, Ly.buf[LANE_BUF_G], nullptr, nullptr, nullptr, &mx);
+            }
             colsum(g, Ly.buf[LANE_BUF_DELTAS], B, (int)Ly.O, Ly.buf[LANE_BUF_BIAS_GRAD]);
             continue;
         }
         // wgrad sums: G_l = X_l^T D_l ; gb_l = colsum(D_l)
+        const GemmMax mx = wgrad_mx(l);
         gemm(g, GemmOp::TN, (int)Ly.I, (int)Ly.O, B, in, (int)Ly.I, Ly.buf[LANE_BUF_DELTAS], (int)Ly.O, Epi::STORE,
-             Ly.buf[LANE_BUF_G], nullptr, nullptr, nullptr);
+             Ly.buf[LANE_BUF_G], nullptr, nullptr, nullptr, &mx);
         colsum(g, Ly.buf[LANE_BUF_DELTAS], B, (int)Ly.O, Ly.buf[LANE_BUF_BIAS_GRAD]);
         if (allreduce) {
             // layer l's G and bias pieces: one contiguous span of the grads arena
