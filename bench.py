@@ -318,6 +318,8 @@ def run_minibatch(args, wl):
         parallel.init_comm(dev, rank, world)
     rows = BG // world
     net = lane.build_network(F, H, C, seed=42, device=dev, max_batch=rows)
+    if world > 1 and args.exchange == "nvls":
+        parallel.init_nvls(net, rank, world, tag=os.environ.get("MASTER_PORT", "bench"))
     trainer = parallel.DataParallelTrainer(net, eta, mu, BG, rank, world)
     X, T = po.synthetic_dataset(F, C, nb * BG, 9)
     xd, td = dev.alloc(X.nbytes), dev.alloc(T.nbytes)
@@ -402,6 +404,7 @@ def run_minibatch(args, wl):
             "data": "synthetic",
             "config": {"workload": wl, "description": desc, "layers": widths, "global_batch": BG,
                        "rows_per_rank": rows, "momentum": mu, "eta": eta, "parallelism": f"dp{world}",
+                       "exchange": (args.exchange if world > 1 else "none"),
                        "gemm": gemm_desc,
                        "l2": "256 MB buffer written between timed steps"},
             "roofline": {"bound": "tensor", "kernel": kernel, "achieved": gemm_tf, "peak": peak,
@@ -503,6 +506,9 @@ def main():
     ap.add_argument("--workload", default="c5", choices=sorted(WORKLOADS) + sorted(MINIBATCH))
     ap.add_argument("--epoch", type=int, default=0, help="override samples per step")
     ap.add_argument("--no-cpu", action="store_true", help="skip the cpu_baseline leg")
+    ap.add_argument("--exchange", default="nccl", choices=["nccl", "nvls"],
+                    help="mini-batch gradient exchange at N > 1: per-layer NCCL allreduces (default) or the "
+                         "NVLS fused switch-reduce + update (csrc/nvls.cuh; needs a fabric-attached node)")
     ap.add_argument("--paper-table", action="store_true",
                     help="the paper's per-kernel lane-bench table (reference serial/parallel + b200)")
     ap.add_argument("--fc-neurons", type=int, default=100000, help="--paper-table hidden width")

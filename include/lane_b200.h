@@ -299,6 +299,25 @@ int lane_b200_comm_destroy(lane_b200_ctx* ctx);
  * gradients of every layer) over the context's communicator. */
 int lane_b200_allreduce_grads(lane_b200_net* net);
 
+/* NVLink SHARP: the gradient exchange fused with the update
+ * (csrc/nvls.cuh).  Once a network is NVLS-bound, lane_b200_minibatch_step /
+ * lane_b200_train_minibatch reduce the gradient sums through the NVSwitch
+ * (multimem.ld_reduce) and broadcast the updated W / velocities / mean
+ * gradients (multimem.st), each rank one slice, instead of an NCCL allreduce
+ * followed by a full local update; B_global = rows per step x world.
+ * Sequence: rank 0 _nvls_create (exports a POSIX fd; fd_out may be NULL for a
+ * single rank); every rank _nvls_attach (ranks != 0 import rank 0's fd);
+ * a host barrier; every rank _nvls_bind; a host barrier.  *out = 1 when the
+ * device supports multicast objects. */
+int lane_b200_nvls_supported(lane_b200_ctx* ctx, int* out);
+int lane_b200_nvls_create(lane_b200_net* net, int world, int* fd_out);
+int lane_b200_nvls_attach(lane_b200_net* net, int rank, int world, int fd);
+int lane_b200_nvls_bind(lane_b200_net* net);
+/* *multicast = 1 (bound to a multicast object), 0 (one rank, "local": the GPU
+ * slice could not create a multicast object, so the same slice / update /
+ * barrier kernels run with plain memory operations), -1 (not bound). */
+int lane_b200_nvls_mode(lane_b200_net* net, int* multicast);
+
 #ifdef __cplusplus
 }
 #endif

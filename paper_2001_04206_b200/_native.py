@@ -73,6 +73,11 @@ SIGNATURES = {
     "lane_b200_comm_init": (_I, [_V, _I, _I, _V, _S]),
     "lane_b200_comm_destroy": (_I, [_V]),
     "lane_b200_allreduce_grads": (_I, [_V]),
+    "lane_b200_nvls_supported": (_I, [_V, C.POINTER(_I)]),
+    "lane_b200_nvls_create": (_I, [_V, _I, C.POINTER(_I)]),
+    "lane_b200_nvls_attach": (_I, [_V, _I, _I, _I]),
+    "lane_b200_nvls_bind": (_I, [_V]),
+    "lane_b200_nvls_mode": (_I, [_V, C.POINTER(_I)]),
 }
 
 

@@ -21,6 +21,7 @@
 #include "common.cuh"
 #include "layer_kernels.cuh"
 #include "minibatch.cuh"
+#include "nvls.cuh"
 #include "pipeline.cuh"
 #include "sgd_persistent.cuh"
 #include "sgd_window.cuh"
@@ -203,6 +204,7 @@ struct lane_b200_net {
     uint32_t* order = nullptr;
     size_t order_count = 0;
     MinibatchState mb;  // activations + workspaces of the mini-batch path
+    NvlsState nvls;     // NVLS-bound arena (data parallel over NVSwitch multicast)
     MbGraph mb_graph;   // captured mini-batch step (per configuration)
     InputPipeline pipe;  // pinned staging + copy stream of train_minibatch
     std::vector<cudaEvent_t> plan_events;  // backward_plan_run_timed
@@ -1156,7 +1158,12 @@ int lane_b200_net_destroy(lane_b200_net* net) {
         cudaSetDevice(net->ctx->device);
         cudaStreamSynchronize(net->ctx->stream);
         minibatch_free(net->mb);
-        cudaFree(net->arena);
+        if (net->nvls.bound) {
+            nvls_release(net->nvls);  // the arena lives in the NVLS mapping
+        } else {
+            if (net->nvls.mc) nvls_release(net->nvls);
+            cudaFree(net->arena);
+        }
         cudaFree(net->scratch);
         cudaFree(net->step);
         cudaFree(net->loss_dev);
@@ -1850,6 +1857,75 @@ int lane_b200_allreduce_grads(lane_b200_net* net) {
     return guard([&] {
         if (!net) throw Error(LANE_ERR_CONFIG, "null network");
         allreduce_grads(net->ctx->comm, net->grads, net->grads_count, net->ctx->stream);
+    });
+}
+
+int lane_b200_nvls_supported(lane_b200_ctx* c, int* out) {
+    return guard([&] {
+        if (!c || !out) throw Error(LANE_ERR_CONFIG, "null argument");
+        *out = nvls_supported(c->device) ? 1 : 0;
+    });
+}
+
+// the arena plus one 256-byte barrier counter, multicast-bound
+static size_t nvls_arena_bytes(const lane_b200_net* net) { return net->arena_bytes + 256; }
+
+int lane_b200_nvls_create(lane_b200_net* net, int world, int* fd_out) {
+    return guard([&] {
+        if (!net || world < 1) throw Error(LANE_ERR_CONFIG, "nvls_create: bad arguments");
+        if (net->nvls.mc || net->nvls.local) throw Error(LANE_ERR_CONFIG, "nvls_create: already created");
+        LANE_CUDA(cudaSetDevice(net->ctx->device));
+        nvls_create(net->nvls, net->ctx->device, world, nvls_arena_bytes(net));
+        if (fd_out) *fd_out = nvls_export_fd(net->nvls);
+    });
+}
+
+int lane_b200_nvls_attach(lane_b200_net* net, int rank, int world, int fd) {
+    return guard([&] {
+        if (!net || world < 1 || rank < 0 || rank >= world) throw Error(LANE_ERR_CONFIG, "nvls_attach: bad rank/world");
+        LANE_CUDA(cudaSetDevice(net->ctx->device));
+        if (rank != 0) {
+            if (net->nvls.mc) throw Error(LANE_ERR_CONFIG, "nvls_attach: already attached");
+            nvls_import(net->nvls, net->ctx->device, world, nvls_arena_bytes(net), fd);
+        } else if ((!net->nvls.mc && !net->nvls.local) || net->nvls.world != world) {
+            throw Error(LANE_ERR_CONFIG, "nvls_attach: rank 0 must nvls_create first (same world)");
+        }
+        nvls_add_device(net->nvls, rank);
+    });
+}
+
+int lane_b200_nvls_mode(lane_b200_net* net, int* multicast) {
+    return guard([&] {
+        if (!net || !multicast) throw Error(LANE_ERR_CONFIG, "null argument");
+        *multicast = !net->nvls.bound ? -1 : net->nvls.local ? 0 : 1;
+    });
+}
+
+int lane_b200_nvls_bind(lane_b200_net* net) {
+    return guard([&] {
+        if (!net || !net->nvls.attached || net->nvls.bound) throw Error(LANE_ERR_CONFIG, "nvls_bind: not attached");
+        auto* c = net->ctx;
+        LANE_CUDA(cudaSetDevice(c->device));
+        LANE_CUDA(cudaStreamSynchronize(c->stream));
+        char* old = net->arena;
+        char* base = nvls_bind(net->nvls);
+        // move the arena (weights, velocities, activations) into the bound memory
+        LANE_CUDA(cudaMemcpy(base, old, net->arena_bytes, cudaMemcpyDeviceToDevice));
+        LANE_CUDA(cudaMemset(base + net->arena_bytes, 0, 256));  // barrier counter
+        auto rebase = [&](auto*& p) {
+            using T = std::remove_reference_t<decltype(*p)>;
+            char* q = reinterpret_cast<char*>(p);
+            if (q >= old && q < old + net->arena_bytes) p = reinterpret_cast<T*>(base + (q - old));
+        };
+        for (auto& Ly : net->layers)
+            for (auto& b : Ly.buf) rebase(b);
+        rebase(net->params);
+        rebase(net->grads);
+        rebase(net->target_stage);
+        net->arena = base;
+        net->mb_graph.reset();
+        LANE_CUDA(cudaFree(old));
+        LANE_CUDA(cudaDeviceSynchronize());
     });
 }
 

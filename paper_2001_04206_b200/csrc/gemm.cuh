@@ -336,6 +336,36 @@ __global__ void k_sum_partials(const float* __restrict__ part, int S, size_t cou
     }
 }
 
+// Many partials (S >= 16): CTA = 32 consecutive elements x 8 partial groups
+// (warp w sums partials w, w + 8, ... in order, lane = element), the 8 group
+// sums meet in shared memory in a fixed order -- deterministic, and S / 8
+// dependent loads per thread instead of S.
+__global__ void __launch_bounds__(256) k_sum_partials_wide(const float* __restrict__ part, int S, size_t count,
+                                                           float* __restrict__ out) {
+    __shared__ float red[8][33];
+    const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+    const size_t e = (size_t)blockIdx.x * 32 + lane;
+    float v = 0.0f;
+    if (e < count)
+        for (int s = w; s < S; s += 8) v += __ldg(part + (size_t)s * count + e);
+    red[w][lane] = v;
+    __syncthreads();
+    if (w == 0 && e < count) {
+        float t = red[0][lane];
+#pragma unroll
+        for (int q = 1; q < 8; ++q) t += red[q][lane];
+        out[e] = t;
+    }
+}
+
+inline void sum_partials(GemmCtx& g, const float* part, int S, size_t count, float* out) {
+    if (S >= 16)
+        k_sum_partials_wide<<<(unsigned)((count + 31) / 32), 256, 0, g.stream>>>(part, S, count, out);
+    else
+        k_sum_partials<<<std::max(1, (int)std::min<size_t>(4 * g.sm_count, (count + 255) / 256)), 256, 0,
+                         g.stream>>>(part, S, count, out);
+}
+
 // Column sums gb[o] = sum_b D[b][o], two passes (row chunks, then fixed-order
 // reduction) so tall batches keep every SM busy.
 constexpr int kColChunk = 32;
@@ -389,7 +419,7 @@ inline void colsum(GemmCtx& g, const float* D, int B, int O, float* gb) {
     const int S = (B + kColChunk - 1) / kColChunk;
     ensure_ws(g, (size_t)S * O);
     k_colsum_part<<<dim3((O + 127) / 128, S), 128, 0, g.stream>>>(D, B, O, *g.ws);
-    k_sum_partials<<<std::max(1, std::min(4 * g.sm_count, (O + 255) / 256)), 256, 0, g.stream>>>(*g.ws, S, O, gb);
+    sum_partials(g, *g.ws, S, (size_t)O, gb);
     *g.launches += 2;
 }
 

@@ -22,6 +22,7 @@
 
 #include "common.cuh"
 #include "gemm.cuh"
+#include "nvls.cuh"
 
 namespace lane_b200 {
 
@@ -546,8 +547,52 @@ void minibatch_update(Ctx& c, Net& net, size_t B_global, float eta, float mu, co
 // backward), then every rank applies the identical update with
 // B_global = B * world.  (LANE_B200_MB_BUCKETS=1 forces the allreduce path on
 // a one-rank communicator, where NCCL's sum is the identity.)
+// NVLS-bound network (nvls.cuh): barrier (every rank's gradient sums are
+// written), this rank's slice of the fused switch-reduce + update + multicast
+// store, barrier (every rank's stores have landed before the next forward).
+template <class Ctx, class Net>
+void minibatch_update_nvls(Ctx& c, Net& net, size_t B_global, float eta, float mu) {
+    NvlsState& S = net.nvls;
+    const size_t off_flag = net.arena_bytes;  // the counter after the arena
+    unsigned* uc_flag = reinterpret_cast<unsigned*>(reinterpret_cast<char*>(S.uc) + off_flag);
+    unsigned* mc_flag = reinterpret_cast<unsigned*>(reinterpret_cast<char*>(S.mcva) + off_flag);
+    auto mc = [&](const float* p) {
+        return reinterpret_cast<float*>(reinterpret_cast<char*>(S.mcva) +
+                                        (reinterpret_cast<const char*>(p) - reinterpret_cast<char*>(S.uc)));
+    };
+    float* W = net.params;
+    float* G = net.grads;
+    float* V = net.grads + net.grads_count;
+    const unsigned long long n4 = net.params_count / 4;
+    const unsigned long long beg = n4 * (unsigned long long)S.rank / (unsigned long long)S.world;
+    const unsigned long long end = n4 * (unsigned long long)(S.rank + 1) / (unsigned long long)S.world;
+    const unsigned blocks = static_cast<unsigned>(std::max<unsigned long long>(
+        1, std::min<unsigned long long>(4ull * (unsigned long long)c.sm_count, (end - beg + 255) / 256)));
+    const float invB = 1.0f / static_cast<float>(B_global);
+    if (!S.local) {
+        k_nvls_barrier<true><<<1, 32, 0, c.stream>>>(mc_flag, uc_flag, S.expect, S.world, c.error_flag);
+        k_nvls_update<true><<<blocks, 256, 0, c.stream>>>(mc(W), mc(G), mc(V), reinterpret_cast<const float4*>(W),
+                                                          reinterpret_cast<const float4*>(V), beg, end, invB, -eta,
+                                                          mu);
+        k_nvls_barrier<true><<<1, 32, 0, c.stream>>>(mc_flag, uc_flag, S.expect, S.world, c.error_flag);
+    } else {
+        k_nvls_barrier<false><<<1, 32, 0, c.stream>>>(mc_flag, uc_flag, S.expect, S.world, c.error_flag);
+        k_nvls_update<false><<<blocks, 256, 0, c.stream>>>(mc(W), mc(G), mc(V), reinterpret_cast<const float4*>(W),
+                                                           reinterpret_cast<const float4*>(V), beg, end, invB, -eta,
+                                                           mu);
+        k_nvls_barrier<false><<<1, 32, 0, c.stream>>>(mc_flag, uc_flag, S.expect, S.world, c.error_flag);
+    }
+    c.launches += 3;
+    c.check_launch();
+}
+
 template <class Ctx, class Net>
 void minibatch_body(Ctx& c, Net& net, size_t Bsz, float eta, float mu, double* loss_sum) {
+    if (net.nvls.bound) {
+        minibatch_grads_body(c, net, Bsz, loss_sum, false);
+        minibatch_update_nvls(c, net, Bsz * static_cast<size_t>(net.nvls.world), eta, mu);
+        return;
+    }
     static const bool force_buckets = std::getenv("LANE_B200_MB_BUCKETS") != nullptr;
     const bool allreduce = c.comm.comm && (c.comm.world > 1 || force_buckets);
     const size_t B_global = Bsz * static_cast<size_t>(c.comm.world);

@@ -163,6 +163,12 @@ class Device:
         _check(_native.lib().lane_b200_comm_destroy(self._p))
         self.world = 1
 
+    def nvls_supported(self) -> bool:
+        """Whether this GPU supports NVSwitch multicast objects (NVLS)."""
+        v = C.c_int(0)
+        _check(_native.lib().lane_b200_nvls_supported(self._p, C.byref(v)))
+        return bool(v.value)
+
 
 _default_device: Device | None = None
 
@@ -392,6 +398,25 @@ class FeedForwardNetwork:
 
     def allreduce_grads(self) -> None:
         _check(_native.lib().lane_b200_allreduce_grads(self._p))
+
+    # NVLS fused exchange + update (csrc/nvls.cuh); parallel.init_nvls drives
+    # the multi-rank sequence
+    def nvls_create(self, world: int, export: bool = True) -> int:
+        fd = C.c_int(-1)
+        _check(_native.lib().lane_b200_nvls_create(self._p, world, C.byref(fd) if export else None))
+        return fd.value
+
+    def nvls_attach(self, rank: int, world: int, fd: int = -1) -> None:
+        _check(_native.lib().lane_b200_nvls_attach(self._p, rank, world, fd))
+
+    def nvls_bind(self) -> None:
+        _check(_native.lib().lane_b200_nvls_bind(self._p))
+
+    def nvls_mode(self) -> str:
+        """"multicast", "local" (one rank without a multicast object) or "off"."""
+        v = C.c_int(-1)
+        _check(_native.lib().lane_b200_nvls_mode(self._p, C.byref(v)))
+        return {1: "multicast", 0: "local"}.get(v.value, "off")
 
 
 def build_network(input_width: int, hidden_sizes, classes: int, seed: int = 42,

@@ -13,6 +13,11 @@ rank applies the identical update, with 1/B_global folded into the step:
     G = (1/B_global) * sum_{ranks} sum_{b in shard} delta_b (x) x_b
     DW = mu*DW + (-eta)*G ;  W += DW
 
+With NVLS (``init_nvls``: the arena bound to an NVSwitch multicast object) the
+exchange is fused with the update instead: each rank reduces its slice of the
+gradient sums through the switch, updates it and multicasts W, the velocities
+and the mean gradients back to every rank (csrc/nvls.cuh).
+
 Batch-1 online SGD (configs C1, C2, C4) has a strict sample-to-sample
 dependency and does not shard: N GPUs run N independent replicas.
 """
@@ -51,6 +56,67 @@ def init_comm(device, rank: int, world: int, group=None) -> None:
     if world > 1:
         dist.broadcast_object_list(uid, src=0, group=group)
     device.comm_init(rank, world, uid[0])
+
+
+def _fd_socket_path(tag: str) -> str:
+    return "\0lane_b200_nvls_" + tag  # Linux abstract socket namespace
+
+
+def exchange_fd(fd: int, rank: int, world: int, tag: str, timeout: float = 60.0) -> int:
+    """Rank 0 sends the open file descriptor ``fd`` to ranks 1..world-1 over a
+    Unix-domain socket (SCM_RIGHTS); every other rank returns its received copy.
+    ``tag`` must be unique per job (the socket lives in the abstract namespace)."""
+    import socket
+    import time
+    path = _fd_socket_path(tag)
+    if rank == 0:
+        srv = socket.socket(socket.AF_UNIX, socket.SOCK_STREAM)
+        srv.bind(path)
+        srv.listen(world)
+        srv.settimeout(timeout)
+        try:
+            for _ in range(world - 1):
+                conn, _ = srv.accept()
+                with conn:
+                    socket.send_fds(conn, [b"F"], [fd])
+                    conn.recv(1)  # the peer holds its copy: safe to close ours later
+        finally:
+            srv.close()
+        return fd
+    deadline = time.time() + timeout
+    while True:
+        try:
+            cli = socket.socket(socket.AF_UNIX, socket.SOCK_STREAM)
+            cli.connect(path)
+            break
+        except (FileNotFoundError, ConnectionRefusedError):
+            cli.close()
+            if time.time() > deadline:
+                raise TimeoutError("nvls: rank 0 did not publish its descriptor")
+            time.sleep(0.05)
+    with cli:
+        _, fds, _, _ = socket.recv_fds(cli, 1, 1)
+        cli.sendall(b"A")
+    return fds[0]
+
+
+def init_nvls(net, rank: int, world: int, tag: str = "job", group=None) -> None:
+    """Bind ``net``'s arena to one NVSwitch multicast object shared by the
+    ``world`` ranks (csrc/nvls.cuh): rank 0 creates it and exports a POSIX fd,
+    the fd travels over a Unix socket, every rank adds its GPU, then -- after a
+    barrier -- binds and maps.  torch.distributed only supplies the barriers."""
+    import os
+    import torch.distributed as dist
+    fd = net.nvls_create(world, export=world > 1) if rank == 0 else -1
+    if world > 1:
+        fd = exchange_fd(fd, rank, world, tag)
+    net.nvls_attach(rank, world, fd)
+    if world > 1:
+        dist.barrier(group=group)
+    net.nvls_bind()
+    if world > 1:
+        dist.barrier(group=group)
+        os.close(fd)
 
 
 class DataParallelTrainer:

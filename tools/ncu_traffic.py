@@ -11,7 +11,7 @@ import sys
 
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 RUNS = {  # workload: (bench args, kernel-name substring)
-    "c2": ([], "k_sgd_window"),
+    "c2": (["--workload", "c2"], "k_sgd_window"),
     "c3": (["--workload", "c3"], "k_gemm_tc"),
     "c5": (["--workload", "c5"], "k_gemm_h3"),
 }
