@@ -644,7 +644,8 @@ inline bool tc_use_h3(int M, int N, int K) {
 // single CTAs with split-K otherwise)
 inline void gemm_h3(GemmCtx& g, GemmOp op, int M, int N, int K, const float* A, const float* B, Epi e, float* C,
                     float* C2, const float* bias, const float* aux, const GemmMax* mx, bool* fused_out) {
-    const bool pair = M >= 1024 || (M >= 512 && K >= 2048);
+    static const int pair_min_m = std::getenv("LANE_B200_H3_PAIR_MIN_M") ? std::atoi(std::getenv("LANE_B200_H3_PAIR_MIN_M")) : 0;
+    const bool pair = pair_min_m > 0 ? M >= pair_min_m : (M >= 1024 || (M >= 512 && K >= 2048));
     CUtensorMap ma, mb;
     bool a_mn = false, b_mn = false;
     switch (op) {

@@ -43,6 +43,7 @@ namespace lane_b200 {
 // (8 split warps doing both ran the split pass latency-bound at ~1.1k cycles
 // per K block against ~770 of MMAs)
 constexpr int kH3SplitWarps = 16;
+constexpr int kH3Group = 8;  // raster group (pair tile rows)
 constexpr int kH3Threads = 64 + 32 * kH3SplitWarps;
 
 template <bool PAIR>
@@ -141,8 +142,26 @@ __global__ void __launch_bounds__(kH3Threads, 1)
     uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 32);
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const uint32_t rank = PAIR ? (blockIdx.x & 1u) : 0u;
-    const int m0 = PAIR ? (int)(blockIdx.x >> 1) * 2 * kTcBM + (int)rank * kTcBM : (int)blockIdx.y * kTcBM;
-    const int n0 = PAIR ? (int)blockIdx.y * Cfg::kBN : (int)blockIdx.x * kTcBN;
+    // grouped raster: consecutive pair tiles (launch order) walk kH3Group
+    // tile rows before the next tile column, so a wave of 74 pairs covers an
+    // ~8 x 9 block of tiles and re-reads far fewer A panels from DRAM than
+    // row-major waves that each sweep every tile row
+    int mt, nt;
+    if constexpr (PAIR) {
+        const int tiles_m = (int)(gridDim.x >> 1), tiles_n = (int)gridDim.y;
+        const int p = (int)blockIdx.y * tiles_m + (int)(blockIdx.x >> 1);
+        const int per_group = kH3Group * tiles_n;
+        const int g = p / per_group, first = g * kH3Group;
+        const int gm = min(tiles_m - first, kH3Group);
+        const int rr = p - g * per_group;
+        mt = first + rr % gm;
+        nt = rr / gm;
+    } else {
+        mt = (int)blockIdx.y;
+        nt = (int)blockIdx.x;
+    }
+    const int m0 = PAIR ? mt * 2 * kTcBM + (int)rank * kTcBM : mt * kTcBM;
+    const int n0 = nt * Cfg::kBN;
     const int nbl = n0 + (int)rank * Cfg::kBLocal;  // this CTA's B columns
     const int nkb_all = (args.K + kTcBK - 1) / kTcBK;
     const int kb0 = gridDim.z > 1 ? blockIdx.z * args.kbs : 0;
