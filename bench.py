@@ -69,6 +69,24 @@ def load_traffic(wl):
     return (d["traffic_bytes_per_launch"], d["source"]) if d else (None, None)
 
 
+def chain_latency(wl, plan, kernel_ms, n, clk):
+    """The batch-1 window kernel's latency roofline: cycles per sample of the
+    step (kernel time x the SM clock sampled under load) against the measured
+    dependency floor of the per-sample chain (profiles/chain_floor.json,
+    tools/ubench_chain.cu k_chain_floor).  C2's shape only."""
+    path = os.path.join(ROOT, "profiles", "chain_floor.json")
+    if wl != "c2" or not plan.startswith("window") or not os.path.exists(path):
+        return None
+    d = json.load(open(path))[wl]
+    mhz = clk.summary().get("sm_mhz") or 0
+    if not mhz:
+        return None
+    cyc = kernel_ms / 1e3 / n * mhz * 1e6
+    return {"bound": "latency", "unit": "cycles/sample", "achieved": cyc,
+            "floor": d["floor_cycles_per_sample"], "frac": d["floor_cycles_per_sample"] / cyc,
+            "source": d["source"], "what": d["what"]}
+
+
 def load_peaks():
     p = os.path.join(ROOT, "MEASURED_PEAKS.json")
     if os.path.exists(p):
@@ -638,7 +656,8 @@ def main():
                                  "(DRAM traffic is the inputs only) and is bound by the serial "
                                  "per-sample chain (DESIGN.md section 4.1); achieved uses the whole "
                                  "step (Gram pre-pass + kernel + G/DW), CUDA events on the library "
-                                 "stream"},
+                                 "stream",
+                         "latency": chain_latency(wl, plan, kernel_ms, n, clk)},
             "e2e": {"value": e2e, "unit": "samples/s",
                     "h2d_bytes_per_step": int(X.nbytes + T.nbytes),
                     "d2h_bytes_per_step": 8 * 2 + 4},  # EpochStats (loss sum, hits) + the device error flag

@@ -96,6 +96,96 @@ __global__ void k_bench(float* out, long long* cyc, float seed) {
     if (lane == 0) cyc[T] = t1 - t0;
 }
 
+// The C2 sample chain's critical path only (784-128-10: one warp, 4 hidden
+// units per lane, 10 classes), with none of the off-chain work the window
+// kernel's chain warp also issues (the deferred W1 update, the fetch of the
+// next row, the bias / statistics bookkeeping):
+//   z = c1 d0(s-1) + y + b0; a = tanh z; partial logits (4 FMA x 10) ->
+//   transposed smem tile -> lane k sums class k (8 LDS.128 + tree) -> + b1 ->
+//   redux max -> exp -> smem -> every lane sums the 10 exponentials -> rcp ->
+//   d1 = p - t -> d0 = (1 - a^2) (W1 d1) -> next z.
+// cycles/step of this kernel is the dependency floor a one-warp chain of this
+// algorithm cannot beat (bench.py's C2 line reports it as roofline.latency).
+__global__ void k_chain_floor(float* out, long long* cyc, float seed, int n) {
+    constexpr int C = 10, CC = 10, XS = 36;
+    __shared__ __align__(16) float xr[16 * XS];
+    __shared__ __align__(16) float es[16];
+    const int lane = threadIdx.x;
+    const bool kval = lane < C;
+    const int kr = lane & 15;
+    float w1[4][CC], y[4], b0r[4], dp1[4], t[CC];
+    for (int m = 0; m < 4; ++m) {
+        for (int k = 0; k < CC; ++k) w1[m][k] = seed * 0.01f * (float)((lane * 4 + m) * 7 + k * 3 - 40) / 64.0f;
+        y[m] = seed * 0.1f * (lane - 16) / 16.0f;
+        b0r[m] = 0.01f * m;
+        dp1[m] = 0.0f;
+    }
+    for (int k = 0; k < CC; ++k) t[k] = k == 3 ? 1.0f : 0.0f;
+    for (int e = lane; e < 16 * XS; e += 32) xr[e] = 0.0f;
+    if (lane < 16) es[lane] = 0.0f;
+    const float c1 = -0.01f * seed, b1k = 0.0f;
+    __syncwarp();
+    long long t0 = clock64();
+    for (int i = 0; i < n; ++i) {
+        float a[4];
+#pragma unroll
+        for (int m = 0; m < 4; ++m) a[m] = tanhf(fmaf(c1, dp1[m], y[m]) + b0r[m]);
+#pragma unroll
+        for (int k = 0; k < CC; ++k) {
+            float acc = 0.0f;
+#pragma unroll
+            for (int m = 0; m < 4; ++m) acc = fmaf(a[m], w1[m][k], acc);
+            xr[k * XS + lane] = acc;
+        }
+        __syncwarp();
+        const float4* col = reinterpret_cast<const float4*>(xr + kr * XS);
+        float4 v[8];
+#pragma unroll
+        for (int q = 0; q < 8; ++q) v[q] = col[q];
+        float t8[8];
+#pragma unroll
+        for (int q = 0; q < 8; ++q) t8[q] = (v[q].x + v[q].y) + (v[q].z + v[q].w);
+        const float zown = (((t8[0] + t8[1]) + (t8[2] + t8[3])) + ((t8[4] + t8[5]) + (t8[6] + t8[7]))) + b1k;
+        float mx;
+        asm volatile("redux.sync.max.f32 %0, %1, 0xffffffff;\n" : "=f"(mx) : "f"(kval ? zown : -INFINITY));
+        const float eown = expf(zown - mx);
+        if (kval) es[lane] = eown;
+        __syncwarp();
+        float ek[12];
+#pragma unroll
+        for (int k4 = 0; k4 < 3; ++k4) {
+            const float4 q = reinterpret_cast<const float4*>(es)[k4];
+            ek[4 * k4] = q.x; ek[4 * k4 + 1] = q.y; ek[4 * k4 + 2] = q.z; ek[4 * k4 + 3] = q.w;
+        }
+        ek[10] = ek[11] = 0.0f;
+        float sp[12];
+#pragma unroll
+        for (int k = 0; k < 12; ++k) sp[k] = ek[k];
+#pragma unroll
+        for (int w = 1; w < 12; w <<= 1)
+#pragma unroll
+            for (int k = 0; k + w < 12; k += 2 * w) sp[k] += sp[k + w];
+        float inv;
+        asm volatile("rcp.approx.ftz.f32 %0, %1;\n" : "=f"(inv) : "f"(sp[0]));
+        float d1[CC];
+#pragma unroll
+        for (int k = 0; k < CC; ++k) d1[k] = fmaf(ek[k], inv, -t[k]);
+#pragma unroll
+        for (int m = 0; m < 4; ++m) {
+            float acc0 = 0.0f, acc1 = 0.0f;
+#pragma unroll
+            for (int k = 0; k < CC / 2; ++k) acc0 = fmaf(d1[k], w1[m][k], acc0);
+#pragma unroll
+            for (int k = CC / 2; k < CC; ++k) acc1 = fmaf(d1[k], w1[m][k], acc1);
+            dp1[m] = fmaf(-a[m], a[m], 1.0f) * (acc0 + acc1);
+        }
+        __syncwarp();
+    }
+    long long t1 = clock64();
+    out[lane] = dp1[0] + dp1[1] + dp1[2] + dp1[3];
+    if (lane == 0) cyc[15] = t1 - t0;
+}
+
 int main() {
     float* out;
     long long* cyc;
@@ -121,5 +211,11 @@ int main() {
         cudaDeviceSynchronize();
     }
     for (int t = 0; t < 13; ++t) printf("%-20s %7.1f cycles/step\n", names[t], (double)cyc[t] / N);
+    for (int rep = 0; rep < 3; ++rep) {
+        k_chain_floor<<<1, 32>>>(out, cyc, 0.3f, N);
+        cudaDeviceSynchronize();
+    }
+    printf("%-20s %7.1f cycles/step\n", "c2 chain floor", (double)cyc[15] / N);
+    printf("{\"c2_chain_floor_cycles\": %.1f}\n", (double)cyc[15] / N);
     return 0;
 }
