@@ -111,7 +111,8 @@ def _preload_torch_nccl() -> None:
 def load(check_gpu: bool = True):
     global _lib
     if _lib is None:
-        path = _build.build()  # no-op when up to date
+        # LANE_B200_LIB: an alternative build of the same library (experiments)
+        path = os.environ.get("LANE_B200_LIB") or _build.build()  # no-op when up to date
         _preload_torch_nccl()
         L = C.CDLL(path)
         for name, (res, args) in SIGNATURES.items():
