@@ -678,10 +678,33 @@ inline void gemm_h3(GemmCtx& g, GemmOp op, int M, int N, int K, const float* A, 
         S = (nkb + t.kbs - 1) / t.kbs;
         part = (size_t)S * M * N;
     }
-    // [split-K partials | row maxima of op(A) | column maxima of op(B)]
+    // tail-wave split (pairs, no split-K): when the last wave of pair tiles is
+    // at most half full, its tiles run as two K halves each (twice as many
+    // units, half as long), then k_h3_tail_reduce sums the halves in a fixed
+    // order and applies the epilogue.  C5's 4096^3: 256 tiles on 74 pairs =
+    // 3 full waves + 34 tiles -> 3.5 wave-times instead of 4.
+    static const bool tail_ok = std::getenv("LANE_B200_H3_NOTAIL") == nullptr;
+    size_t tail_floats = 0;
+    if (pair && S == 1 && tail_ok && nkb >= 16) {
+        const int tm = (M + 2 * kTcBM - 1) / (2 * kTcBM), tn = (N + kPN - 1) / kPN;
+        const int T = tm * tn, P = std::max(1, g.sm_count / 2);
+        const int full = (T / P) * P, tail = T - full;
+        if (full > 0 && tail > 0 && 2 * tail <= P) {
+            t.full_units = full;
+            t.tiles_m = tm;
+            t.tiles_n = tn;
+            tail_floats = (size_t)tail * 2 * 65536;
+        }
+    }
+    // [split-K partials or tail-wave halves | row maxima of op(A) | column maxima of op(B)]
+    part = std::max(part, tail_floats);
     ensure_ws(g, part + (size_t)M + (size_t)N);
     float* ws = *g.ws;
     if (S > 1) t.part = ws;
+    if (t.full_units > 0) {
+        t.tail_part = ws;
+        *g.launches += 1;  // the tail reduce
+    }
     unsigned* amax = reinterpret_cast<unsigned*>(ws + part);
     unsigned* bmax = amax + M;
     if (mx && mx->a) {
@@ -698,7 +721,7 @@ inline void gemm_h3(GemmCtx& g, GemmOp op, int M, int N, int K, const float* A, 
         t.bmax = bmax;
         *g.launches += 1;
     }
-    if (mx && mx->orow && S == 1) {
+    if (mx && mx->orow && S == 1) {  // the tail reduce emits its tiles' maxima too
         t.omax_row = mx->orow;
         t.omax_col = mx->ocol;
         *fused_out = true;

@@ -39,11 +39,14 @@
 
 namespace lane_b200 {
 
-// 16 split warps (4 per SM sub-partition): warps 2..9 split A, 10..17 split B
-// (8 split warps doing both ran the split pass latency-bound at ~1.1k cycles
-// per K block against ~770 of MMAs)
+// 16 split warps (4 per SM sub-partition) in two groups of 8 that take
+// alternate K blocks (see the split loop)
 constexpr int kH3SplitWarps = 16;
 constexpr int kH3Group = 8;  // raster group (pair tile rows)
+#ifndef LANE_H3_GROUPS
+#define LANE_H3_GROUPS 4
+#endif
+constexpr int kH3Groups = LANE_H3_GROUPS;  // split-warp groups, each on its own K blocks
 constexpr int kH3Threads = 64 + 32 * kH3SplitWarps;
 
 template <bool PAIR>
@@ -131,6 +134,18 @@ __device__ __forceinline__ void h3_load16(uint32_t t, int r, int khalf, float (&
     }
 }
 
+// pair tile t -> (tile row, tile column): grouped raster, kH3Group tile rows
+// at a time, so a wave of 74 pairs covers an ~8 x 9 block of tiles and
+// re-reads fewer A panels than row-major waves that sweep every tile row
+__device__ __forceinline__ void h3_tile_mn(int t, int tiles_m, int tiles_n, int& mt, int& nt) {
+    const int per_group = kH3Group * tiles_n;
+    const int g = t / per_group, first = g * kH3Group;
+    const int gm = min(tiles_m - first, kH3Group);
+    const int rr = t - g * per_group;
+    mt = first + rr % gm;
+    nt = rr / gm;
+}
+
 template <bool A_MN, bool B_MN, TcEpi E, bool PAIR>
 __global__ void __launch_bounds__(kH3Threads, 1)
     k_gemm_h3(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB, TcArgs args) {
@@ -148,25 +163,38 @@ __global__ void __launch_bounds__(kH3Threads, 1)
     // ~8 x 9 block of tiles and re-reads far fewer A panels from DRAM than
     // row-major waves that each sweep every tile row
     int mt, nt;
+    // tail-wave split (pairs, args.full_units > 0): a 1-D grid of units; the
+    // first full_units are whole tiles, the rest are the two K halves of the
+    // last partial wave's tiles, written raw to args.tail_part and finished
+    // by k_h3_tail_reduce -- the last wave then takes half a wave's time
+    int tail = -1;  // tail unit: 2 * (tile - full_units) + half
+    int tile;
     if constexpr (PAIR) {
-        const int tiles_m = (int)(gridDim.x >> 1), tiles_n = (int)gridDim.y;
-        const int p = (int)blockIdx.y * tiles_m + (int)(blockIdx.x >> 1);
-        const int per_group = kH3Group * tiles_n;
-        const int g = p / per_group, first = g * kH3Group;
-        const int gm = min(tiles_m - first, kH3Group);
-        const int rr = p - g * per_group;
-        mt = first + rr % gm;
-        nt = rr / gm;
+        const int u = (int)(blockIdx.x >> 1) + (int)blockIdx.y * (int)(gridDim.x >> 1);
+        if (args.full_units > 0 && u >= args.full_units) {
+            tail = u - args.full_units;
+            tile = args.full_units + (tail >> 1);
+        } else {
+            tile = u;
+        }
+        const int tiles_m = args.full_units > 0 ? args.tiles_m : (int)(gridDim.x >> 1);
+        const int tiles_n = args.full_units > 0 ? args.tiles_n : (int)gridDim.y;
+        h3_tile_mn(tile, tiles_m, tiles_n, mt, nt);
     } else {
         mt = (int)blockIdx.y;
         nt = (int)blockIdx.x;
+        tile = 0;
     }
     const int m0 = PAIR ? mt * 2 * kTcBM + (int)rank * kTcBM : mt * kTcBM;
     const int n0 = nt * Cfg::kBN;
     const int nbl = n0 + (int)rank * Cfg::kBLocal;  // this CTA's B columns
     const int nkb_all = (args.K + kTcBK - 1) / kTcBK;
-    const int kb0 = gridDim.z > 1 ? blockIdx.z * args.kbs : 0;
-    const int kb1 = gridDim.z > 1 ? min(nkb_all, kb0 + args.kbs) : nkb_all;
+    int kb0 = gridDim.z > 1 ? blockIdx.z * args.kbs : 0;
+    int kb1 = gridDim.z > 1 ? min(nkb_all, kb0 + args.kbs) : nkb_all;
+    if (tail >= 0) {
+        kb0 = (tail & 1) ? nkb_all / 2 : 0;
+        kb1 = (tail & 1) ? nkb_all : nkb_all / 2;
+    }
     const int nkb = kb1 - kb0;
     const bool split = gridDim.z > 1;
     const uint32_t sbase = tc_smem(smem);
@@ -186,10 +214,10 @@ __global__ void __launch_bounds__(kH3Threads, 1)
     if (threadIdx.x == 0) {
         for (int l = 0; l < kL; ++l) {
             tc_mbar_init(full(l), 1);
-            tc_mbar_init(lempty(l), kH3SplitWarps);
+            tc_mbar_init(lempty(l), kH3SplitWarps / kH3Groups);  // one group per K block
         }
         for (int s = 0; s < kS; ++s) {
-            tc_mbar_init(conv(s), kH3SplitWarps);
+            tc_mbar_init(conv(s), kH3SplitWarps / kH3Groups);  // one group per K block
             tc_mbar_init(fempty(s), 1);
         }
         tc_mbar_init(tmem_full, 1);
@@ -225,16 +253,21 @@ __global__ void __launch_bounds__(kH3Threads, 1)
                 const int l = kb % kL;
                 const uint32_t ph = (uint32_t)((kb / kL) & 1);
                 tc_mbar_wait(lempty(l), ph ^ 1);
-                tc_mbar_expect_tx(full(l), Cfg::kA32 + Cfg::kB32);
+                const bool ldA = !(args.diag & 8), ldB = !(args.diag & 4);  // experiments only
+                tc_mbar_expect_tx(full(l), (ldA ? Cfg::kA32 : 0) + (ldB ? Cfg::kB32 : 0));
                 const int k0 = (kb0 + kb) * kTcBK;
-                if constexpr (!A_MN)
-                    tc_tma_2d(&tmA, full(l), landA(l), k0, m0);
-                else
-                    tc_tma_2d(&tmA, full(l), landA(l), m0, k0);
-                if constexpr (!B_MN)
-                    tc_tma_2d(&tmB, full(l), landB(l), k0, nbl);
-                else
-                    tc_tma_2d(&tmB, full(l), landB(l), nbl, k0);
+                if (ldA) {
+                    if constexpr (!A_MN)
+                        tc_tma_2d(&tmA, full(l), landA(l), k0, m0);
+                    else
+                        tc_tma_2d(&tmA, full(l), landA(l), m0, k0);
+                }
+                if (ldB) {
+                    if constexpr (!B_MN)
+                        tc_tma_2d(&tmB, full(l), landB(l), k0, nbl);
+                    else
+                        tc_tma_2d(&tmB, full(l), landB(l), nbl, k0);
+                }
             }
         }
     } else if (warp == 1 && rank == 0) {
@@ -303,32 +336,52 @@ __global__ void __launch_bounds__(kH3Threads, 1)
         __syncwarp();
     } else {
         // ---------------- split pass, then epilogue (warps 2..17) ----------------
-        const int quarter = warp & 3;       // TMEM lanes this warp may access
-        const int r = quarter * 32 + lane;  // A row of the tile / B column of this CTA's half
-        const bool isB = warp >= 2 + kH3SplitWarps / 2;
-        const int khalf = ((warp - 2) >> 2) & 1;  // K columns [16 khalf, +16) of the block
+        // Two groups of 8 warps take alternate K blocks, so two blocks' splits
+        // are in flight at once: one warp's per-block sequence (loads, convert,
+        // TMEM / smem stores, wait::st, fences, barrier round trips) is longer
+        // than the MMAs of a block, and with every warp on every block the
+        // split pass, not the tensor pipe, set the pace.  Within a group a
+        // thread converts one A row and one B column, 16 K values each.
+        constexpr int kWpg = kH3SplitWarps / kH3Groups;  // warps per group (4 or 8)
+        constexpr int kHalves = 8 / kWpg;                // K halves per thread and block (2 or 1)
+        const int grp = (warp - 2) / kWpg;               // this group takes K blocks grp, grp + kH3Groups, ...
+        const int w8 = (warp - 2) % kWpg;
+        const int quarter = warp & 3;              // TMEM lanes this warp may access
+        const int r = quarter * 32 + lane;         // A row of the tile / B column of this CTA's half
+        const int khalf0 = w8 >> 2;                // first K half [16 khalf, +16) of the block
         const int ma = m0 + r, nb = nbl + r;
         const int ea = ma < args.M ? h3_exp(args.amax[ma]) : 0;
         const int eb = nb < args.N ? h3_exp(args.bmax[nb]) : 0;
-        const float sc = isB ? h3_pow2(14 - eb) : h3_pow2(14 - ea);
-        // this thread's B column in the no-swizzle K-major f16 tiles: row r of
-        // 8-row group r/8, K core matrices 2 khalf, 2 khalf + 1
-        const uint32_t boff = (uint32_t)((r >> 3) * 512 + (2 * khalf) * 128 + (r & 7) * 16);
-        for (int kb = 0; kb < nkb; ++kb) {
+        const float sa = h3_pow2(14 - ea), sb = h3_pow2(14 - eb);
+        for (int kb = grp; kb < nkb; kb += kH3Groups) {
             const int l = kb % kL, s = kb % kS;
             tc_mbar_wait(full(l), (uint32_t)((kb / kL) & 1));
             float v[16];
-            uint32_t hi[8], lo[8];
-            if (args.diag & 1) {
+            uint32_t ahi[kHalves][8], alo[kHalves][8], bhi[kHalves][8], blo[kHalves][8];
 #pragma unroll
-                for (int j = 0; j < 8; ++j) hi[j] = lo[j] = 0u;
-            } else {
-                if (!isB)
-                    h3_load16<A_MN>(landA(l), r, khalf, v);
-                else
-                    h3_load16<B_MN>(landB(l), r, khalf, v);
+            for (int h = 0; h < kHalves; ++h) {
+                const int khalf = khalf0 + h;
+                if (args.diag & 1) {
 #pragma unroll
-                for (int j = 0; j < 8; ++j) h3_split2(v[2 * j], v[2 * j + 1], sc, hi[j], lo[j]);
+                    for (int j = 0; j < 8; ++j) ahi[h][j] = alo[h][j] = bhi[h][j] = blo[h][j] = 0u;
+                } else {
+                    if (args.diag & 64) {  // experiment: the conversions without the landing-tile reads
+#pragma unroll
+                        for (int j = 0; j < 16; ++j) v[j] = __int_as_float(0x3f800000 + kb * 16 + j + lane);
+                    } else {
+                        h3_load16<A_MN>(landA(l), r, khalf, v);
+                    }
+#pragma unroll
+                    for (int j = 0; j < 8; ++j) h3_split2(v[2 * j], v[2 * j + 1], sa, ahi[h][j], alo[h][j]);
+                    if (args.diag & 64) {
+#pragma unroll
+                        for (int j = 0; j < 16; ++j) v[j] = __int_as_float(0x3f000000 + kb * 16 + j + lane);
+                    } else {
+                        h3_load16<B_MN>(landB(l), r, khalf, v);
+                    }
+#pragma unroll
+                    for (int j = 0; j < 8; ++j) h3_split2(v[2 * j], v[2 * j + 1], sb, bhi[h][j], blo[h][j]);
+                }
             }
             // landing slot read (the values are consumed above): release it
             __syncwarp();
@@ -336,24 +389,31 @@ __global__ void __launch_bounds__(kH3Threads, 1)
             // f16 slot s free once the MMAs of K block kb - kS have completed
             tc_mbar_wait(fempty(s), (uint32_t)(((kb / kS) & 1) ^ 1));
             asm volatile("tcgen05.fence::after_thread_sync;\n" ::: "memory");
-            if (!isB) {
+#pragma unroll
+            for (int h = 0; h < kHalves; ++h) {
+                const int khalf = khalf0 + h;
                 const uint32_t tA =
                     tmem + ((uint32_t)(quarter * 32) << 16) + (uint32_t)(Cfg::kBN + 32 * s + 8 * khalf);
-                h3_st8(tA, hi);
-                h3_st8(tA + 16u, lo);
-                asm volatile("tcgen05.wait::st.sync.aligned;\n" ::: "memory");
-                asm volatile("tcgen05.fence::before_thread_sync;\n" ::: "memory");
-            } else {
-                const uint32_t bh = tileBh(s) + boff;
-                h3_sts4(bh, hi[0], hi[1], hi[2], hi[3]);
-                h3_sts4(bh + 128, hi[4], hi[5], hi[6], hi[7]);
-                h3_sts4(bh + Cfg::kB16, lo[0], lo[1], lo[2], lo[3]);
-                h3_sts4(bh + Cfg::kB16 + 128, lo[4], lo[5], lo[6], lo[7]);
-                asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");
+                if (!(args.diag & 16)) {
+                    h3_st8(tA, ahi[h]);
+                    h3_st8(tA + 16u, alo[h]);
+                }
+                // this thread's B column in the no-swizzle K-major f16 tiles: row r
+                // of 8-row group r/8, K core matrices 2 khalf, 2 khalf + 1
+                const uint32_t bh = tileBh(s) + (uint32_t)((r >> 3) * 512 + (2 * khalf) * 128 + (r & 7) * 16);
+                if (!(args.diag & 32)) {
+                    h3_sts4(bh, bhi[h][0], bhi[h][1], bhi[h][2], bhi[h][3]);
+                    h3_sts4(bh + 128, bhi[h][4], bhi[h][5], bhi[h][6], bhi[h][7]);
+                    h3_sts4(bh + Cfg::kB16, blo[h][0], blo[h][1], blo[h][2], blo[h][3]);
+                    h3_sts4(bh + Cfg::kB16 + 128, blo[h][4], blo[h][5], blo[h][6], blo[h][7]);
+                }
             }
+            if (!(args.diag & 32)) asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");
+            if (!(args.diag & 16)) asm volatile("tcgen05.wait::st.sync.aligned;\n" ::: "memory");
+            asm volatile("tcgen05.fence::before_thread_sync;\n" ::: "memory");
             __syncwarp();
             if (lane == 0) {
-                if (PAIR && rank == 0 && warp == 2)
+                if (PAIR && rank == 0 && w8 == 0)
                     tc_mbar_expect_tx(conv(s), 16);  // rank 1's forward (16-byte bulk copy)
                 else
                     tc_mbar_arrive(conv(s));
@@ -368,7 +428,7 @@ __global__ void __launch_bounds__(kH3Threads, 1)
         // optional maxima of the output operand the next GEMMs consume (tanh(z)
         // for BIAS_TANH, C otherwise): per row (atomicMax once per thread) and
         // per column (warp max over this warp's 32 rows, one atomicMax per lane)
-        const bool omax = args.omax_row != nullptr && !split;
+        const bool omax = args.omax_row != nullptr && !split && tail < 0;
         unsigned rmax = 0;
 #pragma unroll 1
         for (int c0 = cbeg; c0 < cbeg + kCols; c0 += 32) {
@@ -395,6 +455,15 @@ __global__ void __launch_bounds__(kH3Threads, 1)
                 x[q] = (__uint_as_float(rr[q]) * ia) * ib;
             }
             const bool mrow = m < args.M;
+            if (tail >= 0) {
+                // raw (scales undone) partial of this K half, tile-local [256][256]
+                float* P = args.tail_part + (size_t)tail * (2 * kTcBM * Cfg::kBN) +
+                           (size_t)(m - mt * 2 * kTcBM) * Cfg::kBN + c0;
+#pragma unroll
+                for (int q = 0; q < 8; ++q)
+                    reinterpret_cast<float4*>(P)[q] = make_float4(x[4 * q], x[4 * q + 1], x[4 * q + 2], x[4 * q + 3]);
+                continue;
+            }
             if (split) {
                 if (mrow) {
                     float* P = args.part + (size_t)blockIdx.z * args.M * args.N + (size_t)m * args.N;
@@ -541,6 +610,46 @@ __global__ void __launch_bounds__(256) k_absmax_rc(const float* __restrict__ X, 
     }
 }
 
+
+// Finish the tail-wave tiles: sum the two K halves (half 0 + half 1, fixed
+// order), then the epilogue and the optional output maxima.  Grid
+// (tail tiles, 8 row chunks of 32), 256 threads = the tile's 256 columns.
+template <TcEpi E>
+__global__ void __launch_bounds__(256) k_h3_tail_reduce(TcArgs a) {
+    const int t = a.full_units + (int)blockIdx.x;
+    int mt, nt;
+    h3_tile_mn(t, a.tiles_m, a.tiles_n, mt, nt);
+    const int n = nt * 256 + (int)threadIdx.x;
+    const int lane = threadIdx.x & 31;
+    const float* P0 = a.tail_part + (size_t)(2 * blockIdx.x) * 65536;
+    const float* P1 = P0 + 65536;
+    unsigned cmax = 0;
+    for (int i = 0; i < 32; ++i) {
+        const int lr = (int)blockIdx.y * 32 + i;
+        const int m = mt * 256 + lr;
+        unsigned ob = 0;
+        if (m < a.M && n < a.N) {
+            float v = P0[lr * 256 + threadIdx.x] + P1[lr * 256 + threadIdx.x];
+            const size_t idx = (size_t)m * a.N + n;
+            if constexpr (E == TcEpi::BIAS || E == TcEpi::BIAS_TANH) v = sadd(v, a.bias[n]);
+            if constexpr (E == TcEpi::TANH_GRAD) v = tanh_grad(a.aux[idx], v);
+            a.C[idx] = v;
+            float o = v;
+            if constexpr (E == TcEpi::BIAS_TANH) {
+                o = tanhf(v);
+                a.C2[idx] = o;
+            }
+            ob = __float_as_uint(fabsf(o));
+        }
+        if (a.omax_row) {
+            cmax = max(cmax, ob);
+            const unsigned rm = __reduce_max_sync(0xffffffffu, ob);
+            if (lane == 0 && m < a.M && rm) atomicMax(a.omax_row + m, rm);
+        }
+    }
+    if (a.omax_row && n < a.N && cmax) atomicMax(a.omax_col + n, cmax);
+}
+
 }  // namespace lane_b200
 
 // ---------------------------------------------------------------- host side
@@ -581,6 +690,8 @@ inline void h3_launch(cudaStream_t st, const CUtensorMap& a, const CUtensorMap& 
         cudaLaunchConfig_t cfg = {};
         constexpr int kBN = H3Cfg<true>::kBN;
         cfg.gridDim = dim3(2 * ((args.M + 2 * kTcBM - 1) / (2 * kTcBM)), (args.N + kBN - 1) / kBN, S);
+        if (args.full_units > 0)  // tail-wave split: whole tiles, then two K halves per tail tile
+            cfg.gridDim = dim3(2 * (args.full_units + 2 * (args.tiles_m * args.tiles_n - args.full_units)), 1, 1);
         cfg.blockDim = dim3(kH3Threads);
         cfg.dynamicSmemBytes = smem;
         cfg.stream = st;
@@ -600,6 +711,8 @@ inline void h3_launch(cudaStream_t st, const CUtensorMap& a, const CUtensorMap& 
         const size_t n4 = (size_t)args.M * args.N / 4;
         k_tc_splitk_reduce<E><<<(unsigned)std::min<size_t>(1184, (n4 + 255) / 256), 256, 0, st>>>(args, S);
     }
+    if (PAIR && args.full_units > 0)
+        k_h3_tail_reduce<E><<<dim3((unsigned)(args.tiles_m * args.tiles_n - args.full_units), 8), 256, 0, st>>>(args);
 }
 
 template <TcEpi E, bool PAIR>

@@ -70,11 +70,15 @@ struct TcArgs {
     // of op(B), from which the power-of-two operand scales are derived
     const unsigned* amax = nullptr;
     const unsigned* bmax = nullptr;
-    int diag = 0;  // experiments (LANE_B200_H3_DIAG): 1 skip the split math, 2 skip the MMAs
+    int diag = 0;  // experiments (LANE_B200_H3_DIAG): 1 skip the split math, 2 skip the MMAs, 4 / 8 skip the B / A loads
     // 3xF16 epilogue (optional): max |.| bits of every row / column of the
     // output operand the next GEMMs read (zeroed by the caller)
     unsigned* omax_row = nullptr;
     unsigned* omax_col = nullptr;
+    // 3xF16 CTA pairs, tail-wave split: whole tiles [0, full_units), then the
+    // two K halves of each remaining tile (raw partials in tail_part)
+    int full_units = 0, tiles_m = 0, tiles_n = 0;
+    float* tail_part = nullptr;
 };
 
 // ---- PTX helpers ------------------------------------------------------------

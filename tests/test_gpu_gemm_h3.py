@@ -13,7 +13,10 @@ H3 = 4
 
 @pytest.mark.parametrize("op", [NN, NT, TN])
 @pytest.mark.parametrize("M,N,K", [(128, 128, 32), (256, 512, 2048), (192, 320, 96), (64, 4100, 36),
-                                   (1024, 256, 256), (640, 384, 2048), (512, 128, 4096), (200, 260, 1000)])
+                                   (1024, 256, 256), (640, 384, 2048), (512, 128, 4096), (200, 260, 1000),
+                                   # 80 pair tiles on 74 SM pairs: 74 whole tiles + 6 tiles as two
+                                   # K halves each (tail-wave split, k_h3_tail_reduce); ragged edges
+                                   (2560, 2048, 1024), (2500, 2020, 1000)])
 def test_h3_store_condition_aware(dev, op, M, N, K):
     rs = np.random.default_rng(M * 7 + N * 3 + K + 1)
     A, B, Am, Bm = operands(op, M, N, K, rs)
@@ -21,7 +24,7 @@ def test_h3_store_condition_aware(dev, op, M, N, K):
     ref = Am @ Bm
     cond = np.abs(Am) @ np.abs(Bm)
     err = np.abs(out - ref)
-    assert launched in (3, 4)  # two operand-maxima passes + the kernel (+ the split-K reduce)
+    assert launched in (3, 4)  # two operand-maxima passes + the kernel (+ the split-K / tail reduce)
     assert np.all(err <= 1e-5 * cond + 1e-30), f"max err/cond {np.max(err / (cond + 1e-30)):.3e}"
 
 
@@ -65,7 +68,7 @@ def test_h3_zero_and_tiny_rows(dev):
 
 
 @pytest.mark.parametrize("op", [NN, NT])
-@pytest.mark.parametrize("M,N,K", [(256, 384, 512), (512, 256, 2048), (200, 260, 1000)])
+@pytest.mark.parametrize("M,N,K", [(256, 384, 512), (512, 256, 2048), (200, 260, 1000), (2560, 2048, 1024)])
 def test_h3_fused_epilogues(dev, op, M, N, K):
     rs = np.random.default_rng(5)
     A, B, Am, Bm = operands(op, M, N, K, rs)
