@@ -670,7 +670,8 @@ inline void gemm_h3(GemmCtx& g, GemmOp op, int M, int N, int K, const float* A, 
                            : ((M + kTcBM - 1) / kTcBM) * ((N + kTcBN - 1) / kTcBN);
     const int nkb = (K + kTcBK - 1) / kTcBK;
     static const int kbmin = std::getenv("LANE_B200_TC_SPLITK_KBMIN") ? std::atoi(std::getenv("LANE_B200_TC_SPLITK_KBMIN")) : 24;
-    int S = std::max(1, std::min({4, g.sm_count / std::max(1, tiles), nkb / kbmin}));
+    static const int h3_smax = std::getenv("LANE_B200_H3_SPLITK_MAX") ? std::atoi(std::getenv("LANE_B200_H3_SPLITK_MAX")) : 4;
+    int S = std::max(1, std::min({h3_smax, g.sm_count / std::max(1, tiles), nkb / kbmin}));
     if (K % kTcBK != 0) S = 1;
     size_t part = 0;
     if (S > 1) {
