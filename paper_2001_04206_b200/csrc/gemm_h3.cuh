@@ -467,8 +467,15 @@ __global__ void __launch_bounds__(kH3Threads, 1)
             if (split) {
                 if (mrow) {
                     float* P = args.part + (size_t)blockIdx.z * args.M * args.N + (size_t)m * args.N;
-                    for (int q = 0; q < 32; ++q)
-                        if (nb0 + q < args.N) P[nb0 + q] = x[q];
+                    if (nb0 + 32 <= args.N && (args.N & 3) == 0) {
+#pragma unroll
+                        for (int q = 0; q < 8; ++q)
+                            reinterpret_cast<float4*>(P + nb0)[q] =
+                                make_float4(x[4 * q], x[4 * q + 1], x[4 * q + 2], x[4 * q + 3]);
+                    } else {
+                        for (int q = 0; q < 32; ++q)
+                            if (nb0 + q < args.N) P[nb0 + q] = x[q];
+                    }
                 }
                 continue;
             }

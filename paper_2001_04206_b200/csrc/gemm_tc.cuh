@@ -452,8 +452,16 @@ __global__ void __launch_bounds__(kTcThreads, 1)
                 // raw partial; bias/activation are applied by k_tc_splitk_reduce
                 float* P = args.part + (size_t)blockIdx.z * args.M * args.N + (size_t)m * args.N;
                 const int nb = n0 + c0;
-                for (int q = 0; q < 32; ++q)
-                    if (nb + q < args.N) P[nb + q] = __uint_as_float(r[q]);
+                if (nb + 32 <= args.N && (args.N & 3) == 0) {
+#pragma unroll
+                    for (int q = 0; q < 8; ++q)
+                        reinterpret_cast<float4*>(P + nb)[q] =
+                            make_float4(__uint_as_float(r[4 * q]), __uint_as_float(r[4 * q + 1]),
+                                        __uint_as_float(r[4 * q + 2]), __uint_as_float(r[4 * q + 3]));
+                } else {
+                    for (int q = 0; q < 32; ++q)
+                        if (nb + q < args.N) P[nb + q] = __uint_as_float(r[q]);
+                }
             } else if (m < args.M) {
                 const int nb = n0 + c0;
                 if (nb + 32 <= args.N && (args.N & 3) == 0) {
