@@ -636,6 +636,8 @@ inline int& tc_prec_mode() {
 }
 inline bool tc_use_h3(int M, int N, int K) {
     const int m = tc_prec_mode();
+    static const int min_m = std::getenv("LANE_B200_H3_MIN_M") ? std::atoi(std::getenv("LANE_B200_H3_MIN_M")) : 0;
+    if (m == 2 && min_m > 0) return M >= min_m && K >= 2048 && N >= 256;
     return m == 1 || (m == 2 && (M >= 1024 || (M >= 512 && K >= 2048)) && K >= 2048 && N >= 256);
 }
 
@@ -836,9 +838,11 @@ inline bool gemm_try_tc(GemmCtx& g, GemmOp op, int M, int N, int K, const float*
                            : ((M + kTcBM - 1) / kTcBM) * ((N + kTcBN - 1) / kTcBN);
     const int nkb = K / kTcBK;
     static const int smax = std::getenv("LANE_B200_TC_SPLITK_MAX") ? std::atoi(std::getenv("LANE_B200_TC_SPLITK_MAX")) : 4;
-    // split only when every split keeps >= 24 K blocks: C3's 256x4096x1024
-    // forward ran 29.4 us with two 16-block splits + the reduce, 26.1 us unsplit
-    static const int kbmin = std::getenv("LANE_B200_TC_SPLITK_KBMIN") ? std::atoi(std::getenv("LANE_B200_TC_SPLITK_KBMIN")) : 24;
+    // split while every split keeps >= 8 K blocks: with float4 partial stores
+    // C3 runs 836k samples/s at a 24-block minimum, 857k at 8 (its
+    // 256x4096x1024 forward splits in 4; with scalar partial stores the
+    // unsplit forward had been faster)
+    static const int kbmin = std::getenv("LANE_B200_TC_SPLITK_KBMIN") ? std::atoi(std::getenv("LANE_B200_TC_SPLITK_KBMIN")) : 8;
     int S = std::min({smax, g.sm_count / std::max(1, tiles), nkb / kbmin});
     if (K % kTcBK != 0 || (N & 3) != 0) S = 1;
     if (S > 1) {
