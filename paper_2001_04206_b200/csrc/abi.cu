@@ -1771,7 +1771,17 @@ int lane_b200_train_minibatch(lane_b200_net* net, const float* X_host, const flo
         const size_t steps = full + (tail ? 1 : 0);
         if (steps == 0) throw Error(LANE_ERR_TRAINING, "train_minibatch: fewer samples than one global batch");
         InputPipeline& P = net->pipe;
-        P.reserve(batch * (I + C), steps);
+        // the running loss after every step of the whole call (epochs x steps,
+        // pinned): one host synchronisation at the end instead of one per epoch,
+        // so the pipeline never drains at an epoch boundary
+        P.reserve(batch * (I + C), epochs * steps);
+        // rows straight from page-locked dataset memory when a step's rows are
+        // consecutive (no shuffle): no host gather, no staging copy
+        cudaPointerAttributes ax{}, at{};
+        const bool pinned_src = cudaPointerGetAttributes(&ax, X_host) == cudaSuccess &&
+                                cudaPointerGetAttributes(&at, T_host) == cudaSuccess &&
+                                ax.type == cudaMemoryTypeHost && at.type == cudaMemoryTypeHost;
+        cudaGetLastError();  // a pageable pointer is not an error here
         std::vector<uint32_t> order(n);
         for (size_t k = 0; k < n; ++k) order[k] = static_cast<uint32_t>(k);
         SplitMix64 rng(seed);  // one generator for the whole run, like train (network.cpp:153)
@@ -1781,37 +1791,47 @@ int lane_b200_train_minibatch(lane_b200_net* net, const float* X_host, const flo
             if (shuffle)
                 for (size_t i = n; i > 1; --i) std::swap(order[i - 1], order[rng.below(i)]);
             LANE_CUDA(cudaMemsetAsync(net->loss_dev, 0, sizeof(double), c->stream));
-            size_t local = 0;
             for (size_t s = 0; s < steps; ++s) {
                 const size_t rows = s < full ? batch : tail;
                 const int k = static_cast<int>(done % InputPipeline::kSlots);
-                if (P.pending[k]) LANE_CUDA(cudaEventSynchronize(P.copied[k]));  // pinned slot free
-                gather_rows(X_host, T_host, I, C, order.data() + s * BG + (s < full ? rank * batch : 0), rows,
-                            P.host[k]);
+                const uint32_t* idx = order.data() + s * BG + (s < full ? rank * batch : 0);
+                bool direct = pinned_src;
+                for (size_t j = 1; direct && j < rows; ++j) direct = idx[j] == idx[0] + j;
                 LANE_CUDA(cudaStreamWaitEvent(P.copy, P.consumed[k], 0));  // device slot free
-                LANE_CUDA(cudaMemcpyAsync(P.dev[k], P.host[k], rows * (I + C) * sizeof(float),
-                                          cudaMemcpyHostToDevice, P.copy));
+                if (direct) {
+                    LANE_CUDA(cudaMemcpyAsync(P.dev[k], X_host + static_cast<size_t>(idx[0]) * I,
+                                              rows * I * sizeof(float), cudaMemcpyHostToDevice, P.copy));
+                    LANE_CUDA(cudaMemcpyAsync(P.dev[k] + rows * I, T_host + static_cast<size_t>(idx[0]) * C,
+                                              rows * C * sizeof(float), cudaMemcpyHostToDevice, P.copy));
+                } else {
+                    if (P.pending[k]) LANE_CUDA(cudaEventSynchronize(P.copied[k]));  // pinned slot free
+                    gather_rows(X_host, T_host, I, C, idx, rows, P.host[k]);
+                    LANE_CUDA(cudaMemcpyAsync(P.dev[k], P.host[k], rows * (I + C) * sizeof(float),
+                                              cudaMemcpyHostToDevice, P.copy));
+                }
                 LANE_CUDA(cudaEventRecord(P.copied[k], P.copy));
                 LANE_CUDA(cudaStreamWaitEvent(c->stream, P.copied[k], 0));
                 minibatch_step_impl(net, P.dev[k], P.dev[k] + rows * I, rows, eta, mu, net->loss_dev);
                 LANE_CUDA(cudaEventRecord(P.consumed[k], c->stream));
                 P.pending[k] = true;
                 // the step's result back to the host: the running loss sum (8 bytes, async)
-                LANE_CUDA(cudaMemcpyAsync(P.cum_loss_host + s, net->loss_dev, sizeof(double),
+                LANE_CUDA(cudaMemcpyAsync(P.cum_loss_host + done, net->loss_dev, sizeof(double),
                                           cudaMemcpyDeviceToHost, c->stream));
-                local += rows;
                 ++done;
             }
-            LANE_CUDA(cudaStreamSynchronize(c->stream));
-            c->check_device_error();
-            if (mean_loss_out)
-                mean_loss_out[epoch] = static_cast<float>(P.cum_loss_host[steps - 1] / static_cast<double>(local));
+        }
+        LANE_CUDA(cudaStreamSynchronize(c->stream));
+        c->check_device_error();
+        size_t local = 0;
+        for (size_t s = 0; s < steps; ++s) local += s < full ? batch : tail;
+        for (size_t epoch = 0; epoch < epochs; ++epoch) {
+            const double* cum = P.cum_loss_host + epoch * steps;
+            if (mean_loss_out) mean_loss_out[epoch] = static_cast<float>(cum[steps - 1] / static_cast<double>(local));
             if (step_loss_out)
                 for (size_t s = 0; s < steps; ++s) {
-                    const double prev = s ? P.cum_loss_host[s - 1] : 0.0;
+                    const double prev = s ? cum[s - 1] : 0.0;
                     const size_t rows = s < full ? batch : tail;
-                    step_loss_out[epoch * steps + s] =
-                        static_cast<float>((P.cum_loss_host[s] - prev) / static_cast<double>(rows));
+                    step_loss_out[epoch * steps + s] = static_cast<float>((cum[s] - prev) / static_cast<double>(rows));
                 }
         }
         if (steps_run) *steps_run = done;

@@ -6,7 +6,10 @@
 // to the slot's device buffer once the step that last used the slot has
 // staged it, and the compute stream waits for that copy.  The host runs up to
 // kSlots steps ahead of the GPU, so the gather and the H2D overlap the
-// previous steps' GEMMs and only the first copy of an epoch is exposed.
+// previous steps' GEMMs and only the first copy of a call is exposed (the
+// trainer synchronises once per call, not per epoch).  When a step's rows are
+// consecutive in page-locked dataset memory (no shuffle), the copy stream
+// reads them in place: no gather, no staging slot.
 #pragma once
 
 #include <cuda_runtime.h>
@@ -26,7 +29,7 @@ struct InputPipeline {
     cudaEvent_t consumed[kSlots] = {};  // the step staged the slot (device buffer reusable)
     bool pending[kSlots] = {};
     cudaStream_t copy = nullptr;
-    double* cum_loss_host = nullptr;  // pinned: running loss sum after every step of the epoch
+    double* cum_loss_host = nullptr;  // pinned: running loss sum after every step of the call
     size_t cum_loss_count = 0;
 
     void reserve(size_t floats, size_t steps) {
