@@ -261,6 +261,17 @@ int lane_b200_train_minibatch(lane_b200_net* net, const float* X_host, const flo
  * for the tall long-K shapes, 3xTF32 otherwise; LANE_B200_TC_PREC overrides). */
 int lane_b200_gemm(lane_b200_ctx* ctx, int op, int M, int N, int K, const float* A, const float* B,
                    float* C, float* C2, const float* bias, const float* aux, int epilogue, int use_tc);
+/* The same with caller-supplied 3xF16 operand maxima (float bits of max |.|):
+ * amax per row of op(A) (M), bmax per column of op(B) (N), as
+ * lane_b200_absmax computes them; used when the call runs the 3xF16 kernel
+ * (the mini-batch step computes them once per step, not per GEMM). */
+int lane_b200_gemm_ex(lane_b200_ctx* ctx, int op, int M, int N, int K, const float* A, const float* B,
+                      float* C, float* C2, const float* bias, const float* aux, int epilogue, int use_tc,
+                      const unsigned* amax, const unsigned* bmax);
+/* max |x| (as float bits) of every row and every column of a row-major
+ * rows x cols device matrix (cols % 4 == 0), one pass. */
+int lane_b200_absmax(lane_b200_ctx* ctx, const float* X, int rows, int cols, unsigned* row_max,
+                     unsigned* col_max);
 
 /* ---------------------------------------------- datasets --- */
 /* DataSet (include/lane/dataset.hpp:16-23) held by the library in page-locked

@@ -69,6 +69,8 @@ SIGNATURES = {
     "lane_b200_dataset_enlarge": (_I, [_V, _S, _F, C.POINTER(_U64), C.POINTER(_V)]),
     "lane_b200_dataset_destroy": (_I, [_V]),
     "lane_b200_gemm": (_I, [_V, _I, _I, _I, _I, _V, _V, _V, _V, _V, _V, _I, _I]),
+    "lane_b200_gemm_ex": (_I, [_V, _I, _I, _I, _I, _V, _V, _V, _V, _V, _V, _I, _I, _V, _V]),
+    "lane_b200_absmax": (_I, [_V, _V, _I, _I, _V, _V]),
     "lane_b200_nccl_unique_id": (_I, [_V, _S]),
     "lane_b200_comm_init": (_I, [_V, _I, _I, _V, _S]),
     "lane_b200_comm_destroy": (_I, [_V]),

@@ -1910,6 +1910,24 @@ int lane_b200_dataset_destroy(lane_b200_dataset* d) {
 }
 int lane_b200_gemm(lane_b200_ctx* c, int op, int M, int N, int K, const float* A, const float* B, float* C,
                    float* C2, const float* bias, const float* aux, int epilogue, int use_tc) {
+    return lane_b200_gemm_ex(c, op, M, N, K, A, B, C, C2, bias, aux, epilogue, use_tc, nullptr, nullptr);
+}
+
+int lane_b200_absmax(lane_b200_ctx* c, const float* X, int rows, int cols, unsigned* row_max, unsigned* col_max) {
+    return guard([&] {
+        if (!c || !X || !row_max || !col_max || rows < 1 || cols < 4 || (cols & 3))
+            throw Error(LANE_ERR_CONFIG, "lane_b200_absmax: bad arguments (cols a positive multiple of 4)");
+        LANE_CUDA(cudaMemsetAsync(row_max, 0, (size_t)rows * sizeof(unsigned), c->stream));
+        LANE_CUDA(cudaMemsetAsync(col_max, 0, (size_t)cols * sizeof(unsigned), c->stream));
+        absmax_rc_launch(c->stream, X, rows, cols, row_max, col_max);
+        c->count(1);
+        c->check_launch();
+    });
+}
+
+int lane_b200_gemm_ex(lane_b200_ctx* c, int op, int M, int N, int K, const float* A, const float* B, float* C,
+                      float* C2, const float* bias, const float* aux, int epilogue, int use_tc, const unsigned* amax,
+                      const unsigned* bmax) {
     return guard([&] {
         if (!c) throw Error(LANE_ERR_CONFIG, "null context");
         if (op < 0 || op > 2 || epilogue < 0 || epilogue > 3 || M < 0 || N < 0 || K < 0 || use_tc < 0 || use_tc > 5)
@@ -1930,7 +1948,11 @@ int lane_b200_gemm(lane_b200_ctx* c, int op, int M, int N, int K, const float* A
         if (use_tc == 2) tc_persist_mode() = 2;  // the persistent stream-K kernel for every shape
         if (use_tc == 3) tc_persist_mode() = 0;  // never
         try {
-            gemm(g, o, M, N, K, A, lda, B, ldb, static_cast<Epi>(epilogue), C, C2, bias, aux);
+            GemmMax mx;
+            mx.a = amax;
+            mx.b = bmax;
+            gemm(g, o, M, N, K, A, lda, B, ldb, static_cast<Epi>(epilogue), C, C2, bias, aux,
+                 (amax && bmax) ? &mx : nullptr);
         } catch (...) {
             gemm_tc_mode() = saved;
             tc_persist_mode() = saved_p;

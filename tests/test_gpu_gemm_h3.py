@@ -92,3 +92,37 @@ def test_h3_sass_uses_f16_tensor_cores(dev):
     sass = subprocess.run(["cuobjdump", "-sass", _build.LIB], capture_output=True, text=True).stdout
     # kind::f16 MMAs show up as HMMA-class tcgen05 instructions in the k_gemm_h3 functions
     assert "k_gemm_h3" in sass
+
+
+@pytest.mark.parametrize("op", [NN, NT, TN])
+def test_h3_caller_maxima_bitwise(dev, op):
+    # lane_b200_absmax + lane_b200_gemm_ex (the maxima the step computes once
+    # per step) give the bits of the self-contained call
+    import ctypes as C
+    from paper_2001_04206_b200 import _native
+    L = _native.lib()
+    M, N, K = 1024, 512, 2048
+    rs = np.random.default_rng(17 + op)
+    A, B, Am, Bm = operands(op, M, N, K, rs)
+    ref, _, _ = run(dev, op, M, N, K, A, B, STORE, use_tc=H3)
+    from test_gpu_gemm import put
+    pa, pb = put(dev, A), put(dev, B)
+    ar = (K, M) if op == TN else (M, K)
+    br = (N, K) if op == NT else (K, N)
+    bufs = [dev.alloc(4 * x) for x in (*ar, *br)]
+    assert L.lane_b200_absmax(dev._p, C.c_void_p(pa), ar[0], ar[1], C.c_void_p(bufs[0]), C.c_void_p(bufs[1])) == 0
+    assert L.lane_b200_absmax(dev._p, C.c_void_p(pb), br[0], br[1], C.c_void_p(bufs[2]), C.c_void_p(bufs[3])) == 0
+    amax = bufs[1] if op == TN else bufs[0]
+    bmax = bufs[2] if op == NT else bufs[3]
+    pc = dev.alloc(M * N * 4)
+    before = dev.kernel_launches
+    rc = L.lane_b200_gemm_ex(dev._p, op, M, N, K, C.c_void_p(pa), C.c_void_p(pb), C.c_void_p(pc), None, None, None,
+                             STORE, H3, C.c_void_p(amax), C.c_void_p(bmax))
+    assert rc == 0, L.lane_b200_last_error()
+    dev.sync()
+    assert dev.kernel_launches - before in (1, 2)  # no maxima passes (+ the tail reduce)
+    out = np.zeros((M, N), np.float32)
+    dev.d2h(out, pc)
+    assert np.array_equal(out.view(np.uint32), ref.view(np.uint32))
+    for p in (pa, pb, pc, *bufs):
+        dev.free(p)
