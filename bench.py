@@ -656,8 +656,8 @@ def main():
                        "l2": f"inputs {X.nbytes + T.nbytes} B > 126 MB L2, streamed each step"
                        if X.nbytes + T.nbytes > 126e6 else "inputs fit in L2"},
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
-                         "frac": achieved / peak, "traffic": load_traffic(wl)[0] if wl == "c2" else None,
-                         "traffic_source": load_traffic(wl)[1] if wl == "c2" else None,
+                         "frac": achieved / peak, "traffic": load_traffic(wl)[0],
+                         "traffic_source": load_traffic(wl)[1],
                          "peak_kind": peak_kind,
                          "kernel": {"window": "k_sgd_window", "cluster": "k_sgd_cluster",
                                     "grid": "k_sgd_grid"}.get(plan.split()[0], "layer kernels"),
