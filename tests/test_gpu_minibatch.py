@@ -154,6 +154,10 @@ FULL = {
     # name: (F, H, C, B, eta, mu, steps) -- the bench's C3 and C5 (BASELINE.json configs[2], [4])
     "c3": (1024, [4096, 4096], 10, 256, 0.01, 0.9, 3),
     "c5": (4096, [4096] * 8, 10, 4096, 1e-3, 0.9, 2),
+    # C5's per-rank shards at 2 and 8 ranks (the SCALE runs): 3xF16 with
+    # split-K (B = 512) and without (B = 2048)
+    "c5-rank2": (4096, [4096] * 8, 10, 2048, 1e-3, 0.9, 2),
+    "c5-rank8": (4096, [4096] * 8, 10, 512, 1e-3, 0.9, 2),
 }
 
 
