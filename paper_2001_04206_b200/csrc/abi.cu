@@ -24,6 +24,7 @@
 #include "nvls.cuh"
 #include "pipeline.cuh"
 #include "sgd_persistent.cuh"
+#include "sgd_tiny.cuh"
 #include "sgd_window.cuh"
 
 using namespace lane_b200;
@@ -891,12 +892,64 @@ void stream_layer_path(lane_b200_net* net, const float* X, const float* T, size_
     LANE_CUDA(cudaGraphDestroy(graph));
 }
 
+// the one-warp kernel for tiny one-hidden-layer nets in STRICT numerics (it
+// computes in the reference's order, bit for bit); LANE_B200_SGD_MODE
+// selects another plan
+bool tiny_plan(const lane_b200_net* net) {
+    if (net->n_hidden != 1 || net->ctx->numerics != LANE_NUMERICS_STRICT) return false;
+    const char* mode = std::getenv("LANE_B200_SGD_MODE");
+    if (mode && std::strcmp(mode, "tiny") != 0) return false;
+    return tiny_fits(static_cast<int>(net->input_width), static_cast<int>(net->layers[0].O),
+                     static_cast<int>(net->classes));
+}
+
 void sgd_stream_impl(lane_b200_net* net, const float* X, const float* T, size_t n, const uint32_t* order,
                      size_t n_steps, float eta, double* loss_sum, unsigned long long* correct) {
     check_eta(eta);
     if (n == 0) throw Error(LANE_ERR_TRAINING, "sgd_stream: empty sample set");
     if (!X || !T) throw Error(LANE_ERR_CONFIG, "sgd_stream: null data");
     if (n_steps == 0) return;
+    if (tiny_plan(net)) {
+        // one warp for the whole stream, reference arithmetic (sgd_tiny.cuh)
+        lane_b200_ctx* c = net->ctx;
+        LayerBufs& L0 = net->L(0);
+        LayerBufs& L1 = net->L(1);
+        TinyArgs A{};
+        A.I = static_cast<int>(net->input_width);
+        A.H = static_cast<int>(L0.O);
+        A.C = static_cast<int>(net->classes);
+        A.X = X;
+        A.T = T;
+        A.order = order;
+        A.n = static_cast<long long>(n);
+        A.n_steps = static_cast<long long>(n_steps);
+        A.base = 0;
+        A.neg_eta = -eta;
+        A.W0 = L0.buf[LANE_BUF_W];
+        A.b0 = L0.buf[LANE_BUF_B];
+        A.W1 = L1.buf[LANE_BUF_W];
+        A.b1 = L1.buf[LANE_BUF_B];
+        A.x0 = L0.buf[LANE_BUF_INPUTS];
+        A.z0 = L0.buf[LANE_BUF_NETIN];
+        A.a0 = L0.buf[LANE_BUF_OUTPUTS];
+        A.d0 = L0.buf[LANE_BUF_DELTAS];
+        A.db0 = L0.buf[LANE_BUF_DELTA_BIASES];
+        A.G0 = L0.buf[LANE_BUF_G];
+        A.DW0 = L0.buf[LANE_BUF_DW];
+        A.x1 = L1.buf[LANE_BUF_INPUTS];
+        A.z1 = L1.buf[LANE_BUF_NETIN];
+        A.a1 = L1.buf[LANE_BUF_OUTPUTS];
+        A.d1 = L1.buf[LANE_BUF_DELTAS];
+        A.db1 = L1.buf[LANE_BUF_DELTA_BIASES];
+        A.G1 = L1.buf[LANE_BUF_G];
+        A.DW1 = L1.buf[LANE_BUF_DW];
+        A.loss_sum = loss_sum;
+        A.correct = correct;
+        tiny_launch(c->stream, A);
+        c->count();
+        c->check_launch();
+        return;
+    }
     const SgdPlan P = plan_persistent(net);
     if (P.ok && P.window) {
         // the banded Gram scratch is sized per launch: stream in chunks
@@ -1425,7 +1478,9 @@ int lane_b200_sgd_stream_plan(lane_b200_net* net, char* buf, size_t len) {
         if (!net || !buf || len == 0) throw Error(LANE_ERR_CONFIG, "null argument");
         const SgdPlan P = plan_persistent(net);
         char tmp[128];
-        if (!P.ok)
+        if (tiny_plan(net))
+            std::snprintf(tmp, sizeof tmp, "tiny one warp, reference arithmetic");
+        else if (!P.ok)
             std::snprintf(tmp, sizeof tmp, "layer");
         else if (P.window)
             std::snprintf(tmp, sizeof tmp, "window D=%d KS=%d QPC=%d chain=%dx%dx%d ctas=%d smem=%zu", P.D, P.ks,

@@ -871,3 +871,44 @@ def test_minibatch_random_shapes_vs_oracle(lane, fast, F, H, C, B, mu):
         assert_close(layer.gradients, orc.get(l, po.G), 2e-4, f"G{l}")
     fast.free(Xd)
     fast.free(Td)
+
+
+@pytest.mark.parametrize("F,H,C", [(4, [8], 3), (2, [4], 2), (32, [32], 16), (17, [13], 5)])
+def test_sgd_tiny_stream_bitwise_vs_oracle(lane, strict, F, H, C):
+    """STRICT: the one-warp tiny-net kernel computes in the reference's
+    order, so a 200-sample stream (with an order permutation) equals the
+    oracle's per-sample BackwardPlan::run bit for bit -- every LayerState
+    buffer and the loss sum."""
+    X, T = po.synthetic_dataset(F, C, 50, 5)
+    net = lane.build_network(F, H, C, seed=3, device=strict)
+    assert net.sgd_plan().split()[0] == "tiny"
+    orc = po.OracleNet(F, H, C, seed=3)
+    rs = np.random.default_rng(F * 100 + H[0])
+    order = rs.integers(0, 50, 200).astype(np.uint32)
+    dev = strict
+    xd, td, od, ld = dev.alloc(X.nbytes), dev.alloc(T.nbytes), dev.alloc(order.nbytes), dev.alloc(16)
+    dev.h2d(xd, X)
+    dev.h2d(td, T)
+    dev.h2d(od, order)
+    dev.h2d(ld, np.zeros(2, np.float64))
+    net.sgd_stream(xd, td, 50, 200, 0.05, order_dev=od, loss_dev=ld, correct_dev=ld + 8)
+    dev.sync()
+    want = orc.sgd_run(X, T, 200, 0.05, order)  # loss sum in sample order, double
+    st = np.zeros(2, np.float64)
+    dev.d2h(st, ld)
+    assert st[0] == want, (st[0], want)
+    assert net.hash() == orc.hash(), "tiny stream not bit-identical to the reference order"
+    for li, layer in enumerate(net.layers):
+        for buf in BUFS:
+            assert_bitwise(getattr(layer, buf), orc.get(li, BUFS.index(buf)), f"layer {li} {buf}")
+    for p_ in (xd, td, od, ld):
+        dev.free(p_)
+
+
+
+@pytest.mark.parametrize("F,H,C,want", [(4, [8], 3, "tiny"), (2, [4], 2, "tiny"), (32, [32], 16, "tiny"),
+                                        (33, [32], 16, "layer"), (784, [128], 10, "layer")])
+def test_sgd_plan_selection_strict(lane, strict, F, H, C, want):
+    # STRICT: tiny nets run the one-warp reference-order kernel, the rest the layer path
+    net = lane.build_network(F, H, C, seed=42, device=strict)
+    assert net.sgd_plan().split()[0] == want, net.sgd_plan()
