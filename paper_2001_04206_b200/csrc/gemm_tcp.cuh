@@ -44,12 +44,16 @@ constexpr int kTpAcc = 2;                             // TMEM accumulators
 constexpr int kTpTileElems = kTcBM * kTcBN;
 constexpr int kTpUpdChunk = kTcBM * 32 * 4;  // one 128 x 32 fp32 chunk of W or V (SW128)
 
+// UPDATE keeps 4 W/V chunk slots with loads 3 chunks ahead (2 MMA stages):
+// the update epilogue streams W and V from HBM and is latency-bound with
+// fewer chunks in flight (C3's wgrad + update, DRAM at 37% of peak with 2)
+constexpr int kTpUpdSlots = 4;
 template <int E>
 struct TpCfg {
     static constexpr bool kUpd = E == 4;                    // TpEpi::UPDATE
-    static constexpr int kStages = kUpd ? 3 : kTpStages;
+    static constexpr int kStages = kUpd ? 2 : kTpStages;
     static constexpr size_t kRing = (size_t)kStages * kTpStage;
-    static constexpr size_t kEpi = kUpd ? 2 * 2 * kTpUpdChunk : 0;  // 2 slots x (W, V)
+    static constexpr size_t kEpi = kUpd ? kTpUpdSlots * 2 * kTpUpdChunk : 0;  // slots x (W, V)
     static constexpr size_t kSmem = kRing + kEpi + 1024 + 512;
 };
 
@@ -264,8 +268,8 @@ __global__ void __launch_bounds__(kTpThreads, 1)
         for (int b = 0; b < kTpAcc; ++b) {
             tc_mbar_init(acc_full(b), 1);
             tc_mbar_init(acc_empty(b), kTpEpiWarps);
-            tc_mbar_init(epi_full(b), 1);
         }
+        for (int k = 0; k < kTpUpdSlots; ++k) tc_mbar_init(epi_full(k), 1);
         asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
         asm volatile("prefetch.tensormap [%0];\n" ::"l"(reinterpret_cast<uint64_t>(&tmA)) : "memory");
         asm volatile("prefetch.tensormap [%0];\n" ::"l"(reinterpret_cast<uint64_t>(&tmB)) : "memory");
@@ -414,9 +418,9 @@ __global__ void __launch_bounds__(kTpThreads, 1)
         if constexpr (Cfg::kUpd) {
             if (!args.sk) {
                 // wgrad + update, whole tiles: the leader TMA-loads the W and V
-                // chunks (128 rows x 32 columns, 128B swizzle) two chunks ahead
+                // chunks (128 rows x 32 columns, 128B swizzle) three chunks ahead
                 // -- across unit boundaries, i.e. during the next tile's MMAs --
-                // into two slots; every thread updates its row of the chunk in
+                // into four slots; every thread updates its row of the chunk in
                 // shared memory, G goes straight to global, and the leader
                 // TMA-stores the W and V chunks back.
                 constexpr int kChunks = kTcBN / 32;
@@ -429,7 +433,7 @@ __global__ void __launch_bounds__(kTpThreads, 1)
                     if (!lmore) return;
                     int mt, nt;
                     tp_tile_mn(args, lu.tile, mt, nt);
-                    const int k = lissued & 1;
+                    const int k = lissued % kTpUpdSlots;
                     const uint32_t wdst = tc_smem(epi_buf + (size_t)(2 * k) * kTpUpdChunk);
                     tc_mbar_expect_tx(epi_full(k), (uint32_t)kTpUpdChunk + vbytes);
                     tc_tma_2d(&tmW, epi_full(k), wdst, nt * kTcBN + 32 * lchunk, mt * kTcBM);
@@ -440,10 +444,8 @@ __global__ void __launch_bounds__(kTpThreads, 1)
                         lmore = tp_next(args, lit, lu);
                     }
                 };
-                if (leader) {
-                    issue_load();
-                    issue_load();
-                }
+                if (leader)
+                    for (int q = 0; q < kTpUpdSlots - 1; ++q) issue_load();
                 int gc = 0;  // chunks consumed
                 while (tp_next(args, it, u)) {
                     const int b = n_unit & 1;
@@ -462,8 +464,8 @@ __global__ void __launch_bounds__(kTpThreads, 1)
                             __syncwarp();
                             if (lane == 0) tc_mbar_arrive(acc_empty(b));
                         }
-                        const int k = gc & 1;
-                        tc_mbar_wait(epi_full(k), (uint32_t)((gc >> 1) & 1));
+                        const int k = gc % kTpUpdSlots;
+                        tc_mbar_wait(epi_full(k), (uint32_t)((gc / kTpUpdSlots) & 1));
                         uint8_t* wrow = epi_buf + (size_t)(2 * k) * kTpUpdChunk + row * 128;
                         uint8_t* vrow = wrow + kTpUpdChunk;
                         const bool full_cols = n0 + 32 * c + 32 <= args.N && (args.N & 3) == 0;
@@ -505,8 +507,10 @@ __global__ void __launch_bounds__(kTpThreads, 1)
                             tp_tma_store_2d(&tmW, wsrc, n0 + 32 * c, mt * kTcBM);
                             tp_tma_store_2d(&tmV, wsrc + kTpUpdChunk, n0 + 32 * c, mt * kTcBM);
                             asm volatile("cp.async.bulk.commit_group;\n" ::: "memory");
-                            // the slot is refilled once the stores have read it
-                            asm volatile("cp.async.bulk.wait_group.read 0;\n" ::: "memory");
+                            // the next load refills the previous chunk's slot, once
+                            // that chunk's stores have read it (this chunk's may
+                            // still be in flight)
+                            asm volatile("cp.async.bulk.wait_group.read 1;\n" ::: "memory");
                             issue_load();
                         }
                     }
