@@ -430,13 +430,18 @@ inline void colsum(GemmCtx& g, const float* D, int B, int O, float* gb) {
 // (with the epilogue) by k_sum_partials_epi.
 constexpr int kSkKC = 512;
 __global__ void __launch_bounds__(256) k_gemm_skinny_nn_kc(int M, int N, int K, const float* __restrict__ A,
-                                                           const float* __restrict__ B, float* __restrict__ part) {
+                                                           const float* __restrict__ B, float* __restrict__ part,
+                                                           int rpw) {
     __shared__ __align__(16) float bs[kSkKC * 16];
     const int k0 = blockIdx.y * kSkKC, k1 = min(K, k0 + kSkKC);
     stage_rows(bs, B + (size_t)k0 * N, (k1 - k0) * N);
     __syncthreads();
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    const int m = blockIdx.x * 8 + warp;
+    // rpw rows per warp (up to 8 when the rows are many), so a staged B chunk
+    // serves more rows (C5: 16 MB of B staging instead of 128 MB for 64 MB of A)
+#pragma unroll 1
+    for (int rr = 0; rr < rpw; ++rr) {
+    const int m = (blockIdx.x * 8 + warp) * rpw + rr;
     if (m >= M) return;
     float acc[16];
 #pragma unroll
@@ -470,6 +475,7 @@ __global__ void __launch_bounds__(256) k_gemm_skinny_nn_kc(int M, int N, int K, 
     const float v = acc[0] + __shfl_xor_sync(0xffffffffu, acc[0], 1);
     const int idx = ((lane >> 4) & 1) * 8 + ((lane >> 3) & 1) * 4 + ((lane >> 2) & 1) * 2 + ((lane >> 1) & 1);
     if ((lane & 1) == 0 && idx < N) part[((size_t)blockIdx.y * M + m) * N + idx] = v;
+    }
 }
 
 // out = epilogue(sum_{s < S} part[s]) in a fixed order; bias per column
@@ -520,8 +526,74 @@ __global__ void __launch_bounds__(256) k_gemm_shortk_nt(int M, int N, int K, con
     }
 }
 
+// The same for N % 4 == 0 and many rows (the C5 output layer's dgrad,
+// 4096 x 4096 x 10): thread = 4 consecutive columns (float4 aux loads and C
+// stores), CTA = 1024 columns x 32 rows, rows 4 at a time so four loads are
+// in flight.  The plain kernel's 8-row CTAs re-read their W rows per CTA and
+// moved 4 bytes per thread per row (1.7 TB/s).
+constexpr int kShortRows = 32;  // rows per CTA at most (rows: a multiple of 4)
+template <Epi E>
+__global__ void __launch_bounds__(256) k_gemm_shortk_nt4(int M, int N, int K, const float* __restrict__ D,
+                                                         const float* __restrict__ W, float* __restrict__ C,
+                                                         const float* __restrict__ aux, int rows) {
+    __shared__ float ds[kShortRows][kShortK];
+    const int n4 = blockIdx.x * blockDim.x + threadIdx.x;  // columns 4 n4 .. 4 n4 + 3
+    const int m0 = blockIdx.y * rows;
+    for (int e = threadIdx.x; e < rows * kShortK; e += blockDim.x) {
+        const int r = e / kShortK, k = e - r * kShortK;
+        ds[r][k] = (m0 + r < M && k < K) ? D[(size_t)(m0 + r) * K + k] : 0.0f;
+    }
+    __syncthreads();
+    if (4 * n4 >= N) return;
+    float w[4][kShortK];
+#pragma unroll
+    for (int c = 0; c < 4; ++c)
+#pragma unroll
+        for (int k = 0; k < kShortK; ++k) w[c][k] = k < K ? __ldg(W + (size_t)(4 * n4 + c) * K + k) : 0.0f;
+#pragma unroll 1
+    for (int r0 = 0; r0 < rows; r0 += 4) {
+        float4 t[4];
+        if constexpr (E == Epi::TANH_GRAD) {
+#pragma unroll
+            for (int q = 0; q < 4; ++q)
+                t[q] = m0 + r0 + q < M ? __ldg(reinterpret_cast<const float4*>(aux + (size_t)(m0 + r0 + q) * N) + n4)
+                                       : make_float4(0.f, 0.f, 0.f, 0.f);
+        }
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+            const int m = m0 + r0 + q;
+            if (m >= M) break;
+            float acc[4] = {0.f, 0.f, 0.f, 0.f};
+#pragma unroll
+            for (int k = 0; k < kShortK; ++k)
+#pragma unroll
+                for (int c = 0; c < 4; ++c) acc[c] = fmaf(ds[r0 + q][k], w[c][k], acc[c]);
+            float4 o = make_float4(acc[0], acc[1], acc[2], acc[3]);
+            if constexpr (E == Epi::TANH_GRAD)
+                o = make_float4(tanh_grad(t[q].x, acc[0]), tanh_grad(t[q].y, acc[1]), tanh_grad(t[q].z, acc[2]),
+                                tanh_grad(t[q].w, acc[3]));
+            reinterpret_cast<float4*>(C + (size_t)m * N)[n4] = o;
+        }
+    }
+}
+
 inline bool gemm_try_skinny(GemmCtx& g, GemmOp op, int M, int N, int K, const float* A, int lda, const float* B,
                             int ldb, Epi e, float* C, float* C2, const float* bias, const float* aux) {
+    if (op == GemmOp::NT && K <= kShortK && lda == K && ldb == K && (e == Epi::STORE || e == Epi::TANH_GRAD) &&
+        (N & 3) == 0 && (reinterpret_cast<uintptr_t>(C) & 15) == 0 &&
+        (!aux || (reinterpret_cast<uintptr_t>(aux) & 15) == 0)) {
+        // rows per CTA: up to 32, but at least ~2 CTAs per SM
+        const int colblocks = (N / 4 + 255) / 256;
+        int rows = (M / std::max(1, (2 * g.sm_count + colblocks - 1) / colblocks)) & ~3;
+        rows = std::max(4, std::min(kShortRows, rows));
+        const dim3 grid(colblocks, (M + rows - 1) / rows);
+        if (e == Epi::STORE)
+            k_gemm_shortk_nt4<Epi::STORE><<<grid, 256, 0, g.stream>>>(M, N, K, A, B, C, nullptr, rows);
+        else
+            k_gemm_shortk_nt4<Epi::TANH_GRAD><<<grid, 256, 0, g.stream>>>(M, N, K, A, B, C, aux, rows);
+        *g.launches += 1;
+        return true;
+    }
     if (op == GemmOp::NT && K <= kShortK && lda == K && ldb == K && (e == Epi::STORE || e == Epi::TANH_GRAD)) {
         const dim3 grid((N + 255) / 256, (M + 7) / 8);
         if (e == Epi::STORE)
@@ -536,7 +608,10 @@ inline bool gemm_try_skinny(GemmCtx& g, GemmOp op, int M, int N, int K, const fl
         // long K: chunked, B chunk in shared memory, fixed-order partial sum
         const int S = (K + kSkKC - 1) / kSkKC;
         ensure_ws(g, (size_t)S * M * N);
-        k_gemm_skinny_nn_kc<<<dim3((M + 7) / 8, S), 256, 0, g.stream>>>(M, N, K, A, B, *g.ws);
+        // one row per warp: several rows per warp (less B staging) measured
+        // slower at C5's 4096 x 10 x 4096 (70.7 vs 65 us)
+        const int rpw = 1;
+        k_gemm_skinny_nn_kc<<<dim3((M + 8 * rpw - 1) / (8 * rpw), S), 256, 0, g.stream>>>(M, N, K, A, B, *g.ws, rpw);
         const int blocks = std::max(1, std::min(4 * g.sm_count, (M * N + 255) / 256));
         switch (e) {
             case Epi::STORE: k_sum_partials_epi<Epi::STORE><<<blocks, 256, 0, g.stream>>>(*g.ws, S, M, N, C, C2, bias); break;
