@@ -807,22 +807,25 @@ inline void gemm_h3(GemmCtx& g, GemmOp op, int M, int N, int K, const float* A, 
     static const int diag = std::getenv("LANE_B200_H3_DIAG") ? std::atoi(std::getenv("LANE_B200_H3_DIAG")) : 0;
     t.diag = diag;
     *g.launches += S > 1 ? 1 : 0;
+    // the epilogue's TMA store boxes: 32 columns x 32 rows, 128-byte swizzle
+    const CUtensorMap mc = tc_map(C, M, N, 32, 32, 0);
+    const CUtensorMap mc2 = e == Epi::BIAS_TANH ? tc_map(C2, M, N, 32, 32, 0) : mc;
     switch (e) {
         case Epi::STORE:
-            if (pair) h3_dispatch<TcEpi::STORE, true>(g.stream, a_mn, b_mn, ma, mb, t);
-            else h3_dispatch<TcEpi::STORE, false>(g.stream, a_mn, b_mn, ma, mb, t);
+            if (pair) h3_dispatch<TcEpi::STORE, true>(g.stream, a_mn, b_mn, ma, mb, mc, mc2, t);
+            else h3_dispatch<TcEpi::STORE, false>(g.stream, a_mn, b_mn, ma, mb, mc, mc2, t);
             break;
         case Epi::BIAS:
-            if (pair) h3_dispatch<TcEpi::BIAS, true>(g.stream, a_mn, b_mn, ma, mb, t);
-            else h3_dispatch<TcEpi::BIAS, false>(g.stream, a_mn, b_mn, ma, mb, t);
+            if (pair) h3_dispatch<TcEpi::BIAS, true>(g.stream, a_mn, b_mn, ma, mb, mc, mc2, t);
+            else h3_dispatch<TcEpi::BIAS, false>(g.stream, a_mn, b_mn, ma, mb, mc, mc2, t);
             break;
         case Epi::BIAS_TANH:
-            if (pair) h3_dispatch<TcEpi::BIAS_TANH, true>(g.stream, a_mn, b_mn, ma, mb, t);
-            else h3_dispatch<TcEpi::BIAS_TANH, false>(g.stream, a_mn, b_mn, ma, mb, t);
+            if (pair) h3_dispatch<TcEpi::BIAS_TANH, true>(g.stream, a_mn, b_mn, ma, mb, mc, mc2, t);
+            else h3_dispatch<TcEpi::BIAS_TANH, false>(g.stream, a_mn, b_mn, ma, mb, mc, mc2, t);
             break;
         case Epi::TANH_GRAD:
-            if (pair) h3_dispatch<TcEpi::TANH_GRAD, true>(g.stream, a_mn, b_mn, ma, mb, t);
-            else h3_dispatch<TcEpi::TANH_GRAD, false>(g.stream, a_mn, b_mn, ma, mb, t);
+            if (pair) h3_dispatch<TcEpi::TANH_GRAD, true>(g.stream, a_mn, b_mn, ma, mb, mc, mc2, t);
+            else h3_dispatch<TcEpi::TANH_GRAD, false>(g.stream, a_mn, b_mn, ma, mb, mc, mc2, t);
             break;
     }
     *g.launches += 1;
@@ -844,7 +847,8 @@ inline bool gemm_try_tc(GemmCtx& g, GemmOp op, int M, int N, int K, const float*
                         int ldb, Epi e, float* C, float* C2, const float* bias, const float* aux,
                         const GemmMax* mx = nullptr, bool* fused = nullptr) {
     if (!gemm_tc_mode() || !tc_eligible(M, N, K)) return false;
-    if ((reinterpret_cast<uintptr_t>(A) | reinterpret_cast<uintptr_t>(B) | reinterpret_cast<uintptr_t>(C)) & 15)
+    if ((reinterpret_cast<uintptr_t>(A) | reinterpret_cast<uintptr_t>(B) | reinterpret_cast<uintptr_t>(C) |
+         reinterpret_cast<uintptr_t>(C2)) & 15)
         return false;
     if (gemm_will_h3(op, M, N, K, A, lda, B, ldb, C)) {
         bool f = false;

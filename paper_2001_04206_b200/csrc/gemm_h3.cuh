@@ -114,6 +114,14 @@ __device__ __forceinline__ void h3_sts4(uint32_t a, uint32_t x, uint32_t y, uint
     asm volatile("st.shared.v4.b32 [%0], {%1,%2,%3,%4};\n" ::"r"(a), "r"(x), "r"(y), "r"(z), "r"(w) : "memory");
 }
 
+// TMA store of one 2-D box from shared memory (bulk group)
+__device__ __forceinline__ void h3_tma_store_2d(const CUtensorMap* map, uint32_t src, int c0, int c1) {
+    asm volatile("cp.async.bulk.tensor.2d.global.shared::cta.bulk_group [%0, {%1, %2}], [%3];\n" ::"l"(
+                     reinterpret_cast<uint64_t>(map)),
+                 "r"(c0), "r"(c1), "r"(src)
+                 : "memory");
+}
+
 // 16 consecutive K values of one row (K-major SW128 fp32 tile, 128-byte rows)
 // or of one column (MN-major unswizzled [32 k][128] fp32 tile); t is a
 // shared-window address (explicit ld.shared: no generic-address loads)
@@ -148,7 +156,8 @@ __device__ __forceinline__ void h3_tile_mn(int t, int tiles_m, int tiles_n, int&
 
 template <bool A_MN, bool B_MN, TcEpi E, bool PAIR>
 __global__ void __launch_bounds__(kH3Threads, 1)
-    k_gemm_h3(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB, TcArgs args) {
+    k_gemm_h3(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
+              const __grid_constant__ CUtensorMap tmC, const __grid_constant__ CUtensorMap tmC2, TcArgs args) {
     using Cfg = H3Cfg<PAIR>;
     constexpr int kS = Cfg::kStages, kL = Cfg::kLand;
     extern __shared__ uint8_t h3_raw[];
@@ -430,6 +439,10 @@ __global__ void __launch_bounds__(kH3Threads, 1)
         // per column (warp max over this warp's 32 rows, one atomicMax per lane)
         const bool omax = args.omax_row != nullptr && !split && tail < 0;
         unsigned rmax = 0;
+        // this warp's store staging (C, then C2): 8 KB of the landing ring,
+        // idle once every K block has been split
+        const uint32_t stg = sbase + (uint32_t)((warp - 2) * 8192);
+        bool stg_pending = false;
 #pragma unroll 1
         for (int c0 = cbeg; c0 < cbeg + kCols; c0 += 32) {
             uint32_t rr[32];
@@ -480,41 +493,68 @@ __global__ void __launch_bounds__(kH3Threads, 1)
                 continue;
             }
             uint32_t ob[32];  // |consumed output| bits (0 past M / N)
+            float cv[32], c2v[32];  // the chunk's C and (BIAS_TANH) C2 values of this row
             if (nb0 + 32 <= args.N && (args.N & 3) == 0) {
 #pragma unroll
                 for (int q = 0; q < 8; ++q) {
                     float4 vv = make_float4(x[4 * q], x[4 * q + 1], x[4 * q + 2], x[4 * q + 3]);
                     float4 t = make_float4(0.f, 0.f, 0.f, 0.f);
-                    if (mrow) {
-                        vv = tc_epi4<E>(args, m, nb0 + 4 * q, vv, &t);
-                        *reinterpret_cast<float4*>(args.C + (size_t)m * args.N + nb0 + 4 * q) = vv;
-                        if constexpr (E == TcEpi::BIAS_TANH)
-                            *reinterpret_cast<float4*>(args.C2 + (size_t)m * args.N + nb0 + 4 * q) = t;
-                    }
-                    const float4 o = E == TcEpi::BIAS_TANH ? t : vv;
-                    ob[4 * q + 0] = mrow ? __float_as_uint(fabsf(o.x)) : 0u;
-                    ob[4 * q + 1] = mrow ? __float_as_uint(fabsf(o.y)) : 0u;
-                    ob[4 * q + 2] = mrow ? __float_as_uint(fabsf(o.z)) : 0u;
-                    ob[4 * q + 3] = mrow ? __float_as_uint(fabsf(o.w)) : 0u;
+                    if (mrow) vv = tc_epi4<E>(args, m, nb0 + 4 * q, vv, &t);
+                    cv[4 * q + 0] = vv.x;
+                    cv[4 * q + 1] = vv.y;
+                    cv[4 * q + 2] = vv.z;
+                    cv[4 * q + 3] = vv.w;
+                    c2v[4 * q + 0] = t.x;
+                    c2v[4 * q + 1] = t.y;
+                    c2v[4 * q + 2] = t.z;
+                    c2v[4 * q + 3] = t.w;
                 }
             } else {
 #pragma unroll
                 for (int q = 0; q < 32; ++q) {
                     const int n = nb0 + q;
-                    ob[q] = 0u;
-                    if (n >= args.N || !mrow) continue;
-                    float vv = x[q];
-                    const size_t idx = (size_t)m * args.N + n;
-                    if constexpr (E == TcEpi::BIAS || E == TcEpi::BIAS_TANH) vv = sadd(vv, args.bias[n]);
-                    if constexpr (E == TcEpi::TANH_GRAD) vv = tanh_grad(args.aux[idx], vv);
-                    args.C[idx] = vv;
-                    float o = vv;
-                    if constexpr (E == TcEpi::BIAS_TANH) {
-                        o = tanhf(vv);
-                        args.C2[idx] = o;
+                    float vv = x[q], o2 = 0.0f;
+                    if (n < args.N && mrow) {
+                        const size_t idx = (size_t)m * args.N + n;
+                        if constexpr (E == TcEpi::BIAS || E == TcEpi::BIAS_TANH) vv = sadd(vv, args.bias[n]);
+                        if constexpr (E == TcEpi::TANH_GRAD) vv = tanh_grad(args.aux[idx], vv);
+                        if constexpr (E == TcEpi::BIAS_TANH) o2 = tanhf(vv);
                     }
-                    ob[q] = __float_as_uint(fabsf(o));
+                    cv[q] = vv;
+                    c2v[q] = o2;
                 }
+            }
+#pragma unroll
+            for (int q = 0; q < 32; ++q) {
+                const float o = E == TcEpi::BIAS_TANH ? c2v[q] : cv[q];
+                ob[q] = (mrow && nb0 + q < args.N) ? __float_as_uint(fabsf(o)) : 0u;
+            }
+            // Stores: the warp stages its 32 rows x 32 columns in the (now idle)
+            // landing ring, row-major with the 128-byte swizzle, and one lane
+            // TMA-stores the box -- full-line writes (the tensor map clips rows
+            // and columns past M and N).  Row-per-thread float4 stores touched 32
+            // lines per instruction and cost 53 us of the 4096^3 forward's 350.
+            if (!(args.diag & 128)) {
+                if (lane == 0 && stg_pending) asm volatile("cp.async.bulk.wait_group.read 0;\n" ::: "memory");
+                __syncwarp();
+#pragma unroll
+                for (int q = 0; q < 8; ++q) {
+                    const uint32_t off = (uint32_t)(lane * 128 + ((q ^ (lane & 7)) * 16));
+                    h3_sts4(stg + off, __float_as_uint(cv[4 * q]), __float_as_uint(cv[4 * q + 1]),
+                            __float_as_uint(cv[4 * q + 2]), __float_as_uint(cv[4 * q + 3]));
+                    if constexpr (E == TcEpi::BIAS_TANH)
+                        h3_sts4(stg + 4096 + off, __float_as_uint(c2v[4 * q]), __float_as_uint(c2v[4 * q + 1]),
+                                __float_as_uint(c2v[4 * q + 2]), __float_as_uint(c2v[4 * q + 3]));
+                }
+                asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");
+                __syncwarp();
+                if (lane == 0) {
+                    const int mrow0 = m0 + quarter * 32;
+                    h3_tma_store_2d(&tmC, stg, nb0, mrow0);
+                    if constexpr (E == TcEpi::BIAS_TANH) h3_tma_store_2d(&tmC2, stg + 4096, nb0, mrow0);
+                    asm volatile("cp.async.bulk.commit_group;\n" ::: "memory");
+                }
+                stg_pending = true;
             }
             if (omax) {
                 unsigned mine = 0;
@@ -528,6 +568,7 @@ __global__ void __launch_bounds__(kH3Threads, 1)
             }
         }
         if (omax && m < args.M) atomicMax(args.omax_row + m, rmax);
+        if (lane == 0 && stg_pending) asm volatile("cp.async.bulk.wait_group 0;\n" ::: "memory");
     }
     asm volatile("tcgen05.fence::before_thread_sync;\n" ::: "memory");
     if constexpr (PAIR)
@@ -681,7 +722,8 @@ inline void absmax_launch(cudaStream_t st, const float* X, int R, int C, bool ro
 }
 
 template <bool A_MN, bool B_MN, TcEpi E, bool PAIR>
-inline void h3_launch(cudaStream_t st, const CUtensorMap& a, const CUtensorMap& b, const TcArgs& args) {
+inline void h3_launch(cudaStream_t st, const CUtensorMap& a, const CUtensorMap& b, const CUtensorMap& c,
+                      const CUtensorMap& c2, const TcArgs& args) {
     constexpr size_t smem = H3Cfg<PAIR>::kSmem;
     static std::atomic<uint64_t> configured{0};
     int dev = 0;
@@ -709,10 +751,10 @@ inline void h3_launch(cudaStream_t st, const CUtensorMap& a, const CUtensorMap& 
         attr[0].val.clusterDim.z = 1;
         cfg.attrs = attr;
         cfg.numAttrs = 1;
-        LANE_CUDA(cudaLaunchKernelEx(&cfg, k_gemm_h3<A_MN, B_MN, E, PAIR>, a, b, args));
+        LANE_CUDA(cudaLaunchKernelEx(&cfg, k_gemm_h3<A_MN, B_MN, E, PAIR>, a, b, c, c2, args));
     } else {
         const dim3 grid((args.N + kTcBN - 1) / kTcBN, (args.M + kTcBM - 1) / kTcBM, S);
-        k_gemm_h3<A_MN, B_MN, E, PAIR><<<grid, kH3Threads, smem, st>>>(a, b, args);
+        k_gemm_h3<A_MN, B_MN, E, PAIR><<<grid, kH3Threads, smem, st>>>(a, b, c, c2, args);
     }
     if (S > 1) {
         const size_t n4 = (size_t)args.M * args.N / 4;
@@ -724,11 +766,11 @@ inline void h3_launch(cudaStream_t st, const CUtensorMap& a, const CUtensorMap& 
 
 template <TcEpi E, bool PAIR>
 inline void h3_dispatch(cudaStream_t st, bool a_mn, bool b_mn, const CUtensorMap& a, const CUtensorMap& b,
-                        const TcArgs& args) {
-    if (!a_mn && !b_mn) h3_launch<false, false, E, PAIR>(st, a, b, args);
-    else if (!a_mn && b_mn) h3_launch<false, true, E, PAIR>(st, a, b, args);
-    else if (a_mn && !b_mn) h3_launch<true, false, E, PAIR>(st, a, b, args);
-    else h3_launch<true, true, E, PAIR>(st, a, b, args);
+                        const CUtensorMap& c, const CUtensorMap& c2, const TcArgs& args) {
+    if (!a_mn && !b_mn) h3_launch<false, false, E, PAIR>(st, a, b, c, c2, args);
+    else if (!a_mn && b_mn) h3_launch<false, true, E, PAIR>(st, a, b, c, c2, args);
+    else if (a_mn && !b_mn) h3_launch<true, false, E, PAIR>(st, a, b, c, c2, args);
+    else h3_launch<true, true, E, PAIR>(st, a, b, c, c2, args);
 }
 
 }  // namespace lane_b200
