@@ -42,7 +42,10 @@ namespace lane_b200 {
 // 16 split warps (4 per SM sub-partition) in two groups of 8 that take
 // alternate K blocks (see the split loop)
 constexpr int kH3SplitWarps = 16;
-constexpr int kH3Group = 8;  // raster group (pair tile rows)
+#ifndef LANE_H3_RASTER
+#define LANE_H3_RASTER 8
+#endif
+constexpr int kH3Group = LANE_H3_RASTER;  // raster group (pair tile rows)
 #ifndef LANE_H3_GROUPS
 #define LANE_H3_GROUPS 4
 #endif
@@ -660,42 +663,65 @@ __global__ void __launch_bounds__(256) k_absmax_rc(const float* __restrict__ X, 
 
 
 // Finish the tail-wave tiles: sum the two K halves (half 0 + half 1, fixed
-// order), then the epilogue and the optional output maxima.  Grid
-// (tail tiles, 8 row chunks of 32), 256 threads = the tile's 256 columns.
+// order), then the epilogue and the optional output maxima.  Grid (tail tiles,
+// 16 chunks of 16 rows), 256 threads: 64 float4 columns x 4 row lanes, each
+// thread 4 rows (8 independent float4 loads in flight).  The first version
+// (one column per thread, a 32-row loop of scalar loads) took ~19 us per
+// GEMM at C5 -- 5% of the step.
+constexpr int kTailRows = 16;
 template <TcEpi E>
 __global__ void __launch_bounds__(256) k_h3_tail_reduce(TcArgs a) {
     const int t = a.full_units + (int)blockIdx.x;
     int mt, nt;
     h3_tile_mn(t, a.tiles_m, a.tiles_n, mt, nt);
-    const int n = nt * 256 + (int)threadIdx.x;
-    const int lane = threadIdx.x & 31;
+    const int c4 = (int)threadIdx.x & 63, ry = (int)threadIdx.x >> 6;
+    const int n = nt * 256 + 4 * c4;
+    const bool ncol = n < a.N;  // N % 4 == 0: the float4 is in or out as a whole
     const float* P0 = a.tail_part + (size_t)(2 * blockIdx.x) * 65536;
     const float* P1 = P0 + 65536;
-    unsigned cmax = 0;
-    for (int i = 0; i < 32; ++i) {
-        const int lr = (int)blockIdx.y * 32 + i;
+    float4 v0[4], v1[4];
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+        const int lr = (int)blockIdx.y * kTailRows + ry + 4 * i;
+        v0[i] = *reinterpret_cast<const float4*>(P0 + lr * 256 + 4 * c4);
+        v1[i] = *reinterpret_cast<const float4*>(P1 + lr * 256 + 4 * c4);
+    }
+    unsigned cm[4] = {0u, 0u, 0u, 0u};
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+        const int lr = (int)blockIdx.y * kTailRows + ry + 4 * i;
         const int m = mt * 256 + lr;
-        unsigned ob = 0;
-        if (m < a.M && n < a.N) {
-            float v = P0[lr * 256 + threadIdx.x] + P1[lr * 256 + threadIdx.x];
+        unsigned ob[4] = {0u, 0u, 0u, 0u};
+        if (m < a.M && ncol) {
+            float4 v = make_float4(v0[i].x + v1[i].x, v0[i].y + v1[i].y, v0[i].z + v1[i].z, v0[i].w + v1[i].w);
+            float4 o2 = make_float4(0.f, 0.f, 0.f, 0.f);
+            v = tc_epi4<E>(a, m, n, v, &o2);
             const size_t idx = (size_t)m * a.N + n;
-            if constexpr (E == TcEpi::BIAS || E == TcEpi::BIAS_TANH) v = sadd(v, a.bias[n]);
-            if constexpr (E == TcEpi::TANH_GRAD) v = tanh_grad(a.aux[idx], v);
-            a.C[idx] = v;
-            float o = v;
-            if constexpr (E == TcEpi::BIAS_TANH) {
-                o = tanhf(v);
-                a.C2[idx] = o;
-            }
-            ob = __float_as_uint(fabsf(o));
+            *reinterpret_cast<float4*>(a.C + idx) = v;
+            if constexpr (E == TcEpi::BIAS_TANH) *reinterpret_cast<float4*>(a.C2 + idx) = o2;
+            const float4 o = E == TcEpi::BIAS_TANH ? o2 : v;
+            ob[0] = __float_as_uint(fabsf(o.x));
+            ob[1] = __float_as_uint(fabsf(o.y));
+            ob[2] = __float_as_uint(fabsf(o.z));
+            ob[3] = __float_as_uint(fabsf(o.w));
         }
         if (a.omax_row) {
-            cmax = max(cmax, ob);
-            const unsigned rm = __reduce_max_sync(0xffffffffu, ob);
-            if (lane == 0 && m < a.M && rm) atomicMax(a.omax_row + m, rm);
+#pragma unroll
+            for (int j = 0; j < 4; ++j) cm[j] = max(cm[j], ob[j]);
+            const unsigned rm = __reduce_max_sync(0xffffffffu, max(max(ob[0], ob[1]), max(ob[2], ob[3])));
+            if ((threadIdx.x & 31) == 0 && m < a.M && rm) atomicMax(a.omax_row + m, rm);
         }
     }
-    if (a.omax_row && n < a.N && cmax) atomicMax(a.omax_col + n, cmax);
+    if (a.omax_row) {
+        // column maxima over the block's 16 rows: the 4 row lanes through shared memory
+        __shared__ unsigned sc[4][256];
+#pragma unroll
+        for (int j = 0; j < 4; ++j) sc[ry][4 * c4 + j] = cm[j];
+        __syncthreads();
+        const int col = (int)threadIdx.x;
+        const unsigned v = max(max(sc[0][col], sc[1][col]), max(sc[2][col], sc[3][col]));
+        if (nt * 256 + col < a.N && v) atomicMax(a.omax_col + nt * 256 + col, v);
+    }
 }
 
 }  // namespace lane_b200
@@ -761,7 +787,8 @@ inline void h3_launch(cudaStream_t st, const CUtensorMap& a, const CUtensorMap& 
         k_tc_splitk_reduce<E><<<(unsigned)std::min<size_t>(1184, (n4 + 255) / 256), 256, 0, st>>>(args, S);
     }
     if (PAIR && args.full_units > 0)
-        k_h3_tail_reduce<E><<<dim3((unsigned)(args.tiles_m * args.tiles_n - args.full_units), 8), 256, 0, st>>>(args);
+        k_h3_tail_reduce<E><<<dim3((unsigned)(args.tiles_m * args.tiles_n - args.full_units), 256 / kTailRows), 256, 0,
+                              st>>>(args);
 }
 
 template <TcEpi E, bool PAIR>
