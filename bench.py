@@ -73,11 +73,14 @@ def chain_latency(wl, plan, kernel_ms, n, clk):
     """The batch-1 window kernel's latency roofline: cycles per sample of the
     step (kernel time x the SM clock sampled under load) against the measured
     dependency floor of the per-sample chain (profiles/chain_floor.json,
-    tools/ubench_chain.cu k_chain_floor).  C2's shape only."""
+    tools/ubench_chain.cu: k_chain_floor for C2's one-warp chain,
+    k_chain_floor_cl for the C4 window plans' multi-warp / cluster chains)."""
     path = os.path.join(ROOT, "profiles", "chain_floor.json")
-    if wl != "c2" or not plan.startswith("window") or not os.path.exists(path):
+    if not plan.startswith("window") or not os.path.exists(path):
         return None
-    d = json.load(open(path))[wl]
+    d = json.load(open(path)).get(wl)
+    if not d:
+        return None
     mhz = clk.summary().get("sm_mhz") or 0
     if not mhz:
         return None

@@ -478,63 +478,71 @@ SgdPlan plan_persistent(lane_b200_net* net) {
     const char* mode = std::getenv("LANE_B200_SGD_MODE");
     if (!mode || std::strcmp(mode, "window") == 0) {
         // windowed plan: the chain on one CTA, W0 on H/4 producer CTAs
-        int D = 2;  // measured best at C2 (producers keep up with one block of lag)
-        if (const char* e = std::getenv("LANE_B200_SGD_WIN_D")) D = std::max(2, std::min(std::atoi(e), kWinMaxD));
-        // chain geometry: H <= 128 -> one chain warp x 4 units/lane; <= 256 ->
-        // two warps x 4 (measured at C2: one warp 1.83M samples/s, two 1.68M --
-        // the barrier and the duplicated softmax outweigh the halved H work);
-        // wider -> CS = H/128 chain CTAs in one cluster, one warp each, with a
-        // DSMEM exchange of the slice partial logits per sample
-        int cs = 1;
-        if (H > 256) cs = std::min(kWinMaxCS, next_pow2((H + 127) / 128));
-        const int Hs = H / cs;
-        // one chain warp per 128 units of a cluster slice (1, 2 or 4)
-        int ncw = cs > 1 ? (Hs <= 128 ? 1 : Hs <= 256 ? 2 : Hs <= 512 ? 4 : 8) : (H <= 128 ? 1 : 2);
-        if (const char* e = std::getenv("LANE_B200_SGD_WIN_NCW"))
-            if (cs == 1) ncw = (std::atoi(e) == 1 && H <= 128) ? 1 : 2;
-        const int jpl = ncw == 1 ? 4 : ((cs == 1 && H <= 128) ? 2 : 4);
-        // producers: H/4 column quads (QPC per CTA) x KS row splits (<= 2
-        // splits, >= 32 rows each); rows per split a multiple of 4 (cp.async 16 B)
-        const int quads = std::max(1, H / 4);
-        int pmax = c->sm_count - cs;
-        int ks = std::max(1, std::min({2, pmax / quads, std::max(1, I / 32)}));
-        if (const char* e = std::getenv("LANE_B200_SGD_WIN_KS")) ks = std::max(1, std::min(std::atoi(e), 2));
-        const int rpc = (((I + ks - 1) / ks) + 3) & ~3;
-        ks = (I + rpc - 1) / rpc;
-        // (the d0-direct choice needs the producer variant: wide/smem producers
-        // when the quads per producer exceed 4 -- known after the capacity query;
-        // size the chain CTA for the non-direct ring, the larger of the two)
-        const WinSmem L(32 * jpl * ncw, D, ks, Hs, ncw, cs > 1 && ncw >= 2);
-        const size_t psmem_reg = ProdSmem(rpc, D).total;
-        // producers: register slices up to kWinWideQPC quads, else W0 in smem
-        // (the quad count is only known after the capacity query; size for both)
-        const size_t smem_reg = std::max(L.total, psmem_reg);
-        // co-resident CTAs: one per SM; clusters of cs must also fit the GPCs
-        int max_ctas = c->sm_count;
-        if (cs > 1 && cs <= kWinMaxCS && smem_reg <= c->max_smem_optin)
-            max_ctas = std::min(max_ctas, window_cluster_capacity(cs, smem_reg));
-        pmax = std::max(1, max_ctas - cs);
-        const int qpc = std::max(1, (quads * ks + pmax - 1) / pmax);
-        const int producers = ((quads + qpc - 1) / qpc) * ks;
-        const int grid = ((cs + producers + cs - 1) / cs) * cs;  // a whole number of clusters
-        const bool psm = qpc > kWinWideQPC;  // W0 slices in shared memory
-        const size_t smem = psm ? std::max(L.total, ProdSmemS(rpc, D, qpc).total) : smem_reg;
-        const int nthr = ncw == 4 ? 320 : ncw == 2 ? 256 : 224;
-        if (ncw <= 4 && H % (4 * cs) == 0 && Hs <= 32 * jpl * ncw && cs <= kWinMaxCS && C <= kWinCP &&
-            rpc <= (qpc > kWinMaxQPC ? 2 : kWinMaxNR) * nthr &&
-            qpc <= (cs > 1 ? kWinSmemQPC : 1) && (cs == 1 || ncw == 1 || psm) &&
-            grid <= max_ctas && smem <= c->max_smem_optin) {
-            p.ok = p.window = true;
-            p.jpl = jpl;
-            p.ncw = ncw;
-            p.cs = cs;
-            p.qpc = qpc;
-            p.D = D;
-            p.ks = ks;
-            p.rpc = rpc;
-            p.G = grid;
-            p.smem = smem;
-            return p;
+        // window depth D: 2 measured best at C2 and up to 1024 units (producers
+        // keep up with one block of lag); the 16-CTA cluster chains (H >= 2048)
+        // run 9-15% faster with D = 3 (more lag for the producers' pass), when
+        // the deeper rings fit in shared memory (not at H = 8192)
+        const char* env_d = std::getenv("LANE_B200_SGD_WIN_D");
+        const bool wide = H > 256 && next_pow2((H + 127) / 128) >= kWinMaxCS;
+        for (int D : {wide && !env_d ? 3 : 2, 2}) {
+            if (env_d) D = std::max(2, std::min(std::atoi(env_d), kWinMaxD));
+            // chain geometry: H <= 128 -> one chain warp x 4 units/lane; <= 256 ->
+            // two warps x 4 (measured at C2: one warp 1.83M samples/s, two 1.68M --
+            // the barrier and the duplicated softmax outweigh the halved H work);
+            // wider -> CS = H/128 chain CTAs in one cluster, one warp each, with a
+            // DSMEM exchange of the slice partial logits per sample
+            int cs = 1;
+            if (H > 256) cs = std::min(kWinMaxCS, next_pow2((H + 127) / 128));
+            const int Hs = H / cs;
+            // one chain warp per 128 units of a cluster slice (1, 2 or 4)
+            int ncw = cs > 1 ? (Hs <= 128 ? 1 : Hs <= 256 ? 2 : Hs <= 512 ? 4 : 8) : (H <= 128 ? 1 : 2);
+            if (const char* e = std::getenv("LANE_B200_SGD_WIN_NCW"))
+                if (cs == 1) ncw = (std::atoi(e) == 1 && H <= 128) ? 1 : 2;
+            const int jpl = ncw == 1 ? 4 : ((cs == 1 && H <= 128) ? 2 : 4);
+            // producers: H/4 column quads (QPC per CTA) x KS row splits (<= 2
+            // splits, >= 32 rows each); rows per split a multiple of 4 (cp.async 16 B)
+            const int quads = std::max(1, H / 4);
+            int pmax = c->sm_count - cs;
+            int ks = std::max(1, std::min({2, pmax / quads, std::max(1, I / 32)}));
+            if (const char* e = std::getenv("LANE_B200_SGD_WIN_KS")) ks = std::max(1, std::min(std::atoi(e), 2));
+            const int rpc = (((I + ks - 1) / ks) + 3) & ~3;
+            ks = (I + rpc - 1) / rpc;
+            // (the d0-direct choice needs the producer variant: wide/smem producers
+            // when the quads per producer exceed 4 -- known after the capacity query;
+            // size the chain CTA for the non-direct ring, the larger of the two)
+            const WinSmem L(32 * jpl * ncw, D, ks, Hs, ncw, cs > 1 && ncw >= 2);
+            const size_t psmem_reg = ProdSmem(rpc, D).total;
+            // producers: register slices up to kWinWideQPC quads, else W0 in smem
+            // (the quad count is only known after the capacity query; size for both)
+            const size_t smem_reg = std::max(L.total, psmem_reg);
+            // co-resident CTAs: one per SM; clusters of cs must also fit the GPCs
+            int max_ctas = c->sm_count;
+            if (cs > 1 && cs <= kWinMaxCS && smem_reg <= c->max_smem_optin)
+                max_ctas = std::min(max_ctas, window_cluster_capacity(cs, smem_reg));
+            pmax = std::max(1, max_ctas - cs);
+            const int qpc = std::max(1, (quads * ks + pmax - 1) / pmax);
+            const int producers = ((quads + qpc - 1) / qpc) * ks;
+            const int grid = ((cs + producers + cs - 1) / cs) * cs;  // a whole number of clusters
+            const bool psm = qpc > kWinWideQPC;  // W0 slices in shared memory
+            const size_t smem = psm ? std::max(L.total, ProdSmemS(rpc, D, qpc).total) : smem_reg;
+            const int nthr = ncw == 4 ? 320 : ncw == 2 ? 256 : 224;
+            if (ncw <= 4 && H % (4 * cs) == 0 && Hs <= 32 * jpl * ncw && cs <= kWinMaxCS && C <= kWinCP &&
+                rpc <= (qpc > kWinMaxQPC ? 2 : kWinMaxNR) * nthr &&
+                qpc <= (cs > 1 ? kWinSmemQPC : 1) && (cs == 1 || ncw == 1 || psm) &&
+                grid <= max_ctas && smem <= c->max_smem_optin) {
+                p.ok = p.window = true;
+                p.jpl = jpl;
+                p.ncw = ncw;
+                p.cs = cs;
+                p.qpc = qpc;
+                p.D = D;
+                p.ks = ks;
+                p.rpc = rpc;
+                p.G = grid;
+                p.smem = smem;
+                return p;
+            }
+            if (env_d) break;
         }
         if (mode) return p;
     }

@@ -343,6 +343,7 @@ def test_sgd_stream_fast_vs_oracle(lane, fast, monkeypatch, mode, F, H, C, n, st
     (340, [1024], 10, 32, 60, 1e-3, 2),     # 8 chain CTAs, 2 column quads per producer
     (340, [2048], 10, 32, 45, 1e-3, 3),     # 16 chain CTAs (non-portable cluster), 4 quads per producer
     (340, [4096], 10, 32, 40, 1e-3, 2),     # 16 chain CTAs x 2 warps, W0 slices in producer smem
+    (340, [4096], 10, 32, 50, 1e-3, 3),     # the same at the default lag of the 16-CTA chains
     (340, [8192], 10, 32, 40, 1e-3, 2),     # 16 chain CTAs x 4 warps, d0 straight to L2, 19 quads/producer
     (64, [384], 7, 16, 50, 0.02, 2),        # 4 chain CTAs x 96 units (partial slices)
     (784, [128], 10, 64, 150, 0.01, -2),    # two chain warps (2 units/lane) instead of one
@@ -576,6 +577,14 @@ def test_sgd_plan_selection(lane, fast, F, H, C, want):
     # the fused plan the headline shapes run (no silent fallback to layer kernels)
     net = lane.build_network(F, H, C, seed=42, device=fast)
     assert net.sgd_plan().split()[0] == want, net.sgd_plan()
+
+
+@pytest.mark.parametrize("H,D", [(128, 2), (1024, 2), (2048, 3), (4096, 3), (8192, 2)])
+def test_sgd_window_default_lag(lane, fast, monkeypatch, H, D):
+    # the 16-CTA cluster chains take lag 3 where its rings fit (not at 8192)
+    monkeypatch.delenv("LANE_B200_SGD_WIN_D", raising=False)
+    net = lane.build_network(784 if H == 128 else 340, [H], 10, seed=42, device=fast)
+    assert f" D={D} " in net.sgd_plan(), net.sgd_plan()
 
 
 def test_sgd_window_long_stream_chunks(lane, fast, monkeypatch):

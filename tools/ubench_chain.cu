@@ -3,6 +3,8 @@
 // Each test runs a dependent chain of N steps in one warp and prints cycles/step.
 #include <cstdio>
 #include <cuda_runtime.h>
+#include <algorithm>
+#include <cstdint>
 
 constexpr int N = 4096;
 
@@ -186,6 +188,177 @@ __global__ void k_chain_floor(float* out, long long* cyc, float seed, int n) {
     if (lane == 0) cyc[15] = t1 - t0;
 }
 
+// The same critical path for the wide window plans (C4, H = NCW x CS x 128):
+// NCW chain warps per CTA (each 128 hidden units, 4 per lane) and CS chain
+// CTAs in one thread-block cluster.  Per sample, on top of the one-warp chain:
+//   NCW > 1: per-warp class half sums -> shared memory, one named barrier,
+//            every warp sums the NCW halves;
+//   CS > 1:  chain warp 0 pushes the C slice partials to every peer with
+//            st.async (completing the peer's exchange mbarrier), every warp
+//            waits for all CS and sums them in rank order; the pusher re-arms
+//            the barrier for sample s + 2 -- the window kernel's exchange.
+template <int NCW, int CS>
+__global__ void k_chain_floor_cl(float* out, long long* cyc, float seed, int n) {
+    constexpr int C = 10, CC = 10, XS = 32 * NCW + 4, CP = 16;
+    __shared__ __align__(16) float xr[16 * XS];
+    __shared__ __align__(16) float half[2][NCW][CP];
+    __shared__ __align__(16) float es[NCW][16];
+    __shared__ __align__(16) float gat[2][16][CP];
+    __shared__ __align__(8) unsigned long long xbar[2];
+    const int lane = threadIdx.x & 31, cw = threadIdx.x >> 5;
+    unsigned rank = 0;
+    if (CS > 1) asm volatile("mov.u32 %0, %%cluster_ctarank;\n" : "=r"(rank));
+    const bool kval = lane < C;
+    const int kr = lane & 15;
+    float w1[4][CC], y[4], b0r[4], dp1[4], t[CC];
+    for (int m = 0; m < 4; ++m) {
+        for (int k = 0; k < CC; ++k)
+            w1[m][k] = seed * 0.01f * (float)(((cw * 32 + lane) * 4 + m) * 7 + k * 3 - 40) / 64.0f;
+        y[m] = seed * 0.1f * (lane - 16) / 16.0f;
+        b0r[m] = 0.01f * m;
+        dp1[m] = 0.0f;
+    }
+    for (int k = 0; k < CC; ++k) t[k] = k == 3 ? 1.0f : 0.0f;
+    for (int e = threadIdx.x; e < 16 * XS; e += 32 * NCW) xr[e] = 0.0f;
+    const uint32_t xb0 = (uint32_t)__cvta_generic_to_shared(&xbar[0]);
+    if (threadIdx.x == 0) {
+        for (int p = 0; p < 2; ++p) {
+            asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;\n" ::"r"(xb0 + 8 * p));
+        }
+        asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
+        for (int p = 0; p < 2 && p < n; ++p)
+            asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;\n" ::"r"(xb0 + 8 * p),
+                         "r"(CS * C * 4));
+    }
+    if (CS > 1)
+        asm volatile("barrier.cluster.arrive.release.aligned;\nbarrier.cluster.wait.acquire.aligned;\n" ::: "memory");
+    else
+        __syncthreads();
+    const float c1 = -0.01f * seed, b1k = 0.0f;
+    long long t0 = clock64();
+    for (int i = 0; i < n; ++i) {
+        float a[4];
+#pragma unroll
+        for (int m = 0; m < 4; ++m) a[m] = tanhf(fmaf(c1, dp1[m], y[m]) + b0r[m]);
+#pragma unroll
+        for (int k = 0; k < CC; ++k) {
+            float acc = 0.0f;
+#pragma unroll
+            for (int m = 0; m < 4; ++m) acc = fmaf(a[m], w1[m][k], acc);
+            xr[k * XS + cw * 32 + lane] = acc;
+        }
+        __syncwarp();
+        const float4* col = reinterpret_cast<const float4*>(xr + kr * XS + cw * 32);
+        float4 v[8];
+#pragma unroll
+        for (int q = 0; q < 8; ++q) v[q] = col[q];
+        float t8[8];
+#pragma unroll
+        for (int q = 0; q < 8; ++q) t8[q] = (v[q].x + v[q].y) + (v[q].z + v[q].w);
+        float hs = ((t8[0] + t8[1]) + (t8[2] + t8[3])) + ((t8[4] + t8[5]) + (t8[6] + t8[7]));
+        if (NCW > 1) {
+            if (kval) half[i & 1][cw][lane] = hs;
+            asm volatile("bar.sync 1, %0;\n" ::"r"(32 * NCW) : "memory");
+            float hsum = half[i & 1][0][kr];
+#pragma unroll
+            for (int c = 1; c < NCW; ++c) hsum += half[i & 1][c][kr];
+            hs = hsum;
+        }
+        if (CS > 1) {
+            const int par = i & 1;
+            const uint32_t slot = (uint32_t)__cvta_generic_to_shared(&gat[par][rank][lane]);
+            const uint32_t xb = xb0 + 8 * par;
+            if (cw == 0 && kval)
+                for (int p = 0; p < CS; ++p) {
+                    uint32_t ra, rb;
+                    asm volatile("mapa.shared::cluster.u32 %0, %1, %2;\n" : "=r"(ra) : "r"(slot), "r"(p));
+                    asm volatile("mapa.shared::cluster.u32 %0, %1, %2;\n" : "=r"(rb) : "r"(xb), "r"(p));
+                    asm volatile("st.async.shared::cluster.mbarrier::complete_tx::bytes.b32 [%0], %1, [%2];\n" ::"r"(
+                                     ra),
+                                 "r"(__float_as_uint(hs)), "r"(rb)
+                                 : "memory");
+                }
+            asm volatile(
+                "{\n .reg .pred p;\nW_%=:\n mbarrier.try_wait.parity.acquire.cluster.shared::cta.b64 p, [%0], %1;\n"
+                " @!p bra W_%=;\n}\n" ::"r"(xb),
+                "r"((uint32_t)((i >> 1) & 1))
+                : "memory");
+            if (cw == 0 && lane == 0 && i + 2 < n)
+                asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;\n" ::"r"(xb), "r"(CS * C * 4));
+            float tot = gat[par][0][kr];
+#pragma unroll
+            for (int p = 1; p < CS; ++p) tot += gat[par][p][kr];
+            hs = tot;
+        }
+        const float zown = hs + b1k;
+        float mx;
+        asm volatile("redux.sync.max.f32 %0, %1, 0xffffffff;\n" : "=f"(mx) : "f"(kval ? zown : -INFINITY));
+        const float eown = expf(zown - mx);
+        if (kval) es[cw][lane] = eown;
+        __syncwarp();
+        float ek[12];
+#pragma unroll
+        for (int k4 = 0; k4 < 3; ++k4) {
+            const float4 q = reinterpret_cast<const float4*>(es[cw])[k4];
+            ek[4 * k4] = q.x; ek[4 * k4 + 1] = q.y; ek[4 * k4 + 2] = q.z; ek[4 * k4 + 3] = q.w;
+        }
+        ek[10] = ek[11] = 0.0f;
+        float sp[12];
+#pragma unroll
+        for (int k = 0; k < 12; ++k) sp[k] = ek[k];
+#pragma unroll
+        for (int w = 1; w < 12; w <<= 1)
+#pragma unroll
+            for (int k = 0; k + w < 12; k += 2 * w) sp[k] += sp[k + w];
+        float inv;
+        asm volatile("rcp.approx.ftz.f32 %0, %1;\n" : "=f"(inv) : "f"(sp[0]));
+        float d1[CC];
+#pragma unroll
+        for (int k = 0; k < CC; ++k) d1[k] = fmaf(ek[k], inv, -t[k]);
+#pragma unroll
+        for (int m = 0; m < 4; ++m) {
+            float acc0 = 0.0f, acc1 = 0.0f;
+#pragma unroll
+            for (int k = 0; k < CC / 2; ++k) acc0 = fmaf(d1[k], w1[m][k], acc0);
+#pragma unroll
+            for (int k = CC / 2; k < CC; ++k) acc1 = fmaf(d1[k], w1[m][k], acc1);
+            dp1[m] = fmaf(-a[m], a[m], 1.0f) * (acc0 + acc1);
+        }
+        __syncwarp();
+    }
+    long long t1 = clock64();
+    out[threadIdx.x] = dp1[0] + dp1[1] + dp1[2] + dp1[3];
+    if (threadIdx.x == 0 && rank == 0) cyc[0] = t1 - t0;
+    if (CS > 1)
+        asm volatile("barrier.cluster.arrive.release.aligned;\nbarrier.cluster.wait.acquire.aligned;\n" ::: "memory");
+}
+
+template <int NCW, int CS>
+double run_cl(float* out, long long* cyc) {
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3(CS);
+    cfg.blockDim = dim3(32 * NCW);
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeClusterDimension;
+    attr[0].val.clusterDim.x = CS;
+    attr[0].val.clusterDim.y = 1;
+    attr[0].val.clusterDim.z = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    if (CS > 8) cudaFuncSetAttribute(k_chain_floor_cl<NCW, CS>, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
+    double best = 1e30;
+    for (int rep = 0; rep < 3; ++rep) {
+        cudaError_t e = cudaLaunchKernelEx(&cfg, k_chain_floor_cl<NCW, CS>, out, cyc, 0.3f, N);
+        if (e != cudaSuccess) {
+            printf("launch NCW=%d CS=%d: %s\n", NCW, CS, cudaGetErrorString(e));
+            return -1;
+        }
+        cudaDeviceSynchronize();
+        best = std::min(best, (double)cyc[0] / N);
+    }
+    return best;
+}
+
 int main() {
     float* out;
     long long* cyc;
@@ -216,6 +389,14 @@ int main() {
         cudaDeviceSynchronize();
     }
     printf("%-20s %7.1f cycles/step\n", "c2 chain floor", (double)cyc[15] / N);
-    printf("{\"c2_chain_floor_cycles\": %.1f}\n", (double)cyc[15] / N);
+    const double c2 = (double)cyc[15] / N;
+    // the wide window plans of C4 (340-H-10): H -> (chain warps per CTA, cluster CTAs)
+    const double h256 = run_cl<2, 1>(out, cyc), h512 = run_cl<1, 4>(out, cyc), h1024 = run_cl<1, 8>(out, cyc);
+    const double h2048 = run_cl<1, 16>(out, cyc), h4096 = run_cl<2, 16>(out, cyc), h8192 = run_cl<4, 16>(out, cyc);
+    printf("c4 floors: 256 %.1f 512 %.1f 1024 %.1f 2048 %.1f 4096 %.1f 8192 %.1f cycles/sample\n", h256, h512, h1024,
+           h2048, h4096, h8192);
+    printf("{\"c2_chain_floor_cycles\": %.1f, \"c4-256\": %.1f, \"c4-512\": %.1f, \"c4-1024\": %.1f, "
+           "\"c4-2048\": %.1f, \"c4-4096\": %.1f, \"c4-8192\": %.1f}\n",
+           c2, h256, h512, h1024, h2048, h4096, h8192);
     return 0;
 }
