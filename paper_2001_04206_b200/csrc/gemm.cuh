@@ -478,6 +478,56 @@ __global__ void __launch_bounds__(256) k_gemm_skinny_nn_kc(int M, int N, int K, 
     }
 }
 
+// Skinny NN, row per lane (M >= 2048, N <= 16, K % 4 == 0, 16-byte rows): the
+// output layer's forward at C5 (4096 x 10 x 4096).  Block (256 rows, K chunk
+// of kSrKC): lane = one row of A, which it streams as float4 along K -- the
+// other half of each 32-byte sector is the next iteration's, an L1 hit -- and
+// every B value is a broadcast shared-memory read (the whole warp reads the
+// same k), so a k costs N / 4 broadcast LDS.128 for 32 x N FMAs and no
+// cross-lane reduction.  The partials of the K chunks are summed in a fixed
+// order with the epilogue (k_sum_partials_epi).  The lanes-along-K kernel
+// above pays N conflicted LDS per k and lane: 68 us at C5 against 47 us here
+// (the 64 MB read of A alone would take ~10 us; the 32-row loads are L1-
+// wavefront bound).
+constexpr int kSrKC = 128;
+__global__ void __launch_bounds__(256) k_gemm_skinny_nn_rows(int M, int N, int K, const float* __restrict__ A,
+                                                             const float* __restrict__ B, float* __restrict__ part) {
+    __shared__ __align__(16) float bs[kSrKC * 16];  // [k][16], zero past N
+    const int k0 = blockIdx.y * kSrKC, kn = min(K - k0, kSrKC);
+    for (int e = threadIdx.x; e < kSrKC * 16; e += blockDim.x) {
+        const int k = e >> 4, n = e & 15;
+        bs[e] = (k < kn && n < N) ? __ldg(B + (size_t)(k0 + k) * N + n) : 0.0f;
+    }
+    __syncthreads();
+    const int m = blockIdx.x * 256 + threadIdx.x;
+    if (m >= M) return;
+    const float4* arow = reinterpret_cast<const float4*>(A + (size_t)m * K + k0);
+    const float4* b4 = reinterpret_cast<const float4*>(bs);
+    float acc[16];
+#pragma unroll
+    for (int n = 0; n < 16; ++n) acc[n] = 0.0f;
+#pragma unroll 8
+    for (int q = 0; q < kn / 4; ++q) {
+        const float4 a = __ldg(arow + q);
+        const float av[4] = {a.x, a.y, a.z, a.w};
+#pragma unroll
+        for (int j = 0; j < 4; ++j) {
+#pragma unroll
+            for (int c = 0; c < 4; ++c) {
+                const float4 b = b4[(4 * q + j) * 4 + c];
+                acc[4 * c + 0] = fmaf(av[j], b.x, acc[4 * c + 0]);
+                acc[4 * c + 1] = fmaf(av[j], b.y, acc[4 * c + 1]);
+                acc[4 * c + 2] = fmaf(av[j], b.z, acc[4 * c + 2]);
+                acc[4 * c + 3] = fmaf(av[j], b.w, acc[4 * c + 3]);
+            }
+        }
+    }
+    float* out = part + ((size_t)blockIdx.y * M + m) * N;
+#pragma unroll
+    for (int n = 0; n < 16; ++n)
+        if (n < N) out[n] = acc[n];
+}
+
 // out = epilogue(sum_{s < S} part[s]) in a fixed order; bias per column
 template <Epi E>
 __global__ void k_sum_partials_epi(const float* __restrict__ part, int S, int M, int N, float* __restrict__ C,
@@ -604,6 +654,22 @@ inline bool gemm_try_skinny(GemmCtx& g, GemmOp op, int M, int N, int K, const fl
         return true;
     }
     if (N > 32) return false;
+    if (op == GemmOp::NN && lda == K && ldb == N && e != Epi::TANH_GRAD && N <= 16 && K >= 2 * kSkKC &&
+        M >= 2048 && K % 4 == 0 && (reinterpret_cast<uintptr_t>(A) & 15) == 0) {
+        // enough rows for >= 8 row blocks x the K chunks (C3's 256 rows stay on
+        // the lanes-along-K kernel below: 7 us there against 13 us here)
+        const int S = (K + kSrKC - 1) / kSrKC;
+        ensure_ws(g, (size_t)S * M * N);
+        k_gemm_skinny_nn_rows<<<dim3((M + 255) / 256, S), 256, 0, g.stream>>>(M, N, K, A, B, *g.ws);
+        const int blocks = std::max(1, std::min(4 * g.sm_count, (M * N + 255) / 256));
+        switch (e) {
+            case Epi::STORE: k_sum_partials_epi<Epi::STORE><<<blocks, 256, 0, g.stream>>>(*g.ws, S, M, N, C, C2, bias); break;
+            case Epi::BIAS: k_sum_partials_epi<Epi::BIAS><<<blocks, 256, 0, g.stream>>>(*g.ws, S, M, N, C, C2, bias); break;
+            default: k_sum_partials_epi<Epi::BIAS_TANH><<<blocks, 256, 0, g.stream>>>(*g.ws, S, M, N, C, C2, bias); break;
+        }
+        *g.launches += 2;
+        return true;
+    }
     if (op == GemmOp::NN && lda == K && ldb == N && e != Epi::TANH_GRAD && N <= 16 && K >= 2 * kSkKC) {
         // long K: chunked, B chunk in shared memory, fixed-order partial sum
         const int S = (K + kSkKC - 1) / kSkKC;

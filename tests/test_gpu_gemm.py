@@ -123,10 +123,25 @@ def test_shortk_nt_output_layer_dgrad(dev, epi):
     assert np.all(np.abs(out - g * ref) <= 1e-5 * g * cond + 1e-30)
 
 
+@pytest.mark.parametrize("M,N,K", [(4096, 10, 4096), (1024, 16, 1000), (520, 3, 2049), (4100, 10, 700),
+                                   (256, 10, 4096)])
+def test_skinny_tn_long_k(dev, M, N, K):
+    # op(A)^T B with N <= 16 and a long K: the output layer's wgrad
+    rs = np.random.default_rng(13)
+    A, B, Am, Bm = operands(TN, M, N, K, rs)
+    out, _, launched = run(dev, TN, M, N, K, A, B, STORE)
+    ref = Am @ Bm
+    cond = np.abs(Am) @ np.abs(Bm)
+    assert launched == 2
+    assert np.all(np.abs(out - ref) <= 1e-5 * cond + 1e-30)
+
+
 @pytest.mark.parametrize("epi", [STORE, BIAS, BIAS_TANH])
-def test_skinny_nn_long_k(dev, epi):
+@pytest.mark.parametrize("M,N,K", [(256, 10, 4096 + 96), (4096, 10, 4096), (2100, 16, 2048), (3000, 3, 1100),
+                                   (256, 10, 2050)])
+def test_skinny_nn_long_k(dev, epi, M, N, K):
     # A[M][K] B[K][N<=16] with a long K: chunked, fixed-order partial sums
-    M, N, K = 256, 10, 4096 + 96
+    # (row per lane for M >= 2048 and K % 4 == 0, incl. C5's output layer; lanes along K otherwise)
     rs = np.random.default_rng(12)
     A, B, Am, Bm = operands(NN, M, N, K, rs)
     A *= 0.05
