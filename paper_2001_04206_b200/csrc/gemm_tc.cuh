@@ -556,7 +556,8 @@ inline PFN_encodeTiled tc_encoder() {
 
 // 2-D fp32 row-major tensor [rows x cols] (ld = cols), box {box_inner, box_rows};
 // swizzle: 0 = 128B (K-major MMA operand), 1 = 128B with 32-byte atoms (the
-// MN-major tf32 MMA operand), 2 = none (read by the split warps only)
+// MN-major tf32 MMA operand), 2 = none (read by the split warps only), 3 = 64B
+// (the update epilogue's 16-column W / V chunks)
 inline CUtensorMap tc_map(const float* base, int rows, int cols, int box_inner, int box_rows, int swizzle) {
     CUtensorMap m;
     const cuuint64_t dims[2] = {(cuuint64_t)cols, (cuuint64_t)rows};
@@ -567,6 +568,7 @@ inline CUtensorMap tc_map(const float* base, int rows, int cols, int box_inner, 
                                     box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
                                     swizzle == 1   ? CU_TENSOR_MAP_SWIZZLE_128B_ATOM_32B
                                     : swizzle == 2 ? CU_TENSOR_MAP_SWIZZLE_NONE
+                                    : swizzle == 3 ? CU_TENSOR_MAP_SWIZZLE_64B
                                                    : CU_TENSOR_MAP_SWIZZLE_128B,
                                     CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
     if (r != CUDA_SUCCESS) throw Error(LANE_ERR_CUDA, "cuTensorMapEncodeTiled failed");

@@ -42,16 +42,19 @@ constexpr int kTpBTile = kTcBN * kTcBK * 4;           // 128 x 32 fp32
 constexpr int kTpStage = kTcTile + 2 * kTpBTile;      // A, B, B_lo
 constexpr int kTpAcc = 2;                             // TMEM accumulators
 constexpr int kTpTileElems = kTcBM * kTcBN;
-constexpr int kTpUpdChunk = kTcBM * 32 * 4;  // one 128 x 32 fp32 chunk of W or V (SW128)
+constexpr int kTpUpdCols = 16;                        // columns per W / V chunk
+constexpr int kTpUpdChunk = kTcBM * kTpUpdCols * 4;   // one 128 x 16 fp32 chunk of W or V (64B swizzle)
 
-// UPDATE keeps 4 W/V chunk slots with loads 3 chunks ahead (2 MMA stages):
-// the update epilogue streams W and V from HBM and is latency-bound with
-// fewer chunks in flight (C3's wgrad + update, DRAM at 37% of peak with 2)
-constexpr int kTpUpdSlots = 4;
+// UPDATE: the epilogue streams W and V through 5 chunk slots with loads 4
+// chunks ahead (64 KB in flight), and the ring keeps 3 MMA stages.  (The first
+// version used 128 x 32 chunks: 4 slots left room for 2 ring stages only, and
+// the K-block ring -- TMA latency + split + MMA per stage -- bound the kernel:
+// 93 us for C3's 4096 x 4096 x 256 wgrad + update.)
+constexpr int kTpUpdSlots = 5;
 template <int E>
 struct TpCfg {
     static constexpr bool kUpd = E == 4;                    // TpEpi::UPDATE
-    static constexpr int kStages = kUpd ? 2 : kTpStages;
+    static constexpr int kStages = kUpd ? 3 : kTpStages;
     static constexpr size_t kRing = (size_t)kStages * kTpStage;
     static constexpr size_t kEpi = kUpd ? kTpUpdSlots * 2 * kTpUpdChunk : 0;  // slots x (W, V)
     static constexpr size_t kSmem = kRing + kEpi + 1024 + 512;
@@ -418,12 +421,12 @@ __global__ void __launch_bounds__(kTpThreads, 1)
         if constexpr (Cfg::kUpd) {
             if (!args.sk) {
                 // wgrad + update, whole tiles: the leader TMA-loads the W and V
-                // chunks (128 rows x 32 columns, 128B swizzle) three chunks ahead
+                // chunks (128 rows x 16 columns, 64B swizzle) four chunks ahead
                 // -- across unit boundaries, i.e. during the next tile's MMAs --
-                // into four slots; every thread updates its row of the chunk in
+                // into five slots; every thread updates its row of the chunk in
                 // shared memory, G goes straight to global, and the leader
                 // TMA-stores the W and V chunks back.
-                constexpr int kChunks = kTcBN / 32;
+                constexpr int kChunks = kTcBN / kTpUpdCols;
                 const uint32_t vbytes = args.mu == 0.0f ? 0u : (uint32_t)kTpUpdChunk;
                 long long lit = 0;  // the loads' own cursor over units / chunks
                 TpUnit lu;
@@ -436,8 +439,9 @@ __global__ void __launch_bounds__(kTpThreads, 1)
                     const int k = lissued % kTpUpdSlots;
                     const uint32_t wdst = tc_smem(epi_buf + (size_t)(2 * k) * kTpUpdChunk);
                     tc_mbar_expect_tx(epi_full(k), (uint32_t)kTpUpdChunk + vbytes);
-                    tc_tma_2d(&tmW, epi_full(k), wdst, nt * kTcBN + 32 * lchunk, mt * kTcBM);
-                    if (vbytes) tc_tma_2d(&tmV, epi_full(k), wdst + kTpUpdChunk, nt * kTcBN + 32 * lchunk, mt * kTcBM);
+                    tc_tma_2d(&tmW, epi_full(k), wdst, nt * kTcBN + kTpUpdCols * lchunk, mt * kTcBM);
+                    if (vbytes)
+                        tc_tma_2d(&tmV, epi_full(k), wdst + kTpUpdChunk, nt * kTcBN + kTpUpdCols * lchunk, mt * kTcBM);
                     ++lissued;
                     if (++lchunk == kChunks) {
                         lchunk = 0;
@@ -457,8 +461,8 @@ __global__ void __launch_bounds__(kTpThreads, 1)
                     const uint32_t tacc = tmem + ((uint32_t)(quarter * 32) << 16) + (uint32_t)(b * kTcBN);
 #pragma unroll 1
                     for (int c = 0; c < kChunks; ++c, ++gc) {
-                        float v[32];
-                        tp_ld32(tacc + (uint32_t)(32 * c), v);
+                        float v[kTpUpdCols];
+                        tp_ld16(tacc + (uint32_t)(kTpUpdCols * c), v);
                         if (c == kChunks - 1) {
                             asm volatile("tcgen05.fence::before_thread_sync;\n" ::: "memory");
                             __syncwarp();
@@ -466,12 +470,12 @@ __global__ void __launch_bounds__(kTpThreads, 1)
                         }
                         const int k = gc % kTpUpdSlots;
                         tc_mbar_wait(epi_full(k), (uint32_t)((gc / kTpUpdSlots) & 1));
-                        uint8_t* wrow = epi_buf + (size_t)(2 * k) * kTpUpdChunk + row * 128;
+                        uint8_t* wrow = epi_buf + (size_t)(2 * k) * kTpUpdChunk + row * (4 * kTpUpdCols);
                         uint8_t* vrow = wrow + kTpUpdChunk;
-                        const bool full_cols = n0 + 32 * c + 32 <= args.N && (args.N & 3) == 0;
+                        const bool full_cols = n0 + kTpUpdCols * c + kTpUpdCols <= args.N && (args.N & 3) == 0;
 #pragma unroll
-                        for (int q = 0; q < 8; ++q) {
-                            const int off = ((q ^ (row & 7)) * 16);  // 128B swizzle: chunk q of row r
+                        for (int q = 0; q < kTpUpdCols / 4; ++q) {
+                            const int off = ((q ^ ((row >> 1) & 3)) * 16);  // 64B swizzle: 16-byte unit q of row r
                             float4 w = *reinterpret_cast<const float4*>(wrow + off);
                             float4 vv = args.mu == 0.0f ? make_float4(0.f, 0.f, 0.f, 0.f)
                                                         : *reinterpret_cast<const float4*>(vrow + off);
@@ -489,7 +493,7 @@ __global__ void __launch_bounds__(kTpThreads, 1)
                             }
                             *reinterpret_cast<float4*>(wrow + off) = w;
                             *reinterpret_cast<float4*>(vrow + off) = vv;
-                            const int n = n0 + 32 * c + 4 * q;
+                            const int n = n0 + kTpUpdCols * c + 4 * q;
                             if (m < args.M) {
                                 if (full_cols) {
                                     __stcs(reinterpret_cast<float4*>(args.C + (size_t)m * args.N + n), x);
@@ -504,8 +508,8 @@ __global__ void __launch_bounds__(kTpThreads, 1)
                         tp_epi_bar();
                         if (leader) {
                             const uint32_t wsrc = tc_smem(epi_buf + (size_t)(2 * k) * kTpUpdChunk);
-                            tp_tma_store_2d(&tmW, wsrc, n0 + 32 * c, mt * kTcBM);
-                            tp_tma_store_2d(&tmV, wsrc + kTpUpdChunk, n0 + 32 * c, mt * kTcBM);
+                            tp_tma_store_2d(&tmW, wsrc, n0 + kTpUpdCols * c, mt * kTcBM);
+                            tp_tma_store_2d(&tmV, wsrc + kTpUpdChunk, n0 + kTpUpdCols * c, mt * kTcBM);
                             asm volatile("cp.async.bulk.commit_group;\n" ::: "memory");
                             // the next load refills the previous chunk's slot, once
                             // that chunk's stores have read it (this chunk's may
@@ -679,10 +683,10 @@ inline void tp_launch(cudaStream_t st, const CUtensorMap& ma, const CUtensorMap&
                                        (int)smem));
         configured.fetch_or(bit, std::memory_order_release);
     }
-    // UPDATE: W and V as [M rows x N cols] boxes of 128 rows x 32 columns
-    // (128B swizzle) for the epilogue's TMA loads and stores
-    const CUtensorMap mw = E == TpEpi::UPDATE ? tc_map(p.a.W, p.a.M, p.a.N, 32, kTcBM, 0) : ma;
-    const CUtensorMap mv = E == TpEpi::UPDATE ? tc_map(p.a.V, p.a.M, p.a.N, 32, kTcBM, 0) : ma;
+    // UPDATE: W and V as [M rows x N cols] boxes of 128 rows x 16 columns
+    // (64B swizzle) for the epilogue's TMA loads and stores
+    const CUtensorMap mw = E == TpEpi::UPDATE ? tc_map(p.a.W, p.a.M, p.a.N, kTpUpdCols, kTcBM, 3) : ma;
+    const CUtensorMap mv = E == TpEpi::UPDATE ? tc_map(p.a.V, p.a.M, p.a.N, kTpUpdCols, kTcBM, 3) : ma;
     k_gemm_tcp<A_MN, B_MN, E><<<p.grid, kTpThreads, smem, st>>>(ma, mb, mw, mv, p.a);
 }
 
