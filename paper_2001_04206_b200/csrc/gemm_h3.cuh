@@ -628,14 +628,18 @@ __global__ void __launch_bounds__(256) k_absmax_cols(const float* __restrict__ X
 // max |x| of every row AND every column of a row-major R x C matrix in one
 // pass (both zeroed beforehand): thread = 4 columns x kAbsmaxRows rows, rows
 // loaded 8 at a time (memory-level parallelism); a row's partial over the
-// warp's 128 columns is one redux + one atomicMax
+// warp's 128 columns is one redux, the block's 8 warps meet in shared memory
+// and one atomicMax per row and block goes out (8x fewer same-address
+// atomics than one per warp; C5: 167 -> 159 us per step for 10 matrices)
 __global__ void __launch_bounds__(256) k_absmax_rc(const float* __restrict__ X, int R, int C, unsigned* rows,
                                                    unsigned* cols) {
+    __shared__ unsigned rmax[8][kAbsmaxRows];
     const int c4 = blockIdx.x * blockDim.x + threadIdx.x;
+    const int warp = threadIdx.x >> 5;
     const bool on = 4 * c4 < C;
     const int r0 = blockIdx.y * kAbsmaxRows, r1 = min(R, r0 + kAbsmaxRows);
     unsigned m0 = 0, m1 = 0, m2 = 0, m3 = 0;
-    for (int rb = r0; rb < r1; rb += 8) {
+    for (int rb = r0; rb < r0 + kAbsmaxRows; rb += 8) {
         float4 v[8];
 #pragma unroll
         for (int j = 0; j < 8; ++j)
@@ -650,8 +654,15 @@ __global__ void __launch_bounds__(256) k_absmax_rc(const float* __restrict__ X, 
             m2 = max(m2, c);
             m3 = max(m3, d);
             const unsigned rm = __reduce_max_sync(0xffffffffu, max(max(a, b), max(c, d)));
-            if ((threadIdx.x & 31) == j && rb + j < r1 && rm) atomicMax(rows + rb + j, rm);
+            if ((threadIdx.x & 31) == j) rmax[warp][rb + j - r0] = rm;
         }
+    }
+    __syncthreads();
+    if (threadIdx.x < kAbsmaxRows && r0 + (int)threadIdx.x < r1) {
+        unsigned rm = rmax[0][threadIdx.x];
+#pragma unroll
+        for (int w = 1; w < 8; ++w) rm = max(rm, rmax[w][threadIdx.x]);
+        if (rm) atomicMax(rows + r0 + threadIdx.x, rm);
     }
     if (on) {
         atomicMax(cols + 4 * c4 + 0, m0);
