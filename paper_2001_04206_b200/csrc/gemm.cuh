@@ -47,6 +47,7 @@ struct GemmMax {
     const unsigned* b = nullptr;
     unsigned* orow = nullptr;
     unsigned* ocol = nullptr;
+    float out_scale = 0.0f;  // STORE on the 3xF16 kernel: C = sum * out_scale (0: none)
 };
 
 inline void ensure_ws(GemmCtx& g, size_t count) {
@@ -872,6 +873,7 @@ inline void gemm_h3(GemmCtx& g, GemmOp op, int M, int N, int K, const float* A, 
     }
     static const int diag = std::getenv("LANE_B200_H3_DIAG") ? std::atoi(std::getenv("LANE_B200_H3_DIAG")) : 0;
     t.diag = diag;
+    if (mx && e == Epi::STORE) t.out_scale = mx->out_scale;
     *g.launches += S > 1 ? 1 : 0;
     // the epilogue's TMA store boxes: 32 columns x 32 rows, 128-byte swizzle
     const CUtensorMap mc = tc_map(C, M, N, 32, 32, 0);
@@ -1054,6 +1056,8 @@ inline void gemm(GemmCtx& g, GemmOp op, int M, int N, int K, const float* A, int
                  Epi e, float* C, float* C2, const float* bias, const float* aux, const GemmMax* mx = nullptr) {
     if (M <= 0 || N <= 0) return;
     bool fused = false;
+    if (mx && mx->out_scale != 0.0f && (e != Epi::STORE || !gemm_will_h3(op, M, N, K, A, lda, B, ldb, C)))
+        throw Error(LANE_ERR_CUDA, "gemm: out_scale is a 3xF16 STORE option");
     if (gemm_try_tc(g, op, M, N, K, A, lda, B, ldb, e, C, C2, bias, aux, mx, &fused)) {
     } else if (gemm_try_skinny(g, op, M, N, K, A, lda, B, ldb, e, C, C2, bias, aux)) {
     } else {

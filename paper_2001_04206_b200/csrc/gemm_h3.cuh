@@ -522,6 +522,8 @@ __global__ void __launch_bounds__(kH3Threads, 1)
                         if constexpr (E == TcEpi::BIAS || E == TcEpi::BIAS_TANH) vv = sadd(vv, args.bias[n]);
                         if constexpr (E == TcEpi::TANH_GRAD) vv = tanh_grad(args.aux[idx], vv);
                         if constexpr (E == TcEpi::BIAS_TANH) o2 = tanhf(vv);
+                        if constexpr (E == TcEpi::STORE)
+                            if (args.out_scale != 0.0f) vv = smul(vv, args.out_scale);
                     }
                     cv[q] = vv;
                     c2v[q] = o2;

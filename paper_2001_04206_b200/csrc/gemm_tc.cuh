@@ -79,6 +79,9 @@ struct TcArgs {
     // two K halves of each remaining tile (raw partials in tail_part)
     int full_units = 0, tiles_m = 0, tiles_n = 0;
     float* tail_part = nullptr;
+    // STORE (3xF16 wgrad of a one-rank step): C = sum * out_scale when non-zero
+    // (the mean gradient; the update then neither rescales nor rewrites G)
+    float out_scale = 0.0f;
 };
 
 // ---- PTX helpers ------------------------------------------------------------
@@ -209,6 +212,13 @@ __device__ __forceinline__ float4 tc_epi4(const TcArgs& a, int m, int n, float4 
         v.y = tanh_grad(t.y, v.y);
         v.z = tanh_grad(t.z, v.z);
         v.w = tanh_grad(t.w, v.w);
+    } else if constexpr (E == TcEpi::STORE) {
+        if (a.out_scale != 0.0f) {
+            v.x = smul(v.x, a.out_scale);
+            v.y = smul(v.y, a.out_scale);
+            v.z = smul(v.z, a.out_scale);
+            v.w = smul(v.w, a.out_scale);
+        }
     }
     return v;
 }

@@ -241,6 +241,7 @@ struct UpdSpans {
     int n = 0;
     unsigned long long beg[kMaxUpdSpans], end[kMaxUpdSpans];
 };
+template <bool PRESCALED>
 __global__ void k_momentum_update_spans(float4* __restrict__ W, float4* __restrict__ DW, float4* __restrict__ gsum,
                                         UpdSpans sp, unsigned long long total, float invB, float neg_eta, float mu) {
     for (unsigned long long t = (unsigned long long)blockIdx.x * blockDim.x + threadIdx.x; t < total;
@@ -258,13 +259,14 @@ __global__ void k_momentum_update_spans(float4* __restrict__ W, float4* __restri
         float* wp = &w.x;
 #pragma unroll
         for (int i = 0; i < 4; ++i) {
-            const float gi = smul(gp[i], invB);
+            // PRESCALED: gsum already holds g = sum * invB (the wgrad epilogue's)
+            const float gi = PRESCALED ? gp[i] : smul(gp[i], invB);
             gp[i] = gi;
             const float step = smul(neg_eta, gi);
             vp[i] = mu == 0.0f ? step : sadd(smul(mu, vp[i]), step);
             wp[i] = sadd(wp[i], vp[i]);
         }
-        gsum[e] = g;
+        if (!PRESCALED) gsum[e] = g;
         DW[e] = v;
         W[e] = w;
     }
@@ -345,7 +347,8 @@ MbStats minibatch_stats(Net& net, size_t B, GemmCtx& g, cudaStream_t st) {
 
 struct FusedUpdate {
     float inv_b, eta, mu;
-    bool fused_w[kMaxUpdSpans];  // out: layer l's weights were updated by its wgrad epilogue
+    bool fused_w[kMaxUpdSpans];   // out: layer l's weights were updated by its wgrad epilogue
+    bool scaled_g[kMaxUpdSpans];  // out: layer l's G already holds the mean (3xF16 wgrad epilogue)
 };
 
 template <class Ctx, class Net>
@@ -465,8 +468,16 @@ void minibatch_grads_body(Ctx& c, Net& net, size_t Bsz, double* loss_sum, bool a
             fused->fused_w[l] = gemm_wgrad_update(g, (int)Ly.I, (int)Ly.O, B, in, Ly.buf[LANE_BUF_DELTAS],
                                                             Ly.buf[LANE_BUF_G], W, V, fused->inv_b, -fused->eta,
                                                             fused->mu);
+            fused->scaled_g[l] = false;
             if (!fused->fused_w[l]) {
-                const GemmMax mx = wgrad_mx(l);
+                GemmMax mx = wgrad_mx(l);
+                // the 3xF16 wgrad stores the mean gradient directly (G = sum x 1/B,
+                // the update's own first operation): the update pass then reads
+                // G once and does not rewrite it -- 4 of its 20 bytes per weight
+                if (wgrad_h3(l)) {
+                    mx.out_scale = fused->inv_b;
+                    fused->scaled_g[l] = true;
+                }
                 gemm(g, GemmOp::TN, (int)Ly.I, (int)Ly.O, B, in, (int)Ly.I, Ly.buf[LANE_BUF_DELTAS], (int)Ly.O,
                      Epi::STORE, Ly.buf[LANE_BUF_G], nullptr, nullptr, nullptr, &mx);
             }
@@ -509,28 +520,46 @@ void minibatch_update(Ctx& c, Net& net, size_t B_global, float eta, float mu, co
     float* V = net.grads + net.grads_count;
     const size_t n4 = net.params_count / 4;
     const unsigned blocks_max = 4u * static_cast<unsigned>(c.sm_count);
-    UpdSpans sp;
-    unsigned long long total = 0;
+    UpdSpans sp, ps;  // spans to update from gradient sums / from pre-scaled means
+    unsigned long long total = 0, ptotal = 0;
     const int nl = static_cast<int>(net.layers.size());
     const bool spans = fused != nullptr;
+    auto add = [&](UpdSpans& u, unsigned long long& t, const float* from, const float* to) {
+        u.beg[u.n] = static_cast<unsigned long long>(from - W) / 4;
+        u.end[u.n] = static_cast<unsigned long long>(to - W) / 4;
+        t += u.end[u.n] - u.beg[u.n];
+        ++u.n;
+    };
     if (spans) {
         for (int l = 0; l < nl; ++l) {
             auto& Ly = net.L(l);
             // [W_l | b_l] or [b_l] alone; pieces are 256-byte aligned, so the
             // end of layer l is the start of layer l+1 (or of the grads region)
-            const float* from = fused->fused_w[l] ? Ly.buf[LANE_BUF_B] : Ly.buf[LANE_BUF_W];
             const float* to = l + 1 < nl ? net.L(l + 1).buf[LANE_BUF_W] : net.params + net.params_count;
-            sp.beg[sp.n] = static_cast<unsigned long long>(from - W) / 4;
-            sp.end[sp.n] = static_cast<unsigned long long>(to - W) / 4;
-            total += sp.end[sp.n] - sp.beg[sp.n];
-            ++sp.n;
+            if (fused->fused_w[l]) {
+                add(sp, total, Ly.buf[LANE_BUF_B], to);
+            } else if (fused->scaled_g[l]) {
+                add(ps, ptotal, Ly.buf[LANE_BUF_W], Ly.buf[LANE_BUF_B]);
+                add(sp, total, Ly.buf[LANE_BUF_B], to);
+            } else {
+                add(sp, total, Ly.buf[LANE_BUF_W], to);
+            }
         }
     }
     if (spans) {
-        const unsigned blocks = static_cast<unsigned>(std::max<unsigned long long>(
-            1, std::min<unsigned long long>(blocks_max, (total + 255) / 256)));
-        k_momentum_update_spans<<<blocks, 256, 0, c.stream>>>(reinterpret_cast<float4*>(W), reinterpret_cast<float4*>(V),
-                                                              reinterpret_cast<float4*>(G), sp, total, invB, -eta, mu);
+        auto blocks = [&](unsigned long long t) {
+            return static_cast<unsigned>(
+                std::max<unsigned long long>(1, std::min<unsigned long long>(blocks_max, (t + 255) / 256)));
+        };
+        k_momentum_update_spans<false><<<blocks(total), 256, 0, c.stream>>>(
+            reinterpret_cast<float4*>(W), reinterpret_cast<float4*>(V), reinterpret_cast<float4*>(G), sp, total, invB,
+            -eta, mu);
+        if (ps.n) {
+            k_momentum_update_spans<true><<<blocks(ptotal), 256, 0, c.stream>>>(
+                reinterpret_cast<float4*>(W), reinterpret_cast<float4*>(V), reinterpret_cast<float4*>(G), ps, ptotal,
+                invB, -eta, mu);
+            c.launches += 1;
+        }
     } else {
         k_momentum_update_all<<<std::max<size_t>(1, std::min<size_t>(blocks_max, (n4 + 255) / 256)), 256, 0,
                                 c.stream>>>(reinterpret_cast<float4*>(W), reinterpret_cast<float4*>(V),

@@ -293,6 +293,32 @@ def test_minibatch_grads_then_apply_equals_step_bitwise(lane, dev):
     dev.free(Td)
 
 
+@pytest.mark.parametrize("mu", [0.0, 0.9])
+def test_minibatch_prescaled_h3_wgrad_equals_unfused_bitwise(lane, dev, mu):
+    """2048-wide layers, B = 2048: the wgrads run on the 3xF16 kernel, so a
+    one-rank step stores the mean gradient from the wgrad epilogue (G = sum x
+    1/B) and the update pass reads it without rescaling or rewriting G.  That
+    step equals minibatch_grads + minibatch_apply (gradient sums, then the
+    update's own G = sum x 1/B) bit for bit."""
+    F, H, C_, B = 2048, [2048, 2048], 10, 2048
+    X, T = po.synthetic_dataset(F, C_, 2 * B, 21)
+    n1 = lane.build_network(F, H, C_, seed=8, device=dev, max_batch=B)
+    n2 = lane.build_network(F, H, C_, seed=8, device=dev, max_batch=B)
+    Xd, Td = upload(dev, X), upload(dev, T)
+    for s in range(2):
+        n1.minibatch_step(Xd + s * B * F * 4, Td + s * B * C_ * 4, B, 0.01, mu)
+        n2.minibatch_grads(Xd + s * B * F * 4, Td + s * B * C_ * 4, B)
+        n2.minibatch_apply(B, 0.01, mu)
+    for a, b in zip(n1.layers, n2.layers):
+        assert np.array_equal(a.weights, b.weights)
+        assert np.array_equal(a.delta_weights, b.delta_weights)
+        assert np.array_equal(a.gradients, b.gradients)
+        assert np.array_equal(a.biases, b.biases)
+        assert np.array_equal(a.delta_biases, b.delta_biases)
+    dev.free(Xd)
+    dev.free(Td)
+
+
 def test_two_rank_shards_on_one_gpu(lane):
     """The data-parallel step with two library contexts as the two ranks of a
     global batch (one GPU): each shard's gradient sums, summed elementwise in
