@@ -877,7 +877,11 @@ inline void gemm_h3(GemmCtx& g, GemmOp op, int M, int N, int K, const float* A, 
     *g.launches += S > 1 ? 1 : 0;
     // the epilogue's TMA store boxes: 32 columns x 32 rows, 128-byte swizzle
     const CUtensorMap mc = tc_map(C, M, N, 32, 32, 0);
-    const CUtensorMap mc2 = e == Epi::BIAS_TANH ? tc_map(C2, M, N, 32, 32, 0) : mc;
+    // C2: tanh(z) for the forward; for the dgrad, the activations its
+    // epilogue reads (TMA-prefetched into the landing ring, 32 x 32 boxes)
+    const CUtensorMap mc2 = e == Epi::BIAS_TANH   ? tc_map(C2, M, N, 32, 32, 0)
+                            : e == Epi::TANH_GRAD ? tc_map(aux, M, N, 32, 32, 0)
+                                                  : mc;
     switch (e) {
         case Epi::STORE:
             if (pair) h3_dispatch<TcEpi::STORE, true>(g.stream, a_mn, b_mn, ma, mb, mc, mc2, t);
@@ -916,7 +920,7 @@ inline bool gemm_try_tc(GemmCtx& g, GemmOp op, int M, int N, int K, const float*
                         const GemmMax* mx = nullptr, bool* fused = nullptr) {
     if (!gemm_tc_mode() || !tc_eligible(M, N, K)) return false;
     if ((reinterpret_cast<uintptr_t>(A) | reinterpret_cast<uintptr_t>(B) | reinterpret_cast<uintptr_t>(C) |
-         reinterpret_cast<uintptr_t>(C2)) & 15)
+         reinterpret_cast<uintptr_t>(C2) | reinterpret_cast<uintptr_t>(aux)) & 15)
         return false;
     if (gemm_will_h3(op, M, N, K, A, lda, B, ldb, C)) {
         bool f = false;

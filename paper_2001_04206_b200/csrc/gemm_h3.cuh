@@ -281,6 +281,24 @@ __global__ void __launch_bounds__(kH3Threads, 1)
                         tc_tma_2d(&tmB, full(l), landB(l), nbl, k0);
                 }
             }
+            if constexpr (E == TcEpi::TANH_GRAD && PAIR) {
+                // the dgrad epilogue's activations (tmC2 maps aux): this CTA's
+                // 128 rows x 256 columns into the landing ring as its slots free
+                // up, during the last K blocks' MMAs.  Slot j = the 64 columns
+                // [64 j, 64 j + 64) of epilogue warp group j: two 32-column
+                // halves x 4 row quarters, one 32 x 32 box (4 KB, 128B swizzle) each.
+                if (!split && tail < 0) {
+                    for (int j = 0; j < kL; ++j) {
+                        const int kb = nkb + j, l = kb % kL;
+                        tc_mbar_wait(lempty(l), (uint32_t)(((kb / kL) & 1) ^ 1));
+                        tc_mbar_expect_tx(full(l), (uint32_t)Cfg::kLandBytes);
+                        for (int cc = 0; cc < 2; ++cc)
+                            for (int q = 0; q < 4; ++q)
+                                tc_tma_2d(&tmC2, full(l), landA(l) + (uint32_t)(cc * 16384 + q * 4096),
+                                          n0 + 32 * (2 * j + cc), m0 + 32 * q);
+                    }
+                }
+            }
         }
     } else if (warp == 1 && rank == 0) {
         // ---------------- MMA issuer ----------------
@@ -443,8 +461,17 @@ __global__ void __launch_bounds__(kH3Threads, 1)
         const bool omax = args.omax_row != nullptr && !split && tail < 0;
         unsigned rmax = 0;
         // this warp's store staging (C, then C2): 8 KB of the landing ring,
-        // idle once every K block has been split
-        const uint32_t stg = sbase + (uint32_t)((warp - 2) * 8192);
+        // idle once every K block has been split -- or, for the dgrad, whose
+        // activations the producer prefetches into the landing ring, 4 KB of
+        // the f16 ring (idle once every MMA has completed)
+        const bool aux_smem = E == TcEpi::TANH_GRAD && PAIR && !split && tail < 0;
+        const uint32_t stg = aux_smem ? f16base + (uint32_t)((warp - 2) * 4096) : sbase + (uint32_t)((warp - 2) * 8192);
+        uint32_t aux_base = 0;  // this warp's activations: [column half][row quarter] 4 KB boxes
+        if (aux_smem) {
+            const int kb = nkb + ((warp - 2) >> 2);
+            tc_mbar_wait(full(kb % kL), (uint32_t)((kb / kL) & 1));
+            aux_base = landA(kb % kL) + (uint32_t)(quarter * 4096);
+        }
         bool stg_pending = false;
 #pragma unroll 1
         for (int c0 = cbeg; c0 < cbeg + kCols; c0 += 32) {
@@ -502,7 +529,21 @@ __global__ void __launch_bounds__(kH3Threads, 1)
                 for (int q = 0; q < 8; ++q) {
                     float4 vv = make_float4(x[4 * q], x[4 * q + 1], x[4 * q + 2], x[4 * q + 3]);
                     float4 t = make_float4(0.f, 0.f, 0.f, 0.f);
-                    if (mrow) vv = tc_epi4<E>(args, m, nb0 + 4 * q, vv, &t);
+                    if (aux_smem) {
+                        if constexpr (E == TcEpi::TANH_GRAD) {
+                            float4 a;
+                            asm volatile("ld.shared.v4.f32 {%0,%1,%2,%3}, [%4];\n"
+                                         : "=f"(a.x), "=f"(a.y), "=f"(a.z), "=f"(a.w)
+                                         : "r"(aux_base + (uint32_t)(((c0 >> 5) & 1) * 16384 + lane * 128 +
+                                                                     ((q ^ (lane & 7)) * 16))));
+                            vv.x = tanh_grad(a.x, vv.x);
+                            vv.y = tanh_grad(a.y, vv.y);
+                            vv.z = tanh_grad(a.z, vv.z);
+                            vv.w = tanh_grad(a.w, vv.w);
+                        }
+                    } else if (mrow) {
+                        vv = tc_epi4<E>(args, m, nb0 + 4 * q, vv, &t);
+                    }
                     cv[4 * q + 0] = vv.x;
                     cv[4 * q + 1] = vv.y;
                     cv[4 * q + 2] = vv.z;
