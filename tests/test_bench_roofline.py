@@ -43,3 +43,18 @@ def test_chain_latency_only_for_window_plans():
     assert bench.chain_latency("c2", "grid", 5.0, 10000, _Clk(2000.0)) is None
     assert bench.chain_latency("c4-16384", "window", 5.0, 10000, _Clk(2000.0)) is None  # no floor measured
     assert bench.chain_latency("c2", "window", 5.0, 10000, _Clk(0)) is None  # no clock sample
+
+
+def test_gpus_n_refuses_without_n_gpus(tmp_path):
+    # --gpus N outside torchrun self-launches N ranks, or fails loudly: it never
+    # silently runs one rank (this container has no GPU)
+    import subprocess
+    import torch
+    if torch.cuda.device_count() >= 2:
+        pytest.skip("enough GPUs to launch")
+    env = {k: v for k, v in os.environ.items() if k not in ("WORLD_SIZE", "RANK", "LOCAL_RANK")}
+    r = subprocess.run([sys.executable, os.path.join(ROOT, "bench.py"), "--gpus", "2", "--steps", "1",
+                        "--warmup", "3"], capture_output=True, text=True, env=env, timeout=300)
+    assert r.returncode == 2, (r.returncode, r.stderr[-500:])
+    assert "needs 2 visible GPUs" in r.stderr
+    assert r.stdout.strip() == ""  # no bench line
