@@ -34,27 +34,30 @@
 
 namespace lane_b200 {
 
-constexpr int kTpStages = 4;      // ring stages (3 for UPDATE, whose epilogue stages W / V tiles)
+constexpr int kTpStages = 4;      // ring stages (TMEM: 2 accumulators + 4 x 64 A / A_lo columns)
 constexpr int kTpSplitWarps = 8;
 constexpr int kTpEpiWarps = 4;
 constexpr int kTpThreads = 32 * (2 + kTpSplitWarps + kTpEpiWarps);
 constexpr int kTpBTile = kTcBN * kTcBK * 4;           // 128 x 32 fp32
-constexpr int kTpStage = kTcTile + 2 * kTpBTile;      // A, B, B_lo
+// a stage: A (TMA), B (TMA); B_lo overwrites A once every split warp has
+// read its A rows into registers (A goes on to TMEM), so a stage is 32 KB
+// and the UPDATE kernel keeps 4 stages next to its W / V slots
+constexpr int kTpStage = kTcTile + kTpBTile;
 constexpr int kTpAcc = 2;                             // TMEM accumulators
 constexpr int kTpTileElems = kTcBM * kTcBN;
 constexpr int kTpUpdCols = 16;                        // columns per W / V chunk
 constexpr int kTpUpdChunk = kTcBM * kTpUpdCols * 4;   // one 128 x 16 fp32 chunk of W or V (64B swizzle)
 
-// UPDATE: the epilogue streams W and V through 5 chunk slots with loads 4
-// chunks ahead (64 KB in flight), and the ring keeps 3 MMA stages.  (The first
-// version used 128 x 32 chunks: 4 slots left room for 2 ring stages only, and
-// the K-block ring -- TMA latency + split + MMA per stage -- bound the kernel:
-// 93 us for C3's 4096 x 4096 x 256 wgrad + update.)
-constexpr int kTpUpdSlots = 5;
+// UPDATE: each epilogue warp streams W and V through 6 sub-chunk slots with
+// loads 5 chunks ahead, and the ring keeps 4 MMA stages.  (The first version
+// used 128 x 32 chunks: 4 slots left room for 2 ring stages only, and the
+// K-block ring -- TMA latency + split + MMA per stage -- bound the kernel: 93 us
+// for C3's 4096 x 4096 x 256 wgrad + update.)
+constexpr int kTpUpdSlots = 6;
 template <int E>
 struct TpCfg {
     static constexpr bool kUpd = E == 4;                    // TpEpi::UPDATE
-    static constexpr int kStages = kUpd ? 3 : kTpStages;
+    static constexpr int kStages = kTpStages;
     static constexpr size_t kRing = (size_t)kStages * kTpStage;
     static constexpr size_t kEpi = kUpd ? kTpUpdSlots * 2 * kTpUpdChunk : 0;  // slots x (W, V)
     static constexpr size_t kSmem = kRing + kEpi + 1024 + 512;
@@ -249,7 +252,7 @@ __global__ void __launch_bounds__(kTpThreads, 1)
     uint8_t* epi_buf = smem + Cfg::kRing;  // UPDATE: slot k -> W chunk at 2k, V chunk at 2k+1
     uint64_t* bars = reinterpret_cast<uint64_t*>(smem + Cfg::kRing + Cfg::kEpi);
     // bars: full[S], conv[S], empty[S], acc_full[2], acc_empty[2]; then the TMEM address, the last-arriver flag
-    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 32);
+    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 60);  // after up to 40 barriers
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const uint32_t sbase = tc_smem(smem);
     auto full = [&](int s) { return tc_smem(bars + s); };
@@ -257,10 +260,11 @@ __global__ void __launch_bounds__(kTpThreads, 1)
     auto empty = [&](int s) { return tc_smem(bars + 2 * kTpStages + s); };
     auto acc_full = [&](int b) { return tc_smem(bars + 3 * kTpStages + b); };
     auto acc_empty = [&](int b) { return tc_smem(bars + 3 * kTpStages + 2 + b); };
-    auto epi_full = [&](int k) { return tc_smem(bars + 3 * kTpStages + 4 + k); };
+    // UPDATE: W / V slot k of epilogue warp (row quarter) q
+    auto epi_full = [&](int q, int k) { return tc_smem(bars + 3 * kTpStages + 4 + q * kTpUpdSlots + k); };
     auto tileA = [&](int s) { return sbase + (uint32_t)(s * kTpStage); };
     auto tileB = [&](int s) { return sbase + (uint32_t)(s * kTpStage + kTcTile); };
-    auto tileBlo = [&](int s) { return sbase + (uint32_t)(s * kTpStage + kTcTile + kTpBTile); };
+    auto tileBlo = [&](int s) { return sbase + (uint32_t)(s * kTpStage); };  // over A, after the split
 
     if (threadIdx.x == 0) {
         for (int s = 0; s < kTpStages; ++s) {
@@ -272,7 +276,9 @@ __global__ void __launch_bounds__(kTpThreads, 1)
             tc_mbar_init(acc_full(b), 1);
             tc_mbar_init(acc_empty(b), kTpEpiWarps);
         }
-        for (int k = 0; k < kTpUpdSlots; ++k) tc_mbar_init(epi_full(k), 1);
+        if constexpr (Cfg::kUpd)
+            for (int q = 0; q < 4; ++q)
+                for (int k = 0; k < kTpUpdSlots; ++k) tc_mbar_init(epi_full(q, k), 1);
         asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
         asm volatile("prefetch.tensormap [%0];\n" ::"l"(reinterpret_cast<uint64_t>(&tmA)) : "memory");
         asm volatile("prefetch.tensormap [%0];\n" ::"l"(reinterpret_cast<uint64_t>(&tmB)) : "memory");
@@ -375,7 +381,7 @@ __global__ void __launch_bounds__(kTpThreads, 1)
                 tc_mbar_wait(full(s), ph);
                 const uint8_t* a = smem + (size_t)s * kTpStage;
                 const float4* bsrc = reinterpret_cast<const float4*>(smem + (size_t)s * kTpStage + kTcTile);
-                float4* bl = reinterpret_cast<float4*>(smem + (size_t)s * kTpStage + kTcTile + kTpBTile);
+                float4* bl = reinterpret_cast<float4*>(smem + (size_t)s * kTpStage);  // B_lo over A
                 uint32_t hi[16], lo[16];
                 if constexpr (!A_MN) {
 #pragma unroll
@@ -397,6 +403,8 @@ __global__ void __launch_bounds__(kTpThreads, 1)
                 const uint32_t tA = tmem + ((uint32_t)(quarter * 32) << 16) + (uint32_t)(kAStage0 + 64 * s + 16 * khalf);
                 tc_st16(tA, hi);
                 tc_st16(tA + 32u, lo);
+                // every split warp has its A values in registers: B_lo may overwrite A
+                asm volatile("bar.sync 2, %0;\n" ::"n"(32 * kTpSplitWarps) : "memory");
 #pragma unroll
                 for (int q = 0; q < kTpBTile / 16 / (32 * kTpSplitWarps); ++q) {
                     const int e = ct + 32 * kTpSplitWarps * q;
@@ -420,35 +428,40 @@ __global__ void __launch_bounds__(kTpThreads, 1)
         int n_unit = 0;
         if constexpr (Cfg::kUpd) {
             if (!args.sk) {
-                // wgrad + update, whole tiles: the leader TMA-loads the W and V
-                // chunks (128 rows x 16 columns, 64B swizzle) four chunks ahead
-                // -- across unit boundaries, i.e. during the next tile's MMAs --
-                // into five slots; every thread updates its row of the chunk in
-                // shared memory, G goes straight to global, and the leader
-                // TMA-stores the W and V chunks back.
+                // wgrad + update, whole tiles.  Each epilogue warp streams the W
+                // and V sub-chunks of its own 32 rows (32 x 16 fp32, 64B swizzle,
+                // 2 KB each): its lane 0 TMA-loads them kTpUpdSlots - 1 chunks
+                // ahead -- across unit boundaries, i.e. during the next tile's
+                // MMAs -- every lane updates its row in shared memory, G goes
+                // straight to global, and lane 0 TMA-stores W and V back.  No
+                // barrier across the epilogue warps: each runs its own pipeline.
+                // (With one 128-row chunk per step shared by the 4 warps, a named
+                // barrier per chunk serialised them: 57 us per C3 4096^2 wgrad.)
                 constexpr int kChunks = kTcBN / kTpUpdCols;
-                const uint32_t vbytes = args.mu == 0.0f ? 0u : (uint32_t)kTpUpdChunk;
+                constexpr uint32_t kSub = 32 * kTpUpdCols * 4;  // one warp's W or V sub-chunk
+                const uint32_t vbytes = args.mu == 0.0f ? 0u : kSub;
+                uint8_t* const wbuf = epi_buf + (size_t)quarter * kTpUpdSlots * 2 * kSub;
                 long long lit = 0;  // the loads' own cursor over units / chunks
                 TpUnit lu;
                 bool lmore = tp_next(args, lit, lu);
                 int lchunk = 0, lissued = 0;
-                auto issue_load = [&]() {  // leader only: the next chunk in unit order, if any
+                auto issue_load = [&]() {  // lane 0: the next sub-chunk in unit order, if any
                     if (!lmore) return;
                     int mt, nt;
                     tp_tile_mn(args, lu.tile, mt, nt);
                     const int k = lissued % kTpUpdSlots;
-                    const uint32_t wdst = tc_smem(epi_buf + (size_t)(2 * k) * kTpUpdChunk);
-                    tc_mbar_expect_tx(epi_full(k), (uint32_t)kTpUpdChunk + vbytes);
-                    tc_tma_2d(&tmW, epi_full(k), wdst, nt * kTcBN + kTpUpdCols * lchunk, mt * kTcBM);
-                    if (vbytes)
-                        tc_tma_2d(&tmV, epi_full(k), wdst + kTpUpdChunk, nt * kTcBN + kTpUpdCols * lchunk, mt * kTcBM);
+                    const uint32_t wdst = tc_smem(wbuf + (size_t)(2 * k) * kSub);
+                    const int r0 = mt * kTcBM + quarter * 32;
+                    tc_mbar_expect_tx(epi_full(quarter, k), kSub + vbytes);
+                    tc_tma_2d(&tmW, epi_full(quarter, k), wdst, nt * kTcBN + kTpUpdCols * lchunk, r0);
+                    if (vbytes) tc_tma_2d(&tmV, epi_full(quarter, k), wdst + kSub, nt * kTcBN + kTpUpdCols * lchunk, r0);
                     ++lissued;
                     if (++lchunk == kChunks) {
                         lchunk = 0;
                         lmore = tp_next(args, lit, lu);
                     }
                 };
-                if (leader)
+                if (lane == 0)
                     for (int q = 0; q < kTpUpdSlots - 1; ++q) issue_load();
                 int gc = 0;  // chunks consumed
                 while (tp_next(args, it, u)) {
@@ -469,13 +482,13 @@ __global__ void __launch_bounds__(kTpThreads, 1)
                             if (lane == 0) tc_mbar_arrive(acc_empty(b));
                         }
                         const int k = gc % kTpUpdSlots;
-                        tc_mbar_wait(epi_full(k), (uint32_t)((gc / kTpUpdSlots) & 1));
-                        uint8_t* wrow = epi_buf + (size_t)(2 * k) * kTpUpdChunk + row * (4 * kTpUpdCols);
-                        uint8_t* vrow = wrow + kTpUpdChunk;
+                        tc_mbar_wait(epi_full(quarter, k), (uint32_t)((gc / kTpUpdSlots) & 1));
+                        uint8_t* wrow = wbuf + (size_t)(2 * k) * kSub + lane * (4 * kTpUpdCols);
+                        uint8_t* vrow = wrow + kSub;
                         const bool full_cols = n0 + kTpUpdCols * c + kTpUpdCols <= args.N && (args.N & 3) == 0;
 #pragma unroll
                         for (int q = 0; q < kTpUpdCols / 4; ++q) {
-                            const int off = ((q ^ ((row >> 1) & 3)) * 16);  // 64B swizzle: 16-byte unit q of row r
+                            const int off = ((q ^ ((lane >> 1) & 3)) * 16);  // 64B swizzle: 16-byte unit q of row lane
                             float4 w = *reinterpret_cast<const float4*>(wrow + off);
                             float4 vv = args.mu == 0.0f ? make_float4(0.f, 0.f, 0.f, 0.f)
                                                         : *reinterpret_cast<const float4*>(vrow + off);
@@ -505,11 +518,12 @@ __global__ void __launch_bounds__(kTpThreads, 1)
                         }
                         // generic-proxy smem writes -> visible to the TMA store
                         asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");
-                        tp_epi_bar();
-                        if (leader) {
-                            const uint32_t wsrc = tc_smem(epi_buf + (size_t)(2 * k) * kTpUpdChunk);
-                            tp_tma_store_2d(&tmW, wsrc, n0 + kTpUpdCols * c, mt * kTcBM);
-                            tp_tma_store_2d(&tmV, wsrc + kTpUpdChunk, n0 + kTpUpdCols * c, mt * kTcBM);
+                        __syncwarp();
+                        if (lane == 0) {
+                            const uint32_t wsrc = tc_smem(wbuf + (size_t)(2 * k) * kSub);
+                            const int r0 = mt * kTcBM + quarter * 32;
+                            tp_tma_store_2d(&tmW, wsrc, n0 + kTpUpdCols * c, r0);
+                            tp_tma_store_2d(&tmV, wsrc + kSub, n0 + kTpUpdCols * c, r0);
                             asm volatile("cp.async.bulk.commit_group;\n" ::: "memory");
                             // the next load refills the previous chunk's slot, once
                             // that chunk's stores have read it (this chunk's may
@@ -517,10 +531,11 @@ __global__ void __launch_bounds__(kTpThreads, 1)
                             asm volatile("cp.async.bulk.wait_group.read 1;\n" ::: "memory");
                             issue_load();
                         }
+                        __syncwarp();
                     }
                     ++n_unit;
                 }
-                if (leader) asm volatile("cp.async.bulk.wait_group 0;\n" ::: "memory");
+                if (lane == 0) asm volatile("cp.async.bulk.wait_group 0;\n" ::: "memory");
             }
         }
         while (tp_next(args, it, u)) {
@@ -683,10 +698,10 @@ inline void tp_launch(cudaStream_t st, const CUtensorMap& ma, const CUtensorMap&
                                        (int)smem));
         configured.fetch_or(bit, std::memory_order_release);
     }
-    // UPDATE: W and V as [M rows x N cols] boxes of 128 rows x 16 columns
-    // (64B swizzle) for the epilogue's TMA loads and stores
-    const CUtensorMap mw = E == TpEpi::UPDATE ? tc_map(p.a.W, p.a.M, p.a.N, kTpUpdCols, kTcBM, 3) : ma;
-    const CUtensorMap mv = E == TpEpi::UPDATE ? tc_map(p.a.V, p.a.M, p.a.N, kTpUpdCols, kTcBM, 3) : ma;
+    // UPDATE: W and V as [M rows x N cols] boxes of 32 rows x 16 columns
+    // (64B swizzle) for each epilogue warp's TMA loads and stores
+    const CUtensorMap mw = E == TpEpi::UPDATE ? tc_map(p.a.W, p.a.M, p.a.N, kTpUpdCols, 32, 3) : ma;
+    const CUtensorMap mv = E == TpEpi::UPDATE ? tc_map(p.a.V, p.a.M, p.a.N, kTpUpdCols, 32, 3) : ma;
     k_gemm_tcp<A_MN, B_MN, E><<<p.grid, kTpThreads, smem, st>>>(ma, mb, mw, mv, p.a);
 }
 
