@@ -3,6 +3,7 @@ operand maxima precomputed, CUDA events, 10 reps): the slope per K is the
 main loop, the intercept the fixed cost per GEMM.
 
     KS=512,1024,2048,4096,8192 python tools/gemm_kscan.py
+    ZERO=1 KS=8192 REPS=200 python tools/gemm_kscan.py   # all-zero operands
 """
 import ctypes as C
 import json
@@ -18,7 +19,9 @@ for op, epi in ((0, 2), (1, 0), (2, 0)):
     for K in [int(k) for k in os.environ.get("KS", "512,1024,2048,4096,8192").split(",")]:
         ar = (K, M) if op == 2 else (M, K)
         br = (N, K) if op == 1 else (K, N)
-        a = torch.randn(ar, device="cuda"); b = torch.randn(br, device="cuda")
+        # ZERO=1: all-zero operands (the same work on data that toggles nothing)
+        mk = torch.zeros if os.environ.get("ZERO") == "1" else torch.randn
+        a = mk(ar, device="cuda"); b = mk(br, device="cuda")
         c = torch.empty(M * N, device="cuda"); c2 = torch.empty(M * N, device="cuda"); bias = torch.rand(N, device="cuda")
         bufs = [torch.zeros(x, dtype=torch.int32, device="cuda") for x in (*ar, *br)]
         torch.cuda.synchronize()
@@ -34,7 +37,8 @@ for op, epi in ((0, 2), (1, 0), (2, 0)):
         dev.sync()
         e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         e0.record(stream)
-        for _ in range(10): call()
+        reps = int(os.environ.get("REPS", "10"))
+        for _ in range(reps): call()
         e1.record(stream); e1.synchronize()
-        us = e0.elapsed_time(e1) * 100
+        us = e0.elapsed_time(e1) * 1000 / reps
         print(json.dumps({"op": op, "epi": epi, "K": K, "us": round(us, 1), "tf": round(2.0 * M * N * K / us / 1e6, 1)}), flush=True)
