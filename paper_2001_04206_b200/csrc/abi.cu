@@ -484,8 +484,9 @@ SgdPlan plan_persistent(lane_b200_net* net) {
         // the deeper rings fit in shared memory (not at H = 8192)
         const char* env_d = std::getenv("LANE_B200_SGD_WIN_D");
         const bool wide = H > 256 && next_pow2((H + 127) / 128) >= kWinMaxCS;
-        for (int D : {wide && !env_d ? 3 : 2, 2}) {
-            if (env_d) D = std::max(2, std::min(std::atoi(env_d), kWinMaxD));
+        const int nD = wide && !env_d ? 2 : 1;  // D = 3, then 2; or just 2 (or the override)
+        for (int di = 0; di < nD; ++di) {
+            const int D = env_d ? std::max(2, std::min(std::atoi(env_d), kWinMaxD)) : (nD == 2 && di == 0 ? 3 : 2);
             // chain geometry: H <= 128 -> one chain warp x 4 units/lane; <= 256 ->
             // two warps x 4 (measured at C2: one warp 1.83M samples/s, two 1.68M --
             // the barrier and the duplicated softmax outweigh the halved H work);
@@ -542,7 +543,6 @@ SgdPlan plan_persistent(lane_b200_net* net) {
                 p.smem = smem;
                 return p;
             }
-            if (env_d) break;
         }
         if (mode) return p;
     }

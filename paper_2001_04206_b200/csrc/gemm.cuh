@@ -1061,7 +1061,7 @@ inline void gemm(GemmCtx& g, GemmOp op, int M, int N, int K, const float* A, int
     if (M <= 0 || N <= 0) return;
     bool fused = false;
     if (mx && mx->out_scale != 0.0f && (e != Epi::STORE || !gemm_will_h3(op, M, N, K, A, lda, B, ldb, C)))
-        throw Error(LANE_ERR_CUDA, "gemm: out_scale is a 3xF16 STORE option");
+        throw Error(LANE_ERR_CONFIG, "gemm: out_scale is a 3xF16 STORE option");
     if (gemm_try_tc(g, op, M, N, K, A, lda, B, ldb, e, C, C2, bias, aux, mx, &fused)) {
     } else if (gemm_try_skinny(g, op, M, N, K, A, lda, B, ldb, e, C, C2, bias, aux)) {
     } else {
